@@ -1,0 +1,452 @@
+"""Benchmark of the expert-parallel MoE layer fwd+bwd (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config mixtral|dsmoe|dsv3|tiny]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 ... bench.py --gpus N
+    python bench.py --impl reference ...   # the fp64 CPU oracle (the only reference this tier has)
+    python bench.py --a2a                  # dispatch/combine GB/s sweep vs NCCL all_to_all
+
+A "step" is one forward + backward of the whole layer
+over T tokens of the EP group (T/N per rank, experts sharded E/N per rank).  At N=1 the
+workload is the Mixtral-8x7B layer (BASELINE.json configs[1]: d=4096 E=8 top-2 f=14336
+T=8192, cf=1.25); N>1 shards the same T=8192 tokens (strong scaling).  Timing: CUDA
+events on the launching stream, barrier + synchronize on both sides, max over ranks.
+Inputs (the 2.8 GB of bf16 expert weights per GPU at N=1) are larger than L2.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "MoE layer fwd+bwd tokens/s"
+UNIT = "tokens/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="mixtral", choices=list(synth.CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--a2a", action="store_true", help="dispatch/combine sweep vs NCCL")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-tokens", type=int, default=0)
+    ap.add_argument("--profile-steps", type=int, default=0,
+                    help="run only this many steps without timing (for ncu)")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def init_dist(world, local, backend="nccl"):
+    if world > 1:
+        import torch.distributed as dist
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend, device_id=torch.device(f"cuda:{local}")
+                                if backend == "nccl" else None)
+        return dist
+    return None
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            m = json.load(fh)
+        return dict(hbm=m.get("hbm_gbs", 6650.0), bf16=m.get("bf16_tflops", 1590.0),
+                    bf16_sustained=m.get("bf16_tflops_sustained", 1400.0), source="measured")
+    return dict(hbm=6650.0, bf16=1590.0, bf16_sustained=1400.0, source="fallback")
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"moe_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        os.unlink(self.path)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx), "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+def realised_gemm_flops(layer, cfg):
+    """Algorithmic GEMM FLOPs of one fwd+bwd on this rank from the realised routing:
+    6 * rows * d * f (fwd) + 12 * rows * d * f (bwd), plus the shared experts."""
+    rows = int(layer.expert_rows.sum().item())
+    fl = 18 * rows * cfg.d * cfg.f
+    if cfg.E_s:
+        fl += 18 * layer.dims.T_local * cfg.d * cfg.E_s * cfg.f
+    return fl
+
+
+# ---------------------------------------------------------------------------- our arm
+def run_ours(args):
+    world, rank, local = dist_env()
+    dist = init_dist(world, local)
+    torch.cuda.set_device(local)
+    from paper_2605_05049_b200 import LayerDims, MoELayer
+
+    cfg = synth.CONFIGS[args.config]
+    ep = world
+    T_r = cfg.T // ep
+    dims = LayerDims(T_r, cfg.d, cfg.E, cfg.k, cfg.f, cfg.E_s, cfg.cf, ep, rank)
+    layer = MoELayer(dims, device=local)
+    E_l = cfg.E // ep
+    dev = torch.device(f"cuda:{local}")
+    w_gu, w_down = synth.expert_weights(cfg, range(rank * E_l, (rank + 1) * E_l), device=dev)
+    w_gu_s, w_down_s = synth.shared_weights(cfg, device=dev)
+    layer.set_weights(synth.router_weight(cfg, device=dev), w_gu, w_down, synth.zipf_bias(cfg),
+                      w_gu_s, w_down_s)
+    x_all = synth.tokens(cfg, device=dev)
+    dy_all = synth.grad_output(cfg, device=dev)
+    x = x_all[rank * T_r:(rank + 1) * T_r].contiguous()
+    dy = dy_all[rank * T_r:(rank + 1) * T_r].contiguous()
+    del x_all, dy_all
+    stream = torch.cuda.current_stream()
+
+    if args.profile_steps:
+        for _ in range(args.profile_steps):
+            layer.forward(x)
+            layer.backward(dy)
+        torch.cuda.synchronize()
+        layer.ctx.check_device_error()
+        if rank == 0:
+            print(json.dumps({"profile_steps": args.profile_steps, "config": args.config}))
+        return
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    # GEMM-region events (the dominant kernel family: 6 grouped-GEMM launches per step)
+    gemm_ev = []
+    orig_ffn, orig_ffn_bwd = None, None
+    from paper_2605_05049_b200 import _lib as L
+    import paper_2605_05049_b200.layer as layer_mod
+
+    def timed(fn):
+        def wrapper(*a, **kw):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record(stream)
+            fn(*a, **kw)
+            e.record(stream)
+            gemm_ev.append((s, e))
+        return wrapper
+
+    for _ in range(args.warmup):
+        layer.forward(x)
+        layer.backward(dy)
+    torch.cuda.synchronize()
+    layer.ctx.check_device_error()
+
+    # ---- device-timed region
+    orig_ffn, orig_ffn_bwd = layer_mod.L.moe_expert_ffn, layer_mod.L.moe_expert_ffn_bwd
+    layer_mod.L.moe_expert_ffn = timed(orig_ffn)
+    layer_mod.L.moe_expert_ffn_bwd = timed(orig_ffn_bwd)
+    clocks = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        layer.forward(x)
+        layer.backward(dy)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    layer_mod.L.moe_expert_ffn, layer_mod.L.moe_expert_ffn_bwd = orig_ffn, orig_ffn_bwd
+    layer.ctx.check_device_error()
+    ms = t0.elapsed_time(t1) / args.steps
+    gemm_ms = sum(s.elapsed_time(e) for s, e in gemm_ev) / args.steps
+    gemm_flops = realised_gemm_flops(layer, cfg)
+
+    # ---- end-to-end through the public API with host buffers (pinned), copies timed
+    x_h = x.cpu().pin_memory()
+    dy_h = dy.cpu().pin_memory()
+    y_h = torch.empty_like(x_h).pin_memory()
+    dx_h = torch.empty_like(x_h).pin_memory()
+    x_d = torch.empty_like(x)
+    dy_d = torch.empty_like(dy)
+    barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        x_d.copy_(x_h, non_blocking=True)
+        dy_d.copy_(dy_h, non_blocking=True)
+        y = layer.forward(x_d)
+        dxo = layer.backward(dy_d)
+        y_h.copy_(y, non_blocking=True)
+        dx_h.copy_(dxo, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = e0.elapsed_time(e1) / args.steps
+
+    vals = torch.tensor([ms, e2e_ms, gemm_ms], dtype=torch.float64, device=dev)
+    if dist is not None:
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+    ms, e2e_ms, gemm_ms_max = vals.tolist()
+    if rank != 0:
+        layer.close()
+        return
+    tokens = cfg.T
+    peaks = measured_peaks()
+    achieved = gemm_flops / (gemm_ms * 1e-3) / 1e12
+    out = {
+        "metric": METRIC,
+        "value": tokens / (ms * 1e-3),
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic (seeded N(0,1) tokens, random-init expert/router weights)",
+        "config": {
+            "workload": f"{cfg.name} MoE layer fwd+bwd",
+            "T": cfg.T, "d": cfg.d, "E": cfg.E, "k": cfg.k, "f": cfg.f, "E_shared": cfg.E_s,
+            "capacity_factor": cfg.cf, "zipf_s": cfg.zipf_s,
+            "parallelism": f"ep{world}", "tokens_per_rank": T_r,
+            "l2": "inputs larger than L2 (bf16 expert weights %.2f GB per GPU)" % (
+                (w_gu.numel() + w_down.numel()) * 2 / 1e9),
+        },
+        "e2e": {"value": tokens / (e2e_ms * 1e-3), "unit": UNIT,
+                "h2d_bytes_per_step": int(x_h.numel() * 2 + dy_h.numel() * 2),
+                "d2h_bytes_per_step": int(y_h.numel() * 2 + dx_h.numel() * 2)},
+        "gpu_launches": layer.kernel_launches() * args.steps,
+        "clocks": clk,
+        "roofline": {
+            "kernel": "grouped_gemm_kernel (tcgen05; 6 launches/step: GEMM1+SwiGLU, GEMM2, "
+                      "dgrad x2, wgrad x2)",
+            "bound": "tensor",
+            "achieved": achieved,
+            "peak": peaks["bf16_sustained"],
+            "unit": "TFLOP/s",
+            "frac": achieved / peaks["bf16_sustained"],
+            "traffic": None,
+            "peak_source": peaks["source"] + " bf16_tflops_sustained (kernel timed inside a long step)",
+            "algorithmic_flops_per_step": gemm_flops,
+            "gemm_ms_per_step": gemm_ms,
+            "gemm_share_of_step": gemm_ms / ms,
+        },
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(cfg, args.cpu_sample_tokens or 128, w_gu, w_down, layer)
+    print(json.dumps(out))
+    layer.close()
+
+
+# ---------------------------------------------------------------------------- oracle arm
+def _oracle_inputs(cfg, n_tok, w_gu=None, w_down=None):
+    """Oracle inputs for a bounded sample: the first n_tok tokens of the workload and all
+    E experts' weights as float32 (exact for bf16; the oracle computes in fp64)."""
+    if w_gu is None:
+        w_gu, w_down = synth.expert_weights(cfg, range(cfg.E))
+    f = cfg.f
+    Wg = [w_gu[e, :f].float().cpu().numpy().T for e in range(cfg.E)]
+    Wu = [w_gu[e, f:].float().cpu().numpy().T for e in range(cfg.E)]
+    Wd = [w_down[e].float().cpu().numpy().T for e in range(cfg.E)]
+    x = synth.tokens(cfg, T=cfg.T)[:n_tok].float().numpy()
+    dy = synth.grad_output(cfg, T=cfg.T)[:n_tok].float().numpy()
+    W_r = synth.router_weight(cfg).float().numpy().T
+    shared = None
+    if cfg.E_s:
+        s_gu, s_down = synth.shared_weights(cfg)
+        fs = cfg.E_s * cfg.f
+        shared = (s_gu[:fs].float().numpy().T, s_gu[fs:].float().numpy().T,
+                  s_down.float().numpy().T)
+    bias = synth.zipf_bias(cfg)
+    return x, dy, W_r, Wg, Wu, Wd, shared, None if bias is None else bias.numpy()
+
+
+def _oracle_step(cfg, inp):
+    from oracle import moe_ref as ref
+    x, dy, W_r, Wg, Wu, Wd, shared, bias = inp
+    return ref.layer_forward_backward(x, W_r, Wg, Wu, Wd, dy, cfg.k, cfg.cf, 1, shared=shared,
+                                      bias=bias)
+
+
+def cpu_baseline(cfg, n_tok, w_gu=None, w_down=None, layer=None):
+    if w_gu is not None and w_gu.shape[0] != cfg.E:
+        w_gu = w_down = None
+    inp = _oracle_inputs(cfg, n_tok, w_gu, w_down)
+    t = time.perf_counter()
+    _oracle_step(cfg, inp)
+    dt = time.perf_counter() - t
+    return {"value": n_tok / dt, "unit": UNIT, "cores": len(os.sched_getaffinity(0)),
+            "kind": "oracle",
+            "sample": f"one fwd+bwd of the fp64 NumPy oracle on the first {n_tok} tokens of the "
+                      f"{cfg.name} workload (all {cfg.E} experts, full d/f), {dt:.1f} s"}
+
+
+def run_reference(args):
+    world, rank, local = dist_env()
+    if world > 1 and rank != 0:
+        return
+    cfg = synth.CONFIGS[args.config]
+    n_tok = args.cpu_sample_tokens or (128 if cfg.name != "tiny" else cfg.T)
+    inp = _oracle_inputs(cfg, n_tok)
+    for _ in range(args.warmup):
+        _oracle_step(cfg, inp)
+    t = time.perf_counter()
+    for _ in range(args.steps):
+        _oracle_step(cfg, inp)
+    dt = (time.perf_counter() - t) / max(args.steps, 1)
+    v = n_tok / dt
+    out = {
+        "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded N(0,1) tokens, random-init expert/router weights)",
+        "impl": "reference",
+        "config": {"workload": f"{cfg.name} MoE layer fwd+bwd", "T": cfg.T, "d": cfg.d,
+                   "E": cfg.E, "k": cfg.k, "f": cfg.f, "E_shared": cfg.E_s,
+                   "capacity_factor": cfg.cf, "parallelism": f"ep{args.gpus}"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": len(os.sched_getaffinity(0)),
+                         "kind": "oracle",
+                         "sample": f"each step = one fwd+bwd of the fp64 NumPy oracle on the first "
+                                   f"{n_tok} tokens of the workload (all experts, full d/f)"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out))
+
+
+# ---------------------------------------------------------------------------- a2a sweep
+def run_a2a(args):
+    """Config 5: equal-split all-to-all of a bf16 send buffer, 64 KB .. 1 GB per rank:
+    our NVSwitch peer-store dispatch (moe_dispatch, one expert per rank, no capacity)
+    vs torch.distributed.all_to_all_single (NCCL).  Reports algbw / busbw (nccl-tests)."""
+    world, rank, local = dist_env()
+    dist = init_dist(world, local)
+    torch.cuda.set_device(local)
+    from paper_2605_05049_b200 import _lib as L
+    assert world > 1, "--a2a needs torchrun with >= 2 ranks"
+    d = 4096
+    results = []
+    for p in range(16, 31, 1):
+        size = 1 << p
+        rows = size // (d * 2)
+        if rows < world or rows % world:
+            d_eff = 512
+            rows = size // (d_eff * 2)
+        else:
+            d_eff = d
+        T = rows  # tokens per rank, k=1, E = world (one expert per rank), balanced
+        shape = L.make_shape(T, d_eff, world, 1, 128, 0, 0.0, world, rank)
+        R = L.moe_recv_rows_max(shape)
+        ctx = L.Context(shape, local, 2 * R * d_eff * 2 + 4 * 4096)
+        from paper_2605_05049_b200.layer import _all_gather_bytes
+        ctx.open_peers(_all_gather_bytes(ctx.export_handle()))
+        xr = ctx.symm_empty((R, d_eff), torch.bfloat16)
+        xs = torch.randn((T, d_eff), device="cuda").to(torch.bfloat16)
+        counts = torch.full((world,), T // world, dtype=torch.int32, device="cuda")
+        layout = torch.zeros((L.moe_layout_ints(shape),), dtype=torch.int32, device="cuda")
+        ref_out = torch.empty_like(xs)
+        for _ in range(3):
+            L.moe_dispatch(ctx, xs, counts, layout, xr)
+            dist.all_to_all_single(ref_out, xs)
+        torch.cuda.synchronize()
+        ok = torch.equal(xr[:T], ref_out)
+        it = 20
+        dist.barrier(); torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(it):
+            L.moe_dispatch(ctx, xs, counts, layout, xr)
+        e.record(); torch.cuda.synchronize()
+        t_ours = s.elapsed_time(e) / it
+        dist.barrier(); torch.cuda.synchronize()
+        s.record()
+        for _ in range(it):
+            dist.all_to_all_single(ref_out, xs)
+        e.record(); torch.cuda.synchronize()
+        t_nccl = s.elapsed_time(e) / it
+        v = torch.tensor([t_ours, t_nccl], dtype=torch.float64, device="cuda")
+        dist.all_reduce(v, op=dist.ReduceOp.MAX)
+        t_ours, t_nccl = v.tolist()
+        nbytes = T * d_eff * 2
+        bus = (world - 1) / world
+        results.append({"bytes_per_rank": nbytes, "bitwise_equal_nccl": bool(ok),
+                        "ours_ms": t_ours, "nccl_ms": t_nccl,
+                        "ours_busbw_GBs": nbytes / (t_ours * 1e-3) / 1e9 * bus,
+                        "nccl_busbw_GBs": nbytes / (t_nccl * 1e-3) / 1e9 * bus})
+        ctx.close()
+    if rank == 0:
+        print(json.dumps({"metric": "dispatch all-to-all busbw vs NCCL", "n_gpus": world,
+                          "unit": "GB/s", "nvlink_peak_GBs": 900, "sweep": results}))
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    elif args.a2a:
+        run_a2a(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,228 @@
+/*
+ * moe.h -- C ABI of the B200-native expert-parallel MoE layer (libmoe.so).
+ *
+ * The hot path of arxiv 2605.05049 ("Piper"): one MoE layer under expert
+ * parallelism ("expert data parallelism"; PAPER.md:351-365
+ * dispatch/combine all-to-alls), forward and backward, on 1/2/4/8 B200s of one
+ * NVSwitch box.  Step names follow SURVEY.md §8(a): F0 router logits, F1 route,
+ * F2 permute, F3 dispatch, F4 expert FFN, F5 combine, F6 unpermute, and the
+ * backward twins B0..B6.  Symbols follow PAPER.md Table II.
+ *
+ * Conventions (all entry points)
+ * ------------------------------
+ * - Pointers named x, w_*, logits, ... are DEVICE pointers on the ctx's device;
+ *   `stream` is a cudaStream_t (0 = legacy default stream).  Every call is
+ *   stream-ordered and asynchronous: the returned status covers host-side
+ *   validation and launch only.  Device-side conditions (flag timeout, receive
+ *   overflow) set a device error word read by moe_ctx_get_device_error().
+ * - The caller owns every buffer.  Buffers that a PEER writes into (the
+ *   destinations of the four all-to-alls: xr, ys, dout_r, dxs) must come from
+ *   moe_symm_alloc(); otherwise the call returns MOE_ERR_NOT_SYMMETRIC.
+ * - Validation happens before any launch: MOE_ERR_INVALID_ARG for ep_size not in
+ *   {1,2,4,8}, EP does not divide E, k < 1 or k > E,
+ *   ep_rank outside [0,EP), d or f not a multiple of 64 (TMA/UMMA K-blocks of 64
+ *   bf16), T_local < 0, or a NULL required pointer.  T_local = 0 is legal; the
+ *   collective calls still take part in the exchange.
+ * - Collective calls (moe_dispatch, moe_dispatch_bwd, moe_combine,
+ *   moe_combine_bwd, moe_symm_alloc) must be issued by every EP rank in the same
+ *   order, like NCCL collectives.  Not thread-safe; one ctx per (process, GPU).
+ * - Determinism: identical inputs give bit-identical outputs on every call (no
+ *   float atomics, fixed reduction orders); buffers may be reused across calls.
+ * - Dtypes: bf16 activations/weights/messages (moe_bf16 = raw bf16 bits), fp32
+ *   logits/gates/weight gradients, int32 indices and counts.
+ *
+ * Layouts
+ * -------
+ * Expert weights, K-major ("transposed") for the tensor cores:
+ *   w_gu   [G, 2f, d]  rows 0..f-1 = W_gate^T, rows f..2f-1 = W_up^T
+ *   w_down [G, d, f]   = W_down^T
+ *   w_r    [E, d]      = W_r^T (router)
+ * Send layout (per source rank): rows of xs/ys/dxs are grouped by global
+ *   expert e; expert e's kept rows occupy [off[e], off[e]+counts[e]) with
+ *   off = exclusive scan of counts; inside an expert, rows are in assignment
+ *   order a = j*T_local + t (reading R5, slot-major).
+ * Receive layout (per owner rank): local expert e_l (global e = ep_rank*E_l+e_l)
+ *   owns the segment [seg_base[e_l], seg_base[e_l+1]), seg_base[0] = 0,
+ *   seg_base[e_l+1] = seg_base[e_l] + roundup(expert_rows[e_l], MOE_ALIGN_ROWS).
+ *   Inside a segment rows are ordered (source rank r, position p); rows past
+ *   expert_rows[e_l] are padding and are ZERO in xr and dout_r after the
+ *   transfer (reading R7; the padding makes every expert a whole number of
+ *   128-row UMMA tiles).
+ * Layout record (int32, moe_layout_ints() entries, written by moe_dispatch):
+ *   [MOE_LAYOUT_COUNTS_ALL  .. +EP*E)   counts_all[r][e]  kept rows from source r to expert e
+ *   [MOE_LAYOUT_EXPERT_ROWS .. +E_l)    expert_rows[e_l]  rows received by local expert e_l
+ *   [MOE_LAYOUT_SEG_BASE    .. +E_l+1)  seg_base[e_l]     segment starts (see above)
+ */
+#ifndef MOE_H_
+#define MOE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef uint16_t moe_bf16;       /* raw bfloat16 bits */
+typedef void* moe_stream;        /* cudaStream_t */
+
+#define MOE_ALIGN_ROWS 128       /* receive-segment alignment (rows) */
+#define MOE_IPC_HANDLE_BYTES 64  /* size of one exported symmetric-heap handle */
+#define MOE_MAX_EP 8
+
+typedef enum {
+  MOE_OK = 0,
+  MOE_ERR_INVALID_ARG = 1,
+  MOE_ERR_CUDA = 2,
+  MOE_ERR_NOT_SYMMETRIC = 3,   /* all-to-all destination not from moe_symm_alloc */
+  MOE_ERR_OUT_OF_MEMORY = 4,   /* symmetric heap exhausted */
+  MOE_ERR_RECV_OVERFLOW = 5,   /* device-side: receive rows beyond the buffer */
+  MOE_ERR_TIMEOUT = 6,         /* device-side: a peer flag never arrived (10 s) */
+  MOE_ERR_NOT_READY = 7        /* collective call before moe_ctx_open_peers */
+} moe_status;
+
+enum { MOE_LAYOUT_COUNTS_ALL = 0, MOE_LAYOUT_EXPERT_ROWS = 1, MOE_LAYOUT_SEG_BASE = 2 };
+
+/* Problem statement, Table II symbols + the capacity factor. */
+typedef struct {
+  int64_t T_local;          /* T_r = b*s/EP tokens on this rank (reading R10) */
+  int32_t d;                /* hidden size d_model */
+  int32_t E;                /* routed experts */
+  int32_t k;                /* top-k */
+  int32_t f;                /* expert FFN width d_ffn^MoE */
+  int32_t E_shared;         /* E_s always-active shared experts (width f each; local) */
+  float capacity_factor;    /* cf > 0: C = ceil(cf*k*T_local/E) per (source, expert); cf <= 0: dropless */
+  int32_t ep_size;          /* EP degree (1, 2, 4 or 8) */
+  int32_t ep_rank;          /* rank in the EP group */
+} moe_shape;
+
+typedef struct moe_ctx moe_ctx;   /* opaque: symmetric heap, peer table, flags, scratch */
+
+/* ---------------- context ---------------- */
+
+/* Creates a ctx on `device` and allocates its symmetric heap of `symm_heap_bytes`
+ * (plus an internal region for the count matrix and flags).  EP=1 needs no peers. */
+moe_status moe_ctx_create(moe_ctx** ctx, const moe_shape* shape, int device, size_t symm_heap_bytes);
+/* Writes MOE_IPC_HANDLE_BYTES bytes identifying this rank's heap (cudaIpcMemHandle). */
+moe_status moe_ctx_export_handle(moe_ctx* ctx, void* handle_out);
+/* handles = ep_size * MOE_IPC_HANDLE_BYTES bytes in rank order (all-gathered by the
+ * caller, e.g. over torch.distributed); maps every peer's heap.  Collective. */
+moe_status moe_ctx_open_peers(moe_ctx* ctx, const void* handles);
+/* Bump allocation from the symmetric heap, 256-byte aligned.  Collective: every rank
+ * must request the same sizes in the same order so offsets agree. */
+moe_status moe_symm_alloc(moe_ctx* ctx, size_t bytes, void** ptr);
+/* Synchronises the device; returns MOE_OK or the first device-side error recorded. */
+moe_status moe_ctx_get_device_error(moe_ctx* ctx);
+moe_status moe_ctx_destroy(moe_ctx* ctx);
+const char* moe_status_string(moe_status status);
+
+/* Derived sizes (host-only; no ctx needed). */
+int64_t moe_capacity(const moe_shape* shape);        /* C, or -1 when dropless */
+int64_t moe_recv_rows_max(const moe_shape* shape);   /* rows to allocate for xr / dout_r / dxr */
+int64_t moe_layout_ints(const moe_shape* shape);     /* int32 entries of a layout record */
+int64_t moe_layout_offset(const moe_shape* shape, int field);
+
+/* ---------------- F0 / B0 router ("routing") ---------------- */
+
+/* logits[t,e] = sum_c x[t,c] w_r[e,c] (+ bias[e]); bf16 x bf16 -> fp32 on the tensor
+ * cores.  x [T_local,d], w_r [E,d], bias [E] fp32 or NULL, logits [T_local,E] fp32. */
+moe_status moe_router_logits(moe_ctx* ctx, const moe_bf16* x, const moe_bf16* w_r,
+                             const float* bias_or_null, float* logits, moe_stream stream);
+/* dx_router[t,c] = sum_e dlogits[t,e] w_r[e,c]   (fp32 [T_local,d], overwritten);
+ * dw_r[e,c] (+)= sum_t dlogits[t,e] x[t,c]       (fp32 [E,d]; accumulate != 0 adds). */
+moe_status moe_router_logits_bwd(moe_ctx* ctx, const moe_bf16* x, const moe_bf16* w_r,
+                                 const float* dlogits, float* dx_router, float* dw_r,
+                                 int accumulate, moe_stream stream);
+
+/* ---------------- F1 / B1 route: top-k gating ---------------- */
+
+/* Per token: the k largest fp32 logits ordered by descending value, ties to the lower
+ * expert index (-0.0 == +0.0, NaN below -inf; readings R2, R3); gates = softmax over
+ * the k selected logits (k > 1) or the full-softmax probability of the top expert
+ * (k = 1) (reading R1).  logits [T_local,E] -> topk_idx [T_local,k] int32,
+ * gates [T_local,k] fp32.  Indices are bit-exact functions of the logits. */
+moe_status moe_route(moe_ctx* ctx, const float* logits, int32_t* topk_idx, float* gates,
+                     moe_stream stream);
+/* dlogits[t,e_j] = g_j (dg_j - sum_i g_i dg_i), zero elsewhere (k > 1); k = 1 uses the
+ * full softmax and reads `logits` (may be NULL when k > 1).  dlogits [T_local,E] fp32. */
+moe_status moe_route_bwd(moe_ctx* ctx, const float* logits, const int32_t* topk_idx,
+                         const float* gates, const float* dgates, float* dlogits,
+                         moe_stream stream);
+
+/* ---------------- F2 / B2 permute (PAPER.md:129 token dropping, 231 s_e) ---------------- */
+
+/* Histogram, scan, capacity and scatter, per source rank (readings R4, R5):
+ * p(t,j) = #earlier assignments a' < a = j*T_local+t on the same expert; kept iff
+ * p < C; counts[e] = #kept; dest_row[t,j] = off[e] + p or -1 (dropped);
+ * xs[dest_row[t,j]] = x[t] (bit copy).  counts [E] int32, dest_row [T_local,k] int32,
+ * xs [T_local*k, d] bf16 (rows [0, sum counts) written). */
+moe_status moe_permute(moe_ctx* ctx, const moe_bf16* x, const int32_t* topk_idx,
+                       int32_t* counts, int32_t* dest_row, moe_bf16* xs, moe_stream stream);
+/* dx[t] = bf16( sum_{j kept} dxs[dest_row[t,j]]  (fp32, j order)
+ *               + dx_acc[t] (fp32, optional) + dx_extra[t] (bf16, optional) ), one rounding. */
+moe_status moe_permute_bwd(moe_ctx* ctx, const moe_bf16* dxs, const int32_t* dest_row,
+                           const float* dx_acc_or_null, const moe_bf16* dx_extra_or_null,
+                           moe_bf16* dx, moe_stream stream);
+
+/* ---------------- F3 / B3 dispatch all-to-all ---------------- */
+
+/* Collective.  Exchanges counts into the [EP x E] matrix, writes the layout record,
+ * then stores every send row of xs directly into its owner's xr (NVSwitch peer
+ * stores; local rows by plain stores) at the receive layout above, zeroes xr's
+ * padding rows, and waits until all peers' rows have landed.  xr: symmetric,
+ * moe_recv_rows_max() rows. */
+moe_status moe_dispatch(moe_ctx* ctx, const moe_bf16* xs, const int32_t* counts,
+                        int32_t* layout, moe_bf16* xr, moe_stream stream);
+/* Collective.  Reverse pattern: owner rows of dxr go back to the same send-layout rows
+ * of each source's dxs (symmetric, [T_local*k, d]). */
+moe_status moe_dispatch_bwd(moe_ctx* ctx, const moe_bf16* dxr, const int32_t* layout,
+                            moe_bf16* dxs, moe_stream stream);
+
+/* ---------------- F4 / B4 grouped SwiGLU expert FFN -------- */
+
+/* For each group g (a local expert, or the shared experts as one group of width f):
+ *   G = X_g W_gate, U = X_g W_up, H = silu(G)*U, O_g = H W_down   (reading R8)
+ * X_g = rows [seg_base[g], seg_base[g]+group_rows[g]) of xr with seg_base the
+ * MOE_ALIGN_ROWS-aligned prefix of group_rows (device int32 [n_groups]).  bf16 operands,
+ * fp32 accumulation in TMEM (tcgen05), one bf16 rounding per output.
+ *   g_u_h [rows_cap, 3f] bf16 saved for backward: cols [0,f)=G, [f,2f)=U, [2f,3f)=H
+ *   out   [rows_cap, d]  bf16
+ * Padding rows inside a segment are written as zeros; nothing at or beyond rows_cap is
+ * written.  f must be a multiple of 128. */
+moe_status moe_expert_ffn(moe_ctx* ctx, const moe_bf16* xr, const int32_t* group_rows,
+                          int32_t n_groups, int64_t rows_cap, int32_t f,
+                          const moe_bf16* w_gu, const moe_bf16* w_down,
+                          moe_bf16* g_u_h, moe_bf16* out, moe_stream stream);
+/* Backward of moe_expert_ffn given dout [rows_cap, d] (padding rows must be zero):
+ *   dH = dout W_down^T; dG = dH*U*silu'(G); dU = dH*silu(G)   -> dgu [rows_cap, 2f] bf16
+ *   dxr = dG W_gate^T + dU W_up^T                              -> [rows_cap, d] bf16
+ *   dw_down[g] (+)= H^T dout, dw_gu[g] (+)= X^T [dG dU]        -> fp32, same layouts as
+ *   the weights; accumulate != 0 adds to the existing values.  dgu is caller scratch. */
+moe_status moe_expert_ffn_bwd(moe_ctx* ctx, const moe_bf16* xr, const int32_t* group_rows,
+                              int32_t n_groups, int64_t rows_cap, int32_t f,
+                              const moe_bf16* w_gu, const moe_bf16* w_down,
+                              const moe_bf16* g_u_h, const moe_bf16* dout, moe_bf16* dgu,
+                              moe_bf16* dxr, float* dw_gu, float* dw_down, int accumulate,
+                              moe_stream stream);
+
+/* ---------------- F5+F6 / B6+B5 combine ("same communication in the
+ * reverse direction") ---------------- */
+
+/* Collective.  Owner rows of `out` go back to the same send-layout rows of each
+ * source's ys (symmetric [T_local*k, d]); then
+ *   y[t] = bf16( sum_{j kept} gates[t,j] * ys[dest_row[t,j]] (fp32, j order)
+ *                + y_extra[t] (bf16 shared-expert output, optional) ). */
+moe_status moe_combine(moe_ctx* ctx, const moe_bf16* out, const int32_t* layout,
+                       moe_bf16* ys, const float* gates, const int32_t* dest_row,
+                       const moe_bf16* y_extra_or_null, moe_bf16* y, moe_stream stream);
+/* Collective.  dgates[t,j] = <dy[t], ys[dest_row[t,j]]> (fp32; 0 for dropped slots);
+ * dO rows g[t,j]*dy[t] (bf16) are stored straight into their owner's dout_r
+ * (symmetric, moe_recv_rows_max() rows; padding rows zeroed) at the receive layout. */
+moe_status moe_combine_bwd(moe_ctx* ctx, const moe_bf16* dy, const float* gates,
+                           const int32_t* dest_row, const moe_bf16* ys, const int32_t* layout,
+                           float* dgates, moe_bf16* dout_r, moe_stream stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MOE_H_ */

@@ -140,10 +140,13 @@ def route_bwd(topk_idx, gates, dgates, E, logits=None):
 
 
 def capacity(cf, k, T_r, E):
-    """C = ceil(cf*k*T_r/E) evaluated in fp64, or None (dropless) for cf <= 0."""
-    if cf <= 0:
+    """C = ceil(cf*k*T_r/E) evaluated in fp64 from the fp32 value of cf (the capacity
+    factor is an fp32 number of the problem statement, include/moe.h), or None
+    (dropless) for cf <= 0.  E.g. cf=0.6 is 0.60000002384 in fp32: C(k=2,T=1500,E=8)=226."""
+    cf32 = float(np.float32(cf))
+    if cf32 <= 0:
         return None
-    return int(math.ceil(float(cf) * k * T_r / E))
+    return int(math.ceil(cf32 * k * T_r / E))
 
 
 def positions(topk_idx_r, E, C):

@@ -1,0 +1,294 @@
+"""ctypes binding of libmoe.so (include/moe.h) -- argument marshalling only.
+
+Every function here has the name of the C entry point it calls, takes torch
+tensors (device memory owned by the caller) and passes their raw pointers and
+the current CUDA stream.  No step of the layer is computed in Python.  If the
+library is missing the import fails loudly: there is no fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmoe.so")
+
+MOE_ALIGN_ROWS = 128
+MOE_IPC_HANDLE_BYTES = 64
+LAYOUT_COUNTS_ALL, LAYOUT_EXPERT_ROWS, LAYOUT_SEG_BASE = 0, 1, 2
+
+_STATUS = {
+    0: "MOE_OK", 1: "MOE_ERR_INVALID_ARG", 2: "MOE_ERR_CUDA", 3: "MOE_ERR_NOT_SYMMETRIC",
+    4: "MOE_ERR_OUT_OF_MEMORY", 5: "MOE_ERR_RECV_OVERFLOW", 6: "MOE_ERR_TIMEOUT",
+    7: "MOE_ERR_NOT_READY",
+}
+
+
+class MoEError(RuntimeError):
+    def __init__(self, fn, code):
+        super().__init__(f"{fn} failed: {_STATUS.get(code, code)}")
+        self.code = code
+
+
+class moe_shape(ctypes.Structure):
+    _fields_ = [
+        ("T_local", ctypes.c_int64),
+        ("d", ctypes.c_int32),
+        ("E", ctypes.c_int32),
+        ("k", ctypes.c_int32),
+        ("f", ctypes.c_int32),
+        ("E_shared", ctypes.c_int32),
+        ("capacity_factor", ctypes.c_float),
+        ("ep_size", ctypes.c_int32),
+        ("ep_rank", ctypes.c_int32),
+    ]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} not found: build it with `python -m paper_2605_05049_b200.build` "
+            "(there is no CPU or eager fallback)")
+    return ctypes.CDLL(LIB_PATH)
+
+
+_lib = _load()
+P = ctypes.c_void_p
+I32, I64 = ctypes.c_int32, ctypes.c_int64
+
+_SIGS = {
+    "moe_ctx_create": [ctypes.POINTER(P), ctypes.POINTER(moe_shape), ctypes.c_int, ctypes.c_size_t],
+    "moe_ctx_export_handle": [P, P],
+    "moe_ctx_open_peers": [P, P],
+    "moe_symm_alloc": [P, ctypes.c_size_t, ctypes.POINTER(P)],
+    "moe_ctx_get_device_error": [P],
+    "moe_ctx_destroy": [P],
+    "moe_router_logits": [P, P, P, P, P, P],
+    "moe_router_logits_bwd": [P, P, P, P, P, P, ctypes.c_int, P],
+    "moe_route": [P, P, P, P, P],
+    "moe_route_bwd": [P, P, P, P, P, P, P],
+    "moe_permute": [P, P, P, P, P, P, P],
+    "moe_permute_bwd": [P, P, P, P, P, P, P],
+    "moe_dispatch": [P, P, P, P, P, P],
+    "moe_dispatch_bwd": [P, P, P, P, P],
+    "moe_expert_ffn": [P, P, P, I32, I64, I32, P, P, P, P, P],
+    "moe_expert_ffn_bwd": [P, P, P, I32, I64, I32, P, P, P, P, P, P, P, P, ctypes.c_int, P],
+    "moe_combine": [P, P, P, P, P, P, P, P, P],
+    "moe_combine_bwd": [P, P, P, P, P, P, P, P, P],
+}
+for _name, _args in _SIGS.items():
+    _f = getattr(_lib, _name)
+    _f.argtypes = _args
+    _f.restype = ctypes.c_int
+for _name in ("moe_capacity", "moe_recv_rows_max", "moe_layout_ints"):
+    getattr(_lib, _name).argtypes = [ctypes.POINTER(moe_shape)]
+    getattr(_lib, _name).restype = I64
+_lib.moe_layout_offset.argtypes = [ctypes.POINTER(moe_shape), ctypes.c_int]
+_lib.moe_layout_offset.restype = I64
+_lib.moe_status_string.argtypes = [ctypes.c_int]
+_lib.moe_status_string.restype = ctypes.c_char_p
+
+EXPORTED = sorted(list(_SIGS) + ["moe_capacity", "moe_recv_rows_max", "moe_layout_ints",
+                                 "moe_layout_offset", "moe_status_string"])
+
+
+def _check(fn, code):
+    if code != 0:
+        raise MoEError(fn, code)
+
+
+def _ptr(t, dtype=None, name="tensor"):
+    """Device pointer of a contiguous tensor (None -> NULL)."""
+    if t is None:
+        return None
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name}: expected a torch.Tensor")
+    if not t.is_cuda:
+        raise ValueError(f"{name}: must be a CUDA tensor (libmoe has no CPU path)")
+    if dtype is not None and t.dtype != dtype:
+        raise TypeError(f"{name}: expected {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name}: must be contiguous")
+    return t.data_ptr()
+
+
+def _stream(stream):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def make_shape(T_local, d, E, k, f, E_shared=0, capacity_factor=1.25, ep_size=1, ep_rank=0):
+    return moe_shape(int(T_local), int(d), int(E), int(k), int(f), int(E_shared),
+                     float(capacity_factor), int(ep_size), int(ep_rank))
+
+
+def moe_capacity(shape):
+    return _lib.moe_capacity(ctypes.byref(shape))
+
+
+def moe_recv_rows_max(shape):
+    return _lib.moe_recv_rows_max(ctypes.byref(shape))
+
+
+def moe_layout_ints(shape):
+    return _lib.moe_layout_ints(ctypes.byref(shape))
+
+
+def moe_layout_offset(shape, field):
+    return _lib.moe_layout_offset(ctypes.byref(shape), int(field))
+
+
+def moe_status_string(code):
+    return _lib.moe_status_string(int(code)).decode()
+
+
+class _CudaArray:
+    """Exposes a raw device pointer through __cuda_array_interface__ (zero copy)."""
+
+    def __init__(self, ptr, nbytes):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1",
+                                         "data": (ptr, False), "version": 3, "strides": None}
+
+
+class Context:
+    """Owns a moe_ctx (symmetric heap, peer table, flags).  One per (process, GPU)."""
+
+    def __init__(self, shape: moe_shape, device: int, heap_bytes: int):
+        self.shape = shape
+        self.device = int(device)
+        self._h = P()
+        _check("moe_ctx_create", _lib.moe_ctx_create(ctypes.byref(self._h), ctypes.byref(shape),
+                                                     self.device, int(heap_bytes)))
+        self._views = []
+
+    @property
+    def handle(self):
+        return self._h
+
+    def export_handle(self) -> bytes:
+        buf = ctypes.create_string_buffer(MOE_IPC_HANDLE_BYTES)
+        _check("moe_ctx_export_handle", _lib.moe_ctx_export_handle(self._h, buf))
+        return buf.raw
+
+    def open_peers(self, handles: bytes):
+        buf = ctypes.create_string_buffer(bytes(handles), len(handles))
+        _check("moe_ctx_open_peers", _lib.moe_ctx_open_peers(self._h, buf))
+
+    def symm_empty(self, shape, dtype) -> torch.Tensor:
+        """A tensor in the symmetric heap (collective: same calls on every rank)."""
+        numel = 1
+        for s in shape:
+            numel *= int(s)
+        elem = torch.empty((), dtype=dtype).element_size()
+        nbytes = max(numel * elem, 1)
+        p = P()
+        _check("moe_symm_alloc", _lib.moe_symm_alloc(self._h, nbytes, ctypes.byref(p)))
+        raw = torch.as_tensor(_CudaArray(p.value, nbytes), device=f"cuda:{self.device}")
+        t = raw[: numel * elem].view(dtype).view(*shape)
+        self._views.append(raw)
+        return t
+
+    def device_error(self):
+        return _lib.moe_ctx_get_device_error(self._h)
+
+    def check_device_error(self):
+        _check("moe_ctx_get_device_error", self.device_error())
+
+    def close(self):
+        if self._h:
+            self._views.clear()
+            _lib.moe_ctx_destroy(self._h)
+            self._h = P()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+BF16, F32, I32T = torch.bfloat16, torch.float32, torch.int32
+
+
+def moe_router_logits(ctx, x, w_r, bias, logits, stream=None):
+    _check("moe_router_logits", _lib.moe_router_logits(
+        ctx.handle, _ptr(x, BF16, "x"), _ptr(w_r, BF16, "w_r"), _ptr(bias, F32, "bias"),
+        _ptr(logits, F32, "logits"), _stream(stream)))
+
+
+def moe_router_logits_bwd(ctx, x, w_r, dlogits, dx_router, dw_r, accumulate=False, stream=None):
+    _check("moe_router_logits_bwd", _lib.moe_router_logits_bwd(
+        ctx.handle, _ptr(x, BF16, "x"), _ptr(w_r, BF16, "w_r"), _ptr(dlogits, F32, "dlogits"),
+        _ptr(dx_router, F32, "dx_router"), _ptr(dw_r, F32, "dw_r"), int(bool(accumulate)),
+        _stream(stream)))
+
+
+def moe_route(ctx, logits, topk_idx, gates, stream=None):
+    _check("moe_route", _lib.moe_route(ctx.handle, _ptr(logits, F32, "logits"),
+                                       _ptr(topk_idx, I32T, "topk_idx"), _ptr(gates, F32, "gates"),
+                                       _stream(stream)))
+
+
+def moe_route_bwd(ctx, logits, topk_idx, gates, dgates, dlogits, stream=None):
+    _check("moe_route_bwd", _lib.moe_route_bwd(
+        ctx.handle, _ptr(logits, F32, "logits"), _ptr(topk_idx, I32T, "topk_idx"),
+        _ptr(gates, F32, "gates"), _ptr(dgates, F32, "dgates"), _ptr(dlogits, F32, "dlogits"),
+        _stream(stream)))
+
+
+def moe_permute(ctx, x, topk_idx, counts, dest_row, xs, stream=None):
+    _check("moe_permute", _lib.moe_permute(
+        ctx.handle, _ptr(x, BF16, "x"), _ptr(topk_idx, I32T, "topk_idx"), _ptr(counts, I32T, "counts"),
+        _ptr(dest_row, I32T, "dest_row"), _ptr(xs, BF16, "xs"), _stream(stream)))
+
+
+def moe_permute_bwd(ctx, dxs, dest_row, dx_acc, dx_extra, dx, stream=None):
+    _check("moe_permute_bwd", _lib.moe_permute_bwd(
+        ctx.handle, _ptr(dxs, BF16, "dxs"), _ptr(dest_row, I32T, "dest_row"),
+        _ptr(dx_acc, F32, "dx_acc"), _ptr(dx_extra, BF16, "dx_extra"), _ptr(dx, BF16, "dx"),
+        _stream(stream)))
+
+
+def moe_dispatch(ctx, xs, counts, layout, xr, stream=None):
+    _check("moe_dispatch", _lib.moe_dispatch(
+        ctx.handle, _ptr(xs, BF16, "xs"), _ptr(counts, I32T, "counts"), _ptr(layout, I32T, "layout"),
+        _ptr(xr, BF16, "xr"), _stream(stream)))
+
+
+def moe_dispatch_bwd(ctx, dxr, layout, dxs, stream=None):
+    _check("moe_dispatch_bwd", _lib.moe_dispatch_bwd(
+        ctx.handle, _ptr(dxr, BF16, "dxr"), _ptr(layout, I32T, "layout"), _ptr(dxs, BF16, "dxs"),
+        _stream(stream)))
+
+
+def moe_expert_ffn(ctx, xr, group_rows, n_groups, rows_cap, f, w_gu, w_down, g_u_h, out, stream=None):
+    _check("moe_expert_ffn", _lib.moe_expert_ffn(
+        ctx.handle, _ptr(xr, BF16, "xr"), _ptr(group_rows, I32T, "group_rows"), int(n_groups),
+        int(rows_cap), int(f), _ptr(w_gu, BF16, "w_gu"), _ptr(w_down, BF16, "w_down"),
+        _ptr(g_u_h, BF16, "g_u_h"), _ptr(out, BF16, "out"), _stream(stream)))
+
+
+def moe_expert_ffn_bwd(ctx, xr, group_rows, n_groups, rows_cap, f, w_gu, w_down, g_u_h, dout, dgu,
+                       dxr, dw_gu, dw_down, accumulate=False, stream=None):
+    _check("moe_expert_ffn_bwd", _lib.moe_expert_ffn_bwd(
+        ctx.handle, _ptr(xr, BF16, "xr"), _ptr(group_rows, I32T, "group_rows"), int(n_groups),
+        int(rows_cap), int(f), _ptr(w_gu, BF16, "w_gu"), _ptr(w_down, BF16, "w_down"),
+        _ptr(g_u_h, BF16, "g_u_h"), _ptr(dout, BF16, "dout"), _ptr(dgu, BF16, "dgu"),
+        _ptr(dxr, BF16, "dxr"), _ptr(dw_gu, F32, "dw_gu"), _ptr(dw_down, F32, "dw_down"),
+        int(bool(accumulate)), _stream(stream)))
+
+
+def moe_combine(ctx, out, layout, ys, gates, dest_row, y_extra, y, stream=None):
+    _check("moe_combine", _lib.moe_combine(
+        ctx.handle, _ptr(out, BF16, "out"), _ptr(layout, I32T, "layout"), _ptr(ys, BF16, "ys"),
+        _ptr(gates, F32, "gates"), _ptr(dest_row, I32T, "dest_row"), _ptr(y_extra, BF16, "y_extra"),
+        _ptr(y, BF16, "y"), _stream(stream)))
+
+
+def moe_combine_bwd(ctx, dy, gates, dest_row, ys, layout, dgates, dout_r, stream=None):
+    _check("moe_combine_bwd", _lib.moe_combine_bwd(
+        ctx.handle, _ptr(dy, BF16, "dy"), _ptr(gates, F32, "gates"), _ptr(dest_row, I32T, "dest_row"),
+        _ptr(ys, BF16, "ys"), _ptr(layout, I32T, "layout"), _ptr(dgates, F32, "dgates"),
+        _ptr(dout_r, BF16, "dout_r"), _stream(stream)))

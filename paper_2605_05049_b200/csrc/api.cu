@@ -1,0 +1,459 @@
+// api.cu -- the C ABI of libmoe (include/moe.h): validation, context, symmetric heap,
+// and the launch sequence of every hot-path step.  No compute happens on the host.
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "common.cuh"
+#include "internal.h"
+
+struct moe_ctx {
+  moe_shape s;
+  int device = 0;
+  int E_l = 0;
+  int64_t C = -1;
+  int64_t recv_rows = 0;
+  // symmetric heap: [internal: count matrix | flags][user allocations]
+  char* heap = nullptr;
+  size_t heap_bytes = 0;
+  size_t heap_used = 0;
+  size_t internal_bytes = 0;
+  int64_t countmat_off = 0;
+  int64_t flags_off = 0;
+  cudaIpcMemHandle_t handle;
+  char* peer_base[MOE_MAX_EP] = {};
+  bool peer_opened[MOE_MAX_EP] = {};
+  bool peers_ready = false;
+  uint64_t epoch = 0;
+  // device scratch
+  int32_t* d_err = nullptr;
+  int32_t* d_done = nullptr;
+  int32_t* d_scratch = nullptr;   // permute workspace
+  int32_t* d_rows_T = nullptr;    // one int32 = T_local (router GEMM group size)
+};
+
+namespace {
+
+using moe::CommArgs;
+
+moe_status cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return MOE_OK;
+  fprintf(stderr, "[libmoe] CUDA error: %s\n", cudaGetErrorString(e));
+  return MOE_ERR_CUDA;
+}
+
+#define MOE_TRY_CUDA(expr)                                 \
+  do {                                                     \
+    cudaError_t e_ = (expr);                               \
+    if (e_ != cudaSuccess) return cuda_status(e_);         \
+  } while (0)
+#define MOE_REQUIRE(cond)                                  \
+  do {                                                     \
+    if (!(cond)) return MOE_ERR_INVALID_ARG;               \
+  } while (0)
+
+bool shape_ok(const moe_shape* s) {
+  if (!s) return false;
+  if (s->ep_size != 1 && s->ep_size != 2 && s->ep_size != 4 && s->ep_size != 8) return false;
+  if (s->E <= 0 || s->E > 256 || s->E % s->ep_size) return false;   // EP | E
+  if (s->k < 1 || s->k > s->E || s->k > 32) return false;            // top_k <= E
+  if (s->ep_rank < 0 || s->ep_rank >= s->ep_size) return false;
+  if (s->d <= 0 || s->d % 64 || s->f <= 0 || s->f % 64) return false;
+  if (s->T_local < 0 || s->E_shared < 0) return false;
+  return true;
+}
+
+int64_t capacity_of(const moe_shape* s) {
+  if (s->capacity_factor <= 0.f) return -1;
+  // C = ceil(cf * k * T_r / E) in double (reading R4)
+  double c = static_cast<double>(s->capacity_factor) * s->k * static_cast<double>(s->T_local) / s->E;
+  int64_t ci = static_cast<int64_t>(c);
+  if (static_cast<double>(ci) < c) ++ci;
+  return ci;
+}
+
+int64_t recv_rows_of(const moe_shape* s) {
+  const int64_t EP = s->ep_size, E_l = s->E / s->ep_size;
+  int64_t rows = EP * s->T_local * (s->k < E_l ? s->k : E_l);
+  const int64_t C = capacity_of(s);
+  if (C >= 0 && EP * E_l * C < rows) rows = EP * E_l * C;
+  rows += E_l * (MOE_ALIGN_ROWS - 1);
+  return (rows + MOE_ALIGN_ROWS - 1) / MOE_ALIGN_ROWS * MOE_ALIGN_ROWS;
+}
+
+cudaStream_t st(moe_stream s) { return reinterpret_cast<cudaStream_t>(s); }
+
+bool in_heap(const moe_ctx* c, const void* p) {
+  const char* q = static_cast<const char*>(p);
+  return q >= c->heap + c->internal_bytes && q < c->heap + c->heap_bytes;
+}
+
+CommArgs comm_args(moe_ctx* c) {
+  CommArgs a;
+  memset(&a, 0, sizeof(a));
+  for (int q = 0; q < c->s.ep_size; ++q) a.peers.base[q] = c->peer_base[q];
+  a.ep = c->s.ep_size;
+  a.rank = c->s.ep_rank;
+  a.E = c->s.E;
+  a.E_l = c->E_l;
+  a.d = c->s.d;
+  a.T = c->s.T_local;
+  a.k = c->s.k;
+  a.flags = reinterpret_cast<uint64_t*>(c->heap + c->flags_off);
+  a.flags_off = c->flags_off;
+  a.countmat = reinterpret_cast<int32_t*>(c->heap + c->countmat_off);
+  a.countmat_off = c->countmat_off;
+  a.done = c->d_done;
+  a.err = c->d_err;
+  a.epoch = ++c->epoch;
+  return a;
+}
+
+moe_status set_device(moe_ctx* c) { return cuda_status(cudaSetDevice(c->device)); }
+
+int pick_bn(int n) {
+  if (n % 256 == 0) return 256;
+  if (n % 128 == 0) return 128;
+  return 64;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* moe_status_string(moe_status s) {
+  switch (s) {
+    case MOE_OK: return "MOE_OK";
+    case MOE_ERR_INVALID_ARG: return "MOE_ERR_INVALID_ARG";
+    case MOE_ERR_CUDA: return "MOE_ERR_CUDA";
+    case MOE_ERR_NOT_SYMMETRIC: return "MOE_ERR_NOT_SYMMETRIC";
+    case MOE_ERR_OUT_OF_MEMORY: return "MOE_ERR_OUT_OF_MEMORY";
+    case MOE_ERR_RECV_OVERFLOW: return "MOE_ERR_RECV_OVERFLOW";
+    case MOE_ERR_TIMEOUT: return "MOE_ERR_TIMEOUT";
+    case MOE_ERR_NOT_READY: return "MOE_ERR_NOT_READY";
+  }
+  return "MOE_ERR_UNKNOWN";
+}
+
+int64_t moe_capacity(const moe_shape* s) { return shape_ok(s) ? capacity_of(s) : -2; }
+int64_t moe_recv_rows_max(const moe_shape* s) { return shape_ok(s) ? recv_rows_of(s) : -1; }
+int64_t moe_layout_ints(const moe_shape* s) {
+  if (!shape_ok(s)) return -1;
+  const int64_t E_l = s->E / s->ep_size;
+  return static_cast<int64_t>(s->ep_size) * s->E + 2 * E_l + 1;
+}
+int64_t moe_layout_offset(const moe_shape* s, int field) {
+  if (!shape_ok(s)) return -1;
+  const int64_t E_l = s->E / s->ep_size, base = static_cast<int64_t>(s->ep_size) * s->E;
+  switch (field) {
+    case MOE_LAYOUT_COUNTS_ALL: return 0;
+    case MOE_LAYOUT_EXPERT_ROWS: return base;
+    case MOE_LAYOUT_SEG_BASE: return base + E_l;
+  }
+  return -1;
+}
+
+moe_status moe_ctx_create(moe_ctx** out, const moe_shape* shape, int device, size_t symm_heap_bytes) {
+  MOE_REQUIRE(out && shape_ok(shape));
+  *out = nullptr;
+  moe_ctx* c = new (std::nothrow) moe_ctx();
+  if (!c) return MOE_ERR_OUT_OF_MEMORY;
+  c->s = *shape;
+  c->device = device;
+  c->E_l = shape->E / shape->ep_size;
+  c->C = capacity_of(shape);
+  c->recv_rows = recv_rows_of(shape);
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) { delete c; return cuda_status(e); }
+  const int EP = shape->ep_size;
+  c->countmat_off = 0;
+  c->flags_off = ((2 * EP * shape->E * 4) + 255) / 256 * 256;
+  c->internal_bytes = ((c->flags_off + moe::kNumSlots * EP * 8) + 4095) / 4096 * 4096;
+  c->heap_bytes = c->internal_bytes + (symm_heap_bytes + 255) / 256 * 256;
+  c->heap_used = c->internal_bytes;
+  e = cudaMalloc(&c->heap, c->heap_bytes);
+  if (e == cudaSuccess) e = cudaMemset(c->heap, 0, c->internal_bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_err, 16);
+  if (e == cudaSuccess) e = cudaMemset(c->d_err, 0, 16);
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_done, 16);
+  if (e == cudaSuccess) e = cudaMemset(c->d_done, 0, 16);
+  const int64_t scratch = moe::permute_scratch_ints(shape->T_local, shape->k, shape->E);
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_scratch, scratch * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_rows_T, 16);
+  int32_t tl = static_cast<int32_t>(shape->T_local);
+  if (e == cudaSuccess) e = cudaMemcpy(c->d_rows_T, &tl, 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && EP > 1) e = cudaIpcGetMemHandle(&c->handle, c->heap);
+  if (e != cudaSuccess) {
+    moe_ctx_destroy(c);
+    return cuda_status(e);
+  }
+  c->peer_base[shape->ep_rank] = c->heap;
+  if (EP == 1) c->peers_ready = true;
+  *out = c;
+  return MOE_OK;
+}
+
+moe_status moe_ctx_export_handle(moe_ctx* c, void* handle_out) {
+  MOE_REQUIRE(c && handle_out);
+  static_assert(sizeof(cudaIpcMemHandle_t) == MOE_IPC_HANDLE_BYTES, "IPC handle size");
+  memcpy(handle_out, &c->handle, MOE_IPC_HANDLE_BYTES);
+  return MOE_OK;
+}
+
+moe_status moe_ctx_open_peers(moe_ctx* c, const void* handles) {
+  MOE_REQUIRE(c && (handles || c->s.ep_size == 1));
+  if (set_device(c) != MOE_OK) return MOE_ERR_CUDA;
+  const char* h = static_cast<const char*>(handles);
+  for (int q = 0; q < c->s.ep_size; ++q) {
+    if (q == c->s.ep_rank || c->peer_opened[q]) continue;
+    cudaIpcMemHandle_t hq;
+    memcpy(&hq, h + q * MOE_IPC_HANDLE_BYTES, MOE_IPC_HANDLE_BYTES);
+    void* p = nullptr;
+    MOE_TRY_CUDA(cudaIpcOpenMemHandle(&p, hq, cudaIpcMemLazyEnablePeerAccess));
+    c->peer_base[q] = static_cast<char*>(p);
+    c->peer_opened[q] = true;
+  }
+  c->peers_ready = true;
+  return MOE_OK;
+}
+
+moe_status moe_symm_alloc(moe_ctx* c, size_t bytes, void** ptr) {
+  MOE_REQUIRE(c && ptr);
+  const size_t sz = (bytes + 255) / 256 * 256;
+  if (c->heap_used + sz > c->heap_bytes) return MOE_ERR_OUT_OF_MEMORY;
+  *ptr = c->heap + c->heap_used;
+  c->heap_used += sz;
+  return MOE_OK;
+}
+
+moe_status moe_ctx_get_device_error(moe_ctx* c) {
+  MOE_REQUIRE(c);
+  if (set_device(c) != MOE_OK) return MOE_ERR_CUDA;
+  MOE_TRY_CUDA(cudaDeviceSynchronize());
+  int32_t v = 0;
+  MOE_TRY_CUDA(cudaMemcpy(&v, c->d_err, 4, cudaMemcpyDeviceToHost));
+  if (v == moe::kDevTimeout) return MOE_ERR_TIMEOUT;
+  if (v == moe::kDevOverflow) return MOE_ERR_RECV_OVERFLOW;
+  return MOE_OK;
+}
+
+moe_status moe_ctx_destroy(moe_ctx* c) {
+  if (!c) return MOE_OK;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  for (int q = 0; q < MOE_MAX_EP; ++q)
+    if (c->peer_opened[q]) cudaIpcCloseMemHandle(c->peer_base[q]);
+  cudaFree(c->heap);
+  cudaFree(c->d_err);
+  cudaFree(c->d_done);
+  cudaFree(c->d_scratch);
+  cudaFree(c->d_rows_T);
+  delete c;
+  return MOE_OK;
+}
+
+// ---------------------------------------------------------------- F0 / B0
+moe_status moe_router_logits(moe_ctx* c, const moe_bf16* x, const moe_bf16* w_r,
+                             const float* bias, float* logits, moe_stream s) {
+  MOE_REQUIRE(c && x && w_r && logits);
+  if (c->s.T_local == 0) return MOE_OK;
+  moe::GemmProblem g;
+  g.epi = moe::kEpiF32Rows;
+  const int E = c->s.E;
+  g.BN = E <= 16 ? 16 : E <= 64 ? 64 : E <= 128 ? 128 : 256;
+  g.a_ptr = x; g.a_rows = c->s.T_local; g.a_cols = c->s.d; g.a_ld = c->s.d;
+  g.b_ptr = w_r; g.b_rows = E; g.b_cols = c->s.d; g.b_ld = c->s.d;
+  g.b_group_stride = 0;
+  g.N = E; g.K = c->s.d;
+  g.group_rows = c->d_rows_T; g.n_groups = 1; g.rows_cap = c->s.T_local;
+  g.out = logits; g.ld_out = E;
+  g.bias = bias;
+  return cuda_status(moe::launch_grouped_gemm(g, st(s)));
+}
+
+moe_status moe_router_logits_bwd(moe_ctx* c, const moe_bf16* x, const moe_bf16* w_r,
+                                 const float* dlogits, float* dx_router, float* dw_r,
+                                 int accumulate, moe_stream s) {
+  MOE_REQUIRE(c && x && w_r && dlogits && (dx_router || dw_r));
+  return cuda_status(moe::launch_router_bwd(x, w_r, dlogits, c->s.T_local, c->s.d, c->s.E,
+                                            dx_router, dw_r, accumulate, st(s)));
+}
+
+// ---------------------------------------------------------------- F1 / B1
+moe_status moe_route(moe_ctx* c, const float* logits, int32_t* topk_idx, float* gates, moe_stream s) {
+  MOE_REQUIRE(c && logits && topk_idx && gates);
+  return cuda_status(moe::launch_route(logits, c->s.T_local, c->s.E, c->s.k, topk_idx, gates, st(s)));
+}
+
+moe_status moe_route_bwd(moe_ctx* c, const float* logits, const int32_t* topk_idx, const float* gates,
+                         const float* dgates, float* dlogits, moe_stream s) {
+  MOE_REQUIRE(c && topk_idx && gates && dgates && dlogits && (logits || c->s.k > 1));
+  return cuda_status(moe::launch_route_bwd(logits, topk_idx, gates, dgates, c->s.T_local, c->s.E,
+                                           c->s.k, dlogits, st(s)));
+}
+
+// ---------------------------------------------------------------- F2 / B2
+moe_status moe_permute(moe_ctx* c, const moe_bf16* x, const int32_t* topk_idx, int32_t* counts,
+                       int32_t* dest_row, moe_bf16* xs, moe_stream s) {
+  MOE_REQUIRE(c && x && topk_idx && counts && dest_row && xs);
+  return cuda_status(moe::launch_permute(x, topk_idx, c->s.T_local, c->s.d, c->s.E, c->s.k, c->C,
+                                         counts, dest_row, xs, c->d_scratch, st(s)));
+}
+
+moe_status moe_permute_bwd(moe_ctx* c, const moe_bf16* dxs, const int32_t* dest_row,
+                           const float* dx_acc, const moe_bf16* dx_extra, moe_bf16* dx, moe_stream s) {
+  MOE_REQUIRE(c && dxs && dest_row && dx);
+  return cuda_status(moe::launch_permute_bwd(dxs, dest_row, dx_acc, dx_extra, c->s.T_local, c->s.d,
+                                             c->s.k, dx, st(s)));
+}
+
+// ---------------------------------------------------------------- F3 / B3
+moe_status moe_dispatch(moe_ctx* c, const moe_bf16* xs, const int32_t* counts, int32_t* layout,
+                        moe_bf16* xr, moe_stream s) {
+  MOE_REQUIRE(c && xs && counts && layout && xr);
+  if (!c->peers_ready) return MOE_ERR_NOT_READY;
+  if (!in_heap(c, xr)) return MOE_ERR_NOT_SYMMETRIC;
+  CommArgs a = comm_args(c);
+  MOE_TRY_CUDA(moe::launch_counts_exchange(a, counts, layout, c->recv_rows, st(s)));
+  CommArgs b = comm_args(c);
+  const int64_t dst_off = reinterpret_cast<const char*>(xr) - c->heap;
+  MOE_TRY_CUDA(moe::launch_forward_transfer(b, layout, xs, dst_off, xr, nullptr, nullptr, nullptr,
+                                            nullptr, nullptr, 0, st(s)));
+  return cuda_status(moe::launch_wait_flags(b, moe::kSlotData, st(s)));
+}
+
+moe_status moe_dispatch_bwd(moe_ctx* c, const moe_bf16* dxr, const int32_t* layout, moe_bf16* dxs,
+                            moe_stream s) {
+  MOE_REQUIRE(c && dxr && layout && dxs);
+  if (!c->peers_ready) return MOE_ERR_NOT_READY;
+  if (!in_heap(c, dxs)) return MOE_ERR_NOT_SYMMETRIC;
+  CommArgs a = comm_args(c);
+  const int64_t dst_off = reinterpret_cast<const char*>(dxs) - c->heap;
+  MOE_TRY_CUDA(moe::launch_reverse_transfer(a, layout, dxr, dst_off, st(s)));
+  return cuda_status(moe::launch_wait_flags(a, moe::kSlotData, st(s)));
+}
+
+// ---------------------------------------------------------------- F4 / B4
+moe_status moe_expert_ffn(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows, int32_t n_groups,
+                          int64_t rows_cap, int32_t f, const moe_bf16* w_gu, const moe_bf16* w_down,
+                          moe_bf16* g_u_h, moe_bf16* out, moe_stream s) {
+  MOE_REQUIRE(c && xr && group_rows && w_gu && w_down && g_u_h && out);
+  MOE_REQUIRE(n_groups >= 1 && n_groups <= 256 && rows_cap >= 0 && f > 0 && f % 128 == 0);
+  if (rows_cap == 0) return MOE_OK;
+  const int d = c->s.d;
+  moe::GemmProblem g1;
+  g1.epi = moe::kEpiSwiGLU;
+  g1.BN = 256;
+  g1.a_ptr = xr; g1.a_rows = rows_cap; g1.a_cols = d; g1.a_ld = d;
+  g1.b_ptr = w_gu; g1.b_rows = static_cast<int64_t>(n_groups) * 2 * f; g1.b_cols = d; g1.b_ld = d;
+  g1.b_group_stride = 2 * f; g1.b_split = f;
+  g1.N = 2 * f; g1.K = d;
+  g1.group_rows = group_rows; g1.n_groups = n_groups; g1.rows_cap = rows_cap;
+  g1.out = g_u_h; g1.ld_out = 3 * static_cast<int64_t>(f); g1.f = f;
+  MOE_TRY_CUDA(moe::launch_grouped_gemm(g1, st(s)));
+  moe::GemmProblem g2;
+  g2.epi = moe::kEpiBF16;
+  g2.BN = pick_bn(d);
+  g2.a_ptr = g_u_h + 2 * static_cast<int64_t>(f); g2.a_rows = rows_cap; g2.a_cols = f;
+  g2.a_ld = 3 * static_cast<int64_t>(f);
+  g2.b_ptr = w_down; g2.b_rows = static_cast<int64_t>(n_groups) * d; g2.b_cols = f; g2.b_ld = f;
+  g2.b_group_stride = d;
+  g2.N = d; g2.K = f;
+  g2.group_rows = group_rows; g2.n_groups = n_groups; g2.rows_cap = rows_cap;
+  g2.out = out; g2.ld_out = d;
+  return cuda_status(moe::launch_grouped_gemm(g2, st(s)));
+}
+
+moe_status moe_expert_ffn_bwd(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows,
+                              int32_t n_groups, int64_t rows_cap, int32_t f, const moe_bf16* w_gu,
+                              const moe_bf16* w_down, const moe_bf16* g_u_h, const moe_bf16* dout,
+                              moe_bf16* dgu, moe_bf16* dxr, float* dw_gu, float* dw_down,
+                              int accumulate, moe_stream s) {
+  MOE_REQUIRE(c && xr && group_rows && w_gu && w_down && g_u_h && dout && dgu && dxr && dw_gu && dw_down);
+  MOE_REQUIRE(n_groups >= 1 && n_groups <= 256 && rows_cap >= 0 && f > 0 && f % 128 == 0);
+  const int d = c->s.d;
+  const int64_t F = f;
+  if (rows_cap == 0) {
+    if (!accumulate) {
+      MOE_TRY_CUDA(cudaMemsetAsync(dw_gu, 0, sizeof(float) * n_groups * 2 * F * d, st(s)));
+      MOE_TRY_CUDA(cudaMemsetAsync(dw_down, 0, sizeof(float) * n_groups * F * d, st(s)));
+    }
+    return MOE_OK;
+  }
+  // dgrad-1: dH = dout . W_down^T (+ dSwiGLU epilogue) -> dgu
+  moe::GemmProblem a;
+  a.epi = moe::kEpiDSwiGLU;
+  a.BN = (f % 256 == 0) ? 256 : 128;
+  a.b_mn = true;
+  a.a_ptr = dout; a.a_rows = rows_cap; a.a_cols = d; a.a_ld = d;
+  a.b_ptr = w_down; a.b_rows = static_cast<int64_t>(n_groups) * d; a.b_cols = f; a.b_ld = f;
+  a.b_group_stride = d;
+  a.N = f; a.K = d;
+  a.group_rows = group_rows; a.n_groups = n_groups; a.rows_cap = rows_cap;
+  a.out = dgu; a.ld_out = 2 * F; a.aux = g_u_h; a.ld_aux = 3 * F; a.f = f;
+  MOE_TRY_CUDA(moe::launch_grouped_gemm(a, st(s)));
+  // dgrad-2: dX = [dG dU] . W_gu  -> dxr
+  moe::GemmProblem b;
+  b.epi = moe::kEpiBF16;
+  b.BN = pick_bn(d);
+  b.b_mn = true;
+  b.a_ptr = dgu; b.a_rows = rows_cap; b.a_cols = 2 * F; b.a_ld = 2 * F;
+  b.b_ptr = w_gu; b.b_rows = static_cast<int64_t>(n_groups) * 2 * F; b.b_cols = d; b.b_ld = d;
+  b.b_group_stride = 2 * F;
+  b.N = d; b.K = 2 * f;
+  b.group_rows = group_rows; b.n_groups = n_groups; b.rows_cap = rows_cap;
+  b.out = dxr; b.ld_out = d;
+  MOE_TRY_CUDA(moe::launch_grouped_gemm(b, st(s)));
+  // wgrad: dW_down[g] = dout_g^T H_g   [d, f]
+  moe::GemmProblem w1;
+  w1.epi = moe::kEpiF32Group;
+  w1.BN = (f % 256 == 0) ? 256 : 128;
+  w1.a_mn = true; w1.b_mn = true;
+  w1.a_ptr = dout; w1.a_rows = rows_cap; w1.a_cols = d; w1.a_ld = d;
+  w1.b_ptr = g_u_h + 2 * F; w1.b_rows = rows_cap; w1.b_cols = f; w1.b_ld = 3 * F;
+  w1.M = d; w1.N = f;
+  w1.group_rows = group_rows; w1.n_groups = n_groups; w1.rows_cap = rows_cap;
+  w1.out = dw_down; w1.accumulate = accumulate;
+  MOE_TRY_CUDA(moe::launch_grouped_gemm(w1, st(s)));
+  // wgrad: dW_gu[g] = dgu_g^T X_g   [2f, d]
+  moe::GemmProblem w2;
+  w2.epi = moe::kEpiF32Group;
+  w2.BN = pick_bn(d);
+  w2.a_mn = true; w2.b_mn = true;
+  w2.a_ptr = dgu; w2.a_rows = rows_cap; w2.a_cols = 2 * F; w2.a_ld = 2 * F;
+  w2.b_ptr = xr; w2.b_rows = rows_cap; w2.b_cols = d; w2.b_ld = d;
+  w2.M = 2 * f; w2.N = d;
+  w2.group_rows = group_rows; w2.n_groups = n_groups; w2.rows_cap = rows_cap;
+  w2.out = dw_gu; w2.accumulate = accumulate;
+  return cuda_status(moe::launch_grouped_gemm(w2, st(s)));
+}
+
+// ---------------------------------------------------------------- F5+F6 / B6+B5
+moe_status moe_combine(moe_ctx* c, const moe_bf16* out, const int32_t* layout, moe_bf16* ys,
+                       const float* gates, const int32_t* dest_row, const moe_bf16* y_extra,
+                       moe_bf16* y, moe_stream s) {
+  MOE_REQUIRE(c && out && layout && ys && gates && dest_row && y);
+  if (!c->peers_ready) return MOE_ERR_NOT_READY;
+  if (!in_heap(c, ys)) return MOE_ERR_NOT_SYMMETRIC;
+  CommArgs a = comm_args(c);
+  const int64_t dst_off = reinterpret_cast<const char*>(ys) - c->heap;
+  MOE_TRY_CUDA(moe::launch_reverse_transfer(a, layout, out, dst_off, st(s)));
+  MOE_TRY_CUDA(moe::launch_wait_flags(a, moe::kSlotData, st(s)));
+  return cuda_status(moe::launch_unpermute(ys, gates, dest_row, y_extra, c->s.T_local, c->s.d,
+                                           c->s.k, y, st(s)));
+}
+
+moe_status moe_combine_bwd(moe_ctx* c, const moe_bf16* dy, const float* gates, const int32_t* dest_row,
+                           const moe_bf16* ys, const int32_t* layout, float* dgates, moe_bf16* dout_r,
+                           moe_stream s) {
+  MOE_REQUIRE(c && dy && gates && dest_row && ys && layout && dgates && dout_r);
+  if (!c->peers_ready) return MOE_ERR_NOT_READY;
+  if (!in_heap(c, dout_r)) return MOE_ERR_NOT_SYMMETRIC;
+  CommArgs a = comm_args(c);
+  const int64_t dst_off = reinterpret_cast<const char*>(dout_r) - c->heap;
+  MOE_TRY_CUDA(moe::launch_forward_transfer(a, layout, nullptr, dst_off, dout_r, dest_row, gates, dy,
+                                            ys, dgates, 1, st(s)));
+  return cuda_status(moe::launch_wait_flags(a, moe::kSlotData, st(s)));
+}
+
+}  // extern "C"

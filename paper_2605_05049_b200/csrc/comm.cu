@@ -1,0 +1,324 @@
+// comm.cu -- F3/F5 dispatch/combine and their backward twins over NVSwitch.
+//
+// The paper's all-to-alls (PAPER.md:132 four per layer; PAPER.md:351-356 volumes) are
+// implemented as direct peer stores into symmetric buffers: every rank maps every
+// peer's heap (cudaIpc), so a warp can write a 16-byte vector straight into a peer's
+// receive row over NVLink.  PAPER.md:134 notes the flat point-to-point all-to-all is
+// bandwidth-optimal on a uniform topology; one NVSwitch box is uniform, so there is
+// no hierarchical phase (HALO, is multi-node prior art).
+//
+// Two transfer patterns serve the four all-to-alls:
+//   forward  (dispatch, combine_bwd): source send-layout rows -> owner receive rows
+//   reverse  (combine, dispatch_bwd): owner receive rows -> source send-layout rows
+// Completion protocol per call (epoch = a per-call counter identical on all ranks):
+//   all blocks store rows -> fence.sc.sys -> block counter; the last block publishes
+//   flag[dst][slot][me] = epoch with st.release.sys on every rank; a 1-block wait
+//   kernel spins with ld.acquire.sys until every peer's flag reaches the epoch
+//   (bounded: 10 s, then MOE_ERR_TIMEOUT in the device error word).
+#include "common.cuh"
+#include "internal.h"
+
+namespace moe {
+namespace {
+
+constexpr uint64_t kTimeoutNs = 10ull * 1000 * 1000 * 1000;
+constexpr int kMaxE = 256;  // validated by the C-ABI (E <= 256)
+
+__device__ __forceinline__ uint64_t* peer_flag(const CommArgs& a, int q, int slot, int src) {
+  return reinterpret_cast<uint64_t*>(a.peers.base[q] + a.flags_off) + slot * a.ep + src;
+}
+
+__device__ __forceinline__ int upper_bound_idx(const int32_t* arr, int n, int64_t v) {
+  // largest i in [0, n) with arr[i] <= v  (arr ascending, arr[0] = 0)
+  int lo = 0, hi = n;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (arr[mid] <= v) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// Last block of a transfer kernel publishes the epoch to every destination rank.
+__device__ void signal_done(const CommArgs& a, int slot) {
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int prev = atomicAdd(a.done, 1);
+    if (prev == static_cast<int>(gridDim.x) - 1) {
+      *a.done = 0;
+      __threadfence_system();
+      for (int q = 0; q < a.ep; ++q) st_release_sys(peer_flag(a, q, slot, a.rank), a.epoch);
+    }
+  }
+}
+
+__device__ void wait_all(const CommArgs& a, int slot) {
+  if (threadIdx.x < a.ep) {
+    const uint64_t* f = a.flags + slot * a.ep + threadIdx.x;
+    const uint64_t t0 = globaltimer_ns();
+    while (ld_acquire_sys(f) < a.epoch) {
+      if (globaltimer_ns() - t0 > kTimeoutNs) {
+        set_device_error(a.err, kDevTimeout);
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  __threadfence();
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------- counts exchange
+// One block.  counts[E] of this rank -> row `rank` of every peer's count matrix
+// (parity buffer epoch&1), then wait for all rows, then write the layout record.
+__global__ void counts_exchange_kernel(CommArgs a, const int32_t* __restrict__ counts,
+                                       int32_t* __restrict__ layout, int64_t recv_rows_cap) {
+  const int parity = static_cast<int>(a.epoch & 1);
+  const int E = a.E, EP = a.ep, E_l = a.E_l;
+  for (int i = threadIdx.x; i < EP * E; i += blockDim.x) {
+    const int q = i / E, e = i % E;
+    int32_t* dst = reinterpret_cast<int32_t*>(a.peers.base[q] + a.countmat_off) +
+                   (parity * EP + a.rank) * E + e;
+    *dst = counts[e];
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x < EP) st_release_sys(peer_flag(a, threadIdx.x, kSlotCounts, a.rank), a.epoch);
+  wait_all(a, kSlotCounts);
+  const int32_t* cm = a.countmat + parity * EP * E;
+  for (int i = threadIdx.x; i < EP * E; i += blockDim.x) layout[i] = cm[i];
+  int32_t* expert_rows = layout + EP * E;
+  int32_t* seg_base = expert_rows + E_l;
+  __shared__ int32_t s_rows[kMaxE];
+  for (int el = threadIdx.x; el < E_l; el += blockDim.x) {
+    int32_t s = 0;
+    for (int r = 0; r < EP; ++r) s += cm[r * E + a.rank * E_l + el];
+    s_rows[el] = s;
+    expert_rows[el] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t run = 0;
+    for (int el = 0; el < E_l; ++el) {
+      seg_base[el] = static_cast<int32_t>(run);
+      run += (s_rows[el] + MOE_ALIGN_ROWS - 1) / MOE_ALIGN_ROWS * MOE_ALIGN_ROWS;
+    }
+    seg_base[E_l] = static_cast<int32_t>(run);
+    if (run > recv_rows_cap) set_device_error(a.err, kDevOverflow);
+  }
+}
+
+// Shared prologue: per-expert tables of the forward pattern for THIS source rank.
+//   s_off[e]  = exclusive scan of counts_all[rank][*]  (send layout)
+//   s_dst[e]  = row of (rank, p=0) of expert e in its owner's receive buffer
+struct FwdTables {
+  int32_t off[kMaxE + 1];
+  int32_t dst[kMaxE];
+  int32_t seg[kMaxE + 1];    // local receive segments (for padding)
+  int32_t rows[kMaxE];
+};
+
+__device__ void build_fwd_tables(const CommArgs& a, const int32_t* layout, FwdTables& t) {
+  const int E = a.E, EP = a.ep, E_l = a.E_l;
+  const int32_t* cm = layout;
+  // per-expert rows over all sources, and rows from sources before me
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int32_t all = 0, before = 0;
+    for (int r = 0; r < EP; ++r) {
+      const int32_t c = cm[r * E + e];
+      all += c;
+      if (r < a.rank) before += c;
+    }
+    t.rows[e] = all;
+    t.dst[e] = before;
+  }
+  __syncthreads();
+  if (threadIdx.x < EP) {  // owner q: aligned segment prefix over its experts
+    const int q = threadIdx.x;
+    int32_t run = 0;
+    for (int el = 0; el < E_l; ++el) {
+      const int e = q * E_l + el;
+      t.dst[e] += run;
+      run += (t.rows[e] + MOE_ALIGN_ROWS - 1) / MOE_ALIGN_ROWS * MOE_ALIGN_ROWS;
+    }
+  }
+  if (threadIdx.x == 32) {
+    int32_t run = 0;
+    for (int e = 0; e < E; ++e) {
+      t.off[e] = run;
+      run += cm[a.rank * E + e];
+    }
+    t.off[E] = run;
+  }
+  const int32_t* seg = layout + EP * E + E_l;
+  for (int i = threadIdx.x; i <= E_l; i += blockDim.x) t.seg[i] = seg[i];
+  __syncthreads();
+}
+
+__device__ __forceinline__ void copy_row(uint4* __restrict__ dst, const uint4* __restrict__ src,
+                                         int nvec, int lane) {
+#pragma unroll 4
+  for (int v = lane; v < nvec; v += 32) st_v4(dst + v, ld_nc_v4(src + v));
+}
+
+// Forward pattern.  mode 0: payload = src send row.  mode 1 (combine_bwd): payload of
+// slot (t,j) = gates[t,j] * dy[t] (bf16), and dgates[t,j] = <dy[t], ys[dest_row[t,j]]>.
+template <int MODE>
+__global__ void forward_transfer_kernel(CommArgs a, const int32_t* __restrict__ layout,
+                                        const uint16_t* __restrict__ src, int64_t dst_off,
+                                        uint16_t* __restrict__ local_dst,
+                                        const int32_t* __restrict__ dest_row,
+                                        const float* __restrict__ gates,
+                                        const uint16_t* __restrict__ dy,
+                                        const uint16_t* __restrict__ ys,
+                                        float* __restrict__ dgates) {
+  __shared__ FwdTables tb;
+  build_fwd_tables(a, layout, tb);
+  const int lane = threadIdx.x & 31;
+  const int64_t gwarp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int d = a.d;
+  const int nvec = d / 8;
+  const int64_t row_bytes = static_cast<int64_t>(d) * 2;
+  const int E = a.E, E_l = a.E_l;
+  // padding rows of the local receive buffer (zeroed every call)
+  const int64_t n_pad_rows = tb.seg[E_l];
+  const int64_t n_items = (MODE == 0) ? tb.off[E] : a.T;
+
+  for (int64_t w = gwarp; w < n_items + n_pad_rows; w += nwarps) {
+    if (w >= n_items) {
+      const int64_t row = w - n_items;
+      const int el = upper_bound_idx(tb.seg, E_l + 1, row);
+      const int64_t within = row - tb.seg[el];
+      if (within < tb.rows[a.rank * E_l + el]) continue;  // a data row, not padding
+      uint4* dst = reinterpret_cast<uint4*>(local_dst + row * d);
+      for (int v = lane; v < nvec; v += 32) dst[v] = make_uint4(0u, 0u, 0u, 0u);
+      continue;
+    }
+    if (MODE == 0) {
+      const int64_t row = w;
+      const int e = upper_bound_idx(tb.off, E + 1, row);
+      const int q = e / E_l;
+      const int64_t drow = tb.dst[e] + (row - tb.off[e]);
+      uint4* dst = reinterpret_cast<uint4*>(a.peers.base[q] + dst_off + drow * row_bytes);
+      copy_row(dst, reinterpret_cast<const uint4*>(src + row * d), nvec, lane);
+    } else {
+      const int64_t t = w;
+      for (int j = 0; j < a.k; ++j) {
+        const int32_t row = dest_row[t * a.k + j];
+        if (row < 0) {
+          if (lane == 0) dgates[t * a.k + j] = 0.f;
+          continue;
+        }
+        const float g = gates[t * a.k + j];
+        const int e = upper_bound_idx(tb.off, E + 1, row);
+        const int q = e / E_l;
+        const int64_t drow = tb.dst[e] + (row - tb.off[e]);
+        uint4* dst = reinterpret_cast<uint4*>(a.peers.base[q] + dst_off + drow * row_bytes);
+        const uint4* pdy = reinterpret_cast<const uint4*>(dy + t * d);
+        const uint4* pys = reinterpret_cast<const uint4*>(ys + static_cast<int64_t>(row) * d);
+        float dot = 0.f;
+        for (int v = lane; v < nvec; v += 32) {
+          const uint4 a4 = ld_nc_v4(pdy + v), b4 = ld_nc_v4(pys + v);
+          const uint32_t aw[4] = {a4.x, a4.y, a4.z, a4.w}, bw[4] = {b4.x, b4.y, b4.z, b4.w};
+          uint32_t ow[4];
+#pragma unroll
+          for (int q2 = 0; q2 < 4; ++q2) {
+            const float y0 = bf16_lo(aw[q2]), y1 = bf16_hi(aw[q2]);
+            dot += y0 * bf16_lo(bw[q2]) + y1 * bf16_hi(bw[q2]);
+            ow[q2] = pack_bf16(g * y0, g * y1);
+          }
+          st_v4(dst + v, make_uint4(ow[0], ow[1], ow[2], ow[3]));
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+        if (lane == 0) dgates[t * a.k + j] = dot;
+      }
+    }
+  }
+  signal_done(a, kSlotData);
+}
+
+// Reverse pattern: owner receive rows -> the same send-layout row on the source.
+__global__ void reverse_transfer_kernel(CommArgs a, const int32_t* __restrict__ layout,
+                                        const uint16_t* __restrict__ src, int64_t dst_off) {
+  __shared__ int32_t s_seg[kMaxE + 1];
+  __shared__ int32_t s_rows[kMaxE];
+  __shared__ int32_t s_pre[MOE_MAX_EP][kMaxE];   // rows of expert (rank*E_l+el) from sources < r
+  __shared__ int32_t s_soff[MOE_MAX_EP][kMaxE];  // send-layout offset of that expert on source r
+  const int E = a.E, EP = a.ep, E_l = a.E_l;
+  const int32_t* cm = layout;
+  for (int i = threadIdx.x; i <= E_l; i += blockDim.x) s_seg[i] = layout[EP * E + E_l + i];
+  for (int i = threadIdx.x; i < E_l; i += blockDim.x) s_rows[i] = layout[EP * E + i];
+  for (int el = threadIdx.x; el < E_l; el += blockDim.x) {
+    int32_t run = 0;
+    for (int r = 0; r < EP; ++r) {
+      s_pre[r][el] = run;
+      run += cm[r * E + a.rank * E_l + el];
+    }
+  }
+  if (threadIdx.x < EP) {
+    const int r = threadIdx.x;
+    int32_t run = 0;
+    for (int e = 0; e < a.rank * E_l + E_l; ++e) {
+      if (e >= a.rank * E_l) s_soff[r][e - a.rank * E_l] = run;
+      run += cm[r * E + e];
+    }
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t gwarp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int d = a.d, nvec = d / 8;
+  const int64_t row_bytes = static_cast<int64_t>(d) * 2;
+  const int64_t n_rows = s_seg[E_l];
+  for (int64_t row = gwarp; row < n_rows; row += nwarps) {
+    const int el = upper_bound_idx(s_seg, E_l + 1, row);
+    const int32_t w = static_cast<int32_t>(row - s_seg[el]);
+    if (w >= s_rows[el]) continue;  // padding
+    int r = 0;
+    while (r + 1 < EP && s_pre[r + 1][el] <= w) ++r;
+    const int64_t srow = s_soff[r][el] + (w - s_pre[r][el]);
+    uint4* dst = reinterpret_cast<uint4*>(a.peers.base[r] + dst_off + srow * row_bytes);
+    copy_row(dst, reinterpret_cast<const uint4*>(src + row * d), nvec, lane);
+  }
+  signal_done(a, kSlotData);
+}
+
+__global__ void wait_flags_kernel(CommArgs a, int slot) { wait_all(a, slot); }
+
+int transfer_blocks() { return 2 * num_sms(); }
+
+}  // namespace
+
+cudaError_t launch_counts_exchange(const CommArgs& a, const int32_t* counts, int32_t* layout,
+                                   int64_t recv_rows_cap, cudaStream_t s) {
+  counts_exchange_kernel<<<1, 256, 0, s>>>(a, counts, layout, recv_rows_cap);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_forward_transfer(const CommArgs& a, const int32_t* layout, const uint16_t* src,
+                                    int64_t dst_off, uint16_t* local_dst, const int32_t* dest_row,
+                                    const float* gates, const uint16_t* dy, const uint16_t* ys,
+                                    float* dgates, int mode, cudaStream_t s) {
+  if (mode == 0)
+    forward_transfer_kernel<0><<<transfer_blocks(), 512, 0, s>>>(a, layout, src, dst_off, local_dst,
+                                                                 dest_row, gates, dy, ys, dgates);
+  else
+    forward_transfer_kernel<1><<<transfer_blocks(), 512, 0, s>>>(a, layout, src, dst_off, local_dst,
+                                                                 dest_row, gates, dy, ys, dgates);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reverse_transfer(const CommArgs& a, const int32_t* layout, const uint16_t* src,
+                                    int64_t dst_off, cudaStream_t s) {
+  reverse_transfer_kernel<<<transfer_blocks(), 512, 0, s>>>(a, layout, src, dst_off);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_wait_flags(const CommArgs& a, int slot, cudaStream_t s) {
+  wait_flags_kernel<<<1, 32, 0, s>>>(a, slot);
+  return cudaGetLastError();
+}
+
+}  // namespace moe

@@ -1,0 +1,105 @@
+// internal.h -- host-side interfaces between the C-ABI layer (api.cu) and the
+// kernel translation units.  Not installed; not part of the ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/moe.h"
+
+namespace moe {
+
+// ---------------------------------------------------------------- grouped GEMM
+// One persistent tcgen05 kernel family serves every dense contraction of the
+// layer: D[M,N] = A[M,K] * B[N,K]^T per group.
+enum Epilogue : int {
+  kEpiSwiGLU = 0,   // GEMM1 fwd: acc cols [0,BN/2)=G, [BN/2,BN)=U -> G,U,H bf16 into g_u_h
+  kEpiBF16 = 1,     // plain bf16 store (GEMM2 fwd O, dgrad dX)
+  kEpiDSwiGLU = 2,  // dgrad-1: acc = dH; reads G,U -> dG,dU bf16 into dgu
+  kEpiF32Group = 3, // wgrad: fp32 [M,N] per group (K = the group's rows), optional accumulate
+  kEpiF32Rows = 4,  // router logits: fp32 [rows,N] + bias
+};
+
+struct GemmProblem {
+  int epi = kEpiBF16;
+  int BN = 256;
+  bool a_mn = false, b_mn = false;  // operand major-ness in global memory (MN = contiguous along M/N)
+  // A / B global tensors (bf16, row-major [rows, cols] with leading dimension ld elements)
+  const void* a_ptr = nullptr;
+  int64_t a_rows = 0, a_cols = 0, a_ld = 0;
+  const void* b_ptr = nullptr;
+  int64_t b_rows = 0, b_cols = 0, b_ld = 0;
+  int64_t b_group_stride = 0;  // rows of B per group when B holds weights
+  int64_t b_split = 0;         // SwiGLU: row offset of W_up inside a group (= f)
+  int M = 0, N = 0, K = 0;     // M-grouped: N, K; K-grouped: M, N
+  const int32_t* group_rows = nullptr;  // device [n_groups]
+  int n_groups = 0;
+  int64_t rows_cap = 0;
+  void* out = nullptr;
+  int64_t ld_out = 0;
+  const void* aux = nullptr;  // DSwiGLU: g_u_h
+  int64_t ld_aux = 0;
+  const float* bias = nullptr;
+  int f = 0;
+  int accumulate = 0;
+};
+
+cudaError_t launch_grouped_gemm(const GemmProblem& p, cudaStream_t stream);
+int num_sms();
+
+// ---------------------------------------------------------------- routing / permutation
+cudaError_t launch_route(const float* logits, int64_t T, int E, int k, int32_t* topk_idx,
+                         float* gates, cudaStream_t s);
+cudaError_t launch_route_bwd(const float* logits, const int32_t* topk_idx, const float* gates,
+                             const float* dgates, int64_t T, int E, int k, float* dlogits,
+                             cudaStream_t s);
+cudaError_t launch_router_bwd(const uint16_t* x, const uint16_t* w_r, const float* dlogits,
+                              int64_t T, int d, int E, float* dx_router, float* dw_r,
+                              int accumulate, cudaStream_t s);
+// scratch: int32 workspace of permute_scratch_ints(T,k,E) entries
+int64_t permute_scratch_ints(int64_t T, int k, int E);
+cudaError_t launch_permute(const uint16_t* x, const int32_t* topk_idx, int64_t T, int d, int E,
+                           int k, int64_t C, int32_t* counts, int32_t* dest_row, uint16_t* xs,
+                           int32_t* scratch, cudaStream_t s);
+cudaError_t launch_permute_bwd(const uint16_t* dxs, const int32_t* dest_row, const float* dx_acc,
+                               const uint16_t* dx_extra, int64_t T, int d, int k, uint16_t* dx,
+                               cudaStream_t s);
+cudaError_t launch_unpermute(const uint16_t* ys, const float* gates, const int32_t* dest_row,
+                             const uint16_t* y_extra, int64_t T, int d, int k, uint16_t* y,
+                             cudaStream_t s);
+
+// ---------------------------------------------------------------- transfers (NVSwitch)
+struct PeerTable {
+  char* base[MOE_MAX_EP];  // symmetric heap base of every rank, mapped into this process
+};
+
+struct CommArgs {
+  PeerTable peers;
+  int ep, rank, E, E_l, d;
+  int64_t T, k;
+  uint64_t* flags;       // local flag array [n_slots][EP] in the symmetric heap
+  int64_t flags_off;     // byte offset of the flag array inside every heap
+  int32_t* countmat;     // local count matrix [2][EP][E] in the symmetric heap
+  int64_t countmat_off;
+  int32_t* done;         // local device counter for last-block detection
+  int32_t* err;          // device error word
+  uint64_t epoch;
+};
+enum { kSlotCounts = 0, kSlotData = 1, kNumSlots = 2 };
+
+cudaError_t launch_counts_exchange(const CommArgs& a, const int32_t* counts, int32_t* layout,
+                                   int64_t recv_rows_cap, cudaStream_t s);
+// forward pattern: source send-layout rows -> owners' receive rows (dst_off = byte offset of
+// the destination buffer inside every heap); zeroes the local receive padding.
+//   mode 0: payload rows = src rows (dispatch)
+//   mode 1: payload rows = gates * dy (combine_bwd), also writes dgates
+cudaError_t launch_forward_transfer(const CommArgs& a, const int32_t* layout, const uint16_t* src,
+                                    int64_t dst_off, uint16_t* local_dst, const int32_t* dest_row,
+                                    const float* gates, const uint16_t* dy, const uint16_t* ys,
+                                    float* dgates, int mode, cudaStream_t s);
+// reverse pattern: owner receive rows -> sources' send-layout rows
+cudaError_t launch_reverse_transfer(const CommArgs& a, const int32_t* layout, const uint16_t* src,
+                                    int64_t dst_off, cudaStream_t s);
+cudaError_t launch_wait_flags(const CommArgs& a, int slot, cudaStream_t s);
+
+}  // namespace moe

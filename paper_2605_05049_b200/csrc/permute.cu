@@ -1,0 +1,219 @@
+// permute.cu -- F2 permute (histogram, scan, capacity, scatter), B2 permute_bwd,
+// F6 gate-weighted unpermute.  HBM-bound row movement with 16-byte vectors.
+//
+// Positions are deterministic and bit-exact (no atomic ordering): assignments are
+// visited in slot-major order a = j*T + t (reading R5, PAPER.md:129 token dropping),
+// the rank of an assignment among equal experts is
+//   (earlier chunks, scanned)  +  (earlier warps of the chunk, scanned)  +
+//   (earlier lanes of the warp, __match_any_sync + popc)
+// and C = ceil(cf*k*T/E) decides kept/dropped (reading R4).
+#include "common.cuh"
+#include "internal.h"
+
+namespace moe {
+namespace {
+
+constexpr int kChunk = 1024;  // assignments per block in passes 1 and 3 (32 warps x 32)
+
+__device__ __forceinline__ int expert_of(const int32_t* idx, int64_t a, int64_t T, int k) {
+  const int64_t t = a % T, j = a / T;
+  return idx[t * k + j];
+}
+
+// Pass 1: per-chunk expert histogram.
+__global__ void hist_kernel(const int32_t* __restrict__ idx, int64_t T, int k, int E,
+                            int32_t* __restrict__ chunk_hist /*[nchunks][E]*/) {
+  extern __shared__ int32_t s_hist[];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) s_hist[e] = 0;
+  __syncthreads();
+  const int64_t a = static_cast<int64_t>(blockIdx.x) * kChunk + threadIdx.x;
+  if (a < T * k) atomicAdd(&s_hist[expert_of(idx, a, T, k)], 1);  // order-free count
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x)
+    chunk_hist[static_cast<int64_t>(blockIdx.x) * E + e] = s_hist[e];
+}
+
+// Pass 2: per-expert exclusive scan over chunks (in place -> chunk base), capacity clamp,
+// counts and off = exclusive scan of counts.  One block, thread per expert.
+__global__ void scan_kernel(int32_t* __restrict__ chunk_hist, int nchunks, int E, int64_t C,
+                            int32_t* __restrict__ counts, int32_t* __restrict__ off) {
+  __shared__ int32_t s_cnt[1024];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int32_t run = 0;
+    for (int c = 0; c < nchunks; ++c) {
+      const int32_t h = chunk_hist[static_cast<int64_t>(c) * E + e];
+      chunk_hist[static_cast<int64_t>(c) * E + e] = run;
+      run += h;
+    }
+    const int32_t kept = (C >= 0 && run > C) ? static_cast<int32_t>(C) : run;
+    counts[e] = kept;
+    s_cnt[e] = kept;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int32_t run = 0;
+    for (int e = 0; e < E; ++e) {
+      off[e] = run;
+      run += s_cnt[e];
+    }
+    off[E] = run;
+  }
+}
+
+// Pass 3: stable rank inside the chunk -> p, kept, dest_row.
+__global__ void rank_kernel(const int32_t* __restrict__ idx, int64_t T, int k, int E, int64_t C,
+                            const int32_t* __restrict__ chunk_base, const int32_t* __restrict__ off,
+                            int32_t* __restrict__ dest_row) {
+  extern __shared__ int32_t s_wcnt[];  // [32 warps][E]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < 32 * E; i += blockDim.x) s_wcnt[i] = 0;
+  __syncthreads();
+  const int64_t a = static_cast<int64_t>(blockIdx.x) * kChunk + threadIdx.x;
+  const bool live = a < T * k;
+  const int e = live ? expert_of(idx, a, T, k) : -1 - lane;  // unique dummies never match
+  const unsigned peers = __match_any_sync(0xffffffffu, e);
+  const int in_warp = __popc(peers & ((1u << lane) - 1u));
+  if (live && in_warp == 0) s_wcnt[warp * E + e] = __popc(peers);
+  __syncthreads();
+  for (int ee = threadIdx.x; ee < E; ee += blockDim.x) {  // exclusive scan over warps
+    int32_t run = 0;
+    for (int w = 0; w < 32; ++w) {
+      const int32_t v = s_wcnt[w * E + ee];
+      s_wcnt[w * E + ee] = run;
+      run += v;
+    }
+  }
+  __syncthreads();
+  if (!live) return;
+  const int64_t p = static_cast<int64_t>(chunk_base[static_cast<int64_t>(blockIdx.x) * E + e]) +
+                    s_wcnt[warp * E + e] + in_warp;
+  const bool kept = (C < 0) || (p < C);
+  const int64_t t = a % T, j = a / T;
+  dest_row[t * k + j] = kept ? static_cast<int32_t>(off[e] + p) : -1;
+}
+
+// Pass 4: warp per token; read x_t once per 512-byte chunk, write it to each kept row.
+__global__ void scatter_kernel(const uint16_t* __restrict__ x, const int32_t* __restrict__ dest_row,
+                               int64_t T, int d, int k, uint16_t* __restrict__ xs) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (t >= T) return;
+  int32_t rows[32];
+  int nk = 0;
+  for (int j = 0; j < k; ++j) {
+    const int32_t r = dest_row[t * k + j];
+    if (r >= 0) rows[nk++] = r;
+  }
+  if (nk == 0) return;
+  const int nvec = d / 8;  // 16-byte vectors per row
+  const uint4* src = reinterpret_cast<const uint4*>(x + t * d);
+  for (int v = lane; v < nvec; v += 32) {
+    const uint4 val = ld_nc_v4(src + v);
+    for (int j = 0; j < nk; ++j)
+      reinterpret_cast<uint4*>(xs + static_cast<int64_t>(rows[j]) * d)[v] = val;
+  }
+}
+
+__device__ __forceinline__ void acc_bf16x8(float (&acc)[8], uint4 v, float scale) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    acc[2 * q] += scale * bf16_lo(w[q]);
+    acc[2 * q + 1] += scale * bf16_hi(w[q]);
+  }
+}
+
+// y[t] = bf16( sum_{j kept} g_{t,j} rows[dest_row[t,j]] (j order) + extra_f32[t] + extra_bf16[t] )
+template <bool GATED>
+__global__ void gather_sum_kernel(const uint16_t* __restrict__ rows, const float* __restrict__ gates,
+                                  const int32_t* __restrict__ dest_row, const float* __restrict__ extra_f32,
+                                  const uint16_t* __restrict__ extra_bf16, int64_t T, int d, int k,
+                                  uint16_t* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (t >= T) return;
+  int32_t rws[32];
+  float gs[32];
+  int nk = 0;
+  for (int j = 0; j < k; ++j) {
+    const int32_t r = dest_row[t * k + j];
+    if (r >= 0) {
+      rws[nk] = r;
+      gs[nk] = GATED ? gates[t * k + j] : 1.f;
+      ++nk;
+    }
+  }
+  const int nvec = d / 8;
+  for (int v = lane; v < nvec; v += 32) {
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int j = 0; j < nk; ++j)
+      acc_bf16x8(acc, ld_nc_v4(reinterpret_cast<const uint4*>(rows + static_cast<int64_t>(rws[j]) * d) + v),
+                 gs[j]);
+    if (extra_f32) {
+      const float4* pe = reinterpret_cast<const float4*>(extra_f32 + t * d) + 2 * v;
+      const float4 a = pe[0], b = pe[1];
+      acc[0] += a.x; acc[1] += a.y; acc[2] += a.z; acc[3] += a.w;
+      acc[4] += b.x; acc[5] += b.y; acc[6] += b.z; acc[7] += b.w;
+    }
+    if (extra_bf16)
+      acc_bf16x8(acc, ld_nc_v4(reinterpret_cast<const uint4*>(extra_bf16 + t * d) + v), 1.f);
+    reinterpret_cast<uint4*>(out + t * d)[v] =
+        make_uint4(pack_bf16(acc[0], acc[1]), pack_bf16(acc[2], acc[3]), pack_bf16(acc[4], acc[5]),
+                   pack_bf16(acc[6], acc[7]));
+  }
+}
+
+}  // namespace
+
+int64_t permute_scratch_ints(int64_t T, int k, int E) {
+  const int64_t nchunks = (T * k + kChunk - 1) / kChunk;
+  return (nchunks > 0 ? nchunks : 1) * E + E + 1;
+}
+
+cudaError_t launch_permute(const uint16_t* x, const int32_t* topk_idx, int64_t T, int d, int E,
+                           int k, int64_t C, int32_t* counts, int32_t* dest_row, uint16_t* xs,
+                           int32_t* scratch, cudaStream_t s) {
+  const int64_t nA = T * k;
+  const int nchunks = static_cast<int>((nA + kChunk - 1) / kChunk);
+  int32_t* chunk_hist = scratch;
+  int32_t* off = scratch + static_cast<int64_t>(nchunks > 0 ? nchunks : 1) * E;
+  if (nchunks == 0) {
+    cudaMemsetAsync(counts, 0, sizeof(int32_t) * E, s);
+    return cudaGetLastError();
+  }
+  hist_kernel<<<nchunks, kChunk, E * sizeof(int32_t), s>>>(topk_idx, T, k, E, chunk_hist);
+  scan_kernel<<<1, 256, 0, s>>>(chunk_hist, nchunks, E, C, counts, off);
+  const size_t smem = static_cast<size_t>(32) * E * sizeof(int32_t);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+  }
+  rank_kernel<<<nchunks, kChunk, smem, s>>>(topk_idx, T, k, E, C, chunk_hist, off, dest_row);
+  const int threads = 256;
+  scatter_kernel<<<static_cast<unsigned>((T * 32 + threads - 1) / threads), threads, 0, s>>>(
+      x, dest_row, T, d, k, xs);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_permute_bwd(const uint16_t* dxs, const int32_t* dest_row, const float* dx_acc,
+                               const uint16_t* dx_extra, int64_t T, int d, int k, uint16_t* dx,
+                               cudaStream_t s) {
+  if (T == 0) return cudaSuccess;
+  const int threads = 256;
+  gather_sum_kernel<false><<<static_cast<unsigned>((T * 32 + threads - 1) / threads), threads, 0, s>>>(
+      dxs, nullptr, dest_row, dx_acc, dx_extra, T, d, k, dx);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_unpermute(const uint16_t* ys, const float* gates, const int32_t* dest_row,
+                             const uint16_t* y_extra, int64_t T, int d, int k, uint16_t* y,
+                             cudaStream_t s) {
+  if (T == 0) return cudaSuccess;
+  const int threads = 256;
+  gather_sum_kernel<true><<<static_cast<unsigned>((T * 32 + threads - 1) / threads), threads, 0, s>>>(
+      ys, gates, dest_row, nullptr, y_extra, T, d, k, y);
+  return cudaGetLastError();
+}
+
+}  // namespace moe

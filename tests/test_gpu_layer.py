@@ -1,0 +1,140 @@
+"""End-to-end parity of one MoE layer (forward + backward) at EP=1 through the C ABI
+against the fp64 oracle, given the GPU's fp32 logits as
+the routing boundary (the oracle recomputes nothing discrete from its own logits)."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import moe_ref as ref
+from tests.helpers import TOL, f64, paper_weights, rel_err
+
+pytestmark = pytest.mark.gpu
+
+CASES = {
+    "tiny": synth.CONFIGS["tiny"],
+    "mixtral_small": synth.MoEConfig("mixtral_small", T=1024, d=512, E=8, k=2, f=1024, cf=1.25),
+    "dsmoe_small": synth.MoEConfig("dsmoe_small", T=1024, d=256, E=64, k=6, f=128, cf=1.25, E_s=2),
+    "v3_small_zipf": synth.MoEConfig("v3_small_zipf", T=2048, d=512, E=256, k=8, f=256, cf=0.0,
+                                     zipf_s=1.0),
+    "drops": synth.MoEConfig("drops", T=600, d=128, E=8, k=2, f=256, cf=0.5),
+}
+
+
+def build_layer(cfg, ep_size=1, ep_rank=0, device=0):
+    from paper_2605_05049_b200 import LayerDims, MoELayer
+    T_r = cfg.T // ep_size
+    dims = LayerDims(T_r, cfg.d, cfg.E, cfg.k, cfg.f, cfg.E_s, cfg.cf, ep_size, ep_rank)
+    layer = MoELayer(dims, device=device)
+    E_l = cfg.E // ep_size
+    experts = range(ep_rank * E_l, (ep_rank + 1) * E_l)
+    w_gu, w_down = synth.expert_weights(cfg, experts)
+    w_gu_s, w_down_s = synth.shared_weights(cfg)
+    layer.set_weights(synth.router_weight(cfg), w_gu, w_down, synth.zipf_bias(cfg), w_gu_s, w_down_s)
+    return layer
+
+
+def oracle_layer(cfg, x, dy, logits, ep=1):
+    w_r = f64(synth.router_weight(cfg)).T
+    w_gu, w_down = synth.expert_weights(cfg, range(cfg.E))
+    Wg, Wu, Wd = [], [], []
+    for e in range(cfg.E):
+        a, b, c = paper_weights(w_gu[e], w_down[e], cfg.f)
+        Wg.append(a); Wu.append(b); Wd.append(c)
+    shared = None
+    if cfg.E_s:
+        s_gu, s_down = synth.shared_weights(cfg)
+        shared = paper_weights(s_gu, s_down, cfg.E_s * cfg.f)
+    fw, bw = ref.layer_forward_backward(f64(x), w_r, Wg, Wu, Wd, f64(dy), cfg.k, cfg.cf, ep,
+                                        shared=shared, logits=logits)
+    return fw, bw
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_layer_ep1_parity(name):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    cfg = CASES[name]
+    layer = build_layer(cfg)
+    x = synth.tokens(cfg).cuda()
+    dy = synth.grad_output(cfg).cuda()
+    y = layer.forward(x).clone()
+    dx = layer.backward(dy).clone()
+    torch.cuda.synchronize()
+    layer.ctx.check_device_error()
+    logits = layer.logits.cpu().numpy()
+    # router logits vs fp64 (fp32 accumulation of bf16 products)
+    want_l = ref.router_logits(f64(x), f64(synth.router_weight(cfg)).T,
+                               None if synth.zipf_bias(cfg) is None else f64(synth.zipf_bias(cfg)))
+    assert np.abs(logits - want_l).max() < 1e-3
+    fw, bw = oracle_layer(cfg, x, dy, logits)
+    # discrete parts: bit-exact
+    assert (layer.topk_idx.cpu().numpy() == fw["topk_idx"]).all()
+    pos = fw["plan"]["ranks"][0]
+    assert (layer.counts.cpu().numpy() == pos["counts"]).all()
+    assert (layer.dest_row.cpu().numpy() == pos["dest_row"]).all()
+    lay = layer.layout.cpu().numpy()
+    E_l = cfg.E
+    assert (lay[:cfg.E] == fw["plan"]["counts_all"][0]).all()
+    assert (lay[cfg.E:cfg.E + E_l] == fw["plan"]["layouts"][0]["expert_rows"]).all()
+    # floating parts within tolerance
+    errs = {}
+    errs["gates"] = rel_err(f64(layer.gates), fw["gates"])
+    errs["y"] = rel_err(f64(y), fw["y"])
+    errs["dgates"] = rel_err(f64(layer.dgates), bw["dgates"])
+    errs["dlogits"] = rel_err(f64(layer.dlogits), bw["dlogits"])
+    errs["dx"] = rel_err(f64(dx), bw["dx"])
+    errs["dW_r"] = rel_err(f64(layer.dw_r).T, bw["dW_r"])
+    for e in range(cfg.E):
+        if fw["cache"][e] is None:
+            assert (f64(layer.dw_gu[e]) == 0).all() and (f64(layer.dw_down[e]) == 0).all()
+            continue
+        dgu = f64(layer.dw_gu[e])
+        errs[f"dW_gate{e}"] = rel_err(dgu[:cfg.f].T, bw["dW_gate"][e])
+        errs[f"dW_up{e}"] = rel_err(dgu[cfg.f:].T, bw["dW_up"][e])
+        errs[f"dW_down{e}"] = rel_err(f64(layer.dw_down[e]).T, bw["dW_down"][e])
+    if cfg.E_s:
+        fs = cfg.E_s * cfg.f
+        dgs = f64(layer.dw_gu_s[0])
+        errs["dW_gate_s"] = rel_err(dgs[:fs].T, bw["dW_gate_s"])
+        errs["dW_up_s"] = rel_err(dgs[fs:].T, bw["dW_up_s"])
+        errs["dW_down_s"] = rel_err(f64(layer.dw_down_s[0]).T, bw["dW_down_s"])
+    worst = max(errs, key=errs.get)
+    print(f"{name}: worst {worst} = {errs[worst]:.2e}; y {errs['y']:.2e} dx {errs['dx']:.2e}")
+    bad = {k: v for k, v in errs.items() if not v < TOL}
+    assert not bad, bad
+    layer.close()
+
+
+def test_identity_experts_and_determinism():
+    """FFN bypassed (dispatch -> combine with out = xr): y = (sum_{j kept} g) x within one
+    bf16 rounding; two identical calls are bit-identical."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2605_05049_b200 import _lib as L
+    cfg = CASES["drops"]
+    layer = build_layer(cfg)
+    x = synth.tokens(cfg).cuda()
+    c = layer.ctx
+    L.moe_router_logits(c, x, layer.w_r, None, layer.logits)
+    L.moe_route(c, layer.logits, layer.topk_idx, layer.gates)
+    L.moe_permute(c, x, layer.topk_idx, layer.counts, layer.dest_row, layer.xs)
+    L.moe_dispatch(c, layer.xs, layer.counts, layer.layout, layer.xr)
+    L.moe_combine(c, layer.xr, layer.layout, layer.ys, layer.gates, layer.dest_row, None, layer.y)
+    torch.cuda.synchronize()
+    y1 = layer.y.clone()
+    kept = (layer.dest_row >= 0).float()
+    gs = (layer.gates * kept).sum(1, keepdim=True)
+    want = (gs * x.float()).to(torch.bfloat16)
+    diff = (y1.float() - want.float()).abs()
+    ulp = want.float().abs() * 2.0 ** -7 + 1e-30
+    assert (diff <= ulp).all()
+    # determinism of the whole layer
+    dy = synth.grad_output(cfg).cuda()
+    ya = layer.forward(x).clone(); dxa = layer.backward(dy).clone(); dwa = layer.dw_gu.clone()
+    yb = layer.forward(x).clone(); dxb = layer.backward(dy).clone(); dwb = layer.dw_gu.clone()
+    torch.cuda.synchronize()
+    assert torch.equal(ya, yb) and torch.equal(dxa, dxb) and torch.equal(dwa, dwb)
+    layer.close()

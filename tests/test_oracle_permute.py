@@ -53,6 +53,9 @@ def test_capacity_values():
     assert ref.capacity(1.25, 6, 2048, 64) == 240
     assert ref.capacity(1.25, 8, 4096, 256) == 160
     assert ref.capacity(0.0, 8, 4096, 256) is None
+    # cf is an fp32 value: 0.6f = 0.6000000238 -> 2*1500*0.6f/8 = 225.0000089 -> 226
+    assert ref.capacity(0.6, 2, 1500, 8) == 226
+    assert ref.capacity(0.5, 2, 1500, 8) == 188
 
 
 def test_drop_priority_fixture_is_slot_major():
