@@ -30,6 +30,9 @@ struct moe_ctx {
   int32_t* d_done = nullptr;
   int32_t* d_scratch = nullptr;   // permute workspace
   int32_t* d_rows_T = nullptr;    // one int32 = T_local (router GEMM group size)
+  uint16_t* d_dl_hi = nullptr;    // router backward: bf16 hi/lo split of dlogits [T, Ep]
+  uint16_t* d_dl_lo = nullptr;
+  int Ep = 0;                     // E rounded up to 8
 };
 
 namespace {
@@ -182,6 +185,10 @@ moe_status moe_ctx_create(moe_ctx** out, const moe_shape* shape, int device, siz
   if (e == cudaSuccess) e = cudaMalloc(&c->d_rows_T, 16);
   int32_t tl = static_cast<int32_t>(shape->T_local);
   if (e == cudaSuccess) e = cudaMemcpy(c->d_rows_T, &tl, 4, cudaMemcpyHostToDevice);
+  c->Ep = (shape->E + 7) / 8 * 8;
+  const size_t split_bytes = static_cast<size_t>(shape->T_local > 0 ? shape->T_local : 1) * c->Ep * 2;
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_dl_hi, split_bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_dl_lo, split_bytes);
   if (e == cudaSuccess && EP > 1) e = cudaIpcGetMemHandle(&c->handle, c->heap);
   if (e != cudaSuccess) {
     moe_ctx_destroy(c);
@@ -248,6 +255,8 @@ moe_status moe_ctx_destroy(moe_ctx* c) {
   cudaFree(c->d_done);
   cudaFree(c->d_scratch);
   cudaFree(c->d_rows_T);
+  cudaFree(c->d_dl_hi);
+  cudaFree(c->d_dl_lo);
   delete c;
   return MOE_OK;
 }
@@ -275,8 +284,47 @@ moe_status moe_router_logits_bwd(moe_ctx* c, const moe_bf16* x, const moe_bf16* 
                                  const float* dlogits, float* dx_router, float* dw_r,
                                  int accumulate, moe_stream s) {
   MOE_REQUIRE(c && x && w_r && dlogits && (dx_router || dw_r));
-  return cuda_status(moe::launch_router_bwd(x, w_r, dlogits, c->s.T_local, c->s.d, c->s.E,
-                                            dx_router, dw_r, accumulate, st(s)));
+  const int64_t T = c->s.T_local;
+  const int d = c->s.d, E = c->s.E, Ep = c->Ep;
+  if (T == 0) {
+    if (dw_r && !accumulate) MOE_TRY_CUDA(cudaMemsetAsync(dw_r, 0, sizeof(float) * E * d, st(s)));
+    return MOE_OK;
+  }
+  // dl = hi + lo (bf16 each), then two accumulating tensor-core GEMMs per output
+  MOE_TRY_CUDA(moe::launch_split_hilo(dlogits, T, E, Ep, c->d_dl_hi, c->d_dl_lo, st(s)));
+  const uint16_t* parts[2] = {c->d_dl_hi, c->d_dl_lo};
+  if (dx_router) {  // dx_router[T, d] = dl[T, E] . W_r[E, d]   (B = w_r read MN-major)
+    for (int i = 0; i < 2; ++i) {
+      moe::GemmProblem g;
+      g.epi = moe::kEpiF32Rows;
+      g.BN = pick_bn(d);
+      g.b_mn = true;
+      g.a_ptr = parts[i]; g.a_rows = T; g.a_cols = Ep; g.a_ld = Ep;
+      g.b_ptr = w_r; g.b_rows = E; g.b_cols = d; g.b_ld = d;
+      g.b_group_stride = 0;
+      g.N = d; g.K = (E + 63) / 64 * 64;
+      g.group_rows = c->d_rows_T; g.n_groups = 1; g.rows_cap = T;
+      g.out = dx_router; g.ld_out = d;
+      g.accumulate = i;
+      MOE_TRY_CUDA(moe::launch_grouped_gemm(g, st(s)));
+    }
+  }
+  if (dw_r) {  // dW_r[E, d] (+)= dl^T x  (K = T tokens)
+    for (int i = 0; i < 2; ++i) {
+      moe::GemmProblem g;
+      g.epi = moe::kEpiF32Group;
+      g.BN = pick_bn(d);
+      g.a_mn = true; g.b_mn = true;
+      g.a_ptr = parts[i]; g.a_rows = T; g.a_cols = Ep; g.a_ld = Ep;
+      g.b_ptr = x; g.b_rows = T; g.b_cols = d; g.b_ld = d;
+      g.M = E; g.N = d;
+      g.group_rows = c->d_rows_T; g.n_groups = 1; g.rows_cap = T;
+      g.out = dw_r;
+      g.accumulate = (i == 0) ? accumulate : 1;
+      MOE_TRY_CUDA(moe::launch_grouped_gemm(g, st(s)));
+    }
+  }
+  return MOE_OK;
 }
 
 // ---------------------------------------------------------------- F1 / B1
@@ -414,6 +462,7 @@ moe_status moe_expert_ffn_bwd(moe_ctx* c, const moe_bf16* xr, const int32_t* gro
   w1.M = d; w1.N = f;
   w1.group_rows = group_rows; w1.n_groups = n_groups; w1.rows_cap = rows_cap;
   w1.out = dw_down; w1.accumulate = accumulate;
+  w1.n_fastest = w1.M > w1.N;   // keep the smaller operand slab re-read from L2
   MOE_TRY_CUDA(moe::launch_grouped_gemm(w1, st(s)));
   // wgrad: dW_gu[g] = dgu_g^T X_g   [2f, d]
   moe::GemmProblem w2;
@@ -425,6 +474,7 @@ moe_status moe_expert_ffn_bwd(moe_ctx* c, const moe_bf16* xr, const int32_t* gro
   w2.M = 2 * f; w2.N = d;
   w2.group_rows = group_rows; w2.n_groups = n_groups; w2.rows_cap = rows_cap;
   w2.out = dw_gu; w2.accumulate = accumulate;
+  w2.n_fastest = w2.M > w2.N;
   return cuda_status(moe::launch_grouped_gemm(w2, st(s)));
 }
 

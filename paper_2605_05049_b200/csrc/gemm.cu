@@ -1,12 +1,13 @@
 // gemm.cu -- persistent grouped GEMM on the 5th-generation tensor cores (sm_100a).
 //
 // Serves every dense contraction on the hot path:
-//   F0 router logits   x[T,d] . w_r[E,d]^T                       (M-grouped, 1 group)
+//   F0 router logits   x[T,d] . w_r[E,d]^T                           (M-grouped, 1 group)
 //   F4 GEMM1           xr_g . w_gu_g^T  -> G,U,H (SwiGLU epilogue)   (M-grouped)
 //   F4 GEMM2           H_g  . w_down_g^T -> O                        (M-grouped)
-//   B4 dgrad-1         dO_g . w_down_g   -> dH -> dG,dU (dSwiGLU)     (M-grouped, B MN-major)
-//   B4 dgrad-2         dGU_g . w_gu_g    -> dX                        (M-grouped, B MN-major)
+//   B4 dgrad-1         dO_g . w_down_g   -> dH -> dG,dU (dSwiGLU)    (M-grouped, B MN-major)
+//   B4 dgrad-2         dGU_g . w_gu_g    -> dX                       (M-grouped, B MN-major)
 //   B4 wgrad           dO_g^T H_g, dGU_g^T X_g  (K = the group's rows) (K-grouped, A,B MN-major)
+//   B0 router bwd      dl.W_r, dl^T x  (dl as bf16 hi+lo)
 // The paper's expert GEMMs are "tall-and-skinny" per expert;
 // here all experts of a rank are ONE persistent launch over a (group, m, n) tile list
 // built on the device from the routed row counts, so no host round trip is needed.
@@ -15,9 +16,12 @@
 //   warp 0      TMA producer   (cp.async.bulk.tensor, 128B swizzle, mbarrier ring)
 //   warp 1      MMA issuer     (tcgen05.mma kind::f16, M=128 x N=BN x K=16, fp32 in TMEM)
 //   warp 2      TMEM allocator (2 accumulator stages -> epilogue overlaps the next tile)
-//   warps 4..7  epilogue       (tcgen05.ld 32x32b -> fused activation -> global stores)
+//   warp 3      group tables (device-side prefix sums of the routed rows)
+//   warps 4..7  epilogue       (tcgen05.ld 32x32b -> fused activation -> 128B-swizzled smem
+//                               staging -> TMA store / TMA reduce-add, one 4 KB box per warp)
 #include <algorithm>
 #include <cstdio>
+#include <cstring>
 
 #include "common.cuh"
 #include "internal.h"
@@ -30,6 +34,7 @@ constexpr int kBM = 128;
 constexpr int kBK = 64;  // 64 bf16 = 128 bytes = one 128B-swizzle atom row
 constexpr int kThreads = 256;
 constexpr int kMaxGroups = 256;
+constexpr int kStageBox = 4096;  // per-epilogue-warp staging: 32 rows x 128 bytes
 
 struct KParams {
   int M, N, K;
@@ -37,6 +42,8 @@ struct KParams {
   const int32_t* group_rows;
   int64_t rows_cap;
   int64_t b_group_stride, b_split;
+  int n_fastest;        // tile raster: 1 = n fastest (B slab re-read), 0 = m fastest
+  int direct_store;     // F32Rows only: output pitch not 16B-aligned -> plain stores
   void* out;
   int64_t ld_out;
   const void* aux;
@@ -53,14 +60,15 @@ struct Cfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES_RAW = (196 * 1024) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
+  static constexpr int RING = STAGES * STAGE_BYTES;
   static constexpr int ACC_STRIDE = BN < 32 ? 32 : BN;
   static constexpr int TMEM_COLS = (2 * ACC_STRIDE <= 32)    ? 32
                                    : (2 * ACC_STRIDE <= 64)  ? 64
                                    : (2 * ACC_STRIDE <= 128) ? 128
                                    : (2 * ACC_STRIDE <= 256) ? 256
                                                              : 512;
-  // ring + barriers/tables + alignment slack
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 4096 + 1024;
+  // ring + epilogue staging + barriers/tables + alignment slack
+  static constexpr int SMEM = RING + 4 * kStageBox + 4096 + 1024;
 };
 
 __device__ __forceinline__ int ceil_div(int a, int b) { return (a + b - 1) / b; }
@@ -75,8 +83,7 @@ struct Tile {
 template <bool KGROUPED, int BN>
 __device__ __forceinline__ Tile decode_tile(int t, const int* s_tile_prefix, const int* s_seg,
                                             const int* s_rows, int n_groups, const KParams& p) {
-  // upper_bound over the tile prefix
-  int lo = 0, hi = n_groups;  // find g: prefix[g] <= t < prefix[g+1]
+  int lo = 0, hi = n_groups;  // g with prefix[g] <= t < prefix[g+1]
   while (hi - lo > 1) {
     int mid = (lo + hi) >> 1;
     if (s_tile_prefix[mid] <= t) lo = mid; else hi = mid;
@@ -85,25 +92,47 @@ __device__ __forceinline__ Tile decode_tile(int t, const int* s_tile_prefix, con
   tl.g = lo;
   tl.rows_g = s_rows[lo];
   tl.seg = s_seg[lo];
-  int local = t - s_tile_prefix[lo];
-  if (KGROUPED) {
-    int mt = ceil_div(p.M, kBM);
-    tl.m = local % mt;
-    tl.n = local / mt;
-    tl.nkb = ceil_div(tl.rows_g, kBK);
+  const int local = t - s_tile_prefix[lo];
+  const int mt = KGROUPED ? ceil_div(p.M, kBM) : ceil_div(tl.rows_g, kBM);
+  if (p.n_fastest) {
+    const int nt = ceil_div(p.N, BN);
+    tl.n = local % nt;
+    tl.m = local / nt;
   } else {
-    int mt = ceil_div(tl.rows_g, kBM);
     tl.m = local % mt;
     tl.n = local / mt;
-    tl.nkb = p.K / kBK;
   }
+  tl.nkb = KGROUPED ? ceil_div(tl.rows_g, kBK) : p.K / kBK;
   return tl;
 }
+
+// One thread's 128-byte row of a 32-row box, written 128B-swizzled (16B chunk j of row r at
+// chunk j ^ (r & 7)): conflict-free per quarter warp and the layout TMA SWIZZLE_128B expects.
+__device__ __forceinline__ void stage_row(uint32_t row_addr, int lane, const uint32_t (&w)[32]) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    st_shared_v4(row_addr + ((j ^ (lane & 7)) << 4), w[4 * j], w[4 * j + 1], w[4 * j + 2],
+                 w[4 * j + 3]);
+}
+
+// Before overwriting the warp's staging box: the previous TMA store must have read it.
+__device__ __forceinline__ void staging_acquire(int lane) {
+  if (lane == 0) bulk_wait_read0();
+  __syncwarp();
+}
+// After staging: make the writes visible to the TMA engine; lane 0 then issues the store.
+__device__ __forceinline__ void staging_release() {
+  fence_async_smem();
+  __syncwarp();
+}
+
+__device__ __forceinline__ float silu_f(float g) { return g / (1.f + __expf(-g)); }
 
 template <int BN, bool A_MN, bool B_MN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
-                        const __grid_constant__ CUtensorMap tmB, const KParams p) {
+                        const __grid_constant__ CUtensorMap tmB,
+                        const __grid_constant__ CUtensorMap tmC, const KParams p) {
   using C = Cfg<BN>;
   constexpr bool KGROUPED = (EPI == kEpiF32Group);
   constexpr uint32_t IDESC = idesc_bf16(kBM, BN, A_MN, B_MN);
@@ -113,7 +142,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::STAGES * C::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint8_t* sStage = smem + C::RING;  // 4 x 4 KB, 1024-aligned
+  uint64_t* full = reinterpret_cast<uint64_t*>(sStage + 4 * kStageBox);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
@@ -159,6 +189,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
+    tma_prefetch_desc(&tmC);
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -256,152 +287,194 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp >= 4) {
     // ===================== epilogue =====================
     const int ew = warp - 4;  // TMEM lane quadrant ew*32 .. ew*32+31
-    const int r_in_tile = ew * 32 + lane;
+    const uint32_t row_addr = smem_u32(sStage + ew * kStageBox) + lane * 128;
+    const void* box = sStage + ew * kStageBox;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
       Tile tl = decode_tile<KGROUPED, BN>(t, s_tile_prefix, s_seg, s_rows, n_groups, p);
+      const int mi = tl.m * kBM + ew * 32 + lane;  // row of this thread inside its group
+      const bool valid = KGROUPED ? true : (mi < tl.rows_g);
+      const int row0 = KGROUPED ? (tl.m * kBM + ew * 32) : (tl.seg + tl.m * kBM + ew * 32);
+      const int64_t grow = static_cast<int64_t>(tl.seg) + mi;
+      if (EPI == kEpiDSwiGLU && valid && grow < p.rows_cap) {
+        // warm L2 with this row's saved G and U segments while the MMAs run
+        const uint16_t* a = reinterpret_cast<const uint16_t*>(p.aux) + grow * p.ld_aux + tl.n * BN;
+        prefetch_l2_bulk(a, BN * 2);
+        prefetch_l2_bulk(a + p.f, BN * 2);
+      }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const uint32_t tacc = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * C::ACC_STRIDE;
-      uint32_t r[32];
+      const uint32_t tacc =
+          tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * C::ACC_STRIDE;
 
       if (EPI == kEpiSwiGLU) {
-        const int mi = tl.m * kBM + r_in_tile;
-        const int64_t row = static_cast<int64_t>(tl.seg) + mi;
-        const bool write = row < p.rows_cap;
-        const bool valid = mi < tl.rows_g;
-        uint16_t* o = reinterpret_cast<uint16_t*>(p.out) + row * p.ld_out;
+        // acc cols [0, BN/2) = G, [BN/2, BN) = U for f-columns n*BN/2 ...; write G, U, H
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN / 2; c0 += 32) {
-          uint32_t u[32];
-          tmem_ld32(tacc + c0, r);
-          tmem_ld32(tacc + BN / 2 + c0, u);
+        for (int c0 = 0; c0 < BN / 2; c0 += 64) {
+          uint32_t ga[32], gb[32], ua[32], ub[32], w[32];
+          tmem_ld32(tacc + c0, ga);
+          tmem_ld32(tacc + c0 + 32, gb);
+          tmem_ld32(tacc + BN / 2 + c0, ua);
+          tmem_ld32(tacc + BN / 2 + c0 + 32, ub);
           tmem_ld_wait();
-          if (write) {
-            const int col = tl.n * (BN / 2) + c0;
-            uint4* pg = reinterpret_cast<uint4*>(o + col);
-            uint4* pu = reinterpret_cast<uint4*>(o + p.f + col);
-            uint4* ph = reinterpret_cast<uint4*>(o + 2 * p.f + col);
+          if (!valid) {
 #pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              uint32_t gw[4], uw[4], hw[4];
+            for (int q = 0; q < 32; ++q) ga[q] = gb[q] = ua[q] = ub[q] = 0u;
+          }
+          const int col = tl.n * (BN / 2) + c0;
 #pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                float g0 = __uint_as_float(r[v * 8 + 2 * q]), g1 = __uint_as_float(r[v * 8 + 2 * q + 1]);
-                float u0 = __uint_as_float(u[v * 8 + 2 * q]), u1 = __uint_as_float(u[v * 8 + 2 * q + 1]);
-                if (!valid) { g0 = g1 = u0 = u1 = 0.f; }
-                // H from the fp32 accumulators (one bf16 rounding of each saved tensor)
-                float h0 = g0 / (1.f + __expf(-g0)) * u0;
-                float h1 = g1 / (1.f + __expf(-g1)) * u1;
-                gw[q] = pack_bf16(g0, g1);
-                uw[q] = pack_bf16(u0, u1);
-                hw[q] = pack_bf16(h0, h1);
+          for (int part = 0; part < 3; ++part) {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+              float x0, x1, y0, y1;
+              if (part == 0) {
+                x0 = __uint_as_float(ga[2 * q]); x1 = __uint_as_float(ga[2 * q + 1]);
+                y0 = __uint_as_float(gb[2 * q]); y1 = __uint_as_float(gb[2 * q + 1]);
+              } else if (part == 1) {
+                x0 = __uint_as_float(ua[2 * q]); x1 = __uint_as_float(ua[2 * q + 1]);
+                y0 = __uint_as_float(ub[2 * q]); y1 = __uint_as_float(ub[2 * q + 1]);
+              } else {  // H = silu(G) * U from the fp32 accumulators
+                x0 = silu_f(__uint_as_float(ga[2 * q])) * __uint_as_float(ua[2 * q]);
+                x1 = silu_f(__uint_as_float(ga[2 * q + 1])) * __uint_as_float(ua[2 * q + 1]);
+                y0 = silu_f(__uint_as_float(gb[2 * q])) * __uint_as_float(ub[2 * q]);
+                y1 = silu_f(__uint_as_float(gb[2 * q + 1])) * __uint_as_float(ub[2 * q + 1]);
               }
-              pg[v] = make_uint4(gw[0], gw[1], gw[2], gw[3]);
-              pu[v] = make_uint4(uw[0], uw[1], uw[2], uw[3]);
-              ph[v] = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+              w[q] = pack_bf16(x0, x1);
+              w[16 + q] = pack_bf16(y0, y1);
+            }
+            staging_acquire(lane);
+            stage_row(row_addr, lane, w);
+            staging_release();
+            if (lane == 0) {
+              tma_store_2d(&tmC, box, col + part * p.f, row0);
+              bulk_commit();
             }
           }
         }
-      } else if (EPI == kEpiBF16 || EPI == kEpiDSwiGLU) {
-        const int mi = tl.m * kBM + r_in_tile;
-        const int64_t row = static_cast<int64_t>(tl.seg) + mi;
-        const bool write = row < p.rows_cap;
-        const bool valid = mi < tl.rows_g;
+      } else if (EPI == kEpiBF16) {
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 32) {
-          tmem_ld32(tacc + c0, r);
+        for (int c0 = 0; c0 < BN; c0 += 64) {
+          uint32_t a[32], b[32], w[32];
+          tmem_ld32(tacc + c0, a);
+          tmem_ld32(tacc + c0 + 32, b);
           tmem_ld_wait();
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            w[q] = valid ? pack_bf16(__uint_as_float(a[2 * q]), __uint_as_float(a[2 * q + 1])) : 0u;
+            w[16 + q] = valid ? pack_bf16(__uint_as_float(b[2 * q]), __uint_as_float(b[2 * q + 1])) : 0u;
+          }
+          staging_acquire(lane);
+          stage_row(row_addr, lane, w);
+          staging_release();
+          if (lane == 0) {
+            tma_store_2d(&tmC, box, tl.n * BN + c0, row0);
+            bulk_commit();
+          }
+        }
+      } else if (EPI == kEpiDSwiGLU) {
+        // acc = dH for f-columns n*BN ...; dG = dH*U*silu'(G), dU = dH*silu(G) -> dgu
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 64) {
+          uint32_t a[32], b[32], gw[32], uw[32], w[32];
+          tmem_ld32(tacc + c0, a);
+          tmem_ld32(tacc + c0 + 32, b);
           const int col = tl.n * BN + c0;
-          if (write && col < p.N) {
-            if (EPI == kEpiBF16) {
-              uint4* po = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(p.out) +
-                                                   row * p.ld_out + col);
+          if (valid && grow < p.rows_cap) {
+            const uint16_t* src = reinterpret_cast<const uint16_t*>(p.aux) + grow * p.ld_aux + col;
+            const uint4* pg = reinterpret_cast<const uint4*>(src);
+            const uint4* pu = reinterpret_cast<const uint4*>(src + p.f);
 #pragma unroll
-              for (int v = 0; v < 4; ++v) {
-                uint32_t w[4];
+            for (int v = 0; v < 8; ++v) {
+              const uint4 g4 = pg[v], u4 = pu[v];
+              gw[4 * v] = g4.x; gw[4 * v + 1] = g4.y; gw[4 * v + 2] = g4.z; gw[4 * v + 3] = g4.w;
+              uw[4 * v] = u4.x; uw[4 * v + 1] = u4.y; uw[4 * v + 2] = u4.z; uw[4 * v + 3] = u4.w;
+            }
+          } else {
 #pragma unroll
-                for (int q = 0; q < 4; ++q)
-                  w[q] = valid ? pack_bf16(__uint_as_float(r[v * 8 + 2 * q]),
-                                           __uint_as_float(r[v * 8 + 2 * q + 1]))
-                               : 0u;
-                po[v] = make_uint4(w[0], w[1], w[2], w[3]);
+            for (int q = 0; q < 32; ++q) gw[q] = uw[q] = 0u;
+          }
+          tmem_ld_wait();
+#pragma unroll
+          for (int part = 0; part < 2; ++part) {
+#pragma unroll
+            for (int q = 0; q < 32; ++q) {
+              // packed word q holds columns 2q, 2q+1 of the 64-column chunk
+              const float dh0 = __uint_as_float(q < 16 ? a[2 * q] : b[2 * q - 32]);
+              const float dh1 = __uint_as_float(q < 16 ? a[2 * q + 1] : b[2 * q - 31]);
+              const float g0 = bf16_lo(gw[q]), g1 = bf16_hi(gw[q]);
+              const float s0 = 1.f / (1.f + __expf(-g0)), s1 = 1.f / (1.f + __expf(-g1));
+              float r0, r1;
+              if (part == 0) {
+                r0 = dh0 * bf16_lo(uw[q]) * s0 * (1.f + g0 * (1.f - s0));
+                r1 = dh1 * bf16_hi(uw[q]) * s1 * (1.f + g1 * (1.f - s1));
+              } else {
+                r0 = dh0 * g0 * s0;
+                r1 = dh1 * g1 * s1;
               }
-            } else {
-              // dH -> dG = dH*U*silu'(G), dU = dH*silu(G); G, U from the saved bf16 g_u_h
-              const uint16_t* a = reinterpret_cast<const uint16_t*>(p.aux) + row * p.ld_aux;
-              const uint4* pg = reinterpret_cast<const uint4*>(a + col);
-              const uint4* pu = reinterpret_cast<const uint4*>(a + p.f + col);
-              uint16_t* o = reinterpret_cast<uint16_t*>(p.out) + row * p.ld_out;
-              uint4* pdg = reinterpret_cast<uint4*>(o + col);
-              uint4* pdu = reinterpret_cast<uint4*>(o + p.f + col);
-#pragma unroll
-              for (int v = 0; v < 4; ++v) {
-                uint4 gv = pg[v], uv = pu[v];
-                const uint32_t gw_in[4] = {gv.x, gv.y, gv.z, gv.w};
-                const uint32_t uw_in[4] = {uv.x, uv.y, uv.z, uv.w};
-                uint32_t dgw[4], duw[4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                  float dh0 = __uint_as_float(r[v * 8 + 2 * q]);
-                  float dh1 = __uint_as_float(r[v * 8 + 2 * q + 1]);
-                  float g0 = bf16_lo(gw_in[q]), g1 = bf16_hi(gw_in[q]);
-                  float u0 = bf16_lo(uw_in[q]), u1 = bf16_hi(uw_in[q]);
-                  float s0 = 1.f / (1.f + __expf(-g0)), s1 = 1.f / (1.f + __expf(-g1));
-                  float dg0 = dh0 * u0 * s0 * (1.f + g0 * (1.f - s0));
-                  float dg1 = dh1 * u1 * s1 * (1.f + g1 * (1.f - s1));
-                  float du0 = dh0 * g0 * s0, du1 = dh1 * g1 * s1;
-                  if (!valid) { dg0 = dg1 = du0 = du1 = 0.f; }
-                  dgw[q] = pack_bf16(dg0, dg1);
-                  duw[q] = pack_bf16(du0, du1);
-                }
-                pdg[v] = make_uint4(dgw[0], dgw[1], dgw[2], dgw[3]);
-                pdu[v] = make_uint4(duw[0], duw[1], duw[2], duw[3]);
-              }
+              w[q] = valid ? pack_bf16(r0, r1) : 0u;
+            }
+            staging_acquire(lane);
+            stage_row(row_addr, lane, w);
+            staging_release();
+            if (lane == 0) {
+              tma_store_2d(&tmC, box, col + part * p.f, row0);
+              bulk_commit();
             }
           }
         }
       } else if (EPI == kEpiF32Group) {
-        const int row = tl.m * kBM + r_in_tile;
-        float* o = reinterpret_cast<float*>(p.out) +
-                   static_cast<int64_t>(tl.g) * p.M * p.N + static_cast<int64_t>(row) * p.N;
+        // wgrad: fp32 [M, N] of group g; 3-D tensor map {N, M, G} clips rows >= M per group
+        if (!(tl.nkb == 0 && p.accumulate)) {
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 32) {
-          if (tl.nkb > 0) {
-            tmem_ld32(tacc + c0, r);
-            tmem_ld_wait();
-          } else {
+          for (int c0 = 0; c0 < BN; c0 += 32) {
+            uint32_t a[32];
+            if (tl.nkb > 0) {
+              tmem_ld32(tacc + c0, a);
+              tmem_ld_wait();
+            } else {
 #pragma unroll
-            for (int q = 0; q < 32; ++q) r[q] = 0u;
-          }
-          const int col = tl.n * BN + c0;
-          if (row < p.M && col < p.N) {
-            float4* po = reinterpret_cast<float4*>(o + col);
-#pragma unroll
-            for (int v = 0; v < 8; ++v) {
-              float4 val = make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
-                                       __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
-              if (p.accumulate) {
-                float4 old = po[v];
-                val.x += old.x; val.y += old.y; val.z += old.z; val.w += old.w;
-              }
-              po[v] = val;
+              for (int q = 0; q < 32; ++q) a[q] = 0u;
+            }
+            staging_acquire(lane);
+            stage_row(row_addr, lane, a);
+            staging_release();
+            if (lane == 0) {
+              if (p.accumulate) tma_reduce_add_3d(&tmC, box, tl.n * BN + c0, row0, tl.g);
+              else tma_store_3d(&tmC, box, tl.n * BN + c0, row0, tl.g);
+              bulk_commit();
             }
           }
         }
-      } else {  // kEpiF32Rows: router logits
-        const int64_t row = static_cast<int64_t>(tl.m) * kBM + r_in_tile;
-        float* o = reinterpret_cast<float*>(p.out) + row * p.ld_out;
+      } else {  // kEpiF32Rows: router logits / router dgrad, fp32 [rows, N] (+ bias) (+= old)
 #pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += 32) {
-          tmem_ld32(tacc + c0, r);
+          uint32_t a[32];
+          tmem_ld32(tacc + c0, a);
           tmem_ld_wait();
-          if (row < p.rows_cap) {
+          const int col0 = tl.n * BN + c0;
 #pragma unroll
-            for (int q = 0; q < 32; ++q) {
-              const int col = tl.n * BN + c0 + q;
-              if (col < p.N) o[col] = __uint_as_float(r[q]) + (p.bias ? p.bias[col] : 0.f);
+          for (int q = 0; q < 32; ++q) {
+            float v = __uint_as_float(a[q]);
+            if (p.bias && col0 + q < p.N) v += p.bias[col0 + q];
+            a[q] = valid ? __float_as_uint(v) : 0u;
+          }
+          if (p.direct_store) {
+            if (valid && grow < p.rows_cap) {
+              float* o = reinterpret_cast<float*>(p.out) + grow * p.ld_out;
+#pragma unroll
+              for (int q = 0; q < 32; ++q)
+                if (col0 + q < p.N)
+                  o[col0 + q] = p.accumulate ? o[col0 + q] + __uint_as_float(a[q]) : __uint_as_float(a[q]);
+            }
+          } else {
+            staging_acquire(lane);
+            stage_row(row_addr, lane, a);
+            staging_release();
+            if (lane == 0) {
+              if (p.accumulate) tma_reduce_add_2d(&tmC, box, col0, row0);
+              else tma_store_2d(&tmC, box, col0, row0);
+              bulk_commit();
             }
           }
         }
@@ -411,6 +484,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) mbar_arrive(&tempty[acc]);
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
+    if (lane == 0) bulk_wait0();  // all TMA stores of this warp complete before exit
   }
 
   tc_fence_before();
@@ -440,37 +514,76 @@ EncodeTiledFn get_encode_fn() {
   return fn;
 }
 
-bool make_tmap(CUtensorMap* tm, const void* ptr, int64_t rows, int64_t cols, int64_t ld,
-               int box_cols, int box_rows) {
+// rank-2/3 tensor map, dims innermost first, strides in bytes for dims 1..rank-1
+bool make_tmap(CUtensorMap* tm, CUtensorMapDataType dt, int rank, const void* ptr,
+               const int64_t* dims, const int64_t* strides, const int* box) {
   EncodeTiledFn fn = get_encode_fn();
-  if (!fn || rows <= 0 || cols <= 0) return false;
-  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
-  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 2};
-  cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
-  cuuint32_t es[2] = {1, 1};
-  CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
-                  box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (!fn) return false;
+  cuuint64_t d[3], s[2];
+  cuuint32_t b[3], es[3] = {1, 1, 1};
+  for (int i = 0; i < rank; ++i) {
+    if (dims[i] <= 0) return false;
+    d[i] = static_cast<cuuint64_t>(dims[i]);
+    b[i] = static_cast<cuuint32_t>(box[i]);
+  }
+  for (int i = 0; i < rank - 1; ++i) {
+    if (strides[i] % 16) return false;
+    s[i] = static_cast<cuuint64_t>(strides[i]);
+  }
+  CUresult r = fn(tm, dt, rank, const_cast<void*>(ptr), d, s, b, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
+}
+
+bool make_tmap_bf16(CUtensorMap* tm, const void* ptr, int64_t rows, int64_t cols, int64_t ld,
+                    int box_cols, int box_rows) {
+  const int64_t dims[2] = {cols, rows};
+  const int64_t strides[1] = {ld * 2};
+  const int box[2] = {box_cols, box_rows};
+  return make_tmap(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, ptr, dims, strides, box);
 }
 
 template <int BN, bool A_MN, bool B_MN, int EPI>
 cudaError_t launch_impl(const GemmProblem& g, cudaStream_t stream) {
   using C = Cfg<BN>;
-  CUtensorMap ta, tb;
+  CUtensorMap ta, tb, tc;
   // A box: K-major {64 k, 128 rows}; MN-major {64 m, 64 k}
-  if (!make_tmap(&ta, g.a_ptr, g.a_rows, g.a_cols, g.a_ld, 64, A_MN ? 64 : kBM))
+  if (!make_tmap_bf16(&ta, g.a_ptr, g.a_rows, g.a_cols, g.a_ld, 64, A_MN ? 64 : kBM))
     return cudaErrorInvalidValue;
-  int b_box_rows = B_MN ? 64 : (EPI == kEpiSwiGLU ? BN / 2 : BN);
-  if (!make_tmap(&tb, g.b_ptr, g.b_rows, g.b_cols, g.b_ld, 64, b_box_rows))
+  const int b_box_rows = B_MN ? 64 : (EPI == kEpiSwiGLU ? BN / 2 : BN);
+  if (!make_tmap_bf16(&tb, g.b_ptr, g.b_rows, g.b_cols, g.b_ld, 64, b_box_rows))
     return cudaErrorInvalidValue;
   KParams kp;
+  memset(&kp, 0, sizeof(kp));
+  // output: one 32-row x 128-byte box per epilogue warp
+  if (EPI == kEpiF32Group) {
+    const int64_t dims[3] = {g.N, g.M, g.n_groups};
+    const int64_t strides[2] = {static_cast<int64_t>(g.N) * 4, static_cast<int64_t>(g.M) * g.N * 4};
+    const int box[3] = {32, 32, 1};
+    if (!make_tmap(&tc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, g.out, dims, strides, box))
+      return cudaErrorInvalidValue;
+  } else if (EPI == kEpiF32Rows) {
+    const int64_t dims[2] = {g.N, g.rows_cap};
+    const int64_t strides[1] = {g.ld_out * 4};
+    const int box[2] = {32, 32};
+    if (!make_tmap(&tc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, g.out, dims, strides, box)) {
+      kp.direct_store = 1;  // e.g. E=5 logits: pitch not 16B-aligned
+      tc = ta;
+    }
+  } else {
+    const int64_t cols = (EPI == kEpiSwiGLU) ? 3 * static_cast<int64_t>(g.f)
+                         : (EPI == kEpiDSwiGLU) ? 2 * static_cast<int64_t>(g.f)
+                                                : g.N;
+    if (!make_tmap_bf16(&tc, g.out, g.rows_cap, cols, g.ld_out, 64, 32)) return cudaErrorInvalidValue;
+  }
   kp.M = g.M; kp.N = g.N; kp.K = g.K;
   kp.n_groups = g.n_groups;
   kp.group_rows = g.group_rows;
   kp.rows_cap = g.rows_cap;
   kp.b_group_stride = g.b_group_stride;
   kp.b_split = g.b_split;
+  kp.n_fastest = g.n_fastest;
   kp.out = g.out; kp.ld_out = g.ld_out;
   kp.aux = g.aux; kp.ld_aux = g.ld_aux;
   kp.bias = g.bias;
@@ -483,7 +596,7 @@ cudaError_t launch_impl(const GemmProblem& g, cudaStream_t stream) {
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  kern<<<num_sms(), kThreads, C::SMEM, stream>>>(ta, tb, kp);
+  kern<<<num_sms(), kThreads, C::SMEM, stream>>>(ta, tb, tc, kp);
   return cudaGetLastError();
 }
 
@@ -528,6 +641,12 @@ cudaError_t launch_grouped_gemm(const GemmProblem& g, cudaStream_t s) {
       if (g.BN == 64) return launch_impl<64, true, true, kEpiF32Group>(g, s);
       break;
     case kEpiF32Rows:
+      if (g.b_mn) {
+        if (g.BN == 256) return launch_impl<256, false, true, kEpiF32Rows>(g, s);
+        if (g.BN == 128) return launch_impl<128, false, true, kEpiF32Rows>(g, s);
+        if (g.BN == 64) return launch_impl<64, false, true, kEpiF32Rows>(g, s);
+        break;
+      }
       if (g.BN == 256) return launch_impl<256, false, false, kEpiF32Rows>(g, s);
       if (g.BN == 128) return launch_impl<128, false, false, kEpiF32Rows>(g, s);
       if (g.BN == 64) return launch_impl<64, false, false, kEpiF32Rows>(g, s);

@@ -42,6 +42,7 @@ struct GemmProblem {
   const float* bias = nullptr;
   int f = 0;
   int accumulate = 0;
+  int n_fastest = 0;  // tile raster order: 1 = n fastest (re-read B), 0 = m fastest (re-read A)
 };
 
 cudaError_t launch_grouped_gemm(const GemmProblem& p, cudaStream_t stream);
@@ -53,9 +54,8 @@ cudaError_t launch_route(const float* logits, int64_t T, int E, int k, int32_t* 
 cudaError_t launch_route_bwd(const float* logits, const int32_t* topk_idx, const float* gates,
                              const float* dgates, int64_t T, int E, int k, float* dlogits,
                              cudaStream_t s);
-cudaError_t launch_router_bwd(const uint16_t* x, const uint16_t* w_r, const float* dlogits,
-                              int64_t T, int d, int E, float* dx_router, float* dw_r,
-                              int accumulate, cudaStream_t s);
+cudaError_t launch_split_hilo(const float* dl, int64_t T, int E, int Ep, uint16_t* hi,
+                              uint16_t* lo, cudaStream_t s);
 // scratch: int32 workspace of permute_scratch_ints(T,k,E) entries
 int64_t permute_scratch_ints(int64_t T, int k, int E);
 cudaError_t launch_permute(const uint16_t* x, const int32_t* topk_idx, int64_t T, int d, int E,

@@ -125,79 +125,21 @@ __global__ void route_bwd_kernel(const float* __restrict__ logits, const int32_t
   }
 }
 
-// B0 (part 1): dx_router[t, c] = sum_e dl[t,e] w_r[e,c].  Block: 32 tokens x 256 columns;
-// dl tile staged transposed in smem ([e][t]) so every column thread reads broadcasts.
-template <int TT>
-__global__ void router_dx_kernel(const uint16_t* __restrict__ w_r, const float* __restrict__ dl,
-                                 int64_t T, int d, int E, float* __restrict__ dx) {
-  extern __shared__ float s_dl[];  // [E][TT]
-  const int64_t t0 = static_cast<int64_t>(blockIdx.y) * TT;
-  for (int i = threadIdx.x; i < TT * E; i += blockDim.x) {
-    const int tt = i / E, e = i % E;
-    s_dl[e * TT + tt] = (t0 + tt < T) ? dl[(t0 + tt) * E + e] : 0.f;
-  }
-  __syncthreads();
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= d) return;
-  float acc[TT];
-#pragma unroll
-  for (int i = 0; i < TT; ++i) acc[i] = 0.f;
-  for (int e = 0; e < E; ++e) {
-    const float w = __uint_as_float(static_cast<uint32_t>(w_r[static_cast<int64_t>(e) * d + c]) << 16);
-    const float4* srow = reinterpret_cast<const float4*>(s_dl + e * TT);
-#pragma unroll
-    for (int i = 0; i < TT / 4; ++i) {
-      const float4 v = srow[i];
-      acc[4 * i] += v.x * w; acc[4 * i + 1] += v.y * w;
-      acc[4 * i + 2] += v.z * w; acc[4 * i + 3] += v.w * w;
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < TT; ++i)
-    if (t0 + i < T) dx[(t0 + i) * d + c] = acc[i];
-}
-
-// B0 (part 2): dw_r[e, c] (+)= sum_t dl[t,e] x[t,c].  Block: ET experts x 256 columns,
-// looping over all tokens in a fixed order (deterministic).
-template <int ET>
-__global__ void router_dw_kernel(const uint16_t* __restrict__ x, const float* __restrict__ dl,
-                                 int64_t T, int d, int E, float* __restrict__ dw, int accumulate) {
-  constexpr int TCH = 64;
-  __shared__ __align__(16) float s_dl[TCH][ET];
-  const int e0 = blockIdx.y * ET;
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  float acc[ET];
-#pragma unroll
-  for (int i = 0; i < ET; ++i) acc[i] = 0.f;
-  for (int64_t tb = 0; tb < T; tb += TCH) {
-    __syncthreads();
-    for (int i = threadIdx.x; i < TCH * ET; i += blockDim.x) {
-      const int tt = i / ET, e = i % ET;
-      s_dl[tt][e] = (tb + tt < T && e0 + e < E) ? dl[(tb + tt) * E + e0 + e] : 0.f;
-    }
-    __syncthreads();
-    if (c < d) {
-      const int n = (T - tb < TCH) ? static_cast<int>(T - tb) : TCH;
-      for (int tt = 0; tt < n; ++tt) {
-        const float xv = __uint_as_float(static_cast<uint32_t>(x[(tb + tt) * d + c]) << 16);
-        const float4* srow = reinterpret_cast<const float4*>(&s_dl[tt][0]);
-#pragma unroll
-        for (int i = 0; i < ET / 4; ++i) {
-          const float4 v = srow[i];
-          acc[4 * i] += v.x * xv; acc[4 * i + 1] += v.y * xv;
-          acc[4 * i + 2] += v.z * xv; acc[4 * i + 3] += v.w * xv;
-        }
-      }
-    }
-  }
-  if (c >= d) return;
-#pragma unroll
-  for (int i = 0; i < ET; ++i) {
-    if (e0 + i < E) {
-      float* p = dw + static_cast<int64_t>(e0 + i) * d + c;
-      *p = accumulate ? (*p + acc[i]) : acc[i];
-    }
-  }
+// B0 prologue: split the fp32 router gradient into two bf16 terms, dl = hi + lo + O(2^-16 |dl|),
+// so that dx_router = dl W_r and dW_r = x^T dl run on the tensor cores as two accumulating
+// bf16 GEMMs each with fp32 accuracy of the operand.  Output [T, Ep] (Ep = E rounded up to 8,
+// zero padding) so that every row is 16-byte aligned for TMA.
+__global__ void split_hilo_kernel(const float* __restrict__ dl, int64_t T, int E, int Ep,
+                                  uint16_t* __restrict__ hi, uint16_t* __restrict__ lo) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= T * Ep) return;
+  const int64_t t = i / Ep;
+  const int e = static_cast<int>(i % Ep);
+  const float v = (e < E) ? dl[t * E + e] : 0.f;
+  const __nv_bfloat16 h = __float2bfloat16_rn(v);
+  const __nv_bfloat16 l = __float2bfloat16_rn(v - __bfloat162float(h));
+  hi[i] = *reinterpret_cast<const uint16_t*>(&h);
+  lo[i] = *reinterpret_cast<const uint16_t*>(&l);
 }
 
 }  // namespace
@@ -225,30 +167,11 @@ cudaError_t launch_route_bwd(const float* logits, const int32_t* topk_idx, const
   return cudaGetLastError();
 }
 
-cudaError_t launch_router_bwd(const uint16_t* x, const uint16_t* w_r, const float* dlogits,
-                              int64_t T, int d, int E, float* dx_router, float* dw_r,
-                              int accumulate, cudaStream_t s) {
-  if (T > 0 && dx_router) {
-    constexpr int TT = 32;
-    dim3 grid((d + 255) / 256, static_cast<unsigned>((T + TT - 1) / TT));
-    size_t smem = static_cast<size_t>(TT) * E * sizeof(float);
-    if (smem > 48 * 1024) {
-      cudaError_t e = cudaFuncSetAttribute(router_dx_kernel<TT>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           static_cast<int>(smem));
-      if (e != cudaSuccess) return e;
-    }
-    router_dx_kernel<TT><<<grid, 256, smem, s>>>(w_r, dlogits, T, d, E, dx_router);
-  }
-  if (dw_r) {
-    if (E <= 8) {
-      dim3 grid((d + 255) / 256, 1);
-      router_dw_kernel<8><<<grid, 256, 0, s>>>(x, dlogits, T, d, E, dw_r, accumulate);
-    } else {
-      dim3 grid((d + 255) / 256, (E + 31) / 32);
-      router_dw_kernel<32><<<grid, 256, 0, s>>>(x, dlogits, T, d, E, dw_r, accumulate);
-    }
-  }
+cudaError_t launch_split_hilo(const float* dl, int64_t T, int E, int Ep, uint16_t* hi,
+                              uint16_t* lo, cudaStream_t s) {
+  if (T == 0) return cudaSuccess;
+  const int64_t n = T * Ep;
+  split_hilo_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(dl, T, E, Ep, hi, lo);
   return cudaGetLastError();
 }
 

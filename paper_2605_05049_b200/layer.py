@@ -169,8 +169,9 @@ class MoELayer:
             # router GEMM, route, permute (4), dispatch (3), ffn (2), combine (3)
             n += 1 + 1 + 4 + 3 + 2 + 3 + (2 if self.fs else 0)
         if bwd:
-            # combine_bwd (2), ffn_bwd (4), dispatch_bwd (2), route_bwd, router bwd (2), permute_bwd
-            n += 2 + 4 + 2 + 1 + 2 + 1 + (4 if self.fs else 0)
+            # combine_bwd (2), ffn_bwd (4), dispatch_bwd (2), route_bwd,
+            # router bwd (hi/lo split + 2 dgrad + 2 wgrad GEMMs), permute_bwd
+            n += 2 + 4 + 2 + 1 + 5 + 1 + (4 if self.fs else 0)
         return n
 
     def close(self):
