@@ -247,6 +247,9 @@ def run_ours(args):
     ms, e2e_ms, gemm_ms_max = vals.tolist()
     if rank != 0:
         layer.close()
+        if dist is not None:
+            dist.barrier()
+            dist.destroy_process_group()
         return
     tokens = cfg.T
     peaks = measured_peaks()
@@ -294,8 +297,11 @@ def run_ours(args):
     }
     if world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(cfg, args.cpu_sample_tokens or 128, w_gu, w_down, layer)
-    print(json.dumps(out))
+    print(json.dumps(out), flush=True)
     layer.close()
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 # ---------------------------------------------------------------------------- oracle arm
@@ -435,7 +441,9 @@ def run_a2a(args):
         ctx.close()
     if rank == 0:
         print(json.dumps({"metric": "dispatch all-to-all busbw vs NCCL", "n_gpus": world,
-                          "unit": "GB/s", "nvlink_peak_GBs": 900, "sweep": results}))
+                          "unit": "GB/s", "nvlink_peak_GBs": 900, "sweep": results}), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
 
 
 def main():

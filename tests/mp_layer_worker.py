@@ -1,0 +1,134 @@
+"""torchrun worker: one EP rank per GPU runs the MoE layer on its token shard and its
+experts (NVSwitch peer-store dispatch/combine); rank 0 gathers everything and checks it
+against the fp64 oracle simulating all EP ranks (tests/test_gpu_multi.py launches it).
+
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 \
+        tests/mp_layer_worker.py --config tiny
+Prints one JSON line on rank 0: {"ok": bool, "errors": {...}, ...}.
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import synth  # noqa: E402
+
+CASES = {
+    "tiny": synth.MoEConfig("tiny_ep", T=512, d=64, E=8, k=2, f=128, cf=1.25),
+    "mixtral_small": synth.MoEConfig("mixtral_small", T=2048, d=512, E=8, k=2, f=1024, cf=1.25),
+    "dsmoe_small": synth.MoEConfig("dsmoe_small", T=2048, d=256, E=64, k=6, f=128, cf=1.25, E_s=2),
+    "v3_small_zipf": synth.MoEConfig("v3_small_zipf", T=2048, d=512, E=256, k=8, f=256, cf=0.0,
+                                     zipf_s=1.0),
+    "drops": synth.MoEConfig("drops", T=1024, d=128, E=8, k=2, f=256, cf=0.5),
+}
+
+
+def gather(t):
+    out = [torch.empty_like(t) for _ in range(dist.get_world_size())]
+    dist.all_gather(out, t.contiguous())
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="tiny", choices=list(CASES))
+    ap.add_argument("--iters", type=int, default=3)
+    args = ap.parse_args()
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    ep, rank = dist.get_world_size(), dist.get_rank()
+    cfg = CASES[args.config]
+    from tests.test_gpu_layer import build_layer, oracle_layer
+    from tests.helpers import TOL, f64, rel_err
+
+    layer = build_layer(cfg, ep_size=ep, ep_rank=rank, device=local)
+    T_r = cfg.T // ep
+    x = synth.tokens(cfg).cuda()[rank * T_r:(rank + 1) * T_r].contiguous()
+    dy = synth.grad_output(cfg).cuda()[rank * T_r:(rank + 1) * T_r].contiguous()
+    outs = []
+    for _ in range(args.iters):  # epoch reuse: repeated calls must be bit-identical
+        y = layer.forward(x).clone()
+        dx = layer.backward(dy).clone()
+        outs.append((y, dx, layer.dw_gu.clone()))
+    torch.cuda.synchronize()
+    st = layer.ctx.device_error()
+    repeat_ok = all(torch.equal(o[0], outs[0][0]) and torch.equal(o[1], outs[0][1]) and
+                    torch.equal(o[2], outs[0][2]) for o in outs[1:])
+    y, dx, _ = outs[0]
+    g = {
+        "y": gather(y), "dx": gather(dx), "logits": gather(layer.logits),
+        "topk": gather(layer.topk_idx), "dest": gather(layer.dest_row), "layout": gather(layer.layout),
+        "dw_gu": gather(layer.dw_gu), "dw_down": gather(layer.dw_down), "dw_r": gather(layer.dw_r),
+        "dgates": gather(layer.dgates),
+    }
+    if cfg.E_s:
+        g["dw_gu_s"] = gather(layer.dw_gu_s)
+        g["dw_down_s"] = gather(layer.dw_down_s)
+    flags = torch.tensor([st, int(repeat_ok)], device="cuda")
+    allflags = gather(flags)
+    if rank != 0:
+        dist.barrier()
+        dist.destroy_process_group()
+        return
+    cat = lambda k: torch.cat(g[k]).cpu()
+    x_all = synth.tokens(cfg)
+    dy_all = synth.grad_output(cfg)
+    logits = cat("logits").numpy()
+    fw, bw = oracle_layer(cfg, x_all, dy_all, logits, ep=ep)
+    res = {"config": cfg.name, "ep": ep, "device_status": [int(f[0]) for f in allflags],
+           "repeat_bitwise": [bool(f[1]) for f in allflags]}
+    checks = {}
+    checks["topk"] = bool((cat("topk").numpy() == fw["topk_idx"]).all())
+    checks["dest_row"] = all(bool((g["dest"][r].cpu().numpy() == fw["plan"]["ranks"][r]["dest_row"]).all())
+                             for r in range(ep))
+    E_l = cfg.E // ep
+    lay_ok = True
+    from oracle import moe_ref as ref
+    padded = ref.recv_layout(fw["plan"]["counts_all"], ep, align=128)
+    for r in range(ep):
+        lay = g["layout"][r].cpu().numpy()
+        lay_ok &= bool((lay[:ep * cfg.E].reshape(ep, cfg.E) == fw["plan"]["counts_all"]).all())
+        lay_ok &= bool((lay[ep * cfg.E:ep * cfg.E + E_l] == padded[r]["expert_rows"]).all())
+        lay_ok &= bool((lay[ep * cfg.E + E_l:] == padded[r]["seg_base"]).all())
+    checks["layout"] = lay_ok
+    errs = {}
+    errs["y"] = rel_err(f64(cat("y")), fw["y"])
+    errs["dx"] = rel_err(f64(cat("dx")), bw["dx"])
+    errs["dgates"] = rel_err(f64(cat("dgates")), bw["dgates"])
+    errs["dW_r"] = rel_err(sum(f64(t) for t in g["dw_r"]).T, bw["dW_r"])
+    f = cfg.f
+    for e in range(cfg.E):
+        q, el = e // E_l, e % E_l
+        if fw["cache"][e] is None:
+            continue
+        dgu = f64(g["dw_gu"][q][el])
+        errs[f"dW_gate{e}"] = rel_err(dgu[:f].T, bw["dW_gate"][e])
+        errs[f"dW_up{e}"] = rel_err(dgu[f:].T, bw["dW_up"][e])
+        errs[f"dW_down{e}"] = rel_err(f64(g["dw_down"][q][el]).T, bw["dW_down"][e])
+    if cfg.E_s:
+        fs = cfg.E_s * cfg.f
+        dgs = sum(f64(t[0]) for t in g["dw_gu_s"])     # per-rank partials sum to the global grad
+        errs["dW_gate_s"] = rel_err(dgs[:fs].T, bw["dW_gate_s"])
+        errs["dW_up_s"] = rel_err(dgs[fs:].T, bw["dW_up_s"])
+        errs["dW_down_s"] = rel_err(sum(f64(t[0]) for t in g["dw_down_s"]).T, bw["dW_down_s"])
+    worst = max(errs, key=errs.get)
+    res.update(checks=checks, worst=[worst, errs[worst]], y=errs["y"], dx=errs["dx"])
+    res["ok"] = (all(checks.values()) and all(v < TOL for v in errs.values()) and
+                 all(s == 0 for s in res["device_status"]) and all(res["repeat_bitwise"]))
+    if not res["ok"]:
+        res["bad"] = {k: v for k, v in errs.items() if not v < TOL}
+    print(json.dumps(res), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
