@@ -30,22 +30,26 @@ def build_layer(cfg, ep_size=1, ep_rank=0, device=0):
     layer = MoELayer(dims, device=device)
     E_l = cfg.E // ep_size
     experts = range(ep_rank * E_l, (ep_rank + 1) * E_l)
-    w_gu, w_down = synth.expert_weights(cfg, experts)
-    w_gu_s, w_down_s = synth.shared_weights(cfg)
-    layer.set_weights(synth.router_weight(cfg), w_gu, w_down, synth.zipf_bias(cfg), w_gu_s, w_down_s)
+    dev = torch.device(f"cuda:{device}")
+    # weights drawn on the GPU (the CUDA generator is deterministic per seed), as bench.py does
+    w_gu, w_down = synth.expert_weights(cfg, experts, device=dev)
+    w_gu_s, w_down_s = synth.shared_weights(cfg, device=dev)
+    layer.set_weights(synth.router_weight(cfg, device=dev), w_gu, w_down, synth.zipf_bias(cfg),
+                      w_gu_s, w_down_s)
     return layer
 
 
 def oracle_layer(cfg, x, dy, logits, ep=1):
-    w_r = f64(synth.router_weight(cfg)).T
-    w_gu, w_down = synth.expert_weights(cfg, range(cfg.E))
+    """The fp64 oracle on the same inputs (weights re-drawn from the same CUDA seeds)."""
+    w_r = f64(synth.router_weight(cfg, device="cuda")).T
+    w_gu, w_down = synth.expert_weights(cfg, range(cfg.E), device="cuda")
     Wg, Wu, Wd = [], [], []
     for e in range(cfg.E):
         a, b, c = paper_weights(w_gu[e], w_down[e], cfg.f)
         Wg.append(a); Wu.append(b); Wd.append(c)
     shared = None
     if cfg.E_s:
-        s_gu, s_down = synth.shared_weights(cfg)
+        s_gu, s_down = synth.shared_weights(cfg, device="cuda")
         shared = paper_weights(s_gu, s_down, cfg.E_s * cfg.f)
     fw, bw = ref.layer_forward_backward(f64(x), w_r, Wg, Wu, Wd, f64(dy), cfg.k, cfg.cf, ep,
                                         shared=shared, logits=logits)
@@ -66,7 +70,7 @@ def test_layer_ep1_parity(name):
     layer.ctx.check_device_error()
     logits = layer.logits.cpu().numpy()
     # router logits vs fp64 (fp32 accumulation of bf16 products)
-    want_l = ref.router_logits(f64(x), f64(synth.router_weight(cfg)).T,
+    want_l = ref.router_logits(f64(x), f64(layer.w_r).T,
                                None if synth.zipf_bias(cfg) is None else f64(synth.zipf_bias(cfg)))
     assert np.abs(logits - want_l).max() < 1e-3
     fw, bw = oracle_layer(cfg, x, dy, logits)
