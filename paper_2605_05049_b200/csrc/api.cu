@@ -1,6 +1,7 @@
 // api.cu -- the C ABI of libmoe (include/moe.h): validation, context, symmetric heap,
 // and the launch sequence of every hot-path step.  No compute happens on the host.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 
@@ -113,6 +114,16 @@ CommArgs comm_args(moe_ctx* c) {
 }
 
 moe_status set_device(moe_ctx* c) { return cuda_status(cudaSetDevice(c->device)); }
+
+// CTA-pair (cta_group::2) tiles for the expert GEMMs unless MOE_GEMM_PAIR=0 (A/B testing).
+int gemm_pair() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MOE_GEMM_PAIR");
+    v = (e && e[0] == '0') ? 1 : 2;
+  }
+  return v;
+}
 
 int pick_bn(int n) {
   if (n % 256 == 0) return 256;
@@ -397,6 +408,7 @@ moe_status moe_expert_ffn(moe_ctx* c, const moe_bf16* xr, const int32_t* group_r
   g1.b_group_stride = 2 * f; g1.b_split = f;
   g1.N = 2 * f; g1.K = d;
   g1.group_rows = group_rows; g1.n_groups = n_groups; g1.rows_cap = rows_cap;
+  g1.pair = gemm_pair();
   g1.out = g_u_h; g1.ld_out = 3 * static_cast<int64_t>(f); g1.f = f;
   MOE_TRY_CUDA(moe::launch_grouped_gemm(g1, st(s)));
   moe::GemmProblem g2;
@@ -408,6 +420,7 @@ moe_status moe_expert_ffn(moe_ctx* c, const moe_bf16* xr, const int32_t* group_r
   g2.b_group_stride = d;
   g2.N = d; g2.K = f;
   g2.group_rows = group_rows; g2.n_groups = n_groups; g2.rows_cap = rows_cap;
+  g2.pair = gemm_pair();
   g2.out = out; g2.ld_out = d;
   return cuda_status(moe::launch_grouped_gemm(g2, st(s)));
 }
@@ -438,6 +451,7 @@ moe_status moe_expert_ffn_bwd(moe_ctx* c, const moe_bf16* xr, const int32_t* gro
   a.b_group_stride = d;
   a.N = f; a.K = d;
   a.group_rows = group_rows; a.n_groups = n_groups; a.rows_cap = rows_cap;
+  a.pair = gemm_pair();
   a.out = dgu; a.ld_out = 2 * F; a.aux = g_u_h; a.ld_aux = 3 * F; a.f = f;
   MOE_TRY_CUDA(moe::launch_grouped_gemm(a, st(s)));
   // dgrad-2: dX = [dG dU] . W_gu  -> dxr
@@ -450,6 +464,7 @@ moe_status moe_expert_ffn_bwd(moe_ctx* c, const moe_bf16* xr, const int32_t* gro
   b.b_group_stride = 2 * F;
   b.N = d; b.K = 2 * f;
   b.group_rows = group_rows; b.n_groups = n_groups; b.rows_cap = rows_cap;
+  b.pair = gemm_pair();
   b.out = dxr; b.ld_out = d;
   MOE_TRY_CUDA(moe::launch_grouped_gemm(b, st(s)));
   // wgrad: dW_down[g] = dout_g^T H_g   [d, f]
@@ -461,6 +476,7 @@ moe_status moe_expert_ffn_bwd(moe_ctx* c, const moe_bf16* xr, const int32_t* gro
   w1.b_ptr = g_u_h + 2 * F; w1.b_rows = rows_cap; w1.b_cols = f; w1.b_ld = 3 * F;
   w1.M = d; w1.N = f;
   w1.group_rows = group_rows; w1.n_groups = n_groups; w1.rows_cap = rows_cap;
+  w1.pair = gemm_pair();
   w1.out = dw_down; w1.accumulate = accumulate;
   w1.n_fastest = w1.M > w1.N;   // keep the smaller operand slab re-read from L2
   MOE_TRY_CUDA(moe::launch_grouped_gemm(w1, st(s)));
@@ -473,6 +489,7 @@ moe_status moe_expert_ffn_bwd(moe_ctx* c, const moe_bf16* xr, const int32_t* gro
   w2.b_ptr = xr; w2.b_rows = rows_cap; w2.b_cols = d; w2.b_ld = d;
   w2.M = 2 * f; w2.N = d;
   w2.group_rows = group_rows; w2.n_groups = n_groups; w2.rows_cap = rows_cap;
+  w2.pair = gemm_pair();
   w2.out = dw_gu; w2.accumulate = accumulate;
   w2.n_fastest = w2.M > w2.N;
   return cuda_status(moe::launch_grouped_gemm(w2, st(s)));

@@ -161,6 +161,40 @@ __device__ __forceinline__ void copy_row(uint4* __restrict__ dst, const uint4* _
   for (int v = lane; v < nvec; v += 32) st_v4(dst + v, ld_nc_v4(src + v));
 }
 
+// Copy segments in transfer order.  Segment i moves `count` consecutive rows from
+// src_base.. (local) to dst_base.. on rank dst_rank.  The order is rotated by rank
+// (destination rank+1 first, self last), so at any moment the sources of an all-to-all
+// write to different destinations instead of all hitting the same receiver's links.
+struct SegTable {
+  int32_t prefix[kMaxE + 1];
+  int32_t src_base[kMaxE];
+  int32_t dst_base[kMaxE];
+  int32_t dst_rank[kMaxE];
+  int32_t count[kMaxE];
+};
+
+// Exclusive scan of t.count[0..n) into t.prefix[0..n] (warp 0; n <= kMaxE).
+__device__ void scan_segments(SegTable& t, int n) {
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    int carry = 0;
+    for (int base = 0; base < n; base += 32) {
+      const int i = base + lane;
+      const int c = i < n ? t.count[i] : 0;
+      int x = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (i < n) t.prefix[i] = carry + x - c;
+      carry += __shfl_sync(0xffffffffu, x, 31);
+    }
+    if (lane == 0) t.prefix[n] = carry;
+  }
+  __syncthreads();
+}
+
 // Forward pattern.  mode 0: payload = src send row.  mode 1 (combine_bwd): payload of
 // slot (t,j) = gates[t,j] * dy[t] (bf16), and dgates[t,j] = <dy[t], ys[dest_row[t,j]]>.
 template <int MODE>
@@ -173,7 +207,20 @@ __global__ void forward_transfer_kernel(CommArgs a, const int32_t* __restrict__ 
                                         const uint16_t* __restrict__ ys,
                                         float* __restrict__ dgates) {
   __shared__ FwdTables tb;
+  __shared__ SegTable sg;
   build_fwd_tables(a, layout, tb);
+  if (MODE == 0) {
+    for (int i = threadIdx.x; i < a.E; i += blockDim.x) {
+      const int q = (a.rank + 1 + i / a.E_l) % a.ep;   // rotated owner order
+      const int e = q * a.E_l + i % a.E_l;
+      sg.count[i] = tb.off[e + 1] - tb.off[e];
+      sg.src_base[i] = tb.off[e];
+      sg.dst_base[i] = tb.dst[e];
+      sg.dst_rank[i] = q;
+    }
+    __syncthreads();
+    scan_segments(sg, a.E);
+  }
   const int lane = threadIdx.x & 31;
   const int64_t gwarp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -196,11 +243,11 @@ __global__ void forward_transfer_kernel(CommArgs a, const int32_t* __restrict__ 
       continue;
     }
     if (MODE == 0) {
-      const int64_t row = w;
-      const int e = upper_bound_idx(tb.off, E + 1, row);
-      const int q = e / E_l;
-      const int64_t drow = tb.dst[e] + (row - tb.off[e]);
-      uint4* dst = reinterpret_cast<uint4*>(a.peers.base[q] + dst_off + drow * row_bytes);
+      const int i = upper_bound_idx(sg.prefix, E + 1, w);
+      const int64_t within = w - sg.prefix[i];
+      const int64_t row = sg.src_base[i] + within;
+      const int64_t drow = sg.dst_base[i] + within;
+      uint4* dst = reinterpret_cast<uint4*>(a.peers.base[sg.dst_rank[i]] + dst_off + drow * row_bytes);
       copy_row(dst, reinterpret_cast<const uint4*>(src + row * d), nvec, lane);
     } else {
       const int64_t t = w;
@@ -266,20 +313,30 @@ __global__ void reverse_transfer_kernel(CommArgs a, const int32_t* __restrict__ 
     }
   }
   __syncthreads();
+  __shared__ SegTable sg;
+  const int nseg = EP * E_l;
+  for (int i = threadIdx.x; i < nseg; i += blockDim.x) {
+    const int r = (a.rank + 1 + i / E_l) % EP;   // rotated source order
+    const int el = i % E_l;
+    sg.count[i] = cm[r * E + a.rank * E_l + el];
+    sg.src_base[i] = s_seg[el] + s_pre[r][el];
+    sg.dst_base[i] = s_soff[r][el];
+    sg.dst_rank[i] = r;
+  }
+  __syncthreads();
+  scan_segments(sg, nseg);
   const int lane = threadIdx.x & 31;
   const int64_t gwarp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   const int d = a.d, nvec = d / 8;
   const int64_t row_bytes = static_cast<int64_t>(d) * 2;
-  const int64_t n_rows = s_seg[E_l];
-  for (int64_t row = gwarp; row < n_rows; row += nwarps) {
-    const int el = upper_bound_idx(s_seg, E_l + 1, row);
-    const int32_t w = static_cast<int32_t>(row - s_seg[el]);
-    if (w >= s_rows[el]) continue;  // padding
-    int r = 0;
-    while (r + 1 < EP && s_pre[r + 1][el] <= w) ++r;
-    const int64_t srow = s_soff[r][el] + (w - s_pre[r][el]);
-    uint4* dst = reinterpret_cast<uint4*>(a.peers.base[r] + dst_off + srow * row_bytes);
+  const int64_t n_rows = sg.prefix[nseg];
+  for (int64_t v = gwarp; v < n_rows; v += nwarps) {
+    const int i = upper_bound_idx(sg.prefix, nseg + 1, v);
+    const int64_t within = v - sg.prefix[i];
+    const int64_t row = sg.src_base[i] + within;
+    const int64_t srow = sg.dst_base[i] + within;
+    uint4* dst = reinterpret_cast<uint4*>(a.peers.base[sg.dst_rank[i]] + dst_off + srow * row_bytes);
     copy_row(dst, reinterpret_cast<const uint4*>(src + row * d), nvec, lane);
   }
   signal_done(a, kSlotData);

@@ -21,6 +21,7 @@
 //                               staging -> TMA store / TMA reduce-add, one 4 KB box per warp)
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -53,10 +54,10 @@ struct KParams {
   int accumulate;
 };
 
-template <int BN>
+template <int BN, int PAIR>
 struct Cfg {
   static constexpr int A_BYTES = kBM * kBK * 2;
-  static constexpr int B_BYTES = BN * kBK * 2;
+  static constexpr int B_BYTES = (BN / PAIR) * kBK * 2;  // a CTA pair splits B along N
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES_RAW = (196 * 1024) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
@@ -80,7 +81,7 @@ struct Tile {
   int seg;      // first row of the group's segment
 };
 
-template <bool KGROUPED, int BN>
+template <bool KGROUPED, int BN, int TILE_M>
 __device__ __forceinline__ Tile decode_tile(int t, const int* s_tile_prefix, const int* s_seg,
                                             const int* s_rows, int n_groups, const KParams& p) {
   int lo = 0, hi = n_groups;  // g with prefix[g] <= t < prefix[g+1]
@@ -93,7 +94,7 @@ __device__ __forceinline__ Tile decode_tile(int t, const int* s_tile_prefix, con
   tl.rows_g = s_rows[lo];
   tl.seg = s_seg[lo];
   const int local = t - s_tile_prefix[lo];
-  const int mt = KGROUPED ? ceil_div(p.M, kBM) : ceil_div(tl.rows_g, kBM);
+  const int mt = KGROUPED ? ceil_div(p.M, TILE_M) : ceil_div(tl.rows_g, TILE_M);
   if (p.n_fastest) {
     const int nt = ceil_div(p.N, BN);
     tl.n = local % nt;
@@ -126,16 +127,29 @@ __device__ __forceinline__ void staging_release() {
   __syncwarp();
 }
 
-__device__ __forceinline__ float silu_f(float g) { return g / (1.f + __expf(-g)); }
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+// sigma(g) = 1 / (1 + e^-g) with one ex2.approx and one rcp.approx (no IEEE division)
+__device__ __forceinline__ float sigmoid_f(float g) { return rcp_approx(1.f + __expf(-g)); }
+__device__ __forceinline__ float silu_f(float g) { return g * sigmoid_f(g); }
 
-template <int BN, bool A_MN, bool B_MN, int EPI>
+// PAIR = 2: a cluster of two CTAs on one TPC runs tcgen05.mma.cta_group::2 with M = 256;
+// each CTA stages its own 128 A rows and half of the B tile, the leader (rank 0) issues the
+// MMAs for both, and each CTA's TMEM holds its 128 accumulator rows.
+template <int BN, bool A_MN, bool B_MN, int EPI, int PAIR>
 __global__ void __launch_bounds__(kThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmC, const KParams p) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, PAIR>;
   constexpr bool KGROUPED = (EPI == kEpiF32Group);
-  constexpr uint32_t IDESC = idesc_bf16(kBM, BN, A_MN, B_MN);
+  constexpr int TILE_M = kBM * PAIR;
+  constexpr uint32_t IDESC = idesc_bf16(TILE_M, BN, A_MN, B_MN);
+  const uint32_t rank = (PAIR == 2) ? cluster_ctarank() : 0u;
+  const int tile0 = blockIdx.x / PAIR, tile_step = gridDim.x / PAIR;
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -159,13 +173,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   // ---- group tables: seg_base = 128-aligned prefix of rows; tile prefix
   if (warp == 3) {
     const int NT = ceil_div(p.N, BN);
-    const int MT = ceil_div(p.M, kBM);
+    const int MT = ceil_div(p.M, TILE_M);
     int seg_carry = 0, tile_carry = 0;
     for (int base = 0; base < n_groups; base += 32) {
       int g = base + lane;
       int rows = (g < n_groups) ? p.group_rows[g] : 0;
       int seg_sz = ((rows + MOE_ALIGN_ROWS - 1) / MOE_ALIGN_ROWS) * MOE_ALIGN_ROWS;
-      int tiles = (g < n_groups) ? (KGROUPED ? MT * NT : ceil_div(rows, kBM) * NT) : 0;
+      int tiles = (g < n_groups) ? (KGROUPED ? MT * NT : ceil_div(rows, TILE_M) * NT) : 0;
       int a = seg_sz, b = tiles;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -191,21 +205,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&tmB);
     tma_prefetch_desc(&tmC);
     for (int s = 0; s < C::STAGES; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], PAIR);     // leader: one arrival per producer of the pair
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], 4 * PAIR);  // leader: the epilogue warps of both CTAs
     }
     fence_mbar_init();
   }
   if (warp == 2) {
-    tmem_alloc(tmem_slot, C::TMEM_COLS);
-    tmem_relinquish();
+    if (PAIR == 2) {
+      tmem_alloc_pair(tmem_slot, C::TMEM_COLS);
+      tmem_relinquish_pair();
+    } else {
+      tmem_alloc(tmem_slot, C::TMEM_COLS);
+      tmem_relinquish();
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int total_tiles = s_tile_prefix[n_groups];
@@ -215,51 +234,66 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-        Tile tl = decode_tile<KGROUPED, BN>(t, s_tile_prefix, s_seg, s_rows, n_groups, p);
+      for (int t = tile0; t < total_tiles; t += tile_step) {
+        Tile tl = decode_tile<KGROUPED, BN, TILE_M>(t, s_tile_prefix, s_seg, s_rows, n_groups, p);
         for (int kb = 0; kb < tl.nkb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+          uint32_t bar_addr = smem_u32(&full[stage]);
+          if (PAIR == 2) {
+            bar_addr = mapa_shared(bar_addr, 0);  // completion goes to the leader's barrier
+            if (rank == 0) mbar_arrive_expect_tx(&full[stage], PAIR * C::STAGE_BYTES);
+            else mbar_arrive_cluster_relaxed(bar_addr);
+          } else {
+            mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+          }
+          auto load = [&](void* dst, const CUtensorMap* tm, int c0, int c1) {
+            if (PAIR == 2) tma_load_2d_pair(dst, tm, bar_addr, c0, c1);
+            else tma_load_2d(dst, tm, &full[stage], c0, c1);
+          };
           uint8_t* a_dst = sA + stage * C::A_BYTES;
           uint8_t* b_dst = sB + stage * C::B_BYTES;
+          const int m_row = tl.m * TILE_M + static_cast<int>(rank) * kBM;  // this CTA's A rows
           // ---- A
           if (A_MN) {  // K-grouped wgrad: A[m, k] stored [k rows, m cols]
 #pragma unroll
             for (int i = 0; i < kBM / 64; ++i)
-              tma_load_2d(a_dst + i * 8192, &tmA, &full[stage], tl.m * kBM + i * 64,
-                          tl.seg + kb * kBK);
+              load(a_dst + i * 8192, &tmA, m_row + i * 64, tl.seg + kb * kBK);
           } else {
-            tma_load_2d(a_dst, &tmA, &full[stage], kb * kBK, tl.seg + tl.m * kBM);
+            load(a_dst, &tmA, kb * kBK, tl.seg + m_row);
           }
-          // ---- B
+          // ---- B (a pair splits it along N: rank r holds columns [r*BN/2, (r+1)*BN/2))
+          constexpr int BNC = BN / PAIR;
           if (B_MN) {
             const int krow = KGROUPED ? (tl.seg + kb * kBK)
                                       : static_cast<int>(tl.g * p.b_group_stride) + kb * kBK;
 #pragma unroll
-            for (int i = 0; i < BN / 64; ++i)
-              tma_load_2d(b_dst + i * 8192, &tmB, &full[stage], tl.n * BN + i * 64, krow);
+            for (int i = 0; i < BNC / 64; ++i)
+              load(b_dst + i * 8192, &tmB, tl.n * BN + static_cast<int>(rank) * BNC + i * 64, krow);
           } else if (EPI == kEpiSwiGLU) {
             const int r0 = static_cast<int>(tl.g * p.b_group_stride) + tl.n * (BN / 2);
-            tma_load_2d(b_dst, &tmB, &full[stage], kb * kBK, r0);
-            tma_load_2d(b_dst + (BN / 2) * 128, &tmB, &full[stage], kb * kBK,
-                        r0 + static_cast<int>(p.b_split));
+            if (PAIR == 2) {  // rank 0: W_gate rows (acc cols [0,BN/2)), rank 1: W_up rows
+              load(b_dst, &tmB, kb * kBK, r0 + (rank ? static_cast<int>(p.b_split) : 0));
+            } else {
+              load(b_dst, &tmB, kb * kBK, r0);
+              load(b_dst + (BN / 2) * 128, &tmB, kb * kBK, r0 + static_cast<int>(p.b_split));
+            }
           } else {
-            tma_load_2d(b_dst, &tmB, &full[stage], kb * kBK,
-                        static_cast<int>(tl.g * p.b_group_stride) + tl.n * BN);
+            load(b_dst, &tmB, kb * kBK,
+                 static_cast<int>(tl.g * p.b_group_stride) + tl.n * BN + static_cast<int>(rank) * BNC);
           }
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    // ===================== MMA issuer =====================
-    if (lane == 0) {
+    // ===================== MMA issuer (the leader CTA of a pair) =====================
+    if (lane == 0 && rank == 0) {
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-        Tile tl = decode_tile<KGROUPED, BN>(t, s_tile_prefix, s_seg, s_rows, n_groups, p);
+      for (int t = tile0; t < total_tiles; t += tile_step) {
+        Tile tl = decode_tile<KGROUPED, BN, TILE_M>(t, s_tile_prefix, s_seg, s_rows, n_groups, p);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * C::ACC_STRIDE;
@@ -274,13 +308,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                                         : sdesc_sw128(a_base + kk * 32, 16, 1024);
             const uint64_t bdesc = B_MN ? sdesc_sw128(b_base + kk * 2048, 8192, 1024)
                                         : sdesc_sw128(b_base + kk * 32, 16, 1024);
-            umma_bf16(d_tmem, adesc, bdesc, IDESC, (kb | kk) != 0 ? 1u : 0u);
+            if (PAIR == 2) umma_bf16_pair(d_tmem, adesc, bdesc, IDESC, (kb | kk) != 0 ? 1u : 0u);
+            else umma_bf16(d_tmem, adesc, bdesc, IDESC, (kb | kk) != 0 ? 1u : 0u);
           }
-          umma_commit(&empty[stage]);  // frees the smem slot when these MMAs complete
+          // frees the smem slot (in both CTAs of a pair) when these MMAs complete
+          if (PAIR == 2) umma_commit_pair(&empty[stage], 0x3);
+          else umma_commit(&empty[stage]);
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
-        if (tl.nkb > 0) umma_commit(&tfull[acc]);
-        else mbar_arrive(&tfull[acc]);
+        if (tl.nkb > 0) {
+          if (PAIR == 2) umma_commit_pair(&tfull[acc], 0x3);
+          else umma_commit(&tfull[acc]);
+        } else {
+          mbar_arrive(&tfull[acc]);
+          if (PAIR == 2) mbar_arrive_cluster(mapa_shared(smem_u32(&tfull[acc]), 1));
+        }
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
@@ -291,11 +333,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     const void* box = sStage + ew * kStageBox;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-      Tile tl = decode_tile<KGROUPED, BN>(t, s_tile_prefix, s_seg, s_rows, n_groups, p);
-      const int mi = tl.m * kBM + ew * 32 + lane;  // row of this thread inside its group
+    for (int t = tile0; t < total_tiles; t += tile_step) {
+      Tile tl = decode_tile<KGROUPED, BN, TILE_M>(t, s_tile_prefix, s_seg, s_rows, n_groups, p);
+      const int m_box = tl.m * TILE_M + static_cast<int>(rank) * kBM + ew * 32;  // warp's 1st row
+      const int mi = m_box + lane;  // row of this thread inside its group
       const bool valid = KGROUPED ? true : (mi < tl.rows_g);
-      const int row0 = KGROUPED ? (tl.m * kBM + ew * 32) : (tl.seg + tl.m * kBM + ew * 32);
+      const int row0 = KGROUPED ? m_box : (tl.seg + m_box);
+      // A 256-row pair tile may end past the group's 128-aligned segment: those rows belong to
+      // the next group and are not written here (whole 32-row boxes, segments are 128-aligned).
+      const bool box_in = KGROUPED || m_box < ((tl.rows_g + kBM - 1) / kBM) * kBM;
       const int64_t grow = static_cast<int64_t>(tl.seg) + mi;
       if (EPI == kEpiDSwiGLU && valid && grow < p.rows_cap) {
         // warm L2 with this row's saved G and U segments while the MMAs run
@@ -305,6 +351,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
+      if (box_in) {
       const uint32_t tacc =
           tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * C::ACC_STRIDE;
 
@@ -396,26 +443,24 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           tmem_ld_wait();
 #pragma unroll
-          for (int part = 0; part < 2; ++part) {
+          uint32_t wu[32];  // dU words; w holds the dG words
 #pragma unroll
-            for (int q = 0; q < 32; ++q) {
-              // packed word q holds columns 2q, 2q+1 of the 64-column chunk
-              const float dh0 = __uint_as_float(q < 16 ? a[2 * q] : b[2 * q - 32]);
-              const float dh1 = __uint_as_float(q < 16 ? a[2 * q + 1] : b[2 * q - 31]);
-              const float g0 = bf16_lo(gw[q]), g1 = bf16_hi(gw[q]);
-              const float s0 = 1.f / (1.f + __expf(-g0)), s1 = 1.f / (1.f + __expf(-g1));
-              float r0, r1;
-              if (part == 0) {
-                r0 = dh0 * bf16_lo(uw[q]) * s0 * (1.f + g0 * (1.f - s0));
-                r1 = dh1 * bf16_hi(uw[q]) * s1 * (1.f + g1 * (1.f - s1));
-              } else {
-                r0 = dh0 * g0 * s0;
-                r1 = dh1 * g1 * s1;
-              }
-              w[q] = valid ? pack_bf16(r0, r1) : 0u;
-            }
+          for (int q = 0; q < 32; ++q) {
+            // packed word q holds columns 2q, 2q+1 of the 64-column chunk
+            const float dh0 = __uint_as_float(q < 16 ? a[2 * q] : b[2 * q - 32]);
+            const float dh1 = __uint_as_float(q < 16 ? a[2 * q + 1] : b[2 * q - 31]);
+            const float g0 = bf16_lo(gw[q]), g1 = bf16_hi(gw[q]);
+            const float s0 = sigmoid_f(g0), s1 = sigmoid_f(g1);
+            const float dg0 = dh0 * bf16_lo(uw[q]) * s0 * (1.f + g0 * (1.f - s0));
+            const float dg1 = dh1 * bf16_hi(uw[q]) * s1 * (1.f + g1 * (1.f - s1));
+            w[q] = valid ? pack_bf16(dg0, dg1) : 0u;
+            wu[q] = valid ? pack_bf16(dh0 * g0 * s0, dh1 * g1 * s1) : 0u;
+          }
+#pragma unroll
+          for (int part = 0; part < 2; ++part) {
             staging_acquire(lane);
-            stage_row(row_addr, lane, w);
+            if (part == 0) stage_row(row_addr, lane, w);
+            else stage_row(row_addr, lane, wu);
             staging_release();
             if (lane == 0) {
               tma_store_2d(&tmC, box, col + part * p.f, row0);
@@ -479,19 +524,24 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+      }  // box_in
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if (PAIR == 2 && rank != 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
+        else mbar_arrive(&tempty[acc]);
+      }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
     if (lane == 0) bulk_wait0();  // all TMA stores of this warp complete before exit
   }
 
   tc_fence_before();
-  __syncthreads();
+  if (PAIR == 2) cluster_sync(); else __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, C::TMEM_COLS);
+    if (PAIR == 2) tmem_dealloc_pair(tmem_base, C::TMEM_COLS);
+    else tmem_dealloc(tmem_base, C::TMEM_COLS);
   }
 }
 
@@ -544,14 +594,14 @@ bool make_tmap_bf16(CUtensorMap* tm, const void* ptr, int64_t rows, int64_t cols
   return make_tmap(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, ptr, dims, strides, box);
 }
 
-template <int BN, bool A_MN, bool B_MN, int EPI>
+template <int BN, bool A_MN, bool B_MN, int EPI, int PAIR>
 cudaError_t launch_impl(const GemmProblem& g, cudaStream_t stream) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, PAIR>;
   CUtensorMap ta, tb, tc;
   // A box: K-major {64 k, 128 rows}; MN-major {64 m, 64 k}
   if (!make_tmap_bf16(&ta, g.a_ptr, g.a_rows, g.a_cols, g.a_ld, 64, A_MN ? 64 : kBM))
     return cudaErrorInvalidValue;
-  const int b_box_rows = B_MN ? 64 : (EPI == kEpiSwiGLU ? BN / 2 : BN);
+  const int b_box_rows = B_MN ? 64 : (EPI == kEpiSwiGLU ? BN / 2 : BN / PAIR);
   if (!make_tmap_bf16(&tb, g.b_ptr, g.b_rows, g.b_cols, g.b_ld, 64, b_box_rows))
     return cudaErrorInvalidValue;
   KParams kp;
@@ -589,15 +639,42 @@ cudaError_t launch_impl(const GemmProblem& g, cudaStream_t stream) {
   kp.bias = g.bias;
   kp.f = g.f;
   kp.accumulate = g.accumulate;
-  auto kern = grouped_gemm_kernel<BN, A_MN, B_MN, EPI>;
+  auto kern = grouped_gemm_kernel<BN, A_MN, B_MN, EPI, PAIR>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  kern<<<num_sms(), kThreads, C::SMEM, stream>>>(ta, tb, tc, kp);
-  return cudaGetLastError();
+  if (PAIR == 1) {
+    kern<<<num_sms(), kThreads, C::SMEM, stream>>>(ta, tb, tc, kp);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  // Persistent grid = the number of CTA pairs that can be co-resident (not every SM can
+  // pair: a launch of more clusters would run the excess as a second, serial wave).
+  static int max_clusters = 0;
+  if (max_clusters == 0) {
+    cfg.gridDim = dim3(num_sms() / 2 * 2);
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) n = num_sms() / 2;
+    max_clusters = n;
+    if (getenv("MOE_VERBOSE"))
+      fprintf(stderr, "[libmoe] gemm<BN=%d,epi=%d> pair grid: %d co-resident clusters of 2\n", BN, EPI, n);
+  }
+  cfg.gridDim = dim3(2 * max_clusters);
+  return cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, kp);
 }
 
 }  // namespace
@@ -613,47 +690,36 @@ int num_sms() {
   return n;
 }
 
+#define MOE_GEMM_CASE(BN_, AMN, BMN, EPI_)                                      \
+  if (g.BN == BN_ && g.a_mn == AMN && g.b_mn == BMN && g.epi == EPI_) {          \
+    if (g.pair == 2 && BN_ >= 128) return launch_impl<BN_, AMN, BMN, EPI_, (BN_ >= 128 ? 2 : 1)>(g, s); \
+    return launch_impl<BN_, AMN, BMN, EPI_, 1>(g, s);                            \
+  }
+
 cudaError_t launch_grouped_gemm(const GemmProblem& g, cudaStream_t s) {
   if (g.n_groups <= 0 || g.n_groups > kMaxGroups) return cudaErrorInvalidValue;
-  switch (g.epi) {
-    case kEpiSwiGLU:
-      if (g.BN == 256) return launch_impl<256, false, false, kEpiSwiGLU>(g, s);
-      if (g.BN == 128) return launch_impl<128, false, false, kEpiSwiGLU>(g, s);
-      break;
-    case kEpiBF16:
-      if (!g.b_mn) {
-        if (g.BN == 256) return launch_impl<256, false, false, kEpiBF16>(g, s);
-        if (g.BN == 128) return launch_impl<128, false, false, kEpiBF16>(g, s);
-        if (g.BN == 64) return launch_impl<64, false, false, kEpiBF16>(g, s);
-      } else {
-        if (g.BN == 256) return launch_impl<256, false, true, kEpiBF16>(g, s);
-        if (g.BN == 128) return launch_impl<128, false, true, kEpiBF16>(g, s);
-        if (g.BN == 64) return launch_impl<64, false, true, kEpiBF16>(g, s);
-      }
-      break;
-    case kEpiDSwiGLU:
-      if (g.BN == 256) return launch_impl<256, false, true, kEpiDSwiGLU>(g, s);
-      if (g.BN == 128) return launch_impl<128, false, true, kEpiDSwiGLU>(g, s);
-      break;
-    case kEpiF32Group:
-      if (g.BN == 256) return launch_impl<256, true, true, kEpiF32Group>(g, s);
-      if (g.BN == 128) return launch_impl<128, true, true, kEpiF32Group>(g, s);
-      if (g.BN == 64) return launch_impl<64, true, true, kEpiF32Group>(g, s);
-      break;
-    case kEpiF32Rows:
-      if (g.b_mn) {
-        if (g.BN == 256) return launch_impl<256, false, true, kEpiF32Rows>(g, s);
-        if (g.BN == 128) return launch_impl<128, false, true, kEpiF32Rows>(g, s);
-        if (g.BN == 64) return launch_impl<64, false, true, kEpiF32Rows>(g, s);
-        break;
-      }
-      if (g.BN == 256) return launch_impl<256, false, false, kEpiF32Rows>(g, s);
-      if (g.BN == 128) return launch_impl<128, false, false, kEpiF32Rows>(g, s);
-      if (g.BN == 64) return launch_impl<64, false, false, kEpiF32Rows>(g, s);
-      if (g.BN == 16) return launch_impl<16, false, false, kEpiF32Rows>(g, s);
-      break;
-  }
+  MOE_GEMM_CASE(256, false, false, kEpiSwiGLU)
+  MOE_GEMM_CASE(128, false, false, kEpiSwiGLU)
+  MOE_GEMM_CASE(256, false, false, kEpiBF16)
+  MOE_GEMM_CASE(128, false, false, kEpiBF16)
+  MOE_GEMM_CASE(64, false, false, kEpiBF16)
+  MOE_GEMM_CASE(256, false, true, kEpiBF16)
+  MOE_GEMM_CASE(128, false, true, kEpiBF16)
+  MOE_GEMM_CASE(64, false, true, kEpiBF16)
+  MOE_GEMM_CASE(256, false, true, kEpiDSwiGLU)
+  MOE_GEMM_CASE(128, false, true, kEpiDSwiGLU)
+  MOE_GEMM_CASE(256, true, true, kEpiF32Group)
+  MOE_GEMM_CASE(128, true, true, kEpiF32Group)
+  MOE_GEMM_CASE(64, true, true, kEpiF32Group)
+  MOE_GEMM_CASE(256, false, true, kEpiF32Rows)
+  MOE_GEMM_CASE(128, false, true, kEpiF32Rows)
+  MOE_GEMM_CASE(64, false, true, kEpiF32Rows)
+  MOE_GEMM_CASE(256, false, false, kEpiF32Rows)
+  MOE_GEMM_CASE(128, false, false, kEpiF32Rows)
+  MOE_GEMM_CASE(64, false, false, kEpiF32Rows)
+  MOE_GEMM_CASE(16, false, false, kEpiF32Rows)
   return cudaErrorInvalidValue;
 }
+#undef MOE_GEMM_CASE
 
 }  // namespace moe

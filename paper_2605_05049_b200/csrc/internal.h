@@ -43,6 +43,7 @@ struct GemmProblem {
   int f = 0;
   int accumulate = 0;
   int n_fastest = 0;  // tile raster order: 1 = n fastest (re-read B), 0 = m fastest (re-read A)
+  int pair = 1;       // 2: CTA-pair tiles (tcgen05 cta_group::2, M = 256), BN >= 128 only
 };
 
 cudaError_t launch_grouped_gemm(const GemmProblem& p, cudaStream_t stream);
