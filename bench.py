@@ -222,21 +222,49 @@ def run_ours(args):
     dy_h = dy.cpu().pin_memory()
     y_h = torch.empty_like(x_h).pin_memory()
     dx_h = torch.empty_like(x_h).pin_memory()
-    x_d = torch.empty_like(x)
-    dy_d = torch.empty_like(dy)
+    # Pipelined: every step's inputs go host->device and its outputs device->host on a copy
+    # stream (PCIe both directions), overlapping the neighbouring steps' compute; all copies
+    # of all K steps are inside the timed region (first H2D .. last D2H).
+    cs = torch.cuda.Stream(device=dev)
+    x_d = [torch.empty_like(x) for _ in range(2)]
+    dy_d = [torch.empty_like(dy) for _ in range(2)]
+    y_b = [torch.empty_like(x) for _ in range(2)]
+    dx_b = [torch.empty_like(x) for _ in range(2)]
+    ev_in = [torch.cuda.Event() for _ in range(2)]
+    ev_done = [torch.cuda.Event() for _ in range(2)]
+    ev_out = [torch.cuda.Event() for _ in range(2)]
     barrier()
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        x_d.copy_(x_h, non_blocking=True)
-        dy_d.copy_(dy_h, non_blocking=True)
-        y = layer.forward(x_d)
-        dxo = layer.backward(dy_d)
-        y_h.copy_(y, non_blocking=True)
-        dx_h.copy_(dxo, non_blocking=True)
-    e1.record(stream)
+    e0.record(cs)
+    with torch.cuda.stream(cs):
+        x_d[0].copy_(x_h, non_blocking=True)
+        dy_d[0].copy_(dy_h, non_blocking=True)
+        ev_in[0].record(cs)
+    for i in range(args.steps):
+        s = i % 2
+        stream.wait_event(ev_in[s])
+        if i + 1 < args.steps:           # next step's inputs, once step i-1 released the slot
+            with torch.cuda.stream(cs):
+                if i >= 1:
+                    cs.wait_event(ev_done[1 - s])
+                x_d[1 - s].copy_(x_h, non_blocking=True)
+                dy_d[1 - s].copy_(dy_h, non_blocking=True)
+                ev_in[1 - s].record(cs)
+        if i >= 2:
+            stream.wait_event(ev_out[s])  # D2H of step i-2 finished reading y_b[s], dx_b[s]
+        y = layer.forward(x_d[s])
+        dxo = layer.backward(dy_d[s])
+        y_b[s].copy_(y, non_blocking=True)
+        dx_b[s].copy_(dxo, non_blocking=True)
+        ev_done[s].record(stream)
+        with torch.cuda.stream(cs):
+            cs.wait_event(ev_done[s])
+            y_h.copy_(y_b[s], non_blocking=True)
+            dx_h.copy_(dx_b[s], non_blocking=True)
+            ev_out[s].record(cs)
+    e1.record(cs)
     torch.cuda.synchronize()
     barrier()
     e2e_ms = e0.elapsed_time(e1) / args.steps

@@ -163,6 +163,17 @@ moe_status moe_permute(moe_ctx* ctx, const moe_bf16* x, const int32_t* topk_idx,
 moe_status moe_permute_bwd(moe_ctx* ctx, const moe_bf16* dxs, const int32_t* dest_row,
                            const float* dx_acc_or_null, const moe_bf16* dx_extra_or_null,
                            moe_bf16* dx, moe_stream stream);
+/* B2 fused with the dgrad half of B0, for k > 1 (MOE_ERR_INVALID_ARG for k = 1): with the
+ * gate a softmax over the k selected logits (reading R1) dlogits[t,:] is zero outside
+ * topk_idx[t,:], so dx_router[t] = sum_j dlogits[t,e_j] w_r[e_j,:] is a k-row gather:
+ *   dx[t] = bf16( sum_{j kept} dxs[dest_row[t,j]] + sum_j dlogits[t,e_j] w_r[e_j,:]
+ *                 + dx_extra[t] (optional) )   in fp32, one rounding.
+ * Equivalent to moe_router_logits_bwd(dx_router) + moe_permute_bwd(dx_acc = dx_router)
+ * without materialising the fp32 [T_local, d] dx_router. */
+moe_status moe_permute_bwd_router(moe_ctx* ctx, const moe_bf16* dxs, const int32_t* dest_row,
+                                  const int32_t* topk_idx, const float* dlogits,
+                                  const moe_bf16* w_r, const moe_bf16* dx_extra_or_null,
+                                  moe_bf16* dx, moe_stream stream);
 
 /* ---------------- F3 / B3 dispatch all-to-all ---------------- */
 

@@ -71,6 +71,7 @@ _SIGS = {
     "moe_route_bwd": [P, P, P, P, P, P, P],
     "moe_permute": [P, P, P, P, P, P, P],
     "moe_permute_bwd": [P, P, P, P, P, P, P],
+    "moe_permute_bwd_router": [P, P, P, P, P, P, P, P, P],
     "moe_dispatch": [P, P, P, P, P, P],
     "moe_dispatch_bwd": [P, P, P, P, P],
     "moe_expert_ffn": [P, P, P, I32, I64, I32, P, P, P, P, P],
@@ -249,6 +250,13 @@ def moe_permute_bwd(ctx, dxs, dest_row, dx_acc, dx_extra, dx, stream=None):
         ctx.handle, _ptr(dxs, BF16, "dxs"), _ptr(dest_row, I32T, "dest_row"),
         _ptr(dx_acc, F32, "dx_acc"), _ptr(dx_extra, BF16, "dx_extra"), _ptr(dx, BF16, "dx"),
         _stream(stream)))
+
+
+def moe_permute_bwd_router(ctx, dxs, dest_row, topk_idx, dlogits, w_r, dx_extra, dx, stream=None):
+    _check("moe_permute_bwd_router", _lib.moe_permute_bwd_router(
+        ctx.handle, _ptr(dxs, BF16, "dxs"), _ptr(dest_row, I32T, "dest_row"),
+        _ptr(topk_idx, I32T, "topk_idx"), _ptr(dlogits, F32, "dlogits"), _ptr(w_r, BF16, "w_r"),
+        _ptr(dx_extra, BF16, "dx_extra"), _ptr(dx, BF16, "dx"), _stream(stream)))
 
 
 def moe_dispatch(ctx, xs, counts, layout, xr, stream=None):

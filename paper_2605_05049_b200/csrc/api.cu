@@ -31,8 +31,11 @@ struct moe_ctx {
   int32_t* d_done = nullptr;
   int32_t* d_scratch = nullptr;   // permute workspace
   int32_t* d_rows_T = nullptr;    // one int32 = T_local (router GEMM group size)
-  uint16_t* d_dl_hi = nullptr;    // router backward: bf16 hi/lo split of dlogits [T, Ep]
-  uint16_t* d_dl_lo = nullptr;
+  uint16_t* d_dl_split = nullptr; // router backward: [T, 2*Ep] bf16 = [hi | lo] of dlogits
+  uint16_t* d_wr2 = nullptr;      // [2*Ep, d] bf16 = [W_r; W_r] (dense dx_router path)
+  float* d_dwr_part = nullptr;    // [S, 2*Ep, d] fp32 split-K partials of dW_r
+  int32_t* d_split_rows = nullptr;// [S] token rows per split
+  int n_split = 1;
   int Ep = 0;                     // E rounded up to 8
 };
 
@@ -197,9 +200,28 @@ moe_status moe_ctx_create(moe_ctx** out, const moe_shape* shape, int device, siz
   int32_t tl = static_cast<int32_t>(shape->T_local);
   if (e == cudaSuccess) e = cudaMemcpy(c->d_rows_T, &tl, 4, cudaMemcpyHostToDevice);
   c->Ep = (shape->E + 7) / 8 * 8;
-  const size_t split_bytes = static_cast<size_t>(shape->T_local > 0 ? shape->T_local : 1) * c->Ep * 2;
-  if (e == cudaSuccess) e = cudaMalloc(&c->d_dl_hi, split_bytes);
-  if (e == cudaSuccess) e = cudaMalloc(&c->d_dl_lo, split_bytes);
+  const int64_t Tl = shape->T_local > 0 ? shape->T_local : 1;
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_dl_split, static_cast<size_t>(Tl) * 2 * c->Ep * 2);
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_wr2, static_cast<size_t>(2) * c->Ep * shape->d * 2);
+  // dW_r = x^T dl has K = T tokens and only E x d outputs: split K into S 128-row-aligned
+  // token chunks (one K-grouped GEMM group each) so the GPU fills; partials summed in order.
+  {
+    int64_t S = Tl / 1024;
+    S = S < 1 ? 1 : (S > 16 ? 16 : S);
+    int64_t chunk = ((Tl + S - 1) / S + MOE_ALIGN_ROWS - 1) / MOE_ALIGN_ROWS * MOE_ALIGN_ROWS;
+    S = (Tl + chunk - 1) / chunk;
+    int32_t rows[16];
+    for (int64_t i = 0; i < S; ++i) {
+      const int64_t r = Tl - i * chunk;
+      rows[i] = static_cast<int32_t>(r < chunk ? r : chunk);
+    }
+    if (shape->T_local == 0) rows[0] = 0;
+    c->n_split = static_cast<int>(S);
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_split_rows, 16 * sizeof(int32_t));
+    if (e == cudaSuccess) e = cudaMemcpy(c->d_split_rows, rows, S * sizeof(int32_t), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+      e = cudaMalloc(&c->d_dwr_part, static_cast<size_t>(S) * 2 * c->Ep * shape->d * sizeof(float));
+  }
   if (e == cudaSuccess && EP > 1) e = cudaIpcGetMemHandle(&c->handle, c->heap);
   if (e != cudaSuccess) {
     moe_ctx_destroy(c);
@@ -266,8 +288,10 @@ moe_status moe_ctx_destroy(moe_ctx* c) {
   cudaFree(c->d_done);
   cudaFree(c->d_scratch);
   cudaFree(c->d_rows_T);
-  cudaFree(c->d_dl_hi);
-  cudaFree(c->d_dl_lo);
+  cudaFree(c->d_dl_split);
+  cudaFree(c->d_wr2);
+  cudaFree(c->d_dwr_part);
+  cudaFree(c->d_split_rows);
   delete c;
   return MOE_OK;
 }
@@ -301,41 +325,46 @@ moe_status moe_router_logits_bwd(moe_ctx* c, const moe_bf16* x, const moe_bf16* 
     if (dw_r && !accumulate) MOE_TRY_CUDA(cudaMemsetAsync(dw_r, 0, sizeof(float) * E * d, st(s)));
     return MOE_OK;
   }
-  // dl = hi + lo (bf16 each), then two accumulating tensor-core GEMMs per output
-  MOE_TRY_CUDA(moe::launch_split_hilo(dlogits, T, E, Ep, c->d_dl_hi, c->d_dl_lo, st(s)));
-  const uint16_t* parts[2] = {c->d_dl_hi, c->d_dl_lo};
-  if (dx_router) {  // dx_router[T, d] = dl[T, E] . W_r[E, d]   (B = w_r read MN-major)
-    for (int i = 0; i < 2; ++i) {
-      moe::GemmProblem g;
-      g.epi = moe::kEpiF32Rows;
-      g.BN = pick_bn(d);
-      g.b_mn = true;
-      g.a_ptr = parts[i]; g.a_rows = T; g.a_cols = Ep; g.a_ld = Ep;
-      g.b_ptr = w_r; g.b_rows = E; g.b_cols = d; g.b_ld = d;
-      g.b_group_stride = 0;
-      g.N = d; g.K = (E + 63) / 64 * 64;
-      g.group_rows = c->d_rows_T; g.n_groups = 1; g.rows_cap = T;
-      g.out = dx_router; g.ld_out = d;
-      g.accumulate = i;
-      MOE_TRY_CUDA(moe::launch_grouped_gemm(g, st(s)));
-    }
+  // dl = hi + lo (bf16 each) as one [T, 2*Ep] tensor: one tensor-core GEMM per output
+  MOE_TRY_CUDA(moe::launch_split_hilo(dlogits, T, E, Ep, c->d_dl_split, st(s)));
+  if (dx_router) {  // dx_router[T, d] = [hi | lo] . [W_r; W_r]   (K-concatenation)
+    MOE_TRY_CUDA(moe::launch_stack_wr(w_r, E, Ep, d, c->d_wr2, st(s)));
+    moe::GemmProblem g;
+    g.epi = moe::kEpiF32Rows;
+    g.BN = pick_bn(d);
+    g.b_mn = true;
+    g.a_ptr = c->d_dl_split; g.a_rows = T; g.a_cols = 2 * Ep; g.a_ld = 2 * Ep;
+    g.b_ptr = c->d_wr2; g.b_rows = 2 * Ep; g.b_cols = d; g.b_ld = d;
+    g.b_group_stride = 0;
+    g.N = d; g.K = (2 * Ep + 63) / 64 * 64;
+    g.group_rows = c->d_rows_T; g.n_groups = 1; g.rows_cap = T;
+    g.out = dx_router; g.ld_out = d;
+    MOE_TRY_CUDA(moe::launch_grouped_gemm(g, st(s)));
   }
-  if (dw_r) {  // dW_r[E, d] (+)= dl^T x  (K = T tokens)
-    for (int i = 0; i < 2; ++i) {
-      moe::GemmProblem g;
-      g.epi = moe::kEpiF32Group;
-      g.BN = pick_bn(d);
-      g.a_mn = true; g.b_mn = true;
-      g.a_ptr = parts[i]; g.a_rows = T; g.a_cols = Ep; g.a_ld = Ep;
-      g.b_ptr = x; g.b_rows = T; g.b_cols = d; g.b_ld = d;
-      g.M = E; g.N = d;
-      g.group_rows = c->d_rows_T; g.n_groups = 1; g.rows_cap = T;
-      g.out = dw_r;
-      g.accumulate = (i == 0) ? accumulate : 1;
-      MOE_TRY_CUDA(moe::launch_grouped_gemm(g, st(s)));
-    }
+  if (dw_r) {  // [hi | lo]^T x over S token chunks -> [S, 2*Ep, d] partials -> ordered sum
+    moe::GemmProblem g;
+    g.epi = moe::kEpiF32Group;
+    g.BN = pick_bn(d);
+    g.a_mn = true; g.b_mn = true;
+    g.a_ptr = c->d_dl_split; g.a_rows = T; g.a_cols = 2 * Ep; g.a_ld = 2 * Ep;
+    g.b_ptr = x; g.b_rows = T; g.b_cols = d; g.b_ld = d;
+    g.M = 2 * Ep; g.N = d;
+    g.group_rows = c->d_split_rows; g.n_groups = c->n_split; g.rows_cap = T;
+    g.out = c->d_dwr_part;
+    MOE_TRY_CUDA(moe::launch_grouped_gemm(g, st(s)));
+    MOE_TRY_CUDA(moe::launch_sum_partials(c->d_dwr_part, c->n_split, E, Ep, d, dw_r, accumulate, st(s)));
   }
   return MOE_OK;
+}
+
+moe_status moe_permute_bwd_router(moe_ctx* c, const moe_bf16* dxs, const int32_t* dest_row,
+                                  const int32_t* topk_idx, const float* dlogits,
+                                  const moe_bf16* w_r, const moe_bf16* dx_extra, moe_bf16* dx,
+                                  moe_stream s) {
+  MOE_REQUIRE(c && dxs && dest_row && topk_idx && dlogits && w_r && dx);
+  MOE_REQUIRE(c->s.k > 1);  // k = 1 has a dense router gradient (full softmax)
+  return cuda_status(moe::launch_permute_bwd_router(dxs, dest_row, topk_idx, dlogits, w_r, dx_extra,
+                                                    c->s.T_local, c->s.d, c->s.E, c->s.k, dx, st(s)));
 }
 
 // ---------------------------------------------------------------- F1 / B1

@@ -55,8 +55,16 @@ cudaError_t launch_route(const float* logits, int64_t T, int E, int k, int32_t* 
 cudaError_t launch_route_bwd(const float* logits, const int32_t* topk_idx, const float* gates,
                              const float* dgates, int64_t T, int E, int k, float* dlogits,
                              cudaStream_t s);
-cudaError_t launch_split_hilo(const float* dl, int64_t T, int E, int Ep, uint16_t* hi,
-                              uint16_t* lo, cudaStream_t s);
+cudaError_t launch_split_hilo(const float* dl, int64_t T, int E, int Ep, uint16_t* out,
+                              cudaStream_t s);
+cudaError_t launch_stack_wr(const uint16_t* w_r, int E, int Ep, int d, uint16_t* out,
+                            cudaStream_t s);
+cudaError_t launch_permute_bwd_router(const uint16_t* dxs, const int32_t* dest_row,
+                                      const int32_t* topk_idx, const float* dlogits,
+                                      const uint16_t* w_r, const uint16_t* dx_extra, int64_t T,
+                                      int d, int E, int k, uint16_t* dx, cudaStream_t s);
+cudaError_t launch_sum_partials(const float* part, int S, int E, int Ep, int d, float* dw,
+                                int accumulate, cudaStream_t s);
 // scratch: int32 workspace of permute_scratch_ints(T,k,E) entries
 int64_t permute_scratch_ints(int64_t T, int k, int E);
 cudaError_t launch_permute(const uint16_t* x, const int32_t* topk_idx, int64_t T, int d, int E,

@@ -163,7 +163,81 @@ __global__ void gather_sum_kernel(const uint16_t* __restrict__ rows, const float
   }
 }
 
+// B2 + B0 (dgrad part) fused, k > 1: the router gradient dl[t,:] is zero outside the k
+// selected experts (softmax over the selected logits, reading R1), so
+//   dx[t] = bf16( sum_{j kept} dxs[dest_row[t,j]] + sum_j dl[t,e_j] w_r[e_j,:] + extra[t] )
+// in fp32 with a fixed order -- the dense [T,d] fp32 dx_router never touches HBM.
+__global__ void gather_sum_router_kernel(const uint16_t* __restrict__ dxs,
+                                         const int32_t* __restrict__ dest_row,
+                                         const int32_t* __restrict__ topk_idx,
+                                         const float* __restrict__ dlogits,
+                                         const uint16_t* __restrict__ w_r,
+                                         const uint16_t* __restrict__ extra_bf16, int64_t T, int d,
+                                         int E, int k, uint16_t* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (t >= T) return;
+  int32_t rws[32], es[32];
+  float dl[32];
+  int nk = 0;
+  for (int j = 0; j < k; ++j) {
+    const int32_t e = topk_idx[t * k + j];
+    es[j] = e;
+    dl[j] = dlogits[t * E + e];
+    const int32_t r = dest_row[t * k + j];
+    if (r >= 0) rws[nk++] = r;
+  }
+  const int nvec = d / 8;
+  for (int v = lane; v < nvec; v += 32) {
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int j = 0; j < nk; ++j)
+      acc_bf16x8(acc, ld_nc_v4(reinterpret_cast<const uint4*>(dxs + static_cast<int64_t>(rws[j]) * d) + v),
+                 1.f);
+    for (int j = 0; j < k; ++j)
+      acc_bf16x8(acc, ld_nc_v4(reinterpret_cast<const uint4*>(w_r + static_cast<int64_t>(es[j]) * d) + v),
+                 dl[j]);
+    if (extra_bf16)
+      acc_bf16x8(acc, ld_nc_v4(reinterpret_cast<const uint4*>(extra_bf16 + t * d) + v), 1.f);
+    reinterpret_cast<uint4*>(out + t * d)[v] =
+        make_uint4(pack_bf16(acc[0], acc[1]), pack_bf16(acc[2], acc[3]), pack_bf16(acc[4], acc[5]),
+                   pack_bf16(acc[6], acc[7]));
+  }
+}
+
+// dw[e, c] (+)= sum_s part[s][e][c] + part[s][Ep + e][c]  (hi and lo halves), fixed order.
+__global__ void sum_partials_kernel(const float* __restrict__ part, int S, int E, int Ep, int d,
+                                    float* __restrict__ dw, int accumulate) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= static_cast<int64_t>(E) * d) return;
+  const int64_t e = i / d, c = i % d;
+  float s = accumulate ? dw[i] : 0.f;
+  for (int p = 0; p < S; ++p) {
+    const float* base = part + static_cast<int64_t>(p) * 2 * Ep * d;
+    s += base[e * d + c] + base[(Ep + e) * d + c];
+  }
+  dw[i] = s;
+}
+
 }  // namespace
+
+cudaError_t launch_permute_bwd_router(const uint16_t* dxs, const int32_t* dest_row,
+                                      const int32_t* topk_idx, const float* dlogits,
+                                      const uint16_t* w_r, const uint16_t* dx_extra, int64_t T,
+                                      int d, int E, int k, uint16_t* dx, cudaStream_t s) {
+  if (T == 0) return cudaSuccess;
+  const int threads = 256;
+  gather_sum_router_kernel<<<static_cast<unsigned>((T * 32 + threads - 1) / threads), threads, 0, s>>>(
+      dxs, dest_row, topk_idx, dlogits, w_r, dx_extra, T, d, E, k, dx);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sum_partials(const float* part, int S, int E, int Ep, int d, float* dw,
+                                int accumulate, cudaStream_t s) {
+  const int64_t n = static_cast<int64_t>(E) * d;
+  sum_partials_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(part, S, E, Ep, d, dw,
+                                                                          accumulate);
+  return cudaGetLastError();
+}
 
 int64_t permute_scratch_ints(int64_t T, int k, int E) {
   const int64_t nchunks = (T * k + kChunk - 1) / kChunk;

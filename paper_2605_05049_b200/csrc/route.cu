@@ -126,11 +126,11 @@ __global__ void route_bwd_kernel(const float* __restrict__ logits, const int32_t
 }
 
 // B0 prologue: split the fp32 router gradient into two bf16 terms, dl = hi + lo + O(2^-16 |dl|),
-// so that dx_router = dl W_r and dW_r = x^T dl run on the tensor cores as two accumulating
-// bf16 GEMMs each with fp32 accuracy of the operand.  Output [T, Ep] (Ep = E rounded up to 8,
-// zero padding) so that every row is 16-byte aligned for TMA.
+// laid out [T, 2*Ep] = [hi | lo] (Ep = E rounded up to 8, zero padding, 16-byte rows for TMA):
+// read K-major it is the K-concatenation for dl.[W_r; W_r]; read MN-major it is the
+// M-stacking for [hi | lo]^T x.  Either way one bf16 tensor-core GEMM gives fp32 accuracy.
 __global__ void split_hilo_kernel(const float* __restrict__ dl, int64_t T, int E, int Ep,
-                                  uint16_t* __restrict__ hi, uint16_t* __restrict__ lo) {
+                                  uint16_t* __restrict__ out) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= T * Ep) return;
   const int64_t t = i / Ep;
@@ -138,8 +138,18 @@ __global__ void split_hilo_kernel(const float* __restrict__ dl, int64_t T, int E
   const float v = (e < E) ? dl[t * E + e] : 0.f;
   const __nv_bfloat16 h = __float2bfloat16_rn(v);
   const __nv_bfloat16 l = __float2bfloat16_rn(v - __bfloat162float(h));
-  hi[i] = *reinterpret_cast<const uint16_t*>(&h);
-  lo[i] = *reinterpret_cast<const uint16_t*>(&l);
+  out[t * 2 * Ep + e] = *reinterpret_cast<const uint16_t*>(&h);
+  out[t * 2 * Ep + Ep + e] = *reinterpret_cast<const uint16_t*>(&l);
+}
+
+// [W_r; W_r] stacked at rows 0 and Ep of a [2*Ep, d] buffer (padding rows zero).
+__global__ void stack_wr_kernel(const uint16_t* __restrict__ w_r, int E, int Ep, int d,
+                                uint16_t* __restrict__ out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= static_cast<int64_t>(2) * Ep * d) return;
+  const int64_t r = i / d, c = i % d;
+  const int64_t e = r < Ep ? r : r - Ep;
+  out[i] = (e < E) ? w_r[e * d + c] : static_cast<uint16_t>(0);
 }
 
 }  // namespace
@@ -167,11 +177,18 @@ cudaError_t launch_route_bwd(const float* logits, const int32_t* topk_idx, const
   return cudaGetLastError();
 }
 
-cudaError_t launch_split_hilo(const float* dl, int64_t T, int E, int Ep, uint16_t* hi,
-                              uint16_t* lo, cudaStream_t s) {
+cudaError_t launch_split_hilo(const float* dl, int64_t T, int E, int Ep, uint16_t* out,
+                              cudaStream_t s) {
   if (T == 0) return cudaSuccess;
   const int64_t n = T * Ep;
-  split_hilo_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(dl, T, E, Ep, hi, lo);
+  split_hilo_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(dl, T, E, Ep, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stack_wr(const uint16_t* w_r, int E, int Ep, int d, uint16_t* out,
+                            cudaStream_t s) {
+  const int64_t n = static_cast<int64_t>(2) * Ep * d;
+  stack_wr_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(w_r, E, Ep, d, out);
   return cudaGetLastError();
 }
 

@@ -157,9 +157,15 @@ class MoELayer:
                                  self.dw_down_s, accumulate)
             dx_extra = self.dx_s
         L.moe_route_bwd(c, self.logits, self.topk_idx, self.gates, self.dgates, self.dlogits)
-        L.moe_router_logits_bwd(c, self.x, self.w_r, self.dlogits, self.dx_router, self.dw_r,
-                                accumulate)
-        L.moe_permute_bwd(c, self.dxs, self.dest_row, self.dx_router, dx_extra, self.dx)
+        if self.dims.k > 1:
+            # dl is k-sparse: dx_router is gathered inside the permute backward (exact fp32)
+            L.moe_router_logits_bwd(c, self.x, self.w_r, self.dlogits, None, self.dw_r, accumulate)
+            L.moe_permute_bwd_router(c, self.dxs, self.dest_row, self.topk_idx, self.dlogits,
+                                     self.w_r, dx_extra, self.dx)
+        else:
+            L.moe_router_logits_bwd(c, self.x, self.w_r, self.dlogits, self.dx_router, self.dw_r,
+                                    accumulate)
+            L.moe_permute_bwd(c, self.dxs, self.dest_row, self.dx_router, dx_extra, self.dx)
         return self.dx
 
     def kernel_launches(self, fwd=True, bwd=True) -> int:
@@ -170,8 +176,9 @@ class MoELayer:
             n += 1 + 1 + 4 + 3 + 2 + 3 + (2 if self.fs else 0)
         if bwd:
             # combine_bwd (2), ffn_bwd (4), dispatch_bwd (2), route_bwd,
-            # router bwd (hi/lo split + 2 dgrad + 2 wgrad GEMMs), permute_bwd
-            n += 2 + 4 + 2 + 1 + 5 + 1 + (4 if self.fs else 0)
+            # router bwd (hi/lo split, split-K dW_r GEMM, partial sum; k = 1 adds the
+            # stacked-W_r copy and the dense dgrad GEMM), permute_bwd
+            n += 2 + 4 + 2 + 1 + 3 + (0 if self.dims.k > 1 else 2) + 1 + (4 if self.fs else 0)
         return n
 
     def close(self):

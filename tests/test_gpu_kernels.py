@@ -162,6 +162,42 @@ def test_router_bwd(L, T, d, E):
     ctx.close()
 
 
+@pytest.mark.parametrize("T,d,E,k", [(1000, 512, 8, 2), (700, 1024, 64, 6), (300, 7168, 256, 8)])
+def test_permute_bwd_router_fused(L, T, d, E, k):
+    """B2 + B0-dgrad fused (k-sparse router gradient) == oracle dx = sum dxs rows + dl W_r^T."""
+    ctx, _ = make_ctx(L, T, d, E, k, 128, cf=1.0)
+    cfg = synth.MoEConfig("t", T=T, d=d, E=E, k=k, f=128, cf=1.0)
+    w_r = synth.router_weight(cfg).cuda()
+    logits = synth.random_logits(T, E, seed=21).cuda()
+    idx = torch.empty((T, k), dtype=torch.int32, device="cuda")
+    g = torch.empty((T, k), dtype=torch.float32, device="cuda")
+    L.moe_route(ctx, logits, idx, g)
+    x = torch.randn((T, d), device="cuda").to(torch.bfloat16)
+    counts = torch.empty((E,), dtype=torch.int32, device="cuda")
+    dest = torch.empty((T, k), dtype=torch.int32, device="cuda")
+    xs = torch.zeros((T * k, d), dtype=torch.bfloat16, device="cuda")
+    L.moe_permute(ctx, x, idx, counts, dest, xs)          # xs doubles as a dxs stand-in
+    dg = synth.random_logits(T, k, seed=22).cuda()
+    dl = torch.empty((T, E), dtype=torch.float32, device="cuda")
+    L.moe_route_bwd(ctx, logits, idx, g, dg, dl)
+    extra = torch.randn((T, d), device="cuda").to(torch.bfloat16)
+    dx = torch.empty((T, d), dtype=torch.bfloat16, device="cuda")
+    L.moe_permute_bwd_router(ctx, xs, dest, idx, dl, w_r, extra, dx)
+    torch.cuda.synchronize()
+    pos = ref.positions(idx.cpu().numpy(), E, ref.capacity(1.0, k, T, E))
+    want = ref.permute_bwd(f64(xs), pos["dest_row"])
+    want += ref.router_logits_bwd(f64(x), f64(w_r).T, f64(dl))[0] + f64(extra)
+    assert rel_err(f64(dx), want) < 8e-3
+    # the dense path gives the same numbers: dx_router GEMM + moe_permute_bwd(dx_acc)
+    dxr = torch.empty((T, d), dtype=torch.float32, device="cuda")
+    L.moe_router_logits_bwd(ctx, x, w_r, dl, dxr, None, False)
+    dx2 = torch.empty_like(dx)
+    L.moe_permute_bwd(ctx, xs, dest, dxr, extra, dx2)
+    torch.cuda.synchronize()
+    assert rel_err(f64(dx2), f64(dx)) < 8e-3
+    ctx.close()
+
+
 # ---------------------------------------------------------------- F4 / B4 grouped expert FFN
 def _ffn_case(rows, d, f, seed=0):
     g = torch.Generator(device="cpu")

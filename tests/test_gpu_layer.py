@@ -20,6 +20,8 @@ CASES = {
     "v3_small_zipf": synth.MoEConfig("v3_small_zipf", T=2048, d=512, E=256, k=8, f=256, cf=0.0,
                                      zipf_s=1.0),
     "drops": synth.MoEConfig("drops", T=600, d=128, E=8, k=2, f=256, cf=0.5),
+    # k = 1 (Switch-style): dense router gradient -> the GEMM path of moe_router_logits_bwd
+    "switch_k1": synth.MoEConfig("switch_k1", T=512, d=128, E=8, k=1, f=256, cf=1.25),
 }
 
 
