@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--a2a", action="store_true", help="dispatch/combine sweep vs NCCL")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-tokens", type=int, default=0)
+    ap.add_argument("--breakdown", action="store_true",
+                    help="per-phase CUDA-event breakdown of a step (max over ranks), no bench line")
     ap.add_argument("--profile-steps", type=int, default=0,
                     help="run only this many steps without timing (for ncu)")
     return ap.parse_args()
@@ -92,7 +94,7 @@ class ClockSampler:
                  "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except FileNotFoundError:
             self.proc = None
@@ -157,6 +159,36 @@ def run_ours(args):
     dy = dy_all[rank * T_r:(rank + 1) * T_r].contiguous()
     del x_all, dy_all
     stream = torch.cuda.current_stream()
+
+    if args.breakdown:
+        for _ in range(max(args.warmup, 3)):
+            layer.forward(x)
+            layer.backward(dy)
+        torch.cuda.synchronize()
+        acc = {}
+        for _ in range(args.steps):
+            layer.marks = []
+            layer.forward(x)
+            layer.backward(dy)
+            torch.cuda.synchronize()
+            prev = layer.marks[0][1]
+            for name, ev in layer.marks[1:]:
+                acc[name] = acc.get(name, 0.0) + prev.elapsed_time(ev)
+                prev = ev
+        layer.marks = None
+        names = list(acc)
+        v = torch.tensor([acc[n] / args.steps for n in names], dtype=torch.float64, device=dev)
+        if dist is not None:
+            dist.all_reduce(v, op=dist.ReduceOp.MAX)
+        if rank == 0:
+            tot = sum(v.tolist())
+            print(json.dumps({"breakdown_ms_max_over_ranks": {n: round(t, 4) for n, t in zip(names, v.tolist())},
+                              "sum_ms": tot, "config": args.config, "n_gpus": world}))
+        layer.close()
+        if dist is not None:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
 
     if args.profile_steps:
         for _ in range(args.profile_steps):
@@ -380,7 +412,19 @@ def run_reference(args):
     if world > 1 and rank != 0:
         return
     cfg = synth.CONFIGS[args.config]
-    n_tok = args.cpu_sample_tokens or (128 if cfg.name != "tiny" else cfg.T)
+    n_tok = args.cpu_sample_tokens
+    if not n_tok:
+        if cfg.name == "tiny":
+            n_tok = cfg.T
+        else:
+            # size each step so the whole K+W run stays within ~2 minutes of host time:
+            # one calibration step on 32 tokens, then tokens per step in [16, 256]
+            probe = _oracle_inputs(cfg, 32)
+            t0 = time.perf_counter()
+            _oracle_step(cfg, probe)
+            per_tok = (time.perf_counter() - t0) / 32
+            budget = 120.0 / max(args.steps + args.warmup, 1)
+            n_tok = int(min(256, max(16, budget / per_tok)))
     inp = _oracle_inputs(cfg, n_tok)
     for _ in range(args.warmup):
         _oracle_step(cfg, inp)

@@ -402,12 +402,8 @@ moe_status moe_dispatch(moe_ctx* c, const moe_bf16* xs, const int32_t* counts, i
   if (!c->peers_ready) return MOE_ERR_NOT_READY;
   if (!in_heap(c, xr)) return MOE_ERR_NOT_SYMMETRIC;
   CommArgs a = comm_args(c);
-  MOE_TRY_CUDA(moe::launch_counts_exchange(a, counts, layout, c->recv_rows, st(s)));
-  CommArgs b = comm_args(c);
   const int64_t dst_off = reinterpret_cast<const char*>(xr) - c->heap;
-  MOE_TRY_CUDA(moe::launch_forward_transfer(b, layout, xs, dst_off, xr, nullptr, nullptr, nullptr,
-                                            nullptr, nullptr, 0, st(s)));
-  return cuda_status(moe::launch_wait_flags(b, moe::kSlotData, st(s)));
+  return cuda_status(moe::launch_dispatch(a, counts, layout, c->recv_rows, xs, dst_off, xr, st(s)));
 }
 
 moe_status moe_dispatch_bwd(moe_ctx* c, const moe_bf16* dxr, const int32_t* layout, moe_bf16* dxs,
@@ -417,8 +413,7 @@ moe_status moe_dispatch_bwd(moe_ctx* c, const moe_bf16* dxr, const int32_t* layo
   if (!in_heap(c, dxs)) return MOE_ERR_NOT_SYMMETRIC;
   CommArgs a = comm_args(c);
   const int64_t dst_off = reinterpret_cast<const char*>(dxs) - c->heap;
-  MOE_TRY_CUDA(moe::launch_reverse_transfer(a, layout, dxr, dst_off, st(s)));
-  return cuda_status(moe::launch_wait_flags(a, moe::kSlotData, st(s)));
+  return cuda_status(moe::launch_reverse_transfer(a, layout, dxr, dst_off, st(s)));
 }
 
 // ---------------------------------------------------------------- F4 / B4
@@ -534,7 +529,6 @@ moe_status moe_combine(moe_ctx* c, const moe_bf16* out, const int32_t* layout, m
   CommArgs a = comm_args(c);
   const int64_t dst_off = reinterpret_cast<const char*>(ys) - c->heap;
   MOE_TRY_CUDA(moe::launch_reverse_transfer(a, layout, out, dst_off, st(s)));
-  MOE_TRY_CUDA(moe::launch_wait_flags(a, moe::kSlotData, st(s)));
   return cuda_status(moe::launch_unpermute(ys, gates, dest_row, y_extra, c->s.T_local, c->s.d,
                                            c->s.k, y, st(s)));
 }
@@ -547,9 +541,9 @@ moe_status moe_combine_bwd(moe_ctx* c, const moe_bf16* dy, const float* gates, c
   if (!in_heap(c, dout_r)) return MOE_ERR_NOT_SYMMETRIC;
   CommArgs a = comm_args(c);
   const int64_t dst_off = reinterpret_cast<const char*>(dout_r) - c->heap;
-  MOE_TRY_CUDA(moe::launch_forward_transfer(a, layout, nullptr, dst_off, dout_r, dest_row, gates, dy,
-                                            ys, dgates, 1, st(s)));
-  return cuda_status(moe::launch_wait_flags(a, moe::kSlotData, st(s)));
+  return cuda_status(moe::launch_combine_bwd_transfer(a, const_cast<int32_t*>(layout), dst_off,
+                                                      dout_r, dest_row, gates, dy, ys, dgates,
+                                                      st(s)));
 }
 
 }  // extern "C"

@@ -38,18 +38,48 @@ __device__ __forceinline__ int upper_bound_idx(const int32_t* arr, int n, int64_
   return lo;
 }
 
-// Last block of a transfer kernel publishes the epoch to every destination rank.
-__device__ void signal_done(const CommArgs& a, int slot) {
+__device__ void wait_all(const CommArgs& a, int slot);
+
+// Last block of a transfer kernel publishes the epoch to every destination rank and then
+// (wait_after) waits until every peer's rows have landed here, so the whole collective is a
+// single launch: the kernel completes only when this rank's receive buffer is complete.
+__device__ void signal_done(const CommArgs& a, int slot, bool wait_after) {
+  __shared__ int s_last;
   __threadfence_system();
   __syncthreads();
   if (threadIdx.x == 0) {
     const int prev = atomicAdd(a.done, 1);
-    if (prev == static_cast<int>(gridDim.x) - 1) {
-      *a.done = 0;
+    s_last = (prev == static_cast<int>(gridDim.x) - 1);
+    if (s_last) {
+      a.done[0] = 0;
+      a.done[1] = 0;  // publish_counts ticket (every block has passed it)
       __threadfence_system();
       for (int q = 0; q < a.ep; ++q) st_release_sys(peer_flag(a, q, slot, a.rank), a.epoch);
     }
   }
+  __syncthreads();
+  if (wait_after && s_last) wait_all(a, slot);
+}
+
+// Publishes this rank's E counts into row `rank` of every peer's count matrix (parity
+// buffer epoch & 1).  Done by whichever block of the launch arrives first (ticket), so it
+// cannot be starved by blocks that are already spinning on the counts flags.
+__device__ void publish_counts(const CommArgs& a, const int32_t* counts) {
+  __shared__ int s_first;
+  if (threadIdx.x == 0) s_first = (atomicAdd(a.done + 1, 1) == 0);
+  __syncthreads();
+  if (!s_first) return;
+  const int parity = static_cast<int>(a.epoch & 1);
+  const int E = a.E, EP = a.ep;
+  for (int i = threadIdx.x; i < EP * E; i += blockDim.x) {
+    const int q = i / E, e = i % E;
+    int32_t* dst = reinterpret_cast<int32_t*>(a.peers.base[q] + a.countmat_off) +
+                   (parity * EP + a.rank) * E + e;
+    *dst = counts[e];
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x < EP) st_release_sys(peer_flag(a, threadIdx.x, kSlotCounts, a.rank), a.epoch);
 }
 
 __device__ void wait_all(const CommArgs& a, int slot) {
@@ -68,59 +98,20 @@ __device__ void wait_all(const CommArgs& a, int slot) {
   __syncthreads();
 }
 
-// ---------------------------------------------------------------- counts exchange
-// One block.  counts[E] of this rank -> row `rank` of every peer's count matrix
-// (parity buffer epoch&1), then wait for all rows, then write the layout record.
-__global__ void counts_exchange_kernel(CommArgs a, const int32_t* __restrict__ counts,
-                                       int32_t* __restrict__ layout, int64_t recv_rows_cap) {
-  const int parity = static_cast<int>(a.epoch & 1);
-  const int E = a.E, EP = a.ep, E_l = a.E_l;
-  for (int i = threadIdx.x; i < EP * E; i += blockDim.x) {
-    const int q = i / E, e = i % E;
-    int32_t* dst = reinterpret_cast<int32_t*>(a.peers.base[q] + a.countmat_off) +
-                   (parity * EP + a.rank) * E + e;
-    *dst = counts[e];
-  }
-  __threadfence_system();
-  __syncthreads();
-  if (threadIdx.x < EP) st_release_sys(peer_flag(a, threadIdx.x, kSlotCounts, a.rank), a.epoch);
-  wait_all(a, kSlotCounts);
-  const int32_t* cm = a.countmat + parity * EP * E;
-  for (int i = threadIdx.x; i < EP * E; i += blockDim.x) layout[i] = cm[i];
-  int32_t* expert_rows = layout + EP * E;
-  int32_t* seg_base = expert_rows + E_l;
-  __shared__ int32_t s_rows[kMaxE];
-  for (int el = threadIdx.x; el < E_l; el += blockDim.x) {
-    int32_t s = 0;
-    for (int r = 0; r < EP; ++r) s += cm[r * E + a.rank * E_l + el];
-    s_rows[el] = s;
-    expert_rows[el] = s;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int64_t run = 0;
-    for (int el = 0; el < E_l; ++el) {
-      seg_base[el] = static_cast<int32_t>(run);
-      run += (s_rows[el] + MOE_ALIGN_ROWS - 1) / MOE_ALIGN_ROWS * MOE_ALIGN_ROWS;
-    }
-    seg_base[E_l] = static_cast<int32_t>(run);
-    if (run > recv_rows_cap) set_device_error(a.err, kDevOverflow);
-  }
-}
-
-// Shared prologue: per-expert tables of the forward pattern for THIS source rank.
-//   s_off[e]  = exclusive scan of counts_all[rank][*]  (send layout)
-//   s_dst[e]  = row of (rank, p=0) of expert e in its owner's receive buffer
+// Shared prologue: per-expert tables of the forward pattern for THIS source rank, from the
+// [EP x E] count matrix cm.
+//   off[e]  = exclusive scan of counts_all[rank][*]  (send layout)
+//   dst[e]  = row of (rank, p=0) of expert e in its owner's receive buffer
+//   seg[el] = this rank's receive segments (128-aligned prefix of its experts' rows)
 struct FwdTables {
   int32_t off[kMaxE + 1];
   int32_t dst[kMaxE];
-  int32_t seg[kMaxE + 1];    // local receive segments (for padding)
+  int32_t seg[kMaxE + 1];
   int32_t rows[kMaxE];
 };
 
-__device__ void build_fwd_tables(const CommArgs& a, const int32_t* layout, FwdTables& t) {
+__device__ void build_fwd_tables(const CommArgs& a, const int32_t* cm, FwdTables& t) {
   const int E = a.E, EP = a.ep, E_l = a.E_l;
-  const int32_t* cm = layout;
   // per-expert rows over all sources, and rows from sources before me
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
     int32_t all = 0, before = 0;
@@ -138,9 +129,11 @@ __device__ void build_fwd_tables(const CommArgs& a, const int32_t* layout, FwdTa
     int32_t run = 0;
     for (int el = 0; el < E_l; ++el) {
       const int e = q * E_l + el;
+      if (q == a.rank) t.seg[el] = run;
       t.dst[e] += run;
       run += (t.rows[e] + MOE_ALIGN_ROWS - 1) / MOE_ALIGN_ROWS * MOE_ALIGN_ROWS;
     }
+    if (q == a.rank) t.seg[E_l] = run;
   }
   if (threadIdx.x == 32) {
     int32_t run = 0;
@@ -150,8 +143,6 @@ __device__ void build_fwd_tables(const CommArgs& a, const int32_t* layout, FwdTa
     }
     t.off[E] = run;
   }
-  const int32_t* seg = layout + EP * E + E_l;
-  for (int i = threadIdx.x; i <= E_l; i += blockDim.x) t.seg[i] = seg[i];
   __syncthreads();
 }
 
@@ -197,8 +188,12 @@ __device__ void scan_segments(SegTable& t, int n) {
 
 // Forward pattern.  mode 0: payload = src send row.  mode 1 (combine_bwd): payload of
 // slot (t,j) = gates[t,j] * dy[t] (bf16), and dgates[t,j] = <dy[t], ys[dest_row[t,j]]>.
+// mode 0 is the whole dispatch in one launch: counts exchange (first block), every block
+// waits for all peers' counts, the first block writes the layout record, rows are stored,
+// and the last block waits for every peer's rows.
 template <int MODE>
-__global__ void forward_transfer_kernel(CommArgs a, const int32_t* __restrict__ layout,
+__global__ void forward_transfer_kernel(CommArgs a, int32_t* __restrict__ layout,
+                                        const int32_t* __restrict__ counts, int64_t recv_rows_cap,
                                         const uint16_t* __restrict__ src, int64_t dst_off,
                                         uint16_t* __restrict__ local_dst,
                                         const int32_t* __restrict__ dest_row,
@@ -208,7 +203,20 @@ __global__ void forward_transfer_kernel(CommArgs a, const int32_t* __restrict__ 
                                         float* __restrict__ dgates) {
   __shared__ FwdTables tb;
   __shared__ SegTable sg;
-  build_fwd_tables(a, layout, tb);
+  const int32_t* cm = layout;
+  if (MODE == 0) {
+    publish_counts(a, counts);
+    wait_all(a, kSlotCounts);
+    cm = a.countmat + static_cast<int>(a.epoch & 1) * a.ep * a.E;
+  }
+  build_fwd_tables(a, cm, tb);
+  if (MODE == 0 && blockIdx.x == 0) {  // layout record for the later calls of this layer
+    const int EP = a.ep, E = a.E, E_l = a.E_l;
+    for (int i = threadIdx.x; i < EP * E; i += blockDim.x) layout[i] = cm[i];
+    for (int el = threadIdx.x; el < E_l; el += blockDim.x) layout[EP * E + el] = tb.rows[a.rank * E_l + el];
+    for (int el = threadIdx.x; el <= E_l; el += blockDim.x) layout[EP * E + E_l + el] = tb.seg[el];
+    if (threadIdx.x == 0 && tb.seg[E_l] > recv_rows_cap) set_device_error(a.err, kDevOverflow);
+  }
   if (MODE == 0) {
     for (int i = threadIdx.x; i < a.E; i += blockDim.x) {
       const int q = (a.rank + 1 + i / a.E_l) % a.ep;   // rotated owner order
@@ -283,7 +291,7 @@ __global__ void forward_transfer_kernel(CommArgs a, const int32_t* __restrict__ 
       }
     }
   }
-  signal_done(a, kSlotData);
+  signal_done(a, kSlotData, /*wait_after=*/true);
 }
 
 // Reverse pattern: owner receive rows -> the same send-layout row on the source.
@@ -339,42 +347,35 @@ __global__ void reverse_transfer_kernel(CommArgs a, const int32_t* __restrict__ 
     uint4* dst = reinterpret_cast<uint4*>(a.peers.base[sg.dst_rank[i]] + dst_off + srow * row_bytes);
     copy_row(dst, reinterpret_cast<const uint4*>(src + row * d), nvec, lane);
   }
-  signal_done(a, kSlotData);
+  signal_done(a, kSlotData, /*wait_after=*/true);
 }
 
-__global__ void wait_flags_kernel(CommArgs a, int slot) { wait_all(a, slot); }
-
+// 2 blocks of 512 threads per SM (all co-resident: blocks spin on peer flags).
 int transfer_blocks() { return 2 * num_sms(); }
 
 }  // namespace
 
-cudaError_t launch_counts_exchange(const CommArgs& a, const int32_t* counts, int32_t* layout,
-                                   int64_t recv_rows_cap, cudaStream_t s) {
-  counts_exchange_kernel<<<1, 256, 0, s>>>(a, counts, layout, recv_rows_cap);
+cudaError_t launch_dispatch(const CommArgs& a, const int32_t* counts, int32_t* layout,
+                            int64_t recv_rows_cap, const uint16_t* src, int64_t dst_off,
+                            uint16_t* local_dst, cudaStream_t s) {
+  forward_transfer_kernel<0><<<transfer_blocks(), 512, 0, s>>>(
+      a, layout, counts, recv_rows_cap, src, dst_off, local_dst, nullptr, nullptr, nullptr, nullptr,
+      nullptr);
   return cudaGetLastError();
 }
 
-cudaError_t launch_forward_transfer(const CommArgs& a, const int32_t* layout, const uint16_t* src,
-                                    int64_t dst_off, uint16_t* local_dst, const int32_t* dest_row,
-                                    const float* gates, const uint16_t* dy, const uint16_t* ys,
-                                    float* dgates, int mode, cudaStream_t s) {
-  if (mode == 0)
-    forward_transfer_kernel<0><<<transfer_blocks(), 512, 0, s>>>(a, layout, src, dst_off, local_dst,
-                                                                 dest_row, gates, dy, ys, dgates);
-  else
-    forward_transfer_kernel<1><<<transfer_blocks(), 512, 0, s>>>(a, layout, src, dst_off, local_dst,
-                                                                 dest_row, gates, dy, ys, dgates);
+cudaError_t launch_combine_bwd_transfer(const CommArgs& a, int32_t* layout, int64_t dst_off,
+                                        uint16_t* local_dst, const int32_t* dest_row,
+                                        const float* gates, const uint16_t* dy, const uint16_t* ys,
+                                        float* dgates, cudaStream_t s) {
+  forward_transfer_kernel<1><<<transfer_blocks(), 512, 0, s>>>(
+      a, layout, nullptr, 0, nullptr, dst_off, local_dst, dest_row, gates, dy, ys, dgates);
   return cudaGetLastError();
 }
 
 cudaError_t launch_reverse_transfer(const CommArgs& a, const int32_t* layout, const uint16_t* src,
                                     int64_t dst_off, cudaStream_t s) {
   reverse_transfer_kernel<<<transfer_blocks(), 512, 0, s>>>(a, layout, src, dst_off);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_wait_flags(const CommArgs& a, int slot, cudaStream_t s) {
-  wait_flags_kernel<<<1, 32, 0, s>>>(a, slot);
   return cudaGetLastError();
 }
 

@@ -96,19 +96,21 @@ struct CommArgs {
 };
 enum { kSlotCounts = 0, kSlotData = 1, kNumSlots = 2 };
 
-cudaError_t launch_counts_exchange(const CommArgs& a, const int32_t* counts, int32_t* layout,
-                                   int64_t recv_rows_cap, cudaStream_t s);
-// forward pattern: source send-layout rows -> owners' receive rows (dst_off = byte offset of
-// the destination buffer inside every heap); zeroes the local receive padding.
-//   mode 0: payload rows = src rows (dispatch)
-//   mode 1: payload rows = gates * dy (combine_bwd), also writes dgates
-cudaError_t launch_forward_transfer(const CommArgs& a, const int32_t* layout, const uint16_t* src,
-                                    int64_t dst_off, uint16_t* local_dst, const int32_t* dest_row,
-                                    const float* gates, const uint16_t* dy, const uint16_t* ys,
-                                    float* dgates, int mode, cudaStream_t s);
-// reverse pattern: owner receive rows -> sources' send-layout rows
+// Each collective is ONE launch that returns only when this rank's destination buffer is
+// complete (the last block waits for every peer's flag).  dst_off = byte offset of the
+// destination buffer inside every rank's symmetric heap.
+// Forward pattern (source send-layout rows -> owners' receive rows; zeroes local padding):
+//   dispatch: counts exchange + layout record + rows of src
+cudaError_t launch_dispatch(const CommArgs& a, const int32_t* counts, int32_t* layout,
+                            int64_t recv_rows_cap, const uint16_t* src, int64_t dst_off,
+                            uint16_t* local_dst, cudaStream_t s);
+//   combine_bwd: payload rows gates * dy, and dgates = <dy, ys rows>
+cudaError_t launch_combine_bwd_transfer(const CommArgs& a, int32_t* layout, int64_t dst_off,
+                                        uint16_t* local_dst, const int32_t* dest_row,
+                                        const float* gates, const uint16_t* dy, const uint16_t* ys,
+                                        float* dgates, cudaStream_t s);
+// Reverse pattern: owner receive rows -> sources' send-layout rows
 cudaError_t launch_reverse_transfer(const CommArgs& a, const int32_t* layout, const uint16_t* src,
                                     int64_t dst_off, cudaStream_t s);
-cudaError_t launch_wait_flags(const CommArgs& a, int slot, cudaStream_t s);
 
 }  // namespace moe

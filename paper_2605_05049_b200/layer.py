@@ -119,23 +119,39 @@ class MoELayer:
             self.w_down_s = w_down_s.to(dev, torch.bfloat16).contiguous()
 
     # ------------------------------------------------------------------ forward
+    # per-phase CUDA-event markers (bench.py --breakdown); off by default
+    marks = None
+
+    def _mark(self, name):
+        if self.marks is not None:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            self.marks.append((name, ev))
+
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         """x [T_local, d] bf16 on this rank's device -> y [T_local, d] bf16."""
         c = self.ctx
         self.x = x
         f, T = self.dims.f, self.dims.T_local
+        self._mark("start")
         L.moe_router_logits(c, x, self.w_r, self.bias, self.logits)
         L.moe_route(c, self.logits, self.topk_idx, self.gates)
+        self._mark("F0+F1 router,route")
         L.moe_permute(c, x, self.topk_idx, self.counts, self.dest_row, self.xs)
+        self._mark("F2 permute")
         L.moe_dispatch(c, self.xs, self.counts, self.layout, self.xr)
+        self._mark("F3 dispatch")
         L.moe_expert_ffn(c, self.xr, self.expert_rows, self.E_l, self.R, f, self.w_gu, self.w_down,
                          self.g_u_h, self.out)
+        self._mark("F4 expert ffn")
         y_extra = None
         if self.fs:
             L.moe_expert_ffn(c, x, self.rows_T, 1, T, self.fs, self.w_gu_s, self.w_down_s,
                              self.g_u_h_s, self.y_s)
             y_extra = self.y_s
+            self._mark("F4s shared ffn")
         L.moe_combine(c, self.out, self.layout, self.ys, self.gates, self.dest_row, y_extra, self.y)
+        self._mark("F5+F6 combine")
         return self.y
 
     # ------------------------------------------------------------------ backward
@@ -146,39 +162,46 @@ class MoELayer:
         f, T = self.dims.f, self.dims.T_local
         L.moe_combine_bwd(c, dy, self.gates, self.dest_row, self.ys, self.layout, self.dgates,
                           self.dout_r)
+        self._mark("B6+B5 combine_bwd")
         L.moe_expert_ffn_bwd(c, self.xr, self.expert_rows, self.E_l, self.R, f, self.w_gu,
                              self.w_down, self.g_u_h, self.dout_r, self.dgu, self.dxr, self.dw_gu,
                              self.dw_down, accumulate)
+        self._mark("B4 expert ffn_bwd")
         L.moe_dispatch_bwd(c, self.dxr, self.layout, self.dxs)
+        self._mark("B3 dispatch_bwd")
         dx_extra = None
         if self.fs:
             L.moe_expert_ffn_bwd(c, self.x, self.rows_T, 1, T, self.fs, self.w_gu_s, self.w_down_s,
                                  self.g_u_h_s, dy, self.dgu_s, self.dx_s, self.dw_gu_s,
                                  self.dw_down_s, accumulate)
             dx_extra = self.dx_s
+            self._mark("B4s shared ffn_bwd")
         L.moe_route_bwd(c, self.logits, self.topk_idx, self.gates, self.dgates, self.dlogits)
         if self.dims.k > 1:
             # dl is k-sparse: dx_router is gathered inside the permute backward (exact fp32)
             L.moe_router_logits_bwd(c, self.x, self.w_r, self.dlogits, None, self.dw_r, accumulate)
+            self._mark("B1+B0 route_bwd,router dW")
             L.moe_permute_bwd_router(c, self.dxs, self.dest_row, self.topk_idx, self.dlogits,
                                      self.w_r, dx_extra, self.dx)
         else:
             L.moe_router_logits_bwd(c, self.x, self.w_r, self.dlogits, self.dx_router, self.dw_r,
                                     accumulate)
+            self._mark("B1+B0 route_bwd,router dW")
             L.moe_permute_bwd(c, self.dxs, self.dest_row, self.dx_router, dx_extra, self.dx)
+        self._mark("B2 permute_bwd")
         return self.dx
 
     def kernel_launches(self, fwd=True, bwd=True) -> int:
         """Number of libmoe kernels one forward / backward launches (for bench.py)."""
         n = 0
         if fwd:
-            # router GEMM, route, permute (4), dispatch (3), ffn (2), combine (3)
-            n += 1 + 1 + 4 + 3 + 2 + 3 + (2 if self.fs else 0)
+            # router GEMM, route, permute (4), dispatch (1 fused launch), ffn (2), combine (2)
+            n += 1 + 1 + 4 + 1 + 2 + 2 + (2 if self.fs else 0)
         if bwd:
-            # combine_bwd (2), ffn_bwd (4), dispatch_bwd (2), route_bwd,
+            # combine_bwd (1), ffn_bwd (4), dispatch_bwd (1), route_bwd,
             # router bwd (hi/lo split, split-K dW_r GEMM, partial sum; k = 1 adds the
             # stacked-W_r copy and the dense dgrad GEMM), permute_bwd
-            n += 2 + 4 + 2 + 1 + 3 + (0 if self.dims.k > 1 else 2) + 1 + (4 if self.fs else 0)
+            n += 1 + 4 + 1 + 1 + 3 + (0 if self.dims.k > 1 else 2) + 1 + (4 if self.fs else 0)
         return n
 
     def close(self):
