@@ -216,6 +216,31 @@ moe_status moe_expert_ffn_bwd(moe_ctx* ctx, const moe_bf16* xr, const int32_t* g
                               moe_bf16* dxr, float* dw_gu, float* dw_down, int accumulate,
                               moe_stream stream);
 
+/* ---------------- fused compute + all-to-all (PAPER.md:126 overlap
+ * within MoE layers) ---------------- */
+
+/* Collective.  F4 + F5 + F6 in one call for the routed experts of this rank (n_groups = E_l,
+ * group rows and receive segments from `layout`, rows_cap = moe_recv_rows_max): GEMM1 +
+ * SwiGLU, then GEMM2 whose epilogue stores every output row O[w] of local expert e_l from
+ * source r straight into rank r's ys (symmetric) at the send-layout row -- NVSwitch peer
+ * stores overlapped with the GEMM's own tiles, no local O buffer and no separate transfer
+ * kernel -- then waits for every rank's rows and computes y as moe_combine does.
+ * Bit-identical results to moe_expert_ffn + moe_combine. */
+moe_status moe_expert_ffn_combine(moe_ctx* ctx, const moe_bf16* xr, const int32_t* layout,
+                                  const moe_bf16* w_gu, const moe_bf16* w_down, moe_bf16* g_u_h,
+                                  moe_bf16* ys, const float* gates, const int32_t* dest_row,
+                                  const moe_bf16* y_extra_or_null, moe_bf16* y, moe_stream stream);
+/* Collective.  B4 + B3 in one call: as moe_expert_ffn_bwd for the routed experts, but the
+ * dgrad-2 epilogue stores every dX row straight into its source rank's dxs (symmetric) at
+ * the send-layout row; the weight-gradient GEMMs run while those stores drain, and the call
+ * ends by waiting for every rank's rows.  Bit-identical to moe_expert_ffn_bwd +
+ * moe_dispatch_bwd. */
+moe_status moe_expert_ffn_bwd_dispatch(moe_ctx* ctx, const moe_bf16* xr, const int32_t* layout,
+                                       const moe_bf16* w_gu, const moe_bf16* w_down,
+                                       const moe_bf16* g_u_h, const moe_bf16* dout, moe_bf16* dgu,
+                                       moe_bf16* dxs, float* dw_gu, float* dw_down, int accumulate,
+                                       moe_stream stream);
+
 /* ---------------- F5+F6 / B6+B5 combine ("same communication in the
  * reverse direction") ---------------- */
 

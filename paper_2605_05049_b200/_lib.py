@@ -49,7 +49,7 @@ class moe_shape(ctypes.Structure):
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(
-            f"{LIB_PATH} not found: build it with `python -m paper_2605_05049_b200.build` "
+            f"{LIB_PATH} not found: build it with `python paper_2605_05049_b200/build.py` "
             "(there is no CPU or eager fallback)")
     return ctypes.CDLL(LIB_PATH)
 
@@ -76,6 +76,8 @@ _SIGS = {
     "moe_dispatch_bwd": [P, P, P, P, P],
     "moe_expert_ffn": [P, P, P, I32, I64, I32, P, P, P, P, P],
     "moe_expert_ffn_bwd": [P, P, P, I32, I64, I32, P, P, P, P, P, P, P, P, ctypes.c_int, P],
+    "moe_expert_ffn_combine": [P, P, P, P, P, P, P, P, P, P, P, P],
+    "moe_expert_ffn_bwd_dispatch": [P, P, P, P, P, P, P, P, P, P, P, ctypes.c_int, P],
     "moe_combine": [P, P, P, P, P, P, P, P, P],
     "moe_combine_bwd": [P, P, P, P, P, P, P, P, P],
 }
@@ -286,6 +288,24 @@ def moe_expert_ffn_bwd(ctx, xr, group_rows, n_groups, rows_cap, f, w_gu, w_down,
         _ptr(g_u_h, BF16, "g_u_h"), _ptr(dout, BF16, "dout"), _ptr(dgu, BF16, "dgu"),
         _ptr(dxr, BF16, "dxr"), _ptr(dw_gu, F32, "dw_gu"), _ptr(dw_down, F32, "dw_down"),
         int(bool(accumulate)), _stream(stream)))
+
+
+def moe_expert_ffn_combine(ctx, xr, layout, w_gu, w_down, g_u_h, ys, gates, dest_row, y_extra, y,
+                           stream=None):
+    _check("moe_expert_ffn_combine", _lib.moe_expert_ffn_combine(
+        ctx.handle, _ptr(xr, BF16, "xr"), _ptr(layout, I32T, "layout"), _ptr(w_gu, BF16, "w_gu"),
+        _ptr(w_down, BF16, "w_down"), _ptr(g_u_h, BF16, "g_u_h"), _ptr(ys, BF16, "ys"),
+        _ptr(gates, F32, "gates"), _ptr(dest_row, I32T, "dest_row"), _ptr(y_extra, BF16, "y_extra"),
+        _ptr(y, BF16, "y"), _stream(stream)))
+
+
+def moe_expert_ffn_bwd_dispatch(ctx, xr, layout, w_gu, w_down, g_u_h, dout, dgu, dxs, dw_gu, dw_down,
+                                accumulate=False, stream=None):
+    _check("moe_expert_ffn_bwd_dispatch", _lib.moe_expert_ffn_bwd_dispatch(
+        ctx.handle, _ptr(xr, BF16, "xr"), _ptr(layout, I32T, "layout"), _ptr(w_gu, BF16, "w_gu"),
+        _ptr(w_down, BF16, "w_down"), _ptr(g_u_h, BF16, "g_u_h"), _ptr(dout, BF16, "dout"),
+        _ptr(dgu, BF16, "dgu"), _ptr(dxs, BF16, "dxs"), _ptr(dw_gu, F32, "dw_gu"),
+        _ptr(dw_down, F32, "dw_down"), int(bool(accumulate)), _stream(stream)))
 
 
 def moe_combine(ctx, out, layout, ys, gates, dest_row, y_extra, y, stream=None):

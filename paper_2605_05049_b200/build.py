@@ -1,7 +1,7 @@
 """Builds libmoe.so in-tree with nvcc for sm_100a (no JIT cache, no torch extension).
 
-    python -m paper_2605_05049_b200.build          # incremental
-    python -m paper_2605_05049_b200.build --force  # rebuild
+    python paper_2605_05049_b200/build.py          # incremental
+    python paper_2605_05049_b200/build.py --force  # rebuild
 """
 from __future__ import annotations
 

@@ -417,10 +417,17 @@ moe_status moe_dispatch_bwd(moe_ctx* c, const moe_bf16* dxr, const int32_t* layo
 }
 
 // ---------------------------------------------------------------- F4 / B4
-moe_status moe_expert_ffn(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows, int32_t n_groups,
-                          int64_t rows_cap, int32_t f, const moe_bf16* w_gu, const moe_bf16* w_down,
-                          moe_bf16* g_u_h, moe_bf16* out, moe_stream s) {
-  MOE_REQUIRE(c && xr && group_rows && w_gu && w_down && g_u_h && out);
+namespace {
+// Fused reverse all-to-all target of a BF16 GEMM epilogue (nullptr: plain local store).
+struct Scatter {
+  const CommArgs* comm;
+  int64_t off;
+  const int32_t* layout;
+};
+
+moe_status ffn_fwd(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows, int32_t n_groups,
+                   int64_t rows_cap, int32_t f, const moe_bf16* w_gu, const moe_bf16* w_down,
+                   moe_bf16* g_u_h, moe_bf16* out, const Scatter* sc, moe_stream s) {
   MOE_REQUIRE(n_groups >= 1 && n_groups <= 256 && rows_cap >= 0 && f > 0 && f % 128 == 0);
   if (rows_cap == 0) return MOE_OK;
   const int d = c->s.d;
@@ -445,16 +452,26 @@ moe_status moe_expert_ffn(moe_ctx* c, const moe_bf16* xr, const int32_t* group_r
   g2.N = d; g2.K = f;
   g2.group_rows = group_rows; g2.n_groups = n_groups; g2.rows_cap = rows_cap;
   g2.pair = gemm_pair();
-  g2.out = out; g2.ld_out = d;
+  g2.out = out ? static_cast<void*>(out) : static_cast<void*>(g_u_h); g2.ld_out = d;
+  if (sc) {
+    g2.scatter = 1; g2.scatter_off = sc->off; g2.scatter_layout = sc->layout; g2.comm = sc->comm;
+  }
   return cuda_status(moe::launch_grouped_gemm(g2, st(s)));
 }
+}  // namespace
 
-moe_status moe_expert_ffn_bwd(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows,
-                              int32_t n_groups, int64_t rows_cap, int32_t f, const moe_bf16* w_gu,
-                              const moe_bf16* w_down, const moe_bf16* g_u_h, const moe_bf16* dout,
-                              moe_bf16* dgu, moe_bf16* dxr, float* dw_gu, float* dw_down,
-                              int accumulate, moe_stream s) {
-  MOE_REQUIRE(c && xr && group_rows && w_gu && w_down && g_u_h && dout && dgu && dxr && dw_gu && dw_down);
+moe_status moe_expert_ffn(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows, int32_t n_groups,
+                          int64_t rows_cap, int32_t f, const moe_bf16* w_gu, const moe_bf16* w_down,
+                          moe_bf16* g_u_h, moe_bf16* out, moe_stream s) {
+  MOE_REQUIRE(c && xr && group_rows && w_gu && w_down && g_u_h && out);
+  return ffn_fwd(c, xr, group_rows, n_groups, rows_cap, f, w_gu, w_down, g_u_h, out, nullptr, s);
+}
+
+namespace {
+moe_status ffn_bwd(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows, int32_t n_groups,
+                   int64_t rows_cap, int32_t f, const moe_bf16* w_gu, const moe_bf16* w_down,
+                   const moe_bf16* g_u_h, const moe_bf16* dout, moe_bf16* dgu, moe_bf16* dxr,
+                   float* dw_gu, float* dw_down, int accumulate, const Scatter* sc, moe_stream s) {
   MOE_REQUIRE(n_groups >= 1 && n_groups <= 256 && rows_cap >= 0 && f > 0 && f % 128 == 0);
   const int d = c->s.d;
   const int64_t F = f;
@@ -489,7 +506,10 @@ moe_status moe_expert_ffn_bwd(moe_ctx* c, const moe_bf16* xr, const int32_t* gro
   b.N = d; b.K = 2 * f;
   b.group_rows = group_rows; b.n_groups = n_groups; b.rows_cap = rows_cap;
   b.pair = gemm_pair();
-  b.out = dxr; b.ld_out = d;
+  b.out = dxr ? static_cast<void*>(dxr) : static_cast<void*>(dgu); b.ld_out = d;
+  if (sc) {  // dX rows go straight back to their source ranks (dispatch_bwd fused)
+    b.scatter = 1; b.scatter_off = sc->off; b.scatter_layout = sc->layout; b.comm = sc->comm;
+  }
   MOE_TRY_CUDA(moe::launch_grouped_gemm(b, st(s)));
   // wgrad: dW_down[g] = dout_g^T H_g   [d, f]
   moe::GemmProblem w1;
@@ -517,6 +537,54 @@ moe_status moe_expert_ffn_bwd(moe_ctx* c, const moe_bf16* xr, const int32_t* gro
   w2.out = dw_gu; w2.accumulate = accumulate;
   w2.n_fastest = w2.M > w2.N;
   return cuda_status(moe::launch_grouped_gemm(w2, st(s)));
+}
+}  // namespace
+
+moe_status moe_expert_ffn_bwd(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows,
+                              int32_t n_groups, int64_t rows_cap, int32_t f, const moe_bf16* w_gu,
+                              const moe_bf16* w_down, const moe_bf16* g_u_h, const moe_bf16* dout,
+                              moe_bf16* dgu, moe_bf16* dxr, float* dw_gu, float* dw_down,
+                              int accumulate, moe_stream s) {
+  MOE_REQUIRE(c && xr && group_rows && w_gu && w_down && g_u_h && dout && dgu && dxr && dw_gu && dw_down);
+  return ffn_bwd(c, xr, group_rows, n_groups, rows_cap, f, w_gu, w_down, g_u_h, dout, dgu, dxr,
+                 dw_gu, dw_down, accumulate, nullptr, s);
+}
+
+// ---------------------------------------------------------------- F4+F5+F6 / B4+B3 fused
+moe_status moe_expert_ffn_combine(moe_ctx* c, const moe_bf16* xr, const int32_t* layout,
+                                  const moe_bf16* w_gu, const moe_bf16* w_down, moe_bf16* g_u_h,
+                                  moe_bf16* ys, const float* gates, const int32_t* dest_row,
+                                  const moe_bf16* y_extra, moe_bf16* y, moe_stream s) {
+  MOE_REQUIRE(c && xr && layout && w_gu && w_down && g_u_h && ys && gates && dest_row && y);
+  if (!c->peers_ready) return MOE_ERR_NOT_READY;
+  if (!in_heap(c, ys)) return MOE_ERR_NOT_SYMMETRIC;
+  CommArgs a = comm_args(c);
+  const Scatter sc{&a, reinterpret_cast<const char*>(ys) - c->heap, layout};
+  const int32_t* expert_rows = layout + static_cast<int64_t>(c->s.ep_size) * c->s.E;
+  moe_status r = ffn_fwd(c, xr, expert_rows, c->E_l, c->recv_rows, c->s.f, w_gu, w_down, g_u_h,
+                         nullptr, &sc, s);
+  if (r != MOE_OK) return r;
+  MOE_TRY_CUDA(moe::launch_wait_flags(a, moe::kSlotData, st(s)));
+  return cuda_status(moe::launch_unpermute(ys, gates, dest_row, y_extra, c->s.T_local, c->s.d,
+                                           c->s.k, y, st(s)));
+}
+
+moe_status moe_expert_ffn_bwd_dispatch(moe_ctx* c, const moe_bf16* xr, const int32_t* layout,
+                                       const moe_bf16* w_gu, const moe_bf16* w_down,
+                                       const moe_bf16* g_u_h, const moe_bf16* dout, moe_bf16* dgu,
+                                       moe_bf16* dxs, float* dw_gu, float* dw_down, int accumulate,
+                                       moe_stream s) {
+  MOE_REQUIRE(c && xr && layout && w_gu && w_down && g_u_h && dout && dgu && dxs && dw_gu && dw_down);
+  if (!c->peers_ready) return MOE_ERR_NOT_READY;
+  if (!in_heap(c, dxs)) return MOE_ERR_NOT_SYMMETRIC;
+  CommArgs a = comm_args(c);
+  const Scatter sc{&a, reinterpret_cast<const char*>(dxs) - c->heap, layout};
+  const int32_t* expert_rows = layout + static_cast<int64_t>(c->s.ep_size) * c->s.E;
+  moe_status r = ffn_bwd(c, xr, expert_rows, c->E_l, c->recv_rows, c->s.f, w_gu, w_down, g_u_h, dout,
+                         dgu, nullptr, dw_gu, dw_down, accumulate, &sc, s);
+  if (r != MOE_OK) return r;
+  // the dX rows streamed to the sources during dgrad-2 and the two wgrad GEMMs
+  return cuda_status(moe::launch_wait_flags(a, moe::kSlotData, st(s)));
 }
 
 // ---------------------------------------------------------------- F5+F6 / B6+B5

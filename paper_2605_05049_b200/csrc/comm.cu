@@ -350,10 +350,18 @@ __global__ void reverse_transfer_kernel(CommArgs a, const int32_t* __restrict__ 
   signal_done(a, kSlotData, /*wait_after=*/true);
 }
 
+// Waits for every rank's data flag of this epoch (the GEMM-fused reverse all-to-alls).
+__global__ void wait_flags_kernel(CommArgs a, int slot) { wait_all(a, slot); }
+
 // 2 blocks of 512 threads per SM (all co-resident: blocks spin on peer flags).
 int transfer_blocks() { return 2 * num_sms(); }
 
 }  // namespace
+
+cudaError_t launch_wait_flags(const CommArgs& a, int slot, cudaStream_t s) {
+  wait_flags_kernel<<<1, 32, 0, s>>>(a, slot);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_dispatch(const CommArgs& a, const int32_t* counts, int32_t* layout,
                             int64_t recv_rows_cap, const uint16_t* src, int64_t dst_off,

@@ -52,6 +52,14 @@ struct KParams {
   const float* bias;
   int f;
   int accumulate;
+  // BF16 epilogue fused with the reverse all-to-all (combine / dispatch_bwd): row w of local
+  // expert e_l from source r is stored straight into rank r's symmetric buffer at
+  // scatter_off, send-layout row soff[r][e_l] + (w - pre[r][e_l]); the last CTA publishes
+  // the epoch flag to every rank.  comm.layout = counts_all [EP x E].
+  int scatter;
+  int64_t scatter_off;
+  const int32_t* scatter_layout;
+  CommArgs comm;
 };
 
 template <int BN, int PAIR>
@@ -68,8 +76,8 @@ struct Cfg {
                                    : (2 * ACC_STRIDE <= 128) ? 128
                                    : (2 * ACC_STRIDE <= 256) ? 256
                                                              : 512;
-  // ring + epilogue staging + barriers/tables + alignment slack
-  static constexpr int SMEM = RING + 4 * kStageBox + 4096 + 1024;
+  // ring + epilogue staging + barriers/tables (incl. scatter tables) + alignment slack
+  static constexpr int SMEM = RING + 4 * kStageBox + 6144 + 1024;
 };
 
 __device__ __forceinline__ int ceil_div(int a, int b) { return (a + b - 1) / b; }
@@ -165,6 +173,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   int* s_tile_prefix = reinterpret_cast<int*>(tmem_slot + 4);  // [kMaxGroups+1]
   int* s_seg = s_tile_prefix + kMaxGroups + 1;                   // [kMaxGroups+1]
   int* s_rows = s_seg + kMaxGroups + 1;                          // [kMaxGroups]
+  int* s_pre = s_rows + kMaxGroups;                              // scatter: [EP][E_l] (<= 256)
+  int* s_soff = s_pre + kMaxGroups;                              // scatter: [EP][E_l]
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -221,6 +231,27 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else {
       tmem_alloc(tmem_slot, C::TMEM_COLS);
       tmem_relinquish();
+    }
+    if (EPI == kEpiBF16 && p.scatter) {
+      // reverse-pattern tables of the local experts (same definitions as comm.cu):
+      //   pre[r][el]  = rows of expert (rank*E_l + el) from sources < r  (receive order)
+      //   soff[r][el] = send-layout offset of that expert on source r
+      const CommArgs& a = p.comm;
+      const int32_t* cm = p.scatter_layout;
+      for (int el = lane; el < a.E_l; el += 32) {
+        int run = 0;
+        for (int r = 0; r < a.ep; ++r) {
+          s_pre[r * a.E_l + el] = run;
+          run += cm[r * a.E + a.rank * a.E_l + el];
+        }
+      }
+      if (lane < a.ep) {
+        int run = 0;
+        for (int e = 0; e < (a.rank + 1) * a.E_l; ++e) {
+          if (e >= a.rank * a.E_l) s_soff[lane * a.E_l + e - a.rank * a.E_l] = run;
+          run += cm[lane * a.E + e];
+        }
+      }
     }
   }
   tc_fence_before();
@@ -411,12 +442,28 @@ __global__ void __launch_bounds__(kThreads, 1)
             w[q] = valid ? pack_bf16(__uint_as_float(a[2 * q]), __uint_as_float(a[2 * q + 1])) : 0u;
             w[16 + q] = valid ? pack_bf16(__uint_as_float(b[2 * q]), __uint_as_float(b[2 * q + 1])) : 0u;
           }
-          staging_acquire(lane);
-          stage_row(row_addr, lane, w);
-          staging_release();
-          if (lane == 0) {
-            tma_store_2d(&tmC, box, tl.n * BN + c0, row0);
-            bulk_commit();
+          if (p.scatter) {
+            // fused reverse all-to-all: this row goes straight to its source rank's buffer
+            // (NVSwitch peer stores for remote ranks), 128 contiguous bytes per thread
+            if (valid) {
+              const int E_l = p.comm.E_l, g = tl.g;
+              int r = 0;
+              while (r + 1 < p.comm.ep && s_pre[(r + 1) * E_l + g] <= mi) ++r;
+              const int64_t drow = s_soff[r * E_l + g] + (mi - s_pre[r * E_l + g]);
+              uint4* dst = reinterpret_cast<uint4*>(p.comm.peers.base[r] + p.scatter_off +
+                                                    (drow * p.N + tl.n * BN + c0) * 2);
+#pragma unroll
+              for (int v = 0; v < 8; ++v)
+                st_v4(dst + v, make_uint4(w[4 * v], w[4 * v + 1], w[4 * v + 2], w[4 * v + 3]));
+            }
+          } else {
+            staging_acquire(lane);
+            stage_row(row_addr, lane, w);
+            staging_release();
+            if (lane == 0) {
+              tma_store_2d(&tmC, box, tl.n * BN + c0, row0);
+              bulk_commit();
+            }
           }
         }
       } else if (EPI == kEpiDSwiGLU) {
@@ -534,10 +581,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
     if (lane == 0) bulk_wait0();  // all TMA stores of this warp complete before exit
+    if (EPI == kEpiBF16 && p.scatter) __threadfence_system();  // peer row stores -> flag
   }
 
   tc_fence_before();
   if (PAIR == 2) cluster_sync(); else __syncthreads();
+  if (EPI == kEpiBF16 && p.scatter && threadIdx.x == 0) {
+    // the last CTA to finish publishes the epoch to every rank (as comm.cu's signal_done)
+    const CommArgs& a = p.comm;
+    if (atomicAdd(a.done, 1) == static_cast<int>(gridDim.x) - 1) {
+      a.done[0] = 0;
+      __threadfence_system();
+      for (int q = 0; q < a.ep; ++q)
+        st_release_sys(reinterpret_cast<uint64_t*>(a.peers.base[q] + a.flags_off) +
+                           kSlotData * a.ep + a.rank,
+                       a.epoch);
+    }
+  }
   if (warp == 2) {
     tc_fence_after();
     if (PAIR == 2) tmem_dealloc_pair(tmem_base, C::TMEM_COLS);
@@ -639,6 +699,13 @@ cudaError_t launch_impl(const GemmProblem& g, cudaStream_t stream) {
   kp.bias = g.bias;
   kp.f = g.f;
   kp.accumulate = g.accumulate;
+  kp.scatter = g.scatter;
+  if (g.scatter) {
+    if (EPI != kEpiBF16 || !g.comm || !g.scatter_layout) return cudaErrorInvalidValue;
+    kp.scatter_off = g.scatter_off;
+    kp.scatter_layout = g.scatter_layout;
+    kp.comm = *g.comm;
+  }
   auto kern = grouped_gemm_kernel<BN, A_MN, B_MN, EPI, PAIR>;
   static bool attr_set = false;
   if (!attr_set) {

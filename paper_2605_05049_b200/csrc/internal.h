@@ -44,6 +44,12 @@ struct GemmProblem {
   int accumulate = 0;
   int n_fastest = 0;  // tile raster order: 1 = n fastest (re-read B), 0 = m fastest (re-read A)
   int pair = 1;       // 2: CTA-pair tiles (tcgen05 cta_group::2, M = 256), BN >= 128 only
+  // kEpiBF16 only: fused reverse all-to-all (rows -> source ranks' symmetric buffer at
+  // scatter_off), the kernel's last CTA publishes comm->epoch on the data flags
+  int scatter = 0;
+  int64_t scatter_off = 0;
+  const int32_t* scatter_layout = nullptr;  // counts_all [EP x E]
+  const struct CommArgs* comm = nullptr;
 };
 
 cudaError_t launch_grouped_gemm(const GemmProblem& p, cudaStream_t stream);
@@ -112,5 +118,7 @@ cudaError_t launch_combine_bwd_transfer(const CommArgs& a, int32_t* layout, int6
 // Reverse pattern: owner receive rows -> sources' send-layout rows
 cudaError_t launch_reverse_transfer(const CommArgs& a, const int32_t* layout, const uint16_t* src,
                                     int64_t dst_off, cudaStream_t s);
+// 1-block wait for every rank's flag of a.epoch (after a GEMM with a fused scatter epilogue)
+cudaError_t launch_wait_flags(const CommArgs& a, int slot, cudaStream_t s);
 
 }  // namespace moe

@@ -48,8 +48,11 @@ def _all_gather_bytes(payload: bytes, group=None) -> bytes:
 
 
 class MoELayer:
-    def __init__(self, dims: LayerDims, device: int = 0, group=None):
+    def __init__(self, dims: LayerDims, device: int = 0, group=None, fused: bool = True):
+        """fused=True uses the compute+all-to-all entry points (moe_expert_ffn_combine,
+        moe_expert_ffn_bwd_dispatch); False issues the step-by-step calls (same results)."""
         self.dims = dims
+        self.fused = fused
         self.device = torch.device(f"cuda:{device}")
         self.shape = L.make_shape(dims.T_local, dims.d, dims.E, dims.k, dims.f, dims.E_shared,
                                   dims.capacity_factor, dims.ep_size, dims.ep_rank)
@@ -141,17 +144,24 @@ class MoELayer:
         self._mark("F2 permute")
         L.moe_dispatch(c, self.xs, self.counts, self.layout, self.xr)
         self._mark("F3 dispatch")
-        L.moe_expert_ffn(c, self.xr, self.expert_rows, self.E_l, self.R, f, self.w_gu, self.w_down,
-                         self.g_u_h, self.out)
-        self._mark("F4 expert ffn")
         y_extra = None
         if self.fs:
             L.moe_expert_ffn(c, x, self.rows_T, 1, T, self.fs, self.w_gu_s, self.w_down_s,
                              self.g_u_h_s, self.y_s)
             y_extra = self.y_s
             self._mark("F4s shared ffn")
-        L.moe_combine(c, self.out, self.layout, self.ys, self.gates, self.dest_row, y_extra, self.y)
-        self._mark("F5+F6 combine")
+        if self.fused:
+            # GEMM2's epilogue stores O rows straight into the sources' ys (combine fused)
+            L.moe_expert_ffn_combine(c, self.xr, self.layout, self.w_gu, self.w_down, self.g_u_h,
+                                     self.ys, self.gates, self.dest_row, y_extra, self.y)
+            self._mark("F4+F5+F6 expert ffn + combine")
+        else:
+            L.moe_expert_ffn(c, self.xr, self.expert_rows, self.E_l, self.R, f, self.w_gu,
+                             self.w_down, self.g_u_h, self.out)
+            self._mark("F4 expert ffn")
+            L.moe_combine(c, self.out, self.layout, self.ys, self.gates, self.dest_row, y_extra,
+                          self.y)
+            self._mark("F5+F6 combine")
         return self.y
 
     # ------------------------------------------------------------------ backward
@@ -163,12 +173,20 @@ class MoELayer:
         L.moe_combine_bwd(c, dy, self.gates, self.dest_row, self.ys, self.layout, self.dgates,
                           self.dout_r)
         self._mark("B6+B5 combine_bwd")
-        L.moe_expert_ffn_bwd(c, self.xr, self.expert_rows, self.E_l, self.R, f, self.w_gu,
-                             self.w_down, self.g_u_h, self.dout_r, self.dgu, self.dxr, self.dw_gu,
-                             self.dw_down, accumulate)
-        self._mark("B4 expert ffn_bwd")
-        L.moe_dispatch_bwd(c, self.dxr, self.layout, self.dxs)
-        self._mark("B3 dispatch_bwd")
+        if self.fused:
+            # dgrad-2's epilogue stores dX rows straight into the sources' dxs; the wgrad
+            # GEMMs run while those stores drain
+            L.moe_expert_ffn_bwd_dispatch(c, self.xr, self.layout, self.w_gu, self.w_down,
+                                          self.g_u_h, self.dout_r, self.dgu, self.dxs, self.dw_gu,
+                                          self.dw_down, accumulate)
+            self._mark("B4+B3 expert ffn_bwd + dispatch_bwd")
+        else:
+            L.moe_expert_ffn_bwd(c, self.xr, self.expert_rows, self.E_l, self.R, f, self.w_gu,
+                                 self.w_down, self.g_u_h, self.dout_r, self.dgu, self.dxr,
+                                 self.dw_gu, self.dw_down, accumulate)
+            self._mark("B4 expert ffn_bwd")
+            L.moe_dispatch_bwd(c, self.dxr, self.layout, self.dxs)
+            self._mark("B3 dispatch_bwd")
         dx_extra = None
         if self.fs:
             L.moe_expert_ffn_bwd(c, self.x, self.rows_T, 1, T, self.fs, self.w_gu_s, self.w_down_s,

@@ -40,6 +40,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="tiny", choices=list(CASES))
     ap.add_argument("--iters", type=int, default=3)
+    ap.add_argument("--stepwise", action="store_true", help="unfused step-by-step calls")
     args = ap.parse_args()
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -50,6 +51,7 @@ def main():
     from tests.helpers import TOL, f64, rel_err
 
     layer = build_layer(cfg, ep_size=ep, ep_rank=rank, device=local)
+    layer.fused = not args.stepwise
     T_r = cfg.T // ep
     x = synth.tokens(cfg).cuda()[rank * T_r:(rank + 1) * T_r].contiguous()
     dy = synth.grad_output(cfg).cuda()[rank * T_r:(rank + 1) * T_r].contiguous()

@@ -144,3 +144,27 @@ def test_identity_experts_and_determinism():
     torch.cuda.synchronize()
     assert torch.equal(ya, yb) and torch.equal(dxa, dxb) and torch.equal(dwa, dwb)
     layer.close()
+
+
+@pytest.mark.parametrize("name", ["mixtral_small", "dsmoe_small", "drops"])
+def test_fused_and_stepwise_paths_bit_identical(name):
+    """moe_expert_ffn_combine / moe_expert_ffn_bwd_dispatch (GEMM epilogues storing rows
+    straight into the sources' buffers) give bit-identical y, dx and weight gradients to
+    the step-by-step moe_expert_ffn + moe_combine / moe_expert_ffn_bwd + moe_dispatch_bwd."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    cfg = CASES[name]
+    x = synth.tokens(cfg).cuda()
+    dy = synth.grad_output(cfg).cuda()
+    outs = []
+    for fused in (True, False):
+        layer = build_layer(cfg)
+        layer.fused = fused
+        y = layer.forward(x).clone()
+        dx = layer.backward(dy).clone()
+        torch.cuda.synchronize()
+        layer.ctx.check_device_error()
+        outs.append((y, dx, layer.dw_gu.clone(), layer.dw_down.clone(), layer.dgates.clone()))
+        layer.close()
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)

@@ -1,6 +1,6 @@
 """Multi-GPU parity of the expert-parallel layer (NVSwitch peer-store dispatch/combine):
 one torchrun rank per GPU, results gathered on rank 0 and checked against the fp64 oracle
-simulating every EP rank (tests/mp_layer_worker.py).  Skipped with fewer than 2 GPUs."""
+simulating every EP rank (tests/mp_layer_worker.py).  Skipped with fewer GPUs than ranks."""
 import json
 import os
 import subprocess
@@ -11,16 +11,17 @@ import torch
 
 pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CONFIGS = ["tiny", "mixtral_small", "dsmoe_small", "v3_small_zipf", "drops"]
 
 
 def n_gpus():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-def run_worker(nproc, config, port):
+def run_worker(nproc, config, port, extra=()):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr=127.0.0.1", f"--master-port={port}",
-           os.path.join(ROOT, "tests", "mp_layer_worker.py"), "--config", config]
+           os.path.join(ROOT, "tests", "mp_layer_worker.py"), "--config", config, *extra]
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     lines = [l for l in p.stdout.splitlines() if l.startswith("{")]
     assert p.returncode == 0 and lines, f"worker failed:\n{p.stdout[-3000:]}\n{p.stderr[-3000:]}"
@@ -28,11 +29,22 @@ def run_worker(nproc, config, port):
 
 
 @pytest.mark.parametrize("nproc", [2, 4, 8])
-@pytest.mark.parametrize("config", ["tiny", "mixtral_small", "dsmoe_small", "v3_small_zipf", "drops"])
+@pytest.mark.parametrize("config", CONFIGS)
 def test_layer_ep_parity(nproc, config):
+    """Fused path (GEMM epilogues store rows straight into peers' buffers)."""
     if n_gpus() < nproc:
         pytest.skip(f"needs {nproc} GPUs")
-    port = 29500 + nproc * 10 + ["tiny", "mixtral_small", "dsmoe_small", "v3_small_zipf", "drops"].index(config)
-    res = run_worker(nproc, config, port)
+    res = run_worker(nproc, config, 29500 + nproc * 10 + CONFIGS.index(config))
+    print(res)
+    assert res["ok"], res
+
+
+@pytest.mark.parametrize("nproc", [2, 4])
+@pytest.mark.parametrize("config", ["mixtral_small", "dsmoe_small"])
+def test_layer_ep_parity_stepwise(nproc, config):
+    """Step-by-step path (separate transfer kernels for combine and dispatch_bwd)."""
+    if n_gpus() < nproc:
+        pytest.skip(f"needs {nproc} GPUs")
+    res = run_worker(nproc, config, 29700 + nproc * 10 + CONFIGS.index(config), ("--stepwise",))
     print(res)
     assert res["ok"], res
