@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--a2a", action="store_true", help="dispatch/combine sweep vs NCCL")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--stepwise", action="store_true",
+                    help="step-by-step C-ABI calls instead of the fused compute+all-to-all ones")
     ap.add_argument("--cpu-sample-tokens", type=int, default=0)
     ap.add_argument("--breakdown", action="store_true",
                     help="per-phase CUDA-event breakdown of a step (max over ranks), no bench line")
@@ -125,6 +127,18 @@ class ClockSampler:
                 "reasons": sorted(reasons)}
 
 
+def gemm_traffic(config, world):
+    """DRAM bytes per step of the 6 expert-GEMM launches from the committed ncu --set full
+    capture (profiles/gemm_traffic.json), for the configuration it was captured on."""
+    p = os.path.join(ROOT, "profiles", "gemm_traffic.json")
+    key = f"{config}_ep{world}"
+    try:
+        with open(p) as fh:
+            return json.load(fh)[key]["dram_bytes_per_step"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def realised_gemm_flops(layer, cfg):
     """Algorithmic GEMM FLOPs of one fwd+bwd on this rank from the realised routing:
     6 * rows * d * f (fwd) + 12 * rows * d * f (bwd), plus the shared experts."""
@@ -146,7 +160,7 @@ def run_ours(args):
     ep = world
     T_r = cfg.T // ep
     dims = LayerDims(T_r, cfg.d, cfg.E, cfg.k, cfg.f, cfg.E_s, cfg.cf, ep, rank)
-    layer = MoELayer(dims, device=local)
+    layer = MoELayer(dims, device=local, fused=not args.stepwise)
     E_l = cfg.E // ep
     dev = torch.device(f"cuda:{local}")
     w_gu, w_down = synth.expert_weights(cfg, range(rank * E_l, (rank + 1) * E_l), device=dev)
@@ -206,8 +220,6 @@ def run_ours(args):
 
     # GEMM-region events (the dominant kernel family: 6 grouped-GEMM launches per step)
     gemm_ev = []
-    orig_ffn, orig_ffn_bwd = None, None
-    from paper_2605_05049_b200 import _lib as L
     import paper_2605_05049_b200.layer as layer_mod
 
     def timed(fn):
@@ -226,9 +238,13 @@ def run_ours(args):
     layer.ctx.check_device_error()
 
     # ---- device-timed region
-    orig_ffn, orig_ffn_bwd = layer_mod.L.moe_expert_ffn, layer_mod.L.moe_expert_ffn_bwd
-    layer_mod.L.moe_expert_ffn = timed(orig_ffn)
-    layer_mod.L.moe_expert_ffn_bwd = timed(orig_ffn_bwd)
+    # the grouped-GEMM calls (fused: their epilogues also store rows to the peers, and the
+    # calls end with the flag wait / unpermute -- so the measured region is conservative)
+    hooked = ["moe_expert_ffn", "moe_expert_ffn_bwd", "moe_expert_ffn_combine",
+              "moe_expert_ffn_bwd_dispatch"]
+    originals = {n: getattr(layer_mod.L, n) for n in hooked}
+    for n in hooked:
+        setattr(layer_mod.L, n, timed(originals[n]))
     clocks = ClockSampler(local)
     barrier()
     torch.cuda.synchronize()
@@ -243,7 +259,8 @@ def run_ours(args):
     torch.cuda.synchronize()
     barrier()
     clk = clocks.stop()
-    layer_mod.L.moe_expert_ffn, layer_mod.L.moe_expert_ffn_bwd = orig_ffn, orig_ffn_bwd
+    for n in hooked:
+        setattr(layer_mod.L, n, originals[n])
     layer.ctx.check_device_error()
     ms = t0.elapsed_time(t1) / args.steps
     gemm_ms = sum(s.elapsed_time(e) for s, e in gemm_ev) / args.steps
@@ -341,14 +358,15 @@ def run_ours(args):
         "gpu_launches": layer.kernel_launches() * args.steps,
         "clocks": clk,
         "roofline": {
-            "kernel": "grouped_gemm_kernel (tcgen05; 6 launches/step: GEMM1+SwiGLU, GEMM2, "
-                      "dgrad x2, wgrad x2)",
+            "kernel": "grouped_gemm_kernel (tcgen05 cta_group::2; 6 launches/step: GEMM1+SwiGLU, "
+                      "GEMM2(+combine stores), dgrad-1+dSwiGLU, dgrad-2(+dispatch_bwd stores), "
+                      "wgrad x2); timed region = the FFN C-ABI calls",
             "bound": "tensor",
             "achieved": achieved,
             "peak": peaks["bf16_sustained"],
             "unit": "TFLOP/s",
             "frac": achieved / peaks["bf16_sustained"],
-            "traffic": None,
+            "traffic": gemm_traffic(args.config, world),
             "peak_source": peaks["source"] + " bf16_tflops_sustained (kernel timed inside a long step)",
             "algorithmic_flops_per_step": gemm_flops,
             "gemm_ms_per_step": gemm_ms,

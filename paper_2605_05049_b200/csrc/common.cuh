@@ -156,6 +156,17 @@ MOE_DEVINL void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "m
 MOE_DEVINL void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+// 1-D bulk copy shared -> global (any global address incl. NVSwitch-mapped peer memory),
+// completion tracked by the issuing thread's bulk groups.
+MOE_DEVINL void bulk_copy_s2g(void* gdst, uint32_t smem_src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+               "r"(smem_src), "r"(bytes)
+               : "memory");
+}
+// async-proxy global writes (bulk copies) -> ordered before later generic-proxy operations
+MOE_DEVINL void fence_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
 MOE_DEVINL void prefetch_l2_bulk(const void* gptr, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gptr), "r"(bytes) : "memory");
 }

@@ -443,18 +443,23 @@ __global__ void __launch_bounds__(kThreads, 1)
             w[16 + q] = valid ? pack_bf16(__uint_as_float(b[2 * q]), __uint_as_float(b[2 * q + 1])) : 0u;
           }
           if (p.scatter) {
-            // fused reverse all-to-all: this row goes straight to its source rank's buffer
-            // (NVSwitch peer stores for remote ranks), 128 contiguous bytes per thread
+            // fused reverse all-to-all: this row's 128 bytes go straight to its source rank's
+            // buffer as one asynchronous bulk copy (NVSwitch for remote ranks), so the NVLink
+            // latency is absorbed by the copy engine, not by the epilogue warps
+            bulk_wait_read0();                       // my previous copy has read my row
+            const uint32_t lin = smem_u32(box) + lane * 128;   // linear (unswizzled) row
+#pragma unroll
+            for (int v = 0; v < 8; ++v)
+              st_shared_v4(lin + v * 16, w[4 * v], w[4 * v + 1], w[4 * v + 2], w[4 * v + 3]);
+            fence_async_smem();
             if (valid) {
               const int E_l = p.comm.E_l, g = tl.g;
               int r = 0;
               while (r + 1 < p.comm.ep && s_pre[(r + 1) * E_l + g] <= mi) ++r;
               const int64_t drow = s_soff[r * E_l + g] + (mi - s_pre[r * E_l + g]);
-              uint4* dst = reinterpret_cast<uint4*>(p.comm.peers.base[r] + p.scatter_off +
-                                                    (drow * p.N + tl.n * BN + c0) * 2);
-#pragma unroll
-              for (int v = 0; v < 8; ++v)
-                st_v4(dst + v, make_uint4(w[4 * v], w[4 * v + 1], w[4 * v + 2], w[4 * v + 3]));
+              bulk_copy_s2g(p.comm.peers.base[r] + p.scatter_off + (drow * p.N + tl.n * BN + c0) * 2,
+                            lin, 128);
+              bulk_commit();
             }
           } else {
             staging_acquire(lane);
@@ -580,8 +585,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
-    if (lane == 0) bulk_wait0();  // all TMA stores of this warp complete before exit
-    if (EPI == kEpiBF16 && p.scatter) __threadfence_system();  // peer row stores -> flag
+    if (EPI == kEpiBF16 && p.scatter) {
+      bulk_wait0();            // every lane's row copies complete ...
+      fence_async_global();    // ... and ordered before the flag release below
+      __threadfence_system();
+    } else if (lane == 0) {
+      bulk_wait0();            // all TMA stores of this warp complete before exit
+    }
   }
 
   tc_fence_before();
