@@ -111,6 +111,11 @@ moe_status moe_ctx_open_peers(moe_ctx* ctx, const void* handles);
 /* Bump allocation from the symmetric heap, 256-byte aligned.  Collective: every rank
  * must request the same sizes in the same order so offsets agree. */
 moe_status moe_symm_alloc(moe_ctx* ctx, size_t bytes, void** ptr);
+/* SM budgets for the calls issued after it (0 = all SMs): grouped-GEMM launches use at most
+ * gemm_sms SMs and all-to-all transfer launches 2 blocks on each of comm_sms SMs, so that a
+ * GEMM and a transfer issued on two streams run concurrently on disjoint SMs (used to overlap
+ * the shared-expert GEMMs with dispatch / combine_bwd). */
+moe_status moe_ctx_set_sm_limits(moe_ctx* ctx, int gemm_sms, int comm_sms);
 /* Synchronises the device; returns MOE_OK or the first device-side error recorded. */
 moe_status moe_ctx_get_device_error(moe_ctx* ctx);
 moe_status moe_ctx_destroy(moe_ctx* ctx);

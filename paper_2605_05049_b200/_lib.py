@@ -64,6 +64,7 @@ _SIGS = {
     "moe_ctx_open_peers": [P, P],
     "moe_symm_alloc": [P, ctypes.c_size_t, ctypes.POINTER(P)],
     "moe_ctx_get_device_error": [P],
+    "moe_ctx_set_sm_limits": [P, ctypes.c_int, ctypes.c_int],
     "moe_ctx_destroy": [P],
     "moe_router_logits": [P, P, P, P, P, P],
     "moe_router_logits_bwd": [P, P, P, P, P, P, ctypes.c_int, P],
@@ -192,6 +193,10 @@ class Context:
         t = raw[: numel * elem].view(dtype).view(*shape)
         self._views.append(raw)
         return t
+
+    def set_sm_limits(self, gemm_sms: int, comm_sms: int):
+        _check("moe_ctx_set_sm_limits", _lib.moe_ctx_set_sm_limits(self._h, int(gemm_sms),
+                                                                   int(comm_sms)))
 
     def device_error(self):
         return _lib.moe_ctx_get_device_error(self._h)

@@ -37,6 +37,8 @@ struct moe_ctx {
   int32_t* d_split_rows = nullptr;// [S] token rows per split
   int n_split = 1;
   int Ep = 0;                     // E rounded up to 8
+  int gemm_sms = 0;               // SM budgets (0 = all): a GEMM and a transfer running
+  int comm_sms = 0;               //   concurrently on two streams use disjoint SMs
 };
 
 namespace {
@@ -113,6 +115,7 @@ CommArgs comm_args(moe_ctx* c) {
   a.done = c->d_done;
   a.err = c->d_err;
   a.epoch = ++c->epoch;
+  a.blocks = c->comm_sms > 0 ? 2 * c->comm_sms : 0;
   return a;
 }
 
@@ -263,6 +266,13 @@ moe_status moe_symm_alloc(moe_ctx* c, size_t bytes, void** ptr) {
   if (c->heap_used + sz > c->heap_bytes) return MOE_ERR_OUT_OF_MEMORY;
   *ptr = c->heap + c->heap_used;
   c->heap_used += sz;
+  return MOE_OK;
+}
+
+moe_status moe_ctx_set_sm_limits(moe_ctx* c, int gemm_sms, int comm_sms) {
+  MOE_REQUIRE(c && gemm_sms >= 0 && comm_sms >= 0);
+  c->gemm_sms = gemm_sms;
+  c->comm_sms = comm_sms;
   return MOE_OK;
 }
 
@@ -440,6 +450,7 @@ moe_status ffn_fwd(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows, in
   g1.N = 2 * f; g1.K = d;
   g1.group_rows = group_rows; g1.n_groups = n_groups; g1.rows_cap = rows_cap;
   g1.pair = gemm_pair();
+  g1.max_ctas = c->gemm_sms;
   g1.out = g_u_h; g1.ld_out = 3 * static_cast<int64_t>(f); g1.f = f;
   MOE_TRY_CUDA(moe::launch_grouped_gemm(g1, st(s)));
   moe::GemmProblem g2;
@@ -452,6 +463,7 @@ moe_status ffn_fwd(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows, in
   g2.N = d; g2.K = f;
   g2.group_rows = group_rows; g2.n_groups = n_groups; g2.rows_cap = rows_cap;
   g2.pair = gemm_pair();
+  g2.max_ctas = c->gemm_sms;
   g2.out = out ? static_cast<void*>(out) : static_cast<void*>(g_u_h); g2.ld_out = d;
   if (sc) {
     g2.scatter = 1; g2.scatter_off = sc->off; g2.scatter_layout = sc->layout; g2.comm = sc->comm;
@@ -493,6 +505,7 @@ moe_status ffn_bwd(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows, in
   a.N = f; a.K = d;
   a.group_rows = group_rows; a.n_groups = n_groups; a.rows_cap = rows_cap;
   a.pair = gemm_pair();
+  a.max_ctas = c->gemm_sms;
   a.out = dgu; a.ld_out = 2 * F; a.aux = g_u_h; a.ld_aux = 3 * F; a.f = f;
   MOE_TRY_CUDA(moe::launch_grouped_gemm(a, st(s)));
   // dgrad-2: dX = [dG dU] . W_gu  -> dxr
@@ -506,6 +519,7 @@ moe_status ffn_bwd(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows, in
   b.N = d; b.K = 2 * f;
   b.group_rows = group_rows; b.n_groups = n_groups; b.rows_cap = rows_cap;
   b.pair = gemm_pair();
+  b.max_ctas = c->gemm_sms;
   b.out = dxr ? static_cast<void*>(dxr) : static_cast<void*>(dgu); b.ld_out = d;
   if (sc) {  // dX rows go straight back to their source ranks (dispatch_bwd fused)
     b.scatter = 1; b.scatter_off = sc->off; b.scatter_layout = sc->layout; b.comm = sc->comm;
@@ -521,6 +535,7 @@ moe_status ffn_bwd(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows, in
   w1.M = d; w1.N = f;
   w1.group_rows = group_rows; w1.n_groups = n_groups; w1.rows_cap = rows_cap;
   w1.pair = gemm_pair();
+  w1.max_ctas = c->gemm_sms;
   w1.out = dw_down; w1.accumulate = accumulate;
   w1.n_fastest = w1.M > w1.N;   // keep the smaller operand slab re-read from L2
   MOE_TRY_CUDA(moe::launch_grouped_gemm(w1, st(s)));
@@ -534,6 +549,7 @@ moe_status ffn_bwd(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows, in
   w2.M = 2 * f; w2.N = d;
   w2.group_rows = group_rows; w2.n_groups = n_groups; w2.rows_cap = rows_cap;
   w2.pair = gemm_pair();
+  w2.max_ctas = c->gemm_sms;
   w2.out = dw_gu; w2.accumulate = accumulate;
   w2.n_fastest = w2.M > w2.N;
   return cuda_status(moe::launch_grouped_gemm(w2, st(s)));

@@ -354,7 +354,7 @@ __global__ void reverse_transfer_kernel(CommArgs a, const int32_t* __restrict__ 
 __global__ void wait_flags_kernel(CommArgs a, int slot) { wait_all(a, slot); }
 
 // 2 blocks of 512 threads per SM (all co-resident: blocks spin on peer flags).
-int transfer_blocks() { return 2 * num_sms(); }
+int transfer_blocks(const CommArgs& a) { return a.blocks > 0 ? a.blocks : 2 * num_sms(); }
 
 }  // namespace
 
@@ -366,7 +366,7 @@ cudaError_t launch_wait_flags(const CommArgs& a, int slot, cudaStream_t s) {
 cudaError_t launch_dispatch(const CommArgs& a, const int32_t* counts, int32_t* layout,
                             int64_t recv_rows_cap, const uint16_t* src, int64_t dst_off,
                             uint16_t* local_dst, cudaStream_t s) {
-  forward_transfer_kernel<0><<<transfer_blocks(), 512, 0, s>>>(
+  forward_transfer_kernel<0><<<transfer_blocks(a), 512, 0, s>>>(
       a, layout, counts, recv_rows_cap, src, dst_off, local_dst, nullptr, nullptr, nullptr, nullptr,
       nullptr);
   return cudaGetLastError();
@@ -376,14 +376,14 @@ cudaError_t launch_combine_bwd_transfer(const CommArgs& a, int32_t* layout, int6
                                         uint16_t* local_dst, const int32_t* dest_row,
                                         const float* gates, const uint16_t* dy, const uint16_t* ys,
                                         float* dgates, cudaStream_t s) {
-  forward_transfer_kernel<1><<<transfer_blocks(), 512, 0, s>>>(
+  forward_transfer_kernel<1><<<transfer_blocks(a), 512, 0, s>>>(
       a, layout, nullptr, 0, nullptr, dst_off, local_dst, dest_row, gates, dy, ys, dgates);
   return cudaGetLastError();
 }
 
 cudaError_t launch_reverse_transfer(const CommArgs& a, const int32_t* layout, const uint16_t* src,
                                     int64_t dst_off, cudaStream_t s) {
-  reverse_transfer_kernel<<<transfer_blocks(), 512, 0, s>>>(a, layout, src, dst_off);
+  reverse_transfer_kernel<<<transfer_blocks(a), 512, 0, s>>>(a, layout, src, dst_off);
   return cudaGetLastError();
 }
 

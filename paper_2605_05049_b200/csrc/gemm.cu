@@ -724,7 +724,8 @@ cudaError_t launch_impl(const GemmProblem& g, cudaStream_t stream) {
     attr_set = true;
   }
   if (PAIR == 1) {
-    kern<<<num_sms(), kThreads, C::SMEM, stream>>>(ta, tb, tc, kp);
+    const int grid = (g.max_ctas > 0 && g.max_ctas < num_sms()) ? g.max_ctas : num_sms();
+    kern<<<grid, kThreads, C::SMEM, stream>>>(ta, tb, tc, kp);
     return cudaGetLastError();
   }
   cudaLaunchConfig_t cfg;
@@ -750,7 +751,9 @@ cudaError_t launch_impl(const GemmProblem& g, cudaStream_t stream) {
     if (getenv("MOE_VERBOSE"))
       fprintf(stderr, "[libmoe] gemm<BN=%d,epi=%d> pair grid: %d co-resident clusters of 2\n", BN, EPI, n);
   }
-  cfg.gridDim = dim3(2 * max_clusters);
+  int clusters = max_clusters;
+  if (g.max_ctas > 0 && g.max_ctas / 2 < clusters) clusters = g.max_ctas / 2 > 0 ? g.max_ctas / 2 : 1;
+  cfg.gridDim = dim3(2 * clusters);
   return cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, kp);
 }
 

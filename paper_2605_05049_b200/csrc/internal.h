@@ -43,6 +43,7 @@ struct GemmProblem {
   int f = 0;
   int accumulate = 0;
   int n_fastest = 0;  // tile raster order: 1 = n fastest (re-read B), 0 = m fastest (re-read A)
+  int max_ctas = 0;   // SM budget (0 = all SMs); used to run a GEMM beside a transfer
   int pair = 1;       // 2: CTA-pair tiles (tcgen05 cta_group::2, M = 256), BN >= 128 only
   // kEpiBF16 only: fused reverse all-to-all (rows -> source ranks' symmetric buffer at
   // scatter_off), the kernel's last CTA publishes comm->epoch on the data flags
@@ -99,6 +100,7 @@ struct CommArgs {
   int32_t* done;         // local device counter for last-block detection
   int32_t* err;          // device error word
   uint64_t epoch;
+  int blocks;            // transfer kernel blocks (0 = 2 per SM)
 };
 enum { kSlotCounts = 0, kSlotData = 1, kNumSlots = 2 };
 

@@ -53,6 +53,8 @@ class MoELayer:
         moe_expert_ffn_bwd_dispatch); False issues the step-by-step calls (same results)."""
         self.dims = dims
         self.fused = fused
+        self.overlap = True   # shared-expert GEMMs beside dispatch / combine_bwd (E_s > 0)
+        self._side = None
         self.device = torch.device(f"cuda:{device}")
         self.shape = L.make_shape(dims.T_local, dims.d, dims.E, dims.k, dims.f, dims.E_shared,
                                   dims.capacity_factor, dims.ep_size, dims.ep_rank)
@@ -124,6 +126,31 @@ class MoELayer:
     # ------------------------------------------------------------------ forward
     # per-phase CUDA-event markers (bench.py --breakdown); off by default
     marks = None
+    # SMs given to an all-to-all that runs beside a GEMM (the GEMM gets the rest)
+    comm_sms = 20
+
+    def _concurrent(self, comm_fn, gemm_fn):
+        """comm_fn(stream) on a side stream with `comm_sms` SMs, gemm_fn(stream) on the current
+        stream with the remaining SMs; both ordered after everything issued so far, and the
+        current stream waits for both at the end."""
+        main = torch.cuda.current_stream(self.device)
+        if self._side is None:
+            self._side = torch.cuda.Stream(device=self.device)
+        side = self._side
+        start = torch.cuda.Event()
+        start.record(main)
+        side.wait_event(start)
+        n_sms = torch.cuda.get_device_properties(self.device).multi_processor_count
+        # GEMM first: its CTAs (one per SM, ~213 KB smem) take their SMs, the transfer blocks
+        # fill the SMs left over
+        self.ctx.set_sm_limits(n_sms - self.comm_sms, 0)
+        gemm_fn(main)
+        self.ctx.set_sm_limits(0, self.comm_sms)
+        comm_fn(side)
+        self.ctx.set_sm_limits(0, 0)
+        done = torch.cuda.Event()
+        done.record(side)
+        main.wait_event(done)
 
     def _mark(self, name):
         if self.marks is not None:
@@ -142,14 +169,25 @@ class MoELayer:
         self._mark("F0+F1 router,route")
         L.moe_permute(c, x, self.topk_idx, self.counts, self.dest_row, self.xs)
         self._mark("F2 permute")
-        L.moe_dispatch(c, self.xs, self.counts, self.layout, self.xr)
-        self._mark("F3 dispatch")
         y_extra = None
-        if self.fs:
-            L.moe_expert_ffn(c, x, self.rows_T, 1, T, self.fs, self.w_gu_s, self.w_down_s,
-                             self.g_u_h_s, self.y_s)
+        if self.fs and self.overlap:
+            # shared experts (local tokens, no exchange) run beside the dispatch all-to-all on
+            # disjoint SMs: dispatch on a side stream, shared GEMMs on this one
+            self._concurrent(lambda s: L.moe_dispatch(c, self.xs, self.counts, self.layout,
+                                                      self.xr, stream=s),
+                             lambda s: L.moe_expert_ffn(c, x, self.rows_T, 1, T, self.fs,
+                                                        self.w_gu_s, self.w_down_s, self.g_u_h_s,
+                                                        self.y_s, stream=s))
             y_extra = self.y_s
-            self._mark("F4s shared ffn")
+            self._mark("F3 dispatch || F4s shared ffn")
+        else:
+            L.moe_dispatch(c, self.xs, self.counts, self.layout, self.xr)
+            self._mark("F3 dispatch")
+            if self.fs:
+                L.moe_expert_ffn(c, x, self.rows_T, 1, T, self.fs, self.w_gu_s, self.w_down_s,
+                                 self.g_u_h_s, self.y_s)
+                y_extra = self.y_s
+                self._mark("F4s shared ffn")
         if self.fused:
             # GEMM2's epilogue stores O rows straight into the sources' ys (combine fused)
             L.moe_expert_ffn_combine(c, self.xr, self.layout, self.w_gu, self.w_down, self.g_u_h,
@@ -170,9 +208,23 @@ class MoELayer:
         (and dw_gu_s, dw_down_s) as fp32 per-rank gradients."""
         c = self.ctx
         f, T = self.dims.f, self.dims.T_local
-        L.moe_combine_bwd(c, dy, self.gates, self.dest_row, self.ys, self.layout, self.dgates,
-                          self.dout_r)
-        self._mark("B6+B5 combine_bwd")
+        shared_done = False
+        if self.fs and self.overlap:
+            # shared-expert backward (needs only dy) beside the combine_bwd all-to-all
+            self._concurrent(lambda s: L.moe_combine_bwd(c, dy, self.gates, self.dest_row, self.ys,
+                                                         self.layout, self.dgates, self.dout_r,
+                                                         stream=s),
+                             lambda s: L.moe_expert_ffn_bwd(c, self.x, self.rows_T, 1, T, self.fs,
+                                                            self.w_gu_s, self.w_down_s,
+                                                            self.g_u_h_s, dy, self.dgu_s,
+                                                            self.dx_s, self.dw_gu_s,
+                                                            self.dw_down_s, accumulate, stream=s))
+            shared_done = True
+            self._mark("B6+B5 combine_bwd || B4s shared ffn_bwd")
+        else:
+            L.moe_combine_bwd(c, dy, self.gates, self.dest_row, self.ys, self.layout, self.dgates,
+                              self.dout_r)
+            self._mark("B6+B5 combine_bwd")
         if self.fused:
             # dgrad-2's epilogue stores dX rows straight into the sources' dxs; the wgrad
             # GEMMs run while those stores drain
@@ -187,12 +239,11 @@ class MoELayer:
             self._mark("B4 expert ffn_bwd")
             L.moe_dispatch_bwd(c, self.dxr, self.layout, self.dxs)
             self._mark("B3 dispatch_bwd")
-        dx_extra = None
-        if self.fs:
+        dx_extra = self.dx_s if self.fs else None
+        if self.fs and not shared_done:
             L.moe_expert_ffn_bwd(c, self.x, self.rows_T, 1, T, self.fs, self.w_gu_s, self.w_down_s,
                                  self.g_u_h_s, dy, self.dgu_s, self.dx_s, self.dw_gu_s,
                                  self.dw_down_s, accumulate)
-            dx_extra = self.dx_s
             self._mark("B4s shared ffn_bwd")
         L.moe_route_bwd(c, self.logits, self.topk_idx, self.gates, self.dgates, self.dlogits)
         if self.dims.k > 1:
