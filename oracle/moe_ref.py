@@ -202,29 +202,36 @@ def permute_bwd(dxs, dest_row):
 # ---------------------------------------------------------------------------
 
 
-def recv_layout(counts_all, ep, align=1):
-    """counts_all [EP, E] (kept rows from source r to expert e).  For owner q:
+def recv_layout(counts_all, ep, align=1, placement=None):
+    """counts_all [EP, E] (kept rows from source r to expert e).  placement[e] = global slot
+    of expert e (owner = slot // E_l, local slot = slot % E_l; default contiguous slot = e,
+    reading R7; expert migration, NEXT-2, permutes it).  For owner q, per local slot el:
     recv_counts[q] [E_l, EP]; expert_rows[q] [E_l]; seg_base[q] [E_l+1] with
-    seg_base[e_l+1] = seg_base[e_l] + roundup(expert_rows[e_l], align);
-    src_base[q] [E_l, EP] = seg_base[e_l] + sum_{r'<r} counts[r'][e]."""
+    seg_base[el+1] = seg_base[el] + roundup(expert_rows[el], align);
+    src_base[q] [E_l, EP] = seg_base[el] + sum_{r'<r} counts[r'][e]; expert[q] [E_l]."""
     counts_all = np.asarray(counts_all, np.int64)
     EP, E = counts_all.shape
     if EP != ep or E % ep:
         raise ValueError("counts_all must be [EP, E] with EP | E")
     E_l = E // ep
+    placement = np.arange(E) if placement is None else np.asarray(placement, np.int64)
+    expert_at = np.empty(E, np.int64)
+    expert_at[placement] = np.arange(E)
     out = []
     for q in range(ep):
-        rc = counts_all[:, q * E_l:(q + 1) * E_l].T.copy()          # [E_l, EP]
+        experts = expert_at[q * E_l:(q + 1) * E_l]
+        rc = counts_all[:, experts].T.copy()                           # [E_l, EP]
         rows = rc.sum(axis=1)
         padded = -(-rows // align) * align
         seg = np.concatenate(([0], np.cumsum(padded)))
         src = seg[:-1, None] + np.concatenate((np.zeros((E_l, 1), np.int64),
                                                np.cumsum(rc, axis=1)[:, :-1]), axis=1)
-        out.append(dict(recv_counts=rc, expert_rows=rows, seg_base=seg, src_base=src))
+        out.append(dict(recv_counts=rc, expert_rows=rows, seg_base=seg, src_base=src,
+                        expert=experts))
     return out
 
 
-def dispatch_plan(topk_idx, E, ep, C, align=1):
+def dispatch_plan(topk_idx, E, ep, C, align=1, placement=None):
     """Whole-EP-group routing plan.  topk_idx [T,k] global (rank r owns rows
     r*T_r..(r+1)*T_r-1).  Returns per-rank `positions` results, the [EP,E] count
     matrix, the receive layouts and recv_row[T,k] = row of slot (t,j) in its
@@ -237,15 +244,16 @@ def dispatch_plan(topk_idx, E, ep, C, align=1):
     E_l = E // ep
     ranks = [positions(topk_idx[r * T_r:(r + 1) * T_r], E, C) for r in range(ep)]
     counts_all = np.stack([r_["counts"] for r_ in ranks])
-    layouts = recv_layout(counts_all, ep, align)
-    owner = topk_idx // E_l
+    placement = np.arange(E) if placement is None else np.asarray(placement, np.int64)
+    layouts = recv_layout(counts_all, ep, align, placement)
+    owner = placement[topk_idx] // E_l
     recv_row = np.full((T, k), -1, np.int64)
     for r in range(ep):
         pos = ranks[r]
         sl = slice(r * T_r, (r + 1) * T_r)
         e = topk_idx[sl]
-        q = e // E_l
-        el = e % E_l
+        q = placement[e] // E_l
+        el = placement[e] % E_l
         base = np.empty_like(e)
         for qq in range(ep):
             m = q == qq
