@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--a2a", action="store_true", help="dispatch/combine sweep vs NCCL")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--rebalance", action="store_true",
+                    help="expert migration before timing: observe loads, Alg. 2, move experts")
     ap.add_argument("--stepwise", action="store_true",
                     help="step-by-step C-ABI calls instead of the fused compute+all-to-all ones")
     ap.add_argument("--cpu-sample-tokens", type=int, default=0)
@@ -236,6 +238,29 @@ def run_ours(args):
         layer.backward(dy)
     torch.cuda.synchronize()
     layer.ctx.check_device_error()
+    rebal = None
+    if args.rebalance:
+        # expert migration (§VI): observe the routed load per expert, run Alg. 2,
+        # move the experts, re-warm; the migration itself is outside the timed steps
+        def rank_rows():
+            n = torch.tensor([int(layer.expert_rows.sum().item())], device=dev)
+            if dist is not None:
+                allr = [torch.zeros_like(n) for _ in range(world)]
+                dist.all_gather(allr, n)
+                return [int(v.item()) for v in allr]
+            return [int(n.item())]
+        before = rank_rows()
+        for _ in range(3):
+            layer.forward(x)
+            layer.observe_loads()
+            layer.backward(dy)
+        swaps, moved = layer.rebalance()
+        for _ in range(args.warmup):
+            layer.forward(x)
+            layer.backward(dy)
+        torch.cuda.synchronize()
+        rebal = {"swaps": swaps, "experts_moved": moved, "rank_rows_before": before,
+                 "rank_rows_after": rank_rows()}
 
     # ---- device-timed region
     # the grouped-GEMM calls (fused: their epilogues also store rows to the peers, and the
@@ -349,6 +374,7 @@ def run_ours(args):
             "T": cfg.T, "d": cfg.d, "E": cfg.E, "k": cfg.k, "f": cfg.f, "E_shared": cfg.E_s,
             "capacity_factor": cfg.cf, "zipf_s": cfg.zipf_s,
             "parallelism": f"ep{world}", "tokens_per_rank": T_r,
+            "expert_migration": rebal,
             "l2": "inputs larger than L2 (bf16 expert weights %.2f GB per GPU)" % (
                 (w_gu.numel() + w_down.numel()) * 2 / 1e9),
         },

@@ -111,6 +111,21 @@ moe_status moe_ctx_open_peers(moe_ctx* ctx, const void* handles);
 /* Bump allocation from the symmetric heap, 256-byte aligned.  Collective: every rank
  * must request the same sizes in the same order so offsets agree. */
 moe_status moe_symm_alloc(moe_ctx* ctx, size_t bytes, void** ptr);
+/* Expert placement (SURVEY.md §8(f) NEXT-2 expert migration, §VI): placement[e] =
+ * global slot of expert e (host int32 [E], a permutation of [0, E)); expert e then lives on
+ * rank placement[e] / E_l in local slot placement[e] % E_l, and every receive layout, GEMM
+ * group g (= local slot) and weight index w_gu[g], w_down[g] refers to slots.  Default: the
+ * identity (contiguous ownership).  Collective: every rank sets the same placement; it
+ * synchronises the device.  MOE_ERR_INVALID_ARG if not a permutation. */
+moe_status moe_ctx_set_placement(moe_ctx* ctx, const int32_t* placement);
+/* Alg. 2 of PAPER.md:672-706 (hill-climbing swap-based minimal rebalancing) on host data:
+ * groups = the EP owners' slots, item loads = loads[e] (e.g. the routed rows per expert from
+ * the layout record); at most max_iters (paper: T = 100) iterations, each swapping the pair
+ * of experts between the most- and least-loaded ranks that reduces their difference most
+ * (ties: lowest index).  placement (host [E]) is updated in place; n_swaps = swaps applied.
+ * Deterministic: every rank computes the same result from the same loads. */
+moe_status moe_rebalance(const int64_t* loads, int32_t E, int32_t ep, int32_t max_iters,
+                         int32_t* placement, int32_t* n_swaps);
 /* SM budgets for the calls issued after it (0 = all SMs): grouped-GEMM launches use at most
  * gemm_sms SMs and all-to-all transfer launches 2 blocks on each of comm_sms SMs, so that a
  * GEMM and a transfer issued on two streams run concurrently on disjoint SMs (used to overlap

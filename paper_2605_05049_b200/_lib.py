@@ -65,6 +65,8 @@ _SIGS = {
     "moe_symm_alloc": [P, ctypes.c_size_t, ctypes.POINTER(P)],
     "moe_ctx_get_device_error": [P],
     "moe_ctx_set_sm_limits": [P, ctypes.c_int, ctypes.c_int],
+    "moe_ctx_set_placement": [P, P],
+    "moe_rebalance": [P, I32, I32, I32, P, P],
     "moe_ctx_destroy": [P],
     "moe_router_logits": [P, P, P, P, P, P],
     "moe_router_logits_bwd": [P, P, P, P, P, P, ctypes.c_int, P],
@@ -144,6 +146,16 @@ def moe_layout_offset(shape, field):
     return _lib.moe_layout_offset(ctypes.byref(shape), int(field))
 
 
+def moe_rebalance(loads, ep, placement=None, max_iters=100):
+    """Alg. 2 in libmoe: returns (new placement list, swap count)."""
+    E = len(loads)
+    ld = (ctypes.c_int64 * E)(*[int(v) for v in loads])
+    pl = (ctypes.c_int32 * E)(*([int(v) for v in placement] if placement is not None else range(E)))
+    n = ctypes.c_int32(0)
+    _check("moe_rebalance", _lib.moe_rebalance(ld, E, int(ep), int(max_iters), pl, ctypes.byref(n)))
+    return list(pl), n.value
+
+
 def moe_status_string(code):
     return _lib.moe_status_string(int(code)).decode()
 
@@ -193,6 +205,11 @@ class Context:
         t = raw[: numel * elem].view(dtype).view(*shape)
         self._views.append(raw)
         return t
+
+    def set_placement(self, placement):
+        """placement: sequence of E ints (expert -> global slot), collective."""
+        arr = (ctypes.c_int32 * len(placement))(*[int(v) for v in placement])
+        _check("moe_ctx_set_placement", _lib.moe_ctx_set_placement(self._h, arr))
 
     def set_sm_limits(self, gemm_sms: int, comm_sms: int):
         _check("moe_ctx_set_sm_limits", _lib.moe_ctx_set_sm_limits(self._h, int(gemm_sms),

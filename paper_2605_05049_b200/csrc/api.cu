@@ -4,6 +4,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <new>
+#include <utility>
+#include <vector>
 
 #include "common.cuh"
 #include "internal.h"
@@ -37,6 +39,8 @@ struct moe_ctx {
   int32_t* d_split_rows = nullptr;// [S] token rows per split
   int n_split = 1;
   int Ep = 0;                     // E rounded up to 8
+  int32_t* d_place = nullptr;     // [E] expert -> global slot (identity unless migrated)
+  int32_t* d_expert_at = nullptr; // [E] global slot -> expert
   int gemm_sms = 0;               // SM budgets (0 = all): a GEMM and a transfer running
   int comm_sms = 0;               //   concurrently on two streams use disjoint SMs
 };
@@ -116,7 +120,45 @@ CommArgs comm_args(moe_ctx* c) {
   a.err = c->d_err;
   a.epoch = ++c->epoch;
   a.blocks = c->comm_sms > 0 ? 2 * c->comm_sms : 0;
+  a.place = c->d_place;
+  a.expert_at = c->d_expert_at;
   return a;
+}
+
+// Alg. 2 of PAPER.md:672-706 (hill-climbing swap rebalancing) on the owners' slot loads,
+// exact integer arithmetic; tie rules as oracle/migration.py (reading R16).
+int rebalance_groups(std::vector<std::vector<int64_t>>& G, std::vector<std::vector<int>>& ids,
+                     int T) {
+  const int K = static_cast<int>(G.size());
+  int c = 0;
+  for (int t = 0; t < T; ++t) {
+    std::vector<int64_t> s(K, 0);
+    for (int k = 0; k < K; ++k)
+      for (int64_t v : G[k]) s[k] += v;
+    int kp = 0, km = 0;
+    for (int k = 1; k < K; ++k) {
+      if (s[k] > s[kp]) kp = k;   // first maximum
+      if (s[k] < s[km]) km = k;   // first minimum
+    }
+    const int64_t delta = s[kp] - s[km];
+    int bi = -1, bj = -1;
+    int64_t best = 0;
+    for (size_t i = 0; i < G[kp].size(); ++i)
+      for (size_t j = 0; j < G[km].size(); ++j) {
+        int64_t d2 = (s[kp] - G[kp][i] + G[km][j]) - (s[km] - G[km][j] + G[kp][i]);
+        if (d2 < 0) d2 = -d2;
+        if (d2 < delta && delta - d2 > best) {
+          best = delta - d2;
+          bi = static_cast<int>(i);
+          bj = static_cast<int>(j);
+        }
+      }
+    if (bi < 0) break;
+    std::swap(G[kp][bi], G[km][bj]);
+    std::swap(ids[kp][bi], ids[km][bj]);
+    ++c;
+  }
+  return c;
 }
 
 moe_status set_device(moe_ctx* c) { return cuda_status(cudaSetDevice(c->device)); }
@@ -225,6 +267,16 @@ moe_status moe_ctx_create(moe_ctx** out, const moe_shape* shape, int device, siz
     if (e == cudaSuccess)
       e = cudaMalloc(&c->d_dwr_part, static_cast<size_t>(S) * 2 * c->Ep * shape->d * sizeof(float));
   }
+  {
+    std::vector<int32_t> ident(shape->E);
+    for (int i = 0; i < shape->E; ++i) ident[i] = i;
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_place, shape->E * sizeof(int32_t));
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_expert_at, shape->E * sizeof(int32_t));
+    if (e == cudaSuccess)
+      e = cudaMemcpy(c->d_place, ident.data(), shape->E * sizeof(int32_t), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+      e = cudaMemcpy(c->d_expert_at, ident.data(), shape->E * sizeof(int32_t), cudaMemcpyHostToDevice);
+  }
   if (e == cudaSuccess && EP > 1) e = cudaIpcGetMemHandle(&c->handle, c->heap);
   if (e != cudaSuccess) {
     moe_ctx_destroy(c);
@@ -269,6 +321,46 @@ moe_status moe_symm_alloc(moe_ctx* c, size_t bytes, void** ptr) {
   return MOE_OK;
 }
 
+moe_status moe_ctx_set_placement(moe_ctx* c, const int32_t* placement) {
+  MOE_REQUIRE(c && placement);
+  const int E = c->s.E;
+  std::vector<int32_t> inv(E, -1);
+  for (int e = 0; e < E; ++e) {
+    const int32_t s = placement[e];
+    if (s < 0 || s >= E || inv[s] != -1) return MOE_ERR_INVALID_ARG;  // not a permutation
+    inv[s] = e;
+  }
+  if (set_device(c) != MOE_OK) return MOE_ERR_CUDA;
+  MOE_TRY_CUDA(cudaDeviceSynchronize());  // no kernel may still read the old placement
+  MOE_TRY_CUDA(cudaMemcpy(c->d_place, placement, E * sizeof(int32_t), cudaMemcpyHostToDevice));
+  MOE_TRY_CUDA(cudaMemcpy(c->d_expert_at, inv.data(), E * sizeof(int32_t), cudaMemcpyHostToDevice));
+  return MOE_OK;
+}
+
+moe_status moe_rebalance(const int64_t* loads, int32_t E, int32_t ep, int32_t max_iters,
+                         int32_t* placement, int32_t* n_swaps) {
+  MOE_REQUIRE(loads && placement && E > 0 && ep > 0 && E % ep == 0 && max_iters >= 0);
+  const int E_l = E / ep;
+  std::vector<int32_t> expert_at(E, -1);
+  for (int e = 0; e < E; ++e) {
+    if (placement[e] < 0 || placement[e] >= E || expert_at[placement[e]] != -1)
+      return MOE_ERR_INVALID_ARG;
+    expert_at[placement[e]] = e;
+  }
+  std::vector<std::vector<int64_t>> G(ep, std::vector<int64_t>(E_l));
+  std::vector<std::vector<int>> ids(ep, std::vector<int>(E_l));
+  for (int q = 0; q < ep; ++q)
+    for (int el = 0; el < E_l; ++el) {
+      ids[q][el] = expert_at[q * E_l + el];
+      G[q][el] = loads[ids[q][el]];
+    }
+  const int c = rebalance_groups(G, ids, max_iters);
+  for (int q = 0; q < ep; ++q)
+    for (int el = 0; el < E_l; ++el) placement[ids[q][el]] = q * E_l + el;
+  if (n_swaps) *n_swaps = c;
+  return MOE_OK;
+}
+
 moe_status moe_ctx_set_sm_limits(moe_ctx* c, int gemm_sms, int comm_sms) {
   MOE_REQUIRE(c && gemm_sms >= 0 && comm_sms >= 0);
   c->gemm_sms = gemm_sms;
@@ -302,6 +394,8 @@ moe_status moe_ctx_destroy(moe_ctx* c) {
   cudaFree(c->d_wr2);
   cudaFree(c->d_dwr_part);
   cudaFree(c->d_split_rows);
+  cudaFree(c->d_place);
+  cudaFree(c->d_expert_at);
   delete c;
   return MOE_OK;
 }

@@ -128,7 +128,7 @@ __device__ void build_fwd_tables(const CommArgs& a, const int32_t* cm, FwdTables
     const int q = threadIdx.x;
     int32_t run = 0;
     for (int el = 0; el < E_l; ++el) {
-      const int e = q * E_l + el;
+      const int e = a.expert_at[q * E_l + el];   // the expert in owner q's slot el
       if (q == a.rank) t.seg[el] = run;
       t.dst[e] += run;
       run += (t.rows[e] + MOE_ALIGN_ROWS - 1) / MOE_ALIGN_ROWS * MOE_ALIGN_ROWS;
@@ -213,14 +213,15 @@ __global__ void forward_transfer_kernel(CommArgs a, int32_t* __restrict__ layout
   if (MODE == 0 && blockIdx.x == 0) {  // layout record for the later calls of this layer
     const int EP = a.ep, E = a.E, E_l = a.E_l;
     for (int i = threadIdx.x; i < EP * E; i += blockDim.x) layout[i] = cm[i];
-    for (int el = threadIdx.x; el < E_l; el += blockDim.x) layout[EP * E + el] = tb.rows[a.rank * E_l + el];
+    for (int el = threadIdx.x; el < E_l; el += blockDim.x)
+      layout[EP * E + el] = tb.rows[a.expert_at[a.rank * E_l + el]];
     for (int el = threadIdx.x; el <= E_l; el += blockDim.x) layout[EP * E + E_l + el] = tb.seg[el];
     if (threadIdx.x == 0 && tb.seg[E_l] > recv_rows_cap) set_device_error(a.err, kDevOverflow);
   }
   if (MODE == 0) {
     for (int i = threadIdx.x; i < a.E; i += blockDim.x) {
       const int q = (a.rank + 1 + i / a.E_l) % a.ep;   // rotated owner order
-      const int e = q * a.E_l + i % a.E_l;
+      const int e = a.expert_at[q * a.E_l + i % a.E_l];
       sg.count[i] = tb.off[e + 1] - tb.off[e];
       sg.src_base[i] = tb.off[e];
       sg.dst_base[i] = tb.dst[e];
@@ -245,7 +246,7 @@ __global__ void forward_transfer_kernel(CommArgs a, int32_t* __restrict__ layout
       const int64_t row = w - n_items;
       const int el = upper_bound_idx(tb.seg, E_l + 1, row);
       const int64_t within = row - tb.seg[el];
-      if (within < tb.rows[a.rank * E_l + el]) continue;  // a data row, not padding
+      if (within < tb.rows[a.expert_at[a.rank * E_l + el]]) continue;  // data row, not padding
       uint4* dst = reinterpret_cast<uint4*>(local_dst + row * d);
       for (int v = lane; v < nvec; v += 32) dst[v] = make_uint4(0u, 0u, 0u, 0u);
       continue;
@@ -267,7 +268,7 @@ __global__ void forward_transfer_kernel(CommArgs a, int32_t* __restrict__ layout
         }
         const float g = gates[t * a.k + j];
         const int e = upper_bound_idx(tb.off, E + 1, row);
-        const int q = e / E_l;
+        const int q = a.place[e] / E_l;
         const int64_t drow = tb.dst[e] + (row - tb.off[e]);
         uint4* dst = reinterpret_cast<uint4*>(a.peers.base[q] + dst_off + drow * row_bytes);
         const uint4* pdy = reinterpret_cast<const uint4*>(dy + t * d);
@@ -299,24 +300,26 @@ __global__ void reverse_transfer_kernel(CommArgs a, const int32_t* __restrict__ 
                                         const uint16_t* __restrict__ src, int64_t dst_off) {
   __shared__ int32_t s_seg[kMaxE + 1];
   __shared__ int32_t s_rows[kMaxE];
-  __shared__ int32_t s_pre[MOE_MAX_EP][kMaxE];   // rows of expert (rank*E_l+el) from sources < r
+  __shared__ int32_t s_pre[MOE_MAX_EP][kMaxE];   // rows of my slot el's expert from sources < r
   __shared__ int32_t s_soff[MOE_MAX_EP][kMaxE];  // send-layout offset of that expert on source r
   const int E = a.E, EP = a.ep, E_l = a.E_l;
   const int32_t* cm = layout;
   for (int i = threadIdx.x; i <= E_l; i += blockDim.x) s_seg[i] = layout[EP * E + E_l + i];
   for (int i = threadIdx.x; i < E_l; i += blockDim.x) s_rows[i] = layout[EP * E + i];
   for (int el = threadIdx.x; el < E_l; el += blockDim.x) {
+    const int e = a.expert_at[a.rank * E_l + el];
     int32_t run = 0;
     for (int r = 0; r < EP; ++r) {
       s_pre[r][el] = run;
-      run += cm[r * E + a.rank * E_l + el];
+      run += cm[r * E + e];
     }
   }
-  if (threadIdx.x < EP) {
+  if (threadIdx.x < EP) {  // source r's send layout: experts in global order
     const int r = threadIdx.x;
     int32_t run = 0;
-    for (int e = 0; e < a.rank * E_l + E_l; ++e) {
-      if (e >= a.rank * E_l) s_soff[r][e - a.rank * E_l] = run;
+    for (int e = 0; e < E; ++e) {
+      const int slot = a.place[e];
+      if (slot / E_l == a.rank) s_soff[r][slot % E_l] = run;
       run += cm[r * E + e];
     }
   }
@@ -326,7 +329,7 @@ __global__ void reverse_transfer_kernel(CommArgs a, const int32_t* __restrict__ 
   for (int i = threadIdx.x; i < nseg; i += blockDim.x) {
     const int r = (a.rank + 1 + i / E_l) % EP;   // rotated source order
     const int el = i % E_l;
-    sg.count[i] = cm[r * E + a.rank * E_l + el];
+    sg.count[i] = cm[r * E + a.expert_at[a.rank * E_l + el]];
     sg.src_base[i] = s_seg[el] + s_pre[r][el];
     sg.dst_base[i] = s_soff[r][el];
     sg.dst_rank[i] = r;

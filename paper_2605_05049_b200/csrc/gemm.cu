@@ -239,16 +239,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       const CommArgs& a = p.comm;
       const int32_t* cm = p.scatter_layout;
       for (int el = lane; el < a.E_l; el += 32) {
+        const int e = a.expert_at[a.rank * a.E_l + el];  // expert in my slot el
         int run = 0;
         for (int r = 0; r < a.ep; ++r) {
           s_pre[r * a.E_l + el] = run;
-          run += cm[r * a.E + a.rank * a.E_l + el];
+          run += cm[r * a.E + e];
         }
       }
-      if (lane < a.ep) {
+      if (lane < a.ep) {  // source `lane`'s send layout: experts in global order
         int run = 0;
-        for (int e = 0; e < (a.rank + 1) * a.E_l; ++e) {
-          if (e >= a.rank * a.E_l) s_soff[lane * a.E_l + e - a.rank * a.E_l] = run;
+        for (int e = 0; e < a.E; ++e) {
+          const int slot = a.place[e];
+          if (slot / a.E_l == a.rank) s_soff[lane * a.E_l + slot % a.E_l] = run;
           run += cm[lane * a.E + e];
         }
       }

@@ -101,6 +101,10 @@ struct CommArgs {
   int32_t* err;          // device error word
   uint64_t epoch;
   int blocks;            // transfer kernel blocks (0 = 2 per SM)
+  // expert placement (NEXT-2 migration): place[e] = global slot of expert e (owner =
+  // slot / E_l, local slot = slot % E_l), expert_at = its inverse; device [E] each
+  const int32_t* place;
+  const int32_t* expert_at;
 };
 enum { kSlotCounts = 0, kSlotData = 1, kNumSlots = 2 };
 

@@ -55,6 +55,8 @@ class MoELayer:
         self.fused = fused
         self.overlap = True   # shared-expert GEMMs beside dispatch / combine_bwd (E_s > 0)
         self._side = None
+        self.placement = list(range(dims.E))   # expert -> global slot (contiguous at start)
+        self.loads = None
         self.device = torch.device(f"cuda:{device}")
         self.shape = L.make_shape(dims.T_local, dims.d, dims.E, dims.k, dims.f, dims.E_shared,
                                   dims.capacity_factor, dims.ep_size, dims.ep_rank)
@@ -259,6 +261,73 @@ class MoELayer:
             L.moe_permute_bwd(c, self.dxs, self.dest_row, self.dx_router, dx_extra, self.dx)
         self._mark("B2 permute_bwd")
         return self.dx
+
+    # ------------------------------------------------------------------ expert migration
+    # SURVEY.md §8(f) NEXT-2 / PAPER.md §VI: the router "maintains token distribution"
+    # (PAPER.md:648); Alg. 2 rebalances; experts move with their weights.
+
+    def observe_loads(self):
+        """Adds this call's routed rows per expert (from the layout record, identical on every
+        rank) to the running load histogram.  One small device->host copy (a sync point)."""
+        EP, E = self.dims.ep_size, self.dims.E
+        cm = self.layout[:EP * E].view(EP, E).sum(0).to(torch.int64).cpu()
+        self.loads = cm if getattr(self, "loads", None) is None else self.loads + cm
+        return self.loads
+
+    def rebalance(self, loads=None, max_iters=100, group=None):
+        """Runs Alg. 2 (libmoe moe_rebalance) on the load histogram and migrates the experts
+        that moved.  Every rank computes the same placement from the same loads, so no extra
+        agreement step is needed.  Returns (swap count, experts moved)."""
+        loads = self.loads if loads is None else loads
+        new, swaps = L.moe_rebalance([int(v) for v in loads], self.dims.ep_size, self.placement,
+                                     max_iters)
+        moved = self.migrate(new, group)
+        self.loads = None
+        return swaps, moved
+
+    def migrate(self, new_placement, group=None):
+        """Moves expert weights to the owners given by new_placement (expert -> global slot)
+        and switches the ctx to it.  Slot tensors are re-indexed locally; experts that change
+        rank are exchanged with NCCL point-to-point (3 d f bf16 parameters each; the paper's
+        48 d f bytes per expert also count optimizer state)."""
+        E_l, EP, r = self.E_l, self.dims.ep_size, self.dims.ep_rank
+        old = list(self.placement)
+        new = [int(v) for v in new_placement]
+        new_gu = torch.empty_like(self.w_gu)
+        new_down = torch.empty_like(self.w_down)
+        ops = []
+        moved = 0
+        import torch.distributed as dist
+        for e in range(self.dims.E):
+            oq, ol = divmod(old[e], E_l)
+            nq, nl = divmod(new[e], E_l)
+            if oq != nq:
+                moved += 1
+            if nq == r and oq == r:
+                new_gu[nl].copy_(self.w_gu[ol])
+                new_down[nl].copy_(self.w_down[ol])
+            elif nq == r:
+                ops += [dist.P2POp(dist.irecv, new_gu[nl], oq, group),
+                        dist.P2POp(dist.irecv, new_down[nl], oq, group)]
+            elif oq == r:
+                ops += [dist.P2POp(dist.isend, self.w_gu[ol].contiguous(), nq, group),
+                        dist.P2POp(dist.isend, self.w_down[ol].contiguous(), nq, group)]
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        torch.cuda.synchronize(self.device)
+        self.w_gu, self.w_down = new_gu, new_down
+        self.placement = new
+        self.ctx.set_placement(new)
+        return moved
+
+    def experts_of_slots(self):
+        """Global expert id held in each local slot of this rank."""
+        inv = [0] * self.dims.E
+        for e, s in enumerate(self.placement):
+            inv[s] = e
+        r, E_l = self.dims.ep_rank, self.E_l
+        return inv[r * E_l:(r + 1) * E_l]
 
     def kernel_launches(self, fwd=True, bwd=True) -> int:
         """Number of libmoe kernels one forward / backward launches (for bench.py)."""

@@ -41,6 +41,8 @@ def main():
     ap.add_argument("--config", default="tiny", choices=list(CASES))
     ap.add_argument("--iters", type=int, default=3)
     ap.add_argument("--stepwise", action="store_true", help="unfused step-by-step calls")
+    ap.add_argument("--rebalance", action="store_true",
+                    help="observe loads, run Alg. 2 (moe_rebalance) and migrate before checking")
     args = ap.parse_args()
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -55,6 +57,12 @@ def main():
     T_r = cfg.T // ep
     x = synth.tokens(cfg).cuda()[rank * T_r:(rank + 1) * T_r].contiguous()
     dy = synth.grad_output(cfg).cuda()[rank * T_r:(rank + 1) * T_r].contiguous()
+    place = None
+    if args.rebalance:
+        layer.forward(x)
+        layer.observe_loads()
+        swaps, moved = layer.rebalance(group=None)
+        place = list(layer.placement)
     outs = []
     for _ in range(args.iters):  # epoch reuse: repeated calls must be bit-identical
         y = layer.forward(x).clone()
@@ -85,7 +93,7 @@ def main():
     dy_all = synth.grad_output(cfg)
     logits = cat("logits").numpy()
     fw, bw = oracle_layer(cfg, x_all, dy_all, logits, ep=ep)
-    res = {"config": cfg.name, "ep": ep, "device_status": [int(f[0]) for f in allflags],
+    res = {"config": cfg.name, "ep": ep, "rebalanced": place is not None, "device_status": [int(f[0]) for f in allflags],
            "repeat_bitwise": [bool(f[1]) for f in allflags]}
     checks = {}
     checks["topk"] = bool((cat("topk").numpy() == fw["topk_idx"]).all())
@@ -94,7 +102,7 @@ def main():
     E_l = cfg.E // ep
     lay_ok = True
     from oracle import moe_ref as ref
-    padded = ref.recv_layout(fw["plan"]["counts_all"], ep, align=128)
+    padded = ref.recv_layout(fw["plan"]["counts_all"], ep, align=128, placement=place)
     for r in range(ep):
         lay = g["layout"][r].cpu().numpy()
         lay_ok &= bool((lay[:ep * cfg.E].reshape(ep, cfg.E) == fw["plan"]["counts_all"]).all())
@@ -108,7 +116,7 @@ def main():
     errs["dW_r"] = rel_err(sum(f64(t) for t in g["dw_r"]).T, bw["dW_r"])
     f = cfg.f
     for e in range(cfg.E):
-        q, el = e // E_l, e % E_l
+        q, el = divmod(e if place is None else place[e], E_l)
         if fw["cache"][e] is None:
             continue
         dgu = f64(g["dw_gu"][q][el])

@@ -79,3 +79,24 @@ def test_binding_refuses_cpu_tensors(lib):
     import torch
     with pytest.raises(ValueError):
         lib._ptr(torch.zeros(4), name="x")
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_rebalance_matches_oracle_alg2(lib, seed):
+    """libmoe's C++ Alg. 2 (moe_rebalance) == the oracle's hill_climb, swap for swap."""
+    import numpy as np
+    from oracle import migration as mig
+    rng = np.random.default_rng(seed)
+    ep = int(rng.choice([2, 4, 8]))
+    E = ep * int(rng.integers(1, 9))
+    loads = rng.zipf(1.3, E).clip(max=10**6) if seed % 2 else rng.integers(0, 5000, E)
+    start = rng.permutation(E)
+    want, c_want = mig.rebalance_placement(loads, ep, start)
+    got, c_got = lib.moe_rebalance(list(loads), ep, list(start))
+    assert c_got == c_want
+    assert list(got) == list(want)
+
+
+def test_rebalance_rejects_non_permutation(lib):
+    with pytest.raises(lib.MoEError):
+        lib.moe_rebalance([1, 2, 3, 4], 2, [0, 0, 1, 2])

@@ -168,3 +168,36 @@ def test_fused_and_stepwise_paths_bit_identical(name):
         layer.close()
     for a, b in zip(*outs):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("name", ["v3_small_zipf", "dsmoe_small"])
+def test_expert_placement_is_bit_identical(name):
+    """Expert migration (NEXT-2): after migrate() to a random placement (experts in other
+    slots, weights moved with them) the layer's y, dx and every expert's weight gradient are
+    bit-identical to the contiguous placement, and the layout record equals the oracle's
+    placement-aware receive layout."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    cfg = CASES[name]
+    layer = build_layer(cfg)
+    x = synth.tokens(cfg).cuda()
+    dy = synth.grad_output(cfg).cuda()
+    y0 = layer.forward(x).clone()
+    dx0 = layer.backward(dy).clone()
+    gu0, dn0 = layer.dw_gu.clone(), layer.dw_down.clone()
+    perm = np.random.default_rng(5).permutation(cfg.E)
+    assert layer.migrate(perm) == 0          # EP = 1: slots move, nothing crosses ranks
+    y1 = layer.forward(x).clone()
+    dx1 = layer.backward(dy).clone()
+    torch.cuda.synchronize()
+    layer.ctx.check_device_error()
+    assert torch.equal(y0, y1) and torch.equal(dx0, dx1)
+    for slot, e in enumerate(layer.experts_of_slots()):
+        assert torch.equal(layer.dw_gu[slot], gu0[e]) and torch.equal(layer.dw_down[slot], dn0[e])
+    idx = layer.topk_idx.cpu().numpy()
+    plan = ref.dispatch_plan(idx, cfg.E, 1, ref.capacity(cfg.cf, cfg.k, cfg.T, cfg.E), align=128,
+                             placement=perm)
+    lay = layer.layout.cpu().numpy()
+    assert (lay[cfg.E:2 * cfg.E] == plan["layouts"][0]["expert_rows"]).all()
+    assert (lay[2 * cfg.E:] == plan["layouts"][0]["seg_base"]).all()
+    layer.close()

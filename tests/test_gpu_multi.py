@@ -48,3 +48,16 @@ def test_layer_ep_parity_stepwise(nproc, config):
     res = run_worker(nproc, config, 29700 + nproc * 10 + CONFIGS.index(config), ("--stepwise",))
     print(res)
     assert res["ok"], res
+
+
+@pytest.mark.parametrize("nproc", [2, 4])
+@pytest.mark.parametrize("config", ["v3_small_zipf", "dsmoe_small"])
+def test_layer_ep_parity_after_migration(nproc, config):
+    """Expert migration (NEXT-2): loads observed, Alg. 2 placement computed in libmoe, expert
+    weights moved between ranks; the layer still matches the oracle (layout under the new
+    placement, outputs and every expert's gradients)."""
+    if n_gpus() < nproc:
+        pytest.skip(f"needs {nproc} GPUs")
+    res = run_worker(nproc, config, 29800 + nproc * 10 + CONFIGS.index(config), ("--rebalance",))
+    print(res)
+    assert res["ok"] and res["rebalanced"], res
