@@ -176,13 +176,14 @@ def run_ours(args):
     del x_all, dy_all
     stream = torch.cuda.current_stream()
 
-    if args.breakdown:
-        for _ in range(max(args.warmup, 3)):
-            layer.forward(x)
-            layer.backward(dy)
-        torch.cuda.synchronize()
+    def breakdown():
+        """Per-phase CUDA-event times of a step (ranks barrier-aligned before every step, so
+        a phase that waits for a peer shows load imbalance, not launch skew)."""
         acc = {}
         for _ in range(args.steps):
+            if dist is not None:
+                dist.barrier()
+            torch.cuda.synchronize()
             layer.marks = []
             layer.forward(x)
             layer.backward(dy)
@@ -199,12 +200,12 @@ def run_ours(args):
         if rank == 0:
             tot = sum(v.tolist())
             print(json.dumps({"breakdown_ms_max_over_ranks": {n: round(t, 4) for n, t in zip(names, v.tolist())},
-                              "sum_ms": tot, "config": args.config, "n_gpus": world}))
+                              "sum_ms": tot, "config": args.config, "n_gpus": world,
+                              "rebalanced": bool(args.rebalance)}))
         layer.close()
         if dist is not None:
             dist.barrier()
             dist.destroy_process_group()
-        return
 
     if args.profile_steps:
         for _ in range(args.profile_steps):
@@ -261,6 +262,8 @@ def run_ours(args):
         torch.cuda.synchronize()
         rebal = {"swaps": swaps, "experts_moved": moved, "rank_rows_before": before,
                  "rank_rows_after": rank_rows()}
+    if args.breakdown:
+        return breakdown()
 
     # ---- device-timed region
     # the grouped-GEMM calls (fused: their epilogues also store rows to the peers, and the

@@ -42,6 +42,9 @@ CONFIGS = {
     "mixtral": MoEConfig("mixtral", T=8192, d=4096, E=8, k=2, f=14336, cf=1.25),
     "dsmoe": MoEConfig("dsmoe", T=16384, d=2048, E=64, k=6, f=1408, cf=1.25, E_s=2),
     "dsv3": MoEConfig("dsv3", T=32768, d=7168, E=256, k=8, f=2048, cf=0.0, zipf_s=1.0),
+    # profiling proxy (not a BASELINE config): one balanced EP=4 rank of dsv3 on one GPU --
+    # 64 experts x ~1024 rows, d=7168, f=2048
+    "dsv3_slice": MoEConfig("dsv3_slice", T=8192, d=7168, E=64, k=8, f=2048, cf=0.0),
 }
 
 SEED_X = 1
