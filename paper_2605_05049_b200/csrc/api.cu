@@ -27,7 +27,6 @@ struct moe_ctx {
   char* peer_base[MOE_MAX_EP] = {};
   bool peer_opened[MOE_MAX_EP] = {};
   bool peers_ready = false;
-  uint64_t epoch = 0;
   // device scratch
   int32_t* d_err = nullptr;
   int32_t* d_done = nullptr;
@@ -118,7 +117,7 @@ CommArgs comm_args(moe_ctx* c) {
   a.countmat_off = c->countmat_off;
   a.done = c->d_done;
   a.err = c->d_err;
-  a.epoch = ++c->epoch;
+  a.epoch_ptr = reinterpret_cast<uint64_t*>(c->d_done + 4);
   a.blocks = c->comm_sms > 0 ? 2 * c->comm_sms : 0;
   a.place = c->d_place;
   a.expert_at = c->d_expert_at;
@@ -237,8 +236,9 @@ moe_status moe_ctx_create(moe_ctx** out, const moe_shape* shape, int device, siz
   if (e == cudaSuccess) e = cudaMemset(c->heap, 0, c->internal_bytes);
   if (e == cudaSuccess) e = cudaMalloc(&c->d_err, 16);
   if (e == cudaSuccess) e = cudaMemset(c->d_err, 0, 16);
-  if (e == cudaSuccess) e = cudaMalloc(&c->d_done, 16);
-  if (e == cudaSuccess) e = cudaMemset(c->d_done, 0, 16);
+  // [0] last-block counter, [1] counts ticket, [4..5] = uint64 collective epoch
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_done, 32);
+  if (e == cudaSuccess) e = cudaMemset(c->d_done, 0, 32);
   const int64_t scratch = moe::permute_scratch_ints(shape->T_local, shape->k, shape->E);
   if (e == cudaSuccess) e = cudaMalloc(&c->d_scratch, scratch * 4);
   if (e == cudaSuccess) e = cudaMalloc(&c->d_rows_T, 16);

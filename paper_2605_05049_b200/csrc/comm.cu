@@ -40,6 +40,14 @@ __device__ __forceinline__ int upper_bound_idx(const int32_t* arr, int n, int64_
 
 __device__ void wait_all(const CommArgs& a, int slot);
 
+__device__ __forceinline__ uint64_t load_epoch(const CommArgs& a) {
+  return *reinterpret_cast<volatile const uint64_t*>(a.epoch_ptr) + 1;
+}
+// The collective is complete on this rank: publish the epoch for the next call.
+__device__ __forceinline__ void commit_epoch(const CommArgs& a) {
+  if (threadIdx.x == 0) *reinterpret_cast<volatile uint64_t*>(a.epoch_ptr) = a.epoch;
+}
+
 // Last block of a transfer kernel publishes the epoch to every destination rank and then
 // (wait_after) waits until every peer's rows have landed here, so the whole collective is a
 // single launch: the kernel completes only when this rank's receive buffer is complete.
@@ -58,7 +66,10 @@ __device__ void signal_done(const CommArgs& a, int slot, bool wait_after) {
     }
   }
   __syncthreads();
-  if (wait_after && s_last) wait_all(a, slot);
+  if (wait_after && s_last) {
+    wait_all(a, slot);
+    commit_epoch(a);   // every block read the epoch before counting itself in `done`
+  }
 }
 
 // Publishes this rank's E counts into row `rank` of every peer's count matrix (parity
@@ -203,6 +214,7 @@ __global__ void forward_transfer_kernel(CommArgs a, int32_t* __restrict__ layout
                                         float* __restrict__ dgates) {
   __shared__ FwdTables tb;
   __shared__ SegTable sg;
+  a.epoch = load_epoch(a);
   const int32_t* cm = layout;
   if (MODE == 0) {
     publish_counts(a, counts);
@@ -302,6 +314,7 @@ __global__ void reverse_transfer_kernel(CommArgs a, const int32_t* __restrict__ 
   __shared__ int32_t s_rows[kMaxE];
   __shared__ int32_t s_pre[MOE_MAX_EP][kMaxE];   // rows of my slot el's expert from sources < r
   __shared__ int32_t s_soff[MOE_MAX_EP][kMaxE];  // send-layout offset of that expert on source r
+  a.epoch = load_epoch(a);
   const int E = a.E, EP = a.ep, E_l = a.E_l;
   const int32_t* cm = layout;
   for (int i = threadIdx.x; i <= E_l; i += blockDim.x) s_seg[i] = layout[EP * E + E_l + i];
@@ -354,7 +367,12 @@ __global__ void reverse_transfer_kernel(CommArgs a, const int32_t* __restrict__ 
 }
 
 // Waits for every rank's data flag of this epoch (the GEMM-fused reverse all-to-alls).
-__global__ void wait_flags_kernel(CommArgs a, int slot) { wait_all(a, slot); }
+// The GEMM that preceded it published load_epoch(a) (the counter is not advanced until here).
+__global__ void wait_flags_kernel(CommArgs a, int slot) {
+  a.epoch = load_epoch(a);
+  wait_all(a, slot);
+  commit_epoch(a);
+}
 
 // 2 blocks of 512 threads per SM (all co-resident: blocks spin on peer flags).
 int transfer_blocks(const CommArgs& a) { return a.blocks > 0 ? a.blocks : 2 * num_sms(); }

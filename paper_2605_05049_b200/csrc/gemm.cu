@@ -603,11 +603,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     const CommArgs& a = p.comm;
     if (atomicAdd(a.done, 1) == static_cast<int>(gridDim.x) - 1) {
       a.done[0] = 0;
+      // device-resident epoch: advanced only by the wait_flags launch that follows
+      const uint64_t epoch = *reinterpret_cast<volatile const uint64_t*>(a.epoch_ptr) + 1;
       __threadfence_system();
       for (int q = 0; q < a.ep; ++q)
         st_release_sys(reinterpret_cast<uint64_t*>(a.peers.base[q] + a.flags_off) +
                            kSlotData * a.ep + a.rank,
-                       a.epoch);
+                       epoch);
     }
   }
   if (warp == 2) {

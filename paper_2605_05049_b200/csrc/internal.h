@@ -99,7 +99,11 @@ struct CommArgs {
   int64_t countmat_off;
   int32_t* done;         // local device counter for last-block detection
   int32_t* err;          // device error word
-  uint64_t epoch;
+  // Per-call epoch (identical on every rank): kernels read *epoch_ptr + 1 at their start and
+  // the LAST kernel of a collective stores it back once every peer's flag has arrived, so the
+  // counter lives on the device and the whole step can be replayed from a CUDA graph.
+  uint64_t* epoch_ptr;
+  uint64_t epoch;        // set on the device at kernel start (load_epoch)
   int blocks;            // transfer kernel blocks (0 = 2 per SM)
   // expert placement (NEXT-2 migration): place[e] = global slot of expert e (owner =
   // slot / E_l, local slot = slot % E_l), expert_at = its inverse; device [E] each

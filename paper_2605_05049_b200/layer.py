@@ -262,6 +262,32 @@ class MoELayer:
         self._mark("B2 permute_bwd")
         return self.dx
 
+    # ------------------------------------------------------------------ CUDA graph
+    def capture(self, x: torch.Tensor, dy: torch.Tensor, accumulate: bool = False, post=None):
+        """Records forward(x) + backward(dy) (+ post(), e.g. copies of self.y / self.dx) into a
+        CUDA graph and returns it; graph.replay() reruns the step on the CURRENT contents of x
+        and dy.  The collectives' epoch lives on the device (it is advanced by the kernels, not
+        baked into their arguments), so every replay is a fresh exchange.  All ranks of the EP
+        group must capture (one eager warm-up step, then the capture) and replay in lockstep.
+        Placement changes (migrate) invalidate the graph: capture again afterwards."""
+        dev = self.device
+        s = torch.cuda.Stream(device=dev)
+        s.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(s):
+            self.forward(x)
+            self.backward(dy, accumulate)
+            if post is not None:
+                post()
+        torch.cuda.current_stream(dev).wait_stream(s)
+        torch.cuda.synchronize(dev)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            self.forward(x)
+            self.backward(dy, accumulate)
+            if post is not None:
+                post()
+        return g
+
     # ------------------------------------------------------------------ expert migration
     # SURVEY.md §8(f) NEXT-2 / PAPER.md §VI: the router "maintains token distribution"
     # (PAPER.md:648); Alg. 2 rebalances; experts move with their weights.

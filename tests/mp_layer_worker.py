@@ -43,6 +43,8 @@ def main():
     ap.add_argument("--stepwise", action="store_true", help="unfused step-by-step calls")
     ap.add_argument("--rebalance", action="store_true",
                     help="observe loads, run Alg. 2 (moe_rebalance) and migrate before checking")
+    ap.add_argument("--graph", action="store_true",
+                    help="also replay the step from a CUDA graph (device-side collective epoch)")
     args = ap.parse_args()
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -68,6 +70,30 @@ def main():
         y = layer.forward(x).clone()
         dx = layer.backward(dy).clone()
         outs.append((y, dx, layer.dw_gu.clone()))
+    graph_ok = True
+    if args.graph:
+        # replays must match the eager step bit for bit (every replay is a fresh exchange), and
+        # a replay on new input contents must match the eager step on those contents
+        xg, dyg = x.clone(), dy.clone()
+        yb, dxb, dwb = torch.empty_like(x), torch.empty_like(x), torch.empty_like(layer.dw_gu)
+
+        def post():
+            yb.copy_(layer.y)
+            dxb.copy_(layer.dx)
+            dwb.copy_(layer.dw_gu)
+        graph = layer.capture(xg, dyg, post=post)
+        for _ in range(args.iters):
+            graph.replay()
+            outs.append((yb.clone(), dxb.clone(), dwb.clone()))
+        x2 = synth.tokens(cfg, seed=11).cuda()[rank * T_r:(rank + 1) * T_r].contiguous()
+        xg.copy_(x2)
+        graph.replay()
+        y2g = yb.clone()
+        y2e = layer.forward(x2).clone()
+        layer.backward(dy)
+        graph_ok = bool(torch.equal(y2g, y2e)) and not torch.equal(y2g, outs[0][0])
+        layer.forward(x)     # the gathered layer state below is the step on x
+        layer.backward(dy)
     torch.cuda.synchronize()
     st = layer.ctx.device_error()
     repeat_ok = all(torch.equal(o[0], outs[0][0]) and torch.equal(o[1], outs[0][1]) and
@@ -82,7 +108,7 @@ def main():
     if cfg.E_s:
         g["dw_gu_s"] = gather(layer.dw_gu_s)
         g["dw_down_s"] = gather(layer.dw_down_s)
-    flags = torch.tensor([st, int(repeat_ok)], device="cuda")
+    flags = torch.tensor([st, int(repeat_ok and graph_ok)], device="cuda")
     allflags = gather(flags)
     if rank != 0:
         dist.barrier()

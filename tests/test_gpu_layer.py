@@ -201,3 +201,35 @@ def test_expert_placement_is_bit_identical(name):
     assert (lay[cfg.E:2 * cfg.E] == plan["layouts"][0]["expert_rows"]).all()
     assert (lay[2 * cfg.E:] == plan["layouts"][0]["seg_base"]).all()
     layer.close()
+
+
+@pytest.mark.parametrize("name", ["mixtral_small", "dsmoe_small"])
+def test_graph_replay_bit_identical(name):
+    """MoELayer.capture: the fwd+bwd step replayed from a CUDA graph equals the eager step bit
+    for bit, and a replay after overwriting the captured input equals the eager step on it."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    cfg = CASES[name]
+    layer = build_layer(cfg)
+    x = synth.tokens(cfg).cuda()
+    dy = synth.grad_output(cfg).cuda()
+    y0 = layer.forward(x).clone()
+    dx0 = layer.backward(dy).clone()
+    gu0 = layer.dw_gu.clone()
+    xg, dyg = x.clone(), dy.clone()
+    g = layer.capture(xg, dyg)
+    for _ in range(3):
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(layer.y, y0) and torch.equal(layer.dx, dx0)
+        assert torch.equal(layer.dw_gu, gu0)
+    x2 = synth.tokens(cfg, seed=11).cuda()
+    xg.copy_(x2)
+    g.replay()
+    y2g, dx2g = layer.y.clone(), layer.dx.clone()
+    y2 = layer.forward(x2).clone()
+    dx2 = layer.backward(dy).clone()
+    torch.cuda.synchronize()
+    layer.ctx.check_device_error()
+    assert torch.equal(y2g, y2) and torch.equal(dx2g, dx2) and not torch.equal(y2, y0)
+    layer.close()

@@ -61,3 +61,19 @@ def test_layer_ep_parity_after_migration(nproc, config):
     res = run_worker(nproc, config, 29800 + nproc * 10 + CONFIGS.index(config), ("--rebalance",))
     print(res)
     assert res["ok"] and res["rebalanced"], res
+
+
+@pytest.mark.parametrize("nproc", [2, 4])
+@pytest.mark.parametrize("config", ["mixtral_small", "dsmoe_small"])
+@pytest.mark.parametrize("stepwise", [False, True])
+def test_layer_ep_graph_replay(nproc, config, stepwise):
+    """The whole fwd+bwd step captured in a CUDA graph: the collectives' epoch is advanced on
+    the device, so replays are fresh exchanges, bit-identical to eager steps, and read the
+    current contents of the captured inputs."""
+    if n_gpus() < nproc:
+        pytest.skip(f"needs {nproc} GPUs")
+    extra = ("--graph",) + (("--stepwise",) if stepwise else ())
+    res = run_worker(nproc, config, 29900 + nproc * 10 + CONFIGS.index(config) + 5 * stepwise,
+                     extra)
+    print(res)
+    assert res["ok"], res
