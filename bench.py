@@ -533,8 +533,10 @@ def run_reference(args):
 # ---------------------------------------------------------------------------- a2a sweep
 def run_a2a(args):
     """Config 5: equal-split all-to-all of a bf16 send buffer, 64 KB .. 1 GB per rank:
-    our NVSwitch peer-store dispatch (moe_dispatch, one expert per rank, no capacity)
-    vs torch.distributed.all_to_all_single (NCCL).  Reports algbw / busbw (nccl-tests)."""
+    our NVSwitch peer-store dispatch (moe_dispatch, one expert per rank, no capacity; it
+    exchanges the counts itself) vs torch.distributed.all_to_all_single (NCCL) with static
+    splits, and vs NCCL used with data-dependent splits (counts all-to-all, host read-back,
+    variable all-to-all).  Eager and CUDA-graph timings.  Reports busbw (nccl-tests)."""
     world, rank, local = dist_env()
     dist = init_dist(world, local)
     torch.cuda.set_device(local)
@@ -566,7 +568,11 @@ def run_a2a(args):
             dist.all_to_all_single(ref_out, xs)
         torch.cuda.synchronize()
         ok = torch.equal(xr[:T], ref_out)
-        it = 20
+        # enough calls that the ranks' launch skew after the barrier is amortised
+        it = 200 if size <= (16 << 20) else 20
+        for _ in range(it):   # clocks up, caches warm
+            L.moe_dispatch(ctx, xs, counts, layout, xr)
+            dist.all_to_all_single(ref_out, xs)
         dist.barrier(); torch.cuda.synchronize()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
@@ -580,15 +586,66 @@ def run_a2a(args):
             dist.all_to_all_single(ref_out, xs)
         e.record(); torch.cuda.synchronize()
         t_nccl = s.elapsed_time(e) / it
-        v = torch.tensor([t_ours, t_nccl], dtype=torch.float64, device="cuda")
+        # the same `it` calls replayed from CUDA graphs: device time without the host
+        # launch path (small messages are launch-bound when issued eagerly)
+        def graph_of(fn):
+            s2 = torch.cuda.Stream()
+            s2.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s2):
+                fn()
+            torch.cuda.current_stream().wait_stream(s2)
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s2):
+                for _ in range(it):
+                    fn()
+            return g
+        tg = []
+        for fn in (lambda: L.moe_dispatch(ctx, xs, counts, layout, xr),
+                   lambda: dist.all_to_all_single(ref_out, xs)):
+            try:
+                g = graph_of(fn)
+                g.replay()
+                dist.barrier(); torch.cuda.synchronize()
+                s.record()
+                g.replay()
+                e.record(); torch.cuda.synchronize()
+                tg.append(s.elapsed_time(e) / it)
+                del g
+            except Exception:   # capture unsupported: report eager only
+                tg.append(float("nan"))
+        ok = ok and torch.equal(xr[:T], ref_out)
+        # NCCL as an MoE dispatch with data-dependent sizes uses it: all-to-all of the counts,
+        # the splits read back on the host, then the variable-size all-to-all
+        send_counts = counts.clone()
+        recv_counts = torch.empty_like(send_counts)
+
+        def nccl_dynamic():
+            dist.all_to_all_single(recv_counts, send_counts)
+            out_splits = recv_counts.tolist()
+            dist.all_to_all_single(ref_out, xs, output_split_sizes=out_splits,
+                                   input_split_sizes=[T // world] * world)
+        nccl_dynamic()
+        dist.barrier(); torch.cuda.synchronize()
+        s.record()
+        for _ in range(it):
+            nccl_dynamic()
+        e.record(); torch.cuda.synchronize()
+        t_dyn = s.elapsed_time(e) / it
+        ok = ok and torch.equal(xr[:T], ref_out)
+        v = torch.tensor([t_ours, t_nccl, *tg, t_dyn], dtype=torch.float64, device="cuda")
         dist.all_reduce(v, op=dist.ReduceOp.MAX)
-        t_ours, t_nccl = v.tolist()
+        t_ours, t_nccl, tg_ours, tg_nccl, t_dyn = v.tolist()
         nbytes = T * d_eff * 2
         bus = (world - 1) / world
         results.append({"bytes_per_rank": nbytes, "bitwise_equal_nccl": bool(ok),
                         "ours_ms": t_ours, "nccl_ms": t_nccl,
+                        "ours_graph_ms": tg_ours, "nccl_graph_ms": tg_nccl,
+                        "nccl_dynamic_ms": t_dyn,
                         "ours_busbw_GBs": nbytes / (t_ours * 1e-3) / 1e9 * bus,
-                        "nccl_busbw_GBs": nbytes / (t_nccl * 1e-3) / 1e9 * bus})
+                        "nccl_busbw_GBs": nbytes / (t_nccl * 1e-3) / 1e9 * bus,
+                        "ours_graph_busbw_GBs": nbytes / (tg_ours * 1e-3) / 1e9 * bus,
+                        "nccl_graph_busbw_GBs": nbytes / (tg_nccl * 1e-3) / 1e9 * bus})
         ctx.close()
     if rank == 0:
         print(json.dumps({"metric": "dispatch all-to-all busbw vs NCCL", "n_gpus": world,

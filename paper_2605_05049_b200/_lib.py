@@ -13,7 +13,8 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmoe.so")
+# MOE_LIB: an instrumented in-tree build of the same sources (tools/trace_a2a.py)
+LIB_PATH = os.environ.get("MOE_LIB") or os.path.join(_HERE, "libmoe.so")
 
 MOE_ALIGN_ROWS = 128
 MOE_IPC_HANDLE_BYTES = 64

@@ -21,6 +21,18 @@
 namespace moe {
 namespace {
 
+// Latency tracing (build with -DMOE_TRACE only): globaltimer stamps of the phases of the
+// last dispatch call, read with moe_debug_trace (not part of the C ABI).
+#ifdef MOE_TRACE
+__device__ unsigned long long g_trace[64][8];   // [epoch % 64][stamp]
+#define MOE_TRACE_AT(i, cond)                                                        \
+  do {                                                                               \
+    if ((cond) && threadIdx.x == 0) g_trace[a.epoch % 64][i] = globaltimer_ns();     \
+  } while (0)
+#else
+#define MOE_TRACE_AT(i, cond) do {} while (0)
+#endif
+
 constexpr uint64_t kTimeoutNs = 10ull * 1000 * 1000 * 1000;
 constexpr int kMaxE = 256;  // validated by the C-ABI (E <= 256)
 
@@ -53,21 +65,26 @@ __device__ __forceinline__ void commit_epoch(const CommArgs& a) {
 // single launch: the kernel completes only when this rank's receive buffer is complete.
 __device__ void signal_done(const CommArgs& a, int slot, bool wait_after) {
   __shared__ int s_last;
-  __threadfence_system();
+  // bar.sync orders the block's stores before thread 0's fence.sc.sys, which is cumulative
+  // over them (the grid-barrier pattern): one system fence per block, not per thread
   __syncthreads();
   if (threadIdx.x == 0) {
+    __threadfence_system();
     const int prev = atomicAdd(a.done, 1);
     s_last = (prev == static_cast<int>(gridDim.x) - 1);
+    MOE_TRACE_AT(4, s_last);
     if (s_last) {
       a.done[0] = 0;
       a.done[1] = 0;  // publish_counts ticket (every block has passed it)
-      __threadfence_system();
-      for (int q = 0; q < a.ep; ++q) st_release_sys(peer_flag(a, q, slot, a.rank), a.epoch);
     }
   }
   __syncthreads();
+  // the last block's lanes 0..EP-1 release the epoch to every destination rank at once
+  // (one st.release per lane, issued as one warp instruction)
+  if (s_last && threadIdx.x < a.ep) st_release_sys(peer_flag(a, threadIdx.x, slot, a.rank), a.epoch);
   if (wait_after && s_last) {
     wait_all(a, slot);
+    MOE_TRACE_AT(5, true);
     commit_epoch(a);   // every block read the epoch before counting itself in `done`
   }
 }
@@ -88,9 +105,10 @@ __device__ void publish_counts(const CommArgs& a, const int32_t* counts) {
                    (parity * EP + a.rank) * E + e;
     *dst = counts[e];
   }
-  __threadfence_system();
+  // bar.sync orders the block's count stores before the lanes' st.release.sys (cumulative)
   __syncthreads();
   if (threadIdx.x < EP) st_release_sys(peer_flag(a, threadIdx.x, kSlotCounts, a.rank), a.epoch);
+  MOE_TRACE_AT(6, true);
 }
 
 __device__ void wait_all(const CommArgs& a, int slot) {
@@ -121,6 +139,27 @@ struct FwdTables {
   int32_t rows[kMaxE];
 };
 
+// Exclusive scan by ONE warp of n values val(i) (i ascending); out(i, prefix) is called for
+// every i < n with its exclusive prefix.  Returns the total (in every lane).
+template <typename V, typename O>
+__device__ __forceinline__ int32_t warp_scan(int n, V val, O out) {
+  const int lane = threadIdx.x & 31;
+  int32_t carry = 0;
+  for (int base = 0; base < n; base += 32) {
+    const int i = base + lane;
+    const int32_t c = i < n ? val(i) : 0;
+    int32_t x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (i < n) out(i, carry + x - c);
+    carry += __shfl_sync(0xffffffffu, x, 31);
+  }
+  return carry;
+}
+
 __device__ void build_fwd_tables(const CommArgs& a, const int32_t* cm, FwdTables& t) {
   const int E = a.E, EP = a.ep, E_l = a.E_l;
   // per-expert rows over all sources, and rows from sources before me
@@ -135,32 +174,37 @@ __device__ void build_fwd_tables(const CommArgs& a, const int32_t* cm, FwdTables
     t.dst[e] = before;
   }
   __syncthreads();
-  if (threadIdx.x < EP) {  // owner q: aligned segment prefix over its experts
-    const int q = threadIdx.x;
-    int32_t run = 0;
-    for (int el = 0; el < E_l; ++el) {
-      const int e = a.expert_at[q * E_l + el];   // the expert in owner q's slot el
-      if (q == a.rank) t.seg[el] = run;
-      t.dst[e] += run;
-      run += (t.rows[e] + MOE_ALIGN_ROWS - 1) / MOE_ALIGN_ROWS * MOE_ALIGN_ROWS;
-    }
-    if (q == a.rank) t.seg[E_l] = run;
-  }
-  if (threadIdx.x == 32) {
-    int32_t run = 0;
-    for (int e = 0; e < E; ++e) {
-      t.off[e] = run;
-      run += cm[a.rank * E + e];
-    }
-    t.off[E] = run;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp < EP) {  // warp q: owner q's aligned segment prefix over its slots
+    const int q = warp;
+    const int32_t total = warp_scan(
+        E_l,
+        [&](int el) {
+          const int32_t r = t.rows[a.expert_at[q * E_l + el]];
+          return (r + MOE_ALIGN_ROWS - 1) / MOE_ALIGN_ROWS * MOE_ALIGN_ROWS;
+        },
+        [&](int el, int32_t pre) {
+          if (q == a.rank) t.seg[el] = pre;
+          t.dst[a.expert_at[q * E_l + el]] += pre;
+        });
+    if (q == a.rank && lane == 0) t.seg[E_l] = total;
+  } else if (warp == EP) {  // send layout: exclusive scan of my counts
+    const int32_t total = warp_scan(
+        E, [&](int e) { return cm[a.rank * E + e]; }, [&](int e, int32_t pre) { t.off[e] = pre; });
+    if (lane == 0) t.off[E] = total;
   }
   __syncthreads();
 }
 
-__device__ __forceinline__ void copy_row(uint4* __restrict__ dst, const uint4* __restrict__ src,
-                                         int nvec, int lane) {
-#pragma unroll 4
-  for (int v = lane; v < nvec; v += 32) st_v4(dst + v, ld_nc_v4(src + v));
+// A row of nvec 16-byte vectors is copied in parts of kPartVec vectors (2 KB, 4 per lane).
+constexpr int kPartVec = 128;
+__device__ __forceinline__ int row_parts(int nvec) { return (nvec + kPartVec - 1) / kPartVec; }
+__device__ __forceinline__ void copy_part(uint4* __restrict__ dst, const uint4* __restrict__ src,
+                                          int nvec, int part, int lane) {
+  const int v0 = part * kPartVec;
+  const int v1 = min(nvec, v0 + kPartVec);
+#pragma unroll
+  for (int v = v0 + lane; v < v1; v += 32) st_v4(dst + v, ld_nc_v4(src + v));
 }
 
 // Copy segments in transfer order.  Segment i moves `count` consecutive rows from
@@ -178,21 +222,9 @@ struct SegTable {
 // Exclusive scan of t.count[0..n) into t.prefix[0..n] (warp 0; n <= kMaxE).
 __device__ void scan_segments(SegTable& t, int n) {
   if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    int carry = 0;
-    for (int base = 0; base < n; base += 32) {
-      const int i = base + lane;
-      const int c = i < n ? t.count[i] : 0;
-      int x = c;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-      }
-      if (i < n) t.prefix[i] = carry + x - c;
-      carry += __shfl_sync(0xffffffffu, x, 31);
-    }
-    if (lane == 0) t.prefix[n] = carry;
+    const int32_t total = warp_scan(
+        n, [&](int i) { return t.count[i]; }, [&](int i, int32_t pre) { t.prefix[i] = pre; });
+    if (threadIdx.x == 0) t.prefix[n] = total;
   }
   __syncthreads();
 }
@@ -216,9 +248,11 @@ __global__ void forward_transfer_kernel(CommArgs a, int32_t* __restrict__ layout
   __shared__ SegTable sg;
   a.epoch = load_epoch(a);
   const int32_t* cm = layout;
+  MOE_TRACE_AT(0, MODE == 0 && blockIdx.x == 0);
   if (MODE == 0) {
     publish_counts(a, counts);
     wait_all(a, kSlotCounts);
+    MOE_TRACE_AT(1, blockIdx.x == 0);
     cm = a.countmat + static_cast<int>(a.epoch & 1) * a.ep * a.E;
   }
   build_fwd_tables(a, cm, tb);
@@ -241,6 +275,7 @@ __global__ void forward_transfer_kernel(CommArgs a, int32_t* __restrict__ layout
     }
     __syncthreads();
     scan_segments(sg, a.E);
+    MOE_TRACE_AT(2, blockIdx.x == 0);
   }
   const int lane = threadIdx.x & 31;
   const int64_t gwarp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -251,7 +286,10 @@ __global__ void forward_transfer_kernel(CommArgs a, int32_t* __restrict__ layout
   const int E = a.E, E_l = a.E_l;
   // padding rows of the local receive buffer (zeroed every call)
   const int64_t n_pad_rows = tb.seg[E_l];
-  const int64_t n_items = (MODE == 0) ? tb.off[E] : a.T;
+  // mode 0 work item = one 2 KB part of a row (a few rows still spread over many warps);
+  // mode 1 = one token (its k rows and their dot products)
+  const int parts = (MODE == 0) ? row_parts(nvec) : 1;
+  const int64_t n_items = (MODE == 0) ? static_cast<int64_t>(tb.off[E]) * parts : a.T;
 
   for (int64_t w = gwarp; w < n_items + n_pad_rows; w += nwarps) {
     if (w >= n_items) {
@@ -264,12 +302,14 @@ __global__ void forward_transfer_kernel(CommArgs a, int32_t* __restrict__ layout
       continue;
     }
     if (MODE == 0) {
-      const int i = upper_bound_idx(sg.prefix, E + 1, w);
-      const int64_t within = w - sg.prefix[i];
+      const int64_t r = w / parts;
+      const int part = static_cast<int>(w - r * parts);
+      const int i = upper_bound_idx(sg.prefix, E + 1, r);
+      const int64_t within = r - sg.prefix[i];
       const int64_t row = sg.src_base[i] + within;
       const int64_t drow = sg.dst_base[i] + within;
       uint4* dst = reinterpret_cast<uint4*>(a.peers.base[sg.dst_rank[i]] + dst_off + drow * row_bytes);
-      copy_row(dst, reinterpret_cast<const uint4*>(src + row * d), nvec, lane);
+      copy_part(dst, reinterpret_cast<const uint4*>(src + row * d), nvec, part, lane);
     } else {
       const int64_t t = w;
       for (int j = 0; j < a.k; ++j) {
@@ -304,6 +344,7 @@ __global__ void forward_transfer_kernel(CommArgs a, int32_t* __restrict__ layout
       }
     }
   }
+  MOE_TRACE_AT(3, MODE == 0 && blockIdx.x == 0);
   signal_done(a, kSlotData, /*wait_after=*/true);
 }
 
@@ -311,14 +352,12 @@ __global__ void forward_transfer_kernel(CommArgs a, int32_t* __restrict__ layout
 __global__ void reverse_transfer_kernel(CommArgs a, const int32_t* __restrict__ layout,
                                         const uint16_t* __restrict__ src, int64_t dst_off) {
   __shared__ int32_t s_seg[kMaxE + 1];
-  __shared__ int32_t s_rows[kMaxE];
   __shared__ int32_t s_pre[MOE_MAX_EP][kMaxE];   // rows of my slot el's expert from sources < r
   __shared__ int32_t s_soff[MOE_MAX_EP][kMaxE];  // send-layout offset of that expert on source r
   a.epoch = load_epoch(a);
   const int E = a.E, EP = a.ep, E_l = a.E_l;
   const int32_t* cm = layout;
   for (int i = threadIdx.x; i <= E_l; i += blockDim.x) s_seg[i] = layout[EP * E + E_l + i];
-  for (int i = threadIdx.x; i < E_l; i += blockDim.x) s_rows[i] = layout[EP * E + i];
   for (int el = threadIdx.x; el < E_l; el += blockDim.x) {
     const int e = a.expert_at[a.rank * E_l + el];
     int32_t run = 0;
@@ -327,14 +366,14 @@ __global__ void reverse_transfer_kernel(CommArgs a, const int32_t* __restrict__ 
       run += cm[r * E + e];
     }
   }
-  if (threadIdx.x < EP) {  // source r's send layout: experts in global order
-    const int r = threadIdx.x;
-    int32_t run = 0;
-    for (int e = 0; e < E; ++e) {
-      const int slot = a.place[e];
-      if (slot / E_l == a.rank) s_soff[r][slot % E_l] = run;
-      run += cm[r * E + e];
-    }
+  if ((threadIdx.x >> 5) < EP) {  // warp r: source r's send layout, experts in global order
+    const int r = threadIdx.x >> 5;
+    warp_scan(
+        E, [&](int e) { return cm[r * E + e]; },
+        [&](int e, int32_t pre) {
+          const int slot = a.place[e];
+          if (slot / E_l == a.rank) s_soff[r][slot % E_l] = pre;
+        });
   }
   __syncthreads();
   __shared__ SegTable sg;
@@ -354,14 +393,17 @@ __global__ void reverse_transfer_kernel(CommArgs a, const int32_t* __restrict__ 
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   const int d = a.d, nvec = d / 8;
   const int64_t row_bytes = static_cast<int64_t>(d) * 2;
-  const int64_t n_rows = sg.prefix[nseg];
-  for (int64_t v = gwarp; v < n_rows; v += nwarps) {
+  const int parts = row_parts(nvec);
+  const int64_t n_items = static_cast<int64_t>(sg.prefix[nseg]) * parts;
+  for (int64_t w = gwarp; w < n_items; w += nwarps) {
+    const int64_t v = w / parts;
+    const int part = static_cast<int>(w - v * parts);
     const int i = upper_bound_idx(sg.prefix, nseg + 1, v);
     const int64_t within = v - sg.prefix[i];
     const int64_t row = sg.src_base[i] + within;
     const int64_t srow = sg.dst_base[i] + within;
     uint4* dst = reinterpret_cast<uint4*>(a.peers.base[sg.dst_rank[i]] + dst_off + srow * row_bytes);
-    copy_row(dst, reinterpret_cast<const uint4*>(src + row * d), nvec, lane);
+    copy_part(dst, reinterpret_cast<const uint4*>(src + row * d), nvec, part, lane);
   }
   signal_done(a, kSlotData, /*wait_after=*/true);
 }
@@ -374,10 +416,24 @@ __global__ void wait_flags_kernel(CommArgs a, int slot) {
   commit_epoch(a);
 }
 
-// 2 blocks of 512 threads per SM (all co-resident: blocks spin on peer flags).
-int transfer_blocks(const CommArgs& a) { return a.blocks > 0 ? a.blocks : 2 * num_sms(); }
+// Up to 2 blocks of 512 threads per SM (all co-resident: blocks spin on peer flags), and no
+// more than one block per 32 work items (2 KB row parts): small messages are latency-bound,
+// and every extra block adds to the launch and to the last-block count.
+int transfer_blocks(const CommArgs& a, int64_t rows) {
+  int64_t b = a.blocks > 0 ? a.blocks : 2 * num_sms();
+  const int64_t parts = (a.d / 8 + 127) / 128;
+  const int64_t need = (rows * parts + 31) / 32;
+  if (need < b) b = need;
+  return static_cast<int>(b < 1 ? 1 : b);
+}
 
 }  // namespace
+
+#ifdef MOE_TRACE
+extern "C" int moe_debug_trace(unsigned long long* out) {   // [64][8]
+  return static_cast<int>(cudaMemcpyFromSymbol(out, g_trace, sizeof(g_trace)));
+}
+#endif
 
 cudaError_t launch_wait_flags(const CommArgs& a, int slot, cudaStream_t s) {
   wait_flags_kernel<<<1, 32, 0, s>>>(a, slot);
@@ -387,7 +443,7 @@ cudaError_t launch_wait_flags(const CommArgs& a, int slot, cudaStream_t s) {
 cudaError_t launch_dispatch(const CommArgs& a, const int32_t* counts, int32_t* layout,
                             int64_t recv_rows_cap, const uint16_t* src, int64_t dst_off,
                             uint16_t* local_dst, cudaStream_t s) {
-  forward_transfer_kernel<0><<<transfer_blocks(a), 512, 0, s>>>(
+  forward_transfer_kernel<0><<<transfer_blocks(a, a.T * a.k), 512, 0, s>>>(
       a, layout, counts, recv_rows_cap, src, dst_off, local_dst, nullptr, nullptr, nullptr, nullptr,
       nullptr);
   return cudaGetLastError();
@@ -397,14 +453,16 @@ cudaError_t launch_combine_bwd_transfer(const CommArgs& a, int32_t* layout, int6
                                         uint16_t* local_dst, const int32_t* dest_row,
                                         const float* gates, const uint16_t* dy, const uint16_t* ys,
                                         float* dgates, cudaStream_t s) {
-  forward_transfer_kernel<1><<<transfer_blocks(a), 512, 0, s>>>(
+  forward_transfer_kernel<1><<<transfer_blocks(a, a.T * a.k), 512, 0, s>>>(
       a, layout, nullptr, 0, nullptr, dst_off, local_dst, dest_row, gates, dy, ys, dgates);
   return cudaGetLastError();
 }
 
 cudaError_t launch_reverse_transfer(const CommArgs& a, const int32_t* layout, const uint16_t* src,
                                     int64_t dst_off, cudaStream_t s) {
-  reverse_transfer_kernel<<<transfer_blocks(a), 512, 0, s>>>(a, layout, src, dst_off);
+  // receive rows <= EP * T * k
+  reverse_transfer_kernel<<<transfer_blocks(a, a.T * a.k * a.ep), 512, 0, s>>>(a, layout, src,
+                                                                              dst_off);
   return cudaGetLastError();
 }
 

@@ -496,7 +496,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int q = 0; q < 32; ++q) gw[q] = uw[q] = 0u;
           }
           tmem_ld_wait();
-#pragma unroll
           uint32_t wu[32];  // dU words; w holds the dG words
 #pragma unroll
           for (int q = 0; q < 32; ++q) {

@@ -27,6 +27,8 @@ CASES = {
     "v3_small_zipf": synth.MoEConfig("v3_small_zipf", T=2048, d=512, E=256, k=8, f=256, cf=0.0,
                                      zipf_s=1.0),
     "drops": synth.MoEConfig("drops", T=1024, d=128, E=8, k=2, f=256, cf=0.5),
+    # one expert per rank at nproc 4 (the Mixtral EP=8 layout, E_l = 1, on 4 GPUs)
+    "el1": synth.MoEConfig("el1", T=2048, d=512, E=4, k=2, f=1024, cf=1.25),
 }
 
 

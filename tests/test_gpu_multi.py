@@ -77,3 +77,13 @@ def test_layer_ep_graph_replay(nproc, config, stepwise):
                      extra)
     print(res)
     assert res["ok"], res
+
+
+@pytest.mark.parametrize("extra", [(), ("--stepwise",), ("--graph",)])
+def test_layer_one_expert_per_rank(extra):
+    """E_l = 1 (Mixtral's EP=8 layout) at EP=4: E=4 experts, one per rank."""
+    if n_gpus() < 4:
+        pytest.skip("needs 4 GPUs")
+    res = run_worker(4, "el1", 29990 + len(extra) + (3 if "--graph" in extra else 0), extra)
+    print(res)
+    assert res["ok"], res
