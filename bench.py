@@ -50,9 +50,15 @@ def parse():
     ap.add_argument("--cpu-sample-tokens", type=int, default=0)
     ap.add_argument("--breakdown", action="store_true",
                     help="per-phase CUDA-event breakdown of a step (max over ranks), no bench line")
+    ap.add_argument("--chunks", type=int, default=None,
+                    help="NEXT-1 chunked a2a || GEMM overlap: owner-slot ranges (1 = off)")
+    ap.add_argument("--comm-sms", type=int, default=None,
+                    help="SMs given to an all-to-all running beside a GEMM (MoELayer.comm_sms)")
     ap.add_argument("--graph", action="store_true",
                     help="also time the step replayed from a CUDA graph (MoELayer.capture); "
                          "the headline uses the faster of eager / graph")
+    ap.add_argument("--gemm-compare", action="store_true",
+                    help="expert FFN GEMMs: libmoe vs cuBLAS (torch) on one GPU, no bench line")
     ap.add_argument("--profile-steps", type=int, default=0,
                     help="run only this many steps without timing (for ncu)")
     return ap.parse_args()
@@ -166,6 +172,10 @@ def run_ours(args):
     T_r = cfg.T // ep
     dims = LayerDims(T_r, cfg.d, cfg.E, cfg.k, cfg.f, cfg.E_s, cfg.cf, ep, rank)
     layer = MoELayer(dims, device=local, fused=not args.stepwise)
+    if args.chunks is not None:
+        layer.chunks = args.chunks
+    if args.comm_sms is not None:
+        layer.comm_sms = args.comm_sms
     E_l = cfg.E // ep
     dev = torch.device(f"cuda:{local}")
     w_gu, w_down = synth.expert_weights(cfg, range(rank * E_l, (rank + 1) * E_l), device=dev)
@@ -272,7 +282,8 @@ def run_ours(args):
     # the grouped-GEMM calls (fused: their epilogues also store rows to the peers, and the
     # calls end with the flag wait / unpermute -- so the measured region is conservative)
     hooked = ["moe_expert_ffn", "moe_expert_ffn_bwd", "moe_expert_ffn_combine",
-              "moe_expert_ffn_bwd_dispatch"]
+              "moe_expert_ffn_bwd_dispatch", "moe_expert_ffn_up", "moe_expert_ffn_down_combine",
+              "moe_expert_ffn_bwd_dh", "moe_expert_ffn_bwd_dx_dispatch"]
     originals = {n: getattr(layer_mod.L, n) for n in hooked}
     for n in hooked:
         setattr(layer_mod.L, n, timed(originals[n]))
@@ -407,6 +418,7 @@ def run_ours(args):
             "capacity_factor": cfg.cf, "zipf_s": cfg.zipf_s,
             "parallelism": f"ep{world}", "tokens_per_rank": T_r,
             "expert_migration": rebal,
+            "a2a_gemm_chunks": len(layer._ranges() or [None]),
             "cuda_graph": use_graph,
             "eager_ms_per_step": eager_ms,
             "graph_ms_per_step": graph_ms if args.graph else None,
@@ -654,10 +666,97 @@ def run_a2a(args):
     dist.destroy_process_group()
 
 
+def run_gemm_compare(args):
+    """Expert FFN fwd+bwd GEMMs of one rank (balanced rows, EP = 1) through libmoe vs the same
+    contractions issued to cuBLAS via torch (per-expert matmuls + elementwise SwiGLU), in the
+    same process and power state; plus one large square cuBLAS GEMM as the box's dense-bf16
+    reference.  Context for the roofline fraction, not a bench line."""
+    torch.cuda.set_device(0)
+    from paper_2605_05049_b200 import _lib as L
+    cfg = synth.CONFIGS[args.config]
+    E, d, f = cfg.E, cfg.d, cfg.f
+    rows = cfg.T * cfg.k // E
+    R = rows * E
+    dev = torch.device("cuda:0")
+    shape = L.make_shape(cfg.T, d, E, cfg.k, f, 0, 0.0, 1, 0)
+    ctx = L.Context(shape, 0, 4096)
+    g = torch.Generator(device=dev)
+    g.manual_seed(0)
+    bf = torch.bfloat16
+    xr = torch.randn((R, d), device=dev, generator=g).to(bf)
+    dout = torch.randn((R, d), device=dev, generator=g).to(bf)
+    w_gu, w_down = synth.expert_weights(cfg, range(E), device=dev)
+    group_rows = torch.full((E,), rows, dtype=torch.int32, device=dev)
+    g_u_h = torch.empty((R, 3 * f), dtype=bf, device=dev)
+    out = torch.empty((R, d), dtype=bf, device=dev)
+    dgu = torch.empty((R, 2 * f), dtype=bf, device=dev)
+    dxr = torch.empty((R, d), dtype=bf, device=dev)
+    dw_gu = torch.empty((E, 2 * f, d), dtype=torch.float32, device=dev)
+    dw_down = torch.empty((E, d, f), dtype=torch.float32, device=dev)
+
+    def ours():
+        L.moe_expert_ffn(ctx, xr, group_rows, E, R, f, w_gu, w_down, g_u_h, out)
+        L.moe_expert_ffn_bwd(ctx, xr, group_rows, E, R, f, w_gu, w_down, g_u_h, dout, dgu, dxr,
+                             dw_gu, dw_down)
+
+    # cuBLAS gets the six contractions only (its SwiGLU / dSwiGLU inputs precomputed): the
+    # libmoe side also runs its fused epilogues, so the comparison favours cuBLAS
+    H_all = g_u_h[:, 2 * f:].contiguous()
+    dGU_all = torch.randn((R, 2 * f), device=dev, generator=g).to(bf)
+    o_buf = torch.empty((rows, d), dtype=bf, device=dev)
+    gu_buf = torch.empty((rows, 2 * f), dtype=bf, device=dev)
+    dh_buf = torch.empty((rows, f), dtype=bf, device=dev)
+
+    def cublas():
+        for e in range(E):
+            X = xr[e * rows:(e + 1) * rows]
+            dO = dout[e * rows:(e + 1) * rows]
+            H = H_all[e * rows:(e + 1) * rows]
+            dGU = dGU_all[e * rows:(e + 1) * rows]
+            torch.mm(X, w_gu[e].t(), out=gu_buf)
+            torch.mm(H, w_down[e].t(), out=o_buf)
+            torch.mm(dO, w_down[e], out=dh_buf)
+            torch.mm(dGU, w_gu[e], out=o_buf)
+            torch.mm(dO.t(), H, out_dtype=torch.float32)
+            torch.mm(dGU.t(), X, out_dtype=torch.float32)
+
+    def timeit(fn, n):
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(n):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / n
+
+    flops = 18.0 * R * d * f
+    res = {"config": cfg.name, "rows_per_expert": rows, "experts": E, "flops": flops}
+    n = 8192
+    A = torch.randn((n, n), device=dev, generator=g).to(bf)
+    B = torch.randn((n, n), device=dev, generator=g).to(bf)
+    clocks = ClockSampler(0)
+    t = {}
+    for name, fn, it in (("ours", ours, args.steps), ("cublas", cublas, args.steps),
+                         ("square", lambda: torch.mm(A, B), 200)):
+        clocks.start()
+        t[name] = timeit(fn, it)
+        res[f"clocks_{name}"] = clocks.stop()
+    t_ours, t_cub, t_sq = t["ours"], t["cublas"], t["square"]
+    res.update(ours_ms=t_ours, cublas_ms=t_cub, ours_tflops=flops / t_ours / 1e9,
+               cublas_tflops=flops / t_cub / 1e9, cublas_square8192_tflops=2 * n ** 3 / t_sq / 1e9)
+    print(json.dumps(res), flush=True)
+    ctx.close()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.gemm_compare:
+        run_gemm_compare(args)
     elif args.a2a:
         run_a2a(args)
     else:

@@ -261,6 +261,62 @@ moe_status moe_expert_ffn_bwd_dispatch(moe_ctx* ctx, const moe_bf16* xr, const i
                                        moe_bf16* dxs, float* dw_gu, float* dw_down, int accumulate,
                                        moe_stream stream);
 
+/* ---------------- chunked overlap of the all-to-alls with the expert GEMMs (NEXT-1:
+ * "chunked dispatch -> GEMM") ----------------
+ * The owner slots [0, E_l) are cut into ranges.  The transfer of range c+1 runs on a second
+ * stream (moe_ctx_set_sm_limits gives it comm_sms SMs) while the first expert GEMM of range c
+ * runs on this one; no kernel ever waits for a kernel of the other stream, so the two
+ * launches cannot deadlock whatever the SM scheduler does.  Every range call is a
+ * collective (all ranks, same ranges, same order).  Results are bit-identical to the
+ * unchunked calls: the ranges partition the rows, and every output row is computed by the
+ * same kernel code with the same operands.
+ *
+ *   forward : moe_dispatch_range(r0) ; [moe_dispatch_range(r1) || moe_expert_ffn_up(r0)] ;
+ *             ... ; moe_expert_ffn_up(r_last) ; moe_expert_ffn_down_combine
+ *   backward: moe_combine_bwd_range(r0) ; [moe_combine_bwd_range(r1) || moe_expert_ffn_bwd_dh(r0)] ;
+ *             ... ; moe_expert_ffn_bwd_dh(r_last) ; moe_expert_ffn_bwd_dx_dispatch
+ */
+
+/* Collective.  moe_dispatch for the rows bound to owner slots [slot_begin, slot_end) only
+ * (padding rows of those slots zeroed).  The range with slot_begin == 0 must come first in
+ * a step: it exchanges the counts and writes the whole layout record; the later ranges read
+ * the counts from that record (counts may then be NULL).  moe_dispatch == the range
+ * [0, E_l).  0 <= slot_begin < slot_end <= E_l, else MOE_ERR_INVALID_ARG. */
+moe_status moe_dispatch_range(moe_ctx* ctx, const moe_bf16* xs, const int32_t* counts_or_null,
+                              int32_t* layout, moe_bf16* xr, int32_t slot_begin,
+                              int32_t slot_end, moe_stream stream);
+/* Collective.  moe_combine_bwd for the rows bound to owner slots [slot_begin, slot_end):
+ * their dO rows and dgates entries (dropped slots' dgates = 0 are written by the range with
+ * slot_begin == 0).  moe_combine_bwd == the range [0, E_l). */
+moe_status moe_combine_bwd_range(moe_ctx* ctx, const moe_bf16* dy, const float* gates,
+                                 const int32_t* dest_row, const moe_bf16* ys,
+                                 const int32_t* layout, float* dgates, moe_bf16* dout_r,
+                                 int32_t slot_begin, int32_t slot_end, moe_stream stream);
+/* Not collective.  GEMM1 + SwiGLU (G, U, H into g_u_h) for the local experts in slots
+ * [slot_begin, slot_end), rows from the layout record. */
+moe_status moe_expert_ffn_up(moe_ctx* ctx, const moe_bf16* xr, const int32_t* layout,
+                             int32_t slot_begin, int32_t slot_end, const moe_bf16* w_gu,
+                             moe_bf16* g_u_h, moe_stream stream);
+/* Collective.  The rest of moe_expert_ffn_combine after every range's moe_expert_ffn_up:
+ * GEMM2 with the combine stores fused into its epilogue, the flag wait and y. */
+moe_status moe_expert_ffn_down_combine(moe_ctx* ctx, const int32_t* layout,
+                                       const moe_bf16* w_down, moe_bf16* g_u_h, moe_bf16* ys,
+                                       const float* gates, const int32_t* dest_row,
+                                       const moe_bf16* y_extra_or_null, moe_bf16* y,
+                                       moe_stream stream);
+/* Not collective.  dgrad-1 + dSwiGLU (dG, dU into dgu) for slots [slot_begin, slot_end). */
+moe_status moe_expert_ffn_bwd_dh(moe_ctx* ctx, const int32_t* layout, int32_t slot_begin,
+                                 int32_t slot_end, const moe_bf16* w_down, const moe_bf16* g_u_h,
+                                 const moe_bf16* dout, moe_bf16* dgu, moe_stream stream);
+/* Collective.  The rest of moe_expert_ffn_bwd_dispatch after every range's
+ * moe_expert_ffn_bwd_dh: dgrad-2 with the dispatch_bwd stores fused, both weight-gradient
+ * GEMMs, the flag wait. */
+moe_status moe_expert_ffn_bwd_dx_dispatch(moe_ctx* ctx, const moe_bf16* xr, const int32_t* layout,
+                                          const moe_bf16* w_gu, const moe_bf16* g_u_h,
+                                          const moe_bf16* dout, const moe_bf16* dgu, moe_bf16* dxs,
+                                          float* dw_gu, float* dw_down, int accumulate,
+                                          moe_stream stream);
+
 /* ---------------- F5+F6 / B6+B5 combine ("same communication in the
  * reverse direction") ---------------- */
 

@@ -84,6 +84,12 @@ _SIGS = {
     "moe_expert_ffn_bwd_dispatch": [P, P, P, P, P, P, P, P, P, P, P, ctypes.c_int, P],
     "moe_combine": [P, P, P, P, P, P, P, P, P],
     "moe_combine_bwd": [P, P, P, P, P, P, P, P, P],
+    "moe_dispatch_range": [P, P, P, P, P, I32, I32, P],
+    "moe_combine_bwd_range": [P, P, P, P, P, P, P, P, I32, I32, P],
+    "moe_expert_ffn_up": [P, P, P, I32, I32, P, P, P],
+    "moe_expert_ffn_down_combine": [P, P, P, P, P, P, P, P, P, P],
+    "moe_expert_ffn_bwd_dh": [P, P, I32, I32, P, P, P, P, P],
+    "moe_expert_ffn_bwd_dx_dispatch": [P, P, P, P, P, P, P, P, P, P, ctypes.c_int, P],
 }
 for _name, _args in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -343,3 +349,49 @@ def moe_combine_bwd(ctx, dy, gates, dest_row, ys, layout, dgates, dout_r, stream
         ctx.handle, _ptr(dy, BF16, "dy"), _ptr(gates, F32, "gates"), _ptr(dest_row, I32T, "dest_row"),
         _ptr(ys, BF16, "ys"), _ptr(layout, I32T, "layout"), _ptr(dgates, F32, "dgates"),
         _ptr(dout_r, BF16, "dout_r"), _stream(stream)))
+
+
+# ---- NEXT-1 chunked overlap: slot-range transfers and the expert GEMM phases (include/moe.h)
+def moe_dispatch_range(ctx, xs, counts, layout, xr, slot_begin, slot_end, stream=None):
+    _check("moe_dispatch_range", _lib.moe_dispatch_range(
+        ctx.handle, _ptr(xs, BF16, "xs"), _ptr(counts, I32T, "counts"), _ptr(layout, I32T, "layout"),
+        _ptr(xr, BF16, "xr"), int(slot_begin), int(slot_end), _stream(stream)))
+
+
+def moe_combine_bwd_range(ctx, dy, gates, dest_row, ys, layout, dgates, dout_r, slot_begin,
+                          slot_end, stream=None):
+    _check("moe_combine_bwd_range", _lib.moe_combine_bwd_range(
+        ctx.handle, _ptr(dy, BF16, "dy"), _ptr(gates, F32, "gates"), _ptr(dest_row, I32T, "dest_row"),
+        _ptr(ys, BF16, "ys"), _ptr(layout, I32T, "layout"), _ptr(dgates, F32, "dgates"),
+        _ptr(dout_r, BF16, "dout_r"), int(slot_begin), int(slot_end), _stream(stream)))
+
+
+def moe_expert_ffn_up(ctx, xr, layout, slot_begin, slot_end, w_gu, g_u_h, stream=None):
+    _check("moe_expert_ffn_up", _lib.moe_expert_ffn_up(
+        ctx.handle, _ptr(xr, BF16, "xr"), _ptr(layout, I32T, "layout"), int(slot_begin),
+        int(slot_end), _ptr(w_gu, BF16, "w_gu"), _ptr(g_u_h, BF16, "g_u_h"), _stream(stream)))
+
+
+def moe_expert_ffn_down_combine(ctx, layout, w_down, g_u_h, ys, gates, dest_row, y_extra, y,
+                                stream=None):
+    _check("moe_expert_ffn_down_combine", _lib.moe_expert_ffn_down_combine(
+        ctx.handle, _ptr(layout, I32T, "layout"), _ptr(w_down, BF16, "w_down"),
+        _ptr(g_u_h, BF16, "g_u_h"), _ptr(ys, BF16, "ys"), _ptr(gates, F32, "gates"),
+        _ptr(dest_row, I32T, "dest_row"), _ptr(y_extra, BF16, "y_extra"), _ptr(y, BF16, "y"),
+        _stream(stream)))
+
+
+def moe_expert_ffn_bwd_dh(ctx, layout, slot_begin, slot_end, w_down, g_u_h, dout, dgu, stream=None):
+    _check("moe_expert_ffn_bwd_dh", _lib.moe_expert_ffn_bwd_dh(
+        ctx.handle, _ptr(layout, I32T, "layout"), int(slot_begin), int(slot_end),
+        _ptr(w_down, BF16, "w_down"), _ptr(g_u_h, BF16, "g_u_h"), _ptr(dout, BF16, "dout"),
+        _ptr(dgu, BF16, "dgu"), _stream(stream)))
+
+
+def moe_expert_ffn_bwd_dx_dispatch(ctx, xr, layout, w_gu, g_u_h, dout, dgu, dxs, dw_gu, dw_down,
+                                   accumulate=False, stream=None):
+    _check("moe_expert_ffn_bwd_dx_dispatch", _lib.moe_expert_ffn_bwd_dx_dispatch(
+        ctx.handle, _ptr(xr, BF16, "xr"), _ptr(layout, I32T, "layout"), _ptr(w_gu, BF16, "w_gu"),
+        _ptr(g_u_h, BF16, "g_u_h"), _ptr(dout, BF16, "dout"), _ptr(dgu, BF16, "dgu"),
+        _ptr(dxs, BF16, "dxs"), _ptr(dw_gu, F32, "dw_gu"), _ptr(dw_down, F32, "dw_down"),
+        int(bool(accumulate)), _stream(stream)))

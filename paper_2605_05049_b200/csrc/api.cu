@@ -500,14 +500,22 @@ moe_status moe_permute_bwd(moe_ctx* c, const moe_bf16* dxs, const int32_t* dest_
 }
 
 // ---------------------------------------------------------------- F3 / B3
-moe_status moe_dispatch(moe_ctx* c, const moe_bf16* xs, const int32_t* counts, int32_t* layout,
-                        moe_bf16* xr, moe_stream s) {
-  MOE_REQUIRE(c && xs && counts && layout && xr);
+moe_status moe_dispatch_range(moe_ctx* c, const moe_bf16* xs, const int32_t* counts, int32_t* layout,
+                              moe_bf16* xr, int32_t slot_begin, int32_t slot_end, moe_stream s) {
+  MOE_REQUIRE(c && xs && layout && xr && (counts || slot_begin > 0));
+  MOE_REQUIRE(slot_begin >= 0 && slot_begin < slot_end && slot_end <= c->E_l);
   if (!c->peers_ready) return MOE_ERR_NOT_READY;
   if (!in_heap(c, xr)) return MOE_ERR_NOT_SYMMETRIC;
   CommArgs a = comm_args(c);
   const int64_t dst_off = reinterpret_cast<const char*>(xr) - c->heap;
-  return cuda_status(moe::launch_dispatch(a, counts, layout, c->recv_rows, xs, dst_off, xr, st(s)));
+  return cuda_status(moe::launch_dispatch(a, counts, layout, c->recv_rows, xs, dst_off, xr,
+                                          slot_begin, slot_end, st(s)));
+}
+
+moe_status moe_dispatch(moe_ctx* c, const moe_bf16* xs, const int32_t* counts, int32_t* layout,
+                        moe_bf16* xr, moe_stream s) {
+  MOE_REQUIRE(c && counts);
+  return moe_dispatch_range(c, xs, counts, layout, xr, 0, c->E_l, s);
 }
 
 moe_status moe_dispatch_bwd(moe_ctx* c, const moe_bf16* dxr, const int32_t* layout, moe_bf16* dxs,
@@ -529,10 +537,12 @@ struct Scatter {
   const int32_t* layout;
 };
 
-moe_status ffn_fwd(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows, int32_t n_groups,
-                   int64_t rows_cap, int32_t f, const moe_bf16* w_gu, const moe_bf16* w_down,
-                   moe_bf16* g_u_h, moe_bf16* out, const Scatter* sc, moe_stream s) {
-  MOE_REQUIRE(n_groups >= 1 && n_groups <= 256 && rows_cap >= 0 && f > 0 && f % 128 == 0);
+// GEMM1 + SwiGLU epilogue for groups [g0, n_groups): xr -> g_u_h (G, U, H)
+moe_status ffn_up(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows, int32_t g0,
+                  int32_t n_groups, int64_t rows_cap, int32_t f, const moe_bf16* w_gu,
+                  moe_bf16* g_u_h, moe_stream s) {
+  MOE_REQUIRE(n_groups >= 1 && n_groups <= 256 && g0 >= 0 && g0 < n_groups && rows_cap >= 0 &&
+              f > 0 && f % 128 == 0);
   if (rows_cap == 0) return MOE_OK;
   const int d = c->s.d;
   moe::GemmProblem g1;
@@ -542,11 +552,20 @@ moe_status ffn_fwd(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows, in
   g1.b_ptr = w_gu; g1.b_rows = static_cast<int64_t>(n_groups) * 2 * f; g1.b_cols = d; g1.b_ld = d;
   g1.b_group_stride = 2 * f; g1.b_split = f;
   g1.N = 2 * f; g1.K = d;
-  g1.group_rows = group_rows; g1.n_groups = n_groups; g1.rows_cap = rows_cap;
+  g1.group_rows = group_rows; g1.n_groups = n_groups; g1.group_begin = g0; g1.rows_cap = rows_cap;
   g1.pair = gemm_pair();
   g1.max_ctas = c->gemm_sms;
   g1.out = g_u_h; g1.ld_out = 3 * static_cast<int64_t>(f); g1.f = f;
-  MOE_TRY_CUDA(moe::launch_grouped_gemm(g1, st(s)));
+  return cuda_status(moe::launch_grouped_gemm(g1, st(s)));
+}
+
+// GEMM2: H (inside g_u_h) -> out, or straight into the sources' ys (sc, combine fused)
+moe_status ffn_down(moe_ctx* c, const int32_t* group_rows, int32_t n_groups, int64_t rows_cap,
+                    int32_t f, const moe_bf16* w_down, moe_bf16* g_u_h, moe_bf16* out,
+                    const Scatter* sc, moe_stream s) {
+  MOE_REQUIRE(n_groups >= 1 && n_groups <= 256 && rows_cap >= 0 && f > 0 && f % 128 == 0);
+  if (rows_cap == 0) return MOE_OK;
+  const int d = c->s.d;
   moe::GemmProblem g2;
   g2.epi = moe::kEpiBF16;
   g2.BN = pick_bn(d);
@@ -564,6 +583,14 @@ moe_status ffn_fwd(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows, in
   }
   return cuda_status(moe::launch_grouped_gemm(g2, st(s)));
 }
+
+moe_status ffn_fwd(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows, int32_t n_groups,
+                   int64_t rows_cap, int32_t f, const moe_bf16* w_gu, const moe_bf16* w_down,
+                   moe_bf16* g_u_h, moe_bf16* out, const Scatter* sc, moe_stream s) {
+  moe_status r = ffn_up(c, xr, group_rows, 0, n_groups, rows_cap, f, w_gu, g_u_h, s);
+  if (r != MOE_OK) return r;
+  return ffn_down(c, group_rows, n_groups, rows_cap, f, w_down, g_u_h, out, sc, s);
+}
 }  // namespace
 
 moe_status moe_expert_ffn(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows, int32_t n_groups,
@@ -574,10 +601,35 @@ moe_status moe_expert_ffn(moe_ctx* c, const moe_bf16* xr, const int32_t* group_r
 }
 
 namespace {
-moe_status ffn_bwd(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows, int32_t n_groups,
-                   int64_t rows_cap, int32_t f, const moe_bf16* w_gu, const moe_bf16* w_down,
-                   const moe_bf16* g_u_h, const moe_bf16* dout, moe_bf16* dgu, moe_bf16* dxr,
-                   float* dw_gu, float* dw_down, int accumulate, const Scatter* sc, moe_stream s) {
+// dgrad-1: dH = dout . W_down^T (+ dSwiGLU epilogue) -> dgu, for groups [g0, n_groups)
+moe_status ffn_bwd_dh(moe_ctx* c, const int32_t* group_rows, int32_t g0, int32_t n_groups,
+                      int64_t rows_cap, int32_t f, const moe_bf16* w_down, const moe_bf16* g_u_h,
+                      const moe_bf16* dout, moe_bf16* dgu, moe_stream s) {
+  MOE_REQUIRE(n_groups >= 1 && n_groups <= 256 && g0 >= 0 && g0 < n_groups && rows_cap >= 0 &&
+              f > 0 && f % 128 == 0);
+  if (rows_cap == 0) return MOE_OK;
+  const int d = c->s.d;
+  const int64_t F = f;
+  moe::GemmProblem a;
+  a.epi = moe::kEpiDSwiGLU;
+  a.BN = (f % 256 == 0) ? 256 : 128;
+  a.b_mn = true;
+  a.a_ptr = dout; a.a_rows = rows_cap; a.a_cols = d; a.a_ld = d;
+  a.b_ptr = w_down; a.b_rows = static_cast<int64_t>(n_groups) * d; a.b_cols = f; a.b_ld = f;
+  a.b_group_stride = d;
+  a.N = f; a.K = d;
+  a.group_rows = group_rows; a.n_groups = n_groups; a.group_begin = g0; a.rows_cap = rows_cap;
+  a.pair = gemm_pair();
+  a.max_ctas = c->gemm_sms;
+  a.out = dgu; a.ld_out = 2 * F; a.aux = g_u_h; a.ld_aux = 3 * F; a.f = f;
+  return cuda_status(moe::launch_grouped_gemm(a, st(s)));
+}
+
+// dgrad-2 (-> dxr, or straight into the sources' dxs: dispatch_bwd fused) and both wgrads
+moe_status ffn_bwd_dx(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows, int32_t n_groups,
+                      int64_t rows_cap, int32_t f, const moe_bf16* w_gu, const moe_bf16* g_u_h,
+                      const moe_bf16* dout, const moe_bf16* dgu, moe_bf16* dxr, float* dw_gu,
+                      float* dw_down, int accumulate, const Scatter* sc, moe_stream s) {
   MOE_REQUIRE(n_groups >= 1 && n_groups <= 256 && rows_cap >= 0 && f > 0 && f % 128 == 0);
   const int d = c->s.d;
   const int64_t F = f;
@@ -588,20 +640,6 @@ moe_status ffn_bwd(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows, in
     }
     return MOE_OK;
   }
-  // dgrad-1: dH = dout . W_down^T (+ dSwiGLU epilogue) -> dgu
-  moe::GemmProblem a;
-  a.epi = moe::kEpiDSwiGLU;
-  a.BN = (f % 256 == 0) ? 256 : 128;
-  a.b_mn = true;
-  a.a_ptr = dout; a.a_rows = rows_cap; a.a_cols = d; a.a_ld = d;
-  a.b_ptr = w_down; a.b_rows = static_cast<int64_t>(n_groups) * d; a.b_cols = f; a.b_ld = f;
-  a.b_group_stride = d;
-  a.N = f; a.K = d;
-  a.group_rows = group_rows; a.n_groups = n_groups; a.rows_cap = rows_cap;
-  a.pair = gemm_pair();
-  a.max_ctas = c->gemm_sms;
-  a.out = dgu; a.ld_out = 2 * F; a.aux = g_u_h; a.ld_aux = 3 * F; a.f = f;
-  MOE_TRY_CUDA(moe::launch_grouped_gemm(a, st(s)));
   // dgrad-2: dX = [dG dU] . W_gu  -> dxr
   moe::GemmProblem b;
   b.epi = moe::kEpiBF16;
@@ -614,7 +652,7 @@ moe_status ffn_bwd(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows, in
   b.group_rows = group_rows; b.n_groups = n_groups; b.rows_cap = rows_cap;
   b.pair = gemm_pair();
   b.max_ctas = c->gemm_sms;
-  b.out = dxr ? static_cast<void*>(dxr) : static_cast<void*>(dgu); b.ld_out = d;
+  b.out = dxr ? static_cast<void*>(dxr) : const_cast<moe_bf16*>(dgu); b.ld_out = d;
   if (sc) {  // dX rows go straight back to their source ranks (dispatch_bwd fused)
     b.scatter = 1; b.scatter_off = sc->off; b.scatter_layout = sc->layout; b.comm = sc->comm;
   }
@@ -648,6 +686,16 @@ moe_status ffn_bwd(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows, in
   w2.n_fastest = w2.M > w2.N;
   return cuda_status(moe::launch_grouped_gemm(w2, st(s)));
 }
+
+moe_status ffn_bwd(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows, int32_t n_groups,
+                   int64_t rows_cap, int32_t f, const moe_bf16* w_gu, const moe_bf16* w_down,
+                   const moe_bf16* g_u_h, const moe_bf16* dout, moe_bf16* dgu, moe_bf16* dxr,
+                   float* dw_gu, float* dw_down, int accumulate, const Scatter* sc, moe_stream s) {
+  moe_status r = ffn_bwd_dh(c, group_rows, 0, n_groups, rows_cap, f, w_down, g_u_h, dout, dgu, s);
+  if (r != MOE_OK) return r;
+  return ffn_bwd_dx(c, xr, group_rows, n_groups, rows_cap, f, w_gu, g_u_h, dout, dgu, dxr, dw_gu,
+                    dw_down, accumulate, sc, s);
+}
 }  // namespace
 
 moe_status moe_expert_ffn_bwd(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows,
@@ -661,6 +709,33 @@ moe_status moe_expert_ffn_bwd(moe_ctx* c, const moe_bf16* xr, const int32_t* gro
 }
 
 // ---------------------------------------------------------------- F4+F5+F6 / B4+B3 fused
+moe_status moe_expert_ffn_up(moe_ctx* c, const moe_bf16* xr, const int32_t* layout,
+                             int32_t slot_begin, int32_t slot_end, const moe_bf16* w_gu,
+                             moe_bf16* g_u_h, moe_stream s) {
+  MOE_REQUIRE(c && xr && layout && w_gu && g_u_h);
+  MOE_REQUIRE(slot_begin >= 0 && slot_begin < slot_end && slot_end <= c->E_l);
+  const int32_t* expert_rows = layout + static_cast<int64_t>(c->s.ep_size) * c->s.E;
+  return ffn_up(c, xr, expert_rows, slot_begin, slot_end, c->recv_rows, c->s.f, w_gu, g_u_h, s);
+}
+
+moe_status moe_expert_ffn_down_combine(moe_ctx* c, const int32_t* layout, const moe_bf16* w_down,
+                                       moe_bf16* g_u_h, moe_bf16* ys, const float* gates,
+                                       const int32_t* dest_row, const moe_bf16* y_extra,
+                                       moe_bf16* y, moe_stream s) {
+  MOE_REQUIRE(c && layout && w_down && g_u_h && ys && gates && dest_row && y);
+  if (!c->peers_ready) return MOE_ERR_NOT_READY;
+  if (!in_heap(c, ys)) return MOE_ERR_NOT_SYMMETRIC;
+  CommArgs a = comm_args(c);
+  const Scatter sc{&a, reinterpret_cast<const char*>(ys) - c->heap, layout};
+  const int32_t* expert_rows = layout + static_cast<int64_t>(c->s.ep_size) * c->s.E;
+  moe_status r = ffn_down(c, expert_rows, c->E_l, c->recv_rows, c->s.f, w_down, g_u_h, nullptr,
+                          &sc, s);
+  if (r != MOE_OK) return r;
+  MOE_TRY_CUDA(moe::launch_wait_flags(a, moe::kSlotData, st(s)));
+  return cuda_status(moe::launch_unpermute(ys, gates, dest_row, y_extra, c->s.T_local, c->s.d,
+                                           c->s.k, y, st(s)));
+}
+
 moe_status moe_expert_ffn_combine(moe_ctx* c, const moe_bf16* xr, const int32_t* layout,
                                   const moe_bf16* w_gu, const moe_bf16* w_down, moe_bf16* g_u_h,
                                   moe_bf16* ys, const float* gates, const int32_t* dest_row,
@@ -668,15 +743,37 @@ moe_status moe_expert_ffn_combine(moe_ctx* c, const moe_bf16* xr, const int32_t*
   MOE_REQUIRE(c && xr && layout && w_gu && w_down && g_u_h && ys && gates && dest_row && y);
   if (!c->peers_ready) return MOE_ERR_NOT_READY;
   if (!in_heap(c, ys)) return MOE_ERR_NOT_SYMMETRIC;
-  CommArgs a = comm_args(c);
-  const Scatter sc{&a, reinterpret_cast<const char*>(ys) - c->heap, layout};
-  const int32_t* expert_rows = layout + static_cast<int64_t>(c->s.ep_size) * c->s.E;
-  moe_status r = ffn_fwd(c, xr, expert_rows, c->E_l, c->recv_rows, c->s.f, w_gu, w_down, g_u_h,
-                         nullptr, &sc, s);
+  moe_status r = moe_expert_ffn_up(c, xr, layout, 0, c->E_l, w_gu, g_u_h, s);
   if (r != MOE_OK) return r;
-  MOE_TRY_CUDA(moe::launch_wait_flags(a, moe::kSlotData, st(s)));
-  return cuda_status(moe::launch_unpermute(ys, gates, dest_row, y_extra, c->s.T_local, c->s.d,
-                                           c->s.k, y, st(s)));
+  return moe_expert_ffn_down_combine(c, layout, w_down, g_u_h, ys, gates, dest_row, y_extra, y, s);
+}
+
+moe_status moe_expert_ffn_bwd_dh(moe_ctx* c, const int32_t* layout, int32_t slot_begin,
+                                 int32_t slot_end, const moe_bf16* w_down, const moe_bf16* g_u_h,
+                                 const moe_bf16* dout, moe_bf16* dgu, moe_stream s) {
+  MOE_REQUIRE(c && layout && w_down && g_u_h && dout && dgu);
+  MOE_REQUIRE(slot_begin >= 0 && slot_begin < slot_end && slot_end <= c->E_l);
+  const int32_t* expert_rows = layout + static_cast<int64_t>(c->s.ep_size) * c->s.E;
+  return ffn_bwd_dh(c, expert_rows, slot_begin, slot_end, c->recv_rows, c->s.f, w_down, g_u_h,
+                    dout, dgu, s);
+}
+
+moe_status moe_expert_ffn_bwd_dx_dispatch(moe_ctx* c, const moe_bf16* xr, const int32_t* layout,
+                                          const moe_bf16* w_gu, const moe_bf16* g_u_h,
+                                          const moe_bf16* dout, const moe_bf16* dgu, moe_bf16* dxs,
+                                          float* dw_gu, float* dw_down, int accumulate,
+                                          moe_stream s) {
+  MOE_REQUIRE(c && xr && layout && w_gu && g_u_h && dout && dgu && dxs && dw_gu && dw_down);
+  if (!c->peers_ready) return MOE_ERR_NOT_READY;
+  if (!in_heap(c, dxs)) return MOE_ERR_NOT_SYMMETRIC;
+  CommArgs a = comm_args(c);
+  const Scatter sc{&a, reinterpret_cast<const char*>(dxs) - c->heap, layout};
+  const int32_t* expert_rows = layout + static_cast<int64_t>(c->s.ep_size) * c->s.E;
+  moe_status r = ffn_bwd_dx(c, xr, expert_rows, c->E_l, c->recv_rows, c->s.f, w_gu, g_u_h, dout,
+                            dgu, nullptr, dw_gu, dw_down, accumulate, &sc, s);
+  if (r != MOE_OK) return r;
+  // the dX rows streamed to the sources during dgrad-2 and the two wgrad GEMMs
+  return cuda_status(moe::launch_wait_flags(a, moe::kSlotData, st(s)));
 }
 
 moe_status moe_expert_ffn_bwd_dispatch(moe_ctx* c, const moe_bf16* xr, const int32_t* layout,
@@ -687,14 +784,10 @@ moe_status moe_expert_ffn_bwd_dispatch(moe_ctx* c, const moe_bf16* xr, const int
   MOE_REQUIRE(c && xr && layout && w_gu && w_down && g_u_h && dout && dgu && dxs && dw_gu && dw_down);
   if (!c->peers_ready) return MOE_ERR_NOT_READY;
   if (!in_heap(c, dxs)) return MOE_ERR_NOT_SYMMETRIC;
-  CommArgs a = comm_args(c);
-  const Scatter sc{&a, reinterpret_cast<const char*>(dxs) - c->heap, layout};
-  const int32_t* expert_rows = layout + static_cast<int64_t>(c->s.ep_size) * c->s.E;
-  moe_status r = ffn_bwd(c, xr, expert_rows, c->E_l, c->recv_rows, c->s.f, w_gu, w_down, g_u_h, dout,
-                         dgu, nullptr, dw_gu, dw_down, accumulate, &sc, s);
+  moe_status r = moe_expert_ffn_bwd_dh(c, layout, 0, c->E_l, w_down, g_u_h, dout, dgu, s);
   if (r != MOE_OK) return r;
-  // the dX rows streamed to the sources during dgrad-2 and the two wgrad GEMMs
-  return cuda_status(moe::launch_wait_flags(a, moe::kSlotData, st(s)));
+  return moe_expert_ffn_bwd_dx_dispatch(c, xr, layout, w_gu, g_u_h, dout, dgu, dxs, dw_gu, dw_down,
+                                        accumulate, s);
 }
 
 // ---------------------------------------------------------------- F5+F6 / B6+B5
@@ -711,17 +804,26 @@ moe_status moe_combine(moe_ctx* c, const moe_bf16* out, const int32_t* layout, m
                                            c->s.k, y, st(s)));
 }
 
-moe_status moe_combine_bwd(moe_ctx* c, const moe_bf16* dy, const float* gates, const int32_t* dest_row,
-                           const moe_bf16* ys, const int32_t* layout, float* dgates, moe_bf16* dout_r,
-                           moe_stream s) {
+moe_status moe_combine_bwd_range(moe_ctx* c, const moe_bf16* dy, const float* gates,
+                                 const int32_t* dest_row, const moe_bf16* ys, const int32_t* layout,
+                                 float* dgates, moe_bf16* dout_r, int32_t slot_begin,
+                                 int32_t slot_end, moe_stream s) {
   MOE_REQUIRE(c && dy && gates && dest_row && ys && layout && dgates && dout_r);
+  MOE_REQUIRE(slot_begin >= 0 && slot_begin < slot_end && slot_end <= c->E_l);
   if (!c->peers_ready) return MOE_ERR_NOT_READY;
   if (!in_heap(c, dout_r)) return MOE_ERR_NOT_SYMMETRIC;
   CommArgs a = comm_args(c);
   const int64_t dst_off = reinterpret_cast<const char*>(dout_r) - c->heap;
   return cuda_status(moe::launch_combine_bwd_transfer(a, const_cast<int32_t*>(layout), dst_off,
                                                       dout_r, dest_row, gates, dy, ys, dgates,
-                                                      st(s)));
+                                                      slot_begin, slot_end, st(s)));
+}
+
+moe_status moe_combine_bwd(moe_ctx* c, const moe_bf16* dy, const float* gates, const int32_t* dest_row,
+                           const moe_bf16* ys, const int32_t* layout, float* dgates, moe_bf16* dout_r,
+                           moe_stream s) {
+  MOE_REQUIRE(c);
+  return moe_combine_bwd_range(c, dy, gates, dest_row, ys, layout, dgates, dout_r, 0, c->E_l, s);
 }
 
 }  // extern "C"

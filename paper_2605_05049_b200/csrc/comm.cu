@@ -243,20 +243,23 @@ __global__ void forward_transfer_kernel(CommArgs a, int32_t* __restrict__ layout
                                         const float* __restrict__ gates,
                                         const uint16_t* __restrict__ dy,
                                         const uint16_t* __restrict__ ys,
-                                        float* __restrict__ dgates) {
+                                        float* __restrict__ dgates, int s0, int s1) {
   __shared__ FwdTables tb;
   __shared__ SegTable sg;
   a.epoch = load_epoch(a);
   const int32_t* cm = layout;
+  // the first range (s0 == 0) of a dispatch exchanges the counts and writes the layout
+  // record; later ranges of the same step read the counts back from that record
+  const bool exchange = (MODE == 0 && s0 == 0);
   MOE_TRACE_AT(0, MODE == 0 && blockIdx.x == 0);
-  if (MODE == 0) {
+  if (exchange) {
     publish_counts(a, counts);
     wait_all(a, kSlotCounts);
     MOE_TRACE_AT(1, blockIdx.x == 0);
     cm = a.countmat + static_cast<int>(a.epoch & 1) * a.ep * a.E;
   }
   build_fwd_tables(a, cm, tb);
-  if (MODE == 0 && blockIdx.x == 0) {  // layout record for the later calls of this layer
+  if (exchange && blockIdx.x == 0) {  // layout record for the later calls of this layer
     const int EP = a.ep, E = a.E, E_l = a.E_l;
     for (int i = threadIdx.x; i < EP * E; i += blockDim.x) layout[i] = cm[i];
     for (int el = threadIdx.x; el < E_l; el += blockDim.x)
@@ -267,8 +270,9 @@ __global__ void forward_transfer_kernel(CommArgs a, int32_t* __restrict__ layout
   if (MODE == 0) {
     for (int i = threadIdx.x; i < a.E; i += blockDim.x) {
       const int q = (a.rank + 1 + i / a.E_l) % a.ep;   // rotated owner order
-      const int e = a.expert_at[q * a.E_l + i % a.E_l];
-      sg.count[i] = tb.off[e + 1] - tb.off[e];
+      const int el = i % a.E_l;
+      const int e = a.expert_at[q * a.E_l + el];
+      sg.count[i] = (el >= s0 && el < s1) ? tb.off[e + 1] - tb.off[e] : 0;
       sg.src_base[i] = tb.off[e];
       sg.dst_base[i] = tb.dst[e];
       sg.dst_rank[i] = q;
@@ -284,16 +288,17 @@ __global__ void forward_transfer_kernel(CommArgs a, int32_t* __restrict__ layout
   const int nvec = d / 8;
   const int64_t row_bytes = static_cast<int64_t>(d) * 2;
   const int E = a.E, E_l = a.E_l;
-  // padding rows of the local receive buffer (zeroed every call)
-  const int64_t n_pad_rows = tb.seg[E_l];
+  // padding rows of the local receive buffer in slots [s0, s1) (zeroed every call)
+  const int64_t pad_base = tb.seg[s0];
+  const int64_t n_pad_rows = tb.seg[s1] - pad_base;
   // mode 0 work item = one 2 KB part of a row (a few rows still spread over many warps);
   // mode 1 = one token (its k rows and their dot products)
   const int parts = (MODE == 0) ? row_parts(nvec) : 1;
-  const int64_t n_items = (MODE == 0) ? static_cast<int64_t>(tb.off[E]) * parts : a.T;
+  const int64_t n_items = (MODE == 0) ? static_cast<int64_t>(sg.prefix[E]) * parts : a.T;
 
   for (int64_t w = gwarp; w < n_items + n_pad_rows; w += nwarps) {
     if (w >= n_items) {
-      const int64_t row = w - n_items;
+      const int64_t row = pad_base + (w - n_items);
       const int el = upper_bound_idx(tb.seg, E_l + 1, row);
       const int64_t within = row - tb.seg[el];
       if (within < tb.rows[a.expert_at[a.rank * E_l + el]]) continue;  // data row, not padding
@@ -315,11 +320,13 @@ __global__ void forward_transfer_kernel(CommArgs a, int32_t* __restrict__ layout
       for (int j = 0; j < a.k; ++j) {
         const int32_t row = dest_row[t * a.k + j];
         if (row < 0) {
-          if (lane == 0) dgates[t * a.k + j] = 0.f;
+          if (lane == 0 && s0 == 0) dgates[t * a.k + j] = 0.f;
           continue;
         }
-        const float g = gates[t * a.k + j];
         const int e = upper_bound_idx(tb.off, E + 1, row);
+        const int slot = a.place[e] % E_l;
+        if (slot < s0 || slot >= s1) continue;   // another range's row
+        const float g = gates[t * a.k + j];
         const int q = a.place[e] / E_l;
         const int64_t drow = tb.dst[e] + (row - tb.off[e]);
         uint4* dst = reinterpret_cast<uint4*>(a.peers.base[q] + dst_off + drow * row_bytes);
@@ -419,6 +426,12 @@ __global__ void wait_flags_kernel(CommArgs a, int slot) {
 // Up to 2 blocks of 512 threads per SM (all co-resident: blocks spin on peer flags), and no
 // more than one block per 32 work items (2 KB row parts): small messages are latency-bound,
 // and every extra block adds to the launch and to the last-block count.
+// With an SM budget (a transfer running beside a GEMM on another stream) every block also
+// reserves unused dynamic shared memory, so it cannot be co-scheduled on an SM that holds a
+// ~215 KB GEMM CTA: the copy blocks stay on the SMs the GEMM left free instead of stealing
+// issue and load/store slots from GEMM CTAs.
+int transfer_smem(const CommArgs& a) { return a.blocks > 0 ? 32 * 1024 : 0; }
+
 int transfer_blocks(const CommArgs& a, int64_t rows) {
   int64_t b = a.blocks > 0 ? a.blocks : 2 * num_sms();
   const int64_t parts = (a.d / 8 + 127) / 128;
@@ -442,27 +455,28 @@ cudaError_t launch_wait_flags(const CommArgs& a, int slot, cudaStream_t s) {
 
 cudaError_t launch_dispatch(const CommArgs& a, const int32_t* counts, int32_t* layout,
                             int64_t recv_rows_cap, const uint16_t* src, int64_t dst_off,
-                            uint16_t* local_dst, cudaStream_t s) {
-  forward_transfer_kernel<0><<<transfer_blocks(a, a.T * a.k), 512, 0, s>>>(
+                            uint16_t* local_dst, int s0, int s1, cudaStream_t s) {
+  const int64_t rows = a.T * a.k * (s1 - s0) / a.E_l + a.T;   // range share (+ slack)
+  forward_transfer_kernel<0><<<transfer_blocks(a, rows), 512, transfer_smem(a), s>>>(
       a, layout, counts, recv_rows_cap, src, dst_off, local_dst, nullptr, nullptr, nullptr, nullptr,
-      nullptr);
+      nullptr, s0, s1);
   return cudaGetLastError();
 }
 
 cudaError_t launch_combine_bwd_transfer(const CommArgs& a, int32_t* layout, int64_t dst_off,
                                         uint16_t* local_dst, const int32_t* dest_row,
                                         const float* gates, const uint16_t* dy, const uint16_t* ys,
-                                        float* dgates, cudaStream_t s) {
-  forward_transfer_kernel<1><<<transfer_blocks(a, a.T * a.k), 512, 0, s>>>(
-      a, layout, nullptr, 0, nullptr, dst_off, local_dst, dest_row, gates, dy, ys, dgates);
+                                        float* dgates, int s0, int s1, cudaStream_t s) {
+  forward_transfer_kernel<1><<<transfer_blocks(a, a.T * a.k), 512, transfer_smem(a), s>>>(
+      a, layout, nullptr, 0, nullptr, dst_off, local_dst, dest_row, gates, dy, ys, dgates, s0, s1);
   return cudaGetLastError();
 }
 
 cudaError_t launch_reverse_transfer(const CommArgs& a, const int32_t* layout, const uint16_t* src,
                                     int64_t dst_off, cudaStream_t s) {
   // receive rows <= EP * T * k
-  reverse_transfer_kernel<<<transfer_blocks(a, a.T * a.k * a.ep), 512, 0, s>>>(a, layout, src,
-                                                                              dst_off);
+  reverse_transfer_kernel<<<transfer_blocks(a, a.T * a.k * a.ep), 512, transfer_smem(a), s>>>(
+      a, layout, src, dst_off);
   return cudaGetLastError();
 }
 

@@ -40,6 +40,7 @@ constexpr int kStageBox = 4096;  // per-epilogue-warp staging: 32 rows x 128 byt
 struct KParams {
   int M, N, K;
   int n_groups;
+  int group_begin;      // tiles only for groups >= group_begin (segment bases still from 0)
   const int32_t* group_rows;
   int64_t rows_cap;
   int64_t b_group_stride, b_split;
@@ -189,7 +190,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       int g = base + lane;
       int rows = (g < n_groups) ? p.group_rows[g] : 0;
       int seg_sz = ((rows + MOE_ALIGN_ROWS - 1) / MOE_ALIGN_ROWS) * MOE_ALIGN_ROWS;
-      int tiles = (g < n_groups) ? (KGROUPED ? MT * NT : ceil_div(rows, TILE_M) * NT) : 0;
+      int tiles = (g < n_groups && g >= p.group_begin)
+                      ? (KGROUPED ? MT * NT : ceil_div(rows, TILE_M) * NT) : 0;
       int a = seg_sz, b = tiles;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -702,6 +704,7 @@ cudaError_t launch_impl(const GemmProblem& g, cudaStream_t stream) {
   }
   kp.M = g.M; kp.N = g.N; kp.K = g.K;
   kp.n_groups = g.n_groups;
+  kp.group_begin = g.group_begin;
   kp.group_rows = g.group_rows;
   kp.rows_cap = g.rows_cap;
   kp.b_group_stride = g.b_group_stride;

@@ -34,6 +34,7 @@ struct GemmProblem {
   int M = 0, N = 0, K = 0;     // M-grouped: N, K; K-grouped: M, N
   const int32_t* group_rows = nullptr;  // device [n_groups]
   int n_groups = 0;
+  int group_begin = 0;  // M-grouped: tiles only for groups [group_begin, n_groups)
   int64_t rows_cap = 0;
   void* out = nullptr;
   int64_t ld_out = 0;
@@ -117,14 +118,16 @@ enum { kSlotCounts = 0, kSlotData = 1, kNumSlots = 2 };
 // destination buffer inside every rank's symmetric heap.
 // Forward pattern (source send-layout rows -> owners' receive rows; zeroes local padding):
 //   dispatch: counts exchange + layout record + rows of src
+// Both move only the rows bound for owner slots [s0, s1) (NEXT-1 chunked overlap); the
+// range with s0 == 0 of a dispatch also exchanges the counts and writes the layout record.
 cudaError_t launch_dispatch(const CommArgs& a, const int32_t* counts, int32_t* layout,
                             int64_t recv_rows_cap, const uint16_t* src, int64_t dst_off,
-                            uint16_t* local_dst, cudaStream_t s);
+                            uint16_t* local_dst, int s0, int s1, cudaStream_t s);
 //   combine_bwd: payload rows gates * dy, and dgates = <dy, ys rows>
 cudaError_t launch_combine_bwd_transfer(const CommArgs& a, int32_t* layout, int64_t dst_off,
                                         uint16_t* local_dst, const int32_t* dest_row,
                                         const float* gates, const uint16_t* dy, const uint16_t* ys,
-                                        float* dgates, cudaStream_t s);
+                                        float* dgates, int s0, int s1, cudaStream_t s);
 // Reverse pattern: owner receive rows -> sources' send-layout rows
 cudaError_t launch_reverse_transfer(const CommArgs& a, const int32_t* layout, const uint16_t* src,
                                     int64_t dst_off, cudaStream_t s);

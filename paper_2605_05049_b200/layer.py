@@ -171,6 +171,9 @@ class MoELayer:
         self._mark("F0+F1 router,route")
         L.moe_permute(c, x, self.topk_idx, self.counts, self.dest_row, self.xs)
         self._mark("F2 permute")
+        ranges = self._ranges()
+        if ranges:
+            return self._forward_chunked(x, ranges)
         y_extra = None
         if self.fs and self.overlap:
             # shared experts (local tokens, no exchange) run beside the dispatch all-to-all on
@@ -204,12 +207,97 @@ class MoELayer:
             self._mark("F5+F6 combine")
         return self.y
 
+    # ------------------------------------------------------------------ NEXT-1 chunked overlap
+    # Owner slots cut into `chunks` ranges: the all-to-all of range i+1 (side stream, comm_sms
+    # SMs) runs beside the first expert GEMM of range i (this stream, the other SMs).  Used by
+    # the fused path when EP > 1 and E_l > 1; chunks = 1 turns it off.
+    chunks = 1
+
+    def _ranges(self):
+        E_l, n = self.E_l, min(self.chunks, self.E_l)
+        if not self.fused or self.dims.ep_size == 1 or n < 2:
+            return None
+        bounds = [E_l * i // n for i in range(n + 1)]
+        return list(zip(bounds[:-1], bounds[1:]))
+
+    def _forward_chunked(self, x, ranges):
+        c, T = self.ctx, self.dims.T_local
+        b0, e0 = ranges[0]
+        y_extra = None
+        if self.fs and self.overlap:
+            self._concurrent(lambda s: L.moe_dispatch_range(c, self.xs, self.counts, self.layout,
+                                                            self.xr, b0, e0, stream=s),
+                             lambda s: L.moe_expert_ffn(c, x, self.rows_T, 1, T, self.fs,
+                                                        self.w_gu_s, self.w_down_s, self.g_u_h_s,
+                                                        self.y_s, stream=s))
+            y_extra = self.y_s
+        else:
+            L.moe_dispatch_range(c, self.xs, self.counts, self.layout, self.xr, b0, e0)
+            if self.fs:
+                L.moe_expert_ffn(c, x, self.rows_T, 1, T, self.fs, self.w_gu_s, self.w_down_s,
+                                 self.g_u_h_s, self.y_s)
+                y_extra = self.y_s
+        self._mark("F3 dispatch (range 0)")
+        for (pb, pe), (b, e) in zip(ranges[:-1], ranges[1:]):
+            self._concurrent(
+                lambda s, b=b, e=e: L.moe_dispatch_range(c, self.xs, None, self.layout, self.xr,
+                                                         b, e, stream=s),
+                lambda s, pb=pb, pe=pe: L.moe_expert_ffn_up(c, self.xr, self.layout, pb, pe,
+                                                            self.w_gu, self.g_u_h, stream=s))
+        L.moe_expert_ffn_up(c, self.xr, self.layout, ranges[-1][0], ranges[-1][1], self.w_gu,
+                            self.g_u_h)
+        self._mark("F3 dispatch || F4 GEMM1 (chunked)")
+        L.moe_expert_ffn_down_combine(c, self.layout, self.w_down, self.g_u_h, self.ys, self.gates,
+                                      self.dest_row, y_extra, self.y)
+        self._mark("F4 GEMM2 + F5 combine + F6")
+        return self.y
+
+    def _backward_chunked(self, dy, accumulate, ranges):
+        c, T = self.ctx, self.dims.T_local
+        b0, e0 = ranges[0]
+        if self.fs and self.overlap:
+            self._concurrent(lambda s: L.moe_combine_bwd_range(c, dy, self.gates, self.dest_row,
+                                                               self.ys, self.layout, self.dgates,
+                                                               self.dout_r, b0, e0, stream=s),
+                             lambda s: L.moe_expert_ffn_bwd(c, self.x, self.rows_T, 1, T, self.fs,
+                                                            self.w_gu_s, self.w_down_s,
+                                                            self.g_u_h_s, dy, self.dgu_s,
+                                                            self.dx_s, self.dw_gu_s,
+                                                            self.dw_down_s, accumulate, stream=s))
+        else:
+            L.moe_combine_bwd_range(c, dy, self.gates, self.dest_row, self.ys, self.layout,
+                                    self.dgates, self.dout_r, b0, e0)
+            if self.fs:
+                L.moe_expert_ffn_bwd(c, self.x, self.rows_T, 1, T, self.fs, self.w_gu_s,
+                                     self.w_down_s, self.g_u_h_s, dy, self.dgu_s, self.dx_s,
+                                     self.dw_gu_s, self.dw_down_s, accumulate)
+        self._mark("B6+B5 combine_bwd (range 0)")
+        for (pb, pe), (b, e) in zip(ranges[:-1], ranges[1:]):
+            self._concurrent(
+                lambda s, b=b, e=e: L.moe_combine_bwd_range(c, dy, self.gates, self.dest_row,
+                                                            self.ys, self.layout, self.dgates,
+                                                            self.dout_r, b, e, stream=s),
+                lambda s, pb=pb, pe=pe: L.moe_expert_ffn_bwd_dh(c, self.layout, pb, pe,
+                                                                self.w_down, self.g_u_h,
+                                                                self.dout_r, self.dgu, stream=s))
+        L.moe_expert_ffn_bwd_dh(c, self.layout, ranges[-1][0], ranges[-1][1], self.w_down,
+                                self.g_u_h, self.dout_r, self.dgu)
+        self._mark("B5 combine_bwd || B4 dgrad-1 (chunked)")
+        L.moe_expert_ffn_bwd_dx_dispatch(c, self.xr, self.layout, self.w_gu, self.g_u_h,
+                                         self.dout_r, self.dgu, self.dxs, self.dw_gu, self.dw_down,
+                                         accumulate)
+        self._mark("B4 dgrad-2 + B3 dispatch_bwd + wgrad")
+        return self._backward_tail(dy, accumulate, True)
+
     # ------------------------------------------------------------------ backward
     def backward(self, dy: torch.Tensor, accumulate: bool = False) -> torch.Tensor:
         """dy [T_local, d] bf16 -> dx [T_local, d] bf16; fills dw_r, dw_gu, dw_down
         (and dw_gu_s, dw_down_s) as fp32 per-rank gradients."""
         c = self.ctx
         f, T = self.dims.f, self.dims.T_local
+        ranges = self._ranges()
+        if ranges:
+            return self._backward_chunked(dy, accumulate, ranges)
         shared_done = False
         if self.fs and self.overlap:
             # shared-expert backward (needs only dy) beside the combine_bwd all-to-all
@@ -241,6 +329,11 @@ class MoELayer:
             self._mark("B4 expert ffn_bwd")
             L.moe_dispatch_bwd(c, self.dxr, self.layout, self.dxs)
             self._mark("B3 dispatch_bwd")
+        return self._backward_tail(dy, accumulate, shared_done)
+
+    def _backward_tail(self, dy, accumulate, shared_done):
+        """Shared experts (if not yet done), route / router backward and permute backward."""
+        c, T = self.ctx, self.dims.T_local
         dx_extra = self.dx_s if self.fs else None
         if self.fs and not shared_done:
             L.moe_expert_ffn_bwd(c, self.x, self.rows_T, 1, T, self.fs, self.w_gu_s, self.w_down_s,
@@ -361,6 +454,8 @@ class MoELayer:
         if fwd:
             # router GEMM, route, permute (4), dispatch (1 fused launch), ffn (2), combine (2)
             n += 1 + 1 + 4 + 1 + 2 + 2 + (2 if self.fs else 0)
+        extra = 2 * (len(self._ranges()) - 1) if self._ranges() else 0   # per range: a2a + GEMM
+        n += extra * (int(fwd) + int(bwd))
         if bwd:
             # combine_bwd (1), ffn_bwd (4), dispatch_bwd (1), route_bwd,
             # router bwd (hi/lo split, split-K dW_r GEMM, partial sum; k = 1 adds the

@@ -45,6 +45,7 @@ def main():
     ap.add_argument("--stepwise", action="store_true", help="unfused step-by-step calls")
     ap.add_argument("--rebalance", action="store_true",
                     help="observe loads, run Alg. 2 (moe_rebalance) and migrate before checking")
+    ap.add_argument("--chunks", type=int, default=None, help="MoELayer.chunks (NEXT-1 overlap)")
     ap.add_argument("--graph", action="store_true",
                     help="also replay the step from a CUDA graph (device-side collective epoch)")
     args = ap.parse_args()
@@ -58,6 +59,8 @@ def main():
 
     layer = build_layer(cfg, ep_size=ep, ep_rank=rank, device=local)
     layer.fused = not args.stepwise
+    if args.chunks is not None:
+        layer.chunks = args.chunks
     T_r = cfg.T // ep
     x = synth.tokens(cfg).cuda()[rank * T_r:(rank + 1) * T_r].contiguous()
     dy = synth.grad_output(cfg).cuda()[rank * T_r:(rank + 1) * T_r].contiguous()
@@ -73,6 +76,17 @@ def main():
         dx = layer.backward(dy).clone()
         outs.append((y, dx, layer.dw_gu.clone()))
     graph_ok = True
+    if args.chunks is None or args.chunks > 1:
+        # the chunked overlap (default) and the unchunked calls give bit-identical results
+        saved = layer.chunks
+        layer.chunks = 1
+        y1 = layer.forward(x).clone()
+        dx1 = layer.backward(dy).clone()
+        graph_ok &= bool(torch.equal(y1, outs[0][0]) and torch.equal(dx1, outs[0][1]) and
+                         torch.equal(layer.dw_gu, outs[0][2]))
+        layer.chunks = saved
+        layer.forward(x)
+        layer.backward(dy)
     if args.graph:
         # replays must match the eager step bit for bit (every replay is a fresh exchange), and
         # a replay on new input contents must match the eager step on those contents

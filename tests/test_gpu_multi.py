@@ -87,3 +87,15 @@ def test_layer_one_expert_per_rank(extra):
     res = run_worker(4, "el1", 29990 + len(extra) + (3 if "--graph" in extra else 0), extra)
     print(res)
     assert res["ok"], res
+
+
+@pytest.mark.parametrize("nproc", [2, 4])
+@pytest.mark.parametrize("config", ["mixtral_small", "v3_small_zipf"])
+def test_layer_ep_parity_unchunked(nproc, config):
+    """chunks = 1: one dispatch / combine_bwd launch each, no GEMM beside them (the default
+    chunked overlap is covered by the other tests, which also check it is bit-identical)."""
+    if n_gpus() < nproc:
+        pytest.skip(f"needs {nproc} GPUs")
+    res = run_worker(nproc, config, 29960 + nproc * 4 + CONFIGS.index(config), ("--chunks", "1"))
+    print(res)
+    assert res["ok"], res
