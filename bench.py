@@ -59,6 +59,10 @@ def parse():
                          "the headline uses the faster of eager / graph")
     ap.add_argument("--gemm-compare", action="store_true",
                     help="expert FFN GEMMs: libmoe vs cuBLAS (torch) on one GPU, no bench line")
+    ap.add_argument("--gemm-experts", type=int, default=0,
+                    help="--gemm-compare: experts on the GPU (default: the config's E)")
+    ap.add_argument("--gemm-rows", type=int, default=0,
+                    help="--gemm-compare: rows per expert (default: T*k/E)")
     ap.add_argument("--profile-steps", type=int, default=0,
                     help="run only this many steps without timing (for ncu)")
     return ap.parse_args()
@@ -676,6 +680,10 @@ def run_gemm_compare(args):
     cfg = synth.CONFIGS[args.config]
     E, d, f = cfg.E, cfg.d, cfg.f
     rows = cfg.T * cfg.k // E
+    if args.gemm_experts:   # one EP rank's share: E_l experts of `rows` rows
+        E = args.gemm_experts
+        rows = args.gemm_rows or rows
+        cfg = synth.MoEConfig(f"{cfg.name}_E{E}_r{rows}", T=rows * E, d=d, E=E, k=1, f=f, cf=0.0)
     R = rows * E
     dev = torch.device("cuda:0")
     shape = L.make_shape(cfg.T, d, E, cfg.k, f, 0, 0.0, 1, 0)

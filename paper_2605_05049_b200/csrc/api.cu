@@ -42,6 +42,8 @@ struct moe_ctx {
   int32_t* d_expert_at = nullptr; // [E] global slot -> expert
   int gemm_sms = 0;               // SM budgets (0 = all): a GEMM and a transfer running
   int comm_sms = 0;               //   concurrently on two streams use disjoint SMs
+  float* d_sk_ws = nullptr;       // stream-K partial accumulators (expert GEMMs)
+  int* d_sk_flags = nullptr;      // [2][kStreamKSlots] ready / consumed counters
 };
 
 namespace {
@@ -172,6 +174,19 @@ int gemm_pair() {
   return v;
 }
 
+// Stream-K tail for the expert GEMMs (the last partial wave cut into k-chunks spread over
+// every cluster, gemm.cu make_sched) when MOE_STREAM_K=1, read at every call.  Off by
+// default: measured slower on B200 (Mixtral EP=8 shapes: GEMM2 161 -> 206 us) -- the
+// finisher's fp32 partial reads and the extra pipeline fills cost more than the idle
+// clusters of the plain last wave (profiles/r01/README.md).
+void use_stream_k(const moe_ctx* c, moe::GemmProblem& g) {
+  const char* e = getenv("MOE_STREAM_K");
+  if (!(e && e[0] == '1')) return;
+  g.sk_ws = c->d_sk_ws;
+  g.sk_ws_bytes = moe::kStreamKWorkspaceBytes;
+  g.sk_flags = c->d_sk_flags;
+}
+
 int pick_bn(int n) {
   if (n % 256 == 0) return 256;
   if (n % 128 == 0) return 128;
@@ -277,6 +292,9 @@ moe_status moe_ctx_create(moe_ctx** out, const moe_shape* shape, int device, siz
     if (e == cudaSuccess)
       e = cudaMemcpy(c->d_expert_at, ident.data(), shape->E * sizeof(int32_t), cudaMemcpyHostToDevice);
   }
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_sk_ws, moe::kStreamKWorkspaceBytes);
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_sk_flags, 2 * moe::kStreamKSlots * sizeof(int));
+  if (e == cudaSuccess) e = cudaMemset(c->d_sk_flags, 0, 2 * moe::kStreamKSlots * sizeof(int));
   if (e == cudaSuccess && EP > 1) e = cudaIpcGetMemHandle(&c->handle, c->heap);
   if (e != cudaSuccess) {
     moe_ctx_destroy(c);
@@ -388,6 +406,8 @@ moe_status moe_ctx_destroy(moe_ctx* c) {
   cudaFree(c->heap);
   cudaFree(c->d_err);
   cudaFree(c->d_done);
+  cudaFree(c->d_sk_ws);
+  cudaFree(c->d_sk_flags);
   cudaFree(c->d_scratch);
   cudaFree(c->d_rows_T);
   cudaFree(c->d_dl_split);
@@ -556,6 +576,7 @@ moe_status ffn_up(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows, int
   g1.pair = gemm_pair();
   g1.max_ctas = c->gemm_sms;
   g1.out = g_u_h; g1.ld_out = 3 * static_cast<int64_t>(f); g1.f = f;
+  use_stream_k(c, g1);
   return cuda_status(moe::launch_grouped_gemm(g1, st(s)));
 }
 
@@ -578,6 +599,7 @@ moe_status ffn_down(moe_ctx* c, const int32_t* group_rows, int32_t n_groups, int
   g2.pair = gemm_pair();
   g2.max_ctas = c->gemm_sms;
   g2.out = out ? static_cast<void*>(out) : static_cast<void*>(g_u_h); g2.ld_out = d;
+  use_stream_k(c, g2);
   if (sc) {
     g2.scatter = 1; g2.scatter_off = sc->off; g2.scatter_layout = sc->layout; g2.comm = sc->comm;
   }
@@ -622,6 +644,7 @@ moe_status ffn_bwd_dh(moe_ctx* c, const int32_t* group_rows, int32_t g0, int32_t
   a.pair = gemm_pair();
   a.max_ctas = c->gemm_sms;
   a.out = dgu; a.ld_out = 2 * F; a.aux = g_u_h; a.ld_aux = 3 * F; a.f = f;
+  use_stream_k(c, a);
   return cuda_status(moe::launch_grouped_gemm(a, st(s)));
 }
 
@@ -653,6 +676,7 @@ moe_status ffn_bwd_dx(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows,
   b.pair = gemm_pair();
   b.max_ctas = c->gemm_sms;
   b.out = dxr ? static_cast<void*>(dxr) : const_cast<moe_bf16*>(dgu); b.ld_out = d;
+  use_stream_k(c, b);
   if (sc) {  // dX rows go straight back to their source ranks (dispatch_bwd fused)
     b.scatter = 1; b.scatter_off = sc->off; b.scatter_layout = sc->layout; b.comm = sc->comm;
   }

@@ -52,7 +52,15 @@ struct GemmProblem {
   int64_t scatter_off = 0;
   const int32_t* scatter_layout = nullptr;  // counts_all [EP x E]
   const struct CommArgs* comm = nullptr;
+  // stream-K tail for the M-grouped epilogues (SwiGLU, BF16, DSwiGLU); null = off
+  float* sk_ws = nullptr;
+  int64_t sk_ws_bytes = 0;
+  int* sk_flags = nullptr;   // [2][kStreamKSlots] int32 (ready, consumed), zero between launches
 };
+// stream-K workspace: up to 336 partial accumulators of 128 x 256 fp32 (168 of 256 x 256):
+// a tail of rem < 3/4 of the clusters cut into <= 4 chunks has <= 3 rem partials
+constexpr int kStreamKSlots = 336;
+constexpr int64_t kStreamKWorkspaceBytes = static_cast<int64_t>(kStreamKSlots) * 128 * 256 * 4;
 
 cudaError_t launch_grouped_gemm(const GemmProblem& p, cudaStream_t stream);
 int num_sms();

@@ -18,11 +18,12 @@ def n_gpus():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-def run_worker(nproc, config, port, extra=()):
+def run_worker(nproc, config, port, extra=(), env=None):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr=127.0.0.1", f"--master-port={port}",
            os.path.join(ROOT, "tests", "mp_layer_worker.py"), "--config", config, *extra]
-    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT,
+                       env=None if env is None else {**os.environ, **env})
     lines = [l for l in p.stdout.splitlines() if l.startswith("{")]
     assert p.returncode == 0 and lines, f"worker failed:\n{p.stdout[-3000:]}\n{p.stderr[-3000:]}"
     return json.loads(lines[-1])
@@ -91,11 +92,14 @@ def test_layer_one_expert_per_rank(extra):
 
 @pytest.mark.parametrize("nproc", [2, 4])
 @pytest.mark.parametrize("config", ["mixtral_small", "v3_small_zipf"])
-def test_layer_ep_parity_unchunked(nproc, config):
-    """chunks = 1: one dispatch / combine_bwd launch each, no GEMM beside them (the default
-    chunked overlap is covered by the other tests, which also check it is bit-identical)."""
+@pytest.mark.parametrize("stream_k", ["1", "0"])
+def test_layer_ep_parity_chunked(nproc, config, stream_k):
+    """NEXT-1 chunked overlap (chunks = 4: dispatch / combine_bwd per owner-slot range beside the
+    previous range's GEMM) matches the oracle; with MOE_STREAM_K=0 it is also bit-identical to
+    the unchunked calls (checked inside the worker)."""
     if n_gpus() < nproc:
         pytest.skip(f"needs {nproc} GPUs")
-    res = run_worker(nproc, config, 29960 + nproc * 4 + CONFIGS.index(config), ("--chunks", "1"))
+    res = run_worker(nproc, config, 30100 + nproc * 10 + CONFIGS.index(config) + 40 * int(stream_k),
+                     ("--chunks", "4"), env={"MOE_STREAM_K": stream_k})
     print(res)
     assert res["ok"], res
