@@ -154,6 +154,44 @@ def gemm_traffic(config, world):
         return None
 
 
+def layer_roofline(layer, cfg, peaks, nvl_gbs=900.0):
+    """SURVEY.md §8(d) d.3 serial layer roofline from the realised routing (the layout
+    record's [EP x E] count matrix and the expert placement, identical on every rank):
+    sum over the steps of max(F/pi, B_hbm/beta_hbm, B_nvl/beta_nvl) on the hottest rank,
+    pi = measured sustained bf16, beta_hbm = measured HBM copy bandwidth, beta_nvl = 900 GB/s
+    per direction.  Steps: router GEMM (fwd + 2 bwd), permute / unpermute / permute_bwd /
+    combine_bwd's dO writes (HBM), 4 all-to-alls (NVLink, max of egress and ingress), expert
+    GEMMs fwd + bwd (18 d f per routed row, shared experts on the local tokens)."""
+    EP, E, d, f, k = layer.dims.ep_size, cfg.E, cfg.d, cfg.f, cfg.k
+    T_r = layer.dims.T_local
+    cm = layer.layout[:EP * E].view(EP, E).to(torch.int64).cpu()
+    owner = torch.tensor([s // layer.E_l for s in layer.placement])
+    pi = peaks["bf16_sustained"] * 1e12
+    bh = peaks["hbm"] * 1e9
+    bn = nvl_gbs * 1e9
+    row = d * 2
+    per_rank = []
+    for r in range(EP):
+        mine = owner == r
+        recv = int(cm[:, mine].sum())
+        send = int(cm[r].sum())
+        egress = int(cm[r, ~mine].sum()) * row
+        ingress = int(cm[:, mine].sum() - cm[r, mine].sum()) * row
+        t = 3 * 2 * T_r * d * E / pi                          # router fwd + dgrad + wgrad
+        t += 2 * (T_r * row + send * row) / bh                # permute, permute_bwd
+        t += 2 * (send * row + T_r * row) / bh                # unpermute, combine_bwd dO rows
+        t += 4 * max(egress, ingress) / bn                    # dispatch, combine, their twins
+        t += 18 * recv * d * f / pi                           # expert GEMMs fwd + bwd
+        if cfg.E_s:
+            t += 18 * T_r * d * cfg.E_s * f / pi
+        per_rank.append(t * 1e3)
+    hot = max(range(EP), key=lambda r: per_rank[r])
+    return {"serial_ms": per_rank[hot], "hot_rank": hot,
+            "per_rank_ms": [round(v, 4) for v in per_rank],
+            "peaks": {"bf16_tflops": peaks["bf16_sustained"], "hbm_gbs": peaks["hbm"],
+                      "nvlink_gbs_per_direction": nvl_gbs}}
+
+
 def realised_gemm_flops(layer, cfg):
     """Algorithmic GEMM FLOPs of one fwd+bwd on this rank from the realised routing:
     6 * rows * d * f (fwd) + 12 * rows * d * f (bwd), plus the shared experts."""
@@ -238,17 +276,21 @@ def run_ours(args):
         if dist is not None:
             dist.barrier()
 
-    # GEMM-region events (the dominant kernel family: 6 grouped-GEMM launches per step)
+    # Region events inside the timed steps, on the stream each call is issued on: the
+    # grouped-GEMM family (the dominant kernel: 6 launches per step), the permute (HBM) and
+    # the two forward-pattern all-to-alls (NVLink)
     gemm_ev = []
+    region_ev = {"permute": [], "dispatch": [], "combine_bwd": []}
     import paper_2605_05049_b200.layer as layer_mod
 
-    def timed(fn):
+    def timed(fn, bucket=None):
         def wrapper(*a, **kw):
+            st = kw.get("stream") or stream
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s.record(stream)
+            s.record(st)
             fn(*a, **kw)
-            e.record(stream)
-            gemm_ev.append((s, e))
+            e.record(st)
+            (gemm_ev if bucket is None else region_ev[bucket]).append((s, e))
         return wrapper
 
     for _ in range(args.warmup):
@@ -288,9 +330,14 @@ def run_ours(args):
     hooked = ["moe_expert_ffn", "moe_expert_ffn_bwd", "moe_expert_ffn_combine",
               "moe_expert_ffn_bwd_dispatch", "moe_expert_ffn_up", "moe_expert_ffn_down_combine",
               "moe_expert_ffn_bwd_dh", "moe_expert_ffn_bwd_dx_dispatch"]
-    originals = {n: getattr(layer_mod.L, n) for n in hooked}
+    buckets = {"moe_permute": "permute", "moe_dispatch": "dispatch",
+               "moe_dispatch_range": "dispatch", "moe_combine_bwd": "combine_bwd",
+               "moe_combine_bwd_range": "combine_bwd"}
+    originals = {n: getattr(layer_mod.L, n) for n in hooked + list(buckets)}
     for n in hooked:
         setattr(layer_mod.L, n, timed(originals[n]))
+    for n, b in buckets.items():
+        setattr(layer_mod.L, n, timed(originals[n], b))
     clocks = ClockSampler(local)
     barrier()
     torch.cuda.synchronize()
@@ -305,10 +352,12 @@ def run_ours(args):
     torch.cuda.synchronize()
     barrier()
     clk = clocks.stop()
-    for n in hooked:
-        setattr(layer_mod.L, n, originals[n])
+    for n, fn in originals.items():
+        setattr(layer_mod.L, n, fn)
     layer.ctx.check_device_error()
     ms = t0.elapsed_time(t1) / args.steps
+    region_ms = {b: sum(a.elapsed_time(z) for a, z in ev) / args.steps
+                 for b, ev in region_ev.items()}
     eager_ms = ms
     graph_ms = None
     if args.graph:
@@ -385,10 +434,26 @@ def run_ours(args):
     barrier()
     e2e_ms = e0.elapsed_time(e1) / args.steps
 
-    vals = torch.tensor([ms, e2e_ms, gemm_ms, graph_ms or 0.0], dtype=torch.float64, device=dev)
+    # byte counts of this rank's permute and forward-pattern all-to-alls (realised routing)
+    EPw, Ew, row_b = world, cfg.E, cfg.d * 2
+    cmat = layer.layout[:EPw * Ew].view(EPw, Ew).to(torch.int64).cpu()
+    own = torch.tensor([sl // layer.E_l for sl in layer.placement]) == rank
+    send_rows = int(cmat[rank].sum())
+    a2a_bytes = {"egress": int(cmat[rank, ~own].sum()) * row_b,
+                 "ingress": int(cmat[:, own].sum() - cmat[rank, own].sum()) * row_b}
+    permute_bytes = T_r * row_b + send_rows * row_b
+    roof = layer_roofline(layer, cfg, measured_peaks())
+    vals = torch.tensor([ms, e2e_ms, gemm_ms, graph_ms or 0.0, region_ms["permute"]],
+                        dtype=torch.float64, device=dev)
+    # a collective's kernel time on a rank includes waiting for the later ranks; the rank that
+    # arrives last waits least, so the MIN over ranks is the transfer's own duration
+    a2a_t = torch.tensor([region_ms["dispatch"], region_ms["combine_bwd"]], dtype=torch.float64,
+                         device=dev)
     if dist is not None:
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
-    ms, e2e_ms, gemm_ms_max, graph_ms = vals.tolist()
+        dist.all_reduce(a2a_t, op=dist.ReduceOp.MIN)
+    ms, e2e_ms, gemm_ms_max, graph_ms, perm_ms = vals.tolist()
+    disp_ms, cbwd_ms = a2a_t.tolist()
     eager_ms = ms
     use_graph = bool(args.graph and graph_ms < ms)
     if use_graph:
@@ -432,6 +497,30 @@ def run_ours(args):
         "e2e": {"value": tokens / (e2e_ms * 1e-3), "unit": UNIT,
                 "h2d_bytes_per_step": int(x_h.numel() * 2 + dy_h.numel() * 2),
                 "d2h_bytes_per_step": int(y_h.numel() * 2 + dx_h.numel() * 2)},
+        "layer_roofline": {
+            **roof, "frac": roof["serial_ms"] / ms,
+            "definition": "SURVEY.md 8(d) d.3: sum over steps of max(F/pi, B_hbm/beta_hbm, "
+                          "B_nvl/beta_nvl) on the hottest rank, realised routing",
+        },
+        "secondary_rooflines": {
+            "permute": {"bound": "hbm", "ms": perm_ms,
+                        "achieved_gbs": permute_bytes / (perm_ms * 1e-3) / 1e9 if perm_ms else None,
+                        "peak_gbs": peaks["hbm"], "bytes_rank0": permute_bytes,
+                        "note": "4 kernels (histogram, scan, rank, scatter); algorithmic bytes = "
+                                "x read + xs write"},
+            "dispatch": {"bound": "nvlink" if world > 1 else "hbm (EP=1: local copy)",
+                         "ms": disp_ms, "egress_bytes_rank0": a2a_bytes["egress"],
+                         "ingress_bytes_rank0": a2a_bytes["ingress"],
+                         "achieved_gbs_per_direction": max(a2a_bytes.values()) / (disp_ms * 1e-3) / 1e9
+                         if disp_ms and world > 1 else None,
+                         "peak_gbs_per_direction": 900.0,
+                         "note": "one launch incl. the counts handshake and padding zeroing; "
+                                 "min over ranks of the in-step kernel time"},
+            "combine_bwd": {"ms": cbwd_ms,
+                            "achieved_gbs_per_direction": max(a2a_bytes.values()) / (cbwd_ms * 1e-3) / 1e9
+                            if cbwd_ms and world > 1 else None,
+                            "note": "forward pattern + gate multiply + dgates dot products"},
+        },
         "gpu_launches": layer.kernel_launches() * args.steps,
         "clocks": clk,
         "roofline": {
