@@ -244,6 +244,8 @@ __global__ void forward_transfer_kernel(CommArgs a, int32_t* __restrict__ layout
                                         const uint16_t* __restrict__ dy,
                                         const uint16_t* __restrict__ ys,
                                         float* __restrict__ dgates, int s0, int s1) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ FwdTables tb;
   __shared__ SegTable sg;
   a.epoch = load_epoch(a);
@@ -358,6 +360,8 @@ __global__ void forward_transfer_kernel(CommArgs a, int32_t* __restrict__ layout
 // Reverse pattern: owner receive rows -> the same send-layout row on the source.
 __global__ void reverse_transfer_kernel(CommArgs a, const int32_t* __restrict__ layout,
                                         const uint16_t* __restrict__ src, int64_t dst_off) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ int32_t s_seg[kMaxE + 1];
   __shared__ int32_t s_pre[MOE_MAX_EP][kMaxE];   // rows of my slot el's expert from sources < r
   __shared__ int32_t s_soff[MOE_MAX_EP][kMaxE];  // send-layout offset of that expert on source r
@@ -418,6 +422,8 @@ __global__ void reverse_transfer_kernel(CommArgs a, const int32_t* __restrict__ 
 // Waits for every rank's data flag of this epoch (the GEMM-fused reverse all-to-alls).
 // The GEMM that preceded it published load_epoch(a) (the counter is not advanced until here).
 __global__ void wait_flags_kernel(CommArgs a, int slot) {
+  pdl_wait();
+  pdl_trigger();
   a.epoch = load_epoch(a);
   wait_all(a, slot);
   commit_epoch(a);
@@ -449,7 +455,7 @@ extern "C" int moe_debug_trace(unsigned long long* out) {   // [64][8]
 #endif
 
 cudaError_t launch_wait_flags(const CommArgs& a, int slot, cudaStream_t s) {
-  wait_flags_kernel<<<1, 32, 0, s>>>(a, slot);
+  launch_k(wait_flags_kernel, dim3(1), dim3(32), 0, s, a, slot);
   return cudaGetLastError();
 }
 
@@ -457,9 +463,9 @@ cudaError_t launch_dispatch(const CommArgs& a, const int32_t* counts, int32_t* l
                             int64_t recv_rows_cap, const uint16_t* src, int64_t dst_off,
                             uint16_t* local_dst, int s0, int s1, cudaStream_t s) {
   const int64_t rows = a.T * a.k * (s1 - s0) / a.E_l + a.T;   // range share (+ slack)
-  forward_transfer_kernel<0><<<transfer_blocks(a, rows), 512, transfer_smem(a), s>>>(
-      a, layout, counts, recv_rows_cap, src, dst_off, local_dst, nullptr, nullptr, nullptr, nullptr,
-      nullptr, s0, s1);
+  launch_k(forward_transfer_kernel<0>, dim3(transfer_blocks(a, rows)), dim3(512), transfer_smem(a),
+      s, a, layout, counts, recv_rows_cap, src, dst_off, local_dst, nullptr, nullptr, nullptr,
+      nullptr, nullptr, s0, s1);
   return cudaGetLastError();
 }
 
@@ -467,16 +473,17 @@ cudaError_t launch_combine_bwd_transfer(const CommArgs& a, int32_t* layout, int6
                                         uint16_t* local_dst, const int32_t* dest_row,
                                         const float* gates, const uint16_t* dy, const uint16_t* ys,
                                         float* dgates, int s0, int s1, cudaStream_t s) {
-  forward_transfer_kernel<1><<<transfer_blocks(a, a.T * a.k), 512, transfer_smem(a), s>>>(
-      a, layout, nullptr, 0, nullptr, dst_off, local_dst, dest_row, gates, dy, ys, dgates, s0, s1);
+  launch_k(forward_transfer_kernel<1>, dim3(transfer_blocks(a, a.T * a.k)), dim3(512),
+      transfer_smem(a), s, a, layout, nullptr, 0, nullptr, dst_off, local_dst, dest_row, gates, dy,
+      ys, dgates, s0, s1);
   return cudaGetLastError();
 }
 
 cudaError_t launch_reverse_transfer(const CommArgs& a, const int32_t* layout, const uint16_t* src,
                                     int64_t dst_off, cudaStream_t s) {
   // receive rows <= EP * T * k
-  reverse_transfer_kernel<<<transfer_blocks(a, a.T * a.k * a.ep), 512, transfer_smem(a), s>>>(
-      a, layout, src, dst_off);
+  launch_k(reverse_transfer_kernel, dim3(transfer_blocks(a, a.T * a.k * a.ep)), dim3(512),
+      transfer_smem(a), s, a, layout, src, dst_off);
   return cudaGetLastError();
 }
 

@@ -54,6 +54,12 @@ MOE_DEVINL uint64_t ld_acquire_sys(const uint64_t* p) {
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+// Programmatic dependent launch (PDL): every libmoe kernel is launched with programmatic
+// stream serialization, waits for the previous grid (completion + memory visibility) before
+// touching any input, and immediately lets the next grid launch, so the next kernel's launch
+// latency and block scheduling overlap this kernel's run instead of following its tail.
+MOE_DEVINL void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+MOE_DEVINL void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 MOE_DEVINL uint64_t globaltimer_ns() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

@@ -238,6 +238,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmC, const KParams p) {
+  pdl_wait();
+  pdl_trigger();
   using C = Cfg<BN, PAIR>;
   constexpr bool KGROUPED = (EPI == kEpiF32Group);
   constexpr int TILE_M = kBM * PAIR;
@@ -905,15 +907,14 @@ cudaError_t launch_impl(const GemmProblem& g, cudaStream_t stream) {
   if (PAIR == 1) {
     const int grid = (g.max_ctas > 0 && g.max_ctas < num_sms()) ? g.max_ctas : num_sms();
     if (grid > kMaxClusters) kp.stream_k = 0;
-    kern<<<grid, kThreads, C::SMEM, stream>>>(ta, tb, tc, kp);
-    return cudaGetLastError();
+    return launch_k(kern, dim3(grid), dim3(kThreads), C::SMEM, stream, ta, tb, tc, kp);
   }
   cudaLaunchConfig_t cfg;
   memset(&cfg, 0, sizeof(cfg));
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = 2;
   attr[0].val.clusterDim.y = 1;
@@ -934,6 +935,7 @@ cudaError_t launch_impl(const GemmProblem& g, cudaStream_t stream) {
   int clusters = max_clusters;
   if (g.max_ctas > 0 && g.max_ctas / 2 < clusters) clusters = g.max_ctas / 2 > 0 ? g.max_ctas / 2 : 1;
   cfg.gridDim = dim3(2 * clusters);
+  cfg.numAttrs = 1 + pdl_attr(&attr[1]);
   if (clusters > kMaxClusters) kp.stream_k = 0;
   return cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, kp);
 }

@@ -23,6 +23,8 @@ __device__ __forceinline__ int expert_of(const int32_t* idx, int64_t a, int64_t 
 // Pass 1: per-chunk expert histogram.
 __global__ void hist_kernel(const int32_t* __restrict__ idx, int64_t T, int k, int E,
                             int32_t* __restrict__ chunk_hist /*[nchunks][E]*/) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ int32_t s_hist[];
   for (int e = threadIdx.x; e < E; e += blockDim.x) s_hist[e] = 0;
   __syncthreads();
@@ -37,6 +39,8 @@ __global__ void hist_kernel(const int32_t* __restrict__ idx, int64_t T, int k, i
 // counts and off = exclusive scan of counts.  One block, thread per expert.
 __global__ void scan_kernel(int32_t* __restrict__ chunk_hist, int nchunks, int E, int64_t C,
                             int32_t* __restrict__ counts, int32_t* __restrict__ off) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ int32_t s_cnt[1024];
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
     int32_t run = 0;
@@ -64,6 +68,8 @@ __global__ void scan_kernel(int32_t* __restrict__ chunk_hist, int nchunks, int E
 __global__ void rank_kernel(const int32_t* __restrict__ idx, int64_t T, int k, int E, int64_t C,
                             const int32_t* __restrict__ chunk_base, const int32_t* __restrict__ off,
                             int32_t* __restrict__ dest_row) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ int32_t s_wcnt[];  // [32 warps][E]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < 32 * E; i += blockDim.x) s_wcnt[i] = 0;
@@ -95,6 +101,8 @@ __global__ void rank_kernel(const int32_t* __restrict__ idx, int64_t T, int k, i
 // Pass 4: warp per token; read x_t once per 512-byte chunk, write it to each kept row.
 __global__ void scatter_kernel(const uint16_t* __restrict__ x, const int32_t* __restrict__ dest_row,
                                int64_t T, int d, int k, uint16_t* __restrict__ xs) {
+  pdl_wait();
+  pdl_trigger();
   const int lane = threadIdx.x & 31;
   const int64_t t = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   if (t >= T) return;
@@ -129,6 +137,8 @@ __global__ void gather_sum_kernel(const uint16_t* __restrict__ rows, const float
                                   const int32_t* __restrict__ dest_row, const float* __restrict__ extra_f32,
                                   const uint16_t* __restrict__ extra_bf16, int64_t T, int d, int k,
                                   uint16_t* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const int lane = threadIdx.x & 31;
   const int64_t t = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   if (t >= T) return;
@@ -174,6 +184,8 @@ __global__ void gather_sum_router_kernel(const uint16_t* __restrict__ dxs,
                                          const uint16_t* __restrict__ w_r,
                                          const uint16_t* __restrict__ extra_bf16, int64_t T, int d,
                                          int E, int k, uint16_t* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const int lane = threadIdx.x & 31;
   const int64_t t = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   if (t >= T) return;
@@ -207,6 +219,8 @@ __global__ void gather_sum_router_kernel(const uint16_t* __restrict__ dxs,
 // dw[e, c] (+)= sum_s part[s][e][c] + part[s][Ep + e][c]  (hi and lo halves), fixed order.
 __global__ void sum_partials_kernel(const float* __restrict__ part, int S, int E, int Ep, int d,
                                     float* __restrict__ dw, int accumulate) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= static_cast<int64_t>(E) * d) return;
   const int64_t e = i / d, c = i % d;
@@ -226,16 +240,16 @@ cudaError_t launch_permute_bwd_router(const uint16_t* dxs, const int32_t* dest_r
                                       int d, int E, int k, uint16_t* dx, cudaStream_t s) {
   if (T == 0) return cudaSuccess;
   const int threads = 256;
-  gather_sum_router_kernel<<<static_cast<unsigned>((T * 32 + threads - 1) / threads), threads, 0, s>>>(
-      dxs, dest_row, topk_idx, dlogits, w_r, dx_extra, T, d, E, k, dx);
+  launch_k(gather_sum_router_kernel, dim3(static_cast<unsigned>((T * 32 + threads - 1) / threads)),
+      dim3(threads), 0, s, dxs, dest_row, topk_idx, dlogits, w_r, dx_extra, T, d, E, k, dx);
   return cudaGetLastError();
 }
 
 cudaError_t launch_sum_partials(const float* part, int S, int E, int Ep, int d, float* dw,
                                 int accumulate, cudaStream_t s) {
   const int64_t n = static_cast<int64_t>(E) * d;
-  sum_partials_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(part, S, E, Ep, d, dw,
-                                                                          accumulate);
+  launch_k(sum_partials_kernel, dim3(static_cast<unsigned>((n + 255) / 256)), dim3(256), 0, s, part,
+      S, E, Ep, d, dw, accumulate);
   return cudaGetLastError();
 }
 
@@ -255,18 +269,20 @@ cudaError_t launch_permute(const uint16_t* x, const int32_t* topk_idx, int64_t T
     cudaMemsetAsync(counts, 0, sizeof(int32_t) * E, s);
     return cudaGetLastError();
   }
-  hist_kernel<<<nchunks, kChunk, E * sizeof(int32_t), s>>>(topk_idx, T, k, E, chunk_hist);
-  scan_kernel<<<1, 256, 0, s>>>(chunk_hist, nchunks, E, C, counts, off);
+  launch_k(hist_kernel, dim3(nchunks), dim3(kChunk), E * sizeof(int32_t), s, topk_idx, T, k, E,
+      chunk_hist);
+  launch_k(scan_kernel, dim3(1), dim3(256), 0, s, chunk_hist, nchunks, E, C, counts, off);
   const size_t smem = static_cast<size_t>(32) * E * sizeof(int32_t);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
   }
-  rank_kernel<<<nchunks, kChunk, smem, s>>>(topk_idx, T, k, E, C, chunk_hist, off, dest_row);
+  launch_k(rank_kernel, dim3(nchunks), dim3(kChunk), smem, s, topk_idx, T, k, E, C, chunk_hist, off,
+      dest_row);
   const int threads = 256;
-  scatter_kernel<<<static_cast<unsigned>((T * 32 + threads - 1) / threads), threads, 0, s>>>(
-      x, dest_row, T, d, k, xs);
+  launch_k(scatter_kernel, dim3(static_cast<unsigned>((T * 32 + threads - 1) / threads)),
+      dim3(threads), 0, s, x, dest_row, T, d, k, xs);
   return cudaGetLastError();
 }
 
@@ -275,8 +291,8 @@ cudaError_t launch_permute_bwd(const uint16_t* dxs, const int32_t* dest_row, con
                                cudaStream_t s) {
   if (T == 0) return cudaSuccess;
   const int threads = 256;
-  gather_sum_kernel<false><<<static_cast<unsigned>((T * 32 + threads - 1) / threads), threads, 0, s>>>(
-      dxs, nullptr, dest_row, dx_acc, dx_extra, T, d, k, dx);
+  launch_k(gather_sum_kernel<false>, dim3(static_cast<unsigned>((T * 32 + threads - 1) / threads)),
+      dim3(threads), 0, s, dxs, nullptr, dest_row, dx_acc, dx_extra, T, d, k, dx);
   return cudaGetLastError();
 }
 
@@ -285,8 +301,8 @@ cudaError_t launch_unpermute(const uint16_t* ys, const float* gates, const int32
                              cudaStream_t s) {
   if (T == 0) return cudaSuccess;
   const int threads = 256;
-  gather_sum_kernel<true><<<static_cast<unsigned>((T * 32 + threads - 1) / threads), threads, 0, s>>>(
-      ys, gates, dest_row, nullptr, y_extra, T, d, k, y);
+  launch_k(gather_sum_kernel<true>, dim3(static_cast<unsigned>((T * 32 + threads - 1) / threads)),
+      dim3(threads), 0, s, ys, gates, dest_row, nullptr, y_extra, T, d, k, y);
   return cudaGetLastError();
 }
 

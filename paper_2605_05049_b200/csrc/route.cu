@@ -25,6 +25,8 @@ __device__ __forceinline__ uint32_t orderable(float v) {
 template <int PER_LANE>
 __global__ void route_kernel(const float* __restrict__ logits, int64_t T, int E, int k,
                              int32_t* __restrict__ topk_idx, float* __restrict__ gates) {
+  pdl_wait();
+  pdl_trigger();
   const int lane = threadIdx.x & 31;
   const int64_t t = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   if (t >= T) return;
@@ -81,6 +83,8 @@ __global__ void route_kernel(const float* __restrict__ logits, int64_t T, int E,
 __global__ void route_bwd_kernel(const float* __restrict__ logits, const int32_t* __restrict__ idx,
                                  const float* __restrict__ gates, const float* __restrict__ dgates,
                                  int64_t T, int E, int k, float* __restrict__ dl) {
+  pdl_wait();
+  pdl_trigger();
   const int lane = threadIdx.x & 31;
   const int64_t t = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   if (t >= T) return;
@@ -131,6 +135,8 @@ __global__ void route_bwd_kernel(const float* __restrict__ logits, const int32_t
 // M-stacking for [hi | lo]^T x.  Either way one bf16 tensor-core GEMM gives fp32 accuracy.
 __global__ void split_hilo_kernel(const float* __restrict__ dl, int64_t T, int E, int Ep,
                                   uint16_t* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= T * Ep) return;
   const int64_t t = i / Ep;
@@ -145,6 +151,8 @@ __global__ void split_hilo_kernel(const float* __restrict__ dl, int64_t T, int E
 // [W_r; W_r] stacked at rows 0 and Ep of a [2*Ep, d] buffer (padding rows zero).
 __global__ void stack_wr_kernel(const uint16_t* __restrict__ w_r, int E, int Ep, int d,
                                 uint16_t* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= static_cast<int64_t>(2) * Ep * d) return;
   const int64_t r = i / d, c = i % d;
@@ -159,11 +167,12 @@ cudaError_t launch_route(const float* logits, int64_t T, int E, int k, int32_t* 
   if (T == 0) return cudaSuccess;
   const int threads = 256;
   const int64_t blocks = (T * 32 + threads - 1) / threads;
-  if (E <= 32) route_kernel<1><<<blocks, threads, 0, s>>>(logits, T, E, k, topk_idx, gates);
-  else if (E <= 64) route_kernel<2><<<blocks, threads, 0, s>>>(logits, T, E, k, topk_idx, gates);
-  else if (E <= 128) route_kernel<4><<<blocks, threads, 0, s>>>(logits, T, E, k, topk_idx, gates);
-  else if (E <= 256) route_kernel<8><<<blocks, threads, 0, s>>>(logits, T, E, k, topk_idx, gates);
-  else route_kernel<kPerLane><<<blocks, threads, 0, s>>>(logits, T, E, k, topk_idx, gates);
+  if (E <= 32) launch_k(route_kernel<1>, dim3(blocks), dim3(threads), 0, s, logits, T, E, k, topk_idx, gates);
+  else if (E <= 64) launch_k(route_kernel<2>, dim3(blocks), dim3(threads), 0, s, logits, T, E, k, topk_idx, gates);
+  else if (E <= 128) launch_k(route_kernel<4>, dim3(blocks), dim3(threads), 0, s, logits, T, E, k, topk_idx, gates);
+  else if (E <= 256) launch_k(route_kernel<8>, dim3(blocks), dim3(threads), 0, s, logits, T, E, k, topk_idx, gates);
+  else launch_k(route_kernel<kPerLane>, dim3(blocks), dim3(threads), 0, s, logits, T, E, k,
+      topk_idx, gates);
   return cudaGetLastError();
 }
 
@@ -173,7 +182,8 @@ cudaError_t launch_route_bwd(const float* logits, const int32_t* topk_idx, const
   if (T == 0) return cudaSuccess;
   const int threads = 256;
   const int64_t blocks = (T * 32 + threads - 1) / threads;
-  route_bwd_kernel<<<blocks, threads, 0, s>>>(logits, topk_idx, gates, dgates, T, E, k, dlogits);
+  launch_k(route_bwd_kernel, dim3(blocks), dim3(threads), 0, s, logits, topk_idx, gates, dgates, T,
+      E, k, dlogits);
   return cudaGetLastError();
 }
 
@@ -181,14 +191,16 @@ cudaError_t launch_split_hilo(const float* dl, int64_t T, int E, int Ep, uint16_
                               cudaStream_t s) {
   if (T == 0) return cudaSuccess;
   const int64_t n = T * Ep;
-  split_hilo_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(dl, T, E, Ep, out);
+  launch_k(split_hilo_kernel, dim3(static_cast<unsigned>((n + 255) / 256)), dim3(256), 0, s, dl, T,
+      E, Ep, out);
   return cudaGetLastError();
 }
 
 cudaError_t launch_stack_wr(const uint16_t* w_r, int E, int Ep, int d, uint16_t* out,
                             cudaStream_t s) {
   const int64_t n = static_cast<int64_t>(2) * Ep * d;
-  stack_wr_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(w_r, E, Ep, d, out);
+  launch_k(stack_wr_kernel, dim3(static_cast<unsigned>((n + 255) / 256)), dim3(256), 0, s, w_r, E,
+      Ep, d, out);
   return cudaGetLastError();
 }
 
