@@ -256,6 +256,7 @@ moe_status moe_ctx_create(moe_ctx** out, const moe_shape* shape, int device, siz
   if (e == cudaSuccess) e = cudaMemset(c->d_done, 0, 32);
   const int64_t scratch = moe::permute_scratch_ints(shape->T_local, shape->k, shape->E);
   if (e == cudaSuccess) e = cudaMalloc(&c->d_scratch, scratch * 4);
+  if (e == cudaSuccess) e = cudaMemset(c->d_scratch, 0, scratch * 4);   // incl. the block ticket
   if (e == cudaSuccess) e = cudaMalloc(&c->d_rows_T, 16);
   int32_t tl = static_cast<int32_t>(shape->T_local);
   if (e == cudaSuccess) e = cudaMemcpy(c->d_rows_T, &tl, 4, cudaMemcpyHostToDevice);

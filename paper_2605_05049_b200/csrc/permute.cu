@@ -20,12 +20,17 @@ __device__ __forceinline__ int expert_of(const int32_t* idx, int64_t a, int64_t 
   return idx[t * k + j];
 }
 
-// Pass 1: per-chunk expert histogram.
-__global__ void hist_kernel(const int32_t* __restrict__ idx, int64_t T, int k, int E,
-                            int32_t* __restrict__ chunk_hist /*[nchunks][E]*/) {
+// Pass 1: per-chunk expert histogram; the last block to finish (ticket) then runs pass 2:
+// per-expert exclusive scan over chunks (in place -> chunk base), capacity clamp, counts and
+// off = exclusive scan of counts.  One launch instead of two.
+__global__ void hist_scan_kernel(const int32_t* __restrict__ idx, int64_t T, int k, int E,
+                                 int64_t C, int32_t* __restrict__ chunk_hist /*[nchunks][E]*/,
+                                 int32_t* __restrict__ counts, int32_t* __restrict__ off,
+                                 int32_t* __restrict__ ticket) {
   pdl_wait();
   pdl_trigger();
-  extern __shared__ int32_t s_hist[];
+  extern __shared__ int32_t s_hist[];   // [E]
+  __shared__ int s_last;
   for (int e = threadIdx.x; e < E; e += blockDim.x) s_hist[e] = 0;
   __syncthreads();
   const int64_t a = static_cast<int64_t>(blockIdx.x) * kChunk + threadIdx.x;
@@ -33,38 +38,50 @@ __global__ void hist_kernel(const int32_t* __restrict__ idx, int64_t T, int k, i
   __syncthreads();
   for (int e = threadIdx.x; e < E; e += blockDim.x)
     chunk_hist[static_cast<int64_t>(blockIdx.x) * E + e] = s_hist[e];
-}
-
-// Pass 2: per-expert exclusive scan over chunks (in place -> chunk base), capacity clamp,
-// counts and off = exclusive scan of counts.  One block, thread per expert.
-__global__ void scan_kernel(int32_t* __restrict__ chunk_hist, int nchunks, int E, int64_t C,
-                            int32_t* __restrict__ counts, int32_t* __restrict__ off) {
-  pdl_wait();
-  pdl_trigger();
-  __shared__ int32_t s_cnt[1024];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = (atomicAdd(ticket, 1) == static_cast<int>(gridDim.x) - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int nchunks = gridDim.x;
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
     int32_t run = 0;
-    for (int c = 0; c < nchunks; ++c) {
-      const int32_t h = chunk_hist[static_cast<int64_t>(c) * E + e];
+    int c = 0;
+    for (; c + 8 <= nchunks; c += 8) {   // 8 independent loads in flight
+      int32_t h[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) h[q] = __ldcg(chunk_hist + static_cast<int64_t>(c + q) * E + e);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        chunk_hist[static_cast<int64_t>(c + q) * E + e] = run;
+        run += h[q];
+      }
+    }
+    for (; c < nchunks; ++c) {
+      const int32_t h = __ldcg(chunk_hist + static_cast<int64_t>(c) * E + e);
       chunk_hist[static_cast<int64_t>(c) * E + e] = run;
       run += h;
     }
     const int32_t kept = (C >= 0 && run > C) ? static_cast<int32_t>(C) : run;
     counts[e] = kept;
-    s_cnt[e] = kept;
+    s_hist[e] = kept;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     int32_t run = 0;
     for (int e = 0; e < E; ++e) {
       off[e] = run;
-      run += s_cnt[e];
+      run += s_hist[e];
     }
     off[E] = run;
+    *ticket = 0;   // for the next call (stream-ordered)
   }
 }
 
-// Pass 3: stable rank inside the chunk -> p, kept, dest_row.
+// Pass 2: stable rank inside the chunk -> p, kept, dest_row.
 __global__ void rank_kernel(const int32_t* __restrict__ idx, int64_t T, int k, int E, int64_t C,
                             const int32_t* __restrict__ chunk_base, const int32_t* __restrict__ off,
                             int32_t* __restrict__ dest_row) {
@@ -98,7 +115,7 @@ __global__ void rank_kernel(const int32_t* __restrict__ idx, int64_t T, int k, i
   dest_row[t * k + j] = kept ? static_cast<int32_t>(off[e] + p) : -1;
 }
 
-// Pass 4: warp per token; read x_t once per 512-byte chunk, write it to each kept row.
+// Pass 3: warp per token; read x_t once (4 x 16 B in flight per lane), write each kept row.
 __global__ void scatter_kernel(const uint16_t* __restrict__ x, const int32_t* __restrict__ dest_row,
                                int64_t T, int d, int k, uint16_t* __restrict__ xs) {
   pdl_wait();
@@ -115,10 +132,17 @@ __global__ void scatter_kernel(const uint16_t* __restrict__ x, const int32_t* __
   if (nk == 0) return;
   const int nvec = d / 8;  // 16-byte vectors per row
   const uint4* src = reinterpret_cast<const uint4*>(x + t * d);
-  for (int v = lane; v < nvec; v += 32) {
-    const uint4 val = ld_nc_v4(src + v);
-    for (int j = 0; j < nk; ++j)
-      reinterpret_cast<uint4*>(xs + static_cast<int64_t>(rows[j]) * d)[v] = val;
+  for (int v0 = lane; v0 < nvec; v0 += 128) {   // 4 loads in flight per lane
+    uint4 val[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (v0 + 32 * u < nvec) val[u] = ld_nc_v4(src + v0 + 32 * u);
+    for (int j = 0; j < nk; ++j) {
+      uint4* dst = reinterpret_cast<uint4*>(xs + static_cast<int64_t>(rows[j]) * d);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (v0 + 32 * u < nvec) dst[v0 + 32 * u] = val[u];
+    }
   }
 }
 
@@ -154,6 +178,7 @@ __global__ void gather_sum_kernel(const uint16_t* __restrict__ rows, const float
     }
   }
   const int nvec = d / 8;
+#pragma unroll 2
   for (int v = lane; v < nvec; v += 32) {
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     for (int j = 0; j < nk; ++j)
@@ -200,6 +225,7 @@ __global__ void gather_sum_router_kernel(const uint16_t* __restrict__ dxs,
     if (r >= 0) rws[nk++] = r;
   }
   const int nvec = d / 8;
+#pragma unroll 2
   for (int v = lane; v < nvec; v += 32) {
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     for (int j = 0; j < nk; ++j)
@@ -255,7 +281,7 @@ cudaError_t launch_sum_partials(const float* part, int S, int E, int Ep, int d, 
 
 int64_t permute_scratch_ints(int64_t T, int k, int E) {
   const int64_t nchunks = (T * k + kChunk - 1) / kChunk;
-  return (nchunks > 0 ? nchunks : 1) * E + E + 1;
+  return (nchunks > 0 ? nchunks : 1) * E + E + 1 + 1;   // chunk bases, off, block ticket
 }
 
 cudaError_t launch_permute(const uint16_t* x, const int32_t* topk_idx, int64_t T, int d, int E,
@@ -269,9 +295,9 @@ cudaError_t launch_permute(const uint16_t* x, const int32_t* topk_idx, int64_t T
     cudaMemsetAsync(counts, 0, sizeof(int32_t) * E, s);
     return cudaGetLastError();
   }
-  launch_k(hist_kernel, dim3(nchunks), dim3(kChunk), E * sizeof(int32_t), s, topk_idx, T, k, E,
-      chunk_hist);
-  launch_k(scan_kernel, dim3(1), dim3(256), 0, s, chunk_hist, nchunks, E, C, counts, off);
+  int32_t* ticket = off + E + 1;
+  launch_k(hist_scan_kernel, dim3(nchunks), dim3(kChunk), E * sizeof(int32_t), s, topk_idx, T, k,
+           E, C, chunk_hist, counts, off, ticket);
   const size_t smem = static_cast<size_t>(32) * E * sizeof(int32_t);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

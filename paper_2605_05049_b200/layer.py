@@ -452,8 +452,8 @@ class MoELayer:
         """Number of libmoe kernels one forward / backward launches (for bench.py)."""
         n = 0
         if fwd:
-            # router GEMM, route, permute (4), dispatch (1 fused launch), ffn (2), combine (2)
-            n += 1 + 1 + 4 + 1 + 2 + 2 + (2 if self.fs else 0)
+            # router GEMM, route, permute (3), dispatch (1 fused launch), ffn (2), combine (2)
+            n += 1 + 1 + 3 + 1 + 2 + 2 + (2 if self.fs else 0)
         extra = 2 * (len(self._ranges()) - 1) if self._ranges() else 0   # per range: a2a + GEMM
         n += extra * (int(fwd) + int(bwd))
         if bwd:
