@@ -24,8 +24,15 @@
  *   bf16), T_local < 0, or a NULL required pointer.  T_local = 0 is legal; the
  *   collective calls still take part in the exchange.
  * - Collective calls (moe_dispatch, moe_dispatch_bwd, moe_combine,
- *   moe_combine_bwd, moe_symm_alloc) must be issued by every EP rank in the same
- *   order, like NCCL collectives.  Not thread-safe; one ctx per (process, GPU).
+ *   moe_combine_bwd, their _range variants, the fused *_combine / *_dispatch FFN
+ *   calls, moe_symm_alloc) must be issued by every EP rank in the same order, like
+ *   NCCL collectives.  Not thread-safe; one ctx per (process, GPU).
+ * - A collective's destination buffer is written by PEERS from the moment they enter
+ *   the call: a rank must not write it itself (e.g. zero it) after its previous
+ *   collective returned unless every rank has passed that point (a barrier), or the
+ *   peers' rows can be overwritten.  The layer never writes them locally.
+ * - The collectives' epoch counter lives in device memory and is advanced by the
+ *   kernels, so a sequence of calls may be captured once in a CUDA graph and replayed.
  * - Determinism: identical inputs give bit-identical outputs on every call (no
  *   float atomics, fixed reduction orders); buffers may be reused across calls.
  * - Dtypes: bf16 activations/weights/messages (moe_bf16 = raw bf16 bits), fp32

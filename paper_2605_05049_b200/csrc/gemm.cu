@@ -822,9 +822,18 @@ bool make_tmap(CUtensorMap* tm, CUtensorMapDataType dt, int rank, const void* pt
     if (strides[i] % 16) return false;
     s[i] = static_cast<cuuint64_t>(strides[i]);
   }
+  // L2 sector promotion of TMA reads: 256 B by default; MOE_L2_PROMOTION=0/64/128 for A/B runs
+  static CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  static bool promo_read = false;
+  if (!promo_read) {
+    const char* e = getenv("MOE_L2_PROMOTION");
+    if (e && e[0] == '0') promo = CU_TENSOR_MAP_L2_PROMOTION_NONE;
+    else if (e && !strcmp(e, "64")) promo = CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+    else if (e && !strcmp(e, "128")) promo = CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+    promo_read = true;
+  }
   CUresult r = fn(tm, dt, rank, const_cast<void*>(ptr), d, s, b, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  CU_TENSOR_MAP_SWIZZLE_128B, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 

@@ -103,3 +103,21 @@ def test_layer_ep_parity_chunked(nproc, config, stream_k):
                      ("--chunks", "4"), env={"MOE_STREAM_K": stream_k})
     print(res)
     assert res["ok"], res
+
+
+@pytest.mark.parametrize("nproc", [2, 4, 8])
+def test_all_to_all_origin_encoded(nproc):
+    """moe_dispatch / moe_dispatch_bwd / moe_dispatch_range alone with origin-encoded payloads:
+    every received row bit-exact at the oracle's receive layout, padding zeroed, involution,
+    ranges == whole, contiguous and migrated placements (tests/mp_a2a_worker.py)."""
+    if n_gpus() < nproc:
+        pytest.skip(f"needs {nproc} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr=127.0.0.1", f"--master-port={30300 + nproc}",
+           os.path.join(ROOT, "tests", "mp_a2a_worker.py")]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    lines = [l for l in p.stdout.splitlines() if l.startswith("{")]
+    assert p.returncode == 0 and lines, f"worker failed:\n{p.stdout[-3000:]}\n{p.stderr[-3000:]}"
+    res = json.loads(lines[-1])
+    print(res)
+    assert res["ok"], res
