@@ -10,8 +10,10 @@ no kernels, headers, helpers, tables or constant generators.  Inputs come from
 Modules
   moe_ref   the layer, step by step in the paper's notation (Table II)
   counters  FLOP / byte counters evaluated from the realised routing
+  migration Alg. 2 expert migration (NEXT-2)
+  dedup     per-destination-rank deduplicated all-to-all (NEXT-4, reading R18)
 
 Parity pins: see tests/test_oracle_*.py; "parity unpinned" items are listed in
 DESIGN.md §Oracle and in the docstrings below.
 """
-from . import moe_ref, counters  # noqa: F401
+from . import moe_ref, counters, dedup  # noqa: F401
