@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--rebalance", action="store_true",
                     help="expert migration before timing: observe loads, Alg. 2, move experts")
+    ap.add_argument("--dedup", action="store_true",
+                    help="NEXT-4 deduplicated all-to-alls (one row per (token, owner) pair)")
     ap.add_argument("--stepwise", action="store_true",
                     help="step-by-step C-ABI calls instead of the fused compute+all-to-all ones")
     ap.add_argument("--cpu-sample-tokens", type=int, default=0)
@@ -178,8 +180,20 @@ def layer_roofline(layer, cfg, peaks, nvl_gbs=900.0):
         egress = int(cm[r, ~mine].sum()) * row
         ingress = int(cm[:, mine].sum() - cm[r, mine].sum()) * row
         t = 3 * 2 * T_r * d * E / pi                          # router fwd + dgrad + wgrad
-        t += 2 * (T_r * row + send * row) / bh                # permute, permute_bwd
-        t += 2 * (send * row + T_r * row) / bh                # unpermute, combine_bwd dO rows
+        if layer.dedup:
+            # pairs instead of slots on NVLink; HBM: expand (pairs -> receive rows), reduce
+            # (receive rows -> pairs), gathers over pairs, bwd expand also reads O
+            nm = layer.dlayout.view(EP, EP).to(torch.int64).cpu()
+            pairs_out, pairs_in = int(nm[r].sum()), int(nm[:, r].sum())
+            egress = (pairs_out - int(nm[r, r])) * row
+            ingress = (pairs_in - int(nm[r, r])) * row
+            t += 2 * (pairs_out * row + T_r * row) / bh         # y / dx gathers over pairs
+            t += 2 * (pairs_in * row + recv * row) / bh         # fwd expand, dispatch_bwd reduce
+            t += (recv * row + pairs_in * row) / bh             # combine reduce
+            t += (pairs_in * row + 2 * recv * row) / bh         # bwd expand (+ O for dg)
+        else:
+            t += 2 * (T_r * row + send * row) / bh            # permute, permute_bwd
+            t += 2 * (send * row + T_r * row) / bh            # unpermute, combine_bwd dO rows
         t += 4 * max(egress, ingress) / bn                    # dispatch, combine, their twins
         t += 18 * recv * d * f / pi                           # expert GEMMs fwd + bwd
         if cfg.E_s:
@@ -213,7 +227,7 @@ def run_ours(args):
     ep = world
     T_r = cfg.T // ep
     dims = LayerDims(T_r, cfg.d, cfg.E, cfg.k, cfg.f, cfg.E_s, cfg.cf, ep, rank)
-    layer = MoELayer(dims, device=local, fused=not args.stepwise)
+    layer = MoELayer(dims, device=local, fused=not args.stepwise, dedup=args.dedup)
     if args.chunks is not None:
         layer.chunks = args.chunks
     if args.comm_sms is not None:
@@ -332,7 +346,8 @@ def run_ours(args):
               "moe_expert_ffn_bwd_dh", "moe_expert_ffn_bwd_dx_dispatch"]
     buckets = {"moe_permute": "permute", "moe_dispatch": "dispatch",
                "moe_dispatch_range": "dispatch", "moe_combine_bwd": "combine_bwd",
-               "moe_combine_bwd_range": "combine_bwd"}
+               "moe_combine_bwd_range": "combine_bwd", "moe_dedup_dispatch": "dispatch",
+               "moe_dedup_combine_bwd": "combine_bwd"}
     originals = {n: getattr(layer_mod.L, n) for n in hooked + list(buckets)}
     for n in hooked:
         setattr(layer_mod.L, n, timed(originals[n]))
@@ -442,6 +457,11 @@ def run_ours(args):
     a2a_bytes = {"egress": int(cmat[rank, ~own].sum()) * row_b,
                  "ingress": int(cmat[:, own].sum() - cmat[rank, own].sum()) * row_b}
     permute_bytes = T_r * row_b + send_rows * row_b
+    if layer.dedup:   # one row per (token, owner) pair; the permute moves indices only
+        nm = layer.dlayout.view(EPw, EPw).to(torch.int64).cpu()
+        a2a_bytes = {"egress": int(nm[rank].sum() - nm[rank, rank]) * row_b,
+                     "ingress": int(nm[:, rank].sum() - nm[rank, rank]) * row_b}
+        permute_bytes = T_r * cfg.k * 8
     roof = layer_roofline(layer, cfg, measured_peaks())
     vals = torch.tensor([ms, e2e_ms, gemm_ms, graph_ms or 0.0, region_ms["permute"]],
                         dtype=torch.float64, device=dev)
@@ -487,6 +507,7 @@ def run_ours(args):
             "capacity_factor": cfg.cf, "zipf_s": cfg.zipf_s,
             "parallelism": f"ep{world}", "tokens_per_rank": T_r,
             "expert_migration": rebal,
+            "dedup_a2a": bool(layer.dedup),
             "a2a_gemm_chunks": len(layer._ranges() or [None]),
             "cuda_graph": use_graph,
             "eager_ms_per_step": eager_ms,

@@ -182,7 +182,7 @@ moe_status moe_route_bwd(moe_ctx* ctx, const float* logits, const int32_t* topk_
  * p(t,j) = #earlier assignments a' < a = j*T_local+t on the same expert; kept iff
  * p < C; counts[e] = #kept; dest_row[t,j] = off[e] + p or -1 (dropped);
  * xs[dest_row[t,j]] = x[t] (bit copy).  counts [E] int32, dest_row [T_local,k] int32,
- * xs [T_local*k, d] bf16 (rows [0, sum counts) written). */
+ * xs [T_local*k, d] bf16 (rows [0, sum counts) written; NULL = indices only). */
 moe_status moe_permute(moe_ctx* ctx, const moe_bf16* x, const int32_t* topk_idx,
                        int32_t* counts, int32_t* dest_row, moe_bf16* xs, moe_stream stream);
 /* dx[t] = bf16( sum_{j kept} dxs[dest_row[t,j]]  (fp32, j order)
@@ -340,6 +340,79 @@ moe_status moe_combine(moe_ctx* ctx, const moe_bf16* out, const int32_t* layout,
 moe_status moe_combine_bwd(moe_ctx* ctx, const moe_bf16* dy, const float* gates,
                            const int32_t* dest_row, const moe_bf16* ys, const int32_t* layout,
                            float* dgates, moe_bf16* dout_r, moe_stream stream);
+
+/* ---------------- NEXT-4 deduplicated all-to-all (reading R18) -------
+ * The plain dispatch sends one row per kept slot (t, j); a token whose k experts share an
+ * owner crosses NVLink several times with the same bytes.  Here a token crosses once per
+ * (token, owner) PAIR -- X-MoE's "redundancy-based communication bypassing",
+ * the single-box form of the paper's hierarchical all-to-all (which reduces
+ * to its Phase I inside one switch group).  oracle/dedup.py is the definition:
+ *   pair (t, q)  iff some kept slot j of token t has owner(e_j) = q; tslot = rank of t among
+ *                this rank's tokens paired with q (ascending t); ntok[q] = pairs with q.
+ *   source pair rows   pdest[t, q] = pair_base[q] + tslot  (pair_base = exclusive scan of
+ *                      ntok over q), -1 if no pair; rows of part / dxpart / dgpart.
+ *   owner token rows   u = tok_base[r] + tslot for pairs from source r, tok_base[r] =
+ *                      sum_{r'<r} ntok_all[r'][me]; rows of xt / dyt, rlist, glist, dg_own.
+ *   rlist[u][j]        receive row (the plain receive layout above) of slot j of the pair's
+ *                      token if kept and owned here, else -1; glist[u][j] its gate (else 0).
+ *   pair record        dlayout [EP*EP] int32 = ntok_all[r][q], written by moe_dedup_dispatch.
+ * Every other tensor (xr, out, dout_r, dxr, the layout record) is exactly the plain path's, so
+ * the expert FFN calls are unchanged.  The combine partials are rounded to bf16 once on the
+ * owner, so y and dx carry a second bf16 rounding (inside the 2e-2 tolerance, reading R18).
+ * Symmetric buffers (moe_symm_alloc): xt/dyt [moe_dedup_token_rows_max, d] bf16, rlist, glist
+ * [moe_dedup_token_rows_max, k] (owner side); part, dxpart [moe_dedup_pair_rows_max, d] bf16,
+ * dgpart [moe_dedup_pair_rows_max, k] fp32 (source side). */
+
+/* T_local * min(k, EP): bound on a source's pair rows; -1 for an invalid shape. */
+int64_t moe_dedup_pair_rows_max(const moe_shape* shape);
+/* min(EP * T_local, moe_recv_rows_max): bound on an owner's token rows; -1 if invalid. */
+int64_t moe_dedup_token_rows_max(const moe_shape* shape);
+
+/* Not collective.  pdest [T_local, EP] int32 and ntok [EP] int32 from topk_idx and
+ * dest_row (moe_permute's output; xs may be NULL there) under the ctx's expert placement. */
+moe_status moe_dedup_pairs(moe_ctx* ctx, const int32_t* topk_idx, const int32_t* dest_row,
+                           int32_t* pdest, int32_t* ntok, moe_stream stream);
+/* Collective.  F3 deduplicated: exchanges counts and ntok, writes the layout record (as
+ * moe_dispatch) and the pair record dlayout, stores each paired x row once into its owner's
+ * xt (each 2 KB part of x[t] is read once and stored to every owner of t) with the pair's
+ * rlist / glist rows, waits for every peer, then expands locally: xr[rlist[u][j]] = xt[u],
+ * padding rows zeroed.  xr is bit-identical to moe_dispatch's (it need not be symmetric). */
+moe_status moe_dedup_dispatch(moe_ctx* ctx, const moe_bf16* x, const int32_t* counts,
+                              const int32_t* ntok, const int32_t* pdest, const int32_t* dest_row,
+                              const int32_t* topk_idx, const float* gates, int32_t* layout,
+                              int32_t* dlayout, moe_bf16* xt, int32_t* rlist, float* glist,
+                              moe_bf16* xr, moe_stream stream);
+/* Collective.  F5+F6 deduplicated: per pair the owner forms
+ *   part[u] = bf16( sum_{j: rlist[u][j] >= 0} glist[u][j] * out[rlist[u][j]] )  (fp32, j order)
+ * and stores it at the source's pair row; after every peer's rows arrived
+ *   y[t] = bf16( sum_q part[pdest[t,q]] (fp32, q ascending) + y_extra[t] (optional) ). */
+moe_status moe_dedup_combine(moe_ctx* ctx, const moe_bf16* out, const int32_t* dlayout,
+                             const int32_t* rlist, const float* glist, const int32_t* pdest,
+                             const moe_bf16* y_extra_or_null, moe_bf16* part, moe_bf16* y,
+                             moe_stream stream);
+/* Collective.  B6+B5 deduplicated: dy[t] crosses once per pair into the owner's dyt; then,
+ * locally on the owner, dout_r[rl] = bf16(g * dyt[u]) and dg_own[u][j] = <dyt[u], out[rl]>
+ * (fp32; 0 where rlist < 0) -- O never leaves its owner.  dout_r padding rows zeroed. */
+moe_status moe_dedup_combine_bwd(moe_ctx* ctx, const moe_bf16* dy, const int32_t* pdest,
+                                 const int32_t* layout, const int32_t* dlayout,
+                                 const int32_t* rlist, const float* glist, const moe_bf16* out,
+                                 moe_bf16* dyt, float* dg_own, moe_bf16* dout_r,
+                                 moe_stream stream);
+/* Collective.  B3 deduplicated: dxpart[pair row] = bf16( sum_j dxr[rlist[u][j]] ) (fp32, j
+ * order) and dgpart[pair row][j] = dg_own[u][j] go to each source; then locally
+ * dgates[t,j] = dgpart[pdest[t, owner(e_j)]][j] (0 for dropped slots). */
+moe_status moe_dedup_dispatch_bwd(moe_ctx* ctx, const moe_bf16* dxr, const int32_t* dlayout,
+                                  const int32_t* rlist, const float* dg_own, const int32_t* pdest,
+                                  const int32_t* dest_row, const int32_t* topk_idx,
+                                  moe_bf16* dxpart, float* dgpart, float* dgates,
+                                  moe_stream stream);
+/* B2 + B0 dgrad as moe_permute_bwd_router (k > 1), rows from the pair buffer:
+ *   dx[t] = bf16( sum_q dxpart[pdest[t,q]] + sum_j dlogits[t,e_j] w_r[e_j,:] + dx_extra[t] ). */
+moe_status moe_dedup_permute_bwd_router(moe_ctx* ctx, const moe_bf16* dxpart,
+                                        const int32_t* pdest, const int32_t* topk_idx,
+                                        const float* dlogits, const moe_bf16* w_r,
+                                        const moe_bf16* dx_extra_or_null, moe_bf16* dx,
+                                        moe_stream stream);
 
 #ifdef __cplusplus
 }

@@ -90,12 +90,19 @@ _SIGS = {
     "moe_expert_ffn_down_combine": [P, P, P, P, P, P, P, P, P, P],
     "moe_expert_ffn_bwd_dh": [P, P, I32, I32, P, P, P, P, P],
     "moe_expert_ffn_bwd_dx_dispatch": [P, P, P, P, P, P, P, P, P, P, ctypes.c_int, P],
+    "moe_dedup_pairs": [P, P, P, P, P, P],
+    "moe_dedup_dispatch": [P] + [P] * 14,
+    "moe_dedup_combine": [P] * 10,
+    "moe_dedup_combine_bwd": [P] * 12,
+    "moe_dedup_dispatch_bwd": [P] * 12,
+    "moe_dedup_permute_bwd_router": [P] * 9,
 }
 for _name, _args in _SIGS.items():
     _f = getattr(_lib, _name)
     _f.argtypes = _args
     _f.restype = ctypes.c_int
-for _name in ("moe_capacity", "moe_recv_rows_max", "moe_layout_ints"):
+for _name in ("moe_capacity", "moe_recv_rows_max", "moe_layout_ints", "moe_dedup_pair_rows_max",
+              "moe_dedup_token_rows_max"):
     getattr(_lib, _name).argtypes = [ctypes.POINTER(moe_shape)]
     getattr(_lib, _name).restype = I64
 _lib.moe_layout_offset.argtypes = [ctypes.POINTER(moe_shape), ctypes.c_int]
@@ -104,7 +111,8 @@ _lib.moe_status_string.argtypes = [ctypes.c_int]
 _lib.moe_status_string.restype = ctypes.c_char_p
 
 EXPORTED = sorted(list(_SIGS) + ["moe_capacity", "moe_recv_rows_max", "moe_layout_ints",
-                                 "moe_layout_offset", "moe_status_string"])
+                                 "moe_layout_offset", "moe_status_string",
+                                 "moe_dedup_pair_rows_max", "moe_dedup_token_rows_max"])
 
 
 def _check(fn, code):
@@ -147,6 +155,14 @@ def moe_recv_rows_max(shape):
 
 def moe_layout_ints(shape):
     return _lib.moe_layout_ints(ctypes.byref(shape))
+
+
+def moe_dedup_pair_rows_max(shape):
+    return _lib.moe_dedup_pair_rows_max(ctypes.byref(shape))
+
+
+def moe_dedup_token_rows_max(shape):
+    return _lib.moe_dedup_token_rows_max(ctypes.byref(shape))
 
 
 def moe_layout_offset(shape, field):
@@ -395,3 +411,55 @@ def moe_expert_ffn_bwd_dx_dispatch(ctx, xr, layout, w_gu, g_u_h, dout, dgu, dxs,
         _ptr(g_u_h, BF16, "g_u_h"), _ptr(dout, BF16, "dout"), _ptr(dgu, BF16, "dgu"),
         _ptr(dxs, BF16, "dxs"), _ptr(dw_gu, F32, "dw_gu"), _ptr(dw_down, F32, "dw_down"),
         int(bool(accumulate)), _stream(stream)))
+
+
+# ---- NEXT-4 deduplicated all-to-all (include/moe.h, reading R18)
+def moe_dedup_pairs(ctx, topk_idx, dest_row, pdest, ntok, stream=None):
+    _check("moe_dedup_pairs", _lib.moe_dedup_pairs(
+        ctx.handle, _ptr(topk_idx, I32T, "topk_idx"), _ptr(dest_row, I32T, "dest_row"),
+        _ptr(pdest, I32T, "pdest"), _ptr(ntok, I32T, "ntok"), _stream(stream)))
+
+
+def moe_dedup_dispatch(ctx, x, counts, ntok, pdest, dest_row, topk_idx, gates, layout, dlayout,
+                       xt, rlist, glist, xr, stream=None):
+    _check("moe_dedup_dispatch", _lib.moe_dedup_dispatch(
+        ctx.handle, _ptr(x, BF16, "x"), _ptr(counts, I32T, "counts"), _ptr(ntok, I32T, "ntok"),
+        _ptr(pdest, I32T, "pdest"), _ptr(dest_row, I32T, "dest_row"),
+        _ptr(topk_idx, I32T, "topk_idx"), _ptr(gates, F32, "gates"), _ptr(layout, I32T, "layout"),
+        _ptr(dlayout, I32T, "dlayout"), _ptr(xt, BF16, "xt"), _ptr(rlist, I32T, "rlist"),
+        _ptr(glist, F32, "glist"), _ptr(xr, BF16, "xr"), _stream(stream)))
+
+
+def moe_dedup_combine(ctx, out, dlayout, rlist, glist, pdest, y_extra, part, y, stream=None):
+    _check("moe_dedup_combine", _lib.moe_dedup_combine(
+        ctx.handle, _ptr(out, BF16, "out"), _ptr(dlayout, I32T, "dlayout"),
+        _ptr(rlist, I32T, "rlist"), _ptr(glist, F32, "glist"), _ptr(pdest, I32T, "pdest"),
+        _ptr(y_extra, BF16, "y_extra"), _ptr(part, BF16, "part"), _ptr(y, BF16, "y"),
+        _stream(stream)))
+
+
+def moe_dedup_combine_bwd(ctx, dy, pdest, layout, dlayout, rlist, glist, out, dyt, dg_own, dout_r,
+                          stream=None):
+    _check("moe_dedup_combine_bwd", _lib.moe_dedup_combine_bwd(
+        ctx.handle, _ptr(dy, BF16, "dy"), _ptr(pdest, I32T, "pdest"), _ptr(layout, I32T, "layout"),
+        _ptr(dlayout, I32T, "dlayout"), _ptr(rlist, I32T, "rlist"), _ptr(glist, F32, "glist"),
+        _ptr(out, BF16, "out"), _ptr(dyt, BF16, "dyt"), _ptr(dg_own, F32, "dg_own"),
+        _ptr(dout_r, BF16, "dout_r"), _stream(stream)))
+
+
+def moe_dedup_dispatch_bwd(ctx, dxr, dlayout, rlist, dg_own, pdest, dest_row, topk_idx, dxpart,
+                           dgpart, dgates, stream=None):
+    _check("moe_dedup_dispatch_bwd", _lib.moe_dedup_dispatch_bwd(
+        ctx.handle, _ptr(dxr, BF16, "dxr"), _ptr(dlayout, I32T, "dlayout"),
+        _ptr(rlist, I32T, "rlist"), _ptr(dg_own, F32, "dg_own"), _ptr(pdest, I32T, "pdest"),
+        _ptr(dest_row, I32T, "dest_row"), _ptr(topk_idx, I32T, "topk_idx"),
+        _ptr(dxpart, BF16, "dxpart"), _ptr(dgpart, F32, "dgpart"), _ptr(dgates, F32, "dgates"),
+        _stream(stream)))
+
+
+def moe_dedup_permute_bwd_router(ctx, dxpart, pdest, topk_idx, dlogits, w_r, dx_extra, dx,
+                                 stream=None):
+    _check("moe_dedup_permute_bwd_router", _lib.moe_dedup_permute_bwd_router(
+        ctx.handle, _ptr(dxpart, BF16, "dxpart"), _ptr(pdest, I32T, "pdest"),
+        _ptr(topk_idx, I32T, "topk_idx"), _ptr(dlogits, F32, "dlogits"), _ptr(w_r, BF16, "w_r"),
+        _ptr(dx_extra, BF16, "dx_extra"), _ptr(dx, BF16, "dx"), _stream(stream)))

@@ -22,6 +22,7 @@ struct moe_ctx {
   size_t heap_used = 0;
   size_t internal_bytes = 0;
   int64_t countmat_off = 0;
+  int64_t ntokmat_off = 0;
   int64_t flags_off = 0;
   cudaIpcMemHandle_t handle;
   char* peer_base[MOE_MAX_EP] = {};
@@ -117,6 +118,8 @@ CommArgs comm_args(moe_ctx* c) {
   a.flags_off = c->flags_off;
   a.countmat = reinterpret_cast<int32_t*>(c->heap + c->countmat_off);
   a.countmat_off = c->countmat_off;
+  a.ntokmat = reinterpret_cast<int32_t*>(c->heap + c->ntokmat_off);
+  a.ntokmat_off = c->ntokmat_off;
   a.done = c->d_done;
   a.err = c->d_err;
   a.epoch_ptr = reinterpret_cast<uint64_t*>(c->d_done + 4);
@@ -218,6 +221,15 @@ int64_t moe_layout_ints(const moe_shape* s) {
   const int64_t E_l = s->E / s->ep_size;
   return static_cast<int64_t>(s->ep_size) * s->E + 2 * E_l + 1;
 }
+int64_t moe_dedup_pair_rows_max(const moe_shape* s) {
+  if (!shape_ok(s)) return -1;
+  return s->T_local * (s->k < s->ep_size ? s->k : s->ep_size);
+}
+int64_t moe_dedup_token_rows_max(const moe_shape* s) {
+  if (!shape_ok(s)) return -1;
+  const int64_t a = s->ep_size * s->T_local, b = recv_rows_of(s);
+  return a < b ? a : b;
+}
 int64_t moe_layout_offset(const moe_shape* s, int field) {
   if (!shape_ok(s)) return -1;
   const int64_t E_l = s->E / s->ep_size, base = static_cast<int64_t>(s->ep_size) * s->E;
@@ -243,7 +255,8 @@ moe_status moe_ctx_create(moe_ctx** out, const moe_shape* shape, int device, siz
   if (e != cudaSuccess) { delete c; return cuda_status(e); }
   const int EP = shape->ep_size;
   c->countmat_off = 0;
-  c->flags_off = ((2 * EP * shape->E * 4) + 255) / 256 * 256;
+  c->ntokmat_off = ((2 * EP * shape->E * 4) + 255) / 256 * 256;
+  c->flags_off = c->ntokmat_off + ((2 * EP * EP * 4) + 255) / 256 * 256;
   c->internal_bytes = ((c->flags_off + moe::kNumSlots * EP * 8) + 4095) / 4096 * 4096;
   c->heap_bytes = c->internal_bytes + (symm_heap_bytes + 255) / 256 * 256;
   c->heap_used = c->internal_bytes;
@@ -508,7 +521,7 @@ moe_status moe_route_bwd(moe_ctx* c, const float* logits, const int32_t* topk_id
 // ---------------------------------------------------------------- F2 / B2
 moe_status moe_permute(moe_ctx* c, const moe_bf16* x, const int32_t* topk_idx, int32_t* counts,
                        int32_t* dest_row, moe_bf16* xs, moe_stream s) {
-  MOE_REQUIRE(c && x && topk_idx && counts && dest_row && xs);
+  MOE_REQUIRE(c && x && topk_idx && counts && dest_row);   // xs NULL: indices only
   return cuda_status(moe::launch_permute(x, topk_idx, c->s.T_local, c->s.d, c->s.E, c->s.k, c->C,
                                          counts, dest_row, xs, c->d_scratch, st(s)));
 }
@@ -852,3 +865,93 @@ moe_status moe_combine_bwd(moe_ctx* c, const moe_bf16* dy, const float* gates, c
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- NEXT-4 dedup all-to-all
+// Reading R18 (oracle/dedup.py): one row per (token, owner) pair crosses NVLink.
+namespace {
+int64_t heap_off(const moe_ctx* c, const void* p) {
+  return reinterpret_cast<const char*>(p) - c->heap;
+}
+}  // namespace
+
+moe_status moe_dedup_pairs(moe_ctx* c, const int32_t* topk_idx, const int32_t* dest_row,
+                           int32_t* pdest, int32_t* ntok, moe_stream s) {
+  MOE_REQUIRE(c && topk_idx && dest_row && pdest && ntok);
+  return cuda_status(moe::launch_dedup_pairs(topk_idx, dest_row, c->d_place, c->s.T_local, c->s.k,
+                                             c->E_l, c->s.ep_size, pdest, ntok, st(s)));
+}
+
+moe_status moe_dedup_dispatch(moe_ctx* c, const moe_bf16* x, const int32_t* counts,
+                              const int32_t* ntok, const int32_t* pdest, const int32_t* dest_row,
+                              const int32_t* topk_idx, const float* gates, int32_t* layout,
+                              int32_t* dlayout, moe_bf16* xt, int32_t* rlist, float* glist,
+                              moe_bf16* xr, moe_stream s) {
+  MOE_REQUIRE(c && x && counts && ntok && pdest && dest_row && topk_idx && gates && layout &&
+              dlayout && xt && rlist && glist && xr);
+  if (!c->peers_ready) return MOE_ERR_NOT_READY;
+  if (!in_heap(c, xt) || !in_heap(c, rlist) || !in_heap(c, glist)) return MOE_ERR_NOT_SYMMETRIC;
+  CommArgs a = comm_args(c);
+  MOE_TRY_CUDA(moe::launch_dedup_forward(a, 0, layout, dlayout, counts, ntok, c->recv_rows, x,
+                                         pdest, dest_row, topk_idx, gates, heap_off(c, xt),
+                                         heap_off(c, rlist), heap_off(c, glist), st(s)));
+  return cuda_status(moe::launch_dedup_expand(a, 0, layout, dlayout, xt, rlist, glist, nullptr, xr,
+                                              nullptr, st(s)));
+}
+
+moe_status moe_dedup_combine(moe_ctx* c, const moe_bf16* out, const int32_t* dlayout,
+                             const int32_t* rlist, const float* glist, const int32_t* pdest,
+                             const moe_bf16* y_extra, moe_bf16* part, moe_bf16* y, moe_stream s) {
+  MOE_REQUIRE(c && out && dlayout && rlist && glist && pdest && part && y);
+  if (!c->peers_ready) return MOE_ERR_NOT_READY;
+  if (!in_heap(c, part)) return MOE_ERR_NOT_SYMMETRIC;
+  CommArgs a = comm_args(c);
+  MOE_TRY_CUDA(moe::launch_dedup_reduce(a, 0, dlayout, rlist, glist, out, nullptr,
+                                        heap_off(c, part), 0, st(s)));
+  // y[t] = bf16( sum_q part[pdest[t,q]] (q ascending) + y_extra[t] )
+  return cuda_status(moe::launch_permute_bwd(part, pdest, nullptr, y_extra, c->s.T_local, c->s.d,
+                                             c->s.ep_size, y, st(s)));
+}
+
+moe_status moe_dedup_combine_bwd(moe_ctx* c, const moe_bf16* dy, const int32_t* pdest,
+                                 const int32_t* layout, const int32_t* dlayout,
+                                 const int32_t* rlist, const float* glist, const moe_bf16* out,
+                                 moe_bf16* dyt, float* dg_own, moe_bf16* dout_r, moe_stream s) {
+  MOE_REQUIRE(c && dy && pdest && layout && dlayout && rlist && glist && out && dyt && dg_own &&
+              dout_r);
+  if (!c->peers_ready) return MOE_ERR_NOT_READY;
+  if (!in_heap(c, dyt)) return MOE_ERR_NOT_SYMMETRIC;
+  CommArgs a = comm_args(c);
+  MOE_TRY_CUDA(moe::launch_dedup_forward(a, 1, const_cast<int32_t*>(layout),
+                                         const_cast<int32_t*>(dlayout), nullptr, nullptr, 0, dy,
+                                         pdest, nullptr, nullptr, nullptr, heap_off(c, dyt), 0, 0,
+                                         st(s)));
+  return cuda_status(moe::launch_dedup_expand(a, 1, layout, dlayout, dyt, rlist, glist, out,
+                                              dout_r, dg_own, st(s)));
+}
+
+moe_status moe_dedup_dispatch_bwd(moe_ctx* c, const moe_bf16* dxr, const int32_t* dlayout,
+                                  const int32_t* rlist, const float* dg_own, const int32_t* pdest,
+                                  const int32_t* dest_row, const int32_t* topk_idx,
+                                  moe_bf16* dxpart, float* dgpart, float* dgates, moe_stream s) {
+  MOE_REQUIRE(c && dxr && dlayout && rlist && dg_own && pdest && dest_row && topk_idx && dxpart &&
+              dgpart && dgates);
+  if (!c->peers_ready) return MOE_ERR_NOT_READY;
+  if (!in_heap(c, dxpart) || !in_heap(c, dgpart)) return MOE_ERR_NOT_SYMMETRIC;
+  CommArgs a = comm_args(c);
+  MOE_TRY_CUDA(moe::launch_dedup_reduce(a, 1, dlayout, rlist, nullptr, dxr, dg_own,
+                                        heap_off(c, dxpart), heap_off(c, dgpart), st(s)));
+  return cuda_status(moe::launch_dedup_dgates(dest_row, topk_idx, pdest, c->d_place, c->E_l,
+                                              c->s.ep_size, dgpart, c->s.T_local, c->s.k, dgates,
+                                              st(s)));
+}
+
+moe_status moe_dedup_permute_bwd_router(moe_ctx* c, const moe_bf16* dxpart, const int32_t* pdest,
+                                        const int32_t* topk_idx, const float* dlogits,
+                                        const moe_bf16* w_r, const moe_bf16* dx_extra,
+                                        moe_bf16* dx, moe_stream s) {
+  MOE_REQUIRE(c && dxpart && pdest && topk_idx && dlogits && w_r && dx);
+  MOE_REQUIRE(c->s.k > 1);
+  return cuda_status(moe::launch_permute_bwd_router_rows(dxpart, pdest, c->s.ep_size, topk_idx,
+                                                         dlogits, w_r, dx_extra, c->s.T_local,
+                                                         c->s.d, c->s.E, c->s.k, dx, st(s)));
+}

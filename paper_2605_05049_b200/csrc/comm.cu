@@ -92,7 +92,10 @@ __device__ void signal_done(const CommArgs& a, int slot, bool wait_after) {
 // Publishes this rank's E counts into row `rank` of every peer's count matrix (parity
 // buffer epoch & 1).  Done by whichever block of the launch arrives first (ticket), so it
 // cannot be starved by blocks that are already spinning on the counts flags.
-__device__ void publish_counts(const CommArgs& a, const int32_t* counts) {
+// With ntok (the dedup dispatch) this rank's EP pair counts go into row `rank` of every
+// peer's [EP x EP] pair-count matrix under the same release.
+__device__ void publish_counts(const CommArgs& a, const int32_t* counts,
+                               const int32_t* ntok = nullptr) {
   __shared__ int s_first;
   if (threadIdx.x == 0) s_first = (atomicAdd(a.done + 1, 1) == 0);
   __syncthreads();
@@ -105,6 +108,12 @@ __device__ void publish_counts(const CommArgs& a, const int32_t* counts) {
                    (parity * EP + a.rank) * E + e;
     *dst = counts[e];
   }
+  if (ntok)
+    for (int i = threadIdx.x; i < EP * EP; i += blockDim.x) {
+      const int q = i / EP, q2 = i % EP;
+      reinterpret_cast<int32_t*>(a.peers.base[q] + a.ntokmat_off)[(parity * EP + a.rank) * EP + q2] =
+          ntok[q2];
+    }
   // bar.sync orders the block's count stores before the lanes' st.release.sys (cumulative)
   __syncthreads();
   if (threadIdx.x < EP) st_release_sys(peer_flag(a, threadIdx.x, kSlotCounts, a.rank), a.epoch);
@@ -419,6 +428,296 @@ __global__ void reverse_transfer_kernel(CommArgs a, const int32_t* __restrict__ 
   signal_done(a, kSlotData, /*wait_after=*/true);
 }
 
+// ---------------------------------------------------------------- NEXT-4 dedup all-to-all
+// Reading R18 (oracle/dedup.py): a token whose kept slots share an owner crosses
+// NVLink once per (token, owner) PAIR instead of once per slot (X-MoE's
+// "redundancy-based communication bypassing").  Owner q's token
+// buffer holds its pairs ordered (source r, tslot): row tok_base[q][r] + tslot with
+// tok_base[q][r] = sum_{r'<r} ntok[r'][q]; source r's pair buffers hold them ordered
+// (owner q, tslot): row pair_base[r][q] + tslot = pdest[t, q].
+
+// The pair bases of this rank from the pair-count matrix nm [EP x EP]:
+//   tok_base[q]  = first row of my pairs in owner q's token buffer
+//   pair_base[q] = first row of owner q's pairs in my pair buffers (pdest - pair_base = tslot)
+__device__ __forceinline__ void pair_bases(const CommArgs& a, const int32_t* nm, int32_t* tok_base,
+                                           int32_t* pair_base) {
+  const int EP = a.ep;
+  if (threadIdx.x < EP) {
+    const int q = threadIdx.x;
+    int32_t tb = 0, pb = 0;
+    for (int r = 0; r < a.rank; ++r) tb += nm[r * EP + q];
+    for (int q2 = 0; q2 < q; ++q2) pb += nm[a.rank * EP + q2];
+    tok_base[q] = tb;
+    pair_base[q] = pb;
+  }
+  __syncthreads();
+}
+
+// One warp's share of a 2 KB row part: up to 4 x 16 B per lane.
+struct PartBuf {
+  uint4 v[kPartVec / 32];
+};
+__device__ __forceinline__ void load_part(PartBuf& b, const uint4* __restrict__ src, int nvec,
+                                          int part, int lane) {
+  const int v0 = part * kPartVec + lane;
+#pragma unroll
+  for (int i = 0; i < kPartVec / 32; ++i)
+    if (v0 + 32 * i < nvec && v0 + 32 * i < (part + 1) * kPartVec) b.v[i] = ld_nc_v4(src + v0 + 32 * i);
+}
+__device__ __forceinline__ void store_part(uint4* dst, const PartBuf& b, int nvec, int part,
+                                           int lane) {
+  const int v0 = part * kPartVec + lane;
+#pragma unroll
+  for (int i = 0; i < kPartVec / 32; ++i)
+    if (v0 + 32 * i < nvec && v0 + 32 * i < (part + 1) * kPartVec) st_v4(dst + v0 + 32 * i, b.v[i]);
+}
+
+// Forward pattern, deduplicated.  Work item = (token t, 2 KB part): the part is read ONCE and
+// stored to every owner t has a pair with, in rotated owner order.  MODE 0 (dispatch) also
+// exchanges counts and pair counts, writes the layout and pair records, and stores each
+// pair's slot lists (lane j: receive row of slot j if owned by q and kept, else -1; gate).
+template <int MODE>
+__global__ void dedup_forward_kernel(CommArgs a, int32_t* __restrict__ layout,
+                                     int32_t* __restrict__ dlayout,
+                                     const int32_t* __restrict__ counts,
+                                     const int32_t* __restrict__ ntok, int64_t recv_rows_cap,
+                                     const uint16_t* __restrict__ src,
+                                     const int32_t* __restrict__ pdest,
+                                     const int32_t* __restrict__ dest_row,
+                                     const int32_t* __restrict__ topk_idx,
+                                     const float* __restrict__ gates, int64_t tok_off,
+                                     int64_t rlist_off, int64_t glist_off) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ FwdTables tb;
+  __shared__ int32_t s_tok_base[MOE_MAX_EP], s_pair_base[MOE_MAX_EP];
+  a.epoch = load_epoch(a);
+  const int EP = a.ep, E = a.E, E_l = a.E_l;
+  const int32_t* nm = dlayout;
+  if (MODE == 0) {
+    publish_counts(a, counts, ntok);
+    wait_all(a, kSlotCounts);
+    const int parity = static_cast<int>(a.epoch & 1);
+    const int32_t* cm = a.countmat + parity * EP * E;
+    nm = a.ntokmat + parity * EP * EP;
+    build_fwd_tables(a, cm, tb);
+    if (blockIdx.x == 0) {  // layout record (as moe_dispatch) + pair record
+      for (int i = threadIdx.x; i < EP * E; i += blockDim.x) layout[i] = cm[i];
+      for (int el = threadIdx.x; el < E_l; el += blockDim.x)
+        layout[EP * E + el] = tb.rows[a.expert_at[a.rank * E_l + el]];
+      for (int el = threadIdx.x; el <= E_l; el += blockDim.x) layout[EP * E + E_l + el] = tb.seg[el];
+      for (int i = threadIdx.x; i < EP * EP; i += blockDim.x) dlayout[i] = nm[i];
+      if (threadIdx.x == 0 && tb.seg[E_l] > recv_rows_cap) set_device_error(a.err, kDevOverflow);
+    }
+  }
+  pair_bases(a, nm, s_tok_base, s_pair_base);
+  const int lane = threadIdx.x & 31;
+  const int64_t gwarp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int d = a.d, nvec = d / 8, k = static_cast<int>(a.k);
+  const int64_t row_bytes = static_cast<int64_t>(d) * 2;
+  const int parts = row_parts(nvec);
+  const int64_t n_items = a.T * parts;
+  for (int64_t w = gwarp; w < n_items; w += nwarps) {
+    const int64_t t = w / parts;
+    const int part = static_cast<int>(w - t * parts);
+    const int32_t pd = lane < EP ? pdest[t * EP + lane] : -1;   // lane q: pair row for owner q
+    const uint32_t mask = __ballot_sync(0xffffffffu, pd >= 0);
+    if (!mask) continue;
+    PartBuf b;
+    load_part(b, reinterpret_cast<const uint4*>(src + t * d), nvec, part, lane);
+    int32_t rr = -1, qj = -1;
+    float g = 0.f;
+    if (MODE == 0 && part == 0 && lane < k) {
+      const int32_t dr = dest_row[t * k + lane];
+      if (dr >= 0) {
+        const int e = topk_idx[t * k + lane];
+        qj = a.place[e] / E_l;
+        rr = tb.dst[e] + (dr - tb.off[e]);
+        g = gates[t * k + lane];
+      }
+    }
+    for (int i = 0; i < EP; ++i) {
+      const int q = (a.rank + 1 + i) % EP;   // rotated owner order, self last
+      const int32_t pq = __shfl_sync(0xffffffffu, pd, q);
+      if (!((mask >> q) & 1u)) continue;
+      const int64_t u = s_tok_base[q] + (pq - s_pair_base[q]);
+      char* base = a.peers.base[q];
+      store_part(reinterpret_cast<uint4*>(base + tok_off + u * row_bytes), b, nvec, part, lane);
+      if (MODE == 0 && part == 0 && lane < k) {
+        const int32_t rl = (qj == q) ? rr : -1;
+        reinterpret_cast<int32_t*>(base + rlist_off)[u * k + lane] = rl;
+        reinterpret_cast<float*>(base + glist_off)[u * k + lane] = rl >= 0 ? g : 0.f;
+      }
+    }
+  }
+  signal_done(a, kSlotData, /*wait_after=*/true);
+}
+
+// Owner, local.  MODE 0: xr[rlist[u][j]] = tok[u] (work item = (pair, 2 KB part)).
+// MODE 1: dst[rl] = bf16(g * tok[u]) and dg_own[u][j] = <tok[u], O[rl]> (work item = pair).
+// Both zero the padding rows of dst's receive segments.
+template <int MODE>
+__global__ void dedup_expand_kernel(CommArgs a, const int32_t* __restrict__ layout,
+                                    const int32_t* __restrict__ dlayout,
+                                    const uint16_t* __restrict__ tok,
+                                    const int32_t* __restrict__ rlist,
+                                    const float* __restrict__ glist,
+                                    const uint16_t* __restrict__ O, uint16_t* __restrict__ dst,
+                                    float* __restrict__ dg_own) {
+  pdl_wait();
+  pdl_trigger();
+  const int EP = a.ep, E = a.E, E_l = a.E_l, k = static_cast<int>(a.k);
+  __shared__ int32_t s_seg[kMaxE + 1];
+  __shared__ int32_t s_rows[kMaxE];
+  for (int i = threadIdx.x; i <= E_l; i += blockDim.x) s_seg[i] = layout[EP * E + E_l + i];
+  for (int i = threadIdx.x; i < E_l; i += blockDim.x) s_rows[i] = layout[EP * E + i];
+  __syncthreads();
+  int64_t n_pairs = 0;
+  for (int r = 0; r < EP; ++r) n_pairs += dlayout[r * EP + a.rank];
+  const int lane = threadIdx.x & 31;
+  const int64_t gwarp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int d = a.d, nvec = d / 8;
+  const int parts = (MODE == 0) ? row_parts(nvec) : 1;
+  const int64_t n_items = n_pairs * parts;
+  const int64_t n_rows = s_seg[E_l];
+  for (int64_t w = gwarp; w < n_items + n_rows; w += nwarps) {
+    if (w >= n_items) {  // padding rows of the receive segments
+      const int64_t row = w - n_items;
+      const int el = upper_bound_idx(s_seg, E_l + 1, row);
+      if (row - s_seg[el] < s_rows[el]) continue;
+      uint4* z = reinterpret_cast<uint4*>(dst + row * d);
+      for (int v = lane; v < nvec; v += 32) z[v] = make_uint4(0u, 0u, 0u, 0u);
+      continue;
+    }
+    const int64_t u = w / parts;
+    const int part = static_cast<int>(w - u * parts);
+    const int32_t rl_l = lane < k ? rlist[u * k + lane] : -1;
+    const uint4* ptok = reinterpret_cast<const uint4*>(tok + u * d);
+    if (MODE == 0) {
+      PartBuf b;
+      load_part(b, ptok, nvec, part, lane);
+      for (int j = 0; j < k; ++j) {
+        const int32_t rl = __shfl_sync(0xffffffffu, rl_l, j);
+        if (rl >= 0) store_part(reinterpret_cast<uint4*>(dst + static_cast<int64_t>(rl) * d), b, nvec, part, lane);
+      }
+    } else {
+      const float g_l = lane < k ? glist[u * k + lane] : 0.f;
+      for (int j = 0; j < k; ++j) {
+        const int32_t rl = __shfl_sync(0xffffffffu, rl_l, j);
+        const float g = __shfl_sync(0xffffffffu, g_l, j);
+        if (rl < 0) {
+          if (lane == 0) dg_own[u * k + j] = 0.f;
+          continue;
+        }
+        uint4* pdst = reinterpret_cast<uint4*>(dst + static_cast<int64_t>(rl) * d);
+        const uint4* po = reinterpret_cast<const uint4*>(O + static_cast<int64_t>(rl) * d);
+        float dot = 0.f;
+        for (int v = lane; v < nvec; v += 32) {
+          const uint4 a4 = ld_nc_v4(ptok + v), b4 = ld_nc_v4(po + v);
+          const uint32_t aw[4] = {a4.x, a4.y, a4.z, a4.w}, bw[4] = {b4.x, b4.y, b4.z, b4.w};
+          uint32_t ow[4];
+#pragma unroll
+          for (int q2 = 0; q2 < 4; ++q2) {
+            const float y0 = bf16_lo(aw[q2]), y1 = bf16_hi(aw[q2]);
+            dot += y0 * bf16_lo(bw[q2]) + y1 * bf16_hi(bw[q2]);
+            ow[q2] = pack_bf16(g * y0, g * y1);
+          }
+          st_v4(pdst + v, make_uint4(ow[0], ow[1], ow[2], ow[3]));
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+        if (lane == 0) dg_own[u * k + j] = dot;
+      }
+    }
+  }
+}
+
+// Reverse pattern, deduplicated (owner -> sources).  Work item = (pair u, 2 KB part):
+// part[u] = bf16( sum_j w_j rows[rlist[u][j]] ) in fp32, j ascending (MODE 0: w = glist,
+// MODE 1: w = 1), stored at the source's pair row; MODE 1 also sends dg_own[u][*].  Pairs
+// are visited in rotated source order.
+template <int MODE>
+__global__ void dedup_reduce_kernel(CommArgs a, const int32_t* __restrict__ dlayout,
+                                    const int32_t* __restrict__ rlist,
+                                    const float* __restrict__ glist,
+                                    const uint16_t* __restrict__ rows,
+                                    const float* __restrict__ dg_own, int64_t part_off,
+                                    int64_t dgpart_off) {
+  pdl_wait();
+  pdl_trigger();
+  a.epoch = load_epoch(a);
+  const int EP = a.ep, k = static_cast<int>(a.k);
+  __shared__ int32_t s_tok_base[MOE_MAX_EP + 1];   // my token-buffer rows of source r
+  __shared__ int32_t s_pb[MOE_MAX_EP];             // my pairs' first row at source r
+  __shared__ int32_t s_prefix[MOE_MAX_EP + 1];     // rotated source order
+  __shared__ int32_t s_src[MOE_MAX_EP];
+  if (threadIdx.x == 0) {
+    int32_t run = 0;
+    for (int r = 0; r < EP; ++r) {
+      s_tok_base[r] = run;
+      run += dlayout[r * EP + a.rank];
+      int32_t pb = 0;
+      for (int q = 0; q < a.rank; ++q) pb += dlayout[r * EP + q];
+      s_pb[r] = pb;
+    }
+    s_tok_base[EP] = run;
+    int32_t pre = 0;
+    for (int i = 0; i < EP; ++i) {
+      const int r = (a.rank + 1 + i) % EP;
+      s_src[i] = r;
+      s_prefix[i] = pre;
+      pre += dlayout[r * EP + a.rank];
+    }
+    s_prefix[EP] = pre;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t gwarp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int d = a.d, nvec = d / 8;
+  const int64_t row_bytes = static_cast<int64_t>(d) * 2;
+  const int parts = row_parts(nvec);
+  const int64_t n_items = static_cast<int64_t>(s_prefix[EP]) * parts;
+  for (int64_t w = gwarp; w < n_items; w += nwarps) {
+    const int64_t v = w / parts;
+    const int part = static_cast<int>(w - v * parts);
+    const int i = upper_bound_idx(s_prefix, EP + 1, v);
+    const int r = s_src[i];
+    const int64_t u = s_tok_base[r] + (v - s_prefix[i]);
+    const int64_t prow = s_pb[r] + (v - s_prefix[i]);
+    const int32_t rl_l = lane < k ? rlist[u * k + lane] : -1;
+    const float w_l = (MODE == 0) ? (lane < k ? glist[u * k + lane] : 0.f) : 1.f;
+    float acc[kPartVec / 32][8];
+#pragma unroll
+    for (int c = 0; c < kPartVec / 32; ++c)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[c][q] = 0.f;
+    const int v0 = part * kPartVec + lane;
+    const int v1 = min(nvec, (part + 1) * kPartVec);
+    for (int j = 0; j < k; ++j) {
+      const int32_t rl = __shfl_sync(0xffffffffu, rl_l, j);
+      const float wj = __shfl_sync(0xffffffffu, w_l, j);
+      if (rl < 0) continue;
+      const uint4* pr = reinterpret_cast<const uint4*>(rows + static_cast<int64_t>(rl) * d);
+#pragma unroll
+      for (int c = 0; c < kPartVec / 32; ++c)
+        if (v0 + 32 * c < v1) acc_bf16x8(acc[c], ld_nc_v4(pr + v0 + 32 * c), wj);
+    }
+    uint4* pdst = reinterpret_cast<uint4*>(a.peers.base[r] + part_off + prow * row_bytes);
+#pragma unroll
+    for (int c = 0; c < kPartVec / 32; ++c)
+      if (v0 + 32 * c < v1)
+        st_v4(pdst + v0 + 32 * c,
+              make_uint4(pack_bf16(acc[c][0], acc[c][1]), pack_bf16(acc[c][2], acc[c][3]),
+                         pack_bf16(acc[c][4], acc[c][5]), pack_bf16(acc[c][6], acc[c][7])));
+    if (MODE == 1 && part == 0 && lane < k)
+      reinterpret_cast<float*>(a.peers.base[r] + dgpart_off)[prow * k + lane] = dg_own[u * k + lane];
+  }
+  signal_done(a, kSlotData, /*wait_after=*/true);
+}
+
 // Waits for every rank's data flag of this epoch (the GEMM-fused reverse all-to-alls).
 // The GEMM that preceded it published load_epoch(a) (the counter is not advanced until here).
 __global__ void wait_flags_kernel(CommArgs a, int slot) {
@@ -484,6 +783,53 @@ cudaError_t launch_reverse_transfer(const CommArgs& a, const int32_t* layout, co
   // receive rows <= EP * T * k
   launch_k(reverse_transfer_kernel, dim3(transfer_blocks(a, a.T * a.k * a.ep)), dim3(512),
       transfer_smem(a), s, a, layout, src, dst_off);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dedup_forward(const CommArgs& a, int mode, int32_t* layout, int32_t* dlayout,
+                                 const int32_t* counts, const int32_t* ntok,
+                                 int64_t recv_rows_cap, const uint16_t* src,
+                                 const int32_t* pdest, const int32_t* dest_row,
+                                 const int32_t* topk_idx, const float* gates, int64_t tok_off,
+                                 int64_t rlist_off, int64_t glist_off, cudaStream_t s) {
+  const int64_t rows = a.T * (a.k < a.ep ? a.k : a.ep);   // pair rows bound
+  if (mode == 0)
+    launch_k(dedup_forward_kernel<0>, dim3(transfer_blocks(a, rows)), dim3(512), transfer_smem(a), s,
+        a, layout, dlayout, counts, ntok, recv_rows_cap, src, pdest, dest_row, topk_idx, gates,
+        tok_off, rlist_off, glist_off);
+  else
+    launch_k(dedup_forward_kernel<1>, dim3(transfer_blocks(a, rows)), dim3(512), transfer_smem(a), s,
+        a, layout, dlayout, counts, ntok, recv_rows_cap, src, pdest, dest_row, topk_idx, gates,
+        tok_off, rlist_off, glist_off);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dedup_expand(const CommArgs& a, int mode, const int32_t* layout,
+                                const int32_t* dlayout, const uint16_t* tok,
+                                const int32_t* rlist, const float* glist, const uint16_t* O,
+                                uint16_t* dst, float* dg_own, cudaStream_t s) {
+  // local kernel, sized like the transfer it follows (an SM budget beside a GEMM applies too)
+  const int64_t rows = a.T * a.k * a.ep;   // receive rows bound
+  if (mode == 0)
+    launch_k(dedup_expand_kernel<0>, dim3(transfer_blocks(a, rows)), dim3(512), transfer_smem(a), s,
+        a, layout, dlayout, tok, rlist, glist, O, dst, dg_own);
+  else
+    launch_k(dedup_expand_kernel<1>, dim3(transfer_blocks(a, rows)), dim3(512), transfer_smem(a), s,
+        a, layout, dlayout, tok, rlist, glist, O, dst, dg_own);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dedup_reduce(const CommArgs& a, int mode, const int32_t* dlayout,
+                                const int32_t* rlist, const float* glist, const uint16_t* rows,
+                                const float* dg_own, int64_t part_off, int64_t dgpart_off,
+                                cudaStream_t s) {
+  const int64_t n = a.T * a.ep;   // pairs received bound
+  if (mode == 0)
+    launch_k(dedup_reduce_kernel<0>, dim3(transfer_blocks(a, n)), dim3(512), transfer_smem(a), s, a,
+        dlayout, rlist, glist, rows, dg_own, part_off, dgpart_off);
+  else
+    launch_k(dedup_reduce_kernel<1>, dim3(transfer_blocks(a, n)), dim3(512), transfer_smem(a), s, a,
+        dlayout, rlist, glist, rows, dg_own, part_off, dgpart_off);
   return cudaGetLastError();
 }
 

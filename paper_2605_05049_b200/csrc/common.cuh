@@ -350,4 +350,14 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn, bool 
          (static_cast<uint32_t>(M >> 4) << 24);
 }
 
+// acc[i] += scale * bf16 value i of the 8 packed in v (fp32)
+__device__ __forceinline__ void acc_bf16x8(float (&acc)[8], uint4 v, float scale) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    acc[2 * q] += scale * bf16_lo(w[q]);
+    acc[2 * q + 1] += scale * bf16_hi(w[q]);
+  }
+}
+
 }  // namespace moe

@@ -123,6 +123,22 @@ cudaError_t launch_permute(const uint16_t* x, const int32_t* topk_idx, int64_t T
 cudaError_t launch_permute_bwd(const uint16_t* dxs, const int32_t* dest_row, const float* dx_acc,
                                const uint16_t* dx_extra, int64_t T, int d, int k, uint16_t* dx,
                                cudaStream_t s);
+// B2 + B0 dgrad with a row-list width kr independent of k (dedup pair rows: kr = EP)
+cudaError_t launch_permute_bwd_router_rows(const uint16_t* dxs, const int32_t* rows, int kr,
+                                           const int32_t* topk_idx, const float* dlogits,
+                                           const uint16_t* w_r, const uint16_t* dx_extra,
+                                           int64_t T, int d, int E, int k, uint16_t* dx,
+                                           cudaStream_t s);
+// NEXT-4 dedup, source side (reading R18): pdest [T,EP] = pair row of (t, q) or -1,
+// ntok [EP] pairs per owner; one block
+cudaError_t launch_dedup_pairs(const int32_t* topk_idx, const int32_t* dest_row,
+                               const int32_t* place, int64_t T, int k, int E_l, int EP,
+                               int32_t* pdest, int32_t* ntok, cudaStream_t s);
+// dgates[t,j] = dgpart[pdest[t, owner(e_j)] * k + j] (0 for dropped slots)
+cudaError_t launch_dedup_dgates(const int32_t* dest_row, const int32_t* topk_idx,
+                                const int32_t* pdest, const int32_t* place, int E_l, int EP,
+                                const float* dgpart, int64_t T, int k, float* dgates,
+                                cudaStream_t s);
 cudaError_t launch_unpermute(const uint16_t* ys, const float* gates, const int32_t* dest_row,
                              const uint16_t* y_extra, int64_t T, int d, int k, uint16_t* y,
                              cudaStream_t s);
@@ -140,6 +156,8 @@ struct CommArgs {
   int64_t flags_off;     // byte offset of the flag array inside every heap
   int32_t* countmat;     // local count matrix [2][EP][E] in the symmetric heap
   int64_t countmat_off;
+  int32_t* ntokmat;      // local pair-count matrix [2][EP][EP] (dedup all-to-all, NEXT-4)
+  int64_t ntokmat_off;
   int32_t* done;         // local device counter for last-block detection
   int32_t* err;          // device error word
   // Per-call epoch (identical on every rank): kernels read *epoch_ptr + 1 at their start and
@@ -173,6 +191,29 @@ cudaError_t launch_combine_bwd_transfer(const CommArgs& a, int32_t* layout, int6
 // Reverse pattern: owner receive rows -> sources' send-layout rows
 cudaError_t launch_reverse_transfer(const CommArgs& a, const int32_t* layout, const uint16_t* src,
                                     int64_t dst_off, cudaStream_t s);
+// NEXT-4 deduplicated all-to-all (reading R18; oracle/dedup.py).  Token rows cross once per
+// (token, owner) pair into the owner's token buffer (tok_off); rlist/glist (rlist_off,
+// glist_off: [pair, k]) name each pair's receive rows and gates on the owner.
+//   mode 0 (dispatch): counts + pair counts exchange, layout + pair record, x rows, lists
+//   mode 1 (combine_bwd): dy rows (pair layout from dlayout)
+cudaError_t launch_dedup_forward(const CommArgs& a, int mode, int32_t* layout, int32_t* dlayout,
+                                 const int32_t* counts, const int32_t* ntok,
+                                 int64_t recv_rows_cap, const uint16_t* src,
+                                 const int32_t* pdest, const int32_t* dest_row,
+                                 const int32_t* topk_idx, const float* gates, int64_t tok_off,
+                                 int64_t rlist_off, int64_t glist_off, cudaStream_t s);
+// Owner, local: mode 0 xr[rlist[u][j]] = tok[u]; mode 1 dst[rl] = bf16(g * tok[u]) and
+// dg_own[u][j] = <tok[u], O[rl]>; both zero dst's padding rows
+cudaError_t launch_dedup_expand(const CommArgs& a, int mode, const int32_t* layout,
+                                const int32_t* dlayout, const uint16_t* tok,
+                                const int32_t* rlist, const float* glist, const uint16_t* O,
+                                uint16_t* dst, float* dg_own, cudaStream_t s);
+// Collective, owner -> sources: part[u] = sum_j w_j rows[rlist[u][j]] (mode 0: w = glist;
+// mode 1: w = 1, and dg_own[u][*] goes along to dgpart) at the source's pair row
+cudaError_t launch_dedup_reduce(const CommArgs& a, int mode, const int32_t* dlayout,
+                                const int32_t* rlist, const float* glist, const uint16_t* rows,
+                                const float* dg_own, int64_t part_off, int64_t dgpart_off,
+                                cudaStream_t s);
 // 1-block wait for every rank's flag of a.epoch (after a GEMM with a fused scatter epilogue)
 cudaError_t launch_wait_flags(const CommArgs& a, int slot, cudaStream_t s);
 

@@ -146,14 +146,6 @@ __global__ void scatter_kernel(const uint16_t* __restrict__ x, const int32_t* __
   }
 }
 
-__device__ __forceinline__ void acc_bf16x8(float (&acc)[8], uint4 v, float scale) {
-  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    acc[2 * q] += scale * bf16_lo(w[q]);
-    acc[2 * q + 1] += scale * bf16_hi(w[q]);
-  }
-}
 
 // y[t] = bf16( sum_{j kept} g_{t,j} rows[dest_row[t,j]] (j order) + extra_f32[t] + extra_bf16[t] )
 template <bool GATED>
@@ -208,7 +200,7 @@ __global__ void gather_sum_router_kernel(const uint16_t* __restrict__ dxs,
                                          const float* __restrict__ dlogits,
                                          const uint16_t* __restrict__ w_r,
                                          const uint16_t* __restrict__ extra_bf16, int64_t T, int d,
-                                         int E, int k, uint16_t* __restrict__ out) {
+                                         int E, int k, int kr, uint16_t* __restrict__ out) {
   pdl_wait();
   pdl_trigger();
   const int lane = threadIdx.x & 31;
@@ -221,7 +213,9 @@ __global__ void gather_sum_router_kernel(const uint16_t* __restrict__ dxs,
     const int32_t e = topk_idx[t * k + j];
     es[j] = e;
     dl[j] = dlogits[t * E + e];
-    const int32_t r = dest_row[t * k + j];
+  }
+  for (int j = 0; j < kr; ++j) {   // row list: dest_row [T,k] (kr = k) or dedup pdest [T,EP]
+    const int32_t r = dest_row[t * kr + j];
     if (r >= 0) rws[nk++] = r;
   }
   const int nvec = d / 8;
@@ -258,6 +252,113 @@ __global__ void sum_partials_kernel(const float* __restrict__ part, int S, int E
   dw[i] = s;
 }
 
+
+// ---------------------------------------------------------------- NEXT-4 dedup pairs
+// Reading R18 (oracle/dedup.py `pairs`): token t has a PAIR with owner q iff one of its kept
+// slots j has owner(e_j) = place[e_j] / E_l = q.  pdest[t, q] = pair_base[q] + tslot, tslot =
+// rank of t among this rank's tokens paired with q (ascending t), pair_base = exclusive scan
+// of ntok over q; -1 if no pair.  One block: thread i owns a contiguous token range; the
+// per-owner counts are block-scanned (EP <= 8 lanes of a warp scan per thread).
+constexpr int kPairThreads = 1024;
+
+__device__ __forceinline__ uint32_t owner_mask(const int32_t* __restrict__ topk_idx,
+                                               const int32_t* __restrict__ dest_row,
+                                               const int32_t* s_place, int64_t t, int k, int E_l) {
+  uint32_t m = 0;
+  for (int j = 0; j < k; ++j)
+    if (dest_row[t * k + j] >= 0) m |= 1u << (s_place[topk_idx[t * k + j]] / E_l);
+  return m;
+}
+
+__global__ void __launch_bounds__(kPairThreads) dedup_pairs_kernel(
+    const int32_t* __restrict__ topk_idx, const int32_t* __restrict__ dest_row,
+    const int32_t* __restrict__ place, int64_t T, int k, int E_l, int EP,
+    int32_t* __restrict__ pdest, int32_t* __restrict__ ntok) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ int32_t s_place[256];
+  __shared__ int32_t s_warp[kPairThreads / 32][MOE_MAX_EP];
+  __shared__ int32_t s_total[MOE_MAX_EP];
+  const int E = E_l * EP;
+  for (int i = threadIdx.x; i < E; i += blockDim.x) s_place[i] = place[i];
+  __syncthreads();
+  const int64_t per = (T + kPairThreads - 1) / kPairThreads;
+  const int64_t t0 = threadIdx.x * per, t1 = min(T, t0 + per);
+  int32_t c[MOE_MAX_EP];
+#pragma unroll
+  for (int q = 0; q < MOE_MAX_EP; ++q) c[q] = 0;
+  for (int64_t t = t0; t < t1; ++t) {
+    const uint32_t m = owner_mask(topk_idx, dest_row, s_place, t, k, E_l);
+#pragma unroll
+    for (int q = 0; q < MOE_MAX_EP; ++q) c[q] += (m >> q) & 1u;
+  }
+  // exclusive scan over threads, per owner: warp shuffles, then warp totals
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int32_t x[MOE_MAX_EP];
+#pragma unroll
+  for (int q = 0; q < MOE_MAX_EP; ++q) {
+    x[q] = c[q];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, x[q], o);
+      if (lane >= o) x[q] += y;
+    }
+    if (lane == 31) s_warp[warp][q] = x[q];
+    x[q] -= c[q];   // exclusive within the warp
+  }
+  __syncthreads();
+  if (threadIdx.x < MOE_MAX_EP) {
+    const int q = threadIdx.x;
+    int32_t run = 0;
+    for (int w = 0; w < kPairThreads / 32; ++w) {
+      const int32_t v = s_warp[w][q];
+      s_warp[w][q] = run;
+      run += v;
+    }
+    s_total[q] = run;
+  }
+  __syncthreads();
+  int32_t base[MOE_MAX_EP];
+  int32_t pb = 0;
+#pragma unroll
+  for (int q = 0; q < MOE_MAX_EP; ++q) {
+    base[q] = pb + s_warp[warp][q] + x[q];
+    pb += s_total[q];
+  }
+  for (int64_t t = t0; t < t1; ++t) {
+    const uint32_t m = owner_mask(topk_idx, dest_row, s_place, t, k, E_l);
+#pragma unroll
+    for (int q = 0; q < MOE_MAX_EP; ++q) {
+      if (q >= EP) break;
+      const bool on = (m >> q) & 1u;
+      pdest[t * EP + q] = on ? base[q] : -1;
+      base[q] += on;
+    }
+  }
+  if (threadIdx.x < EP) ntok[threadIdx.x] = s_total[threadIdx.x];
+}
+
+// dgates[t,j] = dgpart[pdest[t, owner(e_j)] * k + j] for kept slots, 0 for dropped ones.
+__global__ void dedup_dgates_kernel(const int32_t* __restrict__ dest_row,
+                                    const int32_t* __restrict__ topk_idx,
+                                    const int32_t* __restrict__ pdest,
+                                    const int32_t* __restrict__ place, int E_l, int EP,
+                                    const float* __restrict__ dgpart, int64_t T, int k,
+                                    float* __restrict__ dgates) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= T * k) return;
+  const int64_t t = i / k;
+  const int j = static_cast<int>(i - t * k);
+  float v = 0.f;
+  if (dest_row[i] >= 0) {
+    const int q = place[topk_idx[i]] / E_l;
+    v = dgpart[static_cast<int64_t>(pdest[t * EP + q]) * k + j];
+  }
+  dgates[i] = v;
+}
+
 }  // namespace
 
 cudaError_t launch_permute_bwd_router(const uint16_t* dxs, const int32_t* dest_row,
@@ -267,7 +368,38 @@ cudaError_t launch_permute_bwd_router(const uint16_t* dxs, const int32_t* dest_r
   if (T == 0) return cudaSuccess;
   const int threads = 256;
   launch_k(gather_sum_router_kernel, dim3(static_cast<unsigned>((T * 32 + threads - 1) / threads)),
-      dim3(threads), 0, s, dxs, dest_row, topk_idx, dlogits, w_r, dx_extra, T, d, E, k, dx);
+      dim3(threads), 0, s, dxs, dest_row, topk_idx, dlogits, w_r, dx_extra, T, d, E, k, k, dx);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_permute_bwd_router_rows(const uint16_t* dxs, const int32_t* rows, int kr,
+                                           const int32_t* topk_idx, const float* dlogits,
+                                           const uint16_t* w_r, const uint16_t* dx_extra,
+                                           int64_t T, int d, int E, int k, uint16_t* dx,
+                                           cudaStream_t s) {
+  if (T == 0) return cudaSuccess;
+  const int threads = 256;
+  launch_k(gather_sum_router_kernel, dim3(static_cast<unsigned>((T * 32 + threads - 1) / threads)),
+      dim3(threads), 0, s, dxs, rows, topk_idx, dlogits, w_r, dx_extra, T, d, E, k, kr, dx);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dedup_pairs(const int32_t* topk_idx, const int32_t* dest_row,
+                               const int32_t* place, int64_t T, int k, int E_l, int EP,
+                               int32_t* pdest, int32_t* ntok, cudaStream_t s) {
+  launch_k(dedup_pairs_kernel, dim3(1), dim3(kPairThreads), 0, s, topk_idx, dest_row, place, T, k,
+      E_l, EP, pdest, ntok);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dedup_dgates(const int32_t* dest_row, const int32_t* topk_idx,
+                                const int32_t* pdest, const int32_t* place, int E_l, int EP,
+                                const float* dgpart, int64_t T, int k, float* dgates,
+                                cudaStream_t s) {
+  if (T == 0) return cudaSuccess;
+  const int64_t n = T * k;
+  launch_k(dedup_dgates_kernel, dim3(static_cast<unsigned>((n + 255) / 256)), dim3(256), 0, s,
+      dest_row, topk_idx, pdest, place, E_l, EP, dgpart, T, k, dgates);
   return cudaGetLastError();
 }
 
@@ -307,6 +439,7 @@ cudaError_t launch_permute(const uint16_t* x, const int32_t* topk_idx, int64_t T
   launch_k(rank_kernel, dim3(nchunks), dim3(kChunk), smem, s, topk_idx, T, k, E, C, chunk_hist, off,
       dest_row);
   const int threads = 256;
+  if (!xs) return cudaGetLastError();   // indices only (the dedup dispatch reads x directly)
   launch_k(scatter_kernel, dim3(static_cast<unsigned>((T * 32 + threads - 1) / threads)),
       dim3(threads), 0, s, x, dest_row, T, d, k, xs);
   return cudaGetLastError();

@@ -48,11 +48,15 @@ def _all_gather_bytes(payload: bytes, group=None) -> bytes:
 
 
 class MoELayer:
-    def __init__(self, dims: LayerDims, device: int = 0, group=None, fused: bool = True):
+    def __init__(self, dims: LayerDims, device: int = 0, group=None, fused: bool = True,
+                 dedup: bool = False):
         """fused=True uses the compute+all-to-all entry points (moe_expert_ffn_combine,
-        moe_expert_ffn_bwd_dispatch); False issues the step-by-step calls (same results)."""
+        moe_expert_ffn_bwd_dispatch); False issues the step-by-step calls (same results).
+        dedup=True (k > 1) uses the deduplicated all-to-alls (NEXT-4, reading R18: one row per
+        (token, owner) pair; the combine partials add one bf16 rounding)."""
         self.dims = dims
         self.fused = fused
+        self.dedup = bool(dedup) and dims.k > 1
         self.overlap = True   # shared-expert GEMMs beside dispatch / combine_bwd (E_s > 0)
         self._side = None
         self.placement = list(range(dims.E))   # expert -> global slot (contiguous at start)
@@ -67,6 +71,10 @@ class MoELayer:
         self.R = L.moe_recv_rows_max(self.shape)
         R = self.R
         heap = 2 * (R * d * 2) + 2 * (max(T * k, 1) * d * 2) + 4 * 4096
+        if self.dedup:
+            self.tok_max = max(L.moe_dedup_token_rows_max(self.shape), 1)
+            self.pair_max = max(L.moe_dedup_pair_rows_max(self.shape), 1)
+            heap += self.tok_max * (d * 2 + 8 * k) + self.pair_max * 4 * k + 4 * 4096
         self.ctx = L.Context(self.shape, device, heap)
         if dims.ep_size > 1:
             handles = _all_gather_bytes(self.ctx.export_handle(), group)
@@ -78,6 +86,18 @@ class MoELayer:
         self.dxs = self.ctx.symm_empty((max(T * k, 1), d), torch.bfloat16)
         dev = self.device
         bf, f32, i32 = torch.bfloat16, torch.float32, torch.int32
+        if self.dedup:
+            # owner side (peer-written): token rows (x in the forward, dy in the backward) and
+            # each pair's slot lists; source side: dgpart (the pair partials reuse ys / dxs)
+            EP = dims.ep_size
+            self.xt = self.ctx.symm_empty((self.tok_max, d), torch.bfloat16)
+            self.rlist = self.ctx.symm_empty((self.tok_max, k), torch.int32)
+            self.glist = self.ctx.symm_empty((self.tok_max, k), torch.float32)
+            self.dgpart = self.ctx.symm_empty((self.pair_max, k), torch.float32)
+            self.pdest = torch.empty((T, EP), dtype=i32, device=dev)
+            self.ntok = torch.empty((EP,), dtype=i32, device=dev)
+            self.dlayout = torch.zeros((EP * EP,), dtype=i32, device=dev)
+            self.dg_own = torch.empty((self.tok_max, k), dtype=f32, device=dev)
         self.logits = torch.empty((T, E), dtype=f32, device=dev)
         self.topk_idx = torch.empty((T, k), dtype=i32, device=dev)
         self.gates = torch.empty((T, k), dtype=f32, device=dev)
@@ -169,6 +189,8 @@ class MoELayer:
         L.moe_router_logits(c, x, self.w_r, self.bias, self.logits)
         L.moe_route(c, self.logits, self.topk_idx, self.gates)
         self._mark("F0+F1 router,route")
+        if self.dedup:
+            return self._forward_dedup(x)
         L.moe_permute(c, x, self.topk_idx, self.counts, self.dest_row, self.xs)
         self._mark("F2 permute")
         ranges = self._ranges()
@@ -207,6 +229,63 @@ class MoELayer:
             self._mark("F5+F6 combine")
         return self.y
 
+    # ------------------------------------------------------------------ NEXT-4 dedup all-to-all
+    def _forward_dedup(self, x):
+        c, T, f = self.ctx, self.dims.T_local, self.dims.f
+        L.moe_permute(c, x, self.topk_idx, self.counts, self.dest_row, None)
+        L.moe_dedup_pairs(c, self.topk_idx, self.dest_row, self.pdest, self.ntok)
+        self._mark("F2 permute (indices) + pairs")
+
+        def dispatch(s):
+            L.moe_dedup_dispatch(c, x, self.counts, self.ntok, self.pdest, self.dest_row,
+                                 self.topk_idx, self.gates, self.layout, self.dlayout, self.xt,
+                                 self.rlist, self.glist, self.xr, stream=s)
+        y_extra = None
+        if self.fs and self.overlap:
+            self._concurrent(dispatch, lambda s: L.moe_expert_ffn(
+                c, x, self.rows_T, 1, T, self.fs, self.w_gu_s, self.w_down_s, self.g_u_h_s,
+                self.y_s, stream=s))
+            y_extra = self.y_s
+        else:
+            dispatch(None)
+            if self.fs:
+                L.moe_expert_ffn(c, x, self.rows_T, 1, T, self.fs, self.w_gu_s, self.w_down_s,
+                                 self.g_u_h_s, self.y_s)
+                y_extra = self.y_s
+        self._mark("F3 dedup dispatch + expand")
+        L.moe_expert_ffn(c, self.xr, self.expert_rows, self.E_l, self.R, f, self.w_gu, self.w_down,
+                         self.g_u_h, self.out)
+        self._mark("F4 expert ffn")
+        L.moe_dedup_combine(c, self.out, self.dlayout, self.rlist, self.glist, self.pdest, y_extra,
+                            self.ys, self.y)
+        self._mark("F5+F6 dedup combine")
+        return self.y
+
+    def _backward_dedup(self, dy, accumulate):
+        c, T, f = self.ctx, self.dims.T_local, self.dims.f
+
+        def combine_bwd(s):
+            L.moe_dedup_combine_bwd(c, dy, self.pdest, self.layout, self.dlayout, self.rlist,
+                                    self.glist, self.out, self.xt, self.dg_own, self.dout_r,
+                                    stream=s)
+        shared_done = False
+        if self.fs and self.overlap:
+            self._concurrent(combine_bwd, lambda s: L.moe_expert_ffn_bwd(
+                c, self.x, self.rows_T, 1, T, self.fs, self.w_gu_s, self.w_down_s, self.g_u_h_s,
+                dy, self.dgu_s, self.dx_s, self.dw_gu_s, self.dw_down_s, accumulate, stream=s))
+            shared_done = True
+        else:
+            combine_bwd(None)
+        self._mark("B6+B5 dedup combine_bwd")
+        L.moe_expert_ffn_bwd(c, self.xr, self.expert_rows, self.E_l, self.R, f, self.w_gu,
+                             self.w_down, self.g_u_h, self.dout_r, self.dgu, self.dxr, self.dw_gu,
+                             self.dw_down, accumulate)
+        self._mark("B4 expert ffn_bwd")
+        L.moe_dedup_dispatch_bwd(c, self.dxr, self.dlayout, self.rlist, self.dg_own, self.pdest,
+                                 self.dest_row, self.topk_idx, self.dxs, self.dgpart, self.dgates)
+        self._mark("B3 dedup dispatch_bwd")
+        return self._backward_tail(dy, accumulate, shared_done)
+
     # ------------------------------------------------------------------ NEXT-1 chunked overlap
     # Owner slots cut into `chunks` ranges: the all-to-all of range i+1 (side stream, comm_sms
     # SMs) runs beside the first expert GEMM of range i (this stream, the other SMs).  Used by
@@ -215,7 +294,7 @@ class MoELayer:
 
     def _ranges(self):
         E_l, n = self.E_l, min(self.chunks, self.E_l)
-        if not self.fused or self.dims.ep_size == 1 or n < 2:
+        if not self.fused or self.dedup or self.dims.ep_size == 1 or n < 2:
             return None
         bounds = [E_l * i // n for i in range(n + 1)]
         return list(zip(bounds[:-1], bounds[1:]))
@@ -295,6 +374,8 @@ class MoELayer:
         (and dw_gu_s, dw_down_s) as fp32 per-rank gradients."""
         c = self.ctx
         f, T = self.dims.f, self.dims.T_local
+        if self.dedup:
+            return self._backward_dedup(dy, accumulate)
         ranges = self._ranges()
         if ranges:
             return self._backward_chunked(dy, accumulate, ranges)
@@ -345,8 +426,12 @@ class MoELayer:
             # dl is k-sparse: dx_router is gathered inside the permute backward (exact fp32)
             L.moe_router_logits_bwd(c, self.x, self.w_r, self.dlogits, None, self.dw_r, accumulate)
             self._mark("B1+B0 route_bwd,router dW")
-            L.moe_permute_bwd_router(c, self.dxs, self.dest_row, self.topk_idx, self.dlogits,
-                                     self.w_r, dx_extra, self.dx)
+            if self.dedup:   # dxs holds the dedup pair partials, rows pdest [T, EP]
+                L.moe_dedup_permute_bwd_router(c, self.dxs, self.pdest, self.topk_idx,
+                                               self.dlogits, self.w_r, dx_extra, self.dx)
+            else:
+                L.moe_permute_bwd_router(c, self.dxs, self.dest_row, self.topk_idx, self.dlogits,
+                                         self.w_r, dx_extra, self.dx)
         else:
             L.moe_router_logits_bwd(c, self.x, self.w_r, self.dlogits, self.dx_router, self.dw_r,
                                     accumulate)
@@ -451,6 +536,15 @@ class MoELayer:
     def kernel_launches(self, fwd=True, bwd=True) -> int:
         """Number of libmoe kernels one forward / backward launches (for bench.py)."""
         n = 0
+        if self.dedup:
+            # fwd: router GEMM, route, permute (2, no scatter), pairs, dispatch (transfer +
+            # expand), ffn (2), combine (reduce + gather); bwd: combine_bwd (transfer + expand),
+            # ffn_bwd (4), dispatch_bwd (reduce + dgates), route_bwd, router bwd (3), permute_bwd
+            if fwd:
+                n += 1 + 1 + 2 + 1 + 2 + 2 + 2 + (2 if self.fs else 0)
+            if bwd:
+                n += 2 + 4 + 2 + 1 + 3 + 1 + (4 if self.fs else 0)
+            return n
         if fwd:
             # router GEMM, route, permute (3), dispatch (1 fused launch), ffn (2), combine (2)
             n += 1 + 1 + 3 + 1 + 2 + 2 + (2 if self.fs else 0)

@@ -46,6 +46,8 @@ def main():
     ap.add_argument("--rebalance", action="store_true",
                     help="observe loads, run Alg. 2 (moe_rebalance) and migrate before checking")
     ap.add_argument("--chunks", type=int, default=None, help="MoELayer.chunks (NEXT-1 overlap)")
+    ap.add_argument("--dedup", action="store_true",
+                    help="NEXT-4 deduplicated all-to-alls (pair tables and xr checked bitwise)")
     ap.add_argument("--graph", action="store_true",
                     help="also replay the step from a CUDA graph (device-side collective epoch)")
     args = ap.parse_args()
@@ -57,7 +59,7 @@ def main():
     from tests.test_gpu_layer import build_layer, oracle_layer
     from tests.helpers import TOL, f64, rel_err
 
-    layer = build_layer(cfg, ep_size=ep, ep_rank=rank, device=local)
+    layer = build_layer(cfg, ep_size=ep, ep_rank=rank, device=local, dedup=args.dedup)
     layer.fused = not args.stepwise
     if args.chunks is not None:
         layer.chunks = args.chunks
@@ -122,6 +124,10 @@ def main():
         "dw_gu": gather(layer.dw_gu), "dw_down": gather(layer.dw_down), "dw_r": gather(layer.dw_r),
         "dgates": gather(layer.dgates),
     }
+    if args.dedup:
+        g["pdest"] = gather(layer.pdest)
+        g["dlayout"] = gather(layer.dlayout)
+        g["xr"] = gather(layer.xr)
     if cfg.E_s:
         g["dw_gu_s"] = gather(layer.dw_gu_s)
         g["dw_down_s"] = gather(layer.dw_down_s)
@@ -152,6 +158,26 @@ def main():
         lay_ok &= bool((lay[ep * cfg.E:ep * cfg.E + E_l] == padded[r]["expert_rows"]).all())
         lay_ok &= bool((lay[ep * cfg.E + E_l:] == padded[r]["seg_base"]).all())
     checks["layout"] = lay_ok
+    if args.dedup:
+        from oracle import dedup as dd
+        P = dd.plan(fw["topk_idx"], fw["gates"], cfg.E, ep, fw["C"], align=128, placement=place)
+        ok = True
+        for r in range(ep):
+            pb = P["layout"]["pair_base"][r]
+            ts = P["pairs"][r]["tslot"]
+            want = np.where(ts >= 0, ts + pb[None, :], -1)
+            ok &= bool((g["pdest"][r].cpu().numpy() == want).all())
+            ok &= bool((g["dlayout"][r].cpu().numpy() == P["ntok_all"].reshape(-1)).all())
+        checks["dedup_pairs"] = ok
+        # every owner's expanded receive buffer holds x rows at the plain receive layout
+        xa = x_all
+        base = P["base"]   # receive rows under the placement in force (migration included)
+        ok = True
+        for q in range(ep):
+            xr = g["xr"][q].cpu()
+            t, j = np.nonzero((base["recv_row"] >= 0) & (base["owner"] == q))
+            ok &= bool(torch.equal(xr[torch.as_tensor(base["recv_row"][t, j])], xa[torch.as_tensor(t)]))
+        checks["dedup_xr"] = ok
     errs = {}
     errs["y"] = rel_err(f64(cat("y")), fw["y"])
     errs["dx"] = rel_err(f64(cat("dx")), bw["dx"])

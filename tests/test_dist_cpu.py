@@ -85,3 +85,60 @@ def test_oracle_ep_ranks_partition_the_layer():
                 seg0, seg1 = lay["seg_base"][el], lay["seg_base"][el] + lay["expert_rows"][el]
                 m = kept & (idx == q * (E // ep) + el)
                 assert ((plan["recv_row"][m] >= seg0) & (plan["recv_row"][m] < seg1)).all()
+
+
+def _dedup_worker(rank, world, port, q):
+    """One EP rank of the deduplicated exchange (reading R18) with gloo standing in for the
+    NVSwitch stores: local pairs from the rank's own shard, the pair-count exchange, token rows
+    sent once per (token, owner) pair, and the owner's expand into the plain receive layout."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import synth
+        from oracle import dedup as dd
+        from oracle import moe_ref as ref
+        T, E, k, d = 256, 16, 4, 8
+        T_r, E_l = T // world, E // world
+        idx, gates = ref.route(synth.random_logits(T, E, seed=5).numpy(), k)
+        C = ref.capacity(1.0, k, T_r, E)
+        mine = slice(rank * T_r, (rank + 1) * T_r)
+        pos = ref.positions(idx[mine], E, C)                            # this rank only
+        pr = dd.pairs(pos["dest_row"], idx[mine], np.arange(E), E_l, world)
+        ntok = torch.tensor(pr["ntok"], dtype=torch.int64)
+        allnt = [torch.empty_like(ntok) for _ in range(world)]
+        dist.all_gather(allnt, ntok)                                   # the pair-count exchange
+        ntok_all = torch.stack(allnt).numpy()
+        full = dd.plan(idx, gates, E, world, C, align=128)            # single-process reference
+        ok_counts = (ntok_all == full["ntok_all"]).all()
+        x = np.random.default_rng(1).standard_normal((T, d))
+        send = [x[mine][pr["tslot"][:, qq] >= 0] for qq in range(world)]   # tslot order
+        recv = [None] * world
+        dist.all_gather_object(recv, send)                            # gloo as the transport
+        xt = np.concatenate([recv[r][rank] for r in range(world)])   # (source, tslot) order
+        n_rows = int(full["base"]["layouts"][rank]["seg_base"][-1])
+        xr = dd.expand(xt, full["rlist"][rank], n_rows)
+        plain = np.zeros((n_rows, d))
+        b = full["base"]
+        t, j = np.nonzero((b["owner"] == rank) & (b["recv_row"] >= 0))
+        plain[b["recv_row"][t, j]] = x[t]
+        ok_xr = np.array_equal(xr, plain)
+        q.put((rank, bool(ok_counts), bool(ok_xr)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_dedup_exchange():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_dedup_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in res:
+        assert all(r[1:]), r

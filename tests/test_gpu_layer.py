@@ -25,11 +25,11 @@ CASES = {
 }
 
 
-def build_layer(cfg, ep_size=1, ep_rank=0, device=0):
+def build_layer(cfg, ep_size=1, ep_rank=0, device=0, dedup=False):
     from paper_2605_05049_b200 import LayerDims, MoELayer
     T_r = cfg.T // ep_size
     dims = LayerDims(T_r, cfg.d, cfg.E, cfg.k, cfg.f, cfg.E_s, cfg.cf, ep_size, ep_rank)
-    layer = MoELayer(dims, device=device)
+    layer = MoELayer(dims, device=device, dedup=dedup)
     E_l = cfg.E // ep_size
     experts = range(ep_rank * E_l, (ep_rank + 1) * E_l)
     dev = torch.device(f"cuda:{device}")
@@ -58,12 +58,17 @@ def oracle_layer(cfg, x, dy, logits, ep=1):
     return fw, bw
 
 
-@pytest.mark.parametrize("name", list(CASES))
-def test_layer_ep1_parity(name):
+@pytest.mark.parametrize("name,dedup", [(n, False) for n in CASES] +
+                         [(n, True) for n in ("mixtral_small", "dsmoe_small", "v3_small_zipf",
+                                              "drops")])
+def test_layer_ep1_parity(name, dedup):
+    """dedup=True: the NEXT-4 deduplicated all-to-alls (reading R18) on the same checks, plus
+    the pair tables bit-exact against oracle/dedup.py and xr bitwise equal to the plain
+    dispatch's receive buffer."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     cfg = CASES[name]
-    layer = build_layer(cfg)
+    layer = build_layer(cfg, dedup=dedup)
     x = synth.tokens(cfg).cuda()
     dy = synth.grad_output(cfg).cuda()
     y = layer.forward(x).clone()
@@ -85,6 +90,25 @@ def test_layer_ep1_parity(name):
     E_l = cfg.E
     assert (lay[:cfg.E] == fw["plan"]["counts_all"][0]).all()
     assert (lay[cfg.E:cfg.E + E_l] == fw["plan"]["layouts"][0]["expert_rows"]).all()
+    if dedup:
+        from oracle import dedup as dd
+        P = dd.plan(fw["topk_idx"], fw["gates"], cfg.E, 1, fw["C"], align=128)
+        assert (layer.pdest.cpu().numpy() == P["pairs"][0]["tslot"]).all()   # EP=1: pair_base 0
+        assert (layer.ntok.cpu().numpy() == P["ntok_all"][0]).all()
+        assert (layer.dlayout.cpu().numpy() == P["ntok_all"].reshape(-1)).all()
+        n = int(P["layout"]["tok_rows"][0])
+        assert (layer.rlist[:n].cpu().numpy() == P["rlist"][0]).all()
+        gl = layer.glist[:n].cpu().numpy()
+        assert (gl == layer.gates.cpu().numpy()[P["tok"][0]] * (P["rlist"][0] >= 0)).all()
+        # the expanded receive buffer is the plain dispatch's, bit for bit
+        base = fw["plan"]
+        xr = layer.xr.cpu()
+        t, j = np.nonzero(base["recv_row"] >= 0)
+        assert torch.equal(xr[torch.as_tensor(base["recv_row"][t, j])], x.cpu()[torch.as_tensor(t)])
+        n_rows = int(lay[cfg.E + E_l + E_l])
+        pad = np.ones(n_rows, bool)
+        pad[base["recv_row"][t, j]] = False
+        assert (xr[:n_rows][torch.as_tensor(pad)] == 0).all()
     # floating parts within tolerance
     errs = {}
     errs["gates"] = rel_err(f64(layer.gates), fw["gates"])
