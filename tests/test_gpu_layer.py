@@ -100,8 +100,8 @@ def test_layer_ep1_parity(name, dedup):
         assert (layer.rlist[:n].cpu().numpy() == P["rlist"][0]).all()
         gl = layer.glist[:n].cpu().numpy()
         assert (gl == layer.gates.cpu().numpy()[P["tok"][0]] * (P["rlist"][0] >= 0)).all()
-        # the expanded receive buffer is the plain dispatch's, bit for bit
-        base = fw["plan"]
+        # the expanded receive buffer is the plain dispatch's, bit for bit (128-aligned layout)
+        base = P["base"]
         xr = layer.xr.cpu()
         t, j = np.nonzero(base["recv_row"] >= 0)
         assert torch.equal(xr[torch.as_tensor(base["recv_row"][t, j])], x.cpu()[torch.as_tensor(t)])
