@@ -45,8 +45,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--rebalance", action="store_true",
                     help="expert migration before timing: observe loads, Alg. 2, move experts")
-    ap.add_argument("--dedup", action="store_true",
-                    help="NEXT-4 deduplicated all-to-alls (one row per (token, owner) pair)")
+    ap.add_argument("--dedup", nargs="?", const="dispatch", default=None,
+                    choices=["dispatch", "all"],
+                    help="NEXT-4 deduplicated all-to-alls (one row per (token, owner) pair): "
+                         "'dispatch' = dispatch + combine_bwd (default), 'all' = all four")
     ap.add_argument("--stepwise", action="store_true",
                     help="step-by-step C-ABI calls instead of the fused compute+all-to-all ones")
     ap.add_argument("--cpu-sample-tokens", type=int, default=0)
@@ -181,20 +183,26 @@ def layer_roofline(layer, cfg, peaks, nvl_gbs=900.0):
         ingress = int(cm[:, mine].sum() - cm[r, mine].sum()) * row
         t = 3 * 2 * T_r * d * E / pi                          # router fwd + dgrad + wgrad
         if layer.dedup:
-            # pairs instead of slots on NVLink; HBM: expand (pairs -> receive rows), reduce
-            # (receive rows -> pairs), gathers over pairs, bwd expand also reads O
+            # pairs instead of slots on NVLink in the deduplicated directions; HBM: the owner's
+            # expands (pairs -> receive rows), and for mode "all" the pair reduces / gathers
             nm = layer.dlayout.view(EP, EP).to(torch.int64).cpu()
             pairs_out, pairs_in = int(nm[r].sum()), int(nm[:, r].sum())
-            egress = (pairs_out - int(nm[r, r])) * row
-            ingress = (pairs_in - int(nm[r, r])) * row
-            t += 2 * (pairs_out * row + T_r * row) / bh         # y / dx gathers over pairs
-            t += 2 * (pairs_in * row + recv * row) / bh         # fwd expand, dispatch_bwd reduce
-            t += (recv * row + pairs_in * row) / bh             # combine reduce
-            t += (pairs_in * row + 2 * recv * row) / bh         # bwd expand (+ O for dg)
+            p_egress = (pairs_out - int(nm[r, r])) * row
+            p_ingress = (pairs_in - int(nm[r, r])) * row
+            t += 2 * (pairs_in * row + recv * row) / bh         # fwd expand, bwd expand (dO)
+            if layer.dedup_mode == "all":
+                t += 2 * (pairs_out * row + T_r * row) / bh     # y / dx gathers over pairs
+                t += 2 * (recv * row + pairs_in * row) / bh     # combine / dispatch_bwd reduces
+                t += recv * row / bh                            # bwd expand reads O for dg
+                t += 4 * max(p_egress, p_ingress) / bn
+            else:
+                t += (T_r * row + send * row) / bh              # dgates dots at the source
+                t += 2 * (send * row + T_r * row) / bh          # unpermute, permute_bwd
+                t += 2 * max(p_egress, p_ingress) / bn + 2 * max(egress, ingress) / bn
         else:
             t += 2 * (T_r * row + send * row) / bh            # permute, permute_bwd
             t += 2 * (send * row + T_r * row) / bh            # unpermute, combine_bwd dO rows
-        t += 4 * max(egress, ingress) / bn                    # dispatch, combine, their twins
+            t += 4 * max(egress, ingress) / bn                # dispatch, combine, their twins
         t += 18 * recv * d * f / pi                           # expert GEMMs fwd + bwd
         if cfg.E_s:
             t += 18 * T_r * d * cfg.E_s * f / pi
@@ -507,7 +515,7 @@ def run_ours(args):
             "capacity_factor": cfg.cf, "zipf_s": cfg.zipf_s,
             "parallelism": f"ep{world}", "tokens_per_rank": T_r,
             "expert_migration": rebal,
-            "dedup_a2a": bool(layer.dedup),
+            "dedup_a2a": layer.dedup_mode,
             "a2a_gemm_chunks": len(layer._ranges() or [None]),
             "cuda_graph": use_graph,
             "eager_ms_per_step": eager_ms,

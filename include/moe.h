@@ -398,6 +398,17 @@ moe_status moe_dedup_combine_bwd(moe_ctx* ctx, const moe_bf16* dy, const int32_t
                                  const int32_t* rlist, const float* glist, const moe_bf16* out,
                                  moe_bf16* dyt, float* dg_own, moe_bf16* dout_r,
                                  moe_stream stream);
+/* Collective.  B6+B5 with the dispatch direction deduplicated and the combine left to the
+ * fused GEMM2 stores (moe_expert_ffn_combine: O rows already sit in this rank's ys):
+ *   dgates[t,j] = <dy[t], ys[dest_row[t,j]]> (fp32, 0 for dropped slots) at the source, dy[t]
+ * once per pair into the owner's dyt, then on the owner dout_r[rl] = bf16(g * dyt[u]) (padding
+ * rows zeroed).  Bit-identical dgates and dout_r to moe_combine_bwd. */
+moe_status moe_dedup_combine_bwd_ys(moe_ctx* ctx, const moe_bf16* dy, const float* gates,
+                                    const int32_t* dest_row, const moe_bf16* ys,
+                                    const int32_t* pdest, const int32_t* layout,
+                                    const int32_t* dlayout, const int32_t* rlist,
+                                    const float* glist, moe_bf16* dyt, float* dgates,
+                                    moe_bf16* dout_r, moe_stream stream);
 /* Collective.  B3 deduplicated: dxpart[pair row] = bf16( sum_j dxr[rlist[u][j]] ) (fp32, j
  * order) and dgpart[pair row][j] = dg_own[u][j] go to each source; then locally
  * dgates[t,j] = dgpart[pdest[t, owner(e_j)]][j] (0 for dropped slots). */

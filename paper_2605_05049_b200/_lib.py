@@ -95,6 +95,7 @@ _SIGS = {
     "moe_dedup_combine": [P] * 10,
     "moe_dedup_combine_bwd": [P] * 12,
     "moe_dedup_dispatch_bwd": [P] * 12,
+    "moe_dedup_combine_bwd_ys": [P] * 14,
     "moe_dedup_permute_bwd_router": [P] * 9,
 }
 for _name, _args in _SIGS.items():
@@ -463,3 +464,13 @@ def moe_dedup_permute_bwd_router(ctx, dxpart, pdest, topk_idx, dlogits, w_r, dx_
         ctx.handle, _ptr(dxpart, BF16, "dxpart"), _ptr(pdest, I32T, "pdest"),
         _ptr(topk_idx, I32T, "topk_idx"), _ptr(dlogits, F32, "dlogits"), _ptr(w_r, BF16, "w_r"),
         _ptr(dx_extra, BF16, "dx_extra"), _ptr(dx, BF16, "dx"), _stream(stream)))
+
+
+def moe_dedup_combine_bwd_ys(ctx, dy, gates, dest_row, ys, pdest, layout, dlayout, rlist, glist,
+                             dyt, dgates, dout_r, stream=None):
+    _check("moe_dedup_combine_bwd_ys", _lib.moe_dedup_combine_bwd_ys(
+        ctx.handle, _ptr(dy, BF16, "dy"), _ptr(gates, F32, "gates"),
+        _ptr(dest_row, I32T, "dest_row"), _ptr(ys, BF16, "ys"), _ptr(pdest, I32T, "pdest"),
+        _ptr(layout, I32T, "layout"), _ptr(dlayout, I32T, "dlayout"), _ptr(rlist, I32T, "rlist"),
+        _ptr(glist, F32, "glist"), _ptr(dyt, BF16, "dyt"), _ptr(dgates, F32, "dgates"),
+        _ptr(dout_r, BF16, "dout_r"), _stream(stream)))

@@ -32,6 +32,7 @@ struct moe_ctx {
   int32_t* d_err = nullptr;
   int32_t* d_done = nullptr;
   int32_t* d_scratch = nullptr;   // permute workspace
+  int32_t* d_dedup_scratch = nullptr;   // dedup pairs workspace (masks, block bases, ticket)
   int32_t* d_rows_T = nullptr;    // one int32 = T_local (router GEMM group size)
   uint16_t* d_dl_split = nullptr; // router backward: [T, 2*Ep] bf16 = [hi | lo] of dlogits
   uint16_t* d_wr2 = nullptr;      // [2*Ep, d] bf16 = [W_r; W_r] (dense dx_router path)
@@ -270,6 +271,9 @@ moe_status moe_ctx_create(moe_ctx** out, const moe_shape* shape, int device, siz
   const int64_t scratch = moe::permute_scratch_ints(shape->T_local, shape->k, shape->E);
   if (e == cudaSuccess) e = cudaMalloc(&c->d_scratch, scratch * 4);
   if (e == cudaSuccess) e = cudaMemset(c->d_scratch, 0, scratch * 4);   // incl. the block ticket
+  const int64_t dscratch = moe::dedup_scratch_ints(shape->T_local, shape->ep_size);
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_dedup_scratch, dscratch * 4);
+  if (e == cudaSuccess) e = cudaMemset(c->d_dedup_scratch, 0, dscratch * 4);
   if (e == cudaSuccess) e = cudaMalloc(&c->d_rows_T, 16);
   int32_t tl = static_cast<int32_t>(shape->T_local);
   if (e == cudaSuccess) e = cudaMemcpy(c->d_rows_T, &tl, 4, cudaMemcpyHostToDevice);
@@ -423,6 +427,7 @@ moe_status moe_ctx_destroy(moe_ctx* c) {
   cudaFree(c->d_sk_ws);
   cudaFree(c->d_sk_flags);
   cudaFree(c->d_scratch);
+  cudaFree(c->d_dedup_scratch);
   cudaFree(c->d_rows_T);
   cudaFree(c->d_dl_split);
   cudaFree(c->d_wr2);
@@ -878,7 +883,8 @@ moe_status moe_dedup_pairs(moe_ctx* c, const int32_t* topk_idx, const int32_t* d
                            int32_t* pdest, int32_t* ntok, moe_stream s) {
   MOE_REQUIRE(c && topk_idx && dest_row && pdest && ntok);
   return cuda_status(moe::launch_dedup_pairs(topk_idx, dest_row, c->d_place, c->s.T_local, c->s.k,
-                                             c->E_l, c->s.ep_size, pdest, ntok, st(s)));
+                                             c->E_l, c->s.ep_size, pdest, ntok,
+                                             c->d_dedup_scratch, st(s)));
 }
 
 moe_status moe_dedup_dispatch(moe_ctx* c, const moe_bf16* x, const int32_t* counts,
@@ -893,7 +899,8 @@ moe_status moe_dedup_dispatch(moe_ctx* c, const moe_bf16* x, const int32_t* coun
   CommArgs a = comm_args(c);
   MOE_TRY_CUDA(moe::launch_dedup_forward(a, 0, layout, dlayout, counts, ntok, c->recv_rows, x,
                                          pdest, dest_row, topk_idx, gates, heap_off(c, xt),
-                                         heap_off(c, rlist), heap_off(c, glist), st(s)));
+                                         heap_off(c, rlist), heap_off(c, glist), nullptr, nullptr,
+                                         st(s)));
   return cuda_status(moe::launch_dedup_expand(a, 0, layout, dlayout, xt, rlist, glist, nullptr, xr,
                                               nullptr, st(s)));
 }
@@ -924,9 +931,28 @@ moe_status moe_dedup_combine_bwd(moe_ctx* c, const moe_bf16* dy, const int32_t* 
   MOE_TRY_CUDA(moe::launch_dedup_forward(a, 1, const_cast<int32_t*>(layout),
                                          const_cast<int32_t*>(dlayout), nullptr, nullptr, 0, dy,
                                          pdest, nullptr, nullptr, nullptr, heap_off(c, dyt), 0, 0,
-                                         st(s)));
+                                         nullptr, nullptr, st(s)));
   return cuda_status(moe::launch_dedup_expand(a, 1, layout, dlayout, dyt, rlist, glist, out,
                                               dout_r, dg_own, st(s)));
+}
+
+moe_status moe_dedup_combine_bwd_ys(moe_ctx* c, const moe_bf16* dy, const float* gates,
+                                    const int32_t* dest_row, const moe_bf16* ys,
+                                    const int32_t* pdest, const int32_t* layout,
+                                    const int32_t* dlayout, const int32_t* rlist,
+                                    const float* glist, moe_bf16* dyt, float* dgates,
+                                    moe_bf16* dout_r, moe_stream s) {
+  MOE_REQUIRE(c && dy && gates && dest_row && ys && pdest && layout && dlayout && rlist && glist &&
+              dyt && dgates && dout_r);
+  if (!c->peers_ready) return MOE_ERR_NOT_READY;
+  if (!in_heap(c, dyt)) return MOE_ERR_NOT_SYMMETRIC;
+  CommArgs a = comm_args(c);
+  MOE_TRY_CUDA(moe::launch_dedup_forward(a, 1, const_cast<int32_t*>(layout),
+                                         const_cast<int32_t*>(dlayout), nullptr, nullptr, 0, dy,
+                                         pdest, dest_row, nullptr, gates, heap_off(c, dyt), 0, 0,
+                                         ys, dgates, st(s)));
+  return cuda_status(moe::launch_dedup_expand(a, 1, layout, dlayout, dyt, rlist, glist, nullptr,
+                                              dout_r, nullptr, st(s)));
 }
 
 moe_status moe_dedup_dispatch_bwd(moe_ctx* c, const moe_bf16* dxr, const int32_t* dlayout,

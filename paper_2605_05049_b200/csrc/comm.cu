@@ -486,7 +486,8 @@ __global__ void dedup_forward_kernel(CommArgs a, int32_t* __restrict__ layout,
                                      const int32_t* __restrict__ dest_row,
                                      const int32_t* __restrict__ topk_idx,
                                      const float* __restrict__ gates, int64_t tok_off,
-                                     int64_t rlist_off, int64_t glist_off) {
+                                     int64_t rlist_off, int64_t glist_off,
+                                     const uint16_t* __restrict__ ys, float* __restrict__ dgates) {
   pdl_wait();
   pdl_trigger();
   __shared__ FwdTables tb;
@@ -518,7 +519,32 @@ __global__ void dedup_forward_kernel(CommArgs a, int32_t* __restrict__ layout,
   const int64_t row_bytes = static_cast<int64_t>(d) * 2;
   const int parts = row_parts(nvec);
   const int64_t n_items = a.T * parts;
-  for (int64_t w = gwarp; w < n_items; w += nwarps) {
+  // MODE 1 with ys: T more items, dgates[t,j] = <dy[t], ys[dest_row[t,j]]> at the source
+  // (the fused forward leaves no O on the owner: its GEMM2 stored the rows into ys)
+  const int64_t n_dot = (MODE == 1 && ys) ? a.T : 0;
+  for (int64_t w = gwarp; w < n_items + n_dot; w += nwarps) {
+    if (w >= n_items) {
+      const int64_t t = w - n_items;
+      const uint4* pdy = reinterpret_cast<const uint4*>(src + t * d);
+      for (int j = 0; j < k; ++j) {
+        const int32_t row = dest_row[t * k + j];
+        float dot = 0.f;
+        if (row >= 0) {
+          const uint4* pys = reinterpret_cast<const uint4*>(ys + static_cast<int64_t>(row) * d);
+          for (int v = lane; v < nvec; v += 32) {
+            const uint4 a4 = ld_nc_v4(pdy + v), b4 = ld_nc_v4(pys + v);
+            const uint32_t aw[4] = {a4.x, a4.y, a4.z, a4.w}, bw[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+            for (int q2 = 0; q2 < 4; ++q2)
+              dot += bf16_lo(aw[q2]) * bf16_lo(bw[q2]) + bf16_hi(aw[q2]) * bf16_hi(bw[q2]);
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+        }
+        if (lane == 0) dgates[t * k + j] = dot;
+      }
+      continue;
+    }
     const int64_t t = w / parts;
     const int part = static_cast<int>(w - t * parts);
     const int32_t pd = lane < EP ? pdest[t * EP + lane] : -1;   // lane q: pair row for owner q
@@ -608,10 +634,21 @@ __global__ void dedup_expand_kernel(CommArgs a, const int32_t* __restrict__ layo
         const int32_t rl = __shfl_sync(0xffffffffu, rl_l, j);
         const float g = __shfl_sync(0xffffffffu, g_l, j);
         if (rl < 0) {
-          if (lane == 0) dg_own[u * k + j] = 0.f;
+          if (lane == 0 && dg_own) dg_own[u * k + j] = 0.f;
           continue;
         }
         uint4* pdst = reinterpret_cast<uint4*>(dst + static_cast<int64_t>(rl) * d);
+        if (!O) {   // dO rows only (dgates formed at the source)
+          for (int v = lane; v < nvec; v += 32) {
+            const uint4 a4 = ld_nc_v4(ptok + v);
+            const uint32_t aw[4] = {a4.x, a4.y, a4.z, a4.w};
+            uint32_t ow[4];
+#pragma unroll
+            for (int q2 = 0; q2 < 4; ++q2) ow[q2] = pack_bf16(g * bf16_lo(aw[q2]), g * bf16_hi(aw[q2]));
+            st_v4(pdst + v, make_uint4(ow[0], ow[1], ow[2], ow[3]));
+          }
+          continue;
+        }
         const uint4* po = reinterpret_cast<const uint4*>(O + static_cast<int64_t>(rl) * d);
         float dot = 0.f;
         for (int v = lane; v < nvec; v += 32) {
@@ -791,16 +828,17 @@ cudaError_t launch_dedup_forward(const CommArgs& a, int mode, int32_t* layout, i
                                  int64_t recv_rows_cap, const uint16_t* src,
                                  const int32_t* pdest, const int32_t* dest_row,
                                  const int32_t* topk_idx, const float* gates, int64_t tok_off,
-                                 int64_t rlist_off, int64_t glist_off, cudaStream_t s) {
-  const int64_t rows = a.T * (a.k < a.ep ? a.k : a.ep);   // pair rows bound
+                                 int64_t rlist_off, int64_t glist_off, const uint16_t* ys,
+                                 float* dgates, cudaStream_t s) {
+  const int64_t rows = a.T * (a.k < a.ep ? a.k : a.ep) + (ys ? a.T * a.k : 0);   // work bound
   if (mode == 0)
     launch_k(dedup_forward_kernel<0>, dim3(transfer_blocks(a, rows)), dim3(512), transfer_smem(a), s,
         a, layout, dlayout, counts, ntok, recv_rows_cap, src, pdest, dest_row, topk_idx, gates,
-        tok_off, rlist_off, glist_off);
+        tok_off, rlist_off, glist_off, ys, dgates);
   else
     launch_k(dedup_forward_kernel<1>, dim3(transfer_blocks(a, rows)), dim3(512), transfer_smem(a), s,
         a, layout, dlayout, counts, ntok, recv_rows_cap, src, pdest, dest_row, topk_idx, gates,
-        tok_off, rlist_off, glist_off);
+        tok_off, rlist_off, glist_off, ys, dgates);
   return cudaGetLastError();
 }
 

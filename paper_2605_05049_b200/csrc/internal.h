@@ -131,9 +131,11 @@ cudaError_t launch_permute_bwd_router_rows(const uint16_t* dxs, const int32_t* r
                                            cudaStream_t s);
 // NEXT-4 dedup, source side (reading R18): pdest [T,EP] = pair row of (t, q) or -1,
 // ntok [EP] pairs per owner; one block
+// scratch: int32 workspace of dedup_scratch_ints(T, EP) entries, zeroed once (ticket)
+int64_t dedup_scratch_ints(int64_t T, int EP);
 cudaError_t launch_dedup_pairs(const int32_t* topk_idx, const int32_t* dest_row,
                                const int32_t* place, int64_t T, int k, int E_l, int EP,
-                               int32_t* pdest, int32_t* ntok, cudaStream_t s);
+                               int32_t* pdest, int32_t* ntok, int32_t* scratch, cudaStream_t s);
 // dgates[t,j] = dgpart[pdest[t, owner(e_j)] * k + j] (0 for dropped slots)
 cudaError_t launch_dedup_dgates(const int32_t* dest_row, const int32_t* topk_idx,
                                 const int32_t* pdest, const int32_t* place, int E_l, int EP,
@@ -195,15 +197,17 @@ cudaError_t launch_reverse_transfer(const CommArgs& a, const int32_t* layout, co
 // (token, owner) pair into the owner's token buffer (tok_off); rlist/glist (rlist_off,
 // glist_off: [pair, k]) name each pair's receive rows and gates on the owner.
 //   mode 0 (dispatch): counts + pair counts exchange, layout + pair record, x rows, lists
-//   mode 1 (combine_bwd): dy rows (pair layout from dlayout)
+//   mode 1 (combine_bwd): dy rows (pair layout from dlayout); with ys also
+//     dgates[t,j] = <dy[t], ys[dest_row[t,j]]> at the source
 cudaError_t launch_dedup_forward(const CommArgs& a, int mode, int32_t* layout, int32_t* dlayout,
                                  const int32_t* counts, const int32_t* ntok,
                                  int64_t recv_rows_cap, const uint16_t* src,
                                  const int32_t* pdest, const int32_t* dest_row,
                                  const int32_t* topk_idx, const float* gates, int64_t tok_off,
-                                 int64_t rlist_off, int64_t glist_off, cudaStream_t s);
-// Owner, local: mode 0 xr[rlist[u][j]] = tok[u]; mode 1 dst[rl] = bf16(g * tok[u]) and
-// dg_own[u][j] = <tok[u], O[rl]>; both zero dst's padding rows
+                                 int64_t rlist_off, int64_t glist_off, const uint16_t* ys,
+                                 float* dgates, cudaStream_t s);
+// Owner, local: mode 0 xr[rlist[u][j]] = tok[u]; mode 1 dst[rl] = bf16(g * tok[u]) and, with
+// O, dg_own[u][j] = <tok[u], O[rl]>; both zero dst's padding rows
 cudaError_t launch_dedup_expand(const CommArgs& a, int mode, const int32_t* layout,
                                 const int32_t* dlayout, const uint16_t* tok,
                                 const int32_t* rlist, const float* glist, const uint16_t* O,

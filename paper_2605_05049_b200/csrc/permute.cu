@@ -257,57 +257,83 @@ __global__ void sum_partials_kernel(const float* __restrict__ part, int S, int E
 // Reading R18 (oracle/dedup.py `pairs`): token t has a PAIR with owner q iff one of its kept
 // slots j has owner(e_j) = place[e_j] / E_l = q.  pdest[t, q] = pair_base[q] + tslot, tslot =
 // rank of t among this rank's tokens paired with q (ascending t), pair_base = exclusive scan
-// of ntok over q; -1 if no pair.  One block: thread i owns a contiguous token range; the
-// per-owner counts are block-scanned (EP <= 8 lanes of a warp scan per thread).
+// of ntok over q; -1 if no pair.  Two launches over blocks of kPairThreads tokens:
+//   mark : owner bitmask per token, per-block pair counts (__syncthreads_count); the last
+//          block (ticket) scans the block counts per owner into block bases and ntok
+//   write: rank inside the block (warp ballots + warp prefix) + block base -> pdest
 constexpr int kPairThreads = 1024;
 
-__device__ __forceinline__ uint32_t owner_mask(const int32_t* __restrict__ topk_idx,
-                                               const int32_t* __restrict__ dest_row,
-                                               const int32_t* s_place, int64_t t, int k, int E_l) {
-  uint32_t m = 0;
-  for (int j = 0; j < k; ++j)
-    if (dest_row[t * k + j] >= 0) m |= 1u << (s_place[topk_idx[t * k + j]] / E_l);
-  return m;
-}
-
-__global__ void __launch_bounds__(kPairThreads) dedup_pairs_kernel(
+__global__ void __launch_bounds__(kPairThreads) dedup_mark_kernel(
     const int32_t* __restrict__ topk_idx, const int32_t* __restrict__ dest_row,
     const int32_t* __restrict__ place, int64_t T, int k, int E_l, int EP,
-    int32_t* __restrict__ pdest, int32_t* __restrict__ ntok) {
+    uint8_t* __restrict__ masks, int32_t* __restrict__ blk /*[nb][EP]: counts -> bases*/,
+    int32_t* __restrict__ ntok, int32_t* __restrict__ ticket) {
   pdl_wait();
   pdl_trigger();
   __shared__ int32_t s_place[256];
-  __shared__ int32_t s_warp[kPairThreads / 32][MOE_MAX_EP];
-  __shared__ int32_t s_total[MOE_MAX_EP];
+  __shared__ int s_last;
   const int E = E_l * EP;
   for (int i = threadIdx.x; i < E; i += blockDim.x) s_place[i] = place[i];
   __syncthreads();
-  const int64_t per = (T + kPairThreads - 1) / kPairThreads;
-  const int64_t t0 = threadIdx.x * per, t1 = min(T, t0 + per);
-  int32_t c[MOE_MAX_EP];
-#pragma unroll
-  for (int q = 0; q < MOE_MAX_EP; ++q) c[q] = 0;
-  for (int64_t t = t0; t < t1; ++t) {
-    const uint32_t m = owner_mask(topk_idx, dest_row, s_place, t, k, E_l);
-#pragma unroll
-    for (int q = 0; q < MOE_MAX_EP; ++q) c[q] += (m >> q) & 1u;
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * kPairThreads + threadIdx.x;
+  uint32_t m = 0;
+  if (t < T) {
+    for (int j = 0; j < k; ++j)
+      if (dest_row[t * k + j] >= 0) m |= 1u << (s_place[topk_idx[t * k + j]] / E_l);
+    masks[t] = static_cast<uint8_t>(m);
   }
-  // exclusive scan over threads, per owner: warp shuffles, then warp totals
+  for (int q = 0; q < EP; ++q) {
+    const int c = __syncthreads_count((m >> q) & 1u);
+    if (threadIdx.x == 0) blk[blockIdx.x * EP + q] = c;
+  }
+  // last block: exclusive scan of the block counts per owner, offset by pair_base[q]
+  __threadfence();
+  if (threadIdx.x == 0) s_last = (atomicAdd(ticket, 1) == static_cast<int>(gridDim.x) - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    int32_t pair_base = 0;
+    for (int q = 0; q < EP; ++q) {
+      int32_t carry = 0;
+      for (int b0 = 0; b0 < static_cast<int>(gridDim.x); b0 += 32) {
+        const int b = b0 + lane;
+        const int32_t c = b < static_cast<int>(gridDim.x) ? __ldcg(blk + b * EP + q) : 0;
+        int32_t x = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        if (b < static_cast<int>(gridDim.x)) blk[b * EP + q] = pair_base + carry + x - c;
+        carry += __shfl_sync(0xffffffffu, x, 31);
+      }
+      if (lane == 0) ntok[q] = carry;
+      pair_base += carry;
+    }
+    if (lane == 0) *ticket = 0;   // ready for the next call
+  }
+}
+
+__global__ void __launch_bounds__(kPairThreads) dedup_pdest_kernel(
+    const uint8_t* __restrict__ masks, const int32_t* __restrict__ blk, int64_t T, int EP,
+    int32_t* __restrict__ pdest) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ int32_t s_warp[kPairThreads / 32][MOE_MAX_EP];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int32_t x[MOE_MAX_EP];
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * kPairThreads + threadIdx.x;
+  const uint32_t m = t < T ? masks[t] : 0u;
+  int32_t below[MOE_MAX_EP];
 #pragma unroll
   for (int q = 0; q < MOE_MAX_EP; ++q) {
-    x[q] = c[q];
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int32_t y = __shfl_up_sync(0xffffffffu, x[q], o);
-      if (lane >= o) x[q] += y;
-    }
-    if (lane == 31) s_warp[warp][q] = x[q];
-    x[q] -= c[q];   // exclusive within the warp
+    const uint32_t bal = __ballot_sync(0xffffffffu, (m >> q) & 1u);
+    below[q] = __popc(bal & ((1u << lane) - 1u));
+    if (lane == 0) s_warp[warp][q] = __popc(bal);
   }
   __syncthreads();
-  if (threadIdx.x < MOE_MAX_EP) {
+  if (threadIdx.x < MOE_MAX_EP) {   // exclusive scan over the block's warps, per owner
     const int q = threadIdx.x;
     int32_t run = 0;
     for (int w = 0; w < kPairThreads / 32; ++w) {
@@ -315,27 +341,11 @@ __global__ void __launch_bounds__(kPairThreads) dedup_pairs_kernel(
       s_warp[w][q] = run;
       run += v;
     }
-    s_total[q] = run;
   }
   __syncthreads();
-  int32_t base[MOE_MAX_EP];
-  int32_t pb = 0;
-#pragma unroll
-  for (int q = 0; q < MOE_MAX_EP; ++q) {
-    base[q] = pb + s_warp[warp][q] + x[q];
-    pb += s_total[q];
-  }
-  for (int64_t t = t0; t < t1; ++t) {
-    const uint32_t m = owner_mask(topk_idx, dest_row, s_place, t, k, E_l);
-#pragma unroll
-    for (int q = 0; q < MOE_MAX_EP; ++q) {
-      if (q >= EP) break;
-      const bool on = (m >> q) & 1u;
-      pdest[t * EP + q] = on ? base[q] : -1;
-      base[q] += on;
-    }
-  }
-  if (threadIdx.x < EP) ntok[threadIdx.x] = s_total[threadIdx.x];
+  if (t >= T) return;
+  for (int q = 0; q < EP; ++q)
+    pdest[t * EP + q] = ((m >> q) & 1u) ? blk[blockIdx.x * EP + q] + s_warp[warp][q] + below[q] : -1;
 }
 
 // dgates[t,j] = dgpart[pdest[t, owner(e_j)] * k + j] for kept slots, 0 for dropped ones.
@@ -384,11 +394,23 @@ cudaError_t launch_permute_bwd_router_rows(const uint16_t* dxs, const int32_t* r
   return cudaGetLastError();
 }
 
+int64_t dedup_scratch_ints(int64_t T, int EP) {
+  const int64_t nb = (T + kPairThreads - 1) / kPairThreads;
+  return (T + 3) / 4 + (nb > 0 ? nb : 1) * EP + 1;   // masks (bytes), block counts, ticket
+}
+
 cudaError_t launch_dedup_pairs(const int32_t* topk_idx, const int32_t* dest_row,
                                const int32_t* place, int64_t T, int k, int E_l, int EP,
-                               int32_t* pdest, int32_t* ntok, cudaStream_t s) {
-  launch_k(dedup_pairs_kernel, dim3(1), dim3(kPairThreads), 0, s, topk_idx, dest_row, place, T, k,
-      E_l, EP, pdest, ntok);
+                               int32_t* pdest, int32_t* ntok, int32_t* scratch, cudaStream_t s) {
+  if (T == 0) return cudaMemsetAsync(ntok, 0, sizeof(int32_t) * EP, s);
+  const int64_t nb = (T + kPairThreads - 1) / kPairThreads;
+  uint8_t* masks = reinterpret_cast<uint8_t*>(scratch);
+  int32_t* blk = scratch + (T + 3) / 4;
+  int32_t* ticket = blk + nb * EP;
+  launch_k(dedup_mark_kernel, dim3(static_cast<unsigned>(nb)), dim3(kPairThreads), 0, s, topk_idx,
+      dest_row, place, T, k, E_l, EP, masks, blk, ntok, ticket);
+  launch_k(dedup_pdest_kernel, dim3(static_cast<unsigned>(nb)), dim3(kPairThreads), 0, s, masks,
+      blk, T, EP, pdest);
   return cudaGetLastError();
 }
 

@@ -52,11 +52,20 @@ class MoELayer:
                  dedup: bool = False):
         """fused=True uses the compute+all-to-all entry points (moe_expert_ffn_combine,
         moe_expert_ffn_bwd_dispatch); False issues the step-by-step calls (same results).
-        dedup=True (k > 1) uses the deduplicated all-to-alls (NEXT-4, reading R18: one row per
-        (token, owner) pair; the combine partials add one bf16 rounding)."""
+        dedup (k > 1; NEXT-4, reading R18): one row per (token, owner) pair on NVLink.
+          "dispatch" (or True): the dispatch-direction all-to-alls (dispatch, combine_bwd) are
+              deduplicated; combine and dispatch_bwd stay the per-slot transfers fused into the
+              GEMM2 / dgrad-2 epilogues (hidden under the GEMMs); results bit-identical to the
+              plain path.
+          "all": also the reverse direction, as owner-side pair reductions (one extra bf16
+              rounding of y and dx)."""
         self.dims = dims
         self.fused = fused
-        self.dedup = bool(dedup) and dims.k > 1
+        mode = "dispatch" if dedup is True else (dedup or None)
+        if mode not in (None, "dispatch", "all"):
+            raise ValueError(f"dedup must be False, True, 'dispatch' or 'all', got {dedup!r}")
+        self.dedup_mode = mode if dims.k > 1 else None
+        self.dedup = self.dedup_mode is not None
         self.overlap = True   # shared-expert GEMMs beside dispatch / combine_bwd (E_s > 0)
         self._side = None
         self.placement = list(range(dims.E))   # expert -> global slot (contiguous at start)
@@ -215,6 +224,11 @@ class MoELayer:
                                  self.g_u_h_s, self.y_s)
                 y_extra = self.y_s
                 self._mark("F4s shared ffn")
+        return self._forward_reverse(y_extra)
+
+    def _forward_reverse(self, y_extra):
+        """F4 + the per-slot combine (fused into GEMM2's epilogue unless stepwise) + F6."""
+        c, f = self.ctx, self.dims.f
         if self.fused:
             # GEMM2's epilogue stores O rows straight into the sources' ys (combine fused)
             L.moe_expert_ffn_combine(c, self.xr, self.layout, self.w_gu, self.w_down, self.g_u_h,
@@ -253,6 +267,8 @@ class MoELayer:
                                  self.g_u_h_s, self.y_s)
                 y_extra = self.y_s
         self._mark("F3 dedup dispatch + expand")
+        if self.dedup_mode == "dispatch":
+            return self._forward_reverse(y_extra)
         L.moe_expert_ffn(c, self.xr, self.expert_rows, self.E_l, self.R, f, self.w_gu, self.w_down,
                          self.g_u_h, self.out)
         self._mark("F4 expert ffn")
@@ -265,9 +281,14 @@ class MoELayer:
         c, T, f = self.ctx, self.dims.T_local, self.dims.f
 
         def combine_bwd(s):
-            L.moe_dedup_combine_bwd(c, dy, self.pdest, self.layout, self.dlayout, self.rlist,
-                                    self.glist, self.out, self.xt, self.dg_own, self.dout_r,
-                                    stream=s)
+            if self.dedup_mode == "dispatch":   # O rows are in ys (fused GEMM2 stores)
+                L.moe_dedup_combine_bwd_ys(c, dy, self.gates, self.dest_row, self.ys, self.pdest,
+                                           self.layout, self.dlayout, self.rlist, self.glist,
+                                           self.xt, self.dgates, self.dout_r, stream=s)
+            else:
+                L.moe_dedup_combine_bwd(c, dy, self.pdest, self.layout, self.dlayout, self.rlist,
+                                        self.glist, self.out, self.xt, self.dg_own, self.dout_r,
+                                        stream=s)
         shared_done = False
         if self.fs and self.overlap:
             self._concurrent(combine_bwd, lambda s: L.moe_expert_ffn_bwd(
@@ -277,6 +298,8 @@ class MoELayer:
         else:
             combine_bwd(None)
         self._mark("B6+B5 dedup combine_bwd")
+        if self.dedup_mode == "dispatch":
+            return self._backward_reverse(dy, accumulate, shared_done)
         L.moe_expert_ffn_bwd(c, self.xr, self.expert_rows, self.E_l, self.R, f, self.w_gu,
                              self.w_down, self.g_u_h, self.dout_r, self.dgu, self.dxr, self.dw_gu,
                              self.dw_down, accumulate)
@@ -396,6 +419,11 @@ class MoELayer:
             L.moe_combine_bwd(c, dy, self.gates, self.dest_row, self.ys, self.layout, self.dgates,
                               self.dout_r)
             self._mark("B6+B5 combine_bwd")
+        return self._backward_reverse(dy, accumulate, shared_done)
+
+    def _backward_reverse(self, dy, accumulate, shared_done):
+        """B4 + the per-slot dispatch_bwd (fused into dgrad-2's epilogue unless stepwise)."""
+        c, f = self.ctx, self.dims.f
         if self.fused:
             # dgrad-2's epilogue stores dX rows straight into the sources' dxs; the wgrad
             # GEMMs run while those stores drain
@@ -426,7 +454,7 @@ class MoELayer:
             # dl is k-sparse: dx_router is gathered inside the permute backward (exact fp32)
             L.moe_router_logits_bwd(c, self.x, self.w_r, self.dlogits, None, self.dw_r, accumulate)
             self._mark("B1+B0 route_bwd,router dW")
-            if self.dedup:   # dxs holds the dedup pair partials, rows pdest [T, EP]
+            if self.dedup_mode == "all":   # dxs holds the pair partials, rows pdest [T, EP]
                 L.moe_dedup_permute_bwd_router(c, self.dxs, self.pdest, self.topk_idx,
                                                self.dlogits, self.w_r, dx_extra, self.dx)
             else:
@@ -537,13 +565,15 @@ class MoELayer:
         """Number of libmoe kernels one forward / backward launches (for bench.py)."""
         n = 0
         if self.dedup:
-            # fwd: router GEMM, route, permute (2, no scatter), pairs, dispatch (transfer +
-            # expand), ffn (2), combine (reduce + gather); bwd: combine_bwd (transfer + expand),
-            # ffn_bwd (4), dispatch_bwd (reduce + dgates), route_bwd, router bwd (3), permute_bwd
+            # fwd: router GEMM, route, permute (2, no scatter), pairs (2), dispatch (transfer +
+            # expand), ffn (2), combine (reduce + gather | fused: wait + gather); bwd:
+            # combine_bwd (transfer + expand), ffn_bwd (4 | fused: 4 + wait), dispatch_bwd
+            # (reduce + dgates | fused: none), route_bwd, router bwd (3), permute_bwd
+            rev = self.dedup_mode == "dispatch" and self.fused
             if fwd:
-                n += 1 + 1 + 2 + 1 + 2 + 2 + 2 + (2 if self.fs else 0)
+                n += 1 + 1 + 2 + 2 + 2 + 2 + 2 + (2 if self.fs else 0)
             if bwd:
-                n += 2 + 4 + 2 + 1 + 3 + 1 + (4 if self.fs else 0)
+                n += 2 + 4 + (1 if rev else 2) + 1 + 3 + 1 + (4 if self.fs else 0)
             return n
         if fwd:
             # router GEMM, route, permute (3), dispatch (1 fused launch), ffn (2), combine (2)

@@ -46,7 +46,8 @@ def main():
     ap.add_argument("--rebalance", action="store_true",
                     help="observe loads, run Alg. 2 (moe_rebalance) and migrate before checking")
     ap.add_argument("--chunks", type=int, default=None, help="MoELayer.chunks (NEXT-1 overlap)")
-    ap.add_argument("--dedup", action="store_true",
+    ap.add_argument("--dedup", nargs="?", const="dispatch", default=None,
+                    choices=["dispatch", "all"],
                     help="NEXT-4 deduplicated all-to-alls (pair tables and xr checked bitwise)")
     ap.add_argument("--graph", action="store_true",
                     help="also replay the step from a CUDA graph (device-side collective epoch)")

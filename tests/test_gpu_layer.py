@@ -59,12 +59,12 @@ def oracle_layer(cfg, x, dy, logits, ep=1):
 
 
 @pytest.mark.parametrize("name,dedup", [(n, False) for n in CASES] +
-                         [(n, True) for n in ("mixtral_small", "dsmoe_small", "v3_small_zipf",
-                                              "drops")])
+                         [(n, m) for n in ("mixtral_small", "dsmoe_small", "v3_small_zipf",
+                                           "drops") for m in ("dispatch", "all")])
 def test_layer_ep1_parity(name, dedup):
-    """dedup=True: the NEXT-4 deduplicated all-to-alls (reading R18) on the same checks, plus
-    the pair tables bit-exact against oracle/dedup.py and xr bitwise equal to the plain
-    dispatch's receive buffer."""
+    """dedup: the NEXT-4 deduplicated all-to-alls (reading R18) on the same checks, plus the
+    pair tables bit-exact against oracle/dedup.py and xr bitwise equal to the plain dispatch's
+    receive buffer; mode "dispatch" must also give the plain layer's outputs bit for bit."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     cfg = CASES[name]
@@ -109,6 +109,15 @@ def test_layer_ep1_parity(name, dedup):
         pad = np.ones(n_rows, bool)
         pad[base["recv_row"][t, j]] = False
         assert (xr[:n_rows][torch.as_tensor(pad)] == 0).all()
+    if dedup == "dispatch":
+        plain = build_layer(cfg)
+        yp = plain.forward(x).clone()
+        dxp = plain.backward(dy).clone()
+        torch.cuda.synchronize()
+        assert torch.equal(yp, y) and torch.equal(dxp, dx)
+        assert torch.equal(plain.dgates, layer.dgates) and torch.equal(plain.dw_gu, layer.dw_gu)
+        assert torch.equal(plain.dw_down, layer.dw_down) and torch.equal(plain.dw_r, layer.dw_r)
+        plain.close()
     # floating parts within tolerance
     errs = {}
     errs["gates"] = rel_err(f64(layer.gates), fw["gates"])

@@ -127,15 +127,17 @@ def test_all_to_all_origin_encoded(nproc):
 @pytest.mark.parametrize("config,extra", [("dsmoe_small", ()), ("v3_small_zipf", ()),
                                           ("drops", ()), ("v3_small_zipf", ("--rebalance",)),
                                           ("dsmoe_small", ("--graph",))])
-def test_layer_ep_parity_dedup(nproc, config, extra):
+@pytest.mark.parametrize("mode", ["dispatch", "all"])
+def test_layer_ep_parity_dedup(nproc, config, extra, mode):
     """NEXT-4 deduplicated all-to-alls (reading R18): pair tables (pdest, the pair record)
     bit-exact against oracle/dedup.py, every owner's expanded xr bitwise at the plain receive
     layout, outputs and gradients within tolerance, repeated calls (and graph replays)
     bit-identical -- also under a migrated placement."""
     if n_gpus() < nproc:
         pytest.skip(f"needs {nproc} GPUs")
-    port = 30300 + nproc * 10 + CONFIGS.index(config) + 50 * len(extra) + (7 if "--graph" in extra else 0)
-    res = run_worker(nproc, config, port, ("--dedup",) + tuple(extra))
+    port = (30300 + nproc * 10 + CONFIGS.index(config) + 50 * len(extra) +
+            (7 if "--graph" in extra else 0) + (200 if mode == "all" else 0))
+    res = run_worker(nproc, config, port, ("--dedup", mode) + tuple(extra))
     print(res)
     assert res["ok"], res
     assert res["checks"]["dedup_pairs"] and res["checks"]["dedup_xr"], res
