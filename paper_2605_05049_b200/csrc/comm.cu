@@ -208,12 +208,31 @@ __device__ void build_fwd_tables(const CommArgs& a, const int32_t* cm, FwdTables
 // A row of nvec 16-byte vectors is copied in parts of kPartVec vectors (2 KB, 4 per lane).
 constexpr int kPartVec = 128;
 __device__ __forceinline__ int row_parts(int nvec) { return (nvec + kPartVec - 1) / kPartVec; }
+// One warp's share of a 2 KB row part: up to 4 x 16 B per lane.
+struct PartBuf {
+  uint4 v[kPartVec / 32];
+};
+__device__ __forceinline__ void load_part(PartBuf& b, const uint4* __restrict__ src, int nvec,
+                                          int part, int lane) {
+  const int v0 = part * kPartVec + lane;
+#pragma unroll
+  for (int i = 0; i < kPartVec / 32; ++i)
+    if (v0 + 32 * i < nvec && v0 + 32 * i < (part + 1) * kPartVec) b.v[i] = ld_nc_v4(src + v0 + 32 * i);
+}
+__device__ __forceinline__ void store_part(uint4* dst, const PartBuf& b, int nvec, int part,
+                                           int lane) {
+  const int v0 = part * kPartVec + lane;
+#pragma unroll
+  for (int i = 0; i < kPartVec / 32; ++i)
+    if (v0 + 32 * i < nvec && v0 + 32 * i < (part + 1) * kPartVec) st_v4(dst + v0 + 32 * i, b.v[i]);
+}
+
+// all four loads of a lane are issued before its stores
 __device__ __forceinline__ void copy_part(uint4* __restrict__ dst, const uint4* __restrict__ src,
                                           int nvec, int part, int lane) {
-  const int v0 = part * kPartVec;
-  const int v1 = min(nvec, v0 + kPartVec);
-#pragma unroll
-  for (int v = v0 + lane; v < v1; v += 32) st_v4(dst + v, ld_nc_v4(src + v));
+  PartBuf b;
+  load_part(b, src, nvec, part, lane);
+  store_part(dst, b, nvec, part, lane);
 }
 
 // Copy segments in transfer order.  Segment i moves `count` consecutive rows from
@@ -236,6 +255,44 @@ __device__ void scan_segments(SegTable& t, int n) {
     if (threadIdx.x == 0) t.prefix[n] = total;
   }
   __syncthreads();
+}
+
+// Row pass of combine_bwd for one slot: dot = <a, b> over the row (fp32, each lane adding its
+// vectors v = lane, lane+32, ... in increasing v: the accumulation order is fixed) and, with
+// dst, dst = bf16(g * a).  Four vectors of each row per lane are loaded before any is used,
+// so a warp keeps 8 x 512 B in flight instead of waiting on one load pair per iteration.
+__device__ __forceinline__ float dot_scale_row(const uint4* __restrict__ a,
+                                               const uint4* __restrict__ b, uint4* dst, float g,
+                                               int nvec, int lane) {
+  float dot = 0.f;
+  for (int v0 = lane; v0 < nvec; v0 += 128) {
+    uint4 av[4], bv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (v0 + 32 * u < nvec) {
+        av[u] = ld_nc_v4(a + v0 + 32 * u);
+        if (b) bv[u] = ld_nc_v4(b + v0 + 32 * u);
+      }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (v0 + 32 * u >= nvec) break;
+      const uint32_t aw[4] = {av[u].x, av[u].y, av[u].z, av[u].w};
+      uint32_t ow[4];
+#pragma unroll
+      for (int q2 = 0; q2 < 4; ++q2) {
+        const float y0 = bf16_lo(aw[q2]), y1 = bf16_hi(aw[q2]);
+        if (b) {
+          const uint32_t bw = q2 == 0 ? bv[u].x : q2 == 1 ? bv[u].y : q2 == 2 ? bv[u].z : bv[u].w;
+          dot += y0 * bf16_lo(bw) + y1 * bf16_hi(bw);
+        }
+        ow[q2] = pack_bf16(g * y0, g * y1);
+      }
+      if (dst) st_v4(dst + v0 + 32 * u, make_uint4(ow[0], ow[1], ow[2], ow[3]));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+  return dot;
 }
 
 // Forward pattern.  mode 0: payload = src send row.  mode 1 (combine_bwd): payload of
@@ -341,23 +398,9 @@ __global__ void forward_transfer_kernel(CommArgs a, int32_t* __restrict__ layout
         const int q = a.place[e] / E_l;
         const int64_t drow = tb.dst[e] + (row - tb.off[e]);
         uint4* dst = reinterpret_cast<uint4*>(a.peers.base[q] + dst_off + drow * row_bytes);
-        const uint4* pdy = reinterpret_cast<const uint4*>(dy + t * d);
-        const uint4* pys = reinterpret_cast<const uint4*>(ys + static_cast<int64_t>(row) * d);
-        float dot = 0.f;
-        for (int v = lane; v < nvec; v += 32) {
-          const uint4 a4 = ld_nc_v4(pdy + v), b4 = ld_nc_v4(pys + v);
-          const uint32_t aw[4] = {a4.x, a4.y, a4.z, a4.w}, bw[4] = {b4.x, b4.y, b4.z, b4.w};
-          uint32_t ow[4];
-#pragma unroll
-          for (int q2 = 0; q2 < 4; ++q2) {
-            const float y0 = bf16_lo(aw[q2]), y1 = bf16_hi(aw[q2]);
-            dot += y0 * bf16_lo(bw[q2]) + y1 * bf16_hi(bw[q2]);
-            ow[q2] = pack_bf16(g * y0, g * y1);
-          }
-          st_v4(dst + v, make_uint4(ow[0], ow[1], ow[2], ow[3]));
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+        const float dot = dot_scale_row(reinterpret_cast<const uint4*>(dy + t * d),
+                                        reinterpret_cast<const uint4*>(ys + static_cast<int64_t>(row) * d),
+                                        dst, g, nvec, lane);
         if (lane == 0) dgates[t * a.k + j] = dot;
       }
     }
@@ -453,25 +496,6 @@ __device__ __forceinline__ void pair_bases(const CommArgs& a, const int32_t* nm,
   __syncthreads();
 }
 
-// One warp's share of a 2 KB row part: up to 4 x 16 B per lane.
-struct PartBuf {
-  uint4 v[kPartVec / 32];
-};
-__device__ __forceinline__ void load_part(PartBuf& b, const uint4* __restrict__ src, int nvec,
-                                          int part, int lane) {
-  const int v0 = part * kPartVec + lane;
-#pragma unroll
-  for (int i = 0; i < kPartVec / 32; ++i)
-    if (v0 + 32 * i < nvec && v0 + 32 * i < (part + 1) * kPartVec) b.v[i] = ld_nc_v4(src + v0 + 32 * i);
-}
-__device__ __forceinline__ void store_part(uint4* dst, const PartBuf& b, int nvec, int part,
-                                           int lane) {
-  const int v0 = part * kPartVec + lane;
-#pragma unroll
-  for (int i = 0; i < kPartVec / 32; ++i)
-    if (v0 + 32 * i < nvec && v0 + 32 * i < (part + 1) * kPartVec) st_v4(dst + v0 + 32 * i, b.v[i]);
-}
-
 // Forward pattern, deduplicated.  Work item = (token t, 2 KB part): the part is read ONCE and
 // stored to every owner t has a pair with, in rotated owner order.  MODE 0 (dispatch) also
 // exchanges counts and pair counts, writes the layout and pair records, and stores each
@@ -528,19 +552,9 @@ __global__ void dedup_forward_kernel(CommArgs a, int32_t* __restrict__ layout,
       const uint4* pdy = reinterpret_cast<const uint4*>(src + t * d);
       for (int j = 0; j < k; ++j) {
         const int32_t row = dest_row[t * k + j];
-        float dot = 0.f;
-        if (row >= 0) {
-          const uint4* pys = reinterpret_cast<const uint4*>(ys + static_cast<int64_t>(row) * d);
-          for (int v = lane; v < nvec; v += 32) {
-            const uint4 a4 = ld_nc_v4(pdy + v), b4 = ld_nc_v4(pys + v);
-            const uint32_t aw[4] = {a4.x, a4.y, a4.z, a4.w}, bw[4] = {b4.x, b4.y, b4.z, b4.w};
-#pragma unroll
-            for (int q2 = 0; q2 < 4; ++q2)
-              dot += bf16_lo(aw[q2]) * bf16_lo(bw[q2]) + bf16_hi(aw[q2]) * bf16_hi(bw[q2]);
-          }
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-        }
+        const float dot = row < 0 ? 0.f
+            : dot_scale_row(pdy, reinterpret_cast<const uint4*>(ys + static_cast<int64_t>(row) * d),
+                            nullptr, 0.f, nvec, lane);
         if (lane == 0) dgates[t * k + j] = dot;
       }
       continue;
@@ -638,34 +652,11 @@ __global__ void dedup_expand_kernel(CommArgs a, const int32_t* __restrict__ layo
           continue;
         }
         uint4* pdst = reinterpret_cast<uint4*>(dst + static_cast<int64_t>(rl) * d);
-        if (!O) {   // dO rows only (dgates formed at the source)
-          for (int v = lane; v < nvec; v += 32) {
-            const uint4 a4 = ld_nc_v4(ptok + v);
-            const uint32_t aw[4] = {a4.x, a4.y, a4.z, a4.w};
-            uint32_t ow[4];
-#pragma unroll
-            for (int q2 = 0; q2 < 4; ++q2) ow[q2] = pack_bf16(g * bf16_lo(aw[q2]), g * bf16_hi(aw[q2]));
-            st_v4(pdst + v, make_uint4(ow[0], ow[1], ow[2], ow[3]));
-          }
-          continue;
-        }
-        const uint4* po = reinterpret_cast<const uint4*>(O + static_cast<int64_t>(rl) * d);
-        float dot = 0.f;
-        for (int v = lane; v < nvec; v += 32) {
-          const uint4 a4 = ld_nc_v4(ptok + v), b4 = ld_nc_v4(po + v);
-          const uint32_t aw[4] = {a4.x, a4.y, a4.z, a4.w}, bw[4] = {b4.x, b4.y, b4.z, b4.w};
-          uint32_t ow[4];
-#pragma unroll
-          for (int q2 = 0; q2 < 4; ++q2) {
-            const float y0 = bf16_lo(aw[q2]), y1 = bf16_hi(aw[q2]);
-            dot += y0 * bf16_lo(bw[q2]) + y1 * bf16_hi(bw[q2]);
-            ow[q2] = pack_bf16(g * y0, g * y1);
-          }
-          st_v4(pdst + v, make_uint4(ow[0], ow[1], ow[2], ow[3]));
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-        if (lane == 0) dg_own[u * k + j] = dot;
+        // dO rows (and, with O, dg = <dy, O>; without O dgates were formed at the source)
+        const float dot = dot_scale_row(
+            ptok, O ? reinterpret_cast<const uint4*>(O + static_cast<int64_t>(rl) * d) : nullptr,
+            pdst, g, nvec, lane);
+        if (lane == 0 && O) dg_own[u * k + j] = dot;
       }
     }
   }

@@ -3,6 +3,9 @@
 # kernels (permute, unpermute, gathers, EP=1 transfers, route), --set full of the six expert
 # GEMMs on the V3-like rank slice.  Every command first exits 0 without ncu.
 O=gpurun_out
+timeout 900 python -m pytest tests -m gpu -x -q > $O/pytest_gpu1.log 2>&1; echo "pytest=$?" >> $O/pytest_gpu1.log
+timeout 300 python bench.py --breakdown --steps 5 > $O/breakdown1.log 2>&1
+timeout 300 python bench.py > $O/bench1.log 2>&1
 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke=$?" >> $O/smoke.log
 B="python bench.py --profile-steps 2 --no-cpu-baseline"
 $B > $O/plain_mixtral.log 2>&1 && \
