@@ -148,7 +148,9 @@ __global__ void scatter_kernel(const uint16_t* __restrict__ x, const int32_t* __
 
 
 // y[t] = bf16( sum_{j kept} g_{t,j} rows[dest_row[t,j]] (j order) + extra_f32[t] + extra_bf16[t] )
-template <bool GATED>
+// One warp per token.  KMAX >= k is a compile-time bound so the row list stays in registers
+// (static indices, dropped slots skipped in place: the same j-order sum as a compacted list).
+template <bool GATED, int KMAX>
 __global__ void gather_sum_kernel(const uint16_t* __restrict__ rows, const float* __restrict__ gates,
                                   const int32_t* __restrict__ dest_row, const float* __restrict__ extra_f32,
                                   const uint16_t* __restrict__ extra_bf16, int64_t T, int d, int k,
@@ -158,24 +160,25 @@ __global__ void gather_sum_kernel(const uint16_t* __restrict__ rows, const float
   const int lane = threadIdx.x & 31;
   const int64_t t = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   if (t >= T) return;
-  int32_t rws[32];
-  float gs[32];
-  int nk = 0;
-  for (int j = 0; j < k; ++j) {
-    const int32_t r = dest_row[t * k + j];
-    if (r >= 0) {
-      rws[nk] = r;
-      gs[nk] = GATED ? gates[t * k + j] : 1.f;
-      ++nk;
-    }
+  int32_t rws[KMAX];
+  float gs[KMAX];
+#pragma unroll
+  for (int j = 0; j < KMAX; ++j) {
+    rws[j] = j < k ? dest_row[t * k + j] : -1;
+    gs[j] = (GATED && rws[j] >= 0) ? gates[t * k + j] : 1.f;
   }
   const int nvec = d / 8;
-#pragma unroll 2
+  constexpr int kUnroll = KMAX <= 4 ? 2 : 1;   // keep the live row vectors near 8 per lane
+#pragma unroll kUnroll
   for (int v = lane; v < nvec; v += 32) {
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    for (int j = 0; j < nk; ++j)
-      acc_bf16x8(acc, ld_nc_v4(reinterpret_cast<const uint4*>(rows + static_cast<int64_t>(rws[j]) * d) + v),
-                 gs[j]);
+    uint4 val[KMAX];
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j)
+      if (rws[j] >= 0) val[j] = ld_nc_v4(reinterpret_cast<const uint4*>(rows + static_cast<int64_t>(rws[j]) * d) + v);
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j)
+      if (rws[j] >= 0) acc_bf16x8(acc, val[j], gs[j]);
     if (extra_f32) {
       const float4* pe = reinterpret_cast<const float4*>(extra_f32 + t * d) + 2 * v;
       const float4 a = pe[0], b = pe[1];
@@ -194,6 +197,7 @@ __global__ void gather_sum_kernel(const uint16_t* __restrict__ rows, const float
 // selected experts (softmax over the selected logits, reading R1), so
 //   dx[t] = bf16( sum_{j kept} dxs[dest_row[t,j]] + sum_j dl[t,e_j] w_r[e_j,:] + extra[t] )
 // in fp32 with a fixed order -- the dense [T,d] fp32 dx_router never touches HBM.
+template <int KMAX, int KRMAX>
 __global__ void gather_sum_router_kernel(const uint16_t* __restrict__ dxs,
                                          const int32_t* __restrict__ dest_row,
                                          const int32_t* __restrict__ topk_idx,
@@ -206,28 +210,33 @@ __global__ void gather_sum_router_kernel(const uint16_t* __restrict__ dxs,
   const int lane = threadIdx.x & 31;
   const int64_t t = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   if (t >= T) return;
-  int32_t rws[32], es[32];
-  float dl[32];
-  int nk = 0;
-  for (int j = 0; j < k; ++j) {
-    const int32_t e = topk_idx[t * k + j];
-    es[j] = e;
-    dl[j] = dlogits[t * E + e];
+  int32_t rws[KRMAX], es[KMAX];
+  float dl[KMAX];
+#pragma unroll
+  for (int j = 0; j < KMAX; ++j) {
+    es[j] = j < k ? topk_idx[t * k + j] : -1;
+    dl[j] = es[j] >= 0 ? dlogits[t * E + es[j]] : 0.f;
   }
-  for (int j = 0; j < kr; ++j) {   // row list: dest_row [T,k] (kr = k) or dedup pdest [T,EP]
-    const int32_t r = dest_row[t * kr + j];
-    if (r >= 0) rws[nk++] = r;
-  }
+#pragma unroll
+  for (int j = 0; j < KRMAX; ++j)   // row list: dest_row [T,k] (kr = k) or dedup pdest [T,EP]
+    rws[j] = j < kr ? dest_row[t * kr + j] : -1;
   const int nvec = d / 8;
-#pragma unroll 2
+  constexpr int kUnroll = KRMAX <= 4 ? 2 : 1;
+#pragma unroll kUnroll
   for (int v = lane; v < nvec; v += 32) {
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    for (int j = 0; j < nk; ++j)
-      acc_bf16x8(acc, ld_nc_v4(reinterpret_cast<const uint4*>(dxs + static_cast<int64_t>(rws[j]) * d) + v),
-                 1.f);
-    for (int j = 0; j < k; ++j)
-      acc_bf16x8(acc, ld_nc_v4(reinterpret_cast<const uint4*>(w_r + static_cast<int64_t>(es[j]) * d) + v),
-                 dl[j]);
+    uint4 val[KRMAX];
+#pragma unroll
+    for (int j = 0; j < KRMAX; ++j)
+      if (rws[j] >= 0) val[j] = ld_nc_v4(reinterpret_cast<const uint4*>(dxs + static_cast<int64_t>(rws[j]) * d) + v);
+#pragma unroll
+    for (int j = 0; j < KRMAX; ++j)
+      if (rws[j] >= 0) acc_bf16x8(acc, val[j], 1.f);
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j)
+      if (es[j] >= 0)
+        acc_bf16x8(acc, ld_nc_v4(reinterpret_cast<const uint4*>(w_r + static_cast<int64_t>(es[j]) * d) + v),
+                   dl[j]);
     if (extra_bf16)
       acc_bf16x8(acc, ld_nc_v4(reinterpret_cast<const uint4*>(extra_bf16 + t * d) + v), 1.f);
     reinterpret_cast<uint4*>(out + t * d)[v] =
@@ -377,8 +386,14 @@ cudaError_t launch_permute_bwd_router(const uint16_t* dxs, const int32_t* dest_r
                                       int d, int E, int k, uint16_t* dx, cudaStream_t s) {
   if (T == 0) return cudaSuccess;
   const int threads = 256;
-  launch_k(gather_sum_router_kernel, dim3(static_cast<unsigned>((T * 32 + threads - 1) / threads)),
-      dim3(threads), 0, s, dxs, dest_row, topk_idx, dlogits, w_r, dx_extra, T, d, E, k, k, dx);
+  const dim3 grid(static_cast<unsigned>((T * 32 + threads - 1) / threads));
+#define MOE_GSR(K_, KR_) launch_k(gather_sum_router_kernel<K_, KR_>, grid, dim3(threads), 0, s, dxs, \
+                                  dest_row, topk_idx, dlogits, w_r, dx_extra, T, d, E, k, k, dx)
+  if (k <= 2) MOE_GSR(2, 2);
+  else if (k <= 4) MOE_GSR(4, 4);
+  else if (k <= 8) MOE_GSR(8, 8);
+  else MOE_GSR(32, 32);
+#undef MOE_GSR
   return cudaGetLastError();
 }
 
@@ -389,8 +404,14 @@ cudaError_t launch_permute_bwd_router_rows(const uint16_t* dxs, const int32_t* r
                                            cudaStream_t s) {
   if (T == 0) return cudaSuccess;
   const int threads = 256;
-  launch_k(gather_sum_router_kernel, dim3(static_cast<unsigned>((T * 32 + threads - 1) / threads)),
-      dim3(threads), 0, s, dxs, rows, topk_idx, dlogits, w_r, dx_extra, T, d, E, k, kr, dx);
+  const dim3 grid(static_cast<unsigned>((T * 32 + threads - 1) / threads));
+#define MOE_GSR(K_, KR_) launch_k(gather_sum_router_kernel<K_, KR_>, grid, dim3(threads), 0, s, dxs, \
+                                  rows, topk_idx, dlogits, w_r, dx_extra, T, d, E, k, kr, dx)
+  if (kr <= 2 && k <= 2) MOE_GSR(2, 2);
+  else if (kr <= 4 && k <= 4) MOE_GSR(4, 4);
+  else if (kr <= 8 && k <= 8) MOE_GSR(8, 8);
+  else MOE_GSR(32, 32);
+#undef MOE_GSR
   return cudaGetLastError();
 }
 
@@ -472,8 +493,14 @@ cudaError_t launch_permute_bwd(const uint16_t* dxs, const int32_t* dest_row, con
                                cudaStream_t s) {
   if (T == 0) return cudaSuccess;
   const int threads = 256;
-  launch_k(gather_sum_kernel<false>, dim3(static_cast<unsigned>((T * 32 + threads - 1) / threads)),
-      dim3(threads), 0, s, dxs, nullptr, dest_row, dx_acc, dx_extra, T, d, k, dx);
+  const dim3 grid(static_cast<unsigned>((T * 32 + threads - 1) / threads));
+#define MOE_GS(K_) launch_k(gather_sum_kernel<false, K_>, grid, dim3(threads), 0, s, dxs, nullptr, \
+                            dest_row, dx_acc, dx_extra, T, d, k, dx)
+  if (k <= 2) MOE_GS(2);
+  else if (k <= 4) MOE_GS(4);
+  else if (k <= 8) MOE_GS(8);
+  else MOE_GS(32);
+#undef MOE_GS
   return cudaGetLastError();
 }
 
@@ -482,8 +509,14 @@ cudaError_t launch_unpermute(const uint16_t* ys, const float* gates, const int32
                              cudaStream_t s) {
   if (T == 0) return cudaSuccess;
   const int threads = 256;
-  launch_k(gather_sum_kernel<true>, dim3(static_cast<unsigned>((T * 32 + threads - 1) / threads)),
-      dim3(threads), 0, s, ys, gates, dest_row, nullptr, y_extra, T, d, k, y);
+  const dim3 grid(static_cast<unsigned>((T * 32 + threads - 1) / threads));
+#define MOE_GS(K_) launch_k(gather_sum_kernel<true, K_>, grid, dim3(threads), 0, s, ys, gates, \
+                            dest_row, nullptr, y_extra, T, d, k, y)
+  if (k <= 2) MOE_GS(2);
+  else if (k <= 4) MOE_GS(4);
+  else if (k <= 8) MOE_GS(8);
+  else MOE_GS(32);
+#undef MOE_GS
   return cudaGetLastError();
 }
 
