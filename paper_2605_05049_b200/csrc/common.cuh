@@ -157,6 +157,10 @@ MOE_DEVINL void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "
 MOE_DEVINL void bulk_wait_read0() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
+// at most one committed bulk group may still be reading its shared-memory source
+MOE_DEVINL void bulk_wait_read1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
 MOE_DEVINL void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 // Generic-proxy shared-memory writes -> visible to the async (TMA) proxy.
 MOE_DEVINL void fence_async_smem() {

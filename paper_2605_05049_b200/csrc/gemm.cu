@@ -148,12 +148,15 @@ __device__ __forceinline__ Work get_work(const Sched& s, int w) {
   return wk;
 }
 
-template <int BN, int PAIR>
+// STG = staging boxes per epilogue warp: 2 double-buffers the fp32 wgrad epilogue (its K is
+// one expert's rows, so the MMAs of a tile are short and the 256 KB fp32 tile store must
+// overlap the next chunk's staging); the ring gives up one stage for it.
+template <int BN, int PAIR, int STG = 1>
 struct Cfg {
   static constexpr int A_BYTES = kBM * kBK * 2;
   static constexpr int B_BYTES = (BN / PAIR) * kBK * 2;  // a CTA pair splits B along N
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES_RAW = (196 * 1024) / STAGE_BYTES;
+  static constexpr int STAGES_RAW = (196 * 1024 - (STG - 1) * 4 * kStageBox) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int RING = STAGES * STAGE_BYTES;
   static constexpr int ACC_STRIDE = BN < 32 ? 32 : BN;
@@ -163,8 +166,10 @@ struct Cfg {
                                    : (2 * ACC_STRIDE <= 256) ? 256
                                                              : 512;
   // ring + epilogue staging + barriers/tables (incl. scatter tables) + alignment slack
-  static constexpr int SMEM = RING + 4 * kStageBox + 6144 + 1024;
+  static constexpr int SMEM = RING + 4 * STG * kStageBox + 6144 + 1024;
 };
+template <int EPI>
+__host__ __device__ constexpr int staging_boxes() { return EPI == kEpiF32Group ? 2 : 1; }
 
 __device__ __forceinline__ int ceil_div(int a, int b) { return (a + b - 1) / b; }
 
@@ -240,7 +245,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const __grid_constant__ CUtensorMap tmC, const KParams p) {
   pdl_wait();
   pdl_trigger();
-  using C = Cfg<BN, PAIR>;
+  constexpr int STG = staging_boxes<EPI>();
+  using C = Cfg<BN, PAIR, STG>;
   constexpr bool KGROUPED = (EPI == kEpiF32Group);
   constexpr int TILE_M = kBM * PAIR;
   constexpr uint32_t IDESC = idesc_bf16(TILE_M, BN, A_MN, B_MN);
@@ -252,8 +258,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::STAGES * C::A_BYTES;
-  uint8_t* sStage = smem + C::RING;  // 4 x 4 KB, 1024-aligned
-  uint64_t* full = reinterpret_cast<uint64_t*>(sStage + 4 * kStageBox);
+  uint8_t* sStage = smem + C::RING;  // 4 x STG x 4 KB, 1024-aligned
+  uint64_t* full = reinterpret_cast<uint64_t*>(sStage + 4 * STG * kStageBox);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
@@ -459,8 +465,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp >= 4) {
     // ===================== epilogue =====================
     const int ew = warp - 4;  // TMEM lane quadrant ew*32 .. ew*32+31
-    const uint32_t row_addr = smem_u32(sStage + ew * kStageBox) + lane * 128;
-    const void* box = sStage + ew * kStageBox;
+    const uint32_t row_addr = smem_u32(sStage + ew * STG * kStageBox) + lane * 128;
+    const void* box = sStage + ew * STG * kStageBox;
+    int sbuf = 0;   // STG = 2: the staging box the next chunk uses
     int acc = 0;
     uint32_t acc_phase = 0;
     constexpr int kArrive = 4 * PAIR;  // epilogue warps of a cluster
@@ -702,14 +709,19 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
               for (int q = 0; q < 32; ++q) a[q] = 0u;
             }
-            staging_acquire(lane);
-            stage_row(row_addr, lane, a);
+            // double-buffered: only the store that used THIS box must have read it
+            if (lane == 0) bulk_wait_read1();
+            __syncwarp();
+            const uint32_t off = static_cast<uint32_t>(sbuf * kStageBox);
+            stage_row(row_addr + off, lane, a);
             staging_release();
             if (lane == 0) {
-              if (p.accumulate) tma_reduce_add_3d(&tmC, box, tl.n * BN + c0, row0, tl.g);
-              else tma_store_3d(&tmC, box, tl.n * BN + c0, row0, tl.g);
+              const void* b = static_cast<const uint8_t*>(box) + off;
+              if (p.accumulate) tma_reduce_add_3d(&tmC, b, tl.n * BN + c0, row0, tl.g);
+              else tma_store_3d(&tmC, b, tl.n * BN + c0, row0, tl.g);
               bulk_commit();
             }
+            sbuf ^= (STG - 1);
           }
         }
       } else {  // kEpiF32Rows: router logits / router dgrad, fp32 [rows, N] (+ bias) (+= old)
@@ -847,7 +859,7 @@ bool make_tmap_bf16(CUtensorMap* tm, const void* ptr, int64_t rows, int64_t cols
 
 template <int BN, bool A_MN, bool B_MN, int EPI, int PAIR>
 cudaError_t launch_impl(const GemmProblem& g, cudaStream_t stream) {
-  using C = Cfg<BN, PAIR>;
+  using C = Cfg<BN, PAIR, staging_boxes<EPI>()>;
   CUtensorMap ta, tb, tc;
   // A box: K-major {64 k, 128 rows}; MN-major {64 m, 64 k}
   if (!make_tmap_bf16(&ta, g.a_ptr, g.a_rows, g.a_cols, g.a_ld, 64, A_MN ? 64 : kBM))
