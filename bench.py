@@ -119,6 +119,17 @@ class ClockSampler:
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except FileNotFoundError:
             self.proc = None
+            return
+        # nvidia-smi needs ~0.1-0.3 s to print its first line: wait for it, so that a short
+        # timed region (a few ms per step) still has samples taken under its load
+        t0 = time.time()
+        while time.time() - t0 < 3.0:
+            try:
+                if os.path.getsize(self.path) > 0:
+                    break
+            except OSError:
+                pass
+            time.sleep(0.01)
 
     def stop(self):
         if self.proc is None:

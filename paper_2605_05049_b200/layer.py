@@ -157,8 +157,10 @@ class MoELayer:
     # ------------------------------------------------------------------ forward
     # per-phase CUDA-event markers (bench.py --breakdown); off by default
     marks = None
-    # SMs given to an all-to-all that runs beside a GEMM (the GEMM gets the rest)
-    comm_sms = 20
+    # SMs given to an all-to-all that runs beside a GEMM (the GEMM gets the rest).  Measured on
+    # DS-MoE N=4 (profiles/r01/sms_*.json): 20 -> 1.97 ms, 48 -> 1.92 ms (dedup 2.01 -> 1.89),
+    # 74 -> 2.00 ms (dedup)
+    comm_sms = 48
 
     def _concurrent(self, comm_fn, gemm_fn):
         """comm_fn(stream) on a side stream with `comm_sms` SMs, gemm_fn(stream) on the current
