@@ -148,9 +148,11 @@ __device__ __forceinline__ Work get_work(const Sched& s, int w) {
   return wk;
 }
 
-// STG = staging boxes per epilogue warp: 2 double-buffers the fp32 wgrad epilogue (its K is
-// one expert's rows, so the MMAs of a tile are short and the 256 KB fp32 tile store must
-// overlap the next chunk's staging); the ring gives up one stage for it.
+// STG = staging boxes per epilogue warp.  2 double-buffers the fp32 wgrad epilogue (its K is
+// one expert's rows, so a tile's MMAs are short), at the price of one ring stage.  Measured
+// on the V3-like rank slice (ncu, profiles/r01/README.md): wgrad 1.63 -> 1.70 ms and
+// 3.29 -> 3.41 ms, i.e. slower -- the ring stage is worth more; kept at 1.
+constexpr int kWgradStaging = 1;
 template <int BN, int PAIR, int STG = 1>
 struct Cfg {
   static constexpr int A_BYTES = kBM * kBK * 2;
@@ -169,7 +171,7 @@ struct Cfg {
   static constexpr int SMEM = RING + 4 * STG * kStageBox + 6144 + 1024;
 };
 template <int EPI>
-__host__ __device__ constexpr int staging_boxes() { return EPI == kEpiF32Group ? 2 : 1; }
+__host__ __device__ constexpr int staging_boxes() { return EPI == kEpiF32Group ? kWgradStaging : 1; }
 
 __device__ __forceinline__ int ceil_div(int a, int b) { return (a + b - 1) / b; }
 
