@@ -12,8 +12,9 @@ Modules
   counters  FLOP / byte counters evaluated from the realised routing
   migration Alg. 2 expert migration (NEXT-2)
   dedup     per-destination-rank deduplicated all-to-all (NEXT-4, reading R18)
+  pipeline  1F1B schedule of the PP x EP executor and Eq. 4's activation term (NEXT-3, R19)
 
 Parity pins: see tests/test_oracle_*.py; "parity unpinned" items are listed in
 DESIGN.md §Oracle and in the docstrings below.
 """
-from . import moe_ref, counters, dedup  # noqa: F401
+from . import moe_ref, counters, dedup, pipeline  # noqa: F401
