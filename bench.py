@@ -67,6 +67,10 @@ def parse():
                     help="--gemm-compare: experts on the GPU (default: the config's E)")
     ap.add_argument("--gemm-rows", type=int, default=0,
                     help="--gemm-compare: rows per expert (default: T*k/E)")
+    ap.add_argument("--pp", type=int, default=1,
+                    help="NEXT-3: PP x EP pipelined stack (world = PP x EP), 1F1B over --micro")
+    ap.add_argument("--layers", type=int, default=4, help="--pp: MoE layers in the stack")
+    ap.add_argument("--micro", type=int, default=8, help="--pp: micro-batches per step")
     ap.add_argument("--profile-steps", type=int, default=0,
                     help="run only this many steps without timing (for ncu)")
     return ap.parse_args()
@@ -675,6 +679,80 @@ def run_reference(args):
     print(json.dumps(out))
 
 
+# ---------------------------------------------------------------------------- NEXT-3 pipeline
+def run_pipeline(args):
+    """PP x EP executor (paper_2605_05049_b200.pipeline): a stack of --layers MoE layers of the
+    config's shape, --micro micro-batches of T/--micro tokens each per step, 1F1B.  value =
+    tokens of the step / (max-over-ranks device time of one step); not the headline metric."""
+    world, rank, local = dist_env()
+    dist = init_dist(world, local)
+    torch.cuda.set_device(local)
+    from paper_2605_05049_b200 import LayerDims
+    from paper_2605_05049_b200.pipeline import PipelineStack
+    cfg = synth.CONFIGS[args.config]
+    pp, M, Lyr = args.pp, args.micro, args.layers
+    ep = world // pp
+    stage, e = divmod(rank, ep)
+    T_mb = cfg.T // M
+    T_r = T_mb // ep
+    dims = LayerDims(T_r, cfg.d, cfg.E, cfg.k, cfg.f, cfg.E_s, cfg.cf, ep, e)
+    stack = PipelineStack(dims, Lyr, pp, M, device=local, dedup=args.dedup)
+    E_l = cfg.E // ep
+    dev = torch.device(f"cuda:{local}")
+    w_gu, w_down = synth.expert_weights(cfg, range(e * E_l, (e + 1) * E_l), device=dev)
+    w_gu_s, w_down_s = synth.shared_weights(cfg, device=dev)
+    for l in range(Lyr // pp):
+        stack.set_weights(l, synth.router_weight(cfg, device=dev), w_gu, w_down,
+                          synth.zipf_bias(cfg), w_gu_s, w_down_s)
+    x = synth.tokens(cfg, device=dev).view(M, T_mb, cfg.d)
+    dy = synth.grad_output(cfg, device=dev).view(M, T_mb, cfg.d)
+    xs = [x[m, e * T_r:(e + 1) * T_r].contiguous() for m in range(M)]
+    dys = [dy[m, e * T_r:(e + 1) * T_r].contiguous() for m in range(M)]
+    first, last = stage == 0, stage == pp - 1
+
+    def step():
+        stack.step(xs if first else None, dys if last else None)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(args.steps):
+        step()
+    t1.record()
+    torch.cuda.synchronize()
+    dist.barrier()
+    clk = clocks.stop()
+    ms = torch.tensor([t0.elapsed_time(t1) / args.steps], dtype=torch.float64, device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+    # serial per-stage GEMM bound of the step: every stage does M micro-batches of L/PP layers
+    rows = M * T_r * cfg.k
+    gemm_flops = (Lyr // pp) * 18 * rows * cfg.d * cfg.f
+    peaks = measured_peaks()
+    if rank == 0:
+        print(json.dumps({
+            "metric": "PP x EP MoE stack fwd+bwd tokens/s", "value": cfg.T / (ms * 1e-3),
+            "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic (seeded N(0,1) tokens, random-init weights)",
+            "config": {"workload": f"{cfg.name} {Lyr}-layer MoE stack, 1F1B",
+                       "parallelism": f"pp{pp}xep{ep}", "micro_batches": M,
+                       "tokens_per_micro_batch": T_mb, "layers": Lyr,
+                       "dedup_a2a": args.dedup},
+            "gpu_launches": None, "clocks": clk,
+            "stage_gemm_bound_ms": gemm_flops / (peaks["bf16_sustained"] * 1e12) * 1e3,
+            "pipeline_bubble_bound": (pp - 1) / (M + pp - 1),
+        }), flush=True)
+    stack.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 # ---------------------------------------------------------------------------- a2a sweep
 def run_a2a(args):
     """Config 5: equal-split all-to-all of a bf16 send buffer, 64 KB .. 1 GB per rank:
@@ -894,6 +972,8 @@ def main():
         run_reference(args)
     elif args.gemm_compare:
         run_gemm_compare(args)
+    elif args.pp > 1:
+        run_pipeline(args)
     elif args.a2a:
         run_a2a(args)
     else:

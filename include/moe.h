@@ -425,6 +425,19 @@ moe_status moe_dedup_permute_bwd_router(moe_ctx* ctx, const moe_bf16* dxpart,
                                         const moe_bf16* dx_extra_or_null, moe_bf16* dx,
                                         moe_stream stream);
 
+/* ---------------- NEXT-3 PP x EP pipelined executor ----------------
+ * P GPUs as a PP x EP mesh -- PP pipeline stages, each staffed by EP GPUs holding
+ * L/PP MoE layers with E/EP experts per GPU; the 1F1B schedule keeps at
+ * most PP - i micro-batches in flight on stage i.  The layer calls above are unchanged; the
+ * executor (paper_2605_05049_b200/pipeline.py) runs this op list per stage. */
+#define MOE_PIPE_FORWARD 0
+#define MOE_PIPE_BACKWARD 1
+/* Host function (no GPU).  The op list of `stage` (reading R19): ops[2i] = MOE_PIPE_FORWARD or
+ * MOE_PIPE_BACKWARD, ops[2i+1] = micro-batch; *n_ops = 2 * n_micro.  MOE_ERR_INVALID_ARG for
+ * pp < 1, stage outside [0, pp), n_micro < 1, max_ops < 2 * n_micro or NULL pointers. */
+moe_status moe_pipeline_1f1b(int32_t pp, int32_t stage, int32_t n_micro, int32_t* ops,
+                             int32_t max_ops, int32_t* n_ops);
+
 #ifdef __cplusplus
 }
 #endif

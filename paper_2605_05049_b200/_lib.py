@@ -96,6 +96,7 @@ _SIGS = {
     "moe_dedup_combine_bwd": [P] * 12,
     "moe_dedup_dispatch_bwd": [P] * 12,
     "moe_dedup_combine_bwd_ys": [P] * 14,
+    "moe_pipeline_1f1b": [I32, I32, I32, P, I32, P],
     "moe_dedup_permute_bwd_router": [P] * 9,
 }
 for _name, _args in _SIGS.items():
@@ -474,3 +475,17 @@ def moe_dedup_combine_bwd_ys(ctx, dy, gates, dest_row, ys, pdest, layout, dlayou
         _ptr(layout, I32T, "layout"), _ptr(dlayout, I32T, "dlayout"), _ptr(rlist, I32T, "rlist"),
         _ptr(glist, F32, "glist"), _ptr(dyt, BF16, "dyt"), _ptr(dgates, F32, "dgates"),
         _ptr(dout_r, BF16, "dout_r"), _stream(stream)))
+
+
+# ---- NEXT-3 PP x EP executor: the 1F1B op list of one stage (host code in libmoe)
+PIPE_FORWARD, PIPE_BACKWARD = 0, 1
+
+
+def moe_pipeline_1f1b(pp, stage, n_micro):
+    """[(PIPE_FORWARD | PIPE_BACKWARD, micro-batch), ...] of `stage` (reading R19)."""
+    cap = max(2 * int(n_micro), 1)
+    ops = (ctypes.c_int32 * (2 * cap))()
+    n = ctypes.c_int32(0)
+    _check("moe_pipeline_1f1b", _lib.moe_pipeline_1f1b(int(pp), int(stage), int(n_micro), ops,
+                                                       cap, ctypes.byref(n)))
+    return [(ops[2 * i], ops[2 * i + 1]) for i in range(n.value)]

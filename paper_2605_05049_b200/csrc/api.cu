@@ -981,3 +981,28 @@ moe_status moe_dedup_permute_bwd_router(moe_ctx* c, const moe_bf16* dxpart, cons
                                                          dlogits, w_r, dx_extra, c->s.T_local,
                                                          c->s.d, c->s.E, c->s.k, dx, st(s)));
 }
+
+// ---------------------------------------------------------------- NEXT-3 PP x EP executor
+// 1F1B op order of one pipeline stage (reading R19): w = min(PP-i-1, M)
+// warm-up forwards, then one forward + one backward while forwards remain, then the
+// remaining backwards; micro-batches ascending.  Host code: the executor asks for it once.
+moe_status moe_pipeline_1f1b(int32_t pp, int32_t stage, int32_t n_micro, int32_t* ops,
+                             int32_t max_ops, int32_t* n_ops) {
+  MOE_REQUIRE(pp >= 1 && stage >= 0 && stage < pp && n_micro >= 1 && ops && n_ops);
+  MOE_REQUIRE(max_ops >= 2 * n_micro);
+  const int32_t w = (pp - stage - 1) < n_micro ? (pp - stage - 1) : n_micro;
+  int32_t n = 0, nf = 0, nb = 0;
+  auto put = [&](int32_t kind, int32_t m) {
+    ops[2 * n] = kind;
+    ops[2 * n + 1] = m;
+    ++n;
+  };
+  for (; nf < w; ++nf) put(MOE_PIPE_FORWARD, nf);
+  while (nf < n_micro) {
+    put(MOE_PIPE_FORWARD, nf++);
+    put(MOE_PIPE_BACKWARD, nb++);
+  }
+  while (nb < n_micro) put(MOE_PIPE_BACKWARD, nb++);
+  *n_ops = n;
+  return MOE_OK;
+}

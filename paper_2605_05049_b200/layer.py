@@ -161,6 +161,14 @@ class MoELayer:
     # DS-MoE N=4 (profiles/r01/sms_*.json): 20 -> 1.97 ms, 48 -> 1.92 ms (dedup 2.01 -> 1.89),
     # 74 -> 2.00 ms (dedup)
     comm_sms = 48
+    # SM budget of every all-to-all outside the overlap (0 = all SMs); the PP x EP executor
+    # leaves a few SMs free so the NCCL stage-to-stage kernels can always be scheduled beside
+    # a spinning collective
+    base_comm_sms = 0
+
+    def set_base_comm_sms(self, n):
+        self.base_comm_sms = int(n)
+        self.ctx.set_sm_limits(0, self.base_comm_sms)
 
     def _concurrent(self, comm_fn, gemm_fn):
         """comm_fn(stream) on a side stream with `comm_sms` SMs, gemm_fn(stream) on the current
@@ -180,7 +188,7 @@ class MoELayer:
         gemm_fn(main)
         self.ctx.set_sm_limits(0, self.comm_sms)
         comm_fn(side)
-        self.ctx.set_sm_limits(0, 0)
+        self.ctx.set_sm_limits(0, self.base_comm_sms)
         done = torch.cuda.Event()
         done.record(side)
         main.wait_event(done)

@@ -1,0 +1,148 @@
+"""PP x EP pipelined executor of a stack of MoE layers.
+
+PAPER.md:149: the P GPUs form a PP x EP mesh -- PP pipeline stages, each staffed by EP GPUs
+that hold L/PP layers and E/EP experts per layer (expert-data parallelism inside the stage,
+PAPER.md:272); stage i's EP GPU e sends its activations to "its counterpart" (i+1, e)
+ and receives gradients back.  Micro-batches run in the 1F1B order of libmoe's
+moe_pipeline_1f1b (reading R19), so stage i holds at most PP - i
+micro-batches in flight: each layer keeps that many activation contexts (MoELayer instances
+sharing the layer's weights and accumulating into one set of weight gradients).
+
+Mesh: global rank = stage * EP + e (EP groups contiguous, "EP within the fast
+domain").  Stage-to-stage transfers use torch.distributed point-to-point (NCCL), the plumbing;
+every step of every layer runs through libmoe.  Activations leave through a per-micro-batch
+send buffer, so a layer's output buffer can be reused while the transfer is still queued.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import _lib as L
+from .layer import LayerDims, MoELayer
+
+
+class PipelineStack:
+    def __init__(self, dims: LayerDims, n_layers: int, pp: int, n_micro: int, device=0,
+                 fused: bool = True, dedup=False, free_sms: int = 8, layer_cls=MoELayer):
+        """dims: one layer's shape for ONE micro-batch on this EP rank (T_local = tokens of the
+        micro-batch / EP, ep_size = EP, ep_rank = this rank's index in its stage).  Collective
+        over the whole world (every rank builds its stage's EP group).  layer_cls / device=None
+        exist for the CPU (gloo) test of the schedule and the stage-to-stage routing."""
+        import torch.distributed as dist
+        self.dist = dist
+        world, rank = dist.get_world_size(), dist.get_rank()
+        ep = dims.ep_size
+        if world != pp * ep or n_layers % pp:
+            raise ValueError(f"need world == PP x EP and PP | L (world {world}, PP {pp}, EP {ep}, "
+                             f"L {n_layers})")
+        self.pp, self.ep, self.M = pp, ep, n_micro
+        self.stage, self.e = divmod(rank, ep)
+        if dims.ep_rank != self.e:
+            raise ValueError("dims.ep_rank must be this rank's index in its stage")
+        self.device = torch.device("cpu" if device is None else f"cuda:{device}")
+        groups = [dist.new_group(list(range(i * ep, (i + 1) * ep))) for i in range(pp)]
+        self.group = groups[self.stage]
+        self.prev = (self.stage - 1) * ep + self.e if self.stage > 0 else None
+        self.next = (self.stage + 1) * ep + self.e if self.stage < pp - 1 else None
+        self.ops = L.moe_pipeline_1f1b(pp, self.stage, n_micro)
+        self.n_slots = min(pp - self.stage, n_micro)       # PAPER.md:284 in-flight bound
+        self.n_local = n_layers // pp
+        n_sms = (torch.cuda.get_device_properties(self.device).multi_processor_count
+                 if device is not None else 0)
+        self.layers = []                                    # [local layer][slot]
+        for _ in range(self.n_local):
+            slots = [layer_cls(dims, device=device, group=self.group, fused=fused, dedup=dedup)
+                     for _ in range(self.n_slots)]
+            if n_sms:
+                for s in slots:
+                    s.set_base_comm_sms(n_sms - free_sms)
+            self.layers.append(slots)
+        T, d = dims.T_local, dims.d
+        bf = torch.bfloat16
+        buf = lambda: [torch.empty((T, d), dtype=bf, device=self.device) for _ in range(n_micro)]
+        # separate buffers per direction: a received activation stays the first layer's saved
+        # input until the micro-batch's backward, while its gradient arrives in another buffer
+        self.send_act, self.send_grad = buf(), buf()
+        self.recv_act, self.recv_grad = buf(), buf()
+        self.y_out, self.dx_out = buf(), buf()
+        self.record = None   # tests: {(local layer, m): {...}} clones of each layer's tensors
+
+    # ------------------------------------------------------------------ weights
+    def set_weights(self, l, w_r, w_gu, w_down, bias=None, w_gu_s=None, w_down_s=None):
+        """Local layer l (global layer stage * L/PP + l): every activation context shares the
+        weights and the weight-gradient buffers."""
+        slots = self.layers[l]
+        for s in slots:
+            s.set_weights(w_r, w_gu, w_down, bias, w_gu_s, w_down_s)
+        s0 = slots[0]
+        for s in slots[1:]:
+            s.w_r, s.w_gu, s.w_down, s.bias = s0.w_r, s0.w_gu, s0.w_down, s0.bias
+            s.w_gu_s, s.w_down_s = s0.w_gu_s, s0.w_down_s
+            s.dw_r, s.dw_gu, s.dw_down = s0.dw_r, s0.dw_gu, s0.dw_down
+            if s0.fs:
+                s.dw_gu_s, s.dw_down_s = s0.dw_gu_s, s0.dw_down_s
+
+    def grads(self, l):
+        s0 = self.layers[l][0]
+        return s0.dw_r, s0.dw_gu, s0.dw_down
+
+    # ------------------------------------------------------------------ one step
+    def step(self, xs=None, dys=None):
+        """One training step over the M micro-batches in 1F1B order.  Stage 0 passes xs (M
+        tensors [T_local, d] bf16), the last stage dys (the upstream gradients of its outputs).
+        Returns (ys, dxs): the last stage's outputs and stage 0's input gradients (lists of M
+        tensors, valid until the next step), None elsewhere.  Weight gradients of the step are
+        in grads(l) (the first backward overwrites, the others accumulate)."""
+        dist = self.dist
+        pending = []
+        last = self.next is None
+        for kind, m in self.ops:
+            slot = m % self.n_slots
+            if kind == L.PIPE_FORWARD:
+                if self.prev is None:
+                    h = xs[m]
+                else:
+                    dist.irecv(self.recv_act[m], src=self.prev).wait()
+                    h = self.recv_act[m]
+                for l in range(self.n_local):
+                    lay = self.layers[l][slot]
+                    x_in = h
+                    h = lay.forward(h)
+                    if self.record is not None:
+                        self._rec(l, m, x=x_in, y=h, logits=lay.logits, topk=lay.topk_idx,
+                                  dest=lay.dest_row)
+                if last:
+                    self.y_out[m].copy_(h)
+                else:
+                    self.send_act[m].copy_(h)
+                    pending.append(dist.isend(self.send_act[m], dst=self.next))
+            else:
+                if last:
+                    g = dys[m]
+                else:
+                    dist.irecv(self.recv_grad[m], src=self.next).wait()
+                    g = self.recv_grad[m]
+                for l in reversed(range(self.n_local)):
+                    lay = self.layers[l][slot]
+                    dy_in = g
+                    g = lay.backward(g, accumulate=m > 0)
+                    if self.record is not None:
+                        self._rec(l, m, dy=dy_in, dx=g)
+                if self.prev is None:
+                    self.dx_out[m].copy_(g)
+                else:
+                    self.send_grad[m].copy_(g)
+                    pending.append(dist.isend(self.send_grad[m], dst=self.prev))
+        for p in pending:
+            p.wait()
+        return (self.y_out if last else None), (self.dx_out if self.prev is None else None)
+
+    def _rec(self, l, m, **tensors):
+        r = self.record.setdefault((l, m), {})
+        for k, t in tensors.items():
+            r[k] = t.detach().clone()
+
+    def close(self):
+        for slots in self.layers:
+            for s in slots:
+                s.close()

@@ -1,0 +1,141 @@
+"""torchrun worker of the PP x EP pipelined executor (NEXT-3): every rank runs its stage's
+layers in 1F1B order; rank 0 gathers every layer's inputs, outputs, logits and gradients and
+checks each (layer, micro-batch) against the fp64 oracle teacher-forced with the GPU's own
+inputs and logits, the stage-to-stage hand-offs bitwise, and the accumulated weight
+gradients against the oracle's sum over micro-batches (tests/test_gpu_multi.py launches it).
+
+    python -m torch.distributed.run --nproc-per-node 4 --master-addr 127.0.0.1 \\
+        tests/mp_pipe_worker.py --pp 2
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import synth  # noqa: E402
+
+CFG = synth.MoEConfig("pipe_small", T=512, d=256, E=8, k=2, f=256, cf=1.25)
+
+
+def gather(t):
+    out = [torch.empty_like(t) for _ in range(dist.get_world_size())]
+    dist.all_gather(out, t.contiguous())
+    return out
+
+
+def layer_weights(g, experts, device):
+    """Layer g's weights: the synth draws scaled per layer (so the layers differ)."""
+    s = 1.0 + 0.125 * g
+    w_gu, w_down = synth.expert_weights(CFG, experts, device=device)
+    w_r = synth.router_weight(CFG, device=device)
+    return ((w_r.float() * s).bfloat16(), (w_gu.float() * s).bfloat16(),
+            (w_down.float() / s).bfloat16())
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--pp", type=int, default=2)
+    ap.add_argument("--layers", type=int, default=4)
+    ap.add_argument("--micro", type=int, default=4)
+    ap.add_argument("--dedup", default=None)
+    args = ap.parse_args()
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    world, rank = dist.get_world_size(), dist.get_rank()
+    pp, M, Lyr = args.pp, args.micro, args.layers
+    ep = world // pp
+    stage, e = divmod(rank, ep)
+    from paper_2605_05049_b200 import LayerDims
+    from paper_2605_05049_b200.pipeline import PipelineStack
+    from tests.helpers import TOL, f64, paper_weights, rel_err
+    cfg = CFG
+    T_r = cfg.T // ep
+    dims = LayerDims(T_r, cfg.d, cfg.E, cfg.k, cfg.f, 0, cfg.cf, ep, e)
+    stack = PipelineStack(dims, Lyr, pp, M, device=local, dedup=args.dedup)
+    E_l = cfg.E // ep
+    dev = torch.device(f"cuda:{local}")
+    per = Lyr // pp
+    for l in range(per):
+        w_r, w_gu, w_down = layer_weights(stage * per + l, range(e * E_l, (e + 1) * E_l), dev)
+        stack.set_weights(l, w_r, w_gu, w_down)
+    x_all = synth.tokens(cfg, T=M * cfg.T).cuda().view(M, cfg.T, cfg.d)
+    dy_all = synth.grad_output(cfg, T=M * cfg.T).cuda().view(M, cfg.T, cfg.d)
+    xs = [x_all[m, e * T_r:(e + 1) * T_r].contiguous() for m in range(M)]
+    dys = [dy_all[m, e * T_r:(e + 1) * T_r].contiguous() for m in range(M)]
+    stack.step(xs if stage == 0 else None, dys if stage == pp - 1 else None)   # warm-up step
+    stack.record = {}
+    ys, dxs = stack.step(xs if stage == 0 else None, dys if stage == pp - 1 else None)
+    torch.cuda.synchronize()
+    status = max(s.ctx.device_error() for slots in stack.layers for s in slots)
+    rec = stack.record
+    # gather: [rank][local layer][m] tensors
+    keys = ["x", "y", "logits", "topk", "dest", "dy", "dx"]
+    G = {k: [[gather(rec[(l, m)][k]) for m in range(M)] for l in range(per)] for k in keys}
+    dW = [[gather(t) for t in stack.grads(l)] for l in range(per)]   # dw_r, dw_gu, dw_down
+    st = gather(torch.tensor([status], device=dev))
+    if rank != 0:
+        dist.barrier()
+        dist.destroy_process_group()
+        return
+    from oracle import moe_ref as ref
+    errs, checks = {}, {"routing": True, "handoff": True}
+    ranks_of = lambda s_: list(range(s_ * ep, (s_ + 1) * ep))
+    for g in range(Lyr):
+        s_, l = divmod(g, per)
+        rs = ranks_of(s_)
+        W = layer_weights(g, range(cfg.E), "cuda")
+        w_r = f64(W[0]).T
+        Wg, Wu, Wd = zip(*[paper_weights(W[1][x], W[2][x], cfg.f) for x in range(cfg.E)])
+        dWg = dWu = dWd = dWr = None
+        for m in range(M):
+            cat = lambda k: torch.cat([G[k][l][m][r] for r in rs]).cpu()
+            X, Y, LG, DY, DX = cat("x"), cat("y"), cat("logits"), cat("dy"), cat("dx")
+            fw, bw = ref.layer_forward_backward(f64(X), w_r, Wg, Wu, Wd, f64(DY), cfg.k, cfg.cf,
+                                                ep, logits=LG.numpy())
+            checks["routing"] &= bool((cat("topk").numpy() == fw["topk_idx"]).all())
+            for i, r in enumerate(rs):
+                checks["routing"] &= bool((G["dest"][l][m][r].cpu().numpy() ==
+                                           fw["plan"]["ranks"][i]["dest_row"]).all())
+            errs[f"y{g}.{m}"] = rel_err(f64(Y), fw["y"])
+            errs[f"dx{g}.{m}"] = rel_err(f64(DX), bw["dx"])
+            acc = lambda a, b: b if a is None else [u + v for u, v in zip(a, b)]
+            dWg, dWu, dWd = acc(dWg, bw["dW_gate"]), acc(dWu, bw["dW_up"]), acc(dWd, bw["dW_down"])
+            dWr = bw["dW_r"] if dWr is None else dWr + bw["dW_r"]
+            # hand-offs: layer g's output is layer g+1's input, layer g+1's dx is layer g's dy
+            if g + 1 < Lyr:
+                s2, l2 = divmod(g + 1, per)
+                for i in range(ep):
+                    r1, r2 = rs[i], ranks_of(s2)[i]
+                    checks["handoff"] &= bool(torch.equal(G["y"][l][m][r1], G["x"][l2][m][r2]))
+                    checks["handoff"] &= bool(torch.equal(G["dy"][l][m][r1], G["dx"][l2][m][r2]))
+        for x in range(cfg.E):
+            q, el = divmod(x, E_l)
+            r = rs[q]
+            dgu = f64(dW[l][1][r][el])
+            errs[f"dWg{g}.{x}"] = rel_err(dgu[:cfg.f].T, dWg[x])
+            errs[f"dWu{g}.{x}"] = rel_err(dgu[cfg.f:].T, dWu[x])
+            errs[f"dWd{g}.{x}"] = rel_err(f64(dW[l][2][r][el]).T, dWd[x])
+        errs[f"dWr{g}"] = rel_err(sum(f64(dW[l][0][r]) for r in rs).T, dWr)
+    worst = max(errs, key=errs.get)
+    res = {"pp": pp, "ep": ep, "layers": Lyr, "micro": M, "checks": checks,
+           "device_status": [int(t.item()) for t in st], "worst": [worst, errs[worst]],
+           "schedule_stage0": stack.ops if stage == 0 else None}
+    res["ok"] = (all(checks.values()) and all(v < TOL for v in errs.values()) and
+                 all(v == 0 for v in res["device_status"]))
+    if not res["ok"]:
+        res["bad"] = {k: v for k, v in errs.items() if not v < TOL}
+    print(json.dumps(res), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

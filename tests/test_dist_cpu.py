@@ -142,3 +142,102 @@ def test_gloo_world2_dedup_exchange():
         assert p.exitcode == 0
     for r in res:
         assert all(r[1:]), r
+
+
+class _ToyLayer:
+    """CPU stand-in for MoELayer with the interface PipelineStack uses (bf16 activations):
+    y = bf16(a*x + 1), dx = bf16(a*dy), and a 'weight gradient' dw = sum(dy*x) in fp32,
+    overwritten by the first backward and accumulated by the others."""
+
+    def __init__(self, dims, device=None, group=None, fused=True, dedup=False):
+        self.dims = dims
+        self.fs = 0
+        self.a = 1.0
+        self.y = torch.empty(dims.T_local, dims.d, dtype=torch.bfloat16)
+        self.dx = torch.empty(dims.T_local, dims.d, dtype=torch.bfloat16)
+        self.dw_r = torch.zeros(1)
+        self.dw_gu = torch.zeros(1)
+        self.dw_down = torch.zeros(1)
+        self.w_r = self.w_gu = self.w_down = self.bias = self.w_gu_s = self.w_down_s = None
+
+    def set_weights(self, w_r, w_gu, w_down, bias=None, w_gu_s=None, w_down_s=None):
+        self.a = float(w_r)
+
+    def forward(self, x):
+        self.x = x
+        self.y.copy_(self.a * x.float() + 1.0)
+        return self.y
+
+    def backward(self, dy, accumulate=False):
+        v = (dy.float() * self.x.float()).sum().reshape(1)
+        self.dw_r.copy_(self.dw_r + v if accumulate else v)
+        self.dx.copy_(self.a * dy.float())
+        return self.dx
+
+    def close(self):
+        pass
+
+
+def _pipe_worker(rank, world, port, q):
+    """PP=2 x EP=2 over gloo: the 1F1B op lists from libmoe, stage-to-stage activations and
+    gradients, per-micro-batch activation contexts and gradient accumulation -- bitwise
+    against the same bf16 arithmetic done sequentially."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2605_05049_b200 import LayerDims
+        from paper_2605_05049_b200.pipeline import PipelineStack
+        pp, ep, L, M, T, d = 2, 2, 4, 5, 3, 4
+        stage, e = divmod(rank, ep)
+        per = L // pp
+        dims = LayerDims(T, d, 4, 1, 8, 0, 1.0, ep, e)
+        st = PipelineStack(dims, L, pp, M, device=None, layer_cls=_ToyLayer)
+        a = [1.5, -0.5, 2.0, 0.25]                       # per global layer
+        for l in range(per):
+            st.set_weights(l, a[stage * per + l], None, None)
+        g = torch.Generator().manual_seed(7)
+        xs = [(torch.randn(T, d, generator=g) + e).bfloat16() for _ in range(M)]
+        dys = [(torch.randn(T, d, generator=g) - e).bfloat16() for _ in range(M)]
+        ys, dxs = st.step(xs if stage == 0 else None, dys if stage == pp - 1 else None)
+        # the same arithmetic, layer by layer, on this EP index's tokens
+        hs = [[x] for x in xs]
+        gs = [[None] * (L + 1) for _ in range(M)]
+        for m in range(M):
+            for l in range(L):
+                hs[m].append((a[l] * hs[m][l].float() + 1.0).bfloat16())
+            gs[m][L] = dys[m]
+            for l in reversed(range(L)):
+                gs[m][l] = (a[l] * gs[m][l + 1].float()).bfloat16()
+        ok = True
+        if stage == pp - 1:
+            ok &= all(torch.equal(ys[m], hs[m][L]) for m in range(M))
+        if stage == 0:
+            ok &= all(torch.equal(dxs[m], gs[m][0]) for m in range(M))
+        for l in range(per):
+            gl = stage * per + l
+            want = torch.zeros(1)
+            for m in range(M):
+                v = (gs[m][gl + 1].float() * hs[m][gl].float()).sum().reshape(1)
+                want = v if m == 0 else want + v
+            ok &= torch.equal(st.grads(l)[0], want)
+        ok &= st.n_slots == min(pp - stage, M)
+        q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_pipeline_pp2_ep2():
+    world = 4
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_pipe_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in res:
+        assert r[1], r

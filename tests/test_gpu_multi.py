@@ -141,3 +141,23 @@ def test_layer_ep_parity_dedup(nproc, config, extra, mode):
     print(res)
     assert res["ok"], res
     assert res["checks"]["dedup_pairs"] and res["checks"]["dedup_xr"], res
+
+
+@pytest.mark.parametrize("nproc,pp,extra", [(2, 2, ()), (4, 2, ()), (4, 4, ()),
+                                            (4, 2, ("--dedup", "dispatch"))])
+def test_pipeline_pp_x_ep(nproc, pp, extra):
+    """NEXT-3 PP x EP executor (1F1B PAPER.md:282-288): a 4-layer stack over
+    4 micro-batches; every (layer, micro-batch) against the teacher-forced fp64 oracle, the
+    stage-to-stage hand-offs bitwise, accumulated weight gradients vs the oracle's sum."""
+    if n_gpus() < nproc:
+        pytest.skip(f"needs {nproc} GPUs")
+    port = 30700 + nproc * 10 + pp + 5 * len(extra)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.join(ROOT, "tests", "mp_pipe_worker.py"), "--pp", str(pp), *extra]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    lines = [l for l in p.stdout.splitlines() if l.startswith("{")]
+    assert p.returncode == 0 and lines, f"worker failed:\n{p.stdout[-3000:]}\n{p.stderr[-3000:]}"
+    res = json.loads(lines[-1])
+    print(res)
+    assert res["ok"], res
