@@ -711,8 +711,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
               for (int q = 0; q < 32; ++q) a[q] = 0u;
             }
-            // double-buffered: only the store that used THIS box must have read it
-            if (lane == 0) bulk_wait_read1();
+            // the store that last used THIS box must have read it (STG = 2: that is the one
+            // before the most recent; STG = 1: the most recent)
+            if (lane == 0) {
+              if (STG == 2) bulk_wait_read1();
+              else bulk_wait_read0();
+            }
             __syncwarp();
             const uint32_t off = static_cast<uint32_t>(sbuf * kStageBox);
             stage_row(row_addr + off, lane, a);

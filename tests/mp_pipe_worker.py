@@ -76,17 +76,35 @@ def main():
     torch.cuda.synchronize()
     status = max(s.ctx.device_error() for slots in stack.layers for s in slots)
     rec = stack.record
+    # the stack's local layer 0 against a plain MoELayer with the same weights on the same
+    # recorded input and upstream gradient: y, dx and (M = 1) the weight gradients bitwise
+    from paper_2605_05049_b200 import MoELayer
+    plain = MoELayer(dims, device=local, group=stack.group, dedup=args.dedup)
+    w_r, w_gu, w_down = layer_weights(stage * per, range(e * E_l, (e + 1) * E_l), dev)
+    plain.set_weights(w_r, w_gu, w_down)
+    yp = plain.forward(rec[(0, 0)]["x"]).clone()
+    dxp = plain.backward(rec[(0, 0)]["dy"]).clone()
+    torch.cuda.synchronize()
+    dflag = [torch.equal(yp, rec[(0, 0)]["y"]), torch.equal(dxp, rec[(0, 0)]["dx"])]
+    if M == 1:
+        dflag += [torch.equal(plain.dw_gu, stack.grads(0)[1]),
+                  torch.equal(plain.dw_down, stack.grads(0)[2]),
+                  torch.equal(plain.dw_r, stack.grads(0)[0])]
+    direct = all(dflag)
+    plain.close()
     # gather: [rank][local layer][m] tensors
     keys = ["x", "y", "logits", "topk", "dest", "dy", "dx"]
     G = {k: [[gather(rec[(l, m)][k]) for m in range(M)] for l in range(per)] for k in keys}
     dW = [[gather(t) for t in stack.grads(l)] for l in range(per)]   # dw_r, dw_gu, dw_down
     st = gather(torch.tensor([status], device=dev))
+    dflags = gather(torch.tensor([int(direct)], device=dev))
     if rank != 0:
         dist.barrier()
         dist.destroy_process_group()
         return
     from oracle import moe_ref as ref
     errs, checks = {}, {"routing": True, "handoff": True}
+    errs_norm = {}
     ranks_of = lambda s_: list(range(s_ * ep, (s_ + 1) * ep))
     for g in range(Lyr):
         s_, l = divmod(g, per)
@@ -123,8 +141,12 @@ def main():
             errs[f"dWg{g}.{x}"] = rel_err(dgu[:cfg.f].T, dWg[x])
             errs[f"dWu{g}.{x}"] = rel_err(dgu[cfg.f:].T, dWu[x])
             errs[f"dWd{g}.{x}"] = rel_err(f64(dW[l][2][r][el]).T, dWd[x])
+            if x == 0:
+                errs_norm[f"dWd{g}.0"] = float(np.linalg.norm(f64(dW[l][2][r][el]).T) /
+                                               max(np.linalg.norm(dWd[x]), 1e-30))
         errs[f"dWr{g}"] = rel_err(sum(f64(dW[l][0][r]) for r in rs).T, dWr)
     worst = max(errs, key=errs.get)
+    checks["direct_layer0"] = all(bool(t.item()) for t in dflags)
     res = {"pp": pp, "ep": ep, "layers": Lyr, "micro": M, "checks": checks,
            "device_status": [int(t.item()) for t in st], "worst": [worst, errs[worst]],
            "schedule_stage0": stack.ops if stage == 0 else None}
@@ -132,6 +154,7 @@ def main():
                  all(v == 0 for v in res["device_status"]))
     if not res["ok"]:
         res["bad"] = {k: v for k, v in errs.items() if not v < TOL}
+        res["norm_ratio"] = errs_norm
     print(json.dumps(res), flush=True)
     dist.barrier()
     dist.destroy_process_group()
