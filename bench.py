@@ -727,9 +727,29 @@ def run_pipeline(args):
     torch.cuda.synchronize()
     dist.barrier()
     clk = clocks.stop()
-    ms = torch.tensor([t0.elapsed_time(t1) / args.steps], dtype=torch.float64, device=dev)
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    ms = float(ms.item())
+    eager = t0.elapsed_time(t1) / args.steps
+    graph_ms, graph_note = 0.0, None
+    if args.graph:
+        # the whole 1F1B step (layer calls + NCCL hand-offs) replayed from one CUDA graph
+        try:
+            graph = stack.capture(xs if first else None, dys if last else None)
+            for _ in range(args.warmup):
+                graph.replay()
+            torch.cuda.synchronize()
+            dist.barrier()
+            t0.record()
+            for _ in range(args.steps):
+                graph.replay()
+            t1.record()
+            torch.cuda.synchronize()
+            dist.barrier()
+            graph_ms = t0.elapsed_time(t1) / args.steps
+        except Exception as exc:   # reported, the eager number stands
+            graph_note = f"capture failed: {type(exc).__name__}: {str(exc)[:200]}"
+    tt = torch.tensor([eager, graph_ms], dtype=torch.float64, device=dev)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    eager, graph_ms = tt.tolist()
+    ms = graph_ms if (args.graph and graph_ms > 0 and graph_ms < eager) else eager
     # serial per-stage GEMM bound of the step: every stage does M micro-batches of L/PP layers
     rows = M * T_r * cfg.k
     gemm_flops = (Lyr // pp) * 18 * rows * cfg.d * cfg.f
@@ -743,7 +763,8 @@ def run_pipeline(args):
             "config": {"workload": f"{cfg.name} {Lyr}-layer MoE stack, 1F1B",
                        "parallelism": f"pp{pp}xep{ep}", "micro_batches": M,
                        "tokens_per_micro_batch": T_mb, "layers": Lyr,
-                       "dedup_a2a": args.dedup},
+                       "dedup_a2a": args.dedup, "eager_ms_per_step": eager,
+                       "graph_ms_per_step": graph_ms or None, "graph_note": graph_note},
             "gpu_launches": None, "clocks": clk,
             "stage_gemm_bound_ms": gemm_flops / (peaks["bf16_sustained"] * 1e12) * 1e3,
             "pipeline_bubble_bound": (pp - 1) / (M + pp - 1),

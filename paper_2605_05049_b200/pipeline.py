@@ -137,6 +137,26 @@ class PipelineStack:
             p.wait()
         return (self.y_out if last else None), (self.dx_out if self.prev is None else None)
 
+    def capture(self, xs=None, dys=None):
+        """Records one step(xs, dys) -- every layer call and the NCCL stage hand-offs -- into a
+        CUDA graph and returns it; graph.replay() reruns the step on the current contents of
+        xs / dys (outputs in the buffers step() returns).  Collective: every rank captures
+        (one eager warm-up step on the capture stream first) and replays in lockstep."""
+        dev = self.device
+        s = torch.cuda.Stream(device=dev)
+        s.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(s):
+            self.step(xs, dys)
+        torch.cuda.current_stream(dev).wait_stream(s)
+        torch.cuda.synchronize(dev)
+        self.dist.barrier()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            self.step(xs, dys)
+        torch.cuda.synchronize(dev)
+        self.dist.barrier()
+        return g
+
     def _rec(self, l, m, **tensors):
         r = self.record.setdefault((l, m), {})
         for k, t in tensors.items():

@@ -45,6 +45,8 @@ def main():
     ap.add_argument("--layers", type=int, default=4)
     ap.add_argument("--micro", type=int, default=4)
     ap.add_argument("--dedup", default=None)
+    ap.add_argument("--graph", action="store_true",
+                    help="also replay the step from a CUDA graph: bitwise equal to eager")
     args = ap.parse_args()
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -71,6 +73,22 @@ def main():
     xs = [x_all[m, e * T_r:(e + 1) * T_r].contiguous() for m in range(M)]
     dys = [dy_all[m, e * T_r:(e + 1) * T_r].contiguous() for m in range(M)]
     stack.step(xs if stage == 0 else None, dys if stage == pp - 1 else None)   # warm-up step
+    graph_ok = True
+    if args.graph:
+        a_in, a_dy = (xs if stage == 0 else None), (dys if stage == pp - 1 else None)
+        ye, dxe = stack.step(a_in, a_dy)
+        ye = [t.clone() for t in ye] if ye is not None else None
+        dxe = [t.clone() for t in dxe] if dxe is not None else None
+        dwe = [t.clone() for t in stack.grads(0)]
+        graph = stack.capture(a_in, a_dy)
+        graph.replay()
+        torch.cuda.synchronize()
+        if ye is not None:
+            graph_ok &= all(torch.equal(u, v) for u, v in zip(ye, stack.y_out))
+        if dxe is not None:
+            graph_ok &= all(torch.equal(u, v) for u, v in zip(dxe, stack.dx_out))
+        graph_ok &= all(torch.equal(u, v) for u, v in zip(dwe, stack.grads(0)))
+        del graph
     stack.record = {}
     ys, dxs = stack.step(xs if stage == 0 else None, dys if stage == pp - 1 else None)
     torch.cuda.synchronize()
@@ -98,6 +116,7 @@ def main():
     dW = [[gather(t) for t in stack.grads(l)] for l in range(per)]   # dw_r, dw_gu, dw_down
     st = gather(torch.tensor([status], device=dev))
     dflags = gather(torch.tensor([int(direct)], device=dev))
+    gflags = gather(torch.tensor([int(graph_ok)], device=dev))
     if rank != 0:
         dist.barrier()
         dist.destroy_process_group()
@@ -147,6 +166,7 @@ def main():
         errs[f"dWr{g}"] = rel_err(sum(f64(dW[l][0][r]) for r in rs).T, dWr)
     worst = max(errs, key=errs.get)
     checks["direct_layer0"] = all(bool(t.item()) for t in dflags)
+    checks["graph_replay"] = all(bool(t.item()) for t in gflags)
     res = {"pp": pp, "ep": ep, "layers": Lyr, "micro": M, "checks": checks,
            "device_status": [int(t.item()) for t in st], "worst": [worst, errs[worst]],
            "schedule_stage0": stack.ops if stage == 0 else None}

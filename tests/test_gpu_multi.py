@@ -144,14 +144,14 @@ def test_layer_ep_parity_dedup(nproc, config, extra, mode):
 
 
 @pytest.mark.parametrize("nproc,pp,extra", [(2, 2, ()), (4, 2, ()), (4, 4, ()),
-                                            (4, 2, ("--dedup", "dispatch"))])
+                                            (4, 2, ("--dedup", "dispatch")), (4, 2, ("--graph",))])
 def test_pipeline_pp_x_ep(nproc, pp, extra):
     """NEXT-3 PP x EP executor (1F1B PAPER.md:282-288): a 4-layer stack over
     4 micro-batches; every (layer, micro-batch) against the teacher-forced fp64 oracle, the
     stage-to-stage hand-offs bitwise, accumulated weight gradients vs the oracle's sum."""
     if n_gpus() < nproc:
         pytest.skip(f"needs {nproc} GPUs")
-    port = 30700 + nproc * 10 + pp + 5 * len(extra)
+    port = 30700 + nproc * 10 + pp + 5 * len(extra) + (20 if "--graph" in extra else 0)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr=127.0.0.1", f"--master-port={port}",
            os.path.join(ROOT, "tests", "mp_pipe_worker.py"), "--pp", str(pp), *extra]
