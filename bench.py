@@ -4,6 +4,8 @@
     python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 ... bench.py --gpus N
     python bench.py --impl reference ...   # the fp64 CPU oracle (the only reference this tier has)
     python bench.py --a2a                  # dispatch/combine GB/s sweep vs NCCL all_to_all
+    python bench.py --config dsmoe|dsv3 [--rebalance] [--dedup [dispatch|all]]  # fine-grained
+    torchrun ... bench.py --gpus 4 --pp 2 [--graph]   # NEXT-3 PP x EP 1F1B stack (own metric)
 
 A "step" is one forward + backward of the whole layer
 over T tokens of the EP group (T/N per rank, experts sharded E/N per rank).  At N=1 the
