@@ -746,6 +746,10 @@ def run_pipeline(args):
             torch.cuda.synchronize()
             dist.barrier()
             graph_ms = t0.elapsed_time(t1) / args.steps
+            # release the captured NCCL work before the contexts and the process group go
+            # (keeping the graph alive through close/destroy hung the processes at exit)
+            del graph
+            torch.cuda.synchronize()
         except Exception as exc:   # reported, the eager number stands
             graph_note = f"capture failed: {type(exc).__name__}: {str(exc)[:200]}"
     tt = torch.tensor([eager, graph_ms], dtype=torch.float64, device=dev)
