@@ -217,3 +217,28 @@ def test_spec_tinymoe_expert_memory_terms_golden():
         else:
             # balanced routing: every rank holds T*k/EP expert rows
             assert counters.expert_activation_bytes([T * k // ep], d, f) == val
+
+
+def test_router_and_hbm_counters_against_direct_counts():
+    """router_flops: 2 x the multiply-adds a loop over x W_r performs (fwd), twice that for
+    dx = dl W_r^T and dW_r = x^T dl; hbm_bytes_permute / _unpermute: the bytes of the 2-byte
+    arrays the oracle's permute / unpermute read and write (x, the kept rows, y)."""
+    T, d, E = 3, 4, 5
+    macs = 0
+    for t in range(T):
+        for e in range(E):
+            for c in range(d):
+                macs += 1
+    fl = counters.router_flops(T, d, E)
+    assert fl["fwd"] == 2 * macs and fl["bwd"] == 4 * macs
+    import synth
+    T_r, E, k, d = 64, 8, 2, 16
+    idx, _ = ref.route(synth.random_logits(T_r, E, seed=3).numpy(), k)
+    pos = ref.positions(idx, E, ref.capacity(0.75, k, T_r, E))      # with drops
+    x = np.zeros((T_r, d), np.float16)                                # a 2-byte element type
+    rows = int(pos["counts"].sum())
+    xs = ref.permute_rows(x, pos["dest_row"], rows)
+    assert rows < T_r * k
+    assert counters.hbm_bytes_permute(T_r, rows, d) == x.nbytes + xs.nbytes
+    y = np.zeros_like(x)
+    assert counters.hbm_bytes_unpermute(T_r, rows, d) == xs.nbytes + y.nbytes
