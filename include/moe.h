@@ -25,8 +25,10 @@
  *   collective calls still take part in the exchange.
  * - Collective calls (moe_dispatch, moe_dispatch_bwd, moe_combine,
  *   moe_combine_bwd, their _range variants, the fused *_combine / *_dispatch FFN
- *   calls, moe_symm_alloc) must be issued by every EP rank in the same order, like
- *   NCCL collectives.  Not thread-safe; one ctx per (process, GPU).
+ *   calls, the moe_dedup_* all-to-alls, moe_symm_alloc) must be issued by every EP
+ *   rank in the same order, like NCCL collectives.  Not thread-safe; one ctx per
+ *   (process, GPU, layer activation context) -- several ctxs per process are fine
+ *   (the PP x EP executor keeps one per layer and in-flight micro-batch).
  * - A collective's destination buffer is written by PEERS from the moment they enter
  *   the call: a rank must not write it itself (e.g. zero it) after its previous
  *   collective returned unless every rank has passed that point (a barrier), or the
