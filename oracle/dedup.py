@@ -29,6 +29,13 @@ Reading R18, step by step:
 5. Backward.  combine_bwd sends dy_t once per pair; the owner expands dO rows g*dy_t and
    forms dg_{t,j} = <dy_t, O_{t,j}> locally (O never leaves the owner); dispatch_bwd
    returns dxpart[u] = sum_{j on q} dX_{t,j} per pair, and dx_t = sum_q dxpart.
+
+Pins (tests/test_oracle_dedup.py, CPU): pure-Python brute force of the pairs (also under a
+migrated placement); the balanced-fixture closed form ntok[r][q] = max(1, k/E_l) T_r / EP and
+the egress ratio; E_l = 1 or k = 1 reduce to the plain dispatch (one slot per pair, ntok =
+counts per owner); invariants (every kept slot named exactly once, at moe_ref's receive row,
+with its gate); expand rebuilds the plain receive buffer bit for bit; the pair reductions
+reproduce moe_ref's y, dx and dgates to 1e-12; layout bases on a hand-worked matrix.
 """
 from __future__ import annotations
 

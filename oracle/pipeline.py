@@ -14,6 +14,12 @@ Reading R19, the paper being silent on the exact op order: the PipeD
 and one backward while forwards remain, then the remaining backwards; micro-batches in
 ascending order in both directions.  Rank of mesh point (stage i, expert-parallel index e) is
 i * EP + e (EP groups contiguous, the paper's "EP within the fast domain").
+
+Pins (tests/test_oracle_pipeline.py, CPU): every micro-batch forwarded and backwarded once per
+stage, F before B; peak in-flight = min(PP - i, M); a dependency simulation
+drains without deadlock in 2 (M + PP - 1) unit ticks (the 1F1B makespan) with stage 0's first
+backward at tick 2 PP - 1; M(0) - M(PP-1) = L (PP-1)/PP x one micro-batch's activations
+(PAPER.md:334-344).
 """
 from __future__ import annotations
 
