@@ -372,7 +372,7 @@ def run_ours(args):
     buckets = {"moe_permute": "permute", "moe_dispatch": "dispatch",
                "moe_dispatch_range": "dispatch", "moe_combine_bwd": "combine_bwd",
                "moe_combine_bwd_range": "combine_bwd", "moe_dedup_dispatch": "dispatch",
-               "moe_dedup_combine_bwd": "combine_bwd"}
+               "moe_dedup_combine_bwd": "combine_bwd", "moe_dedup_combine_bwd_ys": "combine_bwd"}
     originals = {n: getattr(layer_mod.L, n) for n in hooked + list(buckets)}
     for n in hooked:
         setattr(layer_mod.L, n, timed(originals[n]))
@@ -552,8 +552,10 @@ def run_ours(args):
             "permute": {"bound": "hbm", "ms": perm_ms,
                         "achieved_gbs": permute_bytes / (perm_ms * 1e-3) / 1e9 if perm_ms else None,
                         "peak_gbs": peaks["hbm"], "bytes_rank0": permute_bytes,
-                        "note": "4 kernels (histogram, scan, rank, scatter); algorithmic bytes = "
-                                "x read + xs write"},
+                        "note": ("indices only (dedup: no xs scatter; the dedup dispatch reads x)"
+                                 if layer.dedup else
+                                 "3 kernels (histogram+scan, rank, scatter); algorithmic bytes = "
+                                 "x read + xs write")},
             "dispatch": {"bound": "nvlink" if world > 1 else "hbm (EP=1: local copy)",
                          "ms": disp_ms, "egress_bytes_rank0": a2a_bytes["egress"],
                          "ingress_bytes_rank0": a2a_bytes["ingress"],
