@@ -178,7 +178,7 @@ class _ToyLayer:
         pass
 
 
-def _pipe_worker(rank, world, port, q):
+def _pipe_worker(rank, world, port, q, pp=2, M=5):
     """PP=2 x EP=2 over gloo: the 1F1B op lists from libmoe, stage-to-stage activations and
     gradients, per-micro-batch activation contexts and gradient accumulation -- bitwise
     against the same bf16 arithmetic done sequentially."""
@@ -188,7 +188,8 @@ def _pipe_worker(rank, world, port, q):
     try:
         from paper_2605_05049_b200 import LayerDims
         from paper_2605_05049_b200.pipeline import PipelineStack
-        pp, ep, L, M, T, d = 2, 2, 4, 5, 3, 4
+        ep = world // pp
+        L, T, d = 4, 3, 4
         stage, e = divmod(rank, ep)
         per = L // pp
         dims = LayerDims(T, d, 4, 1, 8, 0, 1.0, ep, e)
@@ -227,12 +228,16 @@ def _pipe_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_gloo_pipeline_pp2_ep2():
+@pytest.mark.parametrize("pp,M", [(2, 5), (4, 2), (4, 6)])
+def test_gloo_pipeline(pp, M):
+    """PP x EP over gloo with 4 ranks: PP2 x EP2 (M = 5), PP4 x EP1 with fewer micro-batches
+    than stages (M = 2: the in-flight bound is M) and with more (M = 6)."""
     world = 4
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_pipe_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_pipe_worker, args=(r, world, port, q, pp, M))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=180) for _ in range(world)]
