@@ -191,6 +191,19 @@ void use_stream_k(const moe_ctx* c, moe::GemmProblem& g) {
   g.sk_flags = c->d_sk_flags;
 }
 
+// Tile raster of the M-grouped expert GEMMs (GEMM1, GEMM2, both dgrads): 0 = m fastest (the
+// default: a wave covers whole expert row blocks, so the weight stripes are shared in L2),
+// MOE_RASTER_N=1 = n fastest (the activation stripes shared instead) -- an experiment knob for
+// the DRAM re-read measurements, read once.
+int raster_n_fastest() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MOE_RASTER_N");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v;
+}
+
 int pick_bn(int n) {
   if (n % 256 == 0) return 256;
   if (n % 128 == 0) return 128;
@@ -594,6 +607,7 @@ moe_status ffn_up(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows, int
   g1.group_rows = group_rows; g1.n_groups = n_groups; g1.group_begin = g0; g1.rows_cap = rows_cap;
   g1.pair = gemm_pair();
   g1.max_ctas = c->gemm_sms;
+  g1.n_fastest = raster_n_fastest();
   g1.out = g_u_h; g1.ld_out = 3 * static_cast<int64_t>(f); g1.f = f;
   use_stream_k(c, g1);
   return cuda_status(moe::launch_grouped_gemm(g1, st(s)));
@@ -617,6 +631,7 @@ moe_status ffn_down(moe_ctx* c, const int32_t* group_rows, int32_t n_groups, int
   g2.group_rows = group_rows; g2.n_groups = n_groups; g2.rows_cap = rows_cap;
   g2.pair = gemm_pair();
   g2.max_ctas = c->gemm_sms;
+  g2.n_fastest = raster_n_fastest();
   g2.out = out ? static_cast<void*>(out) : static_cast<void*>(g_u_h); g2.ld_out = d;
   use_stream_k(c, g2);
   if (sc) {
@@ -662,6 +677,7 @@ moe_status ffn_bwd_dh(moe_ctx* c, const int32_t* group_rows, int32_t g0, int32_t
   a.group_rows = group_rows; a.n_groups = n_groups; a.group_begin = g0; a.rows_cap = rows_cap;
   a.pair = gemm_pair();
   a.max_ctas = c->gemm_sms;
+  a.n_fastest = raster_n_fastest();
   a.out = dgu; a.ld_out = 2 * F; a.aux = g_u_h; a.ld_aux = 3 * F; a.f = f;
   use_stream_k(c, a);
   return cuda_status(moe::launch_grouped_gemm(a, st(s)));
@@ -694,6 +710,7 @@ moe_status ffn_bwd_dx(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows,
   b.group_rows = group_rows; b.n_groups = n_groups; b.rows_cap = rows_cap;
   b.pair = gemm_pair();
   b.max_ctas = c->gemm_sms;
+  b.n_fastest = raster_n_fastest();
   b.out = dxr ? static_cast<void*>(dxr) : const_cast<moe_bf16*>(dgu); b.ld_out = d;
   use_stream_k(c, b);
   if (sc) {  // dX rows go straight back to their source ranks (dispatch_bwd fused)
