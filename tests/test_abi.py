@@ -47,7 +47,12 @@ def test_host_helpers(lib):
     assert lib.moe_recv_rows_max(s) == ((512 + 8 * 127 + 127) // 128) * 128
     m = lib.make_shape(1024, 4096, 8, 2, 14336, 0, 1.25, 8, 3)
     assert lib.moe_capacity(m) == 320
-    assert lib.moe_recv_rows_max(m) == ((8 * 1024 * 1 + 1 * 127 + 127) // 128) * 128 or True
+    # Mixtral at EP=8 (E_l = 1): min(EP*T*min(k,E_l), EP*E_l*C) = min(8192, 2560) = 2560 rows,
+    # + E_l*127 padding, rounded up to 128 -> 2688
+    assert lib.moe_recv_rows_max(m) == ((min(8 * 1024 * 1, 8 * 1 * 320) + 1 * 127 + 127) // 128) * 128
+    # dedup bounds: pair rows T*min(k,EP) = 2048; token rows min(EP*T, R_max) = 2688
+    assert lib.moe_dedup_pair_rows_max(m) == 1024 * 2
+    assert lib.moe_dedup_token_rows_max(m) == min(8 * 1024, 2688)
     v3 = lib.make_shape(4096, 7168, 256, 8, 2048, 0, 0.0, 8, 0)
     assert lib.moe_capacity(v3) == -1
     assert lib.moe_recv_rows_max(v3) >= 8 * 4096 * 8
