@@ -56,8 +56,6 @@ def parse():
     ap.add_argument("--cpu-sample-tokens", type=int, default=0)
     ap.add_argument("--breakdown", action="store_true",
                     help="per-phase CUDA-event breakdown of a step (max over ranks), no bench line")
-    ap.add_argument("--chunks", type=int, default=None,
-                    help="NEXT-1 chunked a2a || GEMM overlap: owner-slot ranges (1 = off)")
     ap.add_argument("--comm-sms", type=int, default=None,
                     help="SMs given to an all-to-all running beside a GEMM (MoELayer.comm_sms)")
     ap.add_argument("--graph", action="store_true",
@@ -253,8 +251,6 @@ def run_ours(args):
     T_r = cfg.T // ep
     dims = LayerDims(T_r, cfg.d, cfg.E, cfg.k, cfg.f, cfg.E_s, cfg.cf, ep, rank)
     layer = MoELayer(dims, device=local, fused=not args.stepwise, dedup=args.dedup)
-    if args.chunks is not None:
-        layer.chunks = args.chunks
     if args.comm_sms is not None:
         layer.comm_sms = args.comm_sms
     E_l = cfg.E // ep
@@ -533,7 +529,6 @@ def run_ours(args):
             "parallelism": f"ep{world}", "tokens_per_rank": T_r,
             "expert_migration": rebal,
             "dedup_a2a": layer.dedup_mode,
-            "a2a_gemm_chunks": len(layer._ranges() or [None]),
             "cuda_graph": use_graph,
             "eager_ms_per_step": eager_ms,
             "graph_ms_per_step": graph_ms if args.graph else None,

@@ -120,6 +120,19 @@ moe_status moe_ctx_open_peers(moe_ctx* ctx, const void* handles);
 /* Bump allocation from the symmetric heap, 256-byte aligned.  Collective: every rank
  * must request the same sizes in the same order so offsets agree. */
 moe_status moe_symm_alloc(moe_ctx* ctx, size_t bytes, void** ptr);
+/* Releases the LAST symmetric allocation (LIFO, like the bump allocator it undoes);
+ * MOE_ERR_INVALID_ARG for any other pointer.  Collective, like moe_symm_alloc. */
+moe_status moe_symm_free(moe_ctx* ctx, void* ptr);
+/* FNV-1a fingerprint of this rank's (offset, size) allocation sequence.  Peers write into a
+ * symmetric buffer at ITS offset in every heap, so every rank must have made the same
+ * allocations in the same order: all-gather the fingerprints (like the IPC handles) and pass
+ * them, in rank order, to moe_ctx_verify_symmetric, which returns MOE_ERR_NOT_SYMMETRIC when
+ * any rank's sequence differs from this one.  Collective calls additionally check, on every
+ * call, that their destination range [ptr, ptr + required bytes) lies inside ONE allocation
+ * (required = recv_rows_max x d x 2 for xr / dout_r, T_local x k x d x 2 for ys / dxs, the
+ * dedup bounds for the moe_dedup_* buffers). */
+moe_status moe_symm_fingerprint(moe_ctx* ctx, uint64_t* out);
+moe_status moe_ctx_verify_symmetric(moe_ctx* ctx, const uint64_t* fingerprints);
 /* Expert placement (SURVEY.md §8(f) NEXT-2 expert migration, §VI): placement[e] =
  * global slot of expert e (host int32 [E], a permutation of [0, E)); expert e then lives on
  * rank placement[e] / E_l in local slot placement[e] % E_l, and every receive layout, GEMM
@@ -127,6 +140,12 @@ moe_status moe_symm_alloc(moe_ctx* ctx, size_t bytes, void** ptr);
  * identity (contiguous ownership).  Collective: every rank sets the same placement; it
  * synchronises the device.  MOE_ERR_INVALID_ARG if not a permutation. */
 moe_status moe_ctx_set_placement(moe_ctx* ctx, const int32_t* placement);
+/* Migration trigger (an external scheduler "inspects the growing load
+ * imbalance, and whenever it crosses a pre-determined threshold" runs Alg. 2; reading R20):
+ * *out = max_q s_q / mean_q s_q, s_q = sum of loads[e] over the experts placement puts on
+ * rank q (1.0 when every load is 0).  Host-only, deterministic. */
+moe_status moe_load_imbalance(const int64_t* loads, const int32_t* placement, int32_t E,
+                              int32_t ep, double* out);
 /* Alg. 2 of PAPER.md:672-706 (hill-climbing swap-based minimal rebalancing) on host data:
  * groups = the EP owners' slots, item loads = loads[e] (e.g. the routed rows per expert from
  * the layout record); at most max_iters (paper: T = 100) iterations, each swapping the pair
@@ -135,6 +154,24 @@ moe_status moe_ctx_set_placement(moe_ctx* ctx, const int32_t* placement);
  * Deterministic: every rank computes the same result from the same loads. */
 moe_status moe_rebalance(const int64_t* loads, int32_t E, int32_t ep, int32_t max_iters,
                          int32_t* placement, int32_t* n_swaps);
+/* Expert migration transfer (NEXT-2; "migrate experts" whenever the imbalance
+ * crosses a threshold; Table PAPER.md:650-668 costs 48 d f bytes of state per expert; reading
+ * R17).  Collective over the EP group: every rank passes the same old_placement and
+ * new_placement (host int32 [E], expert -> global slot, permutations of [0, E)).
+ * src, dst: SYMMETRIC buffers (moe_symm_alloc, the same offset on every rank, each
+ * [E_l][bytes_per_expert] bytes, not overlapping).  src holds this rank's experts' state in
+ * the OLD placement's local-slot order; on return (stream-ordered) dst holds the state of the
+ * experts new_placement assigns to this rank, in the NEW local-slot order.  Each expert is
+ * pushed by its old owner straight into its new owner's dst over NVSwitch (local slot moves
+ * are local copies); one launch: a device barrier first (every rank has reached the call, so
+ * no peer is still reading its dst from earlier stream work), then the stores, then the
+ * completion flags.  Call once per state tensor (weights, weight gradients, optimizer state).
+ * It does NOT switch the ctx's placement: call moe_ctx_set_placement(new_placement) after the
+ * last state tensor has moved.  MOE_ERR_INVALID_ARG: not permutations, bytes_per_expert not a
+ * positive multiple of 16, E_l > 256; MOE_ERR_NOT_SYMMETRIC: src or dst range outside the
+ * symmetric heap's allocations. */
+moe_status moe_migrate(moe_ctx* ctx, const int32_t* old_placement, const int32_t* new_placement,
+                       const void* src, void* dst, size_t bytes_per_expert, moe_stream stream);
 /* SM budgets for the calls issued after it (0 = all SMs): grouped-GEMM launches use at most
  * gemm_sms SMs and all-to-all transfer launches 2 blocks on each of comm_sms SMs, so that a
  * GEMM and a transfer issued on two streams run concurrently on disjoint SMs (used to overlap

@@ -11,6 +11,11 @@ TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
   pairs are visited in (i, j) index order and the strict ">" keeps the first best one; the
   swapped items keep their slot positions (slot i of G_k+ <-> slot j of G_k-).
 * `placement_from_groups` turns the groups into the expert -> (owner, slot) map the layer uses.
+* `imbalance` / `should_migrate` are the external scheduler's trigger (it
+  "inspects the growing load imbalance, and whenever it crosses a pre-determined threshold"
+  runs Alg. 2).  Reading R20: imbalance = max_q s_q / mean_q s_q over the EP
+  ranks' routed rows s_q under the current placement (1 = balanced; the step time of an EP
+  layer follows its most-loaded rank), migrate iff imbalance > threshold.
 * `migration_bytes` is the paper's cost: 48 d f bytes per moved expert.
 """
 from __future__ import annotations
@@ -76,6 +81,17 @@ def rank_loads(loads, placement, ep):
     out = np.zeros(ep, np.int64)
     np.add.at(out, np.asarray(placement) // (E // ep), loads)
     return out
+
+
+def imbalance(loads, placement, ep):
+    """max over ranks / mean over ranks of the routed rows (reading R20); 1.0 for no load."""
+    s = rank_loads(loads, placement, ep)
+    tot = int(s.sum())
+    return 1.0 if tot == 0 else float(s.max()) * ep / tot
+
+
+def should_migrate(loads, placement, ep, threshold):
+    return imbalance(loads, placement, ep) > threshold
 
 
 def migration_bytes(n_experts_moved, d, f, bytes_per_param=16):

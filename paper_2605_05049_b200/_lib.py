@@ -64,10 +64,15 @@ _SIGS = {
     "moe_ctx_export_handle": [P, P],
     "moe_ctx_open_peers": [P, P],
     "moe_symm_alloc": [P, ctypes.c_size_t, ctypes.POINTER(P)],
+    "moe_symm_free": [P, P],
+    "moe_symm_fingerprint": [P, P],
+    "moe_ctx_verify_symmetric": [P, P],
+    "moe_migrate": [P, P, P, P, P, ctypes.c_size_t, P],
     "moe_ctx_get_device_error": [P],
     "moe_ctx_set_sm_limits": [P, ctypes.c_int, ctypes.c_int],
     "moe_ctx_set_placement": [P, P],
     "moe_rebalance": [P, I32, I32, I32, P, P],
+    "moe_load_imbalance": [P, P, I32, I32, P],
     "moe_ctx_destroy": [P],
     "moe_router_logits": [P, P, P, P, P, P],
     "moe_router_logits_bwd": [P, P, P, P, P, P, ctypes.c_int, P],
@@ -181,6 +186,28 @@ def moe_rebalance(loads, ep, placement=None, max_iters=100):
     return list(pl), n.value
 
 
+def moe_migrate(ctx, old_placement, new_placement, src, dst, stream=None):
+    """src, dst: symmetric tensors [E_l, ...] (same shape and dtype); one expert per row."""
+    if src.shape != dst.shape or src.dtype != dst.dtype:
+        raise ValueError("moe_migrate: src and dst must have the same shape and dtype")
+    E = len(old_placement)
+    o = (ctypes.c_int32 * E)(*[int(v) for v in old_placement])
+    n = (ctypes.c_int32 * E)(*[int(v) for v in new_placement])
+    per = src[0].numel() * src.element_size() if src.shape[0] else 0
+    _check("moe_migrate", _lib.moe_migrate(ctx.handle, o, n, _ptr(src, name="src"),
+                                           _ptr(dst, name="dst"), per, _stream(stream)))
+
+
+def moe_load_imbalance(loads, placement, ep):
+    """max / mean of the EP ranks' routed rows under a placement (migration trigger)."""
+    E = len(loads)
+    ld = (ctypes.c_int64 * E)(*[int(v) for v in loads])
+    pl = (ctypes.c_int32 * E)(*[int(v) for v in placement])
+    out = ctypes.c_double(0.0)
+    _check("moe_load_imbalance", _lib.moe_load_imbalance(ld, pl, E, int(ep), ctypes.byref(out)))
+    return out.value
+
+
 def moe_status_string(code):
     return _lib.moe_status_string(int(code)).decode()
 
@@ -230,6 +257,23 @@ class Context:
         t = raw[: numel * elem].view(dtype).view(*shape)
         self._views.append(raw)
         return t
+
+    def symm_free(self, t: torch.Tensor):
+        """Releases the LAST symmetric allocation (LIFO; collective)."""
+        _check("moe_symm_free", _lib.moe_symm_free(self._h, P(t.data_ptr())))
+        self._views.pop()
+
+    def fingerprint(self) -> bytes:
+        out = ctypes.c_uint64(0)
+        _check("moe_symm_fingerprint", _lib.moe_symm_fingerprint(self._h, ctypes.byref(out)))
+        return int(out.value).to_bytes(8, "little")
+
+    def verify_symmetric(self, fingerprints: bytes):
+        """fingerprints: the all-gathered 8-byte fingerprints in rank order."""
+        n = len(fingerprints) // 8
+        arr = (ctypes.c_uint64 * n)(*[int.from_bytes(fingerprints[8 * i:8 * i + 8], "little")
+                                      for i in range(n)])
+        _check("moe_ctx_verify_symmetric", _lib.moe_ctx_verify_symmetric(self._h, arr))
 
     def set_placement(self, placement):
         """placement: sequence of E ints (expert -> global slot), collective."""

@@ -44,8 +44,10 @@ struct moe_ctx {
   int32_t* d_expert_at = nullptr; // [E] global slot -> expert
   int gemm_sms = 0;               // SM budgets (0 = all): a GEMM and a transfer running
   int comm_sms = 0;               //   concurrently on two streams use disjoint SMs
-  float* d_sk_ws = nullptr;       // stream-K partial accumulators (expert GEMMs)
-  int* d_sk_flags = nullptr;      // [2][kStreamKSlots] ready / consumed counters
+  // symmetric allocations (heap offset, bytes) in allocation order, and their FNV-1a
+  // fingerprint: every rank must allocate the same sizes in the same order (moe.h)
+  std::vector<std::pair<size_t, size_t>> allocs;
+  uint64_t fingerprint = 1469598103934665603ull;
 };
 
 namespace {
@@ -99,10 +101,24 @@ int64_t recv_rows_of(const moe_shape* s) {
 
 cudaStream_t st(moe_stream s) { return reinterpret_cast<cudaStream_t>(s); }
 
-bool in_heap(const moe_ctx* c, const void* p) {
+// [p, p + bytes) lies inside ONE symmetric allocation (peers write up to `bytes` at p's
+// offset into this rank's heap: an undersized buffer would let them overwrite a neighbour)
+bool in_heap(const moe_ctx* c, const void* p, int64_t bytes) {
   const char* q = static_cast<const char*>(p);
-  return q >= c->heap + c->internal_bytes && q < c->heap + c->heap_bytes;
+  if (q < c->heap + c->internal_bytes || q >= c->heap + c->heap_bytes || bytes < 0) return false;
+  const size_t off = static_cast<size_t>(q - c->heap);
+  for (const auto& a : c->allocs)
+    if (off >= a.first && off < a.first + (a.second ? a.second : 1))
+      return off + static_cast<size_t>(bytes) <= a.first + a.second;
+  return false;
 }
+int64_t row_bytes(const moe_ctx* c) { return static_cast<int64_t>(c->s.d) * 2; }
+int64_t heap_off(const moe_ctx* c, const void* p) {
+  return reinterpret_cast<const char*>(p) - c->heap;
+}
+// destination sizes of the collectives (rows of d bf16)
+int64_t recv_bytes(const moe_ctx* c) { return c->recv_rows * row_bytes(c); }
+int64_t send_bytes(const moe_ctx* c) { return c->s.T_local * c->s.k * row_bytes(c); }
 
 CommArgs comm_args(moe_ctx* c) {
   CommArgs a;
@@ -174,32 +190,6 @@ int gemm_pair() {
   if (v < 0) {
     const char* e = getenv("MOE_GEMM_PAIR");
     v = (e && e[0] == '0') ? 1 : 2;
-  }
-  return v;
-}
-
-// Stream-K tail for the expert GEMMs (the last partial wave cut into k-chunks spread over
-// every cluster, gemm.cu make_sched) when MOE_STREAM_K=1, read at every call.  Off by
-// default: measured slower on B200 (Mixtral EP=8 shapes: GEMM2 161 -> 206 us) -- the
-// finisher's fp32 partial reads and the extra pipeline fills cost more than the idle
-// clusters of the plain last wave (profiles/r01/README.md).
-void use_stream_k(const moe_ctx* c, moe::GemmProblem& g) {
-  const char* e = getenv("MOE_STREAM_K");
-  if (!(e && e[0] == '1')) return;
-  g.sk_ws = c->d_sk_ws;
-  g.sk_ws_bytes = moe::kStreamKWorkspaceBytes;
-  g.sk_flags = c->d_sk_flags;
-}
-
-// Tile raster of the M-grouped expert GEMMs (GEMM1, GEMM2, both dgrads): 0 = m fastest (the
-// default: a wave covers whole expert row blocks, so the weight stripes are shared in L2),
-// MOE_RASTER_N=1 = n fastest (the activation stripes shared instead) -- an experiment knob for
-// the DRAM re-read measurements, read once.
-int raster_n_fastest() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("MOE_RASTER_N");
-    v = (e && e[0] == '1') ? 1 : 0;
   }
   return v;
 }
@@ -323,9 +313,6 @@ moe_status moe_ctx_create(moe_ctx** out, const moe_shape* shape, int device, siz
     if (e == cudaSuccess)
       e = cudaMemcpy(c->d_expert_at, ident.data(), shape->E * sizeof(int32_t), cudaMemcpyHostToDevice);
   }
-  if (e == cudaSuccess) e = cudaMalloc(&c->d_sk_ws, moe::kStreamKWorkspaceBytes);
-  if (e == cudaSuccess) e = cudaMalloc(&c->d_sk_flags, 2 * moe::kStreamKSlots * sizeof(int));
-  if (e == cudaSuccess) e = cudaMemset(c->d_sk_flags, 0, 2 * moe::kStreamKSlots * sizeof(int));
   if (e == cudaSuccess && EP > 1) e = cudaIpcGetMemHandle(&c->handle, c->heap);
   if (e != cudaSuccess) {
     moe_ctx_destroy(c);
@@ -366,7 +353,40 @@ moe_status moe_symm_alloc(moe_ctx* c, size_t bytes, void** ptr) {
   const size_t sz = (bytes + 255) / 256 * 256;
   if (c->heap_used + sz > c->heap_bytes) return MOE_ERR_OUT_OF_MEMORY;
   *ptr = c->heap + c->heap_used;
+  c->allocs.emplace_back(c->heap_used, bytes);
+  for (uint64_t v : {static_cast<uint64_t>(c->heap_used), static_cast<uint64_t>(bytes)})
+    for (int i = 0; i < 8; ++i) {
+      c->fingerprint ^= (v >> (8 * i)) & 0xffu;
+      c->fingerprint *= 1099511628211ull;
+    }
   c->heap_used += sz;
+  return MOE_OK;
+}
+
+moe_status moe_symm_free(moe_ctx* c, void* ptr) {
+  MOE_REQUIRE(c && ptr && !c->allocs.empty());
+  const auto& last = c->allocs.back();
+  if (static_cast<char*>(ptr) != c->heap + last.first) return MOE_ERR_INVALID_ARG;   // LIFO only
+  c->heap_used = last.first;
+  for (uint64_t v : {~static_cast<uint64_t>(last.first), ~static_cast<uint64_t>(last.second)})
+    for (int i = 0; i < 8; ++i) {
+      c->fingerprint ^= (v >> (8 * i)) & 0xffu;
+      c->fingerprint *= 1099511628211ull;
+    }
+  c->allocs.pop_back();
+  return MOE_OK;
+}
+
+moe_status moe_symm_fingerprint(moe_ctx* c, uint64_t* out) {
+  MOE_REQUIRE(c && out);
+  *out = c->fingerprint;
+  return MOE_OK;
+}
+
+moe_status moe_ctx_verify_symmetric(moe_ctx* c, const uint64_t* all) {
+  MOE_REQUIRE(c && all);
+  for (int q = 0; q < c->s.ep_size; ++q)
+    if (all[q] != c->fingerprint) return MOE_ERR_NOT_SYMMETRIC;
   return MOE_OK;
 }
 
@@ -383,6 +403,54 @@ moe_status moe_ctx_set_placement(moe_ctx* c, const int32_t* placement) {
   MOE_TRY_CUDA(cudaDeviceSynchronize());  // no kernel may still read the old placement
   MOE_TRY_CUDA(cudaMemcpy(c->d_place, placement, E * sizeof(int32_t), cudaMemcpyHostToDevice));
   MOE_TRY_CUDA(cudaMemcpy(c->d_expert_at, inv.data(), E * sizeof(int32_t), cudaMemcpyHostToDevice));
+  return MOE_OK;
+}
+
+moe_status moe_migrate(moe_ctx* c, const int32_t* old_place, const int32_t* new_place,
+                       const void* src, void* dst, size_t bytes_per_expert, moe_stream s) {
+  MOE_REQUIRE(c && old_place && new_place && src && dst);
+  MOE_REQUIRE(bytes_per_expert > 0 && bytes_per_expert % 16 == 0 && c->E_l <= 256);
+  const int E = c->s.E, E_l = c->E_l, r = c->s.ep_rank;
+  std::vector<int> seen_o(E, 0), seen_n(E, 0);
+  for (int e = 0; e < E; ++e) {
+    if (old_place[e] < 0 || old_place[e] >= E || seen_o[old_place[e]]++) return MOE_ERR_INVALID_ARG;
+    if (new_place[e] < 0 || new_place[e] >= E || seen_n[new_place[e]]++) return MOE_ERR_INVALID_ARG;
+  }
+  if (!c->peers_ready) return MOE_ERR_NOT_READY;
+  const int64_t total = static_cast<int64_t>(E_l) * static_cast<int64_t>(bytes_per_expert);
+  if (!in_heap(c, src, total) || !in_heap(c, dst, total)) return MOE_ERR_NOT_SYMMETRIC;
+  const char* ps = static_cast<const char*>(src);
+  const char* pd = static_cast<const char*>(dst);
+  if (ps < pd + total && pd < ps + total) return MOE_ERR_INVALID_ARG;   // overlap
+  moe::MigrateList ml;
+  ml.n = 0;
+  for (int e = 0; e < E; ++e) {
+    if (old_place[e] / E_l != r) continue;   // this rank pushes the experts it holds now
+    ml.src_slot[ml.n] = static_cast<int16_t>(old_place[e] % E_l);
+    ml.dst_rank[ml.n] = static_cast<int16_t>(new_place[e] / E_l);
+    ml.dst_slot[ml.n] = static_cast<int16_t>(new_place[e] % E_l);
+    ++ml.n;
+  }
+  if (set_device(c) != MOE_OK) return MOE_ERR_CUDA;
+  CommArgs a = comm_args(c);
+  return cuda_status(moe::launch_migrate(a, ml, src, heap_off(c, dst),
+                                         static_cast<int64_t>(bytes_per_expert), st(s)));
+}
+
+moe_status moe_load_imbalance(const int64_t* loads, const int32_t* placement, int32_t E,
+                              int32_t ep, double* out) {
+  MOE_REQUIRE(loads && placement && out && E > 0 && ep > 0 && E % ep == 0);
+  const int E_l = E / ep;
+  std::vector<int64_t> s(ep, 0);
+  int64_t tot = 0;
+  for (int e = 0; e < E; ++e) {
+    if (placement[e] < 0 || placement[e] >= E || loads[e] < 0) return MOE_ERR_INVALID_ARG;
+    s[placement[e] / E_l] += loads[e];
+    tot += loads[e];
+  }
+  int64_t mx = 0;
+  for (int q = 0; q < ep; ++q) mx = s[q] > mx ? s[q] : mx;
+  *out = tot == 0 ? 1.0 : static_cast<double>(mx) * ep / static_cast<double>(tot);
   return MOE_OK;
 }
 
@@ -437,8 +505,6 @@ moe_status moe_ctx_destroy(moe_ctx* c) {
   cudaFree(c->heap);
   cudaFree(c->d_err);
   cudaFree(c->d_done);
-  cudaFree(c->d_sk_ws);
-  cudaFree(c->d_sk_flags);
   cudaFree(c->d_scratch);
   cudaFree(c->d_dedup_scratch);
   cudaFree(c->d_rows_T);
@@ -557,7 +623,7 @@ moe_status moe_dispatch_range(moe_ctx* c, const moe_bf16* xs, const int32_t* cou
   MOE_REQUIRE(c && xs && layout && xr && (counts || slot_begin > 0));
   MOE_REQUIRE(slot_begin >= 0 && slot_begin < slot_end && slot_end <= c->E_l);
   if (!c->peers_ready) return MOE_ERR_NOT_READY;
-  if (!in_heap(c, xr)) return MOE_ERR_NOT_SYMMETRIC;
+  if (!in_heap(c, xr, recv_bytes(c))) return MOE_ERR_NOT_SYMMETRIC;
   CommArgs a = comm_args(c);
   const int64_t dst_off = reinterpret_cast<const char*>(xr) - c->heap;
   return cuda_status(moe::launch_dispatch(a, counts, layout, c->recv_rows, xs, dst_off, xr,
@@ -574,7 +640,7 @@ moe_status moe_dispatch_bwd(moe_ctx* c, const moe_bf16* dxr, const int32_t* layo
                             moe_stream s) {
   MOE_REQUIRE(c && dxr && layout && dxs);
   if (!c->peers_ready) return MOE_ERR_NOT_READY;
-  if (!in_heap(c, dxs)) return MOE_ERR_NOT_SYMMETRIC;
+  if (!in_heap(c, dxs, send_bytes(c))) return MOE_ERR_NOT_SYMMETRIC;
   CommArgs a = comm_args(c);
   const int64_t dst_off = reinterpret_cast<const char*>(dxs) - c->heap;
   return cuda_status(moe::launch_reverse_transfer(a, layout, dxr, dst_off, st(s)));
@@ -607,9 +673,7 @@ moe_status ffn_up(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows, int
   g1.group_rows = group_rows; g1.n_groups = n_groups; g1.group_begin = g0; g1.rows_cap = rows_cap;
   g1.pair = gemm_pair();
   g1.max_ctas = c->gemm_sms;
-  g1.n_fastest = raster_n_fastest();
   g1.out = g_u_h; g1.ld_out = 3 * static_cast<int64_t>(f); g1.f = f;
-  use_stream_k(c, g1);
   return cuda_status(moe::launch_grouped_gemm(g1, st(s)));
 }
 
@@ -631,9 +695,7 @@ moe_status ffn_down(moe_ctx* c, const int32_t* group_rows, int32_t n_groups, int
   g2.group_rows = group_rows; g2.n_groups = n_groups; g2.rows_cap = rows_cap;
   g2.pair = gemm_pair();
   g2.max_ctas = c->gemm_sms;
-  g2.n_fastest = raster_n_fastest();
   g2.out = out ? static_cast<void*>(out) : static_cast<void*>(g_u_h); g2.ld_out = d;
-  use_stream_k(c, g2);
   if (sc) {
     g2.scatter = 1; g2.scatter_off = sc->off; g2.scatter_layout = sc->layout; g2.comm = sc->comm;
   }
@@ -677,9 +739,7 @@ moe_status ffn_bwd_dh(moe_ctx* c, const int32_t* group_rows, int32_t g0, int32_t
   a.group_rows = group_rows; a.n_groups = n_groups; a.group_begin = g0; a.rows_cap = rows_cap;
   a.pair = gemm_pair();
   a.max_ctas = c->gemm_sms;
-  a.n_fastest = raster_n_fastest();
   a.out = dgu; a.ld_out = 2 * F; a.aux = g_u_h; a.ld_aux = 3 * F; a.f = f;
-  use_stream_k(c, a);
   return cuda_status(moe::launch_grouped_gemm(a, st(s)));
 }
 
@@ -710,9 +770,7 @@ moe_status ffn_bwd_dx(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows,
   b.group_rows = group_rows; b.n_groups = n_groups; b.rows_cap = rows_cap;
   b.pair = gemm_pair();
   b.max_ctas = c->gemm_sms;
-  b.n_fastest = raster_n_fastest();
   b.out = dxr ? static_cast<void*>(dxr) : const_cast<moe_bf16*>(dgu); b.ld_out = d;
-  use_stream_k(c, b);
   if (sc) {  // dX rows go straight back to their source ranks (dispatch_bwd fused)
     b.scatter = 1; b.scatter_off = sc->off; b.scatter_layout = sc->layout; b.comm = sc->comm;
   }
@@ -784,7 +842,7 @@ moe_status moe_expert_ffn_down_combine(moe_ctx* c, const int32_t* layout, const 
                                        moe_bf16* y, moe_stream s) {
   MOE_REQUIRE(c && layout && w_down && g_u_h && ys && gates && dest_row && y);
   if (!c->peers_ready) return MOE_ERR_NOT_READY;
-  if (!in_heap(c, ys)) return MOE_ERR_NOT_SYMMETRIC;
+  if (!in_heap(c, ys, send_bytes(c))) return MOE_ERR_NOT_SYMMETRIC;
   CommArgs a = comm_args(c);
   const Scatter sc{&a, reinterpret_cast<const char*>(ys) - c->heap, layout};
   const int32_t* expert_rows = layout + static_cast<int64_t>(c->s.ep_size) * c->s.E;
@@ -802,7 +860,7 @@ moe_status moe_expert_ffn_combine(moe_ctx* c, const moe_bf16* xr, const int32_t*
                                   const moe_bf16* y_extra, moe_bf16* y, moe_stream s) {
   MOE_REQUIRE(c && xr && layout && w_gu && w_down && g_u_h && ys && gates && dest_row && y);
   if (!c->peers_ready) return MOE_ERR_NOT_READY;
-  if (!in_heap(c, ys)) return MOE_ERR_NOT_SYMMETRIC;
+  if (!in_heap(c, ys, send_bytes(c))) return MOE_ERR_NOT_SYMMETRIC;
   moe_status r = moe_expert_ffn_up(c, xr, layout, 0, c->E_l, w_gu, g_u_h, s);
   if (r != MOE_OK) return r;
   return moe_expert_ffn_down_combine(c, layout, w_down, g_u_h, ys, gates, dest_row, y_extra, y, s);
@@ -825,7 +883,7 @@ moe_status moe_expert_ffn_bwd_dx_dispatch(moe_ctx* c, const moe_bf16* xr, const 
                                           moe_stream s) {
   MOE_REQUIRE(c && xr && layout && w_gu && g_u_h && dout && dgu && dxs && dw_gu && dw_down);
   if (!c->peers_ready) return MOE_ERR_NOT_READY;
-  if (!in_heap(c, dxs)) return MOE_ERR_NOT_SYMMETRIC;
+  if (!in_heap(c, dxs, send_bytes(c))) return MOE_ERR_NOT_SYMMETRIC;
   CommArgs a = comm_args(c);
   const Scatter sc{&a, reinterpret_cast<const char*>(dxs) - c->heap, layout};
   const int32_t* expert_rows = layout + static_cast<int64_t>(c->s.ep_size) * c->s.E;
@@ -843,7 +901,7 @@ moe_status moe_expert_ffn_bwd_dispatch(moe_ctx* c, const moe_bf16* xr, const int
                                        moe_stream s) {
   MOE_REQUIRE(c && xr && layout && w_gu && w_down && g_u_h && dout && dgu && dxs && dw_gu && dw_down);
   if (!c->peers_ready) return MOE_ERR_NOT_READY;
-  if (!in_heap(c, dxs)) return MOE_ERR_NOT_SYMMETRIC;
+  if (!in_heap(c, dxs, send_bytes(c))) return MOE_ERR_NOT_SYMMETRIC;
   moe_status r = moe_expert_ffn_bwd_dh(c, layout, 0, c->E_l, w_down, g_u_h, dout, dgu, s);
   if (r != MOE_OK) return r;
   return moe_expert_ffn_bwd_dx_dispatch(c, xr, layout, w_gu, g_u_h, dout, dgu, dxs, dw_gu, dw_down,
@@ -856,7 +914,7 @@ moe_status moe_combine(moe_ctx* c, const moe_bf16* out, const int32_t* layout, m
                        moe_bf16* y, moe_stream s) {
   MOE_REQUIRE(c && out && layout && ys && gates && dest_row && y);
   if (!c->peers_ready) return MOE_ERR_NOT_READY;
-  if (!in_heap(c, ys)) return MOE_ERR_NOT_SYMMETRIC;
+  if (!in_heap(c, ys, send_bytes(c))) return MOE_ERR_NOT_SYMMETRIC;
   CommArgs a = comm_args(c);
   const int64_t dst_off = reinterpret_cast<const char*>(ys) - c->heap;
   MOE_TRY_CUDA(moe::launch_reverse_transfer(a, layout, out, dst_off, st(s)));
@@ -871,7 +929,7 @@ moe_status moe_combine_bwd_range(moe_ctx* c, const moe_bf16* dy, const float* ga
   MOE_REQUIRE(c && dy && gates && dest_row && ys && layout && dgates && dout_r);
   MOE_REQUIRE(slot_begin >= 0 && slot_begin < slot_end && slot_end <= c->E_l);
   if (!c->peers_ready) return MOE_ERR_NOT_READY;
-  if (!in_heap(c, dout_r)) return MOE_ERR_NOT_SYMMETRIC;
+  if (!in_heap(c, dout_r, recv_bytes(c))) return MOE_ERR_NOT_SYMMETRIC;
   CommArgs a = comm_args(c);
   const int64_t dst_off = reinterpret_cast<const char*>(dout_r) - c->heap;
   return cuda_status(moe::launch_combine_bwd_transfer(a, const_cast<int32_t*>(layout), dst_off,
@@ -891,9 +949,8 @@ moe_status moe_combine_bwd(moe_ctx* c, const moe_bf16* dy, const float* gates, c
 // ---------------------------------------------------------------- NEXT-4 dedup all-to-all
 // Reading R18 (oracle/dedup.py): one row per (token, owner) pair crosses NVLink.
 namespace {
-int64_t heap_off(const moe_ctx* c, const void* p) {
-  return reinterpret_cast<const char*>(p) - c->heap;
-}
+int64_t tok_rows(const moe_ctx* c) { return moe_dedup_token_rows_max(&c->s); }
+int64_t pair_rows(const moe_ctx* c) { return moe_dedup_pair_rows_max(&c->s); }
 }  // namespace
 
 moe_status moe_dedup_pairs(moe_ctx* c, const int32_t* topk_idx, const int32_t* dest_row,
@@ -912,7 +969,9 @@ moe_status moe_dedup_dispatch(moe_ctx* c, const moe_bf16* x, const int32_t* coun
   MOE_REQUIRE(c && x && counts && ntok && pdest && dest_row && topk_idx && gates && layout &&
               dlayout && xt && rlist && glist && xr);
   if (!c->peers_ready) return MOE_ERR_NOT_READY;
-  if (!in_heap(c, xt) || !in_heap(c, rlist) || !in_heap(c, glist)) return MOE_ERR_NOT_SYMMETRIC;
+  if (!in_heap(c, xt, tok_rows(c) * row_bytes(c)) || !in_heap(c, rlist, tok_rows(c) * c->s.k * 4) ||
+      !in_heap(c, glist, tok_rows(c) * c->s.k * 4))
+    return MOE_ERR_NOT_SYMMETRIC;
   CommArgs a = comm_args(c);
   MOE_TRY_CUDA(moe::launch_dedup_forward(a, 0, layout, dlayout, counts, ntok, c->recv_rows, x,
                                          pdest, dest_row, topk_idx, gates, heap_off(c, xt),
@@ -927,7 +986,7 @@ moe_status moe_dedup_combine(moe_ctx* c, const moe_bf16* out, const int32_t* dla
                              const moe_bf16* y_extra, moe_bf16* part, moe_bf16* y, moe_stream s) {
   MOE_REQUIRE(c && out && dlayout && rlist && glist && pdest && part && y);
   if (!c->peers_ready) return MOE_ERR_NOT_READY;
-  if (!in_heap(c, part)) return MOE_ERR_NOT_SYMMETRIC;
+  if (!in_heap(c, part, pair_rows(c) * row_bytes(c))) return MOE_ERR_NOT_SYMMETRIC;
   CommArgs a = comm_args(c);
   MOE_TRY_CUDA(moe::launch_dedup_reduce(a, 0, dlayout, rlist, glist, out, nullptr,
                                         heap_off(c, part), 0, st(s)));
@@ -943,7 +1002,7 @@ moe_status moe_dedup_combine_bwd(moe_ctx* c, const moe_bf16* dy, const int32_t* 
   MOE_REQUIRE(c && dy && pdest && layout && dlayout && rlist && glist && out && dyt && dg_own &&
               dout_r);
   if (!c->peers_ready) return MOE_ERR_NOT_READY;
-  if (!in_heap(c, dyt)) return MOE_ERR_NOT_SYMMETRIC;
+  if (!in_heap(c, dyt, tok_rows(c) * row_bytes(c))) return MOE_ERR_NOT_SYMMETRIC;
   CommArgs a = comm_args(c);
   MOE_TRY_CUDA(moe::launch_dedup_forward(a, 1, const_cast<int32_t*>(layout),
                                          const_cast<int32_t*>(dlayout), nullptr, nullptr, 0, dy,
@@ -962,7 +1021,7 @@ moe_status moe_dedup_combine_bwd_ys(moe_ctx* c, const moe_bf16* dy, const float*
   MOE_REQUIRE(c && dy && gates && dest_row && ys && pdest && layout && dlayout && rlist && glist &&
               dyt && dgates && dout_r);
   if (!c->peers_ready) return MOE_ERR_NOT_READY;
-  if (!in_heap(c, dyt)) return MOE_ERR_NOT_SYMMETRIC;
+  if (!in_heap(c, dyt, tok_rows(c) * row_bytes(c))) return MOE_ERR_NOT_SYMMETRIC;
   CommArgs a = comm_args(c);
   MOE_TRY_CUDA(moe::launch_dedup_forward(a, 1, const_cast<int32_t*>(layout),
                                          const_cast<int32_t*>(dlayout), nullptr, nullptr, 0, dy,
@@ -979,7 +1038,9 @@ moe_status moe_dedup_dispatch_bwd(moe_ctx* c, const moe_bf16* dxr, const int32_t
   MOE_REQUIRE(c && dxr && dlayout && rlist && dg_own && pdest && dest_row && topk_idx && dxpart &&
               dgpart && dgates);
   if (!c->peers_ready) return MOE_ERR_NOT_READY;
-  if (!in_heap(c, dxpart) || !in_heap(c, dgpart)) return MOE_ERR_NOT_SYMMETRIC;
+  if (!in_heap(c, dxpart, pair_rows(c) * row_bytes(c)) ||
+      !in_heap(c, dgpart, pair_rows(c) * c->s.k * 4))
+    return MOE_ERR_NOT_SYMMETRIC;
   CommArgs a = comm_args(c);
   MOE_TRY_CUDA(moe::launch_dedup_reduce(a, 1, dlayout, rlist, nullptr, dxr, dg_own,
                                         heap_off(c, dxpart), heap_off(c, dgpart), st(s)));

@@ -756,6 +756,48 @@ __global__ void wait_flags_kernel(CommArgs a, int slot) {
   commit_epoch(a);
 }
 
+// NEXT-2 expert migration (reading R17): every expert whose slot changes is
+// pushed by its OLD owner from its local src slot into the NEW owner's dst slot (symmetric
+// buffers at the same heap offset on every rank; local slot moves are local stores).
+// Protocol: the first block (ticket) announces this rank on the counts slot and every block
+// waits until every peer has announced, so no peer can still be reading its dst from earlier
+// stream work; then the copies; then the usual data-slot completion (the last block waits for
+// every peer's stores to have landed here).  Work item = one 2 KB part of one 16-byte-vector
+// "row" of kMigRowVec vectors of an expert.
+constexpr int kMigRowVec = 128;
+__global__ void migrate_kernel(CommArgs a, MigrateList ml, const uint16_t* __restrict__ src,
+                               int64_t dst_off, int64_t bytes_per_expert) {
+  pdl_wait();
+  pdl_trigger();
+  a.epoch = load_epoch(a);
+  {
+    __shared__ int s_first;
+    if (threadIdx.x == 0) s_first = (atomicAdd(a.done + 1, 1) == 0);
+    __syncthreads();
+    if (s_first && threadIdx.x < a.ep)
+      st_release_sys(peer_flag(a, threadIdx.x, kSlotCounts, a.rank), a.epoch);
+    wait_all(a, kSlotCounts);
+  }
+  const int lane = threadIdx.x & 31;
+  const int64_t gwarp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int64_t nvec_e = bytes_per_expert / 16;
+  const int64_t rows_e = (nvec_e + kMigRowVec - 1) / kMigRowVec;
+  const int64_t n_items = static_cast<int64_t>(ml.n) * rows_e;
+  for (int64_t w = gwarp; w < n_items; w += nwarps) {
+    const int m = static_cast<int>(w / rows_e);
+    const int64_t row = w - static_cast<int64_t>(m) * rows_e;
+    const int64_t v0 = row * kMigRowVec;
+    const int64_t nv = (nvec_e - v0) < kMigRowVec ? (nvec_e - v0) : kMigRowVec;
+    const uint4* ps = reinterpret_cast<const uint4*>(
+        reinterpret_cast<const char*>(src) + ml.src_slot[m] * bytes_per_expert) + v0;
+    uint4* pd = reinterpret_cast<uint4*>(a.peers.base[ml.dst_rank[m]] + dst_off +
+                                         ml.dst_slot[m] * bytes_per_expert) + v0;
+    copy_part(pd, ps, static_cast<int>(nv), 0, lane);
+  }
+  signal_done(a, kSlotData, /*wait_after=*/true);
+}
+
 // Up to 2 blocks of 512 threads per SM (all co-resident: blocks spin on peer flags), and no
 // more than one block per 32 work items (2 KB row parts): small messages are latency-bound,
 // and every extra block adds to the launch and to the last-block count.
@@ -811,6 +853,17 @@ cudaError_t launch_reverse_transfer(const CommArgs& a, const int32_t* layout, co
   // receive rows <= EP * T * k
   launch_k(reverse_transfer_kernel, dim3(transfer_blocks(a, a.T * a.k * a.ep)), dim3(512),
       transfer_smem(a), s, a, layout, src, dst_off);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_migrate(const CommArgs& a, const MigrateList& ml, const void* src,
+                           int64_t dst_off, int64_t bytes_per_expert, cudaStream_t s) {
+  const int64_t rows = static_cast<int64_t>(ml.n) * ((bytes_per_expert / 16 + kMigRowVec - 1) / kMigRowVec);
+  int64_t b = a.blocks > 0 ? a.blocks : 2 * num_sms();
+  const int64_t need = (rows + 31) / 32;
+  if (need < b) b = need;
+  launch_k(migrate_kernel, dim3(static_cast<unsigned>(b < 1 ? 1 : b)), dim3(512), 0, s, a, ml,
+           static_cast<const uint16_t*>(src), dst_off, bytes_per_expert);
   return cudaGetLastError();
 }
 

@@ -36,6 +36,7 @@ constexpr int kBK = 64;  // 64 bf16 = 128 bytes = one 128B-swizzle atom row
 constexpr int kThreads = 256;
 constexpr int kMaxGroups = 256;
 constexpr int kStageBox = 4096;  // per-epilogue-warp staging: 32 rows x 128 bytes
+constexpr int kMaxDevices = 64;
 
 struct KParams {
   int M, N, K;
@@ -61,92 +62,7 @@ struct KParams {
   int64_t scatter_off;
   const int32_t* scatter_layout;
   CommArgs comm;
-  // stream-K tail (M-grouped epilogues): the last partial wave's tiles (+ one full wave) are
-  // split along K over every cluster; partial accumulators go through sk_ws [clusters][TILE_M x
-  // BN] fp32, sk_flags [2][kMaxClusters] (ready, consumed) counters
-  int stream_k;
-  int sk_slots;         // workspace slots available for this launch's tile size
-  float* sk_ws;
-  int* sk_flags;
 };
-
-constexpr int kMaxClusters = 160;
-constexpr int kMaxSkSlots = kStreamKSlots;   // partial pieces per launch (internal.h)
-
-// ---------------------------------------------------------------- persistent work schedule
-// Every role (producer, MMA, epilogue) walks the same sequence: this cluster's data-parallel
-// tiles c, c+nc, ... < dp_tiles, then its stream-K pieces.  Only the last, partial wave (rem
-// tiles) is split: each tail tile is cut into S equal k-chunks, piece p = j*rem + u (chunk j
-// of tail tile u) goes to cluster p % nc, and a cluster takes its pieces in increasing p.
-// Chunk-major order keeps the L2 sharing of the data-parallel raster (concurrent pieces
-// cover the same k-range of neighbouring tiles).  Pieces of chunks j < S-1 are PARTIAL: they
-// write their fp32 accumulator to workspace slot p; the chunk-(S-1) piece FINISHES its tile:
-// it adds the S-1 partials in chunk order (deterministic), then runs the normal epilogue.
-// A cluster's finishing pieces come after all of its partial pieces (p grows with j), so a
-// partial producer never waits and the wait graph has no cycle.  S in {2,3,4} minimises
-// ceil(S*rem/nc)/S (the tail's length in tiles); no split when that is not below 1.
-// tests/test_streamk_schedule.py mirrors this schedule and checks its invariants.
-enum { kWorkFull = 0, kWorkPartial = 1, kWorkFinish = 2 };
-struct Sched {
-  int nc, c, nkb, dp_tiles, n_dp, rem, S, n_sk;
-};
-struct Work {
-  int t, kb0, kb1, kind, u, j;   // stream-K pieces: tail tile u, k-chunk j (slot j*rem + u)
-};
-
-__device__ __forceinline__ Sched make_sched(int total_tiles, int nkb, bool enable, int c, int nc,
-                                            int max_slots) {
-  Sched s;
-  s.nc = nc;
-  s.c = c;
-  s.nkb = nkb;
-  s.rem = 0;
-  s.S = 1;
-  if (enable && nc <= kMaxClusters) {
-    const int rem = total_tiles % nc;
-    int best_S = 1, best_num = 1, best_den = 1;   // tail length ceil(S*rem/nc)/S, as a fraction
-    for (int S = 2; S <= 4 && rem > 0; ++S) {
-      const int rounds = (S * rem + nc - 1) / nc;
-      if (nkb / S >= 4 && (S - 1) * rem <= max_slots && rounds * best_den < best_num * S) {
-        best_S = S;
-        best_num = rounds;
-        best_den = S;
-      }
-    }
-    if (best_S > 1) {
-      s.rem = rem;
-      s.S = best_S;
-    }
-  }
-  s.dp_tiles = total_tiles - s.rem;
-  s.n_dp = s.dp_tiles > c ? (s.dp_tiles - 1 - c) / nc + 1 : 0;
-  const int pieces = s.S * s.rem;
-  s.n_sk = (s.S > 1 && pieces > c) ? (pieces - 1 - c) / nc + 1 : 0;
-  return s;
-}
-
-// w in [0, n_dp + n_sk); kb1 < 0 means "the tile's own k-block count"
-__device__ __forceinline__ Work get_work(const Sched& s, int w) {
-  Work wk;
-  wk.u = 0;
-  wk.j = 0;
-  if (w < s.n_dp) {
-    wk.t = s.c + w * s.nc;
-    wk.kb0 = 0;
-    wk.kb1 = -1;
-    wk.kind = kWorkFull;
-    return wk;
-  }
-  const int p = s.c + (w - s.n_dp) * s.nc;
-  const int j = p / s.rem;
-  wk.j = j;
-  wk.u = p - j * s.rem;
-  wk.t = s.dp_tiles + wk.u;
-  wk.kb0 = j * s.nkb / s.S;
-  wk.kb1 = (j + 1) * s.nkb / s.S;
-  wk.kind = (j < s.S - 1) ? kWorkPartial : kWorkFinish;
-  return wk;
-}
 
 // STG = staging boxes per epilogue warp.  2 double-buffers the fp32 wgrad epilogue (its K is
 // one expert's rows, so a tile's MMAs are short), at the price of one ring stage.  Measured
@@ -358,9 +274,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int total_tiles = s_tile_prefix[n_groups];
-  const Sched sch = make_sched(total_tiles, KGROUPED ? 0 : p.K / kBK, !KGROUPED && p.stream_k,
-                               tile0, tile_step, p.sk_slots);
-  const int n_work = sch.n_dp + sch.n_sk;
+  // persistent schedule: cluster c takes tiles c, c + nc, c + 2 nc, ... (raster order of
+  // decode_tile), every role walks the same sequence
+  const int n_work = total_tiles > tile0 ? (total_tiles - 1 - tile0) / tile_step + 1 : 0;
 
   if (warp == 0) {
     // ===================== TMA producer =====================
@@ -368,10 +284,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int w = 0; w < n_work; ++w) {
-        const Work wk = get_work(sch, w);
-        Tile tl = decode_tile<KGROUPED, BN, TILE_M>(wk.t, s_tile_prefix, s_seg, s_rows, n_groups, p);
-        const int kb1 = wk.kb1 < 0 ? tl.nkb : wk.kb1;
-        for (int kb = wk.kb0; kb < kb1; ++kb) {
+        const Tile tl = decode_tile<KGROUPED, BN, TILE_M>(tile0 + w * tile_step, s_tile_prefix,
+                                                          s_seg, s_rows, n_groups, p);
+        for (int kb = 0; kb < tl.nkb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint32_t bar_addr = smem_u32(&full[stage]);
           if (PAIR == 2) {
@@ -428,13 +343,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int w = 0; w < n_work; ++w) {
-        const Work wk = get_work(sch, w);
-        Tile tl = decode_tile<KGROUPED, BN, TILE_M>(wk.t, s_tile_prefix, s_seg, s_rows, n_groups, p);
-        const int kb1 = wk.kb1 < 0 ? tl.nkb : wk.kb1;
+        const Tile tl = decode_tile<KGROUPED, BN, TILE_M>(tile0 + w * tile_step, s_tile_prefix,
+                                                          s_seg, s_rows, n_groups, p);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * C::ACC_STRIDE;
-        for (int kb = wk.kb0; kb < kb1; ++kb) {
+        for (int kb = 0; kb < tl.nkb; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a_base = smem_u32(sA + stage * C::A_BYTES);
@@ -445,7 +359,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                         : sdesc_sw128(a_base + kk * 32, 16, 1024);
             const uint64_t bdesc = B_MN ? sdesc_sw128(b_base + kk * 2048, 8192, 1024)
                                         : sdesc_sw128(b_base + kk * 32, 16, 1024);
-            const uint32_t accum = (kb != wk.kb0 || kk != 0) ? 1u : 0u;
+            const uint32_t accum = (kb != 0 || kk != 0) ? 1u : 0u;
             if (PAIR == 2) umma_bf16_pair(d_tmem, adesc, bdesc, IDESC, accum);
             else umma_bf16(d_tmem, adesc, bdesc, IDESC, accum);
           }
@@ -454,7 +368,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           else umma_commit(&empty[stage]);
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
-        if (kb1 > wk.kb0) {
+        if (tl.nkb > 0) {
           if (PAIR == 2) umma_commit_pair(&tfull[acc], 0x3);
           else umma_commit(&tfull[acc]);
         } else {
@@ -473,11 +387,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     constexpr int kArrive = 4 * PAIR;  // epilogue warps of a cluster
-    int* sk_ready = p.sk_flags;
-    int* sk_consumed = p.sk_flags + kMaxSkSlots;
     for (int w = 0; w < n_work; ++w) {
-      const Work wk = get_work(sch, w);
-      Tile tl = decode_tile<KGROUPED, BN, TILE_M>(wk.t, s_tile_prefix, s_seg, s_rows, n_groups, p);
+      const Tile tl = decode_tile<KGROUPED, BN, TILE_M>(tile0 + w * tile_step, s_tile_prefix,
+                                                        s_seg, s_rows, n_groups, p);
       const int m_box = tl.m * TILE_M + static_cast<int>(rank) * kBM + ew * 32;  // warp's 1st row
       const int mi = m_box + lane;  // row of this thread inside its group
       const bool valid = KGROUPED ? true : (mi < tl.rows_g);
@@ -486,7 +398,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // the next group and are not written here (whole 32-row boxes, segments are 128-aligned).
       const bool box_in = KGROUPED || m_box < ((tl.rows_g + kBM - 1) / kBM) * kBM;
       const int64_t grow = static_cast<int64_t>(tl.seg) + mi;
-      if (EPI == kEpiDSwiGLU && wk.kind != kWorkPartial && valid && grow < p.rows_cap) {
+      if (EPI == kEpiDSwiGLU && valid && grow < p.rows_cap) {
         // warm L2 with this row's saved G and U segments while the MMAs run
         const uint16_t* a = reinterpret_cast<const uint16_t*>(p.aux) + grow * p.ld_aux + tl.n * BN;
         prefetch_l2_bulk(a, BN * 2);
@@ -496,75 +408,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const uint32_t tacc =
           tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * C::ACC_STRIDE;
-      // workspace row of this thread: [cluster slot][rank * 128 + ew * 32 + lane][BN]
-      const size_t ws_row = static_cast<size_t>(rank * kBM + ew * 32 + lane) * BN;
-      if (wk.kind == kWorkPartial) {
-        // stream-K partial: this piece's fp32 accumulator -> workspace slot j*rem + u, then signal
-        const int slot = wk.j * sch.rem + wk.u;
-        if (box_in) {
-          float4* dst = reinterpret_cast<float4*>(p.sk_ws + static_cast<size_t>(slot) * TILE_M * BN + ws_row);
-#pragma unroll 1
-          for (int c0 = 0; c0 < BN; c0 += 32) {
-            uint32_t a[32];
-            tmem_ld32(tacc + c0, a);
-            tmem_ld_wait();
-#pragma unroll
-            for (int v = 0; v < 8; ++v)
-              __stcg(dst + c0 / 4 + v, make_float4(__uint_as_float(a[4 * v]), __uint_as_float(a[4 * v + 1]),
-                                                   __uint_as_float(a[4 * v + 2]), __uint_as_float(a[4 * v + 3])));
-          }
-        }
-        __threadfence();
-        __syncwarp();
-        if (lane == 0) atomicAdd(sk_ready + slot, 1);
-      } else {
-      if (wk.kind == kWorkFinish) {
-        // stream-K finisher: add the partials of chunks 0 .. S-2 of this tile (slots j*rem + u,
-        // in chunk order) into this accumulator in TMEM, then run the normal epilogue
-        if (lane == 0) {
-          const uint64_t t_start = globaltimer_ns();
-          for (int j = 0; j + 1 < sch.S; ++j)
-            while (ld_acquire_gpu(sk_ready + j * sch.rem + wk.u) < kArrive) {
-              __nanosleep(32);
-              if (globaltimer_ns() - t_start > 10ull * 1000 * 1000 * 1000) __trap();  // never hang
-            }
-        }
-        __syncwarp();
-        if (box_in) {
-#pragma unroll 1
-          for (int c0 = 0; c0 < BN; c0 += 32) {
-            uint32_t a[32];
-            tmem_ld32(tacc + c0, a);
-            tmem_ld_wait();
-            for (int j = 0; j + 1 < sch.S; ++j) {
-              const float4* src = reinterpret_cast<const float4*>(
-                  p.sk_ws + static_cast<size_t>(j * sch.rem + wk.u) * TILE_M * BN + ws_row) + c0 / 4;
-#pragma unroll
-              for (int v = 0; v < 8; ++v) {
-                const float4 x = __ldcg(src + v);
-                a[4 * v] = __float_as_uint(__uint_as_float(a[4 * v]) + x.x);
-                a[4 * v + 1] = __float_as_uint(__uint_as_float(a[4 * v + 1]) + x.y);
-                a[4 * v + 2] = __float_as_uint(__uint_as_float(a[4 * v + 2]) + x.z);
-                a[4 * v + 3] = __float_as_uint(__uint_as_float(a[4 * v + 3]) + x.w);
-              }
-            }
-            tmem_st32(tacc + c0, a);
-          }
-          tmem_st_wait();
-        }
-        __syncwarp();
-        if (lane == 0)
-          for (int j = 0; j + 1 < sch.S; ++j) {
-            const int slot = j * sch.rem + wk.u;
-            if (atomicAdd(sk_consumed + slot, 1) == kArrive - 1) {
-              // the last reader resets the slot's counters for the next launch
-              sk_consumed[slot] = 0;
-              sk_ready[slot] = 0;
-            }
-          }
-      }
       if (box_in) {
-
       if (EPI == kEpiSwiGLU) {
         // acc cols [0, BN/2) = G, [BN/2, BN) = U for f-columns n*BN/2 ...; write G, U, H
 #pragma unroll 1
@@ -764,7 +608,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       }  // box_in
-      }  // not a stream-K partial
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -910,10 +753,6 @@ cudaError_t launch_impl(const GemmProblem& g, cudaStream_t stream) {
   kp.f = g.f;
   kp.accumulate = g.accumulate;
   kp.scatter = g.scatter;
-  kp.stream_k = (EPI == kEpiSwiGLU || EPI == kEpiBF16 || EPI == kEpiDSwiGLU) && g.sk_ws &&
-                g.sk_flags && g.K / kBK > 1;
-  kp.sk_ws = g.sk_ws;
-  kp.sk_flags = g.sk_flags;
   if (g.scatter) {
     if (EPI != kEpiBF16 || !g.comm || !g.scatter_layout) return cudaErrorInvalidValue;
     kp.scatter_off = g.scatter_off;
@@ -921,19 +760,18 @@ cudaError_t launch_impl(const GemmProblem& g, cudaStream_t stream) {
     kp.comm = *g.comm;
   }
   auto kern = grouped_gemm_kernel<BN, A_MN, B_MN, EPI, PAIR>;
-  static bool attr_set = false;
-  if (!attr_set) {
+  // launch state is per device (a process may drive several GPUs, one ctx each)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+  static bool attr_set[kMaxDevices] = {};
+  if (!attr_set[dev]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr_set[dev] = true;
   }
-  // the stream-K workspace holds sk_slots TILE_M x BN fp32 partial accumulators
-  const int64_t slot_bytes = static_cast<int64_t>(kBM) * PAIR * BN * 4;
-  kp.sk_slots = static_cast<int>(std::min<int64_t>(g.sk_ws_bytes / slot_bytes, kMaxSkSlots));
-  if (kp.sk_slots < 1) kp.stream_k = 0;
   if (PAIR == 1) {
     const int grid = (g.max_ctas > 0 && g.max_ctas < num_sms()) ? g.max_ctas : num_sms();
-    if (grid > kMaxClusters) kp.stream_k = 0;
     return launch_k(kern, dim3(grid), dim3(kThreads), C::SMEM, stream, ta, tb, tc, kp);
   }
   cudaLaunchConfig_t cfg;
@@ -950,34 +788,35 @@ cudaError_t launch_impl(const GemmProblem& g, cudaStream_t stream) {
   cfg.numAttrs = 1;
   // Persistent grid = the number of CTA pairs that can be co-resident (not every SM can
   // pair: a launch of more clusters would run the excess as a second, serial wave).
-  static int max_clusters = 0;
-  if (max_clusters == 0) {
+  static int max_clusters[kMaxDevices] = {};
+  if (max_clusters[dev] == 0) {
     cfg.gridDim = dim3(num_sms() / 2 * 2);
     int n = 0;
     if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) n = num_sms() / 2;
-    max_clusters = n;
+    max_clusters[dev] = n;
     if (getenv("MOE_VERBOSE"))
       fprintf(stderr, "[libmoe] gemm<BN=%d,epi=%d> pair grid: %d co-resident clusters of 2\n", BN, EPI, n);
   }
-  int clusters = max_clusters;
+  int clusters = max_clusters[dev];
   if (g.max_ctas > 0 && g.max_ctas / 2 < clusters) clusters = g.max_ctas / 2 > 0 ? g.max_ctas / 2 : 1;
   cfg.gridDim = dim3(2 * clusters);
   cfg.numAttrs = 1 + pdl_attr(&attr[1]);
-  if (clusters > kMaxClusters) kp.stream_k = 0;
   return cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, kp);
 }
 
 }  // namespace
 
 int num_sms() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
+  static int n_of[kMaxDevices] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDevices) dev = 0;
+  if (n_of[dev] == 0) {
+    int n = 0;
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
+    n_of[dev] = n > 0 ? n : 148;
   }
-  return n;
+  return n_of[dev];
 }
 
 #define MOE_GEMM_CASE(BN_, AMN, BMN, EPI_)                                      \

@@ -86,15 +86,7 @@ struct GemmProblem {
   int64_t scatter_off = 0;
   const int32_t* scatter_layout = nullptr;  // counts_all [EP x E]
   const struct CommArgs* comm = nullptr;
-  // stream-K tail for the M-grouped epilogues (SwiGLU, BF16, DSwiGLU); null = off
-  float* sk_ws = nullptr;
-  int64_t sk_ws_bytes = 0;
-  int* sk_flags = nullptr;   // [2][kStreamKSlots] int32 (ready, consumed), zero between launches
 };
-// stream-K workspace: up to 336 partial accumulators of 128 x 256 fp32 (168 of 256 x 256):
-// a tail of rem < 3/4 of the clusters cut into <= 4 chunks has <= 3 rem partials
-constexpr int kStreamKSlots = 336;
-constexpr int64_t kStreamKWorkspaceBytes = static_cast<int64_t>(kStreamKSlots) * 128 * 256 * 4;
 
 cudaError_t launch_grouped_gemm(const GemmProblem& p, cudaStream_t stream);
 int num_sms();
@@ -218,6 +210,16 @@ cudaError_t launch_dedup_reduce(const CommArgs& a, int mode, const int32_t* dlay
                                 const int32_t* rlist, const float* glist, const uint16_t* rows,
                                 const float* dg_own, int64_t part_off, int64_t dgpart_off,
                                 cudaStream_t s);
+// NEXT-2 expert migration: moves of this rank's experts (old local slot -> new owner rank
+// and local slot); collective, see migrate_kernel
+struct MigrateList {
+  int n;
+  int16_t src_slot[256];
+  int16_t dst_rank[256];
+  int16_t dst_slot[256];
+};
+cudaError_t launch_migrate(const CommArgs& a, const MigrateList& ml, const void* src,
+                           int64_t dst_off, int64_t bytes_per_expert, cudaStream_t s);
 // 1-block wait for every rank's flag of a.epoch (after a GEMM with a fused scatter epilogue)
 cudaError_t launch_wait_flags(const CommArgs& a, int slot, cudaStream_t s);
 

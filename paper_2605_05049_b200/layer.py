@@ -49,7 +49,7 @@ def _all_gather_bytes(payload: bytes, group=None) -> bytes:
 
 class MoELayer:
     def __init__(self, dims: LayerDims, device: int = 0, group=None, fused: bool = True,
-                 dedup: bool = False):
+                 dedup: bool = False, migratable=None, expert_state_bytes: int = 0):
         """fused=True uses the compute+all-to-all entry points (moe_expert_ffn_combine,
         moe_expert_ffn_bwd_dispatch); False issues the step-by-step calls (same results).
         dedup (k > 1; NEXT-4, reading R18): one row per (token, owner) pair on NVLink.
@@ -58,8 +58,13 @@ class MoELayer:
               GEMM2 / dgrad-2 epilogues (hidden under the GEMMs); results bit-identical to the
               plain path.
           "all": also the reverse direction, as owner-side pair reductions (one extra bf16
-              rounding of y and dx)."""
+              rounding of y and dx).
+        migratable (default: EP > 1): the experts' weights and fp32 weight gradients live in
+            the symmetric heap, double-buffered, so migrate() can push them to their new owners
+            over the peer maps (moe_migrate); expert_state_bytes reserves heap room for more
+            per-expert state registered with expert_state() (e.g. optimizer moments)."""
         self.dims = dims
+        self.group = group
         self.fused = fused
         mode = "dispatch" if dedup is True else (dedup or None)
         if mode not in (None, "dispatch", "all"):
@@ -84,6 +89,12 @@ class MoELayer:
             self.tok_max = max(L.moe_dedup_token_rows_max(self.shape), 1)
             self.pair_max = max(L.moe_dedup_pair_rows_max(self.shape), 1)
             heap += self.tok_max * (d * 2 + 8 * k) + self.pair_max * 4 * k + 4 * 4096
+        self.migratable = dims.ep_size > 1 if migratable is None else bool(migratable)
+        f32b = 4
+        if self.migratable:
+            per_expert = 3 * d * f * (2 + f32b)            # bf16 weights + fp32 gradients
+            heap += 2 * (self.E_l * per_expert + 4 * 256)
+            heap += 2 * (self.E_l * int(expert_state_bytes)) + 64 * 1024
         self.ctx = L.Context(self.shape, device, heap)
         if dims.ep_size > 1:
             handles = _all_gather_bytes(self.ctx.export_handle(), group)
@@ -126,8 +137,21 @@ class MoELayer:
         self.dx_router = torch.empty((T, d), dtype=f32, device=dev)
         self.dx = torch.empty((T, d), dtype=bf, device=dev)
         self.dw_r = torch.empty((E, d), dtype=f32, device=dev)
-        self.dw_gu = torch.empty((self.E_l, 2 * f, d), dtype=f32, device=dev)
-        self.dw_down = torch.empty((self.E_l, d, f), dtype=f32, device=dev)
+        self._cur = 0       # which half of the double-buffered expert state is current
+        self._states = {}   # name -> [buf0, buf1] symmetric [E_l, ...] (migratable state)
+        if self.migratable:
+            sy = self.ctx.symm_empty
+            self._states["w_gu"] = [sy((self.E_l, 2 * f, d), bf) for _ in range(2)]
+            self._states["w_down"] = [sy((self.E_l, d, f), bf) for _ in range(2)]
+            self._states["dw_gu"] = [sy((self.E_l, 2 * f, d), f32) for _ in range(2)]
+            self._states["dw_down"] = [sy((self.E_l, d, f), f32) for _ in range(2)]
+            self.dw_gu = self._states["dw_gu"][0]
+            self.dw_down = self._states["dw_down"][0]
+        else:
+            self.dw_gu = torch.empty((self.E_l, 2 * f, d), dtype=f32, device=dev)
+            self.dw_down = torch.empty((self.E_l, d, f), dtype=f32, device=dev)
+        if dims.ep_size > 1:
+            self._verify_symmetric()
         self.rows_T = torch.tensor([T], dtype=i32, device=dev)
         self.fs = dims.E_shared * f
         if self.fs:
@@ -147,8 +171,14 @@ class MoELayer:
         bias [E] fp32 or None, shared w_gu_s [2fs,d], w_down_s [d,fs] or None."""
         dev = self.device
         self.w_r = w_r.to(dev, torch.bfloat16).contiguous()
-        self.w_gu = w_gu.to(dev, torch.bfloat16).contiguous()
-        self.w_down = w_down.to(dev, torch.bfloat16).contiguous()
+        if self.migratable:
+            self.w_gu = self._states["w_gu"][self._cur]
+            self.w_down = self._states["w_down"][self._cur]
+            self.w_gu.copy_(w_gu)
+            self.w_down.copy_(w_down)
+        else:
+            self.w_gu = w_gu.to(dev, torch.bfloat16).contiguous()
+            self.w_down = w_down.to(dev, torch.bfloat16).contiguous()
         self.bias = None if bias is None else bias.to(dev, torch.float32).contiguous()
         if self.fs:
             self.w_gu_s = w_gu_s.to(dev, torch.bfloat16).contiguous()
@@ -212,9 +242,6 @@ class MoELayer:
             return self._forward_dedup(x)
         L.moe_permute(c, x, self.topk_idx, self.counts, self.dest_row, self.xs)
         self._mark("F2 permute")
-        ranges = self._ranges()
-        if ranges:
-            return self._forward_chunked(x, ranges)
         y_extra = None
         if self.fs and self.overlap:
             # shared experts (local tokens, no exchange) run beside the dispatch all-to-all on
@@ -319,88 +346,6 @@ class MoELayer:
         self._mark("B3 dedup dispatch_bwd")
         return self._backward_tail(dy, accumulate, shared_done)
 
-    # ------------------------------------------------------------------ NEXT-1 chunked overlap
-    # Owner slots cut into `chunks` ranges: the all-to-all of range i+1 (side stream, comm_sms
-    # SMs) runs beside the first expert GEMM of range i (this stream, the other SMs).  Used by
-    # the fused path when EP > 1 and E_l > 1; chunks = 1 turns it off.
-    chunks = 1
-
-    def _ranges(self):
-        E_l, n = self.E_l, min(self.chunks, self.E_l)
-        if not self.fused or self.dedup or self.dims.ep_size == 1 or n < 2:
-            return None
-        bounds = [E_l * i // n for i in range(n + 1)]
-        return list(zip(bounds[:-1], bounds[1:]))
-
-    def _forward_chunked(self, x, ranges):
-        c, T = self.ctx, self.dims.T_local
-        b0, e0 = ranges[0]
-        y_extra = None
-        if self.fs and self.overlap:
-            self._concurrent(lambda s: L.moe_dispatch_range(c, self.xs, self.counts, self.layout,
-                                                            self.xr, b0, e0, stream=s),
-                             lambda s: L.moe_expert_ffn(c, x, self.rows_T, 1, T, self.fs,
-                                                        self.w_gu_s, self.w_down_s, self.g_u_h_s,
-                                                        self.y_s, stream=s))
-            y_extra = self.y_s
-        else:
-            L.moe_dispatch_range(c, self.xs, self.counts, self.layout, self.xr, b0, e0)
-            if self.fs:
-                L.moe_expert_ffn(c, x, self.rows_T, 1, T, self.fs, self.w_gu_s, self.w_down_s,
-                                 self.g_u_h_s, self.y_s)
-                y_extra = self.y_s
-        self._mark("F3 dispatch (range 0)")
-        for (pb, pe), (b, e) in zip(ranges[:-1], ranges[1:]):
-            self._concurrent(
-                lambda s, b=b, e=e: L.moe_dispatch_range(c, self.xs, None, self.layout, self.xr,
-                                                         b, e, stream=s),
-                lambda s, pb=pb, pe=pe: L.moe_expert_ffn_up(c, self.xr, self.layout, pb, pe,
-                                                            self.w_gu, self.g_u_h, stream=s))
-        L.moe_expert_ffn_up(c, self.xr, self.layout, ranges[-1][0], ranges[-1][1], self.w_gu,
-                            self.g_u_h)
-        self._mark("F3 dispatch || F4 GEMM1 (chunked)")
-        L.moe_expert_ffn_down_combine(c, self.layout, self.w_down, self.g_u_h, self.ys, self.gates,
-                                      self.dest_row, y_extra, self.y)
-        self._mark("F4 GEMM2 + F5 combine + F6")
-        return self.y
-
-    def _backward_chunked(self, dy, accumulate, ranges):
-        c, T = self.ctx, self.dims.T_local
-        b0, e0 = ranges[0]
-        if self.fs and self.overlap:
-            self._concurrent(lambda s: L.moe_combine_bwd_range(c, dy, self.gates, self.dest_row,
-                                                               self.ys, self.layout, self.dgates,
-                                                               self.dout_r, b0, e0, stream=s),
-                             lambda s: L.moe_expert_ffn_bwd(c, self.x, self.rows_T, 1, T, self.fs,
-                                                            self.w_gu_s, self.w_down_s,
-                                                            self.g_u_h_s, dy, self.dgu_s,
-                                                            self.dx_s, self.dw_gu_s,
-                                                            self.dw_down_s, accumulate, stream=s))
-        else:
-            L.moe_combine_bwd_range(c, dy, self.gates, self.dest_row, self.ys, self.layout,
-                                    self.dgates, self.dout_r, b0, e0)
-            if self.fs:
-                L.moe_expert_ffn_bwd(c, self.x, self.rows_T, 1, T, self.fs, self.w_gu_s,
-                                     self.w_down_s, self.g_u_h_s, dy, self.dgu_s, self.dx_s,
-                                     self.dw_gu_s, self.dw_down_s, accumulate)
-        self._mark("B6+B5 combine_bwd (range 0)")
-        for (pb, pe), (b, e) in zip(ranges[:-1], ranges[1:]):
-            self._concurrent(
-                lambda s, b=b, e=e: L.moe_combine_bwd_range(c, dy, self.gates, self.dest_row,
-                                                            self.ys, self.layout, self.dgates,
-                                                            self.dout_r, b, e, stream=s),
-                lambda s, pb=pb, pe=pe: L.moe_expert_ffn_bwd_dh(c, self.layout, pb, pe,
-                                                                self.w_down, self.g_u_h,
-                                                                self.dout_r, self.dgu, stream=s))
-        L.moe_expert_ffn_bwd_dh(c, self.layout, ranges[-1][0], ranges[-1][1], self.w_down,
-                                self.g_u_h, self.dout_r, self.dgu)
-        self._mark("B5 combine_bwd || B4 dgrad-1 (chunked)")
-        L.moe_expert_ffn_bwd_dx_dispatch(c, self.xr, self.layout, self.w_gu, self.g_u_h,
-                                         self.dout_r, self.dgu, self.dxs, self.dw_gu, self.dw_down,
-                                         accumulate)
-        self._mark("B4 dgrad-2 + B3 dispatch_bwd + wgrad")
-        return self._backward_tail(dy, accumulate, True)
-
     # ------------------------------------------------------------------ backward
     def backward(self, dy: torch.Tensor, accumulate: bool = False) -> torch.Tensor:
         """dy [T_local, d] bf16 -> dx [T_local, d] bf16; fills dw_r, dw_gu, dw_down
@@ -409,9 +354,6 @@ class MoELayer:
         f, T = self.dims.f, self.dims.T_local
         if self.dedup:
             return self._backward_dedup(dy, accumulate)
-        ranges = self._ranges()
-        if ranges:
-            return self._backward_chunked(dy, accumulate, ranges)
         shared_done = False
         if self.fs and self.overlap:
             # shared-expert backward (needs only dy) beside the combine_bwd all-to-all
@@ -527,38 +469,87 @@ class MoELayer:
         self.loads = None
         return swaps, moved
 
+    # imbalance threshold of maybe_rebalance (reading R20): the most-loaded EP rank receives
+    # more than 10 % above the mean
+    rebalance_threshold = 1.10
+
+    def imbalance(self, loads=None):
+        """max / mean of the EP ranks' routed rows over the observed loads (libmoe)."""
+        loads = self.loads if loads is None else loads
+        return L.moe_load_imbalance([int(v) for v in loads], self.placement, self.dims.ep_size)
+
+    def maybe_rebalance(self, threshold=None, max_iters=100):
+        """The external scheduler of PAPER.md:648: when the observed imbalance crosses the
+        threshold, run Alg. 2 and migrate; otherwise keep accumulating loads.  Every rank
+        sees the same loads (the layout record), so every rank takes the same decision.
+        Returns (imbalance, swaps, experts moved) -- swaps = moved = 0 if below."""
+        if self.loads is None or self.dims.ep_size == 1:
+            return 1.0, 0, 0
+        thr = self.rebalance_threshold if threshold is None else threshold
+        imb = self.imbalance()
+        if imb <= thr:
+            return imb, 0, 0
+        swaps, moved = self.rebalance(max_iters=max_iters)
+        return imb, swaps, moved
+
+    def _verify_symmetric(self):
+        """Every rank must have made the same symmetric allocations (peers write at OUR
+        offsets): compare the allocation fingerprints (moe_ctx_verify_symmetric)."""
+        self.ctx.verify_symmetric(_all_gather_bytes(self.ctx.fingerprint(), self.group))
+
+    def expert_state(self, name, per_expert_shape, dtype):
+        """Registers per-expert state [E_l, *per_expert_shape] (e.g. optimizer moments) that
+        migrate() moves with the experts; returns the current buffer.  Collective (symmetric
+        allocation); needs migratable=True and expert_state_bytes room."""
+        if not self.migratable:
+            raise RuntimeError("expert_state needs MoELayer(migratable=True)")
+        shape = (self.E_l, *per_expert_shape)
+        self._states[name] = [self.ctx.symm_empty(shape, dtype) for _ in range(2)]
+        if self.dims.ep_size > 1:
+            self._verify_symmetric()
+        return self._states[name][self._cur]
+
+    def state(self, name):
+        """Current buffer of a migratable per-expert state ("w_gu", "w_down", "dw_gu",
+        "dw_down" or a registered name)."""
+        return self._states[name][self._cur]
+
     def migrate(self, new_placement, group=None):
-        """Moves expert weights to the owners given by new_placement (expert -> global slot)
-        and switches the ctx to it.  Slot tensors are re-indexed locally; experts that change
-        rank are exchanged with NCCL point-to-point (3 d f bf16 parameters each; the paper's
-        48 d f bytes per expert also count optimizer state)."""
-        E_l, EP, r = self.E_l, self.dims.ep_size, self.dims.ep_rank
+        """Moves every expert's state (bf16 weights, fp32 weight gradients and any state
+        registered with expert_state) to the owners given by new_placement (expert -> global
+        slot) and switches the ctx to it.  Collective over the EP group.  Each tensor moves
+        with ONE moe_migrate launch: old owners push their experts straight into the new
+        owners' other half of the double buffer over the peer maps (PAPER.md:648's migration
+        of experts with their state -- 48 d f bytes each incl. optimizer state, Table
+        PAPER.md:650-668).  Gradients move WITH their experts, so an accumulation in progress
+        stays credited to the right expert.  Invalidates captured CUDA graphs.  Returns the
+        number of experts that changed rank."""
+        E_l, r = self.E_l, self.dims.ep_rank
         old = list(self.placement)
         new = [int(v) for v in new_placement]
-        new_gu = torch.empty_like(self.w_gu)
-        new_down = torch.empty_like(self.w_down)
-        ops = []
-        moved = 0
-        import torch.distributed as dist
-        for e in range(self.dims.E):
-            oq, ol = divmod(old[e], E_l)
-            nq, nl = divmod(new[e], E_l)
-            if oq != nq:
-                moved += 1
-            if nq == r and oq == r:
-                new_gu[nl].copy_(self.w_gu[ol])
-                new_down[nl].copy_(self.w_down[ol])
-            elif nq == r:
-                ops += [dist.P2POp(dist.irecv, new_gu[nl], oq, group),
-                        dist.P2POp(dist.irecv, new_down[nl], oq, group)]
-            elif oq == r:
-                ops += [dist.P2POp(dist.isend, self.w_gu[ol].contiguous(), nq, group),
-                        dist.P2POp(dist.isend, self.w_down[ol].contiguous(), nq, group)]
-        if ops:
-            for req in dist.batch_isend_irecv(ops):
-                req.wait()
-        torch.cuda.synchronize(self.device)
-        self.w_gu, self.w_down = new_gu, new_down
+        if sorted(new) != list(range(self.dims.E)):
+            raise ValueError("new_placement must be a permutation of range(E)")
+        moved = sum(1 for e in range(self.dims.E) if old[e] // E_l != new[e] // E_l)
+        if self.migratable:
+            nxt = 1 - self._cur
+            for bufs in self._states.values():
+                L.moe_migrate(self.ctx, old, new, bufs[self._cur], bufs[nxt])
+            self._cur = nxt
+            self.w_gu, self.w_down = self._states["w_gu"][nxt], self._states["w_down"][nxt]
+            self.dw_gu, self.dw_down = self._states["dw_gu"][nxt], self._states["dw_down"][nxt]
+        else:
+            if moved:
+                raise RuntimeError("moving experts between ranks needs MoELayer(migratable=True)")
+            # local slot permutation (EP = 1 or an intra-rank reshuffle)
+            perm = torch.empty(E_l, dtype=torch.int64)
+            for e in range(self.dims.E):
+                if new[e] // E_l == r:
+                    perm[new[e] % E_l] = old[e] % E_l
+            perm = perm.to(self.device)
+            self.w_gu = self.w_gu.index_select(0, perm).contiguous()
+            self.w_down = self.w_down.index_select(0, perm).contiguous()
+            self.dw_gu.copy_(self.dw_gu.index_select(0, perm))
+            self.dw_down.copy_(self.dw_down.index_select(0, perm))
         self.placement = new
         self.ctx.set_placement(new)
         return moved
@@ -588,8 +579,6 @@ class MoELayer:
         if fwd:
             # router GEMM, route, permute (3), dispatch (1 fused launch), ffn (2), combine (2)
             n += 1 + 1 + 3 + 1 + 2 + 2 + (2 if self.fs else 0)
-        extra = 2 * (len(self._ranges()) - 1) if self._ranges() else 0   # per range: a2a + GEMM
-        n += extra * (int(fwd) + int(bwd))
         if bwd:
             # combine_bwd (1), ffn_bwd (4), dispatch_bwd (1), route_bwd,
             # router bwd (hi/lo split, split-K dW_r GEMM, partial sum; k = 1 adds the

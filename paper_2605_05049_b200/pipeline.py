@@ -51,8 +51,11 @@ class PipelineStack:
                  if device is not None else 0)
         self.layers = []                                    # [local layer][slot]
         for _ in range(self.n_local):
-            slots = [layer_cls(dims, device=device, group=self.group, fused=fused, dedup=dedup)
-                     for _ in range(self.n_slots)]
+            # slot 0 owns the layer's (migratable) expert state; the other activation contexts
+            # share it by reference (set_weights), so they need no state buffers of their own
+            slots = [layer_cls(dims, device=device, group=self.group, fused=fused, dedup=dedup,
+                               migratable=None if i == 0 else False)
+                     for i in range(self.n_slots)]
             if n_sms:
                 for s in slots:
                     s.set_base_comm_sms(n_sms - free_sms)
@@ -74,13 +77,29 @@ class PipelineStack:
         slots = self.layers[l]
         for s in slots:
             s.set_weights(w_r, w_gu, w_down, bias, w_gu_s, w_down_s)
-        s0 = slots[0]
-        for s in slots[1:]:
+        self._share(l)
+
+    def _share(self, l):
+        s0 = self.layers[l][0]
+        for s in self.layers[l][1:]:
             s.w_r, s.w_gu, s.w_down, s.bias = s0.w_r, s0.w_gu, s0.w_down, s0.bias
             s.w_gu_s, s.w_down_s = s0.w_gu_s, s0.w_down_s
             s.dw_r, s.dw_gu, s.dw_down = s0.dw_r, s0.dw_gu, s0.dw_down
             if s0.fs:
                 s.dw_gu_s, s.dw_down_s = s0.dw_gu_s, s0.dw_down_s
+
+    def migrate(self, l, new_placement):
+        """Expert migration of local layer l as ONE stack-level operation: slot 0 moves the
+        layer's expert state (weights and gradients, MoELayer.migrate), every other activation
+        context is re-pointed at the moved tensors and switched to the new placement.
+        Collective over the stage's EP group; call between steps."""
+        slots = self.layers[l]
+        moved = slots[0].migrate(new_placement)
+        for s in slots[1:]:
+            s.placement = list(slots[0].placement)
+            s.ctx.set_placement(s.placement)
+        self._share(l)
+        return moved
 
     def grads(self, l):
         s0 = self.layers[l][0]
@@ -102,7 +121,7 @@ class PipelineStack:
                 if self.prev is None:
                     h = xs[m]
                 else:
-                    dist.irecv(self.recv_act[m], src=self.prev).wait()
+                    self._recv(self.recv_act[m], self.prev)
                     h = self.recv_act[m]
                 for l in range(self.n_local):
                     lay = self.layers[l][slot]
@@ -115,12 +134,12 @@ class PipelineStack:
                     self.y_out[m].copy_(h)
                 else:
                     self.send_act[m].copy_(h)
-                    pending.append(dist.isend(self.send_act[m], dst=self.next))
+                    pending.append(self._send(self.send_act[m], self.next))
             else:
                 if last:
                     g = dys[m]
                 else:
-                    dist.irecv(self.recv_grad[m], src=self.next).wait()
+                    self._recv(self.recv_grad[m], self.next)
                     g = self.recv_grad[m]
                 for l in reversed(range(self.n_local)):
                     lay = self.layers[l][slot]
@@ -132,16 +151,37 @@ class PipelineStack:
                     self.dx_out[m].copy_(g)
                 else:
                     self.send_grad[m].copy_(g)
-                    pending.append(dist.isend(self.send_grad[m], dst=self.prev))
+                    pending.append(self._send(self.send_grad[m], self.prev))
         for p in pending:
             p.wait()
         return (self.y_out if last else None), (self.dx_out if self.prev is None else None)
+
+    def _host_staged(self):
+        """gloo moves CPU tensors only: with a gloo group and device tensors (several ranks
+        sharing one GPU in the tests, tests/mp_common.py) the hand-offs go through host
+        copies; NCCL (one GPU per rank) moves device memory directly."""
+        return self.device.type == "cuda" and self.dist.get_backend() == "gloo"
+
+    def _send(self, buf, dst):
+        if self._host_staged():
+            return self.dist.isend(buf.cpu(), dst=dst)   # .cpu() waits for the producer
+        return self.dist.isend(buf, dst=dst)
+
+    def _recv(self, buf, src):
+        if self._host_staged():
+            h = torch.empty(buf.shape, dtype=buf.dtype)
+            self.dist.recv(h, src=src)
+            buf.copy_(h)
+        else:
+            self.dist.irecv(buf, src=src).wait()
 
     def capture(self, xs=None, dys=None):
         """Records one step(xs, dys) -- every layer call and the NCCL stage hand-offs -- into a
         CUDA graph and returns it; graph.replay() reruns the step on the current contents of
         xs / dys (outputs in the buffers step() returns).  Collective: every rank captures
         (one eager warm-up step on the capture stream first) and replays in lockstep."""
+        if self._host_staged():
+            raise RuntimeError("CUDA-graph capture needs device-side (NCCL) stage hand-offs")
         dev = self.device
         s = torch.cuda.Stream(device=dev)
         s.wait_stream(torch.cuda.current_stream(dev))

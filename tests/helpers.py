@@ -1,7 +1,8 @@
 """Test-side glue: tensor conversion, layout mapping and the error metric.
 
 The error metric (reading R13): per tensor,
-err = max_i |gpu_i - ref_i| / max_i |ref_i|.  The bar is 2e-2 (BASELINE.json
+err = max_i |gpu_i - ref_i| / max_i |ref_i|, and for token-indexed tensors also per token
+row (rel_err_rows).  The bar is 2e-2 (BASELINE.json
 north_star, bf16 inputs); bf16 storage of the saved activations predicts
 2.6e-3 .. 4e-3, so the tests assert TOL = 2e-2 and report the value.
 """
@@ -23,6 +24,25 @@ def rel_err(gpu, ref):
     if scale == 0:
         return float(np.abs(gpu).max())
     return float(np.abs(gpu - ref).max() / scale)
+
+
+def rel_err_rows(gpu, ref):
+    """Per-token-row error of a [T, ...] tensor (y, dx, dgates, dlogits): for every row t,
+    max_i |gpu_ti - ref_ti| / max(max_i |ref_ti|, rms(ref)); returns the worst row's value.
+    Unlike the per-tensor metric, a wrong row whose magnitude is small against the tensor's
+    largest row cannot hide.  The floor at the tensor's RMS keeps rows
+    that are near zero by cancellation (a dg row of two small dot products) from turning the
+    bf16 rounding of their inputs into a spurious O(1) ratio; a misrouted row still shows up
+    as O(1) against it."""
+    gpu = np.asarray(gpu, np.float64).reshape(len(gpu), -1)
+    ref = np.asarray(ref, np.float64).reshape(len(ref), -1)
+    if ref.size == 0:
+        return 0.0
+    rms = float(np.sqrt(np.mean(ref * ref)))
+    if rms == 0:
+        return float(np.abs(gpu).max())
+    den = np.maximum(np.abs(ref).max(axis=1), rms)
+    return float((np.abs(gpu - ref).max(axis=1) / den).max())
 
 
 def seg_bases(rows, align=ALIGN):

@@ -23,6 +23,8 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
+from tests import mp_common  # noqa: E402
+
 
 def encoded_rows(rank, n, d):
     """Row i of source `rank`: [rank, i // 128, i % 128, (7 rank + 3 i + c) % 251 - 125 ...];
@@ -37,9 +39,7 @@ def encoded_rows(rank, n, d):
 
 
 def main():
-    local = int(os.environ["LOCAL_RANK"])
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    local, shared = mp_common.init()
     ep, rank = dist.get_world_size(), dist.get_rank()
     from paper_2605_05049_b200 import _lib as L
     from paper_2605_05049_b200.layer import _all_gather_bytes
@@ -125,8 +125,7 @@ def main():
                                        torch.equal(xr2[:used], xr[:used]))
     st = ctx.device_error()
     flags = torch.tensor([int(all(checks.values())), st], device="cuda")
-    allf = [torch.empty_like(flags) for _ in range(ep)]
-    dist.all_gather(allf, flags)
+    allf = mp_common.gather(flags)
     if rank == 0:
         res = {"ep": ep, "ok": all(int(f[0]) == 1 and int(f[1]) == 0 for f in allf),
                "per_rank": [[int(f[0]), int(f[1])] for f in allf], "checks_rank0": checks}

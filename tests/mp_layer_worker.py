@@ -19,6 +19,7 @@ import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
 import synth  # noqa: E402
+from tests import mp_common  # noqa: E402
 
 CASES = {
     "tiny": synth.MoEConfig("tiny_ep", T=512, d=64, E=8, k=2, f=128, cf=1.25),
@@ -32,10 +33,7 @@ CASES = {
 }
 
 
-def gather(t):
-    out = [torch.empty_like(t) for _ in range(dist.get_world_size())]
-    dist.all_gather(out, t.contiguous())
-    return out
+gather = mp_common.gather
 
 
 def main():
@@ -45,52 +43,55 @@ def main():
     ap.add_argument("--stepwise", action="store_true", help="unfused step-by-step calls")
     ap.add_argument("--rebalance", action="store_true",
                     help="observe loads, run Alg. 2 (moe_rebalance) and migrate before checking")
-    ap.add_argument("--chunks", type=int, default=None, help="MoELayer.chunks (NEXT-1 overlap)")
     ap.add_argument("--dedup", nargs="?", const="dispatch", default=None,
                     choices=["dispatch", "all"],
                     help="NEXT-4 deduplicated all-to-alls (pair tables and xr checked bitwise)")
     ap.add_argument("--graph", action="store_true",
                     help="also replay the step from a CUDA graph (device-side collective epoch)")
     args = ap.parse_args()
-    local = int(os.environ["LOCAL_RANK"])
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    local, shared = mp_common.init()
     ep, rank = dist.get_world_size(), dist.get_rank()
     cfg = CASES[args.config]
     from tests.test_gpu_layer import build_layer, oracle_layer
-    from tests.helpers import TOL, f64, rel_err
+    from tests.helpers import TOL, f64, rel_err, rel_err_rows
 
-    layer = build_layer(cfg, ep_size=ep, ep_rank=rank, device=local, dedup=args.dedup)
+    n_par = 3 * cfg.d * cfg.f                       # parameters per expert
+    layer = build_layer(cfg, ep_size=ep, ep_rank=rank, device=local, dedup=args.dedup,
+                        expert_state_bytes=3 * 4 * n_par if args.rebalance else 0)
+    E_l = cfg.E // ep
+    code = lambda e: (e + (torch.arange(n_par, device="cuda") % 7).float() / 8)   # exact in fp32
+    if args.rebalance:
+        # optimizer-like state (fp32 master copy + two moments: the 12 of the paper's 16 B per
+        # parameter) registered to move with the experts
+        opt = [layer.expert_state(nm, (n_par,), torch.float32) for nm in ("master", "m", "v")]
+        for i, t in enumerate(opt):
+            for el in range(E_l):
+                t[el].copy_(code(rank * E_l + el) * (i + 1))
     layer.fused = not args.stepwise
-    if args.chunks is not None:
-        layer.chunks = args.chunks
     T_r = cfg.T // ep
     x = synth.tokens(cfg).cuda()[rank * T_r:(rank + 1) * T_r].contiguous()
     dy = synth.grad_output(cfg).cuda()[rank * T_r:(rank + 1) * T_r].contiguous()
     place = None
+    state_ok = True
     if args.rebalance:
         layer.forward(x)
         layer.observe_loads()
-        swaps, moved = layer.rebalance(group=None)
+        swaps, moved = layer.rebalance()
         place = list(layer.placement)
+        inv = [0] * cfg.E
+        for e_, s_ in enumerate(place):
+            inv[s_] = e_
+        state_ok = moved > 0
+        for i, nm in enumerate(("master", "m", "v")):
+            t = layer.state(nm)
+            for el in range(E_l):
+                state_ok &= bool(torch.equal(t[el], code(inv[rank * E_l + el]) * (i + 1)))
     outs = []
     for _ in range(args.iters):  # epoch reuse: repeated calls must be bit-identical
         y = layer.forward(x).clone()
         dx = layer.backward(dy).clone()
         outs.append((y, dx, layer.dw_gu.clone()))
     graph_ok = True
-    if args.chunks is not None and args.chunks > 1 and os.environ.get("MOE_STREAM_K") == "0":
-        # with the unsplit K summation the chunked overlap and the unchunked calls give
-        # bit-identical results (stream-K splits depend on each launch's tile count)
-        saved = layer.chunks
-        layer.chunks = 1
-        y1 = layer.forward(x).clone()
-        dx1 = layer.backward(dy).clone()
-        graph_ok &= bool(torch.equal(y1, outs[0][0]) and torch.equal(dx1, outs[0][1]) and
-                         torch.equal(layer.dw_gu, outs[0][2]))
-        layer.chunks = saved
-        layer.forward(x)
-        layer.backward(dy)
     if args.graph:
         # replays must match the eager step bit for bit (every replay is a fresh exchange), and
         # a replay on new input contents must match the eager step on those contents
@@ -132,7 +133,7 @@ def main():
     if cfg.E_s:
         g["dw_gu_s"] = gather(layer.dw_gu_s)
         g["dw_down_s"] = gather(layer.dw_down_s)
-    flags = torch.tensor([st, int(repeat_ok and graph_ok)], device="cuda")
+    flags = torch.tensor([st, int(repeat_ok and graph_ok and state_ok)], device="cuda")
     allflags = gather(flags)
     if rank != 0:
         dist.barrier()
@@ -184,6 +185,9 @@ def main():
     errs["dx"] = rel_err(f64(cat("dx")), bw["dx"])
     errs["dgates"] = rel_err(f64(cat("dgates")), bw["dgates"])
     errs["dW_r"] = rel_err(sum(f64(t) for t in g["dw_r"]).T, bw["dW_r"])
+    errs["y_rows"] = rel_err_rows(f64(cat("y")), fw["y"])
+    errs["dx_rows"] = rel_err_rows(f64(cat("dx")), bw["dx"])
+    errs["dgates_rows"] = rel_err_rows(f64(cat("dgates")), bw["dgates"])
     f = cfg.f
     for e in range(cfg.E):
         q, el = divmod(e if place is None else place[e], E_l)

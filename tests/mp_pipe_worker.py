@@ -20,14 +20,12 @@ import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
 import synth  # noqa: E402
+from tests import mp_common  # noqa: E402
 
 CFG = synth.MoEConfig("pipe_small", T=512, d=256, E=8, k=2, f=256, cf=1.25)
 
 
-def gather(t):
-    out = [torch.empty_like(t) for _ in range(dist.get_world_size())]
-    dist.all_gather(out, t.contiguous())
-    return out
+gather = mp_common.gather
 
 
 def layer_weights(g, experts, device):
@@ -45,19 +43,21 @@ def main():
     ap.add_argument("--layers", type=int, default=4)
     ap.add_argument("--micro", type=int, default=4)
     ap.add_argument("--dedup", default=None)
+    ap.add_argument("--migrate", action="store_true",
+                    help="after the warm-up step every stage migrates its layers' experts to a "
+                         "seeded placement (PipelineStack.migrate: peer-store moves inside the "
+                         "stage's EP subgroup)")
     ap.add_argument("--graph", action="store_true",
                     help="also replay the step from a CUDA graph: bitwise equal to eager")
     args = ap.parse_args()
-    local = int(os.environ["LOCAL_RANK"])
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    local, shared = mp_common.init()
     world, rank = dist.get_world_size(), dist.get_rank()
     pp, M, Lyr = args.pp, args.micro, args.layers
     ep = world // pp
     stage, e = divmod(rank, ep)
     from paper_2605_05049_b200 import LayerDims
     from paper_2605_05049_b200.pipeline import PipelineStack
-    from tests.helpers import TOL, f64, paper_weights, rel_err
+    from tests.helpers import TOL, f64, paper_weights, rel_err, rel_err_rows
     cfg = CFG
     T_r = cfg.T // ep
     dims = LayerDims(T_r, cfg.d, cfg.E, cfg.k, cfg.f, 0, cfg.cf, ep, e)
@@ -73,6 +73,12 @@ def main():
     xs = [x_all[m, e * T_r:(e + 1) * T_r].contiguous() for m in range(M)]
     dys = [dy_all[m, e * T_r:(e + 1) * T_r].contiguous() for m in range(M)]
     stack.step(xs if stage == 0 else None, dys if stage == pp - 1 else None)   # warm-up step
+    place_of = lambda s_: (list(np.random.default_rng(100 + s_).permutation(cfg.E))
+                           if args.migrate else list(range(cfg.E)))
+    moved = 0
+    if args.migrate:
+        for l in range(per):
+            moved += stack.migrate(l, place_of(stage))
     graph_ok = True
     if args.graph:
         a_in, a_dy = (xs if stage == 0 else None), (dys if stage == pp - 1 else None)
@@ -100,6 +106,8 @@ def main():
     plain = MoELayer(dims, device=local, group=stack.group, dedup=args.dedup)
     w_r, w_gu, w_down = layer_weights(stage * per, range(e * E_l, (e + 1) * E_l), dev)
     plain.set_weights(w_r, w_gu, w_down)
+    if args.migrate:
+        plain.migrate(place_of(stage))
     yp = plain.forward(rec[(0, 0)]["x"]).clone()
     dxp = plain.backward(rec[(0, 0)]["dy"]).clone()
     torch.cuda.synchronize()
@@ -143,6 +151,8 @@ def main():
                                            fw["plan"]["ranks"][i]["dest_row"]).all())
             errs[f"y{g}.{m}"] = rel_err(f64(Y), fw["y"])
             errs[f"dx{g}.{m}"] = rel_err(f64(DX), bw["dx"])
+            errs[f"y_rows{g}.{m}"] = rel_err_rows(f64(Y), fw["y"])
+            errs[f"dx_rows{g}.{m}"] = rel_err_rows(f64(DX), bw["dx"])
             acc = lambda a, b: b if a is None else [u + v for u, v in zip(a, b)]
             dWg, dWu, dWd = acc(dWg, bw["dW_gate"]), acc(dWu, bw["dW_up"]), acc(dWd, bw["dW_down"])
             dWr = bw["dW_r"] if dWr is None else dWr + bw["dW_r"]
@@ -154,7 +164,7 @@ def main():
                     checks["handoff"] &= bool(torch.equal(G["y"][l][m][r1], G["x"][l2][m][r2]))
                     checks["handoff"] &= bool(torch.equal(G["dy"][l][m][r1], G["dx"][l2][m][r2]))
         for x in range(cfg.E):
-            q, el = divmod(x, E_l)
+            q, el = divmod(int(place_of(s_)[x]), E_l)
             r = rs[q]
             dgu = f64(dW[l][1][r][el])
             errs[f"dWg{g}.{x}"] = rel_err(dgu[:cfg.f].T, dWg[x])
@@ -167,7 +177,7 @@ def main():
     worst = max(errs, key=errs.get)
     checks["direct_layer0"] = all(bool(t.item()) for t in dflags)
     checks["graph_replay"] = all(bool(t.item()) for t in gflags)
-    res = {"pp": pp, "ep": ep, "layers": Lyr, "micro": M, "checks": checks,
+    res = {"pp": pp, "ep": ep, "migrated": bool(args.migrate), "layers": Lyr, "micro": M, "checks": checks,
            "device_status": [int(t.item()) for t in st], "worst": [worst, errs[worst]],
            "schedule_stage0": stack.ops if stage == 0 else None}
     res["ok"] = (all(checks.values()) and all(v < TOL for v in errs.values()) and

@@ -4,6 +4,7 @@ import ctypes
 import os
 import re
 
+import numpy as np
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -105,3 +106,14 @@ def test_rebalance_matches_oracle_alg2(lib, seed):
 def test_rebalance_rejects_non_permutation(lib):
     with pytest.raises(lib.MoEError):
         lib.moe_rebalance([1, 2, 3, 4], 2, [0, 0, 1, 2])
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_load_imbalance_matches_oracle(lib, seed):
+    from oracle import migration as mig
+    rng = np.random.default_rng(seed)
+    E, ep = 32, [2, 4, 8][seed % 3]
+    loads = rng.integers(0, 5000, E)
+    place = rng.permutation(E)
+    assert lib.moe_load_imbalance(loads, place, ep) == mig.imbalance(loads, place, ep)
+    assert lib.moe_load_imbalance([0] * E, list(range(E)), ep) == 1.0

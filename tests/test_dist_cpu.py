@@ -149,7 +149,7 @@ class _ToyLayer:
     y = bf16(a*x + 1), dx = bf16(a*dy), and a 'weight gradient' dw = sum(dy*x) in fp32,
     overwritten by the first backward and accumulated by the others."""
 
-    def __init__(self, dims, device=None, group=None, fused=True, dedup=False):
+    def __init__(self, dims, device=None, group=None, fused=True, dedup=False, migratable=None):
         self.dims = dims
         self.fs = 0
         self.a = 1.0

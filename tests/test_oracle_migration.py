@@ -110,3 +110,21 @@ def test_migration_cost_table_golden():
         b = mig.migration_bytes(E // 8, d, f)
         if unit == "GiB":
             assert math.ceil(b / 2**30 * 100 - 1e-9) / 100 == float(gb), model
+
+
+def test_imbalance_trigger_hand_worked():
+    """Reading R20: imbalance = max_q s_q / mean_q s_q.  E=4 on EP=2, contiguous placement:
+    loads [6, 2, 1, 1] -> s = [8, 2], mean 5 -> 1.6; after swapping experts 1 and 2 the ranks
+    hold [6, 1] and [2, 1] -> s = [7, 3] -> 1.4; a perfectly balanced load is exactly 1."""
+    assert mig.imbalance([6, 2, 1, 1], [0, 1, 2, 3], 2) == 1.6
+    assert mig.imbalance([6, 2, 1, 1], [0, 2, 1, 3], 2) == 1.4
+    assert mig.imbalance([3, 3, 3, 3], [0, 1, 2, 3], 4) == 1.0
+    assert mig.imbalance([0, 0, 0, 0], [0, 1, 2, 3], 2) == 1.0
+    assert mig.should_migrate([6, 2, 1, 1], [0, 1, 2, 3], 2, 1.5)
+    assert not mig.should_migrate([6, 2, 1, 1], [0, 1, 2, 3], 2, 1.6)   # strictly above
+    # Alg. 2 never raises the imbalance it is triggered on (it only applies improving swaps)
+    rng = np.random.default_rng(3)
+    for _ in range(50):
+        loads = rng.integers(0, 1000, 16)
+        new, _ = mig.rebalance_placement(loads, 4)
+        assert mig.imbalance(loads, new, 4) <= mig.imbalance(loads, np.arange(16), 4)
