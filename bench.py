@@ -173,11 +173,24 @@ def gemm_traffic(config, world):
         return None
 
 
-def layer_roofline(layer, cfg, peaks, nvl_gbs=900.0):
+def gemm_ncu(config, world):
+    """Per-launch ncu metrics of the 6 expert-GEMM launches (tensor-pipe %, SM clock, DRAM
+    bytes) from the committed --set full capture (profiles/gemm_ncu.json), if captured for
+    this configuration."""
+    p = os.path.join(ROOT, "profiles", "gemm_ncu.json")
+    try:
+        with open(p) as fh:
+            return json.load(fh)[f"{config}_ep{world}"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
+def layer_roofline(layer, cfg, peaks, nvl_gbs=900.0, sustained=False):
     """SURVEY.md §8(d) d.3 serial layer roofline from the realised routing (the layout
     record's [EP x E] count matrix and the expert placement, identical on every rank):
     sum over the steps of max(F/pi, B_hbm/beta_hbm, B_nvl/beta_nvl) on the hottest rank,
-    pi = measured sustained bf16, beta_hbm = measured HBM copy bandwidth, beta_nvl = 900 GB/s
+    pi = measured bf16 (burst; sustained=True: the 4 s back-to-back figure),
+    beta_hbm = measured HBM copy bandwidth, beta_nvl = 900 GB/s
     per direction.  Steps: router GEMM (fwd + 2 bwd), permute / unpermute / permute_bwd /
     combine_bwd's dO writes (HBM), 4 all-to-alls (NVLink, max of egress and ingress), expert
     GEMMs fwd + bwd (18 d f per routed row, shared experts on the local tokens)."""
@@ -185,7 +198,8 @@ def layer_roofline(layer, cfg, peaks, nvl_gbs=900.0):
     T_r = layer.dims.T_local
     cm = layer.layout[:EP * E].view(EP, E).to(torch.int64).cpu()
     owner = torch.tensor([s // layer.E_l for s in layer.placement])
-    pi = peaks["bf16_sustained"] * 1e12
+    pi_tf = peaks["bf16_sustained"] if sustained else peaks["bf16"]
+    pi = pi_tf * 1e12
     bh = peaks["hbm"] * 1e9
     bn = nvl_gbs * 1e9
     row = d * 2
@@ -225,7 +239,7 @@ def layer_roofline(layer, cfg, peaks, nvl_gbs=900.0):
     hot = max(range(EP), key=lambda r: per_rank[r])
     return {"serial_ms": per_rank[hot], "hot_rank": hot,
             "per_rank_ms": [round(v, 4) for v in per_rank],
-            "peaks": {"bf16_tflops": peaks["bf16_sustained"], "hbm_gbs": peaks["hbm"],
+            "peaks": {"bf16_tflops": pi_tf, "hbm_gbs": peaks["hbm"],
                       "nvlink_gbs_per_direction": nvl_gbs}}
 
 
@@ -359,21 +373,7 @@ def run_ours(args):
     if args.breakdown:
         return breakdown()
 
-    # ---- device-timed region
-    # the grouped-GEMM calls (fused: their epilogues also store rows to the peers, and the
-    # calls end with the flag wait / unpermute -- so the measured region is conservative)
-    hooked = ["moe_expert_ffn", "moe_expert_ffn_bwd", "moe_expert_ffn_combine",
-              "moe_expert_ffn_bwd_dispatch", "moe_expert_ffn_up", "moe_expert_ffn_down_combine",
-              "moe_expert_ffn_bwd_dh", "moe_expert_ffn_bwd_dx_dispatch"]
-    buckets = {"moe_permute": "permute", "moe_dispatch": "dispatch",
-               "moe_dispatch_range": "dispatch", "moe_combine_bwd": "combine_bwd",
-               "moe_combine_bwd_range": "combine_bwd", "moe_dedup_dispatch": "dispatch",
-               "moe_dedup_combine_bwd": "combine_bwd", "moe_dedup_combine_bwd_ys": "combine_bwd"}
-    originals = {n: getattr(layer_mod.L, n) for n in hooked + list(buckets)}
-    for n in hooked:
-        setattr(layer_mod.L, n, timed(originals[n]))
-    for n, b in buckets.items():
-        setattr(layer_mod.L, n, timed(originals[n], b))
+    # ---- device-timed region: the plain step loop, nothing else on the stream (`value`)
     clocks = ClockSampler(local)
     barrier()
     torch.cuda.synchronize()
@@ -388,17 +388,12 @@ def run_ours(args):
     torch.cuda.synchronize()
     barrier()
     clk = clocks.stop()
-    for n, fn in originals.items():
-        setattr(layer_mod.L, n, fn)
     layer.ctx.check_device_error()
     ms = t0.elapsed_time(t1) / args.steps
-    region_ms = {b: sum(a.elapsed_time(z) for a, z in ev) / args.steps
-                 for b, ev in region_ev.items()}
     eager_ms = ms
     graph_ms = None
     if args.graph:
-        # the same step replayed from one CUDA graph (no host launch overhead); the GEMM-region
-        # events above stay the roofline source (events cannot be timed inside a replay)
+        # the same step replayed from one CUDA graph (no host launch overhead)
         graph = layer.capture(x, dy)
         for _ in range(args.warmup):
             graph.replay()
@@ -415,6 +410,37 @@ def run_ours(args):
         layer.ctx.check_device_error()
         graph_ms = t0.elapsed_time(t1) / args.steps
         del graph
+
+    # ---- a SEPARATE instrumented pass for the per-kernel regions (roofline.achieved): CUDA
+    # events around the C-ABI calls, on the stream each call is issued on -- the grouped-GEMM
+    # family (the dominant kernel: 6 launches per step), the permute (HBM) and the two
+    # forward-pattern all-to-alls (NVLink).  Not part of `value`.
+    hooked = ["moe_expert_ffn", "moe_expert_ffn_bwd", "moe_expert_ffn_combine",
+              "moe_expert_ffn_bwd_dispatch", "moe_expert_ffn_up", "moe_expert_ffn_down_combine",
+              "moe_expert_ffn_bwd_dh", "moe_expert_ffn_bwd_dx_dispatch"]
+    buckets = {"moe_permute": "permute", "moe_dispatch": "dispatch",
+               "moe_combine_bwd": "combine_bwd", "moe_dedup_dispatch": "dispatch",
+               "moe_dedup_combine_bwd": "combine_bwd", "moe_dedup_combine_bwd_ys": "combine_bwd"}
+    originals = {n: getattr(layer_mod.L, n) for n in hooked + list(buckets)}
+    for n in hooked:
+        setattr(layer_mod.L, n, timed(originals[n]))
+    for n, b in buckets.items():
+        setattr(layer_mod.L, n, timed(originals[n], b))
+    barrier()
+    torch.cuda.synchronize()
+    t0.record(stream)
+    for _ in range(args.steps):
+        layer.forward(x)
+        layer.backward(dy)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    for n, fn in originals.items():
+        setattr(layer_mod.L, n, fn)
+    layer.ctx.check_device_error()
+    instr_ms = t0.elapsed_time(t1) / args.steps
+    region_ms = {b: sum(a.elapsed_time(z) for a, z in ev) / args.steps
+                 for b, ev in region_ev.items()}
     gemm_ms = sum(s.elapsed_time(e) for s, e in gemm_ev) / args.steps
     gemm_flops = realised_gemm_flops(layer, cfg)
 
@@ -484,7 +510,8 @@ def run_ours(args):
                      "ingress": int(nm[:, rank].sum() - nm[rank, rank]) * row_b}
         permute_bytes = T_r * cfg.k * 8
     roof = layer_roofline(layer, cfg, measured_peaks())
-    vals = torch.tensor([ms, e2e_ms, gemm_ms, graph_ms or 0.0, region_ms["permute"]],
+    roof_sus = layer_roofline(layer, cfg, measured_peaks(), sustained=True)
+    vals = torch.tensor([ms, e2e_ms, gemm_ms, graph_ms or 0.0, region_ms["permute"], instr_ms],
                         dtype=torch.float64, device=dev)
     # a collective's kernel time on a rank includes waiting for the later ranks; the rank that
     # arrives last waits least, so the MIN over ranks is the transfer's own duration
@@ -493,7 +520,7 @@ def run_ours(args):
     if dist is not None:
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
         dist.all_reduce(a2a_t, op=dist.ReduceOp.MIN)
-    ms, e2e_ms, gemm_ms_max, graph_ms, perm_ms = vals.tolist()
+    ms, e2e_ms, gemm_ms_max, graph_ms, perm_ms, instr_ms = vals.tolist()
     disp_ms, cbwd_ms = a2a_t.tolist()
     eager_ms = ms
     use_graph = bool(args.graph and graph_ms < ms)
@@ -540,8 +567,11 @@ def run_ours(args):
                 "d2h_bytes_per_step": int(y_h.numel() * 2 + dx_h.numel() * 2)},
         "layer_roofline": {
             **roof, "frac": roof["serial_ms"] / ms,
+            "serial_ms_sustained_peak": roof_sus["serial_ms"],
+            "frac_sustained_peak": roof_sus["serial_ms"] / ms,
             "definition": "SURVEY.md 8(d) d.3: sum over steps of max(F/pi, B_hbm/beta_hbm, "
-                          "B_nvl/beta_nvl) on the hottest rank, realised routing",
+                          "B_nvl/beta_nvl) on the hottest rank, realised routing; pi = measured "
+                          "burst bf16 (frac), measured sustained bf16 (frac_sustained_peak)",
         },
         "secondary_rooflines": {
             "permute": {"bound": "hbm", "ms": perm_ms,
@@ -572,14 +602,20 @@ def run_ours(args):
                       "wgrad x2); timed region = the FFN C-ABI calls",
             "bound": "tensor",
             "achieved": achieved,
-            "peak": peaks["bf16_sustained"],
+            "peak": peaks["bf16"],
             "unit": "TFLOP/s",
-            "frac": achieved / peaks["bf16_sustained"],
+            "frac": achieved / peaks["bf16"],
+            "peak_sustained": peaks["bf16_sustained"],
+            "frac_sustained": achieved / peaks["bf16_sustained"],
             "traffic": gemm_traffic(args.config, world),
-            "peak_source": peaks["source"] + " bf16_tflops_sustained (kernel timed inside a long step)",
+            "ncu": gemm_ncu(args.config, world),
+            "peak_source": peaks["source"] + " bf16_tflops (burst, SURVEY.md 8(d) d.3); "
+                           "frac_sustained against bf16_tflops_sustained",
             "algorithmic_flops_per_step": gemm_flops,
             "gemm_ms_per_step": gemm_ms,
-            "gemm_share_of_step": gemm_ms / ms,
+            "gemm_share_of_step": gemm_ms / instr_ms,
+            "timing": "achieved = FLOPs / the GEMM calls' CUDA-event time in a separate "
+                      "instrumented pass (%.3f ms/step); value comes from the plain loop" % instr_ms,
         },
     }
     if world == 1 and not args.no_cpu_baseline:
@@ -781,7 +817,8 @@ def run_pipeline(args):
 def run_a2a(args):
     """Config 5: equal-split all-to-all of a bf16 send buffer, 64 KB .. 1 GB per rank:
     our NVSwitch peer-store dispatch (moe_dispatch, one expert per rank, no capacity; it
-    exchanges the counts itself) vs torch.distributed.all_to_all_single (NCCL) with static
+    exchanges the counts itself), our static equal-split all-to-all (moe_all_to_all: the same
+    layout as NCCL's, no counts round) vs torch.distributed.all_to_all_single (NCCL) with static
     splits, and vs NCCL used with data-dependent splits (counts all-to-all, host read-back,
     variable all-to-all).  Eager and CUDA-graph timings.  Reports busbw (nccl-tests)."""
     world, rank, local = dist_env()
@@ -802,23 +839,28 @@ def run_a2a(args):
         T = rows  # tokens per rank, k=1, E = world (one expert per rank), balanced
         shape = L.make_shape(T, d_eff, world, 1, 128, 0, 0.0, world, rank)
         R = L.moe_recv_rows_max(shape)
-        ctx = L.Context(shape, local, 2 * R * d_eff * 2 + 4 * 4096)
+        ctx = L.Context(shape, local, 2 * R * d_eff * 2 + T * d_eff * 2 + 8 * 4096)
         from paper_2605_05049_b200.layer import _all_gather_bytes
         ctx.open_peers(_all_gather_bytes(ctx.export_handle()))
         xr = ctx.symm_empty((R, d_eff), torch.bfloat16)
+        ra = ctx.symm_empty((world, T // world * d_eff), torch.bfloat16)   # static a2a target
         xs = torch.randn((T, d_eff), device="cuda").to(torch.bfloat16)
         counts = torch.full((world,), T // world, dtype=torch.int32, device="cuda")
         layout = torch.zeros((L.moe_layout_ints(shape),), dtype=torch.int32, device="cuda")
         ref_out = torch.empty_like(xs)
+        xsv = xs.view(world, -1)
         for _ in range(3):
             L.moe_dispatch(ctx, xs, counts, layout, xr)
+            L.moe_all_to_all(ctx, xsv, ra)
             dist.all_to_all_single(ref_out, xs)
         torch.cuda.synchronize()
         ok = torch.equal(xr[:T], ref_out)
+        ok_static = torch.equal(ra.view(-1), ref_out.view(-1))
         # enough calls that the ranks' launch skew after the barrier is amortised
         it = 200 if size <= (16 << 20) else 20
         for _ in range(it):   # clocks up, caches warm
             L.moe_dispatch(ctx, xs, counts, layout, xr)
+            L.moe_all_to_all(ctx, xsv, ra)
             dist.all_to_all_single(ref_out, xs)
         dist.barrier(); torch.cuda.synchronize()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -827,6 +869,12 @@ def run_a2a(args):
             L.moe_dispatch(ctx, xs, counts, layout, xr)
         e.record(); torch.cuda.synchronize()
         t_ours = s.elapsed_time(e) / it
+        dist.barrier(); torch.cuda.synchronize()
+        s.record()
+        for _ in range(it):
+            L.moe_all_to_all(ctx, xsv, ra)
+        e.record(); torch.cuda.synchronize()
+        t_static = s.elapsed_time(e) / it
         dist.barrier(); torch.cuda.synchronize()
         s.record()
         for _ in range(it):
@@ -849,7 +897,8 @@ def run_a2a(args):
             return g
         tg = []
         for fn in (lambda: L.moe_dispatch(ctx, xs, counts, layout, xr),
-                   lambda: dist.all_to_all_single(ref_out, xs)):
+                   lambda: dist.all_to_all_single(ref_out, xs),
+                   lambda: L.moe_all_to_all(ctx, xsv, ra)):
             try:
                 g = graph_of(fn)
                 g.replay()
@@ -880,12 +929,17 @@ def run_a2a(args):
         e.record(); torch.cuda.synchronize()
         t_dyn = s.elapsed_time(e) / it
         ok = ok and torch.equal(xr[:T], ref_out)
-        v = torch.tensor([t_ours, t_nccl, *tg, t_dyn], dtype=torch.float64, device="cuda")
+        ok_static = ok_static and torch.equal(ra.view(-1), ref_out.view(-1))
+        v = torch.tensor([t_ours, t_nccl, *tg, t_dyn, t_static], dtype=torch.float64, device="cuda")
         dist.all_reduce(v, op=dist.ReduceOp.MAX)
-        t_ours, t_nccl, tg_ours, tg_nccl, t_dyn = v.tolist()
+        t_ours, t_nccl, tg_ours, tg_nccl, tg_static, t_dyn, t_static = v.tolist()
         nbytes = T * d_eff * 2
         bus = (world - 1) / world
         results.append({"bytes_per_rank": nbytes, "bitwise_equal_nccl": bool(ok),
+                        "static_bitwise_equal_nccl": bool(ok_static),
+                        "static_ms": t_static, "static_graph_ms": tg_static,
+                        "static_busbw_GBs": nbytes / (t_static * 1e-3) / 1e9 * bus,
+                        "static_graph_busbw_GBs": nbytes / (tg_static * 1e-3) / 1e9 * bus,
                         "ours_ms": t_ours, "nccl_ms": t_nccl,
                         "ours_graph_ms": tg_ours, "nccl_graph_ms": tg_nccl,
                         "nccl_dynamic_ms": t_dyn,

@@ -132,6 +132,12 @@ moe_status moe_symm_free(moe_ctx* ctx, void* ptr);
  * (required = recv_rows_max x d x 2 for xr / dout_r, T_local x k x d x 2 for ys / dxs, the
  * dedup bounds for the moe_dedup_* buffers). */
 moe_status moe_symm_fingerprint(moe_ctx* ctx, uint64_t* out);
+/* Device memory held by the ctx (any pointer may be NULL): the symmetric heap's size and the
+ * bytes allocated from it so far, and the total of every device allocation the ctx made
+ * (heap + scratch).  Host-only; used for the per-stage memory account of the PP x EP executor
+ * against PAPER.md Eq. 4 (1F1B per-stage memory). */
+moe_status moe_ctx_device_bytes(moe_ctx* ctx, size_t* heap_bytes, size_t* heap_used,
+                                size_t* total_bytes);
 moe_status moe_ctx_verify_symmetric(moe_ctx* ctx, const uint64_t* fingerprints);
 /* Expert placement (SURVEY.md §8(f) NEXT-2 expert migration, §VI): placement[e] =
  * global slot of expert e (host int32 [E], a permutation of [0, E)); expert e then lives on
@@ -140,6 +146,14 @@ moe_status moe_ctx_verify_symmetric(moe_ctx* ctx, const uint64_t* fingerprints);
  * identity (contiguous ownership).  Collective: every rank sets the same placement; it
  * synchronises the device.  MOE_ERR_INVALID_ARG if not a permutation. */
 moe_status moe_ctx_set_placement(moe_ctx* ctx, const int32_t* placement);
+/* Equal-split all-to-all over the peer maps (BASELINE.json config 5, the sweep against
+ * ncclAllToAll; SPEC.md:476 transpose law): send = [EP][bytes_per_peer] bytes (device, local),
+ * recv = [EP][bytes_per_peer] SYMMETRIC; chunk q of send lands in chunk `ep_rank` of rank q's
+ * recv.  The layout is static, so one launch does the stores and the completion flags (no
+ * counts round); returns (stream-ordered) when this rank's recv is complete.  Collective.
+ * bytes_per_peer % 16 == 0; 0 is a no-op. */
+moe_status moe_all_to_all(moe_ctx* ctx, const void* send, void* recv, size_t bytes_per_peer,
+                          moe_stream stream);
 /* Migration trigger (an external scheduler "inspects the growing load
  * imbalance, and whenever it crosses a pre-determined threshold" runs Alg. 2; reading R20):
  * *out = max_q s_q / mean_q s_q, s_q = sum of loads[e] over the experts placement puts on
@@ -224,6 +238,15 @@ moe_status moe_route_bwd(moe_ctx* ctx, const float* logits, const int32_t* topk_
  * xs [T_local*k, d] bf16 (rows [0, sum counts) written; NULL = indices only). */
 moe_status moe_permute(moe_ctx* ctx, const moe_bf16* x, const int32_t* topk_idx,
                        int32_t* counts, int32_t* dest_row, moe_bf16* xs, moe_stream stream);
+/* F2 + F3 at EP = 1 ("EP < 2 is local only"): the permute of moe_permute with
+ * the rows written straight into the 128-aligned receive layout xr [moe_recv_rows_max, d]
+ * (by local slot, padding rows zeroed) and the layout record written -- exactly the xr and
+ * layout moe_permute + moe_dispatch produce, without the send-layout copy xs and the
+ * transfer.  counts and dest_row (send-layout rows) are as moe_permute's; xr need not be
+ * symmetric.  MOE_ERR_INVALID_ARG unless ep_size == 1. */
+moe_status moe_permute_dispatch_local(moe_ctx* ctx, const moe_bf16* x, const int32_t* topk_idx,
+                                      int32_t* counts, int32_t* dest_row, int32_t* layout,
+                                      moe_bf16* xr, moe_stream stream);
 /* dx[t] = bf16( sum_{j kept} dxs[dest_row[t,j]]  (fp32, j order)
  *               + dx_acc[t] (fp32, optional) + dx_extra[t] (bf16, optional) ), one rounding. */
 moe_status moe_permute_bwd(moe_ctx* ctx, const moe_bf16* dxs, const int32_t* dest_row,

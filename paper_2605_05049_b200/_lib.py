@@ -66,8 +66,10 @@ _SIGS = {
     "moe_symm_alloc": [P, ctypes.c_size_t, ctypes.POINTER(P)],
     "moe_symm_free": [P, P],
     "moe_symm_fingerprint": [P, P],
+    "moe_ctx_device_bytes": [P, P, P, P],
     "moe_ctx_verify_symmetric": [P, P],
     "moe_migrate": [P, P, P, P, P, ctypes.c_size_t, P],
+    "moe_all_to_all": [P, P, P, ctypes.c_size_t, P],
     "moe_ctx_get_device_error": [P],
     "moe_ctx_set_sm_limits": [P, ctypes.c_int, ctypes.c_int],
     "moe_ctx_set_placement": [P, P],
@@ -79,6 +81,7 @@ _SIGS = {
     "moe_route": [P, P, P, P, P],
     "moe_route_bwd": [P, P, P, P, P, P, P],
     "moe_permute": [P, P, P, P, P, P, P],
+    "moe_permute_dispatch_local": [P, P, P, P, P, P, P, P],
     "moe_permute_bwd": [P, P, P, P, P, P, P],
     "moe_permute_bwd_router": [P, P, P, P, P, P, P, P, P],
     "moe_dispatch": [P, P, P, P, P, P],
@@ -198,6 +201,14 @@ def moe_migrate(ctx, old_placement, new_placement, src, dst, stream=None):
                                            _ptr(dst, name="dst"), per, _stream(stream)))
 
 
+def moe_all_to_all(ctx, send, recv, stream=None):
+    """send [EP, n] (local), recv [EP, n] symmetric, same dtype: recv chunk r on rank q = send
+    chunk q on rank r."""
+    per = send[0].numel() * send.element_size() if send.shape[0] else 0
+    _check("moe_all_to_all", _lib.moe_all_to_all(ctx.handle, _ptr(send, name="send"),
+                                                 _ptr(recv, name="recv"), per, _stream(stream)))
+
+
 def moe_load_imbalance(loads, placement, ep):
     """max / mean of the EP ranks' routed rows under a placement (migration trigger)."""
     E = len(loads)
@@ -262,6 +273,13 @@ class Context:
         """Releases the LAST symmetric allocation (LIFO; collective)."""
         _check("moe_symm_free", _lib.moe_symm_free(self._h, P(t.data_ptr())))
         self._views.pop()
+
+    def device_bytes(self):
+        """(heap bytes, heap bytes allocated, total device bytes of the ctx)."""
+        h, u, t = ctypes.c_size_t(0), ctypes.c_size_t(0), ctypes.c_size_t(0)
+        _check("moe_ctx_device_bytes", _lib.moe_ctx_device_bytes(
+            self._h, ctypes.byref(h), ctypes.byref(u), ctypes.byref(t)))
+        return h.value, u.value, t.value
 
     def fingerprint(self) -> bytes:
         out = ctypes.c_uint64(0)
@@ -336,6 +354,13 @@ def moe_permute(ctx, x, topk_idx, counts, dest_row, xs, stream=None):
     _check("moe_permute", _lib.moe_permute(
         ctx.handle, _ptr(x, BF16, "x"), _ptr(topk_idx, I32T, "topk_idx"), _ptr(counts, I32T, "counts"),
         _ptr(dest_row, I32T, "dest_row"), _ptr(xs, BF16, "xs"), _stream(stream)))
+
+
+def moe_permute_dispatch_local(ctx, x, topk_idx, counts, dest_row, layout, xr, stream=None):
+    _check("moe_permute_dispatch_local", _lib.moe_permute_dispatch_local(
+        ctx.handle, _ptr(x, BF16, "x"), _ptr(topk_idx, I32T, "topk_idx"),
+        _ptr(counts, I32T, "counts"), _ptr(dest_row, I32T, "dest_row"),
+        _ptr(layout, I32T, "layout"), _ptr(xr, BF16, "xr"), _stream(stream)))
 
 
 def moe_permute_bwd(ctx, dxs, dest_row, dx_acc, dx_extra, dx, stream=None):

@@ -48,6 +48,7 @@ struct moe_ctx {
   // fingerprint: every rank must allocate the same sizes in the same order (moe.h)
   std::vector<std::pair<size_t, size_t>> allocs;
   uint64_t fingerprint = 1469598103934665603ull;
+  size_t device_bytes = 0;        // every cudaMalloc of the ctx (heap incl.)
 };
 
 namespace {
@@ -194,6 +195,17 @@ int gemm_pair() {
   return v;
 }
 
+// TMA L2 eviction policies of the expert GEMMs (gemm.cu KParams::l2_hint bits); MOE_L2_HINT
+// overrides for measurements
+int l2_hint() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MOE_L2_HINT");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
 int pick_bn(int n) {
   if (n % 256 == 0) return 256;
   if (n % 128 == 0) return 128;
@@ -245,6 +257,13 @@ int64_t moe_layout_offset(const moe_shape* s, int field) {
   return -1;
 }
 
+// cudaMalloc that adds the size to the ctx's device-memory account (moe_ctx_device_bytes)
+cudaError_t ctx_malloc(moe_ctx* c, void* pp, size_t bytes) {
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(pp), bytes);
+  if (e == cudaSuccess) c->device_bytes += bytes;
+  return e;
+}
+
 moe_status moe_ctx_create(moe_ctx** out, const moe_shape* shape, int device, size_t symm_heap_bytes) {
   MOE_REQUIRE(out && shape_ok(shape));
   *out = nullptr;
@@ -264,26 +283,26 @@ moe_status moe_ctx_create(moe_ctx** out, const moe_shape* shape, int device, siz
   c->internal_bytes = ((c->flags_off + moe::kNumSlots * EP * 8) + 4095) / 4096 * 4096;
   c->heap_bytes = c->internal_bytes + (symm_heap_bytes + 255) / 256 * 256;
   c->heap_used = c->internal_bytes;
-  e = cudaMalloc(&c->heap, c->heap_bytes);
+  e = ctx_malloc(c, &c->heap, c->heap_bytes);
   if (e == cudaSuccess) e = cudaMemset(c->heap, 0, c->internal_bytes);
-  if (e == cudaSuccess) e = cudaMalloc(&c->d_err, 16);
+  if (e == cudaSuccess) e = ctx_malloc(c, &c->d_err, 16);
   if (e == cudaSuccess) e = cudaMemset(c->d_err, 0, 16);
   // [0] last-block counter, [1] counts ticket, [4..5] = uint64 collective epoch
-  if (e == cudaSuccess) e = cudaMalloc(&c->d_done, 32);
+  if (e == cudaSuccess) e = ctx_malloc(c, &c->d_done, 32);
   if (e == cudaSuccess) e = cudaMemset(c->d_done, 0, 32);
   const int64_t scratch = moe::permute_scratch_ints(shape->T_local, shape->k, shape->E);
-  if (e == cudaSuccess) e = cudaMalloc(&c->d_scratch, scratch * 4);
+  if (e == cudaSuccess) e = ctx_malloc(c, &c->d_scratch, scratch * 4);
   if (e == cudaSuccess) e = cudaMemset(c->d_scratch, 0, scratch * 4);   // incl. the block ticket
   const int64_t dscratch = moe::dedup_scratch_ints(shape->T_local, shape->ep_size);
-  if (e == cudaSuccess) e = cudaMalloc(&c->d_dedup_scratch, dscratch * 4);
+  if (e == cudaSuccess) e = ctx_malloc(c, &c->d_dedup_scratch, dscratch * 4);
   if (e == cudaSuccess) e = cudaMemset(c->d_dedup_scratch, 0, dscratch * 4);
-  if (e == cudaSuccess) e = cudaMalloc(&c->d_rows_T, 16);
+  if (e == cudaSuccess) e = ctx_malloc(c, &c->d_rows_T, 16);
   int32_t tl = static_cast<int32_t>(shape->T_local);
   if (e == cudaSuccess) e = cudaMemcpy(c->d_rows_T, &tl, 4, cudaMemcpyHostToDevice);
   c->Ep = (shape->E + 7) / 8 * 8;
   const int64_t Tl = shape->T_local > 0 ? shape->T_local : 1;
-  if (e == cudaSuccess) e = cudaMalloc(&c->d_dl_split, static_cast<size_t>(Tl) * 2 * c->Ep * 2);
-  if (e == cudaSuccess) e = cudaMalloc(&c->d_wr2, static_cast<size_t>(2) * c->Ep * shape->d * 2);
+  if (e == cudaSuccess) e = ctx_malloc(c, &c->d_dl_split, static_cast<size_t>(Tl) * 2 * c->Ep * 2);
+  if (e == cudaSuccess) e = ctx_malloc(c, &c->d_wr2, static_cast<size_t>(2) * c->Ep * shape->d * 2);
   // dW_r = x^T dl has K = T tokens and only E x d outputs: split K into S 128-row-aligned
   // token chunks (one K-grouped GEMM group each) so the GPU fills; partials summed in order.
   {
@@ -298,16 +317,16 @@ moe_status moe_ctx_create(moe_ctx** out, const moe_shape* shape, int device, siz
     }
     if (shape->T_local == 0) rows[0] = 0;
     c->n_split = static_cast<int>(S);
-    if (e == cudaSuccess) e = cudaMalloc(&c->d_split_rows, 16 * sizeof(int32_t));
+    if (e == cudaSuccess) e = ctx_malloc(c, &c->d_split_rows, 16 * sizeof(int32_t));
     if (e == cudaSuccess) e = cudaMemcpy(c->d_split_rows, rows, S * sizeof(int32_t), cudaMemcpyHostToDevice);
     if (e == cudaSuccess)
-      e = cudaMalloc(&c->d_dwr_part, static_cast<size_t>(S) * 2 * c->Ep * shape->d * sizeof(float));
+      e = ctx_malloc(c, &c->d_dwr_part, static_cast<size_t>(S) * 2 * c->Ep * shape->d * sizeof(float));
   }
   {
     std::vector<int32_t> ident(shape->E);
     for (int i = 0; i < shape->E; ++i) ident[i] = i;
-    if (e == cudaSuccess) e = cudaMalloc(&c->d_place, shape->E * sizeof(int32_t));
-    if (e == cudaSuccess) e = cudaMalloc(&c->d_expert_at, shape->E * sizeof(int32_t));
+    if (e == cudaSuccess) e = ctx_malloc(c, &c->d_place, shape->E * sizeof(int32_t));
+    if (e == cudaSuccess) e = ctx_malloc(c, &c->d_expert_at, shape->E * sizeof(int32_t));
     if (e == cudaSuccess)
       e = cudaMemcpy(c->d_place, ident.data(), shape->E * sizeof(int32_t), cudaMemcpyHostToDevice);
     if (e == cudaSuccess)
@@ -377,6 +396,15 @@ moe_status moe_symm_free(moe_ctx* c, void* ptr) {
   return MOE_OK;
 }
 
+moe_status moe_ctx_device_bytes(moe_ctx* c, size_t* heap_bytes, size_t* heap_used,
+                                size_t* total_bytes) {
+  MOE_REQUIRE(c);
+  if (heap_bytes) *heap_bytes = c->heap_bytes;
+  if (heap_used) *heap_used = c->heap_used;
+  if (total_bytes) *total_bytes = c->device_bytes;
+  return MOE_OK;
+}
+
 moe_status moe_symm_fingerprint(moe_ctx* c, uint64_t* out) {
   MOE_REQUIRE(c && out);
   *out = c->fingerprint;
@@ -435,6 +463,19 @@ moe_status moe_migrate(moe_ctx* c, const int32_t* old_place, const int32_t* new_
   CommArgs a = comm_args(c);
   return cuda_status(moe::launch_migrate(a, ml, src, heap_off(c, dst),
                                          static_cast<int64_t>(bytes_per_expert), st(s)));
+}
+
+moe_status moe_all_to_all(moe_ctx* c, const void* send, void* recv, size_t bytes_per_peer,
+                          moe_stream s) {
+  MOE_REQUIRE(c && send && recv && bytes_per_peer % 16 == 0);
+  if (!c->peers_ready) return MOE_ERR_NOT_READY;
+  const int64_t total = static_cast<int64_t>(bytes_per_peer) * c->s.ep_size;
+  if (!in_heap(c, recv, total)) return MOE_ERR_NOT_SYMMETRIC;
+  if (bytes_per_peer == 0) return MOE_OK;
+  if (set_device(c) != MOE_OK) return MOE_ERR_CUDA;
+  CommArgs a = comm_args(c);
+  return cuda_status(moe::launch_all_to_all(a, send, heap_off(c, recv),
+                                            static_cast<int64_t>(bytes_per_peer), st(s)));
 }
 
 moe_status moe_load_imbalance(const int64_t* loads, const int32_t* placement, int32_t E,
@@ -610,6 +651,18 @@ moe_status moe_permute(moe_ctx* c, const moe_bf16* x, const int32_t* topk_idx, i
                                          counts, dest_row, xs, c->d_scratch, st(s)));
 }
 
+moe_status moe_permute_dispatch_local(moe_ctx* c, const moe_bf16* x, const int32_t* topk_idx,
+                                      int32_t* counts, int32_t* dest_row, int32_t* layout,
+                                      moe_bf16* xr, moe_stream s) {
+  MOE_REQUIRE(c && x && topk_idx && counts && dest_row && layout && xr);
+  MOE_REQUIRE(c->s.ep_size == 1);
+  if (set_device(c) != MOE_OK) return MOE_ERR_CUDA;
+  const int64_t pad_max = static_cast<int64_t>(c->E_l) * (MOE_ALIGN_ROWS - 1);
+  return cuda_status(moe::launch_permute(x, topk_idx, c->s.T_local, c->s.d, c->s.E, c->s.k, c->C,
+                                         counts, dest_row, xr, c->d_scratch, st(s), layout,
+                                         c->d_expert_at, pad_max));
+}
+
 moe_status moe_permute_bwd(moe_ctx* c, const moe_bf16* dxs, const int32_t* dest_row,
                            const float* dx_acc, const moe_bf16* dx_extra, moe_bf16* dx, moe_stream s) {
   MOE_REQUIRE(c && dxs && dest_row && dx);
@@ -674,6 +727,7 @@ moe_status ffn_up(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows, int
   g1.pair = gemm_pair();
   g1.max_ctas = c->gemm_sms;
   g1.out = g_u_h; g1.ld_out = 3 * static_cast<int64_t>(f); g1.f = f;
+  g1.l2_hint = l2_hint();
   return cuda_status(moe::launch_grouped_gemm(g1, st(s)));
 }
 
@@ -699,6 +753,7 @@ moe_status ffn_down(moe_ctx* c, const int32_t* group_rows, int32_t n_groups, int
   if (sc) {
     g2.scatter = 1; g2.scatter_off = sc->off; g2.scatter_layout = sc->layout; g2.comm = sc->comm;
   }
+  g2.l2_hint = l2_hint();
   return cuda_status(moe::launch_grouped_gemm(g2, st(s)));
 }
 
@@ -740,6 +795,7 @@ moe_status ffn_bwd_dh(moe_ctx* c, const int32_t* group_rows, int32_t g0, int32_t
   a.pair = gemm_pair();
   a.max_ctas = c->gemm_sms;
   a.out = dgu; a.ld_out = 2 * F; a.aux = g_u_h; a.ld_aux = 3 * F; a.f = f;
+  a.l2_hint = l2_hint();
   return cuda_status(moe::launch_grouped_gemm(a, st(s)));
 }
 
@@ -774,6 +830,7 @@ moe_status ffn_bwd_dx(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows,
   if (sc) {  // dX rows go straight back to their source ranks (dispatch_bwd fused)
     b.scatter = 1; b.scatter_off = sc->off; b.scatter_layout = sc->layout; b.comm = sc->comm;
   }
+  b.l2_hint = l2_hint();
   MOE_TRY_CUDA(moe::launch_grouped_gemm(b, st(s)));
   // wgrad: dW_down[g] = dout_g^T H_g   [d, f]
   moe::GemmProblem w1;
@@ -788,6 +845,7 @@ moe_status ffn_bwd_dx(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows,
   w1.max_ctas = c->gemm_sms;
   w1.out = dw_down; w1.accumulate = accumulate;
   w1.n_fastest = w1.M > w1.N;   // keep the smaller operand slab re-read from L2
+  w1.l2_hint = l2_hint();
   MOE_TRY_CUDA(moe::launch_grouped_gemm(w1, st(s)));
   // wgrad: dW_gu[g] = dgu_g^T X_g   [2f, d]
   moe::GemmProblem w2;
@@ -802,6 +860,7 @@ moe_status ffn_bwd_dx(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows,
   w2.max_ctas = c->gemm_sms;
   w2.out = dw_gu; w2.accumulate = accumulate;
   w2.n_fastest = w2.M > w2.N;
+  w2.l2_hint = l2_hint();
   return cuda_status(moe::launch_grouped_gemm(w2, st(s)));
 }
 

@@ -37,7 +37,7 @@ constexpr uint64_t kTimeoutNs = 10ull * 1000 * 1000 * 1000;
 constexpr int kMaxE = 256;  // validated by the C-ABI (E <= 256)
 
 __device__ __forceinline__ uint64_t* peer_flag(const CommArgs& a, int q, int slot, int src) {
-  return reinterpret_cast<uint64_t*>(a.peers.base[q] + a.flags_off) + slot * a.ep + src;
+  return reinterpret_cast<uint64_t*>(peer_base(a, q) + a.flags_off) + slot * a.ep + src;
 }
 
 __device__ __forceinline__ int upper_bound_idx(const int32_t* arr, int n, int64_t v) {
@@ -104,14 +104,14 @@ __device__ void publish_counts(const CommArgs& a, const int32_t* counts,
   const int E = a.E, EP = a.ep;
   for (int i = threadIdx.x; i < EP * E; i += blockDim.x) {
     const int q = i / E, e = i % E;
-    int32_t* dst = reinterpret_cast<int32_t*>(a.peers.base[q] + a.countmat_off) +
+    int32_t* dst = reinterpret_cast<int32_t*>(peer_base(a, q) + a.countmat_off) +
                    (parity * EP + a.rank) * E + e;
     *dst = counts[e];
   }
   if (ntok)
     for (int i = threadIdx.x; i < EP * EP; i += blockDim.x) {
       const int q = i / EP, q2 = i % EP;
-      reinterpret_cast<int32_t*>(a.peers.base[q] + a.ntokmat_off)[(parity * EP + a.rank) * EP + q2] =
+      reinterpret_cast<int32_t*>(peer_base(a, q) + a.ntokmat_off)[(parity * EP + a.rank) * EP + q2] =
           ntok[q2];
     }
   // bar.sync orders the block's count stores before the lanes' st.release.sys (cumulative)
@@ -381,7 +381,7 @@ __global__ void forward_transfer_kernel(CommArgs a, int32_t* __restrict__ layout
       const int64_t within = r - sg.prefix[i];
       const int64_t row = sg.src_base[i] + within;
       const int64_t drow = sg.dst_base[i] + within;
-      uint4* dst = reinterpret_cast<uint4*>(a.peers.base[sg.dst_rank[i]] + dst_off + drow * row_bytes);
+      uint4* dst = reinterpret_cast<uint4*>(peer_base(a, sg.dst_rank[i]) + dst_off + drow * row_bytes);
       copy_part(dst, reinterpret_cast<const uint4*>(src + row * d), nvec, part, lane);
     } else {
       const int64_t t = w;
@@ -397,7 +397,7 @@ __global__ void forward_transfer_kernel(CommArgs a, int32_t* __restrict__ layout
         const float g = gates[t * a.k + j];
         const int q = a.place[e] / E_l;
         const int64_t drow = tb.dst[e] + (row - tb.off[e]);
-        uint4* dst = reinterpret_cast<uint4*>(a.peers.base[q] + dst_off + drow * row_bytes);
+        uint4* dst = reinterpret_cast<uint4*>(peer_base(a, q) + dst_off + drow * row_bytes);
         const float dot = dot_scale_row(reinterpret_cast<const uint4*>(dy + t * d),
                                         reinterpret_cast<const uint4*>(ys + static_cast<int64_t>(row) * d),
                                         dst, g, nvec, lane);
@@ -465,7 +465,7 @@ __global__ void reverse_transfer_kernel(CommArgs a, const int32_t* __restrict__ 
     const int64_t within = v - sg.prefix[i];
     const int64_t row = sg.src_base[i] + within;
     const int64_t srow = sg.dst_base[i] + within;
-    uint4* dst = reinterpret_cast<uint4*>(a.peers.base[sg.dst_rank[i]] + dst_off + srow * row_bytes);
+    uint4* dst = reinterpret_cast<uint4*>(peer_base(a, sg.dst_rank[i]) + dst_off + srow * row_bytes);
     copy_part(dst, reinterpret_cast<const uint4*>(src + row * d), nvec, part, lane);
   }
   signal_done(a, kSlotData, /*wait_after=*/true);
@@ -582,7 +582,7 @@ __global__ void dedup_forward_kernel(CommArgs a, int32_t* __restrict__ layout,
       const int32_t pq = __shfl_sync(0xffffffffu, pd, q);
       if (!((mask >> q) & 1u)) continue;
       const int64_t u = s_tok_base[q] + (pq - s_pair_base[q]);
-      char* base = a.peers.base[q];
+      char* base = peer_base(a, q);
       store_part(reinterpret_cast<uint4*>(base + tok_off + u * row_bytes), b, nvec, part, lane);
       if (MODE == 0 && part == 0 && lane < k) {
         const int32_t rl = (qj == q) ? rr : -1;
@@ -733,7 +733,7 @@ __global__ void dedup_reduce_kernel(CommArgs a, const int32_t* __restrict__ dlay
       for (int c = 0; c < kPartVec / 32; ++c)
         if (v0 + 32 * c < v1) acc_bf16x8(acc[c], ld_nc_v4(pr + v0 + 32 * c), wj);
     }
-    uint4* pdst = reinterpret_cast<uint4*>(a.peers.base[r] + part_off + prow * row_bytes);
+    uint4* pdst = reinterpret_cast<uint4*>(peer_base(a, r) + part_off + prow * row_bytes);
 #pragma unroll
     for (int c = 0; c < kPartVec / 32; ++c)
       if (v0 + 32 * c < v1)
@@ -741,7 +741,7 @@ __global__ void dedup_reduce_kernel(CommArgs a, const int32_t* __restrict__ dlay
               make_uint4(pack_bf16(acc[c][0], acc[c][1]), pack_bf16(acc[c][2], acc[c][3]),
                          pack_bf16(acc[c][4], acc[c][5]), pack_bf16(acc[c][6], acc[c][7])));
     if (MODE == 1 && part == 0 && lane < k)
-      reinterpret_cast<float*>(a.peers.base[r] + dgpart_off)[prow * k + lane] = dg_own[u * k + lane];
+      reinterpret_cast<float*>(peer_base(a, r) + dgpart_off)[prow * k + lane] = dg_own[u * k + lane];
   }
   signal_done(a, kSlotData, /*wait_after=*/true);
 }
@@ -791,9 +791,41 @@ __global__ void migrate_kernel(CommArgs a, MigrateList ml, const uint16_t* __res
     const int64_t nv = (nvec_e - v0) < kMigRowVec ? (nvec_e - v0) : kMigRowVec;
     const uint4* ps = reinterpret_cast<const uint4*>(
         reinterpret_cast<const char*>(src) + ml.src_slot[m] * bytes_per_expert) + v0;
-    uint4* pd = reinterpret_cast<uint4*>(a.peers.base[ml.dst_rank[m]] + dst_off +
+    uint4* pd = reinterpret_cast<uint4*>(peer_base(a, ml.dst_rank[m]) + dst_off +
                                          ml.dst_slot[m] * bytes_per_expert) + v0;
     copy_part(pd, ps, static_cast<int>(nv), 0, lane);
+  }
+  signal_done(a, kSlotData, /*wait_after=*/true);
+}
+
+// Equal-split all-to-all (config 5 of BASELINE.json; SPEC.md:476 transpose law): chunk q of
+// this rank's send buffer -> chunk `rank` of rank q's symmetric receive buffer.  The layout is
+// static, so there is no counts round: ONE launch of stores (rotated destination order: at any
+// moment the sources write to different receivers) + the data-slot completion flags.
+// Work item = one 2 KB part of one chunk (vectors of 16 bytes).
+__global__ void all_to_all_kernel(CommArgs a, const uint16_t* __restrict__ send, int64_t dst_off,
+                                  int64_t chunk_bytes) {
+  pdl_wait();
+  pdl_trigger();
+  a.epoch = load_epoch(a);
+  const int lane = threadIdx.x & 31;
+  const int64_t gwarp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int64_t nvec = chunk_bytes / 16;
+  const int64_t parts = (nvec + kPartVec - 1) / kPartVec;
+  const int64_t n_items = parts * a.ep;
+  for (int64_t w = gwarp; w < n_items; w += nwarps) {
+    // destination-major with rotation: items [i*parts, (i+1)*parts) go to rank (rank+1+i)%EP
+    const int i = static_cast<int>(w / parts);
+    const int64_t part = w - static_cast<int64_t>(i) * parts;
+    const int q = (a.rank + 1 + i) % a.ep;
+    const int64_t v0 = part * kPartVec;
+    const int nv = static_cast<int>((nvec - v0) < kPartVec ? (nvec - v0) : kPartVec);
+    const uint4* src = reinterpret_cast<const uint4*>(
+        reinterpret_cast<const char*>(send) + static_cast<int64_t>(q) * chunk_bytes) + v0;
+    uint4* dst = reinterpret_cast<uint4*>(peer_base(a, q) + dst_off +
+                                          static_cast<int64_t>(a.rank) * chunk_bytes) + v0;
+    copy_part(dst, src, nv, 0, lane);
   }
   signal_done(a, kSlotData, /*wait_after=*/true);
 }
@@ -853,6 +885,17 @@ cudaError_t launch_reverse_transfer(const CommArgs& a, const int32_t* layout, co
   // receive rows <= EP * T * k
   launch_k(reverse_transfer_kernel, dim3(transfer_blocks(a, a.T * a.k * a.ep)), dim3(512),
       transfer_smem(a), s, a, layout, src, dst_off);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_all_to_all(const CommArgs& a, const void* send, int64_t dst_off,
+                              int64_t chunk_bytes, cudaStream_t s) {
+  const int64_t items = a.ep * ((chunk_bytes / 16 + kPartVec - 1) / kPartVec);
+  int64_t b = a.blocks > 0 ? a.blocks : 2 * num_sms();
+  const int64_t need = (items + 15) / 16;     // 16 warps per block, one 2 KB part each
+  if (need < b) b = need;
+  launch_k(all_to_all_kernel, dim3(static_cast<unsigned>(b < 1 ? 1 : b)), dim3(512), 0, s, a,
+           static_cast<const uint16_t*>(send), dst_off, chunk_bytes);
   return cudaGetLastError();
 }
 

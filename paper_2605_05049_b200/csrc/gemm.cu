@@ -46,6 +46,9 @@ struct KParams {
   int64_t rows_cap;
   int64_t b_group_stride, b_split;
   int n_fastest;        // tile raster: 1 = n fastest (B slab re-read), 0 = m fastest
+  int l2_hint;          // TMA L2 policies: bit 0 = the re-read operand (A for m-fastest,
+                        // B for n-fastest) evict_last, bit 1 = the other evict_first,
+                        // bit 2 = TMA stores evict_first
   int direct_store;     // F32Rows only: output pitch not 16B-aligned -> plain stores
   void* out;
   int64_t ld_out;
@@ -283,6 +286,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      const uint64_t pol_keep = l2_policy_evict_last(), pol_stream = l2_policy_evict_first(),
+                     pol_norm = l2_policy_evict_normal();
+      // the operand the raster re-reads over time: A (m fastest) or B (n fastest)
+      const uint64_t pol_reread = (p.l2_hint & 1) ? pol_keep : pol_norm;
+      const uint64_t pol_other = (p.l2_hint & 2) ? pol_stream : pol_norm;
+      const uint64_t pol_a = p.n_fastest ? pol_other : pol_reread;
+      const uint64_t pol_b = p.n_fastest ? pol_reread : pol_other;
       for (int w = 0; w < n_work; ++w) {
         const Tile tl = decode_tile<KGROUPED, BN, TILE_M>(tile0 + w * tile_step, s_tile_prefix,
                                                           s_seg, s_rows, n_groups, p);
@@ -297,8 +307,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
           }
           auto load = [&](void* dst, const CUtensorMap* tm, int c0, int c1) {
-            if (PAIR == 2) tma_load_2d_pair(dst, tm, bar_addr, c0, c1);
-            else tma_load_2d(dst, tm, &full[stage], c0, c1);
+            const uint64_t pol = (tm == &tmA) ? pol_a : pol_b;
+            if (p.l2_hint) {
+              if (PAIR == 2) tma_load_2d_pair_hint(dst, tm, bar_addr, c0, c1, pol);
+              else tma_load_2d_hint(dst, tm, &full[stage], c0, c1, pol);
+            } else {
+              if (PAIR == 2) tma_load_2d_pair(dst, tm, bar_addr, c0, c1);
+              else tma_load_2d(dst, tm, &full[stage], c0, c1);
+            }
           };
           uint8_t* a_dst = sA + stage * C::A_BYTES;
           uint8_t* b_dst = sB + stage * C::B_BYTES;
@@ -384,6 +400,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t row_addr = smem_u32(sStage + ew * STG * kStageBox) + lane * 128;
     const void* box = sStage + ew * STG * kStageBox;
     int sbuf = 0;   // STG = 2: the staging box the next chunk uses
+    const uint64_t pol_st = l2_policy_evict_first();
     int acc = 0;
     uint32_t acc_phase = 0;
     constexpr int kArrive = 4 * PAIR;  // epilogue warps of a cluster
@@ -448,7 +465,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             stage_row(row_addr, lane, w);
             staging_release();
             if (lane == 0) {
-              tma_store_2d(&tmC, box, col + part * p.f, row0);
+              if (p.l2_hint & 4) tma_store_2d_hint(&tmC, box, col + part * p.f, row0, pol_st);
+              else tma_store_2d(&tmC, box, col + part * p.f, row0);
               bulk_commit();
             }
           }
@@ -480,7 +498,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               int r = 0;
               while (r + 1 < p.comm.ep && s_pre[(r + 1) * E_l + g] <= mi) ++r;
               const int64_t drow = s_soff[r * E_l + g] + (mi - s_pre[r * E_l + g]);
-              bulk_copy_s2g(p.comm.peers.base[r] + p.scatter_off + (drow * p.N + tl.n * BN + c0) * 2,
+              bulk_copy_s2g(peer_base(p.comm, r) + p.scatter_off + (drow * p.N + tl.n * BN + c0) * 2,
                             lin, 128);
               bulk_commit();
             }
@@ -489,7 +507,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             stage_row(row_addr, lane, w);
             staging_release();
             if (lane == 0) {
-              tma_store_2d(&tmC, box, tl.n * BN + c0, row0);
+              if (p.l2_hint & 4) tma_store_2d_hint(&tmC, box, tl.n * BN + c0, row0, pol_st);
+              else tma_store_2d(&tmC, box, tl.n * BN + c0, row0);
               bulk_commit();
             }
           }
@@ -537,7 +556,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             else stage_row(row_addr, lane, wu);
             staging_release();
             if (lane == 0) {
-              tma_store_2d(&tmC, box, col + part * p.f, row0);
+              if (p.l2_hint & 4) tma_store_2d_hint(&tmC, box, col + part * p.f, row0, pol_st);
+              else tma_store_2d(&tmC, box, col + part * p.f, row0);
               bulk_commit();
             }
           }
@@ -636,7 +656,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t epoch = *reinterpret_cast<volatile const uint64_t*>(a.epoch_ptr) + 1;
       __threadfence_system();
       for (int q = 0; q < a.ep; ++q)
-        st_release_sys(reinterpret_cast<uint64_t*>(a.peers.base[q] + a.flags_off) +
+        st_release_sys(reinterpret_cast<uint64_t*>(peer_base(a, q) + a.flags_off) +
                            kSlotData * a.ep + a.rank,
                        epoch);
     }
@@ -747,6 +767,7 @@ cudaError_t launch_impl(const GemmProblem& g, cudaStream_t stream) {
   kp.b_group_stride = g.b_group_stride;
   kp.b_split = g.b_split;
   kp.n_fastest = g.n_fastest;
+  kp.l2_hint = g.l2_hint;
   kp.out = g.out; kp.ld_out = g.ld_out;
   kp.aux = g.aux; kp.ld_aux = g.ld_aux;
   kp.bias = g.bias;

@@ -78,6 +78,7 @@ struct GemmProblem {
   int f = 0;
   int accumulate = 0;
   int n_fastest = 0;  // tile raster order: 1 = n fastest (re-read B), 0 = m fastest (re-read A)
+  int l2_hint = 0;    // TMA L2 eviction policies (gemm.cu KParams::l2_hint)
   int max_ctas = 0;   // SM budget (0 = all SMs); used to run a GEMM beside a transfer
   int pair = 1;       // 2: CTA-pair tiles (tcgen05 cta_group::2, M = 256), BN >= 128 only
   // kEpiBF16 only: fused reverse all-to-all (rows -> source ranks' symmetric buffer at
@@ -109,9 +110,13 @@ cudaError_t launch_sum_partials(const float* part, int S, int E, int Ep, int d, 
                                 int accumulate, cudaStream_t s);
 // scratch: int32 workspace of permute_scratch_ints(T,k,E) entries
 int64_t permute_scratch_ints(int64_t T, int k, int E);
+// layout != null: EP = 1 local path -- xs is then the 128-aligned receive buffer (rows placed
+// by slot, expert_at[slot] = expert, padding zeroed; pad_rows_max bounds the padding rows) and
+// the layout record is written, as moe_dispatch would
 cudaError_t launch_permute(const uint16_t* x, const int32_t* topk_idx, int64_t T, int d, int E,
                            int k, int64_t C, int32_t* counts, int32_t* dest_row, uint16_t* xs,
-                           int32_t* scratch, cudaStream_t s);
+                           int32_t* scratch, cudaStream_t s, int32_t* layout = nullptr,
+                           const int32_t* expert_at = nullptr, int64_t pad_rows_max = 0);
 cudaError_t launch_permute_bwd(const uint16_t* dxs, const int32_t* dest_row, const float* dx_acc,
                                const uint16_t* dx_extra, int64_t T, int d, int k, uint16_t* dx,
                                cudaStream_t s);
@@ -167,6 +172,18 @@ struct CommArgs {
 };
 enum { kSlotCounts = 0, kSlotData = 1, kNumSlots = 2 };
 
+// Heap base of rank q: a select chain over static indices, so the kernel-parameter copy of the
+// peer table is never indexed dynamically (that forced a 208-byte local-memory frame).
+#ifdef __CUDACC__
+__device__ __forceinline__ char* peer_base(const CommArgs& a, int q) {
+  char* p = a.peers.base[0];
+#pragma unroll
+  for (int i = 1; i < MOE_MAX_EP; ++i)
+    if (q == i) p = a.peers.base[i];
+  return p;
+}
+#endif
+
 // Each collective is ONE launch that returns only when this rank's destination buffer is
 // complete (the last block waits for every peer's flag).  dst_off = byte offset of the
 // destination buffer inside every rank's symmetric heap.
@@ -210,6 +227,9 @@ cudaError_t launch_dedup_reduce(const CommArgs& a, int mode, const int32_t* dlay
                                 const int32_t* rlist, const float* glist, const uint16_t* rows,
                                 const float* dg_own, int64_t part_off, int64_t dgpart_off,
                                 cudaStream_t s);
+// equal-split all-to-all: chunk q of send -> chunk rank of rank q's buffer at dst_off
+cudaError_t launch_all_to_all(const CommArgs& a, const void* send, int64_t dst_off,
+                              int64_t chunk_bytes, cudaStream_t s);
 // NEXT-2 expert migration: moves of this rank's experts (old local slot -> new owner rank
 // and local slot); collective, see migrate_kernel
 struct MigrateList {

@@ -23,10 +23,16 @@ __device__ __forceinline__ int expert_of(const int32_t* idx, int64_t a, int64_t 
 // Pass 1: per-chunk expert histogram; the last block to finish (ticket) then runs pass 2:
 // per-expert exclusive scan over chunks (in place -> chunk base), capacity clamp, counts and
 // off = exclusive scan of counts.  One launch instead of two.
+// With `layout` (the EP = 1 local path, moe_permute_dispatch_local) the last block also writes
+// the layout record moe_dispatch would write -- counts_all (= counts), the rows and the
+// 128-aligned segment base of every local slot (expert_at[slot] = expert) -- and
+// shift[e] = seg_base[slot of e] - off[e], the send-row -> receive-row offset of expert e.
 __global__ void hist_scan_kernel(const int32_t* __restrict__ idx, int64_t T, int k, int E,
                                  int64_t C, int32_t* __restrict__ chunk_hist /*[nchunks][E]*/,
                                  int32_t* __restrict__ counts, int32_t* __restrict__ off,
-                                 int32_t* __restrict__ ticket) {
+                                 int32_t* __restrict__ ticket, int32_t* __restrict__ layout,
+                                 const int32_t* __restrict__ expert_at,
+                                 int32_t* __restrict__ shift) {
   pdl_wait();
   pdl_trigger();
   extern __shared__ int32_t s_hist[];   // [E]
@@ -78,6 +84,19 @@ __global__ void hist_scan_kernel(const int32_t* __restrict__ idx, int64_t T, int
     }
     off[E] = run;
     *ticket = 0;   // for the next call (stream-ordered)
+    if (layout) {
+      int32_t seg = 0;
+      for (int sl = 0; sl < E; ++sl) {
+        const int e = expert_at[sl];
+        const int32_t rows = s_hist[e];
+        layout[e] = rows;                       // counts_all[0][e]
+        layout[E + sl] = rows;                  // expert_rows[slot]
+        layout[2 * E + sl] = seg;               // seg_base[slot]
+        shift[e] = seg - off[e];
+        seg += (rows + MOE_ALIGN_ROWS - 1) / MOE_ALIGN_ROWS * MOE_ALIGN_ROWS;
+      }
+      layout[3 * E] = seg;
+    }
   }
 }
 
@@ -116,28 +135,55 @@ __global__ void rank_kernel(const int32_t* __restrict__ idx, int64_t T, int k, i
 }
 
 // Pass 3: warp per token; read x_t once (4 x 16 B in flight per lane), write each kept row.
+// KMAX >= k is a compile-time bound, so the row list lives in registers (static indices).
+// With shift (EP = 1 local path) row dest_row + shift[e] of the 128-aligned receive layout is
+// written instead, and warps past the tokens zero the padding rows of every segment.
+template <int KMAX>
 __global__ void scatter_kernel(const uint16_t* __restrict__ x, const int32_t* __restrict__ dest_row,
-                               int64_t T, int d, int k, uint16_t* __restrict__ xs) {
+                               const int32_t* __restrict__ idx, const int32_t* __restrict__ shift,
+                               const int32_t* __restrict__ layout, int64_t T, int d, int k, int E,
+                               uint16_t* __restrict__ xs) {
   pdl_wait();
   pdl_trigger();
   const int lane = threadIdx.x & 31;
   const int64_t t = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  if (t >= T) return;
-  int32_t rows[32];
-  int nk = 0;
-  for (int j = 0; j < k; ++j) {
-    const int32_t r = dest_row[t * k + j];
-    if (r >= 0) rows[nk++] = r;
-  }
-  if (nk == 0) return;
   const int nvec = d / 8;  // 16-byte vectors per row
+  if (t >= T) {
+    if (!shift) return;
+    // padding rows: warp (t - T) zeroes padding row number (t - T) of the whole buffer
+    const int64_t pr = t - T;
+    int64_t base = 0;
+    for (int sl = 0; sl < E; ++sl) {
+      const int32_t rows = layout[E + sl], seg = layout[2 * E + sl];
+      const int32_t pad = layout[2 * E + sl + 1] - seg - rows;
+      if (pr < base + pad) {
+        uint4* z = reinterpret_cast<uint4*>(xs + (static_cast<int64_t>(seg) + rows + (pr - base)) * d);
+        for (int v = lane; v < nvec; v += 32) z[v] = make_uint4(0u, 0u, 0u, 0u);
+        return;
+      }
+      base += pad;
+    }
+    return;
+  }
+  int32_t rows[KMAX];
+  bool any = false;
+#pragma unroll
+  for (int j = 0; j < KMAX; ++j) {
+    int32_t r = j < k ? dest_row[t * k + j] : -1;
+    if (shift && r >= 0) r += shift[idx[t * k + j]];
+    rows[j] = r;
+    any |= r >= 0;
+  }
+  if (!any) return;
   const uint4* src = reinterpret_cast<const uint4*>(x + t * d);
   for (int v0 = lane; v0 < nvec; v0 += 128) {   // 4 loads in flight per lane
     uint4 val[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u)
       if (v0 + 32 * u < nvec) val[u] = ld_nc_v4(src + v0 + 32 * u);
-    for (int j = 0; j < nk; ++j) {
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) {
+      if (rows[j] < 0) continue;
       uint4* dst = reinterpret_cast<uint4*>(xs + static_cast<int64_t>(rows[j]) * d);
 #pragma unroll
       for (int u = 0; u < 4; ++u)
@@ -145,7 +191,6 @@ __global__ void scatter_kernel(const uint16_t* __restrict__ x, const int32_t* __
     }
   }
 }
-
 
 // y[t] = bf16( sum_{j kept} g_{t,j} rows[dest_row[t,j]] (j order) + extra_f32[t] + extra_bf16[t] )
 // One warp per token.  KMAX >= k is a compile-time bound so the row list stays in registers
@@ -456,23 +501,27 @@ cudaError_t launch_sum_partials(const float* part, int S, int E, int Ep, int d, 
 
 int64_t permute_scratch_ints(int64_t T, int k, int E) {
   const int64_t nchunks = (T * k + kChunk - 1) / kChunk;
-  return (nchunks > 0 ? nchunks : 1) * E + E + 1 + 1;   // chunk bases, off, block ticket
+  // chunk bases, off [E+1], block ticket, shift [E] (EP = 1 local path)
+  return (nchunks > 0 ? nchunks : 1) * E + E + 1 + 1 + E;
 }
 
 cudaError_t launch_permute(const uint16_t* x, const int32_t* topk_idx, int64_t T, int d, int E,
                            int k, int64_t C, int32_t* counts, int32_t* dest_row, uint16_t* xs,
-                           int32_t* scratch, cudaStream_t s) {
+                           int32_t* scratch, cudaStream_t s, int32_t* layout,
+                           const int32_t* expert_at, int64_t pad_rows_max) {
   const int64_t nA = T * k;
   const int nchunks = static_cast<int>((nA + kChunk - 1) / kChunk);
   int32_t* chunk_hist = scratch;
   int32_t* off = scratch + static_cast<int64_t>(nchunks > 0 ? nchunks : 1) * E;
+  int32_t* ticket = off + E + 1;
+  int32_t* shift = ticket + 1;
   if (nchunks == 0) {
     cudaMemsetAsync(counts, 0, sizeof(int32_t) * E, s);
+    if (layout) cudaMemsetAsync(layout, 0, sizeof(int32_t) * (3 * E + 1), s);
     return cudaGetLastError();
   }
-  int32_t* ticket = off + E + 1;
   launch_k(hist_scan_kernel, dim3(nchunks), dim3(kChunk), E * sizeof(int32_t), s, topk_idx, T, k,
-           E, C, chunk_hist, counts, off, ticket);
+           E, C, chunk_hist, counts, off, ticket, layout, expert_at, layout ? shift : nullptr);
   const size_t smem = static_cast<size_t>(32) * E * sizeof(int32_t);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -483,8 +532,17 @@ cudaError_t launch_permute(const uint16_t* x, const int32_t* topk_idx, int64_t T
       dest_row);
   const int threads = 256;
   if (!xs) return cudaGetLastError();   // indices only (the dedup dispatch reads x directly)
-  launch_k(scatter_kernel, dim3(static_cast<unsigned>((T * 32 + threads - 1) / threads)),
-      dim3(threads), 0, s, x, dest_row, T, d, k, xs);
+  const int64_t warps = T + (layout ? pad_rows_max : 0);
+  const dim3 grid(static_cast<unsigned>((warps * 32 + threads - 1) / threads));
+  const int32_t* sh = layout ? shift : nullptr;
+#define MOE_SC(K_) launch_k(scatter_kernel<K_>, grid, dim3(threads), 0, s, x, dest_row, topk_idx, \
+                            sh, layout, T, d, k, E, xs)
+  if (k <= 2) MOE_SC(2);
+  else if (k <= 4) MOE_SC(4);
+  else if (k <= 8) MOE_SC(8);
+  else if (k <= 16) MOE_SC(16);
+  else MOE_SC(32);
+#undef MOE_SC
   return cudaGetLastError();
 }
 

@@ -95,6 +95,7 @@ class MoELayer:
             per_expert = 3 * d * f * (2 + f32b)            # bf16 weights + fp32 gradients
             heap += 2 * (self.E_l * per_expert + 4 * 256)
             heap += 2 * (self.E_l * int(expert_state_bytes)) + 64 * 1024
+        torch_before = torch.cuda.memory_allocated(self.device)
         self.ctx = L.Context(self.shape, device, heap)
         if dims.ep_size > 1:
             handles = _all_gather_bytes(self.ctx.export_handle(), group)
@@ -164,6 +165,8 @@ class MoELayer:
             self.dw_down_s = torch.empty((1, d, fs), dtype=f32, device=dev)
         self.w_r = self.w_gu = self.w_down = self.bias = None
         self.w_gu_s = self.w_down_s = None
+        # device memory this instance allocated (torch tensors + the ctx's allocations)
+        self.torch_bytes = torch.cuda.memory_allocated(self.device) - torch_before
 
     # ------------------------------------------------------------------ weights
     def set_weights(self, w_r, w_gu, w_down, bias=None, w_gu_s=None, w_down_s=None):
@@ -185,6 +188,9 @@ class MoELayer:
             self.w_down_s = w_down_s.to(dev, torch.bfloat16).contiguous()
 
     # ------------------------------------------------------------------ forward
+    # EP = 1: moe_permute_dispatch_local (no send-layout copy, no transfer); False = the
+    # general permute + dispatch path (tests compare the two)
+    local_fast_path = True
     # per-phase CUDA-event markers (bench.py --breakdown); off by default
     marks = None
     # SMs given to an all-to-all that runs beside a GEMM (the GEMM gets the rest).  Measured on
@@ -240,6 +246,18 @@ class MoELayer:
         self._mark("F0+F1 router,route")
         if self.dedup:
             return self._forward_dedup(x)
+        if self.dims.ep_size == 1 and self.local_fast_path:
+            # EP = 1 is local only: the permute writes the receive layout directly
+            L.moe_permute_dispatch_local(c, x, self.topk_idx, self.counts, self.dest_row,
+                                         self.layout, self.xr)
+            self._mark("F2+F3 permute (local)")
+            y_extra = None
+            if self.fs:
+                L.moe_expert_ffn(c, x, self.rows_T, 1, T, self.fs, self.w_gu_s, self.w_down_s,
+                                 self.g_u_h_s, self.y_s)
+                y_extra = self.y_s
+                self._mark("F4s shared ffn")
+            return self._forward_reverse(y_extra)
         L.moe_permute(c, x, self.topk_idx, self.counts, self.dest_row, self.xs)
         self._mark("F2 permute")
         y_extra = None
@@ -473,6 +491,17 @@ class MoELayer:
     # more than 10 % above the mean
     rebalance_threshold = 1.10
 
+    def memory_account(self):
+        """Device bytes held by this layer instance (measured: torch allocations made by the
+        constructor + every allocation of the libmoe ctx) and the part that is the saved expert
+        activations Eq. 4 counts per token-slot as 3 d_ffn + d_model (reading
+        R9): xr [R, d] and g_u_h [R, 3f] for R = moe_recv_rows_max receive rows."""
+        heap, used, ctx_total = self.ctx.device_bytes()
+        saved = self.xr.numel() * 2 + self.g_u_h.numel() * 2
+        return {"torch_bytes": int(self.torch_bytes), "ctx_bytes": int(ctx_total),
+                "total_bytes": int(self.torch_bytes + ctx_total), "heap_bytes": int(heap),
+                "saved_expert_activation_bytes": int(saved), "recv_rows": int(self.R)}
+
     def imbalance(self, loads=None):
         """max / mean of the EP ranks' routed rows over the observed loads (libmoe)."""
         loads = self.loads if loads is None else loads
@@ -579,6 +608,8 @@ class MoELayer:
         if fwd:
             # router GEMM, route, permute (3), dispatch (1 fused launch), ffn (2), combine (2)
             n += 1 + 1 + 3 + 1 + 2 + 2 + (2 if self.fs else 0)
+            if self.dims.ep_size == 1 and self.local_fast_path:
+                n -= 1                     # no dispatch launch (the permute writes xr)
         if bwd:
             # combine_bwd (1), ffn_bwd (4), dispatch_bwd (1), route_bwd,
             # router bwd (hi/lo split, split-K dW_r GEMM, partial sum; k = 1 adds the

@@ -101,6 +101,28 @@ class PipelineStack:
         self._share(l)
         return moved
 
+    def memory_report(self):
+        """Per-stage device memory of this rank against PAPER.md Eq. 4 (1F1B, stage i holds
+        PP - i in-flight micro-batches): for every local layer the number of
+        activation contexts, the measured bytes of each (MoELayer.memory_account), and Eq. 4's
+        expert-activation term for one micro-batch on this rank, 2 (b/M) s k / EP (3 d_ffn +
+        d_model) bytes = 2 T_local k (3 f + d) (reading R19: the attention terms do not exist
+        in an MoE-only stack)."""
+        d0 = self.layers[0][0].dims
+        eq4_term = 2 * d0.T_local * d0.k * (3 * d0.f + d0.d)
+        layers = []
+        for slots in self.layers:
+            acc = [s.memory_account() for s in slots]
+            layers.append({"n_slots": len(slots),
+                           "slot_total_bytes": [a["total_bytes"] for a in acc],
+                           "saved_expert_activation_bytes": [a["saved_expert_activation_bytes"]
+                                                             for a in acc]})
+        return {"stage": self.stage, "pp": self.pp, "in_flight_bound": min(self.pp - self.stage,
+                                                                            self.M),
+                "eq4_expert_activation_bytes_per_microbatch": eq4_term,
+                "stage_bytes": sum(sum(l["slot_total_bytes"]) for l in layers),
+                "layers": layers}
+
     def grads(self, l):
         s0 = self.layers[l][0]
         return s0.dw_r, s0.dw_gu, s0.dw_down

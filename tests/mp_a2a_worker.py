@@ -50,7 +50,7 @@ def main():
     E_l = E // ep
     shape = L.make_shape(T_r, d, E, k, 128, 0, 0.0, ep, rank)
     R = L.moe_recv_rows_max(shape)
-    ctx = L.Context(shape, local, 2 * R * d * 2 + 2 * T_r * k * d * 2 + 4 * 4096)
+    ctx = L.Context(shape, local, 2 * R * d * 2 + 2 * T_r * k * d * 2 + ep * 3 * 128 * 16 + 8 * 4096)
     ctx.open_peers(_all_gather_bytes(ctx.export_handle()))
     xr = ctx.symm_empty((R, d), torch.bfloat16)
     xr2 = ctx.symm_empty((R, d), torch.bfloat16)
@@ -123,6 +123,20 @@ def main():
         used = int(layout2[ep * E + E_l + E_l].item())
         checks[f"{tag}_ranges"] = bool(torch.equal(layout2, layout) and
                                        torch.equal(xr2[:used], xr[:used]))
+    # moe_all_to_all (static equal splits, config 5): the transpose law against the oracle's
+    # brute-force flat_all_to_all on origin-encoded chunks, twice (epoch reuse)
+    n_chunk = 3 * 128
+    send = encoded_rows(rank, ep * n_chunk, 8).reshape(ep, n_chunk * 8).cuda()
+    ra = ctx.symm_empty((ep, n_chunk * 8), torch.bfloat16)
+    allsend = [encoded_rows(r, ep * n_chunk, 8).reshape(-1).float().numpy() for r in range(ep)]
+    want = ref.flat_all_to_all(allsend)[rank]
+    ok = True
+    for _ in range(2):
+        sync()
+        L.moe_all_to_all(ctx, send, ra)
+        torch.cuda.synchronize()
+        ok &= bool(np.array_equal(ra.float().cpu().numpy().reshape(-1), want))
+    checks["static_all_to_all"] = ok
     st = ctx.device_error()
     flags = torch.tensor([int(all(checks.values())), st], device="cuda")
     allf = mp_common.gather(flags)

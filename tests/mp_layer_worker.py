@@ -30,6 +30,11 @@ CASES = {
     "drops": synth.MoEConfig("drops", T=1024, d=128, E=8, k=2, f=256, cf=0.5),
     # one expert per rank at nproc 4 (the Mixtral EP=8 layout, E_l = 1, on 4 GPUs)
     "el1": synth.MoEConfig("el1", T=2048, d=512, E=4, k=2, f=1024, cf=1.25),
+    # expert collapse: a strong Zipf bias sends every token to two experts, so
+    # most ranks receive no rows at all (empty GEMM groups) and send everything away
+    "collapse": synth.MoEConfig("collapse", T=512, d=128, E=8, k=2, f=256, cf=0.0, zipf_s=8.0),
+    # T_local = 0 on every rank: the collectives still run (include/moe.h)
+    "empty": synth.MoEConfig("empty", T=0, d=128, E=8, k=2, f=256, cf=1.25, E_s=1),
 }
 
 
@@ -136,6 +141,19 @@ def main():
     flags = torch.tensor([st, int(repeat_ok and graph_ok and state_ok)], device="cuda")
     allflags = gather(flags)
     if rank != 0:
+        dist.barrier()
+        dist.destroy_process_group()
+        return
+    if cfg.T == 0:
+        zero = all(bool((t == 0).all()) for k in ("dw_gu", "dw_down", "dw_r", "dw_gu_s", "dw_down_s")
+                   for t in g[k])
+        lay0 = all(int(t.abs().sum()) == 0 for t in g["layout"])
+        res = {"config": cfg.name, "ep": ep, "device_status": [int(f[0]) for f in allflags],
+               "repeat_bitwise": [bool(f[1]) for f in allflags], "zero_grads": zero,
+               "empty_layout": lay0}
+        res["ok"] = (zero and lay0 and all(int(f[0]) == 0 for f in allflags) and
+                     all(bool(f[1]) for f in allflags))
+        print(json.dumps(res), flush=True)
         dist.barrier()
         dist.destroy_process_group()
         return

@@ -118,6 +118,9 @@ def main():
                   torch.equal(plain.dw_r, stack.grads(0)[0])]
     direct = all(dflag)
     plain.close()
+    # PAPER.md Eq. 4 per-stage memory account (measured bytes of every activation context)
+    mem_all = [None] * world
+    dist.all_gather_object(mem_all, stack.memory_report())
     # gather: [rank][local layer][m] tensors
     keys = ["x", "y", "logits", "topk", "dest", "dy", "dx"]
     G = {k: [[gather(rec[(l, m)][k]) for m in range(M)] for l in range(per)] for k in keys}
@@ -174,12 +177,35 @@ def main():
                 errs_norm[f"dWd{g}.0"] = float(np.linalg.norm(f64(dW[l][2][r][el]).T) /
                                                max(np.linalg.norm(dWd[x]), 1e-30))
         errs[f"dWr{g}"] = rel_err(sum(f64(dW[l][0][r]) for r in rs).T, dWr)
+    # Eq. 4: stage i keeps PP - i in-flight micro-batches (min with M); the measured memory
+    # difference between the first and last stage is exactly (PP - 1) L/PP activation contexts
+    # (PAPER.md:334-341 Delta M); each context saves 2 R (3f + d) bytes of expert activations
+    # for R = recv_rows_max >= Eq. 4's 2 T_local k (3f + d) (the capacity / alignment slack)
+    mem_ok = True
+    for mr in mem_all:
+        mem_ok &= all(l["n_slots"] == mr["in_flight_bound"] for l in mr["layers"])
+        mem_ok &= mr["in_flight_bound"] == min(pp - mr["stage"], M)
+        for l in mr["layers"]:
+            mem_ok &= all(v >= mr["eq4_expert_activation_bytes_per_microbatch"]
+                          for v in l["saved_expert_activation_bytes"])
+    first = [mr for mr in mem_all if mr["stage"] == 0]
+    last = [mr for mr in mem_all if mr["stage"] == pp - 1]
+    slot_b = first[0]["layers"][0]["slot_total_bytes"][-1]       # a non-owner context
+    dM = first[0]["stage_bytes"] - last[0]["stage_bytes"]
+    if pp > 1 and M >= pp:
+        mem_ok &= dM == (pp - 1) * per * slot_b
+    eq4 = first[0]["eq4_expert_activation_bytes_per_microbatch"]
+    checks["eq4_memory"] = bool(mem_ok)
+    res_mem = {"stage_bytes": [mr["stage_bytes"] for mr in mem_all],
+               "delta_M_measured": dM, "delta_M_eq4_expert_term": (pp - 1) * per * eq4,
+               "context_bytes": slot_b,
+               "saved_over_eq4": first[0]["layers"][0]["saved_expert_activation_bytes"][0] / eq4}
     worst = max(errs, key=errs.get)
     checks["direct_layer0"] = all(bool(t.item()) for t in dflags)
     checks["graph_replay"] = all(bool(t.item()) for t in gflags)
     res = {"pp": pp, "ep": ep, "migrated": bool(args.migrate), "layers": Lyr, "micro": M, "checks": checks,
            "device_status": [int(t.item()) for t in st], "worst": [worst, errs[worst]],
-           "schedule_stage0": stack.ops if stage == 0 else None}
+           "schedule_stage0": stack.ops if stage == 0 else None, "memory": res_mem}
     res["ok"] = (all(checks.values()) and all(v < TOL for v in errs.values()) and
                  all(v == 0 for v in res["device_status"]))
     if not res["ok"]:

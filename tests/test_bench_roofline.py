@@ -22,7 +22,7 @@ def fake_layer(EP, E, T_r, k, dedup=None, ntok=None):
     return lay
 
 
-PEAKS = {"bf16_sustained": 1000.0, "hbm": 5000.0}
+PEAKS = {"bf16": 1000.0, "bf16_sustained": 800.0, "hbm": 5000.0}
 
 
 @pytest.mark.parametrize("EP", [1, 2, 4, 8])
@@ -58,3 +58,15 @@ def test_dedup_roofline_uses_pair_rows_on_nvlink():
     d_hbm = (2 * (T_r * row + recv * row) + (T_r * row + send * row)
              - 2 * (T_r * row + send * row)) / bh
     assert ded["serial_ms"] - plain["serial_ms"] == pytest.approx((d_nvl + d_hbm) * 1e3, rel=1e-9)
+
+
+def test_sustained_variant_uses_the_sustained_peak():
+    E, d, f, k, T_r = 8, 4096, 14336, 2, 8192
+    cfg = types.SimpleNamespace(E=E, d=d, f=f, k=k, E_s=0)
+    lay = fake_layer(1, E, T_r, k)
+    burst = bench.layer_roofline(lay, cfg, PEAKS)
+    sus = bench.layer_roofline(lay, cfg, PEAKS, sustained=True)
+    gemm = (6 * T_r * d * E + 18 * T_r * k * d * f)
+    hbm = 4 * (T_r * 2 * d + T_r * k * 2 * d) / 5000e9
+    assert burst["serial_ms"] == pytest.approx((gemm / 1000e12 + hbm) * 1e3, rel=1e-12)
+    assert sus["serial_ms"] == pytest.approx((gemm / 800e12 + hbm) * 1e3, rel=1e-12)

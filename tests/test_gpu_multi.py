@@ -18,7 +18,7 @@ import torch
 
 pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-CONFIGS = ["tiny", "mixtral_small", "dsmoe_small", "v3_small_zipf", "drops"]
+CONFIGS = ["tiny", "mixtral_small", "dsmoe_small", "v3_small_zipf", "drops", "collapse", "empty"]
 
 
 def n_gpus():
@@ -47,6 +47,8 @@ def run_worker(nproc, config, port, extra=(), env=None):
 @pytest.mark.parametrize("nproc", [2, 4, 8])
 @pytest.mark.parametrize("config", CONFIGS)
 def test_layer_ep_parity(nproc, config):
+    """Every config at EP = 2/4/8 incl. expert collapse (ranks that receive nothing) and
+    T_local = 0 on every rank (the collectives still run; gradients exactly zero)."""
     """Fused path (GEMM epilogues store rows straight into peers' buffers)."""
     need_gpu(nproc)
     res = run_worker(nproc, config, 29500 + nproc * 10 + CONFIGS.index(config))
