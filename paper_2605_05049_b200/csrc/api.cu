@@ -49,6 +49,7 @@ struct moe_ctx {
   std::vector<std::pair<size_t, size_t>> allocs;
   uint64_t fingerprint = 1469598103934665603ull;
   size_t device_bytes = 0;        // every cudaMalloc of the ctx (heap incl.)
+  int32_t* d_sched = nullptr;     // [2] grouped-GEMM tile counter + done counter (zero at rest)
 };
 
 namespace {
@@ -66,6 +67,8 @@ moe_status cuda_status(cudaError_t e) {
     cudaError_t e_ = (expr);                               \
     if (e_ != cudaSuccess) return cuda_status(e_);         \
   } while (0)
+// token-row buffers ([T_local, ...], [T_local*k, ...]) may be NULL when T_local == 0
+#define TOKP(p) ((p) != nullptr || c->s.T_local == 0)
 #define MOE_REQUIRE(cond)                                  \
   do {                                                     \
     if (!(cond)) return MOE_ERR_INVALID_ARG;               \
@@ -195,15 +198,15 @@ int gemm_pair() {
   return v;
 }
 
-// TMA L2 eviction policies of the expert GEMMs (gemm.cu KParams::l2_hint bits); MOE_L2_HINT
-// overrides for measurements
-int l2_hint() {
+// the ctx's dynamic tile-scheduler counters (MOE_GEMM_SCHED=0: the static schedule, for
+// measurements)
+int* gemm_sched(const moe_ctx* c) {
   static int v = -1;
   if (v < 0) {
-    const char* e = getenv("MOE_L2_HINT");
-    v = e ? atoi(e) : 0;
+    const char* e = getenv("MOE_GEMM_SCHED");
+    v = (e && e[0] == '0') ? 0 : 1;
   }
-  return v;
+  return v ? c->d_sched : nullptr;
 }
 
 int pick_bn(int n) {
@@ -286,6 +289,8 @@ moe_status moe_ctx_create(moe_ctx** out, const moe_shape* shape, int device, siz
   e = ctx_malloc(c, &c->heap, c->heap_bytes);
   if (e == cudaSuccess) e = cudaMemset(c->heap, 0, c->internal_bytes);
   if (e == cudaSuccess) e = ctx_malloc(c, &c->d_err, 16);
+  if (e == cudaSuccess) e = ctx_malloc(c, &c->d_sched, 16);
+  if (e == cudaSuccess) e = cudaMemset(c->d_sched, 0, 16);
   if (e == cudaSuccess) e = cudaMemset(c->d_err, 0, 16);
   // [0] last-block counter, [1] counts ticket, [4..5] = uint64 collective epoch
   if (e == cudaSuccess) e = ctx_malloc(c, &c->d_done, 32);
@@ -545,6 +550,7 @@ moe_status moe_ctx_destroy(moe_ctx* c) {
     if (c->peer_opened[q]) cudaIpcCloseMemHandle(c->peer_base[q]);
   cudaFree(c->heap);
   cudaFree(c->d_err);
+  cudaFree(c->d_sched);
   cudaFree(c->d_done);
   cudaFree(c->d_scratch);
   cudaFree(c->d_dedup_scratch);
@@ -562,9 +568,10 @@ moe_status moe_ctx_destroy(moe_ctx* c) {
 // ---------------------------------------------------------------- F0 / B0
 moe_status moe_router_logits(moe_ctx* c, const moe_bf16* x, const moe_bf16* w_r,
                              const float* bias, float* logits, moe_stream s) {
-  MOE_REQUIRE(c && x && w_r && logits);
+  MOE_REQUIRE(c && TOKP(x) && w_r && TOKP(logits));
   if (c->s.T_local == 0) return MOE_OK;
   moe::GemmProblem g;
+  g.sched = gemm_sched(c);
   g.epi = moe::kEpiF32Rows;
   const int E = c->s.E;
   g.BN = E <= 16 ? 16 : E <= 64 ? 64 : E <= 128 ? 128 : 256;
@@ -581,7 +588,7 @@ moe_status moe_router_logits(moe_ctx* c, const moe_bf16* x, const moe_bf16* w_r,
 moe_status moe_router_logits_bwd(moe_ctx* c, const moe_bf16* x, const moe_bf16* w_r,
                                  const float* dlogits, float* dx_router, float* dw_r,
                                  int accumulate, moe_stream s) {
-  MOE_REQUIRE(c && x && w_r && dlogits && (dx_router || dw_r));
+  MOE_REQUIRE(c && TOKP(x) && w_r && TOKP(dlogits) && (dx_router || dw_r));
   const int64_t T = c->s.T_local;
   const int d = c->s.d, E = c->s.E, Ep = c->Ep;
   if (T == 0) {
@@ -593,6 +600,7 @@ moe_status moe_router_logits_bwd(moe_ctx* c, const moe_bf16* x, const moe_bf16* 
   if (dx_router) {  // dx_router[T, d] = [hi | lo] . [W_r; W_r]   (K-concatenation)
     MOE_TRY_CUDA(moe::launch_stack_wr(w_r, E, Ep, d, c->d_wr2, st(s)));
     moe::GemmProblem g;
+    g.sched = gemm_sched(c);
     g.epi = moe::kEpiF32Rows;
     g.BN = pick_bn(d);
     g.b_mn = true;
@@ -606,6 +614,7 @@ moe_status moe_router_logits_bwd(moe_ctx* c, const moe_bf16* x, const moe_bf16* 
   }
   if (dw_r) {  // [hi | lo]^T x over S token chunks -> [S, 2*Ep, d] partials -> ordered sum
     moe::GemmProblem g;
+    g.sched = gemm_sched(c);
     g.epi = moe::kEpiF32Group;
     g.BN = pick_bn(d);
     g.a_mn = true; g.b_mn = true;
@@ -624,7 +633,7 @@ moe_status moe_permute_bwd_router(moe_ctx* c, const moe_bf16* dxs, const int32_t
                                   const int32_t* topk_idx, const float* dlogits,
                                   const moe_bf16* w_r, const moe_bf16* dx_extra, moe_bf16* dx,
                                   moe_stream s) {
-  MOE_REQUIRE(c && dxs && dest_row && topk_idx && dlogits && w_r && dx);
+  MOE_REQUIRE(c && TOKP(dxs) && TOKP(dest_row) && TOKP(topk_idx) && TOKP(dlogits) && w_r && TOKP(dx));
   MOE_REQUIRE(c->s.k > 1);  // k = 1 has a dense router gradient (full softmax)
   return cuda_status(moe::launch_permute_bwd_router(dxs, dest_row, topk_idx, dlogits, w_r, dx_extra,
                                                     c->s.T_local, c->s.d, c->s.E, c->s.k, dx, st(s)));
@@ -632,13 +641,13 @@ moe_status moe_permute_bwd_router(moe_ctx* c, const moe_bf16* dxs, const int32_t
 
 // ---------------------------------------------------------------- F1 / B1
 moe_status moe_route(moe_ctx* c, const float* logits, int32_t* topk_idx, float* gates, moe_stream s) {
-  MOE_REQUIRE(c && logits && topk_idx && gates);
+  MOE_REQUIRE(c && TOKP(logits) && TOKP(topk_idx) && TOKP(gates));
   return cuda_status(moe::launch_route(logits, c->s.T_local, c->s.E, c->s.k, topk_idx, gates, st(s)));
 }
 
 moe_status moe_route_bwd(moe_ctx* c, const float* logits, const int32_t* topk_idx, const float* gates,
                          const float* dgates, float* dlogits, moe_stream s) {
-  MOE_REQUIRE(c && topk_idx && gates && dgates && dlogits && (logits || c->s.k > 1));
+  MOE_REQUIRE(c && TOKP(topk_idx) && TOKP(gates) && TOKP(dgates) && TOKP(dlogits) && (TOKP(logits) || c->s.k > 1));
   return cuda_status(moe::launch_route_bwd(logits, topk_idx, gates, dgates, c->s.T_local, c->s.E,
                                            c->s.k, dlogits, st(s)));
 }
@@ -646,7 +655,7 @@ moe_status moe_route_bwd(moe_ctx* c, const float* logits, const int32_t* topk_id
 // ---------------------------------------------------------------- F2 / B2
 moe_status moe_permute(moe_ctx* c, const moe_bf16* x, const int32_t* topk_idx, int32_t* counts,
                        int32_t* dest_row, moe_bf16* xs, moe_stream s) {
-  MOE_REQUIRE(c && x && topk_idx && counts && dest_row);   // xs NULL: indices only
+  MOE_REQUIRE(c && TOKP(x) && TOKP(topk_idx) && counts && TOKP(dest_row));   // xs NULL: indices only
   return cuda_status(moe::launch_permute(x, topk_idx, c->s.T_local, c->s.d, c->s.E, c->s.k, c->C,
                                          counts, dest_row, xs, c->d_scratch, st(s)));
 }
@@ -654,7 +663,7 @@ moe_status moe_permute(moe_ctx* c, const moe_bf16* x, const int32_t* topk_idx, i
 moe_status moe_permute_dispatch_local(moe_ctx* c, const moe_bf16* x, const int32_t* topk_idx,
                                       int32_t* counts, int32_t* dest_row, int32_t* layout,
                                       moe_bf16* xr, moe_stream s) {
-  MOE_REQUIRE(c && x && topk_idx && counts && dest_row && layout && xr);
+  MOE_REQUIRE(c && TOKP(x) && TOKP(topk_idx) && counts && TOKP(dest_row) && layout && xr);
   MOE_REQUIRE(c->s.ep_size == 1);
   if (set_device(c) != MOE_OK) return MOE_ERR_CUDA;
   const int64_t pad_max = static_cast<int64_t>(c->E_l) * (MOE_ALIGN_ROWS - 1);
@@ -665,7 +674,7 @@ moe_status moe_permute_dispatch_local(moe_ctx* c, const moe_bf16* x, const int32
 
 moe_status moe_permute_bwd(moe_ctx* c, const moe_bf16* dxs, const int32_t* dest_row,
                            const float* dx_acc, const moe_bf16* dx_extra, moe_bf16* dx, moe_stream s) {
-  MOE_REQUIRE(c && dxs && dest_row && dx);
+  MOE_REQUIRE(c && TOKP(dxs) && TOKP(dest_row) && TOKP(dx));
   return cuda_status(moe::launch_permute_bwd(dxs, dest_row, dx_acc, dx_extra, c->s.T_local, c->s.d,
                                              c->s.k, dx, st(s)));
 }
@@ -673,7 +682,7 @@ moe_status moe_permute_bwd(moe_ctx* c, const moe_bf16* dxs, const int32_t* dest_
 // ---------------------------------------------------------------- F3 / B3
 moe_status moe_dispatch_range(moe_ctx* c, const moe_bf16* xs, const int32_t* counts, int32_t* layout,
                               moe_bf16* xr, int32_t slot_begin, int32_t slot_end, moe_stream s) {
-  MOE_REQUIRE(c && xs && layout && xr && (counts || slot_begin > 0));
+  MOE_REQUIRE(c && TOKP(xs) && layout && xr && (counts || slot_begin > 0));
   MOE_REQUIRE(slot_begin >= 0 && slot_begin < slot_end && slot_end <= c->E_l);
   if (!c->peers_ready) return MOE_ERR_NOT_READY;
   if (!in_heap(c, xr, recv_bytes(c))) return MOE_ERR_NOT_SYMMETRIC;
@@ -691,7 +700,7 @@ moe_status moe_dispatch(moe_ctx* c, const moe_bf16* xs, const int32_t* counts, i
 
 moe_status moe_dispatch_bwd(moe_ctx* c, const moe_bf16* dxr, const int32_t* layout, moe_bf16* dxs,
                             moe_stream s) {
-  MOE_REQUIRE(c && dxr && layout && dxs);
+  MOE_REQUIRE(c && dxr && layout && TOKP(dxs));
   if (!c->peers_ready) return MOE_ERR_NOT_READY;
   if (!in_heap(c, dxs, send_bytes(c))) return MOE_ERR_NOT_SYMMETRIC;
   CommArgs a = comm_args(c);
@@ -717,6 +726,7 @@ moe_status ffn_up(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows, int
   if (rows_cap == 0) return MOE_OK;
   const int d = c->s.d;
   moe::GemmProblem g1;
+  g1.sched = gemm_sched(c);
   g1.epi = moe::kEpiSwiGLU;
   g1.BN = 256;
   g1.a_ptr = xr; g1.a_rows = rows_cap; g1.a_cols = d; g1.a_ld = d;
@@ -727,7 +737,6 @@ moe_status ffn_up(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows, int
   g1.pair = gemm_pair();
   g1.max_ctas = c->gemm_sms;
   g1.out = g_u_h; g1.ld_out = 3 * static_cast<int64_t>(f); g1.f = f;
-  g1.l2_hint = l2_hint();
   return cuda_status(moe::launch_grouped_gemm(g1, st(s)));
 }
 
@@ -739,6 +748,7 @@ moe_status ffn_down(moe_ctx* c, const int32_t* group_rows, int32_t n_groups, int
   if (rows_cap == 0) return MOE_OK;
   const int d = c->s.d;
   moe::GemmProblem g2;
+  g2.sched = gemm_sched(c);
   g2.epi = moe::kEpiBF16;
   g2.BN = pick_bn(d);
   g2.a_ptr = g_u_h + 2 * static_cast<int64_t>(f); g2.a_rows = rows_cap; g2.a_cols = f;
@@ -753,7 +763,6 @@ moe_status ffn_down(moe_ctx* c, const int32_t* group_rows, int32_t n_groups, int
   if (sc) {
     g2.scatter = 1; g2.scatter_off = sc->off; g2.scatter_layout = sc->layout; g2.comm = sc->comm;
   }
-  g2.l2_hint = l2_hint();
   return cuda_status(moe::launch_grouped_gemm(g2, st(s)));
 }
 
@@ -769,7 +778,9 @@ moe_status ffn_fwd(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows, in
 moe_status moe_expert_ffn(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows, int32_t n_groups,
                           int64_t rows_cap, int32_t f, const moe_bf16* w_gu, const moe_bf16* w_down,
                           moe_bf16* g_u_h, moe_bf16* out, moe_stream s) {
-  MOE_REQUIRE(c && xr && group_rows && w_gu && w_down && g_u_h && out);
+  // row buffers may be NULL when rows_cap == 0 (e.g. the shared experts of a T_local = 0 rank)
+  const bool r0 = rows_cap == 0;
+  MOE_REQUIRE(c && (xr || r0) && group_rows && w_gu && w_down && (g_u_h || r0) && (out || r0));
   return ffn_fwd(c, xr, group_rows, n_groups, rows_cap, f, w_gu, w_down, g_u_h, out, nullptr, s);
 }
 
@@ -784,6 +795,7 @@ moe_status ffn_bwd_dh(moe_ctx* c, const int32_t* group_rows, int32_t g0, int32_t
   const int d = c->s.d;
   const int64_t F = f;
   moe::GemmProblem a;
+  a.sched = gemm_sched(c);
   a.epi = moe::kEpiDSwiGLU;
   a.BN = (f % 256 == 0) ? 256 : 128;
   a.b_mn = true;
@@ -795,7 +807,6 @@ moe_status ffn_bwd_dh(moe_ctx* c, const int32_t* group_rows, int32_t g0, int32_t
   a.pair = gemm_pair();
   a.max_ctas = c->gemm_sms;
   a.out = dgu; a.ld_out = 2 * F; a.aux = g_u_h; a.ld_aux = 3 * F; a.f = f;
-  a.l2_hint = l2_hint();
   return cuda_status(moe::launch_grouped_gemm(a, st(s)));
 }
 
@@ -816,6 +827,7 @@ moe_status ffn_bwd_dx(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows,
   }
   // dgrad-2: dX = [dG dU] . W_gu  -> dxr
   moe::GemmProblem b;
+  b.sched = gemm_sched(c);
   b.epi = moe::kEpiBF16;
   b.BN = pick_bn(d);
   b.b_mn = true;
@@ -830,10 +842,10 @@ moe_status ffn_bwd_dx(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows,
   if (sc) {  // dX rows go straight back to their source ranks (dispatch_bwd fused)
     b.scatter = 1; b.scatter_off = sc->off; b.scatter_layout = sc->layout; b.comm = sc->comm;
   }
-  b.l2_hint = l2_hint();
   MOE_TRY_CUDA(moe::launch_grouped_gemm(b, st(s)));
   // wgrad: dW_down[g] = dout_g^T H_g   [d, f]
   moe::GemmProblem w1;
+  w1.sched = gemm_sched(c);
   w1.epi = moe::kEpiF32Group;
   w1.BN = (f % 256 == 0) ? 256 : 128;
   w1.a_mn = true; w1.b_mn = true;
@@ -845,10 +857,10 @@ moe_status ffn_bwd_dx(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows,
   w1.max_ctas = c->gemm_sms;
   w1.out = dw_down; w1.accumulate = accumulate;
   w1.n_fastest = w1.M > w1.N;   // keep the smaller operand slab re-read from L2
-  w1.l2_hint = l2_hint();
   MOE_TRY_CUDA(moe::launch_grouped_gemm(w1, st(s)));
   // wgrad: dW_gu[g] = dgu_g^T X_g   [2f, d]
   moe::GemmProblem w2;
+  w2.sched = gemm_sched(c);
   w2.epi = moe::kEpiF32Group;
   w2.BN = pick_bn(d);
   w2.a_mn = true; w2.b_mn = true;
@@ -860,7 +872,6 @@ moe_status ffn_bwd_dx(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows,
   w2.max_ctas = c->gemm_sms;
   w2.out = dw_gu; w2.accumulate = accumulate;
   w2.n_fastest = w2.M > w2.N;
-  w2.l2_hint = l2_hint();
   return cuda_status(moe::launch_grouped_gemm(w2, st(s)));
 }
 
@@ -880,7 +891,9 @@ moe_status moe_expert_ffn_bwd(moe_ctx* c, const moe_bf16* xr, const int32_t* gro
                               const moe_bf16* w_down, const moe_bf16* g_u_h, const moe_bf16* dout,
                               moe_bf16* dgu, moe_bf16* dxr, float* dw_gu, float* dw_down,
                               int accumulate, moe_stream s) {
-  MOE_REQUIRE(c && xr && group_rows && w_gu && w_down && g_u_h && dout && dgu && dxr && dw_gu && dw_down);
+  const bool r0 = rows_cap == 0;
+  MOE_REQUIRE(c && (xr || r0) && group_rows && w_gu && w_down && (g_u_h || r0) && (dout || r0) &&
+              (dgu || r0) && (dxr || r0) && dw_gu && dw_down);
   return ffn_bwd(c, xr, group_rows, n_groups, rows_cap, f, w_gu, w_down, g_u_h, dout, dgu, dxr,
                  dw_gu, dw_down, accumulate, nullptr, s);
 }
@@ -899,7 +912,7 @@ moe_status moe_expert_ffn_down_combine(moe_ctx* c, const int32_t* layout, const 
                                        moe_bf16* g_u_h, moe_bf16* ys, const float* gates,
                                        const int32_t* dest_row, const moe_bf16* y_extra,
                                        moe_bf16* y, moe_stream s) {
-  MOE_REQUIRE(c && layout && w_down && g_u_h && ys && gates && dest_row && y);
+  MOE_REQUIRE(c && layout && w_down && g_u_h && TOKP(ys) && TOKP(gates) && TOKP(dest_row) && TOKP(y));
   if (!c->peers_ready) return MOE_ERR_NOT_READY;
   if (!in_heap(c, ys, send_bytes(c))) return MOE_ERR_NOT_SYMMETRIC;
   CommArgs a = comm_args(c);
@@ -917,7 +930,7 @@ moe_status moe_expert_ffn_combine(moe_ctx* c, const moe_bf16* xr, const int32_t*
                                   const moe_bf16* w_gu, const moe_bf16* w_down, moe_bf16* g_u_h,
                                   moe_bf16* ys, const float* gates, const int32_t* dest_row,
                                   const moe_bf16* y_extra, moe_bf16* y, moe_stream s) {
-  MOE_REQUIRE(c && xr && layout && w_gu && w_down && g_u_h && ys && gates && dest_row && y);
+  MOE_REQUIRE(c && xr && layout && w_gu && w_down && g_u_h && TOKP(ys) && TOKP(gates) && TOKP(dest_row) && TOKP(y));
   if (!c->peers_ready) return MOE_ERR_NOT_READY;
   if (!in_heap(c, ys, send_bytes(c))) return MOE_ERR_NOT_SYMMETRIC;
   moe_status r = moe_expert_ffn_up(c, xr, layout, 0, c->E_l, w_gu, g_u_h, s);
@@ -940,7 +953,7 @@ moe_status moe_expert_ffn_bwd_dx_dispatch(moe_ctx* c, const moe_bf16* xr, const 
                                           const moe_bf16* dout, const moe_bf16* dgu, moe_bf16* dxs,
                                           float* dw_gu, float* dw_down, int accumulate,
                                           moe_stream s) {
-  MOE_REQUIRE(c && xr && layout && w_gu && g_u_h && dout && dgu && dxs && dw_gu && dw_down);
+  MOE_REQUIRE(c && xr && layout && w_gu && g_u_h && dout && dgu && TOKP(dxs) && dw_gu && dw_down);
   if (!c->peers_ready) return MOE_ERR_NOT_READY;
   if (!in_heap(c, dxs, send_bytes(c))) return MOE_ERR_NOT_SYMMETRIC;
   CommArgs a = comm_args(c);
@@ -958,7 +971,7 @@ moe_status moe_expert_ffn_bwd_dispatch(moe_ctx* c, const moe_bf16* xr, const int
                                        const moe_bf16* g_u_h, const moe_bf16* dout, moe_bf16* dgu,
                                        moe_bf16* dxs, float* dw_gu, float* dw_down, int accumulate,
                                        moe_stream s) {
-  MOE_REQUIRE(c && xr && layout && w_gu && w_down && g_u_h && dout && dgu && dxs && dw_gu && dw_down);
+  MOE_REQUIRE(c && xr && layout && w_gu && w_down && g_u_h && dout && dgu && TOKP(dxs) && dw_gu && dw_down);
   if (!c->peers_ready) return MOE_ERR_NOT_READY;
   if (!in_heap(c, dxs, send_bytes(c))) return MOE_ERR_NOT_SYMMETRIC;
   moe_status r = moe_expert_ffn_bwd_dh(c, layout, 0, c->E_l, w_down, g_u_h, dout, dgu, s);
@@ -971,7 +984,7 @@ moe_status moe_expert_ffn_bwd_dispatch(moe_ctx* c, const moe_bf16* xr, const int
 moe_status moe_combine(moe_ctx* c, const moe_bf16* out, const int32_t* layout, moe_bf16* ys,
                        const float* gates, const int32_t* dest_row, const moe_bf16* y_extra,
                        moe_bf16* y, moe_stream s) {
-  MOE_REQUIRE(c && out && layout && ys && gates && dest_row && y);
+  MOE_REQUIRE(c && out && layout && TOKP(ys) && TOKP(gates) && TOKP(dest_row) && TOKP(y));
   if (!c->peers_ready) return MOE_ERR_NOT_READY;
   if (!in_heap(c, ys, send_bytes(c))) return MOE_ERR_NOT_SYMMETRIC;
   CommArgs a = comm_args(c);
@@ -985,7 +998,7 @@ moe_status moe_combine_bwd_range(moe_ctx* c, const moe_bf16* dy, const float* ga
                                  const int32_t* dest_row, const moe_bf16* ys, const int32_t* layout,
                                  float* dgates, moe_bf16* dout_r, int32_t slot_begin,
                                  int32_t slot_end, moe_stream s) {
-  MOE_REQUIRE(c && dy && gates && dest_row && ys && layout && dgates && dout_r);
+  MOE_REQUIRE(c && TOKP(dy) && TOKP(gates) && TOKP(dest_row) && TOKP(ys) && layout && TOKP(dgates) && dout_r);
   MOE_REQUIRE(slot_begin >= 0 && slot_begin < slot_end && slot_end <= c->E_l);
   if (!c->peers_ready) return MOE_ERR_NOT_READY;
   if (!in_heap(c, dout_r, recv_bytes(c))) return MOE_ERR_NOT_SYMMETRIC;
@@ -1014,7 +1027,7 @@ int64_t pair_rows(const moe_ctx* c) { return moe_dedup_pair_rows_max(&c->s); }
 
 moe_status moe_dedup_pairs(moe_ctx* c, const int32_t* topk_idx, const int32_t* dest_row,
                            int32_t* pdest, int32_t* ntok, moe_stream s) {
-  MOE_REQUIRE(c && topk_idx && dest_row && pdest && ntok);
+  MOE_REQUIRE(c && TOKP(topk_idx) && TOKP(dest_row) && TOKP(pdest) && ntok);
   return cuda_status(moe::launch_dedup_pairs(topk_idx, dest_row, c->d_place, c->s.T_local, c->s.k,
                                              c->E_l, c->s.ep_size, pdest, ntok,
                                              c->d_dedup_scratch, st(s)));
@@ -1025,8 +1038,8 @@ moe_status moe_dedup_dispatch(moe_ctx* c, const moe_bf16* x, const int32_t* coun
                               const int32_t* topk_idx, const float* gates, int32_t* layout,
                               int32_t* dlayout, moe_bf16* xt, int32_t* rlist, float* glist,
                               moe_bf16* xr, moe_stream s) {
-  MOE_REQUIRE(c && x && counts && ntok && pdest && dest_row && topk_idx && gates && layout &&
-              dlayout && xt && rlist && glist && xr);
+  MOE_REQUIRE(c && TOKP(x) && counts && ntok && TOKP(pdest) && TOKP(dest_row) && TOKP(topk_idx) && TOKP(gates) && layout &&
+              dlayout && TOKP(xt) && TOKP(rlist) && TOKP(glist) && xr);
   if (!c->peers_ready) return MOE_ERR_NOT_READY;
   if (!in_heap(c, xt, tok_rows(c) * row_bytes(c)) || !in_heap(c, rlist, tok_rows(c) * c->s.k * 4) ||
       !in_heap(c, glist, tok_rows(c) * c->s.k * 4))
@@ -1043,7 +1056,7 @@ moe_status moe_dedup_dispatch(moe_ctx* c, const moe_bf16* x, const int32_t* coun
 moe_status moe_dedup_combine(moe_ctx* c, const moe_bf16* out, const int32_t* dlayout,
                              const int32_t* rlist, const float* glist, const int32_t* pdest,
                              const moe_bf16* y_extra, moe_bf16* part, moe_bf16* y, moe_stream s) {
-  MOE_REQUIRE(c && out && dlayout && rlist && glist && pdest && part && y);
+  MOE_REQUIRE(c && out && dlayout && TOKP(rlist) && TOKP(glist) && TOKP(pdest) && TOKP(part) && TOKP(y));
   if (!c->peers_ready) return MOE_ERR_NOT_READY;
   if (!in_heap(c, part, pair_rows(c) * row_bytes(c))) return MOE_ERR_NOT_SYMMETRIC;
   CommArgs a = comm_args(c);
@@ -1058,7 +1071,7 @@ moe_status moe_dedup_combine_bwd(moe_ctx* c, const moe_bf16* dy, const int32_t* 
                                  const int32_t* layout, const int32_t* dlayout,
                                  const int32_t* rlist, const float* glist, const moe_bf16* out,
                                  moe_bf16* dyt, float* dg_own, moe_bf16* dout_r, moe_stream s) {
-  MOE_REQUIRE(c && dy && pdest && layout && dlayout && rlist && glist && out && dyt && dg_own &&
+  MOE_REQUIRE(c && TOKP(dy) && TOKP(pdest) && layout && dlayout && TOKP(rlist) && TOKP(glist) && out && TOKP(dyt) && TOKP(dg_own) &&
               dout_r);
   if (!c->peers_ready) return MOE_ERR_NOT_READY;
   if (!in_heap(c, dyt, tok_rows(c) * row_bytes(c))) return MOE_ERR_NOT_SYMMETRIC;
@@ -1077,8 +1090,8 @@ moe_status moe_dedup_combine_bwd_ys(moe_ctx* c, const moe_bf16* dy, const float*
                                     const int32_t* dlayout, const int32_t* rlist,
                                     const float* glist, moe_bf16* dyt, float* dgates,
                                     moe_bf16* dout_r, moe_stream s) {
-  MOE_REQUIRE(c && dy && gates && dest_row && ys && pdest && layout && dlayout && rlist && glist &&
-              dyt && dgates && dout_r);
+  MOE_REQUIRE(c && TOKP(dy) && TOKP(gates) && TOKP(dest_row) && TOKP(ys) && TOKP(pdest) && layout && dlayout && TOKP(rlist) && TOKP(glist) &&
+              TOKP(dyt) && TOKP(dgates) && dout_r);
   if (!c->peers_ready) return MOE_ERR_NOT_READY;
   if (!in_heap(c, dyt, tok_rows(c) * row_bytes(c))) return MOE_ERR_NOT_SYMMETRIC;
   CommArgs a = comm_args(c);
@@ -1094,8 +1107,8 @@ moe_status moe_dedup_dispatch_bwd(moe_ctx* c, const moe_bf16* dxr, const int32_t
                                   const int32_t* rlist, const float* dg_own, const int32_t* pdest,
                                   const int32_t* dest_row, const int32_t* topk_idx,
                                   moe_bf16* dxpart, float* dgpart, float* dgates, moe_stream s) {
-  MOE_REQUIRE(c && dxr && dlayout && rlist && dg_own && pdest && dest_row && topk_idx && dxpart &&
-              dgpart && dgates);
+  MOE_REQUIRE(c && dxr && dlayout && TOKP(rlist) && TOKP(dg_own) && TOKP(pdest) && TOKP(dest_row) && TOKP(topk_idx) && TOKP(dxpart) &&
+              TOKP(dgpart) && TOKP(dgates));
   if (!c->peers_ready) return MOE_ERR_NOT_READY;
   if (!in_heap(c, dxpart, pair_rows(c) * row_bytes(c)) ||
       !in_heap(c, dgpart, pair_rows(c) * c->s.k * 4))
@@ -1112,7 +1125,7 @@ moe_status moe_dedup_permute_bwd_router(moe_ctx* c, const moe_bf16* dxpart, cons
                                         const int32_t* topk_idx, const float* dlogits,
                                         const moe_bf16* w_r, const moe_bf16* dx_extra,
                                         moe_bf16* dx, moe_stream s) {
-  MOE_REQUIRE(c && dxpart && pdest && topk_idx && dlogits && w_r && dx);
+  MOE_REQUIRE(c && TOKP(dxpart) && TOKP(pdest) && TOKP(topk_idx) && TOKP(dlogits) && w_r && TOKP(dx));
   MOE_REQUIRE(c->s.k > 1);
   return cuda_status(moe::launch_permute_bwd_router_rows(dxpart, pdest, c->s.ep_size, topk_idx,
                                                          dlogits, w_r, dx_extra, c->s.T_local,

@@ -121,40 +121,6 @@ MOE_DEVINL void tma_load_2d(void* smem_dst, const CUtensorMap* tm, uint64_t* bar
       : "memory");
 }
 
-// L2 eviction-priority policies for TMA (createpolicy): the operand a persistent raster re-reads
-// over time is loaded evict_last, single-use streams evict_first.
-MOE_DEVINL uint64_t l2_policy_evict_last() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-MOE_DEVINL uint64_t l2_policy_evict_first() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-MOE_DEVINL uint64_t l2_policy_evict_normal() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-MOE_DEVINL void tma_load_2d_hint(void* smem_dst, const CUtensorMap* tm, uint64_t* bar, int32_t c0,
-                                 int32_t c1, uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
-      "l"(reinterpret_cast<uint64_t>(tm)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(policy)
-      : "memory");
-}
-MOE_DEVINL void tma_store_2d_hint(const CUtensorMap* tm, const void* smem_src, int32_t c0,
-                                  int32_t c1, uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3}], [%1], %4;" ::"l"(
-          reinterpret_cast<uint64_t>(tm)),
-      "r"(smem_u32(smem_src)), "r"(c0), "r"(c1), "l"(policy)
-      : "memory");
-}
-
 // TMA stores from shared memory (bulk-group completion), plain and reduce-add.
 MOE_DEVINL void tma_store_2d(const CUtensorMap* tm, const void* smem_src, int32_t c0, int32_t c1) {
   asm volatile(
@@ -317,6 +283,32 @@ MOE_DEVINL void mbar_arrive_cluster_relaxed(uint32_t cluster_saddr) {
   asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_saddr)
                : "memory");
 }
+// Store to the same shared-memory word in another CTA of the cluster (DSMEM).
+MOE_DEVINL void st_shared_cluster_u32(uint32_t cluster_saddr, int32_t v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(cluster_saddr), "r"(v) : "memory");
+}
+// Wait with cluster-scope acquire: pairs with a remote mbarrier.arrive.release.cluster, so
+// shared-memory data another CTA wrote before its arrive is visible after the wait.
+MOE_DEVINL bool mbar_try_wait_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+MOE_DEVINL void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  if (mbar_try_wait_cluster(bar, parity)) return;
+  const uint64_t t0 = globaltimer_ns();
+  while (!mbar_try_wait_cluster(bar, parity)) {
+    if (globaltimer_ns() - t0 > 10ull * 1000 * 1000 * 1000) __trap();
+  }
+}
 MOE_DEVINL void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n"
                "barrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -329,15 +321,6 @@ MOE_DEVINL void tma_load_2d_pair(void* smem_dst, const CUtensorMap* tm, uint32_t
       "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(smem_dst)),
       "l"(reinterpret_cast<uint64_t>(tm)), "r"(mbar_cluster_addr), "r"(c0), "r"(c1)
-      : "memory");
-}
-MOE_DEVINL void tma_load_2d_pair_hint(void* smem_dst, const CUtensorMap* tm,
-                                      uint32_t mbar_cluster_addr, int32_t c0, int32_t c1,
-                                      uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-      ".L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
-      "l"(reinterpret_cast<uint64_t>(tm)), "r"(mbar_cluster_addr), "r"(c0), "r"(c1), "l"(policy)
       : "memory");
 }
 MOE_DEVINL void tmem_alloc_pair(uint32_t* dst_smem, uint32_t ncols) {

@@ -20,6 +20,7 @@
 //   warps 4..7  epilogue       (tcgen05.ld 32x32b -> fused activation -> 128B-swizzled smem
 //                               staging -> TMA store / TMA reduce-add, one 4 KB box per warp)
 #include <algorithm>
+#include <climits>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -37,6 +38,7 @@ constexpr int kThreads = 256;
 constexpr int kMaxGroups = 256;
 constexpr int kStageBox = 4096;  // per-epilogue-warp staging: 32 rows x 128 bytes
 constexpr int kMaxDevices = 64;
+constexpr int kSchedQ = 4;       // tile-queue slots of the dynamic scheduler
 
 struct KParams {
   int M, N, K;
@@ -46,9 +48,6 @@ struct KParams {
   int64_t rows_cap;
   int64_t b_group_stride, b_split;
   int n_fastest;        // tile raster: 1 = n fastest (B slab re-read), 0 = m fastest
-  int l2_hint;          // TMA L2 policies: bit 0 = the re-read operand (A for m-fastest,
-                        // B for n-fastest) evict_last, bit 1 = the other evict_first,
-                        // bit 2 = TMA stores evict_first
   int direct_store;     // F32Rows only: output pitch not 16B-aligned -> plain stores
   void* out;
   int64_t ld_out;
@@ -65,6 +64,9 @@ struct KParams {
   int64_t scatter_off;
   const int32_t* scatter_layout;
   CommArgs comm;
+  // dynamic tile scheduler: sched[0] = next tile (global atomic), sched[1] = CTAs done (the
+  // last one resets both for the next launch); nullptr = static c, c + nc, ... schedule
+  int* sched;
 };
 
 // STG = staging boxes per epilogue warp.  2 double-buffers the fp32 wgrad epilogue (its K is
@@ -184,8 +186,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  int* s_tile_prefix = reinterpret_cast<int*>(tmem_slot + 4);  // [kMaxGroups+1]
+  uint64_t* sfull = tempty + 2;    // tile-queue slot q holds a tile index (dynamic schedule)
+  uint64_t* sempty = sfull + kSchedQ;  // ... every consumer of the cluster has read it (leader)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sempty + kSchedQ);
+  int* s_ring = reinterpret_cast<int*>(tmem_slot + 4);            // [kSchedQ] tile indices
+  int* s_tile_prefix = s_ring + kSchedQ;                         // [kMaxGroups+1]
   int* s_seg = s_tile_prefix + kMaxGroups + 1;                   // [kMaxGroups+1]
   int* s_rows = s_seg + kMaxGroups + 1;                          // [kMaxGroups]
   int* s_pre = s_rows + kMaxGroups;                              // scatter: [EP][E_l] (<= 256)
@@ -238,6 +243,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 4 * PAIR);  // leader: the epilogue warps of both CTAs
     }
+    for (int q = 0; q < kSchedQ; ++q) {
+      mbar_init(&sfull[q], 1);             // the scheduler's arrival (local or remote)
+      mbar_init(&sempty[q], 1 + 5 * PAIR); // leader: producers, MMA issuer, epilogue warps
+    }
     fence_mbar_init();
   }
   if (warp == 2) {
@@ -277,25 +286,44 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int total_tiles = s_tile_prefix[n_groups];
-  // persistent schedule: cluster c takes tiles c, c + nc, c + 2 nc, ... (raster order of
-  // decode_tile), every role walks the same sequence
-  const int n_work = total_tiles > tile0 ? (total_tiles - 1 - tile0) / tile_step + 1 : 0;
+  // Persistent schedule.  Dynamic (p.sched): the leader's scheduler thread takes tile indices
+  // from a global atomic counter in raster order (decode_tile) and hands each to every role
+  // of both CTAs through a 4-slot shared-memory queue, so a cluster that runs faster simply
+  // takes more tiles -- a static c, c + nc, ... assignment leaves SMs idle at the end when
+  // their speeds differ (ncu: 9 % inactive SM cycles on dgrad-1).  Static otherwise.
+  const bool dyn = p.sched != nullptr;
+  // w-th tile of this cluster for a consumer role, -1 when the work is exhausted
+  auto next_tile = [&](int w) -> int {
+    if (!dyn) {
+      const int t = tile0 + w * tile_step;
+      return t < total_tiles ? t : -1;
+    }
+    const int q = w % kSchedQ;
+    const uint32_t ph = static_cast<uint32_t>(w / kSchedQ) & 1u;
+    if (PAIR == 2 && rank != 0) mbar_wait_cluster(&sfull[q], ph);
+    else mbar_wait(&sfull[q], ph);
+    const int t = *reinterpret_cast<volatile int*>(&s_ring[q]);
+    // the arrival only has to follow the read of the slot: a relaxed remote arrive (a release
+    // would compile to MEMBAR.ALL.GPU, which also waits for this thread's outstanding stores)
+    // made dependent on the loaded value
+    if (PAIR == 2 && rank != 0) {
+      if (t != INT_MIN) mbar_arrive_cluster_relaxed(mapa_shared(smem_u32(&sempty[q]), 0));
+    } else {
+      mbar_arrive(&sempty[q]);
+    }
+    return t;
+  };
 
   if (warp == 0) {
     // ===================== TMA producer =====================
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      const uint64_t pol_keep = l2_policy_evict_last(), pol_stream = l2_policy_evict_first(),
-                     pol_norm = l2_policy_evict_normal();
-      // the operand the raster re-reads over time: A (m fastest) or B (n fastest)
-      const uint64_t pol_reread = (p.l2_hint & 1) ? pol_keep : pol_norm;
-      const uint64_t pol_other = (p.l2_hint & 2) ? pol_stream : pol_norm;
-      const uint64_t pol_a = p.n_fastest ? pol_other : pol_reread;
-      const uint64_t pol_b = p.n_fastest ? pol_reread : pol_other;
-      for (int w = 0; w < n_work; ++w) {
-        const Tile tl = decode_tile<KGROUPED, BN, TILE_M>(tile0 + w * tile_step, s_tile_prefix,
-                                                          s_seg, s_rows, n_groups, p);
+      for (int w = 0;; ++w) {
+        const int t = next_tile(w);
+        if (t < 0) break;
+        const Tile tl = decode_tile<KGROUPED, BN, TILE_M>(t, s_tile_prefix, s_seg, s_rows,
+                                                          n_groups, p);
         for (int kb = 0; kb < tl.nkb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint32_t bar_addr = smem_u32(&full[stage]);
@@ -307,14 +335,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
           }
           auto load = [&](void* dst, const CUtensorMap* tm, int c0, int c1) {
-            const uint64_t pol = (tm == &tmA) ? pol_a : pol_b;
-            if (p.l2_hint) {
-              if (PAIR == 2) tma_load_2d_pair_hint(dst, tm, bar_addr, c0, c1, pol);
-              else tma_load_2d_hint(dst, tm, &full[stage], c0, c1, pol);
-            } else {
-              if (PAIR == 2) tma_load_2d_pair(dst, tm, bar_addr, c0, c1);
-              else tma_load_2d(dst, tm, &full[stage], c0, c1);
-            }
+            if (PAIR == 2) tma_load_2d_pair(dst, tm, bar_addr, c0, c1);
+            else tma_load_2d(dst, tm, &full[stage], c0, c1);
           };
           uint8_t* a_dst = sA + stage * C::A_BYTES;
           uint8_t* b_dst = sB + stage * C::B_BYTES;
@@ -358,9 +380,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int w = 0; w < n_work; ++w) {
-        const Tile tl = decode_tile<KGROUPED, BN, TILE_M>(tile0 + w * tile_step, s_tile_prefix,
-                                                          s_seg, s_rows, n_groups, p);
+      for (int w = 0;; ++w) {
+        const int t = next_tile(w);
+        if (t < 0) break;
+        const Tile tl = decode_tile<KGROUPED, BN, TILE_M>(t, s_tile_prefix, s_seg, s_rows,
+                                                          n_groups, p);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * C::ACC_STRIDE;
@@ -394,19 +418,40 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
+  } else if (warp == 3) {
+    // ===================== tile scheduler (leader CTA, dynamic schedule) =====================
+    if (dyn && lane == 0 && rank == 0) {
+      for (int i = 0;; ++i) {
+        const int q = i % kSchedQ;
+        const uint32_t ph = static_cast<uint32_t>(i / kSchedQ) & 1u;
+        mbar_wait(&sempty[q], ph ^ 1);              // every consumer has read slot q
+        int t = atomicAdd(p.sched, 1);
+        if (t >= total_tiles) t = -1;               // exhausted: every role stops
+        s_ring[q] = t;
+        if (PAIR == 2) {
+          st_shared_cluster_u32(mapa_shared(smem_u32(&s_ring[q]), 1), t);
+          mbar_arrive_cluster(mapa_shared(smem_u32(&sfull[q]), 1));   // release.cluster
+        }
+        mbar_arrive(&sfull[q]);
+        if (t < 0) break;
+      }
+    }
   } else if (warp >= 4) {
     // ===================== epilogue =====================
     const int ew = warp - 4;  // TMEM lane quadrant ew*32 .. ew*32+31
     const uint32_t row_addr = smem_u32(sStage + ew * STG * kStageBox) + lane * 128;
     const void* box = sStage + ew * STG * kStageBox;
     int sbuf = 0;   // STG = 2: the staging box the next chunk uses
-    const uint64_t pol_st = l2_policy_evict_first();
     int acc = 0;
     uint32_t acc_phase = 0;
     constexpr int kArrive = 4 * PAIR;  // epilogue warps of a cluster
-    for (int w = 0; w < n_work; ++w) {
-      const Tile tl = decode_tile<KGROUPED, BN, TILE_M>(tile0 + w * tile_step, s_tile_prefix,
-                                                        s_seg, s_rows, n_groups, p);
+    for (int w = 0;; ++w) {
+      int t = 0;
+      if (lane == 0) t = next_tile(w);
+      t = __shfl_sync(0xffffffffu, t, 0);
+      if (t < 0) break;
+      const Tile tl = decode_tile<KGROUPED, BN, TILE_M>(t, s_tile_prefix, s_seg, s_rows,
+                                                        n_groups, p);
       const int m_box = tl.m * TILE_M + static_cast<int>(rank) * kBM + ew * 32;  // warp's 1st row
       const int mi = m_box + lane;  // row of this thread inside its group
       const bool valid = KGROUPED ? true : (mi < tl.rows_g);
@@ -465,8 +510,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             stage_row(row_addr, lane, w);
             staging_release();
             if (lane == 0) {
-              if (p.l2_hint & 4) tma_store_2d_hint(&tmC, box, col + part * p.f, row0, pol_st);
-              else tma_store_2d(&tmC, box, col + part * p.f, row0);
+              tma_store_2d(&tmC, box, col + part * p.f, row0);
               bulk_commit();
             }
           }
@@ -507,8 +551,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             stage_row(row_addr, lane, w);
             staging_release();
             if (lane == 0) {
-              if (p.l2_hint & 4) tma_store_2d_hint(&tmC, box, tl.n * BN + c0, row0, pol_st);
-              else tma_store_2d(&tmC, box, tl.n * BN + c0, row0);
+              tma_store_2d(&tmC, box, tl.n * BN + c0, row0);
               bulk_commit();
             }
           }
@@ -556,8 +599,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             else stage_row(row_addr, lane, wu);
             staging_release();
             if (lane == 0) {
-              if (p.l2_hint & 4) tma_store_2d_hint(&tmC, box, col + part * p.f, row0, pol_st);
-              else tma_store_2d(&tmC, box, col + part * p.f, row0);
+              tma_store_2d(&tmC, box, col + part * p.f, row0);
               bulk_commit();
             }
           }
@@ -647,6 +689,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   tc_fence_before();
   if (PAIR == 2) cluster_sync(); else __syncthreads();
+  if (dyn && threadIdx.x == 0) {
+    // every scheduler of the grid has finished (its CTA passed the barrier above before this
+    // CTA's increment can be the last): the last CTA resets the counters for the next launch
+    if (atomicAdd(p.sched + 1, 1) == static_cast<int>(gridDim.x) - 1) {
+      p.sched[0] = 0;
+      p.sched[1] = 0;
+    }
+  }
   if (EPI == kEpiBF16 && p.scatter && threadIdx.x == 0) {
     // the last CTA to finish publishes the epoch to every rank (as comm.cu's signal_done)
     const CommArgs& a = p.comm;
@@ -767,7 +817,7 @@ cudaError_t launch_impl(const GemmProblem& g, cudaStream_t stream) {
   kp.b_group_stride = g.b_group_stride;
   kp.b_split = g.b_split;
   kp.n_fastest = g.n_fastest;
-  kp.l2_hint = g.l2_hint;
+  kp.sched = g.sched;
   kp.out = g.out; kp.ld_out = g.ld_out;
   kp.aux = g.aux; kp.ld_aux = g.ld_aux;
   kp.bias = g.bias;
