@@ -375,9 +375,11 @@ def run_ours(args):
 
     # ---- device-timed region: the plain step loop, nothing else on the stream (`value`)
     clocks = ClockSampler(local)
+    # the sampler first (it waits up to ~0.3 s for nvidia-smi's first line, a different time
+    # on every rank), THEN the barrier: the ranks enter the timed loop together
+    clocks.start()
     barrier()
     torch.cuda.synchronize()
-    clocks.start()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record(stream)
@@ -397,9 +399,9 @@ def run_ours(args):
         graph = layer.capture(x, dy)
         for _ in range(args.warmup):
             graph.replay()
+        clocks.start()
         barrier()
         torch.cuda.synchronize()
-        clocks.start()
         t0.record(stream)
         for _ in range(args.steps):
             graph.replay()
@@ -749,10 +751,10 @@ def run_pipeline(args):
         stack.step(xs if first else None, dys if last else None)
     for _ in range(args.warmup):
         step()
+    clocks = ClockSampler(local)
+    clocks.start()                 # before the barrier: the ranks enter the loop together
     torch.cuda.synchronize()
     dist.barrier()
-    clocks = ClockSampler(local)
-    clocks.start()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record()

@@ -13,8 +13,11 @@
  * - Pointers named x, w_*, logits, ... are DEVICE pointers on the ctx's device;
  *   `stream` is a cudaStream_t (0 = legacy default stream).  Every call is
  *   stream-ordered and asynchronous: the returned status covers host-side
- *   validation and launch only.  Device-side conditions (flag timeout, receive
- *   overflow) set a device error word read by moe_ctx_get_device_error().
+ *   validation and launch only.  A receive overflow sets a device error word read by
+ *   moe_ctx_get_device_error().  A peer flag that never arrives (10 s) records
+ *   MOE_ERR_TIMEOUT in that word and then TRAPS the kernel: the fault is sticky, so the
+ *   process's next synchronising CUDA call fails (MOE_ERR_CUDA from libmoe) rather than
+ *   later calls silently running on an incomplete receive buffer.
  * - The caller owns every buffer.  Buffers that a PEER writes into (the
  *   destinations of the four all-to-alls: xr, ys, dout_r, dxs) must come from
  *   moe_symm_alloc(); otherwise the call returns MOE_ERR_NOT_SYMMETRIC.
@@ -86,7 +89,7 @@ typedef enum {
   MOE_ERR_NOT_SYMMETRIC = 3,   /* all-to-all destination not from moe_symm_alloc */
   MOE_ERR_OUT_OF_MEMORY = 4,   /* symmetric heap exhausted */
   MOE_ERR_RECV_OVERFLOW = 5,   /* device-side: receive rows beyond the buffer */
-  MOE_ERR_TIMEOUT = 6,         /* device-side: a peer flag never arrived (10 s) */
+  MOE_ERR_TIMEOUT = 6,         /* device-side: a peer flag never arrived (10 s; the kernel traps) */
   MOE_ERR_NOT_READY = 7        /* collective call before moe_ctx_open_peers */
 } moe_status;
 

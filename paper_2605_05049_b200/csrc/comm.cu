@@ -35,6 +35,7 @@ __device__ unsigned long long g_trace[64][8];   // [epoch % 64][stamp]
 
 constexpr uint64_t kTimeoutNs = 10ull * 1000 * 1000 * 1000;
 constexpr int kMaxE = 256;  // validated by the C-ABI (E <= 256)
+constexpr int kDyK = 8;     // combine_bwd: slots per token handled with dy read once
 
 __device__ __forceinline__ uint64_t* peer_flag(const CommArgs& a, int q, int slot, int src) {
   return reinterpret_cast<uint64_t*>(peer_base(a, q) + a.flags_off) + slot * a.ep + src;
@@ -89,8 +90,13 @@ __device__ void signal_done(const CommArgs& a, int slot, bool wait_after) {
   }
 }
 
-// Publishes this rank's E counts into row `rank` of every peer's count matrix (parity
-// buffer epoch & 1).  Done by whichever block of the launch arrives first (ticket), so it
+// Publishes this rank's E counts into row `rank` of every peer's count matrix.  ONE buffer is
+// enough (the former epoch-parity double buffer never alternated): rank r writes
+// its counts of dispatch i+1 into peer q's row r only after r's dispatch i completed, which
+// required q's data flag of dispatch i, which q publishes only after every block of its
+// dispatch i built its tables from the count matrix -- so q has finished reading row r.
+// The same argument covers the dedup pair-count matrix.  Done by whichever block of the
+// launch arrives first (ticket), so it
 // cannot be starved by blocks that are already spinning on the counts flags.
 // With ntok (the dedup dispatch) this rank's EP pair counts go into row `rank` of every
 // peer's [EP x EP] pair-count matrix under the same release.
@@ -100,7 +106,7 @@ __device__ void publish_counts(const CommArgs& a, const int32_t* counts,
   if (threadIdx.x == 0) s_first = (atomicAdd(a.done + 1, 1) == 0);
   __syncthreads();
   if (!s_first) return;
-  const int parity = static_cast<int>(a.epoch & 1);
+  const int parity = 0;   // single buffer (see above)
   const int E = a.E, EP = a.ep;
   for (int i = threadIdx.x; i < EP * E; i += blockDim.x) {
     const int q = i / E, e = i % E;
@@ -126,8 +132,12 @@ __device__ void wait_all(const CommArgs& a, int slot) {
     const uint64_t t0 = globaltimer_ns();
     while (ld_acquire_sys(f) < a.epoch) {
       if (globaltimer_ns() - t0 > kTimeoutNs) {
+        // a peer never arrived: record it and fault the kernel.  The fault is sticky, so the
+        // process's next synchronising call fails instead of later steps running on an
+        // incomplete receive buffer (a silent timeout corrupted every later step)
         set_device_error(a.err, kDevTimeout);
-        break;
+        __threadfence_system();
+        __trap();
       }
       __nanosleep(64);
     }
@@ -324,7 +334,7 @@ __global__ void forward_transfer_kernel(CommArgs a, int32_t* __restrict__ layout
     publish_counts(a, counts);
     wait_all(a, kSlotCounts);
     MOE_TRACE_AT(1, blockIdx.x == 0);
-    cm = a.countmat + static_cast<int>(a.epoch & 1) * a.ep * a.E;
+    cm = a.countmat;
   }
   build_fwd_tables(a, cm, tb);
   if (exchange && blockIdx.x == 0) {  // layout record for the later calls of this layer
@@ -383,6 +393,73 @@ __global__ void forward_transfer_kernel(CommArgs a, int32_t* __restrict__ layout
       const int64_t drow = sg.dst_base[i] + within;
       uint4* dst = reinterpret_cast<uint4*>(peer_base(a, sg.dst_rank[i]) + dst_off + drow * row_bytes);
       copy_part(dst, reinterpret_cast<const uint4*>(src + row * d), nvec, part, lane);
+    } else if (a.k <= kDyK) {
+      // one token: dy is read ONCE per 2 KB part for all its slots (the slot loop runs inside
+      // the part loop), each slot's ys part once; lane vectors are visited in increasing v
+      // as in dot_scale_row, so dgates are identical to the per-slot path
+      const int64_t t = w;
+      const int k = static_cast<int>(a.k);
+      uint4* dstp[kDyK];
+      const uint4* ysp[kDyK];
+      float gj[kDyK], dot[kDyK];
+#pragma unroll
+      for (int j = 0; j < kDyK; ++j) {
+        dstp[j] = nullptr;
+        ysp[j] = nullptr;
+        gj[j] = 0.f;
+        dot[j] = 0.f;
+        if (j >= k) continue;
+        const int32_t row = dest_row[t * k + j];
+        if (row < 0) {
+          if (lane == 0 && s0 == 0) dgates[t * k + j] = 0.f;
+          continue;
+        }
+        const int e = upper_bound_idx(tb.off, E + 1, row);
+        const int slot = a.place[e] % E_l;
+        if (slot < s0 || slot >= s1) continue;   // another range's row
+        const int q = a.place[e] / E_l;
+        const int64_t drow = tb.dst[e] + (row - tb.off[e]);
+        dstp[j] = reinterpret_cast<uint4*>(peer_base(a, q) + dst_off + drow * row_bytes);
+        ysp[j] = reinterpret_cast<const uint4*>(ys + static_cast<int64_t>(row) * d);
+        gj[j] = gates[t * k + j];
+      }
+      const uint4* pdy = reinterpret_cast<const uint4*>(dy + t * d);
+      for (int v0 = lane; v0 < nvec; v0 += 128) {
+        uint4 av[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (v0 + 32 * u < nvec) av[u] = ld_nc_v4(pdy + v0 + 32 * u);
+#pragma unroll
+        for (int j = 0; j < kDyK; ++j) {
+          if (ysp[j] == nullptr) continue;
+          uint4 bv[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (v0 + 32 * u < nvec) bv[u] = ld_nc_v4(ysp[j] + v0 + 32 * u);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (v0 + 32 * u >= nvec) break;
+            const uint32_t aw[4] = {av[u].x, av[u].y, av[u].z, av[u].w};
+            const uint32_t bw[4] = {bv[u].x, bv[u].y, bv[u].z, bv[u].w};
+            uint32_t ow[4];
+#pragma unroll
+            for (int q2 = 0; q2 < 4; ++q2) {
+              const float y0 = bf16_lo(aw[q2]), y1 = bf16_hi(aw[q2]);
+              dot[j] += y0 * bf16_lo(bw[q2]) + y1 * bf16_hi(bw[q2]);
+              ow[q2] = pack_bf16(gj[j] * y0, gj[j] * y1);
+            }
+            st_v4(dstp[j] + v0 + 32 * u, make_uint4(ow[0], ow[1], ow[2], ow[3]));
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kDyK; ++j) {
+        if (ysp[j] == nullptr) continue;
+        float v = dot[j];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) dgates[t * k + j] = v;
+      }
     } else {
       const int64_t t = w;
       for (int j = 0; j < a.k; ++j) {
@@ -522,9 +599,8 @@ __global__ void dedup_forward_kernel(CommArgs a, int32_t* __restrict__ layout,
   if (MODE == 0) {
     publish_counts(a, counts, ntok);
     wait_all(a, kSlotCounts);
-    const int parity = static_cast<int>(a.epoch & 1);
-    const int32_t* cm = a.countmat + parity * EP * E;
-    nm = a.ntokmat + parity * EP * EP;
+    const int32_t* cm = a.countmat;
+    nm = a.ntokmat;
     build_fwd_tables(a, cm, tb);
     if (blockIdx.x == 0) {  // layout record (as moe_dispatch) + pair record
       for (int i = threadIdx.x; i < EP * E; i += blockDim.x) layout[i] = cm[i];

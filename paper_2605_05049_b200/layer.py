@@ -48,6 +48,9 @@ def _all_gather_bytes(payload: bytes, group=None) -> bytes:
 
 
 class MoELayer:
+    # extra symmetric-heap room (tests/guard.py puts canary allocations between the buffers)
+    extra_heap_bytes = 0
+
     def __init__(self, dims: LayerDims, device: int = 0, group=None, fused: bool = True,
                  dedup: bool = False, migratable=None, expert_state_bytes: int = 0):
         """fused=True uses the compute+all-to-all entry points (moe_expert_ffn_combine,
@@ -89,6 +92,7 @@ class MoELayer:
             self.tok_max = max(L.moe_dedup_token_rows_max(self.shape), 1)
             self.pair_max = max(L.moe_dedup_pair_rows_max(self.shape), 1)
             heap += self.tok_max * (d * 2 + 8 * k) + self.pair_max * 4 * k + 4 * 4096
+        heap += self.extra_heap_bytes
         self.migratable = dims.ep_size > 1 if migratable is None else bool(migratable)
         f32b = 4
         if self.migratable:
