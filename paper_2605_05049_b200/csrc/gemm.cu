@@ -347,7 +347,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int i = 0; i < kBM / 64; ++i)
               load(a_dst + i * 8192, &tmA, m_row + i * 64, tl.seg + kb * kBK);
           } else {
-            load(a_dst, &tmA, kb * kBK, tl.seg + m_row);
+            // A pair tile may reach past its group's 128-aligned segment (the tail tile of an
+            // expert): this CTA's 128 rows then belong to the NEXT segment and are discarded
+            // by the epilogue.  Load them out of bounds instead -- TMA zero-fills the box
+            // without touching L2/HBM, and the wasted MMAs run on zero operands (less energy
+            // under the power cap).
+            const bool past = m_row >= ((tl.rows_g + kBM - 1) / kBM) * kBM;
+            load(a_dst, &tmA, kb * kBK, past ? (1 << 30) : tl.seg + m_row);
           }
           // ---- B (a pair splits it along N: rank r holds columns [r*BN/2, (r+1)*BN/2))
           constexpr int BNC = BN / PAIR;

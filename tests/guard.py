@@ -41,7 +41,7 @@ def guarded():
         numel = 1
         for s in shape:
             numel *= int(s)
-        esize = torch.empty((), dtype=dtype).element_size()
+        esize = orig_empty((), dtype=dtype).element_size()
         nbytes = numel * esize
         raw = orig_empty((GUARD + nbytes + GUARD,), dtype=torch.uint8, device=device)
         raw.fill_(CANARY)
@@ -57,7 +57,7 @@ def guarded():
             shape = tuple(shape[0])
         dev = torch.device(device) if device is not None else None
         if dev is None or dev.type != "cuda" or kw:
-            return orig_empty(*shape, dtype=dtype, device=device, **kw)
+            return orig_empty(tuple(shape), dtype=dtype, device=device, **kw)
         return _alloc(shape, dtype or torch.float32, dev, False)
 
     def zeros(*shape, dtype=None, device=None, **kw):
@@ -65,7 +65,7 @@ def guarded():
             shape = tuple(shape[0])
         dev = torch.device(device) if device is not None else None
         if dev is None or dev.type != "cuda" or kw:
-            return orig_zeros(*shape, dtype=dtype, device=device, **kw)
+            return orig_zeros(tuple(shape), dtype=dtype, device=device, **kw)
         return _alloc(shape, dtype or torch.float32, dev, True)
 
     def symm_empty(self, shape, dtype):
