@@ -36,9 +36,6 @@ __device__ unsigned long long g_trace[64][8];   // [epoch % 64][stamp]
 constexpr uint64_t kTimeoutNs = 10ull * 1000 * 1000 * 1000;
 constexpr int kMaxE = 256;  // validated by the C-ABI (E <= 256)
 constexpr int kDyK = 8;     // combine_bwd: slots per token handled with dy read once
-// static all-to-all: TMA bulk copies from this many bytes per rank up (SM stores below; the
-// threshold is set from the measured sweep)
-constexpr int64_t kA2aTmaMinBytes = 1ll << 62;
 
 __device__ __forceinline__ uint64_t* peer_flag(const CommArgs& a, int q, int slot, int src) {
   return reinterpret_cast<uint64_t*>(peer_base(a, q) + a.flags_off) + slot * a.ep + src;
@@ -909,72 +906,6 @@ __global__ void __launch_bounds__(512) all_to_all_kernel(CommArgs a, const uint1
   signal_done(a, kSlotData, /*wait_after=*/true);
 }
 
-// The same all-to-all moved by the TMA engines instead of SM load/store instructions: one
-// 32-thread block per SM, thread 0 streams its pieces (up to 32 KB each) through a 4-stage
-// shared-memory ring -- cp.async.bulk global -> shared (local send buffer, mbarrier
-// completion), then cp.async.bulk shared -> global straight into the peer's receive buffer
-// over the NVSwitch mapping.  Piece j's store is issued while the loads of pieces j+1..j+3
-// are in flight; a stage is reloaded once the store that read it has finished reading.
-constexpr int kTmaPiece = 32 * 1024;
-constexpr int kTmaStages = 4;
-__global__ void all_to_all_tma_kernel(CommArgs a, const uint8_t* __restrict__ send,
-                                      int64_t dst_off, int64_t chunk_bytes) {
-  pdl_wait();
-  pdl_trigger();
-  a.epoch = load_epoch(a);
-  extern __shared__ __align__(128) uint8_t ring[];
-  __shared__ __align__(8) uint64_t full[kTmaStages];
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kTmaStages; ++s) mbar_init(&full[s], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const int64_t pieces = (chunk_bytes + kTmaPiece - 1) / kTmaPiece;
-    const int64_t n_items = pieces * a.ep;
-    // this block's items: blockIdx.x, blockIdx.x + gridDim.x, ...  (destination-major with a
-    // per-rank rotation, as the SM-store kernel)
-    const int64_t first = blockIdx.x, step = gridDim.x;
-    const int64_t mine = n_items > first ? (n_items - 1 - first) / step + 1 : 0;
-    auto piece = [&](int64_t j, const uint8_t*& src, uint8_t*& dst) -> uint32_t {
-      const int64_t w = first + j * step;
-      const int i = static_cast<int>(w / pieces);
-      const int64_t off = (w - static_cast<int64_t>(i) * pieces) * kTmaPiece;
-      const int q = (a.rank + 1 + i) % a.ep;
-      src = send + static_cast<int64_t>(q) * chunk_bytes + off;
-      dst = reinterpret_cast<uint8_t*>(peer_base(a, q)) + dst_off +
-            static_cast<int64_t>(a.rank) * chunk_bytes + off;
-      const int64_t n = chunk_bytes - off;
-      return static_cast<uint32_t>(n < kTmaPiece ? n : kTmaPiece);
-    };
-    const uint8_t* src;
-    uint8_t* dst;
-    for (int64_t j = 0; j < mine && j < kTmaStages; ++j) {   // prologue: fill the ring
-      const uint32_t n = piece(j, src, dst);
-      mbar_arrive_expect_tx(&full[j], n);
-      bulk_copy_g2s(smem_u32(ring + j * kTmaPiece), src, n, &full[j]);
-    }
-    for (int64_t j = 0; j < mine; ++j) {
-      const int s = static_cast<int>(j % kTmaStages);
-      mbar_wait(&full[s], static_cast<uint32_t>(j / kTmaStages) & 1u);
-      const uint32_t n = piece(j, src, dst);
-      bulk_copy_s2g(dst, smem_u32(ring + s * kTmaPiece), n);
-      bulk_commit();
-      const int64_t nj = j + kTmaStages - 1;   // the load that reuses the previous stage
-      if (j >= 1 && nj < mine) {
-        bulk_wait_read1();                    // store j-1 has read its stage
-        const int ps = static_cast<int>(nj % kTmaStages);
-        const uint32_t m = piece(nj, src, dst);
-        mbar_arrive_expect_tx(&full[ps], m);
-        bulk_copy_g2s(smem_u32(ring + ps * kTmaPiece), src, m, &full[ps]);
-      }
-    }
-    bulk_wait0();             // every store complete ...
-    fence_async_global();     // ... and ordered before the flag release in signal_done
-  }
-  signal_done(a, kSlotData, /*wait_after=*/true);
-}
-
 // Up to 2 blocks of 512 threads per SM (all co-resident: blocks spin on peer flags), and no
 // more than one block per 32 work items (2 KB row parts): small messages are latency-bound,
 // and every extra block adds to the launch and to the last-block count.
@@ -1035,30 +966,6 @@ cudaError_t launch_reverse_transfer(const CommArgs& a, const int32_t* layout, co
 
 cudaError_t launch_all_to_all(const CommArgs& a, const void* send, int64_t dst_off,
                               int64_t chunk_bytes, cudaStream_t s) {
-  static int tma = -1;   // MOE_A2A_TMA: 1 = TMA bulk copies, 0 = SM stores, default by size
-  if (tma < 0) {
-    const char* e = getenv("MOE_A2A_TMA");
-    tma = e ? (e[0] == '1' ? 1 : 0) : 2;
-  }
-  const bool use_tma = tma == 1 || (tma == 2 && chunk_bytes * a.ep >= kA2aTmaMinBytes);
-  if (use_tma) {
-    static bool attr[64] = {};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    const int smem = kTmaStages * kTmaPiece;
-    if (dev >= 0 && dev < 64 && !attr[dev]) {
-      cudaError_t e = cudaFuncSetAttribute(all_to_all_tma_kernel,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      if (e != cudaSuccess) return e;
-      attr[dev] = true;
-    }
-    const int64_t items = a.ep * ((chunk_bytes + kTmaPiece - 1) / kTmaPiece);
-    int64_t b = a.blocks > 0 ? a.blocks / 2 : num_sms();
-    if (items < b) b = items;
-    launch_k(all_to_all_tma_kernel, dim3(static_cast<unsigned>(b < 1 ? 1 : b)), dim3(32), smem,
-             s, a, static_cast<const uint8_t*>(send), dst_off, chunk_bytes);
-    return cudaGetLastError();
-  }
   const int64_t items = a.ep * ((chunk_bytes / 16 + kPartVec - 1) / kPartVec);
   int64_t b = a.blocks > 0 ? a.blocks : 2 * num_sms();
   const int64_t need = (items + 15) / 16;     // 16 warps per block, one 2 KB part each

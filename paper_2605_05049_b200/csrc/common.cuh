@@ -173,14 +173,6 @@ MOE_DEVINL void bulk_copy_s2g(void* gdst, uint32_t smem_src, uint32_t bytes) {
                "r"(smem_src), "r"(bytes)
                : "memory");
 }
-// 1-D bulk copy global -> shared, completion (bytes) on a CTA-local mbarrier.
-MOE_DEVINL void bulk_copy_g2s(uint32_t smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_dst),
-      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
 // async-proxy global writes (bulk copies) -> ordered before later generic-proxy operations
 MOE_DEVINL void fence_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
