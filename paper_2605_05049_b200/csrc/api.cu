@@ -198,13 +198,16 @@ int gemm_pair() {
   return v;
 }
 
-// the ctx's dynamic tile-scheduler counters (MOE_GEMM_SCHED=0: the static schedule, for
-// measurements)
+// The ctx's dynamic tile-scheduler counters, or nullptr for the static c, c + n_c, ...
+// schedule (the default).  MOE_GEMM_SCHED=1 selects the dynamic scheduler: measured equal
+// within noise at N=1 (Mixtral 13.65 vs 13.81 ms, DS-MoE 6.65 vs 6.64 ms over three A/B pairs
+// on one box; ncu: 11.95 vs 12.37 ms for the six GEMMs, -1.5 GB DRAM reads) but 2.5 % slower
+// at N=4 with unthrottled clocks (3.76-3.82 vs 3.68 ms) -- profiles/r02/sched/.
 int* gemm_sched(const moe_ctx* c) {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("MOE_GEMM_SCHED");
-    v = (e && e[0] == '0') ? 0 : 1;
+    v = (e && e[0] == '1') ? 1 : 0;
   }
   return v ? c->d_sched : nullptr;
 }
@@ -797,7 +800,10 @@ moe_status ffn_bwd_dh(moe_ctx* c, const int32_t* group_rows, int32_t g0, int32_t
   moe::GemmProblem a;
   a.sched = gemm_sched(c);
   a.epi = moe::kEpiDSwiGLU;
-  a.BN = (f % 256 == 0) ? 256 : 128;
+  // 256-column tiles also when f is an odd multiple of 128: the last n-tile is half out of
+  // bounds (zero B columns, no stores) -- cheaper than every tile at 128 columns (DS-MoE
+  // f = 1408: the BN = 128 dgrad-1 ran its tensor pipe 38 % of the time)
+  a.BN = f >= 256 ? 256 : 128;
   a.b_mn = true;
   a.a_ptr = dout; a.a_rows = rows_cap; a.a_cols = d; a.a_ld = d;
   a.b_ptr = w_down; a.b_rows = static_cast<int64_t>(n_groups) * d; a.b_cols = f; a.b_ld = f;
@@ -847,7 +853,7 @@ moe_status ffn_bwd_dx(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows,
   moe::GemmProblem w1;
   w1.sched = gemm_sched(c);
   w1.epi = moe::kEpiF32Group;
-  w1.BN = (f % 256 == 0) ? 256 : 128;
+  w1.BN = f >= 256 ? 256 : 128;   // as dgrad-1; the fp32 tensor map clips columns >= f
   w1.a_mn = true; w1.b_mn = true;
   w1.a_ptr = dout; w1.a_rows = rows_cap; w1.a_cols = d; w1.a_ld = d;
   w1.b_ptr = g_u_h + 2 * F; w1.b_rows = rows_cap; w1.b_cols = f; w1.b_ld = 3 * F;

@@ -38,7 +38,7 @@ constexpr int kThreads = 256;
 constexpr int kMaxGroups = 256;
 constexpr int kStageBox = 4096;  // per-epilogue-warp staging: 32 rows x 128 bytes
 constexpr int kMaxDevices = 64;
-constexpr int kSchedQ = 4;       // tile-queue slots of the dynamic scheduler
+constexpr int kSchedQ = 8;       // tile-queue slots of the dynamic scheduler
 
 struct KParams {
   int M, N, K;
@@ -566,10 +566,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         // acc = dH for f-columns n*BN ...; dG = dH*U*silu'(G), dU = dH*silu(G) -> dgu
 #pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += 64) {
+          const int col = tl.n * BN + c0;
+          // the last tile of an f that is an odd multiple of 128 is half past f: those
+          // accumulator columns are zero (B loaded out of bounds) and have no dG/dU columns
+          if (col >= p.f) break;
           uint32_t a[32], b[32], gw[32], uw[32], w[32];
           tmem_ld32(tacc + c0, a);
           tmem_ld32(tacc + c0 + 32, b);
-          const int col = tl.n * BN + c0;
           if (valid && grow < p.rows_cap) {
             const uint16_t* src = reinterpret_cast<const uint16_t*>(p.aux) + grow * p.ld_aux + col;
             const uint4* pg = reinterpret_cast<const uint4*>(src);
