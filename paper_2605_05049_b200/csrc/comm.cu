@@ -179,6 +179,8 @@ __device__ __forceinline__ int32_t warp_scan(int n, V val, O out) {
   return carry;
 }
 
+// Needs blockDim >= 32 (EP + 1): warps 0..EP-1 scan the owners' segments, warp EP the send
+// layout (every transfer kernel runs 512 threads; a 256-thread variant broke EP = 8).
 __device__ void build_fwd_tables(const CommArgs& a, const int32_t* cm, FwdTables& t) {
   const int E = a.E, EP = a.ep, E_l = a.E_l;
   // per-expert rows over all sources, and rows from sources before me

@@ -40,7 +40,9 @@ def run_worker(nproc, config, port, extra=(), env=None):
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT,
                        env=None if env is None else {**os.environ, **env})
     lines = [l for l in p.stdout.splitlines() if l.startswith("{")]
-    assert p.returncode == 0 and lines, f"worker failed:\n{p.stdout[-3000:]}\n{p.stderr[-3000:]}"
+    errs = [l for l in p.stderr.splitlines() if "Error" in l or "error:" in l][:20]
+    assert p.returncode == 0 and lines, (f"worker failed:\n{p.stdout[-3000:]}\n" +
+                                         "\n".join(errs) + f"\n{p.stderr[-2000:]}")
     return json.loads(lines[-1])
 
 
