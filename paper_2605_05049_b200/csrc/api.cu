@@ -841,7 +841,6 @@ moe_status ffn_bwd_dx(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows,
   b.b_ptr = w_gu; b.b_rows = static_cast<int64_t>(n_groups) * 2 * F; b.b_cols = d; b.b_ld = d;
   b.b_group_stride = 2 * F;
   b.N = d; b.K = 2 * f;
-  b.n_fastest = getenv("MOE_DGRAD2_NFAST") ? 1 : 0;   // EXPERIMENT
   b.group_rows = group_rows; b.n_groups = n_groups; b.rows_cap = rows_cap;
   b.pair = gemm_pair();
   b.max_ctas = c->gemm_sms;
