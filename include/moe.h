@@ -24,7 +24,9 @@
  * - Validation happens before any launch: MOE_ERR_INVALID_ARG for ep_size not in
  *   {1,2,4,8}, EP does not divide E, k < 1 or k > E,
  *   ep_rank outside [0,EP), d or f not a multiple of 64 (TMA/UMMA K-blocks of 64
- *   bf16), T_local < 0, or a NULL required pointer.  T_local = 0 is legal; the
+ *   bf16; the grouped FFN also needs f % 128 == 0 -- narrower than the survey's d % 8,
+ *   f % 16, a deliberate choice: every contraction runs whole 64-wide K-blocks), k > 32,
+ *   E > 256, T_local < 0, or a NULL required pointer.  T_local = 0 is legal; the
  *   collective calls still take part in the exchange.
  * - Collective calls (moe_dispatch, moe_dispatch_bwd, moe_combine,
  *   moe_combine_bwd, their _range variants, the fused *_combine / *_dispatch FFN
@@ -109,6 +111,8 @@ typedef struct {
 } moe_shape;
 
 typedef struct moe_ctx moe_ctx;   /* opaque: symmetric heap, peer table, flags, scratch */
+/* No moe_ctx_attach_nccl (SURVEY.md §8(b) listed it "baseline only"): libmoe has no NCCL
+ * dependency; the NCCL baselines (bench.py --a2a) run through torch.distributed beside it. */
 
 /* ---------------- context ---------------- */
 
