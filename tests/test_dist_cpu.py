@@ -45,7 +45,14 @@ def _worker(rank, world, port, q):
         t = torch.tensor([1.0 + rank, 5.0 - rank], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ok_max = t.tolist() == [float(world), 5.0]
-        q.put((rank, ok_handles, ok_shard, ok_experts, ok_max))
+        # tests/mp_common.gather (the shared-GPU workers' result gather over gloo)
+        from tests import mp_common
+        g = mp_common.gather(torch.full((3,), float(rank)))
+        ok_gather = [t.tolist() for t in g] == [[float(r)] * 3 for r in range(world)]
+        # the symmetric-allocation fingerprint exchange: identical sequences agree
+        fp = (1469598103934665603 ^ 12345).to_bytes(8, "little")
+        ok_fp = _all_gather_bytes(fp) == fp * world
+        q.put((rank, ok_handles, ok_shard, ok_experts, ok_max, ok_gather, ok_fp))
     finally:
         dist.destroy_process_group()
 
