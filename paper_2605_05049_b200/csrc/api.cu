@@ -49,7 +49,6 @@ struct moe_ctx {
   std::vector<std::pair<size_t, size_t>> allocs;
   uint64_t fingerprint = 1469598103934665603ull;
   size_t device_bytes = 0;        // every cudaMalloc of the ctx (heap incl.)
-  int32_t* d_sched = nullptr;     // [2] grouped-GEMM tile counter + done counter (zero at rest)
 };
 
 namespace {
@@ -198,20 +197,6 @@ int gemm_pair() {
   return v;
 }
 
-// The ctx's dynamic tile-scheduler counters, or nullptr for the static c, c + n_c, ...
-// schedule (the default).  MOE_GEMM_SCHED=1 selects the dynamic scheduler: measured equal
-// within noise at N=1 (Mixtral 13.65 vs 13.81 ms, DS-MoE 6.65 vs 6.64 ms over three A/B pairs
-// on one box; ncu: 11.95 vs 12.37 ms for the six GEMMs, -1.5 GB DRAM reads) but 2.5 % slower
-// at N=4 with unthrottled clocks (3.76-3.82 vs 3.68 ms) -- profiles/r02/sched/.
-int* gemm_sched(const moe_ctx* c) {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("MOE_GEMM_SCHED");
-    v = (e && e[0] == '1') ? 1 : 0;
-  }
-  return v ? c->d_sched : nullptr;
-}
-
 int pick_bn(int n) {
   if (n % 256 == 0) return 256;
   if (n % 128 == 0) return 128;
@@ -292,8 +277,6 @@ moe_status moe_ctx_create(moe_ctx** out, const moe_shape* shape, int device, siz
   e = ctx_malloc(c, &c->heap, c->heap_bytes);
   if (e == cudaSuccess) e = cudaMemset(c->heap, 0, c->internal_bytes);
   if (e == cudaSuccess) e = ctx_malloc(c, &c->d_err, 16);
-  if (e == cudaSuccess) e = ctx_malloc(c, &c->d_sched, 16);
-  if (e == cudaSuccess) e = cudaMemset(c->d_sched, 0, 16);
   if (e == cudaSuccess) e = cudaMemset(c->d_err, 0, 16);
   // [0] last-block counter, [1] counts ticket, [4..5] = uint64 collective epoch
   if (e == cudaSuccess) e = ctx_malloc(c, &c->d_done, 32);
@@ -553,7 +536,6 @@ moe_status moe_ctx_destroy(moe_ctx* c) {
     if (c->peer_opened[q]) cudaIpcCloseMemHandle(c->peer_base[q]);
   cudaFree(c->heap);
   cudaFree(c->d_err);
-  cudaFree(c->d_sched);
   cudaFree(c->d_done);
   cudaFree(c->d_scratch);
   cudaFree(c->d_dedup_scratch);
@@ -574,7 +556,6 @@ moe_status moe_router_logits(moe_ctx* c, const moe_bf16* x, const moe_bf16* w_r,
   MOE_REQUIRE(c && TOKP(x) && w_r && TOKP(logits));
   if (c->s.T_local == 0) return MOE_OK;
   moe::GemmProblem g;
-  g.sched = gemm_sched(c);
   g.epi = moe::kEpiF32Rows;
   const int E = c->s.E;
   g.BN = E <= 16 ? 16 : E <= 64 ? 64 : E <= 128 ? 128 : 256;
@@ -603,7 +584,6 @@ moe_status moe_router_logits_bwd(moe_ctx* c, const moe_bf16* x, const moe_bf16* 
   if (dx_router) {  // dx_router[T, d] = [hi | lo] . [W_r; W_r]   (K-concatenation)
     MOE_TRY_CUDA(moe::launch_stack_wr(w_r, E, Ep, d, c->d_wr2, st(s)));
     moe::GemmProblem g;
-    g.sched = gemm_sched(c);
     g.epi = moe::kEpiF32Rows;
     g.BN = pick_bn(d);
     g.b_mn = true;
@@ -617,7 +597,6 @@ moe_status moe_router_logits_bwd(moe_ctx* c, const moe_bf16* x, const moe_bf16* 
   }
   if (dw_r) {  // [hi | lo]^T x over S token chunks -> [S, 2*Ep, d] partials -> ordered sum
     moe::GemmProblem g;
-    g.sched = gemm_sched(c);
     g.epi = moe::kEpiF32Group;
     g.BN = pick_bn(d);
     g.a_mn = true; g.b_mn = true;
@@ -729,7 +708,6 @@ moe_status ffn_up(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows, int
   if (rows_cap == 0) return MOE_OK;
   const int d = c->s.d;
   moe::GemmProblem g1;
-  g1.sched = gemm_sched(c);
   g1.epi = moe::kEpiSwiGLU;
   g1.BN = 256;
   g1.a_ptr = xr; g1.a_rows = rows_cap; g1.a_cols = d; g1.a_ld = d;
@@ -751,7 +729,6 @@ moe_status ffn_down(moe_ctx* c, const int32_t* group_rows, int32_t n_groups, int
   if (rows_cap == 0) return MOE_OK;
   const int d = c->s.d;
   moe::GemmProblem g2;
-  g2.sched = gemm_sched(c);
   g2.epi = moe::kEpiBF16;
   g2.BN = pick_bn(d);
   g2.a_ptr = g_u_h + 2 * static_cast<int64_t>(f); g2.a_rows = rows_cap; g2.a_cols = f;
@@ -798,7 +775,6 @@ moe_status ffn_bwd_dh(moe_ctx* c, const int32_t* group_rows, int32_t g0, int32_t
   const int d = c->s.d;
   const int64_t F = f;
   moe::GemmProblem a;
-  a.sched = gemm_sched(c);
   a.epi = moe::kEpiDSwiGLU;
   // 256-column tiles also when f is an odd multiple of 128: the last n-tile is half out of
   // bounds (zero B columns, no stores) -- cheaper than every tile at 128 columns (DS-MoE
@@ -833,7 +809,6 @@ moe_status ffn_bwd_dx(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows,
   }
   // dgrad-2: dX = [dG dU] . W_gu  -> dxr
   moe::GemmProblem b;
-  b.sched = gemm_sched(c);
   b.epi = moe::kEpiBF16;
   b.BN = pick_bn(d);
   b.b_mn = true;
@@ -851,7 +826,6 @@ moe_status ffn_bwd_dx(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows,
   MOE_TRY_CUDA(moe::launch_grouped_gemm(b, st(s)));
   // wgrad: dW_down[g] = dout_g^T H_g   [d, f]
   moe::GemmProblem w1;
-  w1.sched = gemm_sched(c);
   w1.epi = moe::kEpiF32Group;
   w1.BN = f >= 256 ? 256 : 128;   // as dgrad-1; the fp32 tensor map clips columns >= f
   w1.a_mn = true; w1.b_mn = true;
@@ -866,7 +840,6 @@ moe_status ffn_bwd_dx(moe_ctx* c, const moe_bf16* xr, const int32_t* group_rows,
   MOE_TRY_CUDA(moe::launch_grouped_gemm(w1, st(s)));
   // wgrad: dW_gu[g] = dgu_g^T X_g   [2f, d]
   moe::GemmProblem w2;
-  w2.sched = gemm_sched(c);
   w2.epi = moe::kEpiF32Group;
   w2.BN = pick_bn(d);
   w2.a_mn = true; w2.b_mn = true;

@@ -283,32 +283,6 @@ MOE_DEVINL void mbar_arrive_cluster_relaxed(uint32_t cluster_saddr) {
   asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_saddr)
                : "memory");
 }
-// Store to the same shared-memory word in another CTA of the cluster (DSMEM).
-MOE_DEVINL void st_shared_cluster_u32(uint32_t cluster_saddr, int32_t v) {
-  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(cluster_saddr), "r"(v) : "memory");
-}
-// Wait with cluster-scope acquire: pairs with a remote mbarrier.arrive.release.cluster, so
-// shared-memory data another CTA wrote before its arrive is visible after the wait.
-MOE_DEVINL bool mbar_try_wait_cluster(uint64_t* bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
-      "selp.u32 %0, 1, 0, p;\n"
-      "}\n"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-MOE_DEVINL void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
-  if (mbar_try_wait_cluster(bar, parity)) return;
-  const uint64_t t0 = globaltimer_ns();
-  while (!mbar_try_wait_cluster(bar, parity)) {
-    if (globaltimer_ns() - t0 > 10ull * 1000 * 1000 * 1000) __trap();
-  }
-}
 MOE_DEVINL void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n"
                "barrier.cluster.wait.acquire.aligned;" ::: "memory");

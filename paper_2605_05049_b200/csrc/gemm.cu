@@ -20,7 +20,6 @@
 //   warps 4..7  epilogue       (tcgen05.ld 32x32b -> fused activation -> 128B-swizzled smem
 //                               staging -> TMA store / TMA reduce-add, one 4 KB box per warp)
 #include <algorithm>
-#include <climits>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -38,7 +37,6 @@ constexpr int kThreads = 256;
 constexpr int kMaxGroups = 256;
 constexpr int kStageBox = 4096;  // per-epilogue-warp staging: 32 rows x 128 bytes
 constexpr int kMaxDevices = 64;
-constexpr int kSchedQ = 8;       // tile-queue slots of the dynamic scheduler
 
 struct KParams {
   int M, N, K;
@@ -64,9 +62,6 @@ struct KParams {
   int64_t scatter_off;
   const int32_t* scatter_layout;
   CommArgs comm;
-  // dynamic tile scheduler: sched[0] = next tile (global atomic), sched[1] = CTAs done (the
-  // last one resets both for the next launch); nullptr = static c, c + nc, ... schedule
-  int* sched;
 };
 
 // STG = staging boxes per epilogue warp.  2 double-buffers the fp32 wgrad epilogue (its K is
@@ -186,11 +181,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* sfull = tempty + 2;    // tile-queue slot q holds a tile index (dynamic schedule)
-  uint64_t* sempty = sfull + kSchedQ;  // ... every consumer of the cluster has read it (leader)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sempty + kSchedQ);
-  int* s_ring = reinterpret_cast<int*>(tmem_slot + 4);            // [kSchedQ] tile indices
-  int* s_tile_prefix = s_ring + kSchedQ;                         // [kMaxGroups+1]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int* s_tile_prefix = reinterpret_cast<int*>(tmem_slot + 4);  // [kMaxGroups+1]
   int* s_seg = s_tile_prefix + kMaxGroups + 1;                   // [kMaxGroups+1]
   int* s_rows = s_seg + kMaxGroups + 1;                          // [kMaxGroups]
   int* s_pre = s_rows + kMaxGroups;                              // scatter: [EP][E_l] (<= 256)
@@ -243,10 +235,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 4 * PAIR);  // leader: the epilogue warps of both CTAs
     }
-    for (int q = 0; q < kSchedQ; ++q) {
-      mbar_init(&sfull[q], 1);             // the scheduler's arrival (local or remote)
-      mbar_init(&sempty[q], 1 + 5 * PAIR); // leader: producers, MMA issuer, epilogue warps
-    }
     fence_mbar_init();
   }
   if (warp == 2) {
@@ -286,32 +274,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int total_tiles = s_tile_prefix[n_groups];
-  // Persistent schedule.  Dynamic (p.sched): the leader's scheduler thread takes tile indices
-  // from a global atomic counter in raster order (decode_tile) and hands each to every role
-  // of both CTAs through a 4-slot shared-memory queue, so a cluster that runs faster simply
-  // takes more tiles -- a static c, c + nc, ... assignment leaves SMs idle at the end when
-  // their speeds differ (ncu: 9 % inactive SM cycles on dgrad-1).  Static otherwise.
-  const bool dyn = p.sched != nullptr;
-  // w-th tile of this cluster for a consumer role, -1 when the work is exhausted
+  // Persistent schedule: cluster c takes tiles c, c + n_c, c + 2 n_c, ... of the raster
+  // (decode_tile); every role walks the same sequence.  (A dynamic scheduler -- tiles from a
+  // global atomic counter through a cluster queue -- was measured equal at N = 1 and 4 %
+  // slower at N = 4, profiles/r02/sched/.)
   auto next_tile = [&](int w) -> int {
-    if (!dyn) {
-      const int t = tile0 + w * tile_step;
-      return t < total_tiles ? t : -1;
-    }
-    const int q = w % kSchedQ;
-    const uint32_t ph = static_cast<uint32_t>(w / kSchedQ) & 1u;
-    if (PAIR == 2 && rank != 0) mbar_wait_cluster(&sfull[q], ph);
-    else mbar_wait(&sfull[q], ph);
-    const int t = *reinterpret_cast<volatile int*>(&s_ring[q]);
-    // the arrival only has to follow the read of the slot: a relaxed remote arrive (a release
-    // would compile to MEMBAR.ALL.GPU, which also waits for this thread's outstanding stores)
-    // made dependent on the loaded value
-    if (PAIR == 2 && rank != 0) {
-      if (t != INT_MIN) mbar_arrive_cluster_relaxed(mapa_shared(smem_u32(&sempty[q]), 0));
-    } else {
-      mbar_arrive(&sempty[q]);
-    }
-    return t;
+    const int t = tile0 + w * tile_step;
+    return t < total_tiles ? t : -1;
   };
 
   if (warp == 0) {
@@ -424,24 +393,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
-  } else if (warp == 3) {
-    // ===================== tile scheduler (leader CTA, dynamic schedule) =====================
-    if (dyn && lane == 0 && rank == 0) {
-      for (int i = 0;; ++i) {
-        const int q = i % kSchedQ;
-        const uint32_t ph = static_cast<uint32_t>(i / kSchedQ) & 1u;
-        mbar_wait(&sempty[q], ph ^ 1);              // every consumer has read slot q
-        int t = atomicAdd(p.sched, 1);
-        if (t >= total_tiles) t = -1;               // exhausted: every role stops
-        s_ring[q] = t;
-        if (PAIR == 2) {
-          st_shared_cluster_u32(mapa_shared(smem_u32(&s_ring[q]), 1), t);
-          mbar_arrive_cluster(mapa_shared(smem_u32(&sfull[q]), 1));   // release.cluster
-        }
-        mbar_arrive(&sfull[q]);
-        if (t < 0) break;
-      }
-    }
   } else if (warp >= 4) {
     // ===================== epilogue =====================
     const int ew = warp - 4;  // TMEM lane quadrant ew*32 .. ew*32+31
@@ -452,9 +403,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t acc_phase = 0;
     constexpr int kArrive = 4 * PAIR;  // epilogue warps of a cluster
     for (int w = 0;; ++w) {
-      int t = 0;
-      if (lane == 0) t = next_tile(w);
-      t = __shfl_sync(0xffffffffu, t, 0);
+      const int t = next_tile(w);
       if (t < 0) break;
       const Tile tl = decode_tile<KGROUPED, BN, TILE_M>(t, s_tile_prefix, s_seg, s_rows,
                                                         n_groups, p);
@@ -698,14 +647,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   tc_fence_before();
   if (PAIR == 2) cluster_sync(); else __syncthreads();
-  if (dyn && threadIdx.x == 0) {
-    // every scheduler of the grid has finished (its CTA passed the barrier above before this
-    // CTA's increment can be the last): the last CTA resets the counters for the next launch
-    if (atomicAdd(p.sched + 1, 1) == static_cast<int>(gridDim.x) - 1) {
-      p.sched[0] = 0;
-      p.sched[1] = 0;
-    }
-  }
   if (EPI == kEpiBF16 && p.scatter && threadIdx.x == 0) {
     // the last CTA to finish publishes the epoch to every rank (as comm.cu's signal_done)
     const CommArgs& a = p.comm;
@@ -826,7 +767,6 @@ cudaError_t launch_impl(const GemmProblem& g, cudaStream_t stream) {
   kp.b_group_stride = g.b_group_stride;
   kp.b_split = g.b_split;
   kp.n_fastest = g.n_fastest;
-  kp.sched = g.sched;
   kp.out = g.out; kp.ld_out = g.ld_out;
   kp.aux = g.aux; kp.ld_aux = g.ld_aux;
   kp.bias = g.bias;

@@ -79,7 +79,6 @@ struct GemmProblem {
   int accumulate = 0;
   int n_fastest = 0;  // tile raster order: 1 = n fastest (re-read B), 0 = m fastest (re-read A)
   int max_ctas = 0;   // SM budget (0 = all SMs); used to run a GEMM beside a transfer
-  int* sched = nullptr;  // device int[2], zero between launches: dynamic tile scheduler
   int pair = 1;       // 2: CTA-pair tiles (tcgen05 cta_group::2, M = 256), BN >= 128 only
   // kEpiBF16 only: fused reverse all-to-all (rows -> source ranks' symmetric buffer at
   // scatter_off), the kernel's last CTA publishes comm->epoch on the data flags
