@@ -71,6 +71,10 @@ def parse():
                     help="NEXT-3: PP x EP pipelined stack (world = PP x EP), 1F1B over --micro")
     ap.add_argument("--layers", type=int, default=4, help="--pp: MoE layers in the stack")
     ap.add_argument("--micro", type=int, default=8, help="--pp: micro-batches per step")
+    ap.add_argument("--migrate-bench", action="store_true",
+                    help="NEXT-2: time moe_migrate moving every expert's full training state "
+                         "(bf16 weights, fp32 grads, fp32 master + Adam moments) to another "
+                         "rank, against PAPER.md's 48 d f bytes per expert at 50 GB/s")
     ap.add_argument("--profile-steps", type=int, default=0,
                     help="run only this many steps without timing (for ncu)")
     return ap.parse_args()
@@ -1046,10 +1050,77 @@ def run_gemm_compare(args):
     ctx.close()
 
 
+def run_migrate_bench(args):
+    """NEXT-2 migration cost (Table): the worst case of the
+    paper's table -- every expert moves (placement rotated by one rank) -- with each expert's
+    whole training state: bf16 weights (2 B/param), fp32 weight gradients (4), an fp32 master
+    copy and two fp32 Adam moments (12): 18 B per parameter (>= the paper's 16).  One
+    moe_migrate launch per state tensor, CUDA events on the stream, max over ranks."""
+    world, rank, local = dist_env()
+    dist = init_dist(world, local)
+    torch.cuda.set_device(local)
+    from paper_2605_05049_b200 import LayerDims, MoELayer
+    from paper_2605_05049_b200 import _lib as L
+    assert world > 1, "--migrate-bench needs torchrun with >= 2 ranks"
+    cfg = synth.CONFIGS[args.config]
+    E_l, n_par = cfg.E // world, 3 * cfg.d * cfg.f
+    dims = LayerDims(cfg.T // world, cfg.d, cfg.E, cfg.k, cfg.f, cfg.E_s, cfg.cf, world, rank)
+    layer = MoELayer(dims, device=local, migratable=True, expert_state_bytes=12 * n_par)
+    opt = [layer.expert_state(nm, (n_par,), torch.float32) for nm in ("master", "m", "v")]
+    dev = torch.device(f"cuda:{local}")
+    w_gu, w_down = synth.expert_weights(cfg, range(rank * E_l, (rank + 1) * E_l), device=dev)
+    layer.set_weights(synth.router_weight(cfg, device=dev), w_gu, w_down)
+    for t in opt:
+        t.normal_()
+    layer.dw_gu.normal_()
+    layer.dw_down.normal_()
+    rot = [(s + E_l) % cfg.E for s in range(cfg.E)]       # every expert to the next rank
+    times = []
+    for it in range(args.warmup + args.steps):
+        new = [rot[s] for s in layer.placement]
+        torch.cuda.synchronize()
+        dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        old = list(layer.placement)
+        nxt = 1 - layer._cur
+        for bufs in layer._states.values():
+            L.moe_migrate(layer.ctx, old, new, bufs[layer._cur], bufs[nxt])
+        b.record()
+        torch.cuda.synchronize()
+        layer._cur = nxt
+        layer.placement = new
+        layer.ctx.set_placement(new)
+        if it >= args.warmup:
+            times.append(a.elapsed_time(b))
+    ms = torch.tensor([float(np.median(times))], dtype=torch.float64, device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+    state_bytes = E_l * n_par * (2 + 4 + 12)            # per rank, all moved
+    paper_bytes = 48 * E_l * cfg.d * cfg.f               # PAPER.md:648 per rank (16 B/param)
+    if rank == 0:
+        print(json.dumps({
+            "metric": "expert migration time (every expert moves, full training state)",
+            "n_gpus": world, "config": cfg.name, "experts_per_rank": E_l,
+            "bytes_per_param": 18, "bytes_per_rank": state_bytes, "ms": ms,
+            "gb_per_s_per_rank": state_bytes / (ms * 1e-3) / 1e9,
+            "paper_table_bytes_per_rank": paper_bytes,
+            "paper_model_ms_at_50GBps": paper_bytes / 50e9 * 1e3,
+            "ours_ms_scaled_to_16B_per_param": ms * 16 / 18,
+            "note": "one moe_migrate launch per state tensor (weights x2, grads x2, master, m, "
+                    "v): barrier, peer stores into the new owners' other buffer half, flags"}),
+              flush=True)
+    layer.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.migrate_bench:
+        run_migrate_bench(args)
     elif args.gemm_compare:
         run_gemm_compare(args)
     elif args.pp > 1:

@@ -161,7 +161,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmC, const KParams p) {
-  pdl_wait();
+  // PDL: the setup below (barrier init, tensor-map prefetch, TMEM allocation) touches no
+  // global memory, so it runs before griddepcontrol.wait -- overlapping the previous kernel's
+  // tail; every global access (group tables, operands, outputs) comes after the wait
   pdl_trigger();
   constexpr int STG = staging_boxes<EPI>();
   using C = Cfg<BN, PAIR, STG>;
@@ -192,6 +194,30 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int lane = threadIdx.x & 31;
   const int n_groups = p.n_groups;
 
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    tma_prefetch_desc(&tmC);
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], PAIR);     // leader: one arrival per producer of the pair
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4 * PAIR);  // leader: the epilogue warps of both CTAs
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) {
+    if (PAIR == 2) {
+      tmem_alloc_pair(tmem_slot, C::TMEM_COLS);
+      tmem_relinquish_pair();
+    } else {
+      tmem_alloc(tmem_slot, C::TMEM_COLS);
+      tmem_relinquish();
+    }
+  }
+  pdl_wait();   // the previous kernel's outputs (this launch's inputs) are complete and visible
   // ---- group tables: seg_base = 128-aligned prefix of rows; tile prefix
   if (warp == 3) {
     const int NT = ceil_div(p.N, BN);
@@ -223,28 +249,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       s_tile_prefix[n_groups] = tile_carry;
     }
   }
-  if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&tmA);
-    tma_prefetch_desc(&tmB);
-    tma_prefetch_desc(&tmC);
-    for (int s = 0; s < C::STAGES; ++s) {
-      mbar_init(&full[s], PAIR);     // leader: one arrival per producer of the pair
-      mbar_init(&empty[s], 1);
-    }
-    for (int a = 0; a < 2; ++a) {
-      mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4 * PAIR);  // leader: the epilogue warps of both CTAs
-    }
-    fence_mbar_init();
-  }
   if (warp == 2) {
-    if (PAIR == 2) {
-      tmem_alloc_pair(tmem_slot, C::TMEM_COLS);
-      tmem_relinquish_pair();
-    } else {
-      tmem_alloc(tmem_slot, C::TMEM_COLS);
-      tmem_relinquish();
-    }
     if (EPI == kEpiBF16 && p.scatter) {
       // reverse-pattern tables of the local experts (same definitions as comm.cu):
       //   pre[r][el]  = rows of expert (rank*E_l + el) from sources < r  (receive order)
