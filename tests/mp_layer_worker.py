@@ -80,13 +80,21 @@ def main():
     state_ok = True
     if args.rebalance:
         layer.forward(x)
-        layer.observe_loads()
-        swaps, moved = layer.rebalance()
+        loads = layer.observe_loads()
+        # the paper's external scheduler (reading R20): libmoe's imbalance equals
+        # the oracle's, a threshold above it keeps the placement, one below it migrates
+        from oracle import migration as mig
+        imb0 = mig.imbalance(loads.numpy(), list(range(cfg.E)), ep)
+        state_ok &= abs(layer.imbalance() - imb0) < 1e-12
+        keep = layer.maybe_rebalance(threshold=imb0 + 1.0)
+        state_ok &= keep[1] == 0 and keep[2] == 0 and layer.placement == list(range(cfg.E))
+        imb, swaps, moved = layer.maybe_rebalance(threshold=1.0)
+        state_ok &= abs(imb - imb0) < 1e-12
         place = list(layer.placement)
         inv = [0] * cfg.E
         for e_, s_ in enumerate(place):
             inv[s_] = e_
-        state_ok = moved > 0
+        state_ok &= moved > 0
         for i, nm in enumerate(("master", "m", "v")):
             t = layer.state(nm)
             for el in range(E_l):
