@@ -54,6 +54,7 @@ struct KParams {
   const float* bias;
   int f;
   int accumulate;
+  int aux_tma;          // dSwiGLU: G / U boxes by TMA (tmX) instead of per-lane loads
   // BF16 epilogue fused with the reverse all-to-all (combine / dispatch_bwd): row w of local
   // expert e_l from source r is stored straight into rank r's symmetric buffer at
   // scatter_off, send-layout row soff[r][e_l] + (w - pre[r][e_l]); the last CTA publishes
@@ -160,7 +161,8 @@ template <int BN, bool A_MN, bool B_MN, int EPI, int PAIR>
 __global__ void __launch_bounds__(kThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB,
-                        const __grid_constant__ CUtensorMap tmC, const KParams p) {
+                        const __grid_constant__ CUtensorMap tmC,
+                        const __grid_constant__ CUtensorMap tmX, const KParams p) {
   // PDL: the setup below (barrier init, tensor-map prefetch, TMEM allocation) touches no
   // global memory, so it runs before griddepcontrol.wait -- overlapping the previous kernel's
   // tail; every global access (group tables, operands, outputs) comes after the wait
@@ -183,7 +185,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* abar = tempty + 2;   // dSwiGLU: one per epilogue warp, its G / U box loads
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(abar + 4);
   int* s_tile_prefix = reinterpret_cast<int*>(tmem_slot + 4);  // [kMaxGroups+1]
   int* s_seg = s_tile_prefix + kMaxGroups + 1;                   // [kMaxGroups+1]
   int* s_rows = s_seg + kMaxGroups + 1;                          // [kMaxGroups]
@@ -198,6 +201,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
     tma_prefetch_desc(&tmC);
+    if (EPI == kEpiDSwiGLU) tma_prefetch_desc(&tmX);
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], PAIR);     // leader: one arrival per producer of the pair
       mbar_init(&empty[s], 1);
@@ -206,6 +210,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 4 * PAIR);  // leader: the epilogue warps of both CTAs
     }
+    for (int a = 0; a < 4; ++a) mbar_init(&abar[a], 1);
     fence_mbar_init();
   }
   if (warp == 2) {
@@ -404,6 +409,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t row_addr = smem_u32(sStage + ew * STG * kStageBox) + lane * 128;
     const void* box = sStage + ew * STG * kStageBox;
     int sbuf = 0;   // STG = 2: the staging box the next chunk uses
+    uint32_t aph = 0;   // dSwiGLU: parity of this warp's G / U box barrier
     int acc = 0;
     uint32_t acc_phase = 0;
     constexpr int kArrive = 4 * PAIR;  // epilogue warps of a cluster
@@ -527,7 +533,27 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint32_t a[32], b[32], gw[32], uw[32], w[32];
           tmem_ld32(tacc + c0, a);
           tmem_ld32(tacc + c0 + 32, b);
-          if (valid && grow < p.rows_cap) {
+          if (p.aux_tma) {
+            // G and U boxes [32 rows x 64 cols] through this warp's staging box by TMA (one
+            // instruction each instead of 16 per-lane 16-byte loads; out-of-range rows load as
+            // zeros), read back row-per-lane from the 128B-swizzled layout
+            uint32_t* dst[2] = {gw, uw};
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              staging_acquire(lane);   // the last TMA store from the box has read it
+              if (lane == 0) {
+                mbar_arrive_expect_tx(&abar[ew], kStageBox);
+                tma_load_2d(const_cast<void*>(box), &tmX, &abar[ew], col + h * p.f, row0);
+              }
+              mbar_wait(&abar[ew], aph);
+              aph ^= 1u;
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                ld_shared_v4(row_addr + ((j ^ (lane & 7)) << 4), dst[h][4 * j], dst[h][4 * j + 1],
+                             dst[h][4 * j + 2], dst[h][4 * j + 3]);
+              __syncwarp();
+            }
+          } else if (valid && grow < p.rows_cap) {
             const uint16_t* src = reinterpret_cast<const uint16_t*>(p.aux) + grow * p.ld_aux + col;
             const uint4* pg = reinterpret_cast<const uint4*>(src);
             const uint4* pu = reinterpret_cast<const uint4*>(src + p.f);
@@ -764,6 +790,18 @@ cudaError_t launch_impl(const GemmProblem& g, cudaStream_t stream) {
                                                 : g.N;
     if (!make_tmap_bf16(&tc, g.out, g.rows_cap, cols, g.ld_out, 64, 32)) return cudaErrorInvalidValue;
   }
+  // dSwiGLU: the saved G | U | H rows as 32 x 64 boxes for the epilogue's TMA loads
+  CUtensorMap tx = tc;
+  if (EPI == kEpiDSwiGLU) {
+    static int tma_aux = -1;   // MOE_DSWIGLU_TMA=0: per-lane global loads (measurements)
+    if (tma_aux < 0) {
+      const char* e = getenv("MOE_DSWIGLU_TMA");
+      tma_aux = (e && e[0] == '0') ? 0 : 1;
+    }
+    if (tma_aux && make_tmap_bf16(&tx, g.aux, g.rows_cap, 3 * static_cast<int64_t>(g.f), g.ld_aux,
+                                  64, 32))
+      kp.aux_tma = 1;
+  }
   kp.M = g.M; kp.N = g.N; kp.K = g.K;
   kp.n_groups = g.n_groups;
   kp.group_begin = g.group_begin;
@@ -797,7 +835,7 @@ cudaError_t launch_impl(const GemmProblem& g, cudaStream_t stream) {
   }
   if (PAIR == 1) {
     const int grid = (g.max_ctas > 0 && g.max_ctas < num_sms()) ? g.max_ctas : num_sms();
-    return launch_k(kern, dim3(grid), dim3(kThreads), C::SMEM, stream, ta, tb, tc, kp);
+    return launch_k(kern, dim3(grid), dim3(kThreads), C::SMEM, stream, ta, tb, tc, tx, kp);
   }
   cudaLaunchConfig_t cfg;
   memset(&cfg, 0, sizeof(cfg));
@@ -826,7 +864,7 @@ cudaError_t launch_impl(const GemmProblem& g, cudaStream_t stream) {
   if (g.max_ctas > 0 && g.max_ctas / 2 < clusters) clusters = g.max_ctas / 2 > 0 ? g.max_ctas / 2 : 1;
   cfg.gridDim = dim3(2 * clusters);
   cfg.numAttrs = 1 + pdl_attr(&attr[1]);
-  return cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, kp);
+  return cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, tx, kp);
 }
 
 }  // namespace
