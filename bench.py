@@ -269,6 +269,8 @@ def run_ours(args):
     T_r = cfg.T // ep
     dims = LayerDims(T_r, cfg.d, cfg.E, cfg.k, cfg.f, cfg.E_s, cfg.cf, ep, rank)
     layer = MoELayer(dims, device=local, fused=not args.stepwise, dedup=args.dedup)
+    if os.environ.get("MOE_EP1_GENERAL") == "1":   # measurements: EP = 1 through permute + dispatch
+        layer.local_fast_path = False
     if args.comm_sms is not None:
         layer.comm_sms = args.comm_sms
     E_l = cfg.E // ep
@@ -424,8 +426,10 @@ def run_ours(args):
     hooked = ["moe_expert_ffn", "moe_expert_ffn_bwd", "moe_expert_ffn_combine",
               "moe_expert_ffn_bwd_dispatch", "moe_expert_ffn_up", "moe_expert_ffn_down_combine",
               "moe_expert_ffn_bwd_dh", "moe_expert_ffn_bwd_dx_dispatch"]
-    buckets = {"moe_permute": "permute", "moe_dispatch": "dispatch",
-               "moe_combine_bwd": "combine_bwd", "moe_dedup_dispatch": "dispatch",
+    buckets = {"moe_permute": "permute", "moe_permute_dispatch_local": "permute",
+               "moe_dispatch": "dispatch",
+               "moe_combine_bwd": "combine_bwd", "moe_combine_bwd_local": "combine_bwd",
+               "moe_dedup_dispatch": "dispatch",
                "moe_dedup_combine_bwd": "combine_bwd", "moe_dedup_combine_bwd_ys": "combine_bwd"}
     originals = {n: getattr(layer_mod.L, n) for n in hooked + list(buckets)}
     for n in hooked:

@@ -249,11 +249,31 @@ moe_status moe_permute(moe_ctx* ctx, const moe_bf16* x, const int32_t* topk_idx,
  * the rows written straight into the 128-aligned receive layout xr [moe_recv_rows_max, d]
  * (by local slot, padding rows zeroed) and the layout record written -- exactly the xr and
  * layout moe_permute + moe_dispatch produce, without the send-layout copy xs and the
- * transfer.  counts and dest_row (send-layout rows) are as moe_permute's; xr need not be
- * symmetric.  MOE_ERR_INVALID_ARG unless ep_size == 1. */
+ * transfer.  counts are moe_permute's; dest_row holds each kept slot's row IN xr (the receive
+ * layout; -1 = dropped), so the rest of the EP = 1 layer works on the receive layout in place:
+ * moe_expert_ffn -> moe_unpermute(out, ...) forward, moe_combine_bwd_local ->
+ * moe_expert_ffn_bwd -> moe_permute_bwd(_router)(dxr, ...) backward, with no send-layout
+ * buffers and no completion flags.  xr need not be symmetric.  MOE_ERR_INVALID_ARG unless
+ * ep_size == 1. */
 moe_status moe_permute_dispatch_local(moe_ctx* ctx, const moe_bf16* x, const int32_t* topk_idx,
                                       int32_t* counts, int32_t* dest_row, int32_t* layout,
                                       moe_bf16* xr, moe_stream stream);
+/* F6 alone: y[t] = bf16( sum_{j kept} gates[t,j] * rows[dest_row[t,j]] (j order, fp32)
+ * + y_extra[t] ), one rounding; y_extra may be NULL.  rows: [*, d] in whatever layout
+ * dest_row indexes (the send layout after moe_combine, the receive layout after
+ * moe_permute_dispatch_local). */
+moe_status moe_unpermute(moe_ctx* ctx, const moe_bf16* rows, const float* gates,
+                         const int32_t* dest_row, const moe_bf16* y_extra, moe_bf16* y,
+                         moe_stream stream);
+/* B6 at EP = 1 on the receive layout (dest_row from moe_permute_dispatch_local): for every kept
+ * slot dout_r[dest_row] = bf16(gates * dy[t]) and dgates = <dy[t], out[dest_row]> (fp32, a
+ * fixed order -- bit-identical to moe_combine_bwd's), 0 for dropped slots; the padding rows of
+ * dout_r's segments (layout record) are zeroed.  out: the expert outputs [recv_rows_max, d]
+ * (moe_expert_ffn).  MOE_ERR_INVALID_ARG unless ep_size == 1. */
+moe_status moe_combine_bwd_local(moe_ctx* ctx, const moe_bf16* dy, const float* gates,
+                                 const int32_t* dest_row, const moe_bf16* out,
+                                 const int32_t* layout, float* dgates, moe_bf16* dout_r,
+                                 moe_stream stream);
 /* dx[t] = bf16( sum_{j kept} dxs[dest_row[t,j]]  (fp32, j order)
  *               + dx_acc[t] (fp32, optional) + dx_extra[t] (bf16, optional) ), one rounding. */
 moe_status moe_permute_bwd(moe_ctx* ctx, const moe_bf16* dxs, const int32_t* dest_row,

@@ -82,6 +82,8 @@ _SIGS = {
     "moe_route_bwd": [P, P, P, P, P, P, P],
     "moe_permute": [P, P, P, P, P, P, P],
     "moe_permute_dispatch_local": [P, P, P, P, P, P, P, P],
+    "moe_unpermute": [P, P, P, P, P, P, P],
+    "moe_combine_bwd_local": [P, P, P, P, P, P, P, P, P],
     "moe_permute_bwd": [P, P, P, P, P, P, P],
     "moe_permute_bwd_router": [P, P, P, P, P, P, P, P, P],
     "moe_dispatch": [P, P, P, P, P, P],
@@ -361,6 +363,20 @@ def moe_permute_dispatch_local(ctx, x, topk_idx, counts, dest_row, layout, xr, s
         ctx.handle, _ptr(x, BF16, "x"), _ptr(topk_idx, I32T, "topk_idx"),
         _ptr(counts, I32T, "counts"), _ptr(dest_row, I32T, "dest_row"),
         _ptr(layout, I32T, "layout"), _ptr(xr, BF16, "xr"), _stream(stream)))
+
+
+def moe_unpermute(ctx, rows, gates, dest_row, y_extra, y, stream=None):
+    _check("moe_unpermute", _lib.moe_unpermute(
+        ctx.handle, _ptr(rows, BF16, "rows"), _ptr(gates, F32, "gates"),
+        _ptr(dest_row, I32T, "dest_row"), _ptr(y_extra, BF16, "y_extra"), _ptr(y, BF16, "y"),
+        _stream(stream)))
+
+
+def moe_combine_bwd_local(ctx, dy, gates, dest_row, out, layout, dgates, dout_r, stream=None):
+    _check("moe_combine_bwd_local", _lib.moe_combine_bwd_local(
+        ctx.handle, _ptr(dy, BF16, "dy"), _ptr(gates, F32, "gates"),
+        _ptr(dest_row, I32T, "dest_row"), _ptr(out, BF16, "out"), _ptr(layout, I32T, "layout"),
+        _ptr(dgates, F32, "dgates"), _ptr(dout_r, BF16, "dout_r"), _stream(stream)))
 
 
 def moe_permute_bwd(ctx, dxs, dest_row, dx_acc, dx_extra, dx, stream=None):

@@ -654,6 +654,27 @@ moe_status moe_permute_dispatch_local(moe_ctx* c, const moe_bf16* x, const int32
                                          c->d_expert_at, pad_max));
 }
 
+moe_status moe_unpermute(moe_ctx* c, const moe_bf16* rows, const float* gates,
+                         const int32_t* dest_row, const moe_bf16* y_extra, moe_bf16* y,
+                         moe_stream s) {
+  MOE_REQUIRE(c && rows && TOKP(gates) && TOKP(dest_row) && TOKP(y));
+  return cuda_status(moe::launch_unpermute(rows, gates, dest_row, y_extra, c->s.T_local, c->s.d,
+                                           c->s.k, y, st(s)));
+}
+
+moe_status moe_combine_bwd_local(moe_ctx* c, const moe_bf16* dy, const float* gates,
+                                 const int32_t* dest_row, const moe_bf16* out,
+                                 const int32_t* layout, float* dgates, moe_bf16* dout_r,
+                                 moe_stream s) {
+  MOE_REQUIRE(c && TOKP(dy) && TOKP(gates) && TOKP(dest_row) && out && layout && TOKP(dgates) &&
+              dout_r);
+  MOE_REQUIRE(c->s.ep_size == 1);
+  const int64_t pad_max = static_cast<int64_t>(c->E_l) * (MOE_ALIGN_ROWS - 1);
+  return cuda_status(moe::launch_combine_bwd_local(dy, gates, dest_row, out, layout, c->s.T_local,
+                                                   c->s.d, c->s.k, c->s.E, pad_max, dgates,
+                                                   dout_r, st(s)));
+}
+
 moe_status moe_permute_bwd(moe_ctx* c, const moe_bf16* dxs, const int32_t* dest_row,
                            const float* dx_acc, const moe_bf16* dx_extra, moe_bf16* dx, moe_stream s) {
   MOE_REQUIRE(c && TOKP(dxs) && TOKP(dest_row) && TOKP(dx));

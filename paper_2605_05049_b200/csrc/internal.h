@@ -137,6 +137,13 @@ cudaError_t launch_dedup_dgates(const int32_t* dest_row, const int32_t* topk_idx
                                 const int32_t* pdest, const int32_t* place, int E_l, int EP,
                                 const float* dgpart, int64_t T, int k, float* dgates,
                                 cudaStream_t s);
+// B6 at EP = 1 on the receive layout (dest_row = receive rows): dout rows = g * dy, dgates =
+// <dy, O rows>; zeroes the padding rows of dout's segments (layout record)
+cudaError_t launch_combine_bwd_local(const uint16_t* dy, const float* gates,
+                                     const int32_t* dest_row, const uint16_t* O,
+                                     const int32_t* layout, int64_t T, int d, int k, int E,
+                                     int64_t pad_rows_max, float* dgates, uint16_t* dout,
+                                     cudaStream_t s);
 cudaError_t launch_unpermute(const uint16_t* ys, const float* gates, const int32_t* dest_row,
                              const uint16_t* y_extra, int64_t T, int d, int k, uint16_t* y,
                              cudaStream_t s);

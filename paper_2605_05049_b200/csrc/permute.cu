@@ -139,7 +139,7 @@ __global__ void rank_kernel(const int32_t* __restrict__ idx, int64_t T, int k, i
 // With shift (EP = 1 local path) row dest_row + shift[e] of the 128-aligned receive layout is
 // written instead, and warps past the tokens zero the padding rows of every segment.
 template <int KMAX>
-__global__ void scatter_kernel(const uint16_t* __restrict__ x, const int32_t* __restrict__ dest_row,
+__global__ void scatter_kernel(const uint16_t* __restrict__ x, int32_t* __restrict__ dest_row,
                                const int32_t* __restrict__ idx, const int32_t* __restrict__ shift,
                                const int32_t* __restrict__ layout, int64_t T, int d, int k, int E,
                                uint16_t* __restrict__ xs) {
@@ -174,6 +174,14 @@ __global__ void scatter_kernel(const uint16_t* __restrict__ x, const int32_t* __
     rows[j] = r;
     any |= r >= 0;
   }
+  // local mode: dest_row becomes the receive-layout row (where the row was written), so the
+  // unpermute / permute_bwd gathers read the GEMM outputs in place (no send-layout copies)
+  if (shift && lane == 0) {
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j)
+      if (j < k) dest_row[t * k + j] = rows[j];
+  }
+  __syncwarp();
   if (!any) return;
   const uint4* src = reinterpret_cast<const uint4*>(x + t * d);
   for (int v0 = lane; v0 < nvec; v0 += 128) {   // 4 loads in flight per lane
@@ -189,6 +197,88 @@ __global__ void scatter_kernel(const uint16_t* __restrict__ x, const int32_t* __
       for (int u = 0; u < 4; ++u)
         if (v0 + 32 * u < nvec) dst[v0 + 32 * u] = val[u];
     }
+  }
+}
+
+// B6 at EP = 1, local (the permute wrote the receive rows into dest_row): for each kept slot
+// dO[dest_row] = bf16(g * dy[t]) and dgates = <dy[t], O[dest_row]>, dy read once per token
+// for all its slots; the padding rows of dO's segments are zeroed by the warps past the tokens.
+// The dot product visits a lane's vectors in increasing v and reduces over the warp as the
+// transfer kernel's combine_bwd does, so both paths give identical dgates.
+template <int KMAX>
+__global__ void combine_bwd_local_kernel(const uint16_t* __restrict__ dy,
+                                         const float* __restrict__ gates,
+                                         const int32_t* __restrict__ dest_row,
+                                         const uint16_t* __restrict__ O,
+                                         const int32_t* __restrict__ layout, int64_t T, int d,
+                                         int k, int E, float* __restrict__ dgates,
+                                         uint16_t* __restrict__ dout) {
+  pdl_wait();
+  pdl_trigger();
+  const int lane = threadIdx.x & 31;
+  const int64_t t = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int nvec = d / 8;
+  if (t >= T) {   // padding rows of the receive segments (layout record: expert_rows, seg_base)
+    const int64_t pr = t - T;
+    int64_t base = 0;
+    for (int sl = 0; sl < E; ++sl) {
+      const int32_t rows = layout[E + sl], seg = layout[2 * E + sl];
+      const int32_t pad = layout[2 * E + sl + 1] - seg - rows;
+      if (pr < base + pad) {
+        uint4* z = reinterpret_cast<uint4*>(dout + (static_cast<int64_t>(seg) + rows + (pr - base)) * d);
+        for (int v = lane; v < nvec; v += 32) z[v] = make_uint4(0u, 0u, 0u, 0u);
+        return;
+      }
+      base += pad;
+    }
+    return;
+  }
+  int32_t rw[KMAX];
+  float g[KMAX], dot[KMAX];
+#pragma unroll
+  for (int j = 0; j < KMAX; ++j) {
+    rw[j] = j < k ? dest_row[t * k + j] : -1;
+    g[j] = rw[j] >= 0 ? gates[t * k + j] : 0.f;
+    dot[j] = 0.f;
+  }
+  const uint4* pdy = reinterpret_cast<const uint4*>(dy + t * d);
+  for (int v0 = lane; v0 < nvec; v0 += 128) {
+    uint4 av[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (v0 + 32 * u < nvec) av[u] = ld_nc_v4(pdy + v0 + 32 * u);
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) {
+      if (rw[j] < 0) continue;
+      const uint4* po = reinterpret_cast<const uint4*>(O + static_cast<int64_t>(rw[j]) * d);
+      uint4* pd = reinterpret_cast<uint4*>(dout + static_cast<int64_t>(rw[j]) * d);
+      uint4 bv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (v0 + 32 * u < nvec) bv[u] = ld_nc_v4(po + v0 + 32 * u);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (v0 + 32 * u >= nvec) break;
+        const uint32_t aw[4] = {av[u].x, av[u].y, av[u].z, av[u].w};
+        const uint32_t bw[4] = {bv[u].x, bv[u].y, bv[u].z, bv[u].w};
+        uint32_t ow[4];
+#pragma unroll
+        for (int q2 = 0; q2 < 4; ++q2) {
+          const float y0 = bf16_lo(aw[q2]), y1 = bf16_hi(aw[q2]);
+          dot[j] += y0 * bf16_lo(bw[q2]) + y1 * bf16_hi(bw[q2]);
+          ow[q2] = pack_bf16(g[j] * y0, g[j] * y1);
+        }
+        pd[v0 + 32 * u] = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < KMAX; ++j) {
+    if (j >= k) break;
+    float v = dot[j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) dgates[t * k + j] = rw[j] >= 0 ? v : 0.f;
   }
 }
 
@@ -559,6 +649,25 @@ cudaError_t launch_permute_bwd(const uint16_t* dxs, const int32_t* dest_row, con
   else if (k <= 8) MOE_GS(8);
   else MOE_GS(32);
 #undef MOE_GS
+  return cudaGetLastError();
+}
+
+cudaError_t launch_combine_bwd_local(const uint16_t* dy, const float* gates,
+                                     const int32_t* dest_row, const uint16_t* O,
+                                     const int32_t* layout, int64_t T, int d, int k, int E,
+                                     int64_t pad_rows_max, float* dgates, uint16_t* dout,
+                                     cudaStream_t s) {
+  const int threads = 256;
+  const int64_t warps = T + pad_rows_max;
+  if (warps == 0) return cudaSuccess;
+  const dim3 grid(static_cast<unsigned>((warps * 32 + threads - 1) / threads));
+#define MOE_CB(K_) launch_k(combine_bwd_local_kernel<K_>, grid, dim3(threads), 0, s, dy, gates, \
+                            dest_row, O, layout, T, d, k, E, dgates, dout)
+  if (k <= 2) MOE_CB(2);
+  else if (k <= 4) MOE_CB(4);
+  else if (k <= 8) MOE_CB(8);
+  else MOE_CB(32);
+#undef MOE_CB
   return cudaGetLastError();
 }
 

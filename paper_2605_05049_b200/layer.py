@@ -261,7 +261,14 @@ class MoELayer:
                                  self.g_u_h_s, self.y_s)
                 y_extra = self.y_s
                 self._mark("F4s shared ffn")
-            return self._forward_reverse(y_extra)
+            # dest_row now holds receive rows: the GEMMs write the receive layout with plain
+            # TMA-store epilogues and F6 gathers O in place (no send-layout copy, no flags)
+            L.moe_expert_ffn(c, self.xr, self.expert_rows, self.E_l, self.R, f, self.w_gu,
+                             self.w_down, self.g_u_h, self.out)
+            self._mark("F4 expert ffn")
+            L.moe_unpermute(c, self.out, self.gates, self.dest_row, y_extra, self.y)
+            self._mark("F6 unpermute")
+            return self.y
         L.moe_permute(c, x, self.topk_idx, self.counts, self.dest_row, self.xs)
         self._mark("F2 permute")
         y_extra = None
@@ -376,6 +383,17 @@ class MoELayer:
         f, T = self.dims.f, self.dims.T_local
         if self.dedup:
             return self._backward_dedup(dy, accumulate)
+        if self.dims.ep_size == 1 and self.local_fast_path:
+            # receive layout in place (moe_permute_dispatch_local): dO = g dy and dgates on the
+            # expert outputs, the FFN backward writes dX rows to dxr, the gathers read them there
+            L.moe_combine_bwd_local(c, dy, self.gates, self.dest_row, self.out, self.layout,
+                                    self.dgates, self.dout_r)
+            self._mark("B6 combine_bwd (local)")
+            L.moe_expert_ffn_bwd(c, self.xr, self.expert_rows, self.E_l, self.R, f, self.w_gu,
+                                 self.w_down, self.g_u_h, self.dout_r, self.dgu, self.dxr,
+                                 self.dw_gu, self.dw_down, accumulate)
+            self._mark("B4 expert ffn_bwd")
+            return self._backward_tail(dy, accumulate, False, rows=self.dxr)
         shared_done = False
         if self.fs and self.overlap:
             # shared-expert backward (needs only dy) beside the combine_bwd all-to-all
@@ -414,8 +432,10 @@ class MoELayer:
             self._mark("B3 dispatch_bwd")
         return self._backward_tail(dy, accumulate, shared_done)
 
-    def _backward_tail(self, dy, accumulate, shared_done):
-        """Shared experts (if not yet done), route / router backward and permute backward."""
+    def _backward_tail(self, dy, accumulate, shared_done, rows=None):
+        """Shared experts (if not yet done), route / router backward and permute backward
+        (gathering dX rows from `rows`: dxs, or dxr on the EP = 1 receive layout)."""
+        rows = self.dxs if rows is None else rows
         c, T = self.ctx, self.dims.T_local
         dx_extra = self.dx_s if self.fs else None
         if self.fs and not shared_done:
@@ -432,13 +452,13 @@ class MoELayer:
                 L.moe_dedup_permute_bwd_router(c, self.dxs, self.pdest, self.topk_idx,
                                                self.dlogits, self.w_r, dx_extra, self.dx)
             else:
-                L.moe_permute_bwd_router(c, self.dxs, self.dest_row, self.topk_idx, self.dlogits,
+                L.moe_permute_bwd_router(c, rows, self.dest_row, self.topk_idx, self.dlogits,
                                          self.w_r, dx_extra, self.dx)
         else:
             L.moe_router_logits_bwd(c, self.x, self.w_r, self.dlogits, self.dx_router, self.dw_r,
                                     accumulate)
             self._mark("B1+B0 route_bwd,router dW")
-            L.moe_permute_bwd(c, self.dxs, self.dest_row, self.dx_router, dx_extra, self.dx)
+            L.moe_permute_bwd(c, rows, self.dest_row, self.dx_router, dx_extra, self.dx)
         self._mark("B2 permute_bwd")
         return self.dx
 
@@ -609,11 +629,18 @@ class MoELayer:
             if bwd:
                 n += 2 + 4 + (1 if rev else 2) + 1 + 3 + 1 + (4 if self.fs else 0)
             return n
+        if self.dims.ep_size == 1 and self.local_fast_path:
+            # receive layout in place: fwd router GEMM, route, permute (3), ffn (2), unpermute;
+            # bwd combine_bwd_local, ffn_bwd (4), route_bwd, router bwd (3, +2 for k = 1),
+            # permute_bwd
+            if fwd:
+                n += 1 + 1 + 3 + 2 + 1 + (2 if self.fs else 0)
+            if bwd:
+                n += 1 + 4 + 1 + 3 + (0 if self.dims.k > 1 else 2) + 1 + (4 if self.fs else 0)
+            return n
         if fwd:
             # router GEMM, route, permute (3), dispatch (1 fused launch), ffn (2), combine (2)
             n += 1 + 1 + 3 + 1 + 2 + 2 + (2 if self.fs else 0)
-            if self.dims.ep_size == 1 and self.local_fast_path:
-                n -= 1                     # no dispatch launch (the permute writes xr)
         if bwd:
             # combine_bwd (1), ffn_bwd (4), dispatch_bwd (1), route_bwd,
             # router bwd (hi/lo split, split-K dW_r GEMM, partial sum; k = 1 adds the

@@ -56,3 +56,14 @@ def paper_weights(w_gu, w_down, f):
     W_gate [d,f] = w_gu[:f].T, W_up = w_gu[f:].T, W_down [f,d] = w_down.T."""
     g = f64(w_gu)
     return g[:f].T, g[f:].T, f64(w_down).T
+
+
+def expected_dest_row(layer, topk_idx, C, E):
+    """dest_row the layer reports at EP = 1: the oracle's send-layout row (moe_permute), or on
+    the local receive-layout path (moe_permute_dispatch_local) the oracle's 128-aligned
+    receive row under the layer's placement."""
+    from oracle import moe_ref as ref
+    plan = ref.dispatch_plan(topk_idx, E, 1, C, align=ALIGN, placement=layer.placement)
+    if layer.dims.ep_size == 1 and layer.local_fast_path and not layer.dedup:
+        return plan["recv_row"]
+    return plan["ranks"][0]["dest_row"]

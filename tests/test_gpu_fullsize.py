@@ -14,7 +14,7 @@ import torch
 
 import synth
 from oracle import moe_ref as ref
-from tests.helpers import TOL, f64, paper_weights, rel_err, rel_err_rows
+from tests.helpers import TOL, expected_dest_row, f64, paper_weights, rel_err, rel_err_rows
 
 pytestmark = pytest.mark.gpu
 
@@ -45,7 +45,7 @@ def test_fullsize_sampled_parity(name):
     plan = ref.dispatch_plan(idx, cfg.E, 1, C, align=128)
     pos = plan["ranks"][0]
     assert (layer.counts.cpu().numpy() == pos["counts"]).all()
-    assert (layer.dest_row.cpu().numpy() == pos["dest_row"]).all()
+    assert (layer.dest_row.cpu().numpy() == expected_dest_row(layer, idx, C, cfg.E)).all()
     lay = layer.layout.cpu().numpy()
     assert (lay[cfg.E:2 * cfg.E] == plan["layouts"][0]["expert_rows"]).all()
     assert (lay[2 * cfg.E:] == plan["layouts"][0]["seg_base"]).all()

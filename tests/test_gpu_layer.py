@@ -9,7 +9,7 @@ import torch
 
 import synth
 from oracle import moe_ref as ref
-from tests.helpers import TOL, f64, paper_weights, rel_err, rel_err_rows
+from tests.helpers import TOL, expected_dest_row, f64, paper_weights, rel_err, rel_err_rows
 
 pytestmark = pytest.mark.gpu
 
@@ -85,7 +85,8 @@ def test_layer_ep1_parity(name, dedup):
     assert (layer.topk_idx.cpu().numpy() == fw["topk_idx"]).all()
     pos = fw["plan"]["ranks"][0]
     assert (layer.counts.cpu().numpy() == pos["counts"]).all()
-    assert (layer.dest_row.cpu().numpy() == pos["dest_row"]).all()
+    assert (layer.dest_row.cpu().numpy() == expected_dest_row(layer, fw["topk_idx"], fw["C"],
+                                                              cfg.E)).all()
     lay = layer.layout.cpu().numpy()
     E_l = cfg.E
     assert (lay[:cfg.E] == fw["plan"]["counts_all"][0]).all()
