@@ -133,6 +133,8 @@ def main():
         dist.destroy_process_group()
         return
     from oracle import moe_ref as ref
+    from tests.helpers import ALIGN
+    local_path = ep == 1 and stack.layers[0][0].local_fast_path and not stack.layers[0][0].dedup
     errs, checks = {}, {"routing": True, "handoff": True}
     errs_norm = {}
     ranks_of = lambda s_: list(range(s_ * ep, (s_ + 1) * ep))
@@ -149,9 +151,12 @@ def main():
             fw, bw = ref.layer_forward_backward(f64(X), w_r, Wg, Wu, Wd, f64(DY), cfg.k, cfg.cf,
                                                 ep, logits=LG.numpy())
             checks["routing"] &= bool((cat("topk").numpy() == fw["topk_idx"]).all())
+            if local_path:   # EP = 1 receive-layout path: dest_row = 128-aligned receive row
+                want = [ref.dispatch_plan(fw["topk_idx"], cfg.E, 1, fw["C"], align=ALIGN)["recv_row"]]
+            else:
+                want = [fw["plan"]["ranks"][i]["dest_row"] for i in range(len(rs))]
             for i, r in enumerate(rs):
-                checks["routing"] &= bool((G["dest"][l][m][r].cpu().numpy() ==
-                                           fw["plan"]["ranks"][i]["dest_row"]).all())
+                checks["routing"] &= bool((G["dest"][l][m][r].cpu().numpy() == want[i]).all())
             errs[f"y{g}.{m}"] = rel_err(f64(Y), fw["y"])
             errs[f"dx{g}.{m}"] = rel_err(f64(DX), bw["dx"])
             errs[f"y_rows{g}.{m}"] = rel_err_rows(f64(Y), fw["y"])
