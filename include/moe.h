@@ -346,6 +346,21 @@ moe_status moe_expert_ffn_combine(moe_ctx* ctx, const moe_bf16* xr, const int32_
                                   const moe_bf16* w_gu, const moe_bf16* w_down, moe_bf16* g_u_h,
                                   moe_bf16* ys, const float* gates, const int32_t* dest_row,
                                   const moe_bf16* y_extra_or_null, moe_bf16* y, moe_stream stream);
+/* Collective.  F3 + F4 (up) in ONE launch, the tile-granular dispatch -> GEMM1 overlap
+ * ("computation-communication overlap within MoE layers"; volumes and receive
+ * placement PAPER.md:354-356).  Same arguments and results as moe_dispatch(xs, counts,
+ * layout, xr) followed by moe_expert_ffn_up(xr, layout, 0, E_l, w_gu, g_u_h) -- xr, the
+ * layout record and g_u_h bit-identical -- but inside the persistent GEMM1 launch: two warps
+ * of every CTA push this rank's rows to their owners (NVSwitch peer stores) and release a
+ * per-(owner slot, source) arrival flag as each segment completes, and every GEMM1 tile
+ * starts as soon as the rows of its 128-row A box have arrived instead of after the whole
+ * exchange.  xr must be a symmetric allocation of moe_recv_rows_max rows (else
+ * MOE_ERR_NOT_SYMMETRIC); f % 128 == 0; counts [E] device int32 from moe_permute; xs may be
+ * NULL when T_local == 0.  Follow with moe_expert_ffn_down_combine.  A peer that never
+ * arrives faults the kernel after 10 s (MOE_ERR_TIMEOUT in the device error word). */
+moe_status moe_dispatch_expert_ffn_up(moe_ctx* ctx, const moe_bf16* xs, const int32_t* counts,
+                                      int32_t* layout, moe_bf16* xr, const moe_bf16* w_gu,
+                                      moe_bf16* g_u_h, moe_stream stream);
 /* Collective.  B4 + B3 in one call: as moe_expert_ffn_bwd for the routed experts, but the
  * dgrad-2 epilogue stores every dX row straight into its source rank's dxs (symmetric) at
  * the send-layout row; the weight-gradient GEMMs run while those stores drain, and the call

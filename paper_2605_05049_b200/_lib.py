@@ -97,6 +97,7 @@ _SIGS = {
     "moe_dispatch_range": [P, P, P, P, P, I32, I32, P],
     "moe_combine_bwd_range": [P, P, P, P, P, P, P, P, I32, I32, P],
     "moe_expert_ffn_up": [P, P, P, I32, I32, P, P, P],
+    "moe_dispatch_expert_ffn_up": [P, P, P, P, P, P, P, P],
     "moe_expert_ffn_down_combine": [P, P, P, P, P, P, P, P, P, P],
     "moe_expert_ffn_bwd_dh": [P, P, I32, I32, P, P, P, P, P],
     "moe_expert_ffn_bwd_dx_dispatch": [P, P, P, P, P, P, P, P, P, P, ctypes.c_int, P],
@@ -473,6 +474,13 @@ def moe_expert_ffn_up(ctx, xr, layout, slot_begin, slot_end, w_gu, g_u_h, stream
     _check("moe_expert_ffn_up", _lib.moe_expert_ffn_up(
         ctx.handle, _ptr(xr, BF16, "xr"), _ptr(layout, I32T, "layout"), int(slot_begin),
         int(slot_end), _ptr(w_gu, BF16, "w_gu"), _ptr(g_u_h, BF16, "g_u_h"), _stream(stream)))
+
+
+def moe_dispatch_expert_ffn_up(ctx, xs, counts, layout, xr, w_gu, g_u_h, stream=None):
+    _check("moe_dispatch_expert_ffn_up", _lib.moe_dispatch_expert_ffn_up(
+        ctx.handle, _ptr(xs, BF16, "xs"), _ptr(counts, I32T, "counts"),
+        _ptr(layout, I32T, "layout"), _ptr(xr, BF16, "xr"), _ptr(w_gu, BF16, "w_gu"),
+        _ptr(g_u_h, BF16, "g_u_h"), _stream(stream)))
 
 
 def moe_expert_ffn_down_combine(ctx, layout, w_down, g_u_h, ys, gates, dest_row, y_extra, y,

@@ -24,6 +24,7 @@ struct moe_ctx {
   int64_t countmat_off = 0;
   int64_t ntokmat_off = 0;
   int64_t flags_off = 0;
+  int64_t arrive_off = 0;         // fused dispatch arrival flags [E_l][EP+1] (NEXT-1)
   cudaIpcMemHandle_t handle;
   char* peer_base[MOE_MAX_EP] = {};
   bool peer_opened[MOE_MAX_EP] = {};
@@ -34,6 +35,7 @@ struct moe_ctx {
   int32_t* d_scratch = nullptr;   // permute workspace
   int32_t* d_dedup_scratch = nullptr;   // dedup pairs workspace (masks, block bases, ticket)
   int32_t* d_rows_T = nullptr;    // one int32 = T_local (router GEMM group size)
+  int32_t* d_disp_work = nullptr; // fused dispatch counters [4 + E + E_l] (zero between calls)
   uint16_t* d_dl_split = nullptr; // router backward: [T, 2*Ep] bf16 = [hi | lo] of dlogits
   uint16_t* d_wr2 = nullptr;      // [2*Ep, d] bf16 = [W_r; W_r] (dense dx_router path)
   float* d_dwr_part = nullptr;    // [S, 2*Ep, d] fp32 split-K partials of dW_r
@@ -271,7 +273,9 @@ moe_status moe_ctx_create(moe_ctx** out, const moe_shape* shape, int device, siz
   c->countmat_off = 0;
   c->ntokmat_off = ((2 * EP * shape->E * 4) + 255) / 256 * 256;
   c->flags_off = c->ntokmat_off + ((2 * EP * EP * 4) + 255) / 256 * 256;
-  c->internal_bytes = ((c->flags_off + moe::kNumSlots * EP * 8) + 4095) / 4096 * 4096;
+  c->arrive_off = c->flags_off + ((moe::kNumSlots * EP * 8) + 255) / 256 * 256;
+  c->internal_bytes =
+      ((c->arrive_off + static_cast<int64_t>(c->E_l) * (EP + 1) * 8) + 4095) / 4096 * 4096;
   c->heap_bytes = c->internal_bytes + (symm_heap_bytes + 255) / 256 * 256;
   c->heap_used = c->internal_bytes;
   e = ctx_malloc(c, &c->heap, c->heap_bytes);
@@ -287,6 +291,9 @@ moe_status moe_ctx_create(moe_ctx** out, const moe_shape* shape, int device, siz
   const int64_t dscratch = moe::dedup_scratch_ints(shape->T_local, shape->ep_size);
   if (e == cudaSuccess) e = ctx_malloc(c, &c->d_dedup_scratch, dscratch * 4);
   if (e == cudaSuccess) e = cudaMemset(c->d_dedup_scratch, 0, dscratch * 4);
+  const size_t work_bytes = static_cast<size_t>(4 + shape->E + c->E_l) * 4;
+  if (e == cudaSuccess) e = ctx_malloc(c, &c->d_disp_work, work_bytes);
+  if (e == cudaSuccess) e = cudaMemset(c->d_disp_work, 0, work_bytes);
   if (e == cudaSuccess) e = ctx_malloc(c, &c->d_rows_T, 16);
   int32_t tl = static_cast<int32_t>(shape->T_local);
   if (e == cudaSuccess) e = cudaMemcpy(c->d_rows_T, &tl, 4, cudaMemcpyHostToDevice);
@@ -540,6 +547,7 @@ moe_status moe_ctx_destroy(moe_ctx* c) {
   cudaFree(c->d_scratch);
   cudaFree(c->d_dedup_scratch);
   cudaFree(c->d_rows_T);
+  cudaFree(c->d_disp_work);
   cudaFree(c->d_dl_split);
   cudaFree(c->d_wr2);
   cudaFree(c->d_dwr_part);
@@ -906,6 +914,34 @@ moe_status moe_expert_ffn_up(moe_ctx* c, const moe_bf16* xr, const int32_t* layo
   MOE_REQUIRE(slot_begin >= 0 && slot_begin < slot_end && slot_end <= c->E_l);
   const int32_t* expert_rows = layout + static_cast<int64_t>(c->s.ep_size) * c->s.E;
   return ffn_up(c, xr, expert_rows, slot_begin, slot_end, c->recv_rows, c->s.f, w_gu, g_u_h, s);
+}
+
+moe_status moe_dispatch_expert_ffn_up(moe_ctx* c, const moe_bf16* xs, const int32_t* counts,
+                                      int32_t* layout, moe_bf16* xr, const moe_bf16* w_gu,
+                                      moe_bf16* g_u_h, moe_stream s) {
+  MOE_REQUIRE(c && TOKP(xs) && counts && layout && xr && w_gu && g_u_h);
+  MOE_REQUIRE(c->s.f % 128 == 0);
+  if (!c->peers_ready) return MOE_ERR_NOT_READY;
+  if (!in_heap(c, xr, recv_bytes(c))) return MOE_ERR_NOT_SYMMETRIC;
+  CommArgs a = comm_args(c);
+  const int d = c->s.d, f = c->s.f;
+  moe::GemmProblem g1;
+  g1.epi = moe::kEpiSwiGLUDisp;
+  g1.BN = 256;
+  g1.a_ptr = xr; g1.a_rows = c->recv_rows; g1.a_cols = d; g1.a_ld = d;
+  g1.b_ptr = w_gu; g1.b_rows = static_cast<int64_t>(c->E_l) * 2 * f; g1.b_cols = d; g1.b_ld = d;
+  g1.b_group_stride = 2 * f; g1.b_split = f;
+  g1.N = 2 * f; g1.K = d;
+  g1.n_groups = c->E_l; g1.rows_cap = c->recv_rows;
+  g1.pair = gemm_pair();
+  g1.max_ctas = c->gemm_sms;
+  g1.out = g_u_h; g1.ld_out = 3 * static_cast<int64_t>(f); g1.f = f;
+  g1.comm = &a;
+  g1.disp_src = xs; g1.disp_counts = counts; g1.disp_layout = layout;
+  g1.disp_dst_off = heap_off(c, xr);
+  g1.arrive_off = c->arrive_off;
+  g1.disp_work = c->d_disp_work;
+  return cuda_status(moe::launch_grouped_gemm(g1, st(s)));
 }
 
 moe_status moe_expert_ffn_down_combine(moe_ctx* c, const int32_t* layout, const moe_bf16* w_down,

@@ -41,16 +41,6 @@ __device__ __forceinline__ uint64_t* peer_flag(const CommArgs& a, int q, int slo
   return reinterpret_cast<uint64_t*>(peer_base(a, q) + a.flags_off) + slot * a.ep + src;
 }
 
-__device__ __forceinline__ int upper_bound_idx(const int32_t* arr, int n, int64_t v) {
-  // largest i in [0, n) with arr[i] <= v  (arr ascending, arr[0] = 0)
-  int lo = 0, hi = n;
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (arr[mid] <= v) lo = mid; else hi = mid;
-  }
-  return lo;
-}
-
 __device__ void wait_all(const CommArgs& a, int slot);
 
 __device__ __forceinline__ uint64_t load_epoch(const CommArgs& a) {
@@ -157,27 +147,6 @@ struct FwdTables {
   int32_t seg[kMaxE + 1];
   int32_t rows[kMaxE];
 };
-
-// Exclusive scan by ONE warp of n values val(i) (i ascending); out(i, prefix) is called for
-// every i < n with its exclusive prefix.  Returns the total (in every lane).
-template <typename V, typename O>
-__device__ __forceinline__ int32_t warp_scan(int n, V val, O out) {
-  const int lane = threadIdx.x & 31;
-  int32_t carry = 0;
-  for (int base = 0; base < n; base += 32) {
-    const int i = base + lane;
-    const int32_t c = i < n ? val(i) : 0;
-    int32_t x = c;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
-    }
-    if (i < n) out(i, carry + x - c);
-    carry += __shfl_sync(0xffffffffu, x, 31);
-  }
-  return carry;
-}
 
 // Needs blockDim >= 32 (EP + 1): warps 0..EP-1 scan the owners' segments, warp EP the send
 // layout (every transfer kernel runs 512 threads; a 256-thread variant broke EP = 8).

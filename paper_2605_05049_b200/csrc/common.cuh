@@ -370,4 +370,36 @@ __device__ __forceinline__ void acc_bf16x8(float (&acc)[8], uint4 v, float scale
   }
 }
 
+// largest i in [0, n) with arr[i] <= v  (arr ascending, arr[0] = 0)
+MOE_DEVINL int upper_bound_idx(const int32_t* arr, int n, int64_t v) {
+  int lo = 0, hi = n;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (arr[mid] <= v) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// ---------------------------------------------------------------- warp scan
+// Exclusive scan by ONE warp of n values val(i) (i ascending); out(i, prefix) is called for
+// every i < n with its exclusive prefix.  Returns the total (in every lane).
+template <typename V, typename O>
+MOE_DEVINL int32_t warp_scan(int n, V val, O out) {
+  const int lane = threadIdx.x & 31;
+  int32_t carry = 0;
+  for (int base = 0; base < n; base += 32) {
+    const int i = base + lane;
+    const int32_t c = i < n ? val(i) : 0;
+    int32_t x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (i < n) out(i, carry + x - c);
+    carry += __shfl_sync(0xffffffffu, x, 31);
+  }
+  return carry;
+}
+
 }  // namespace moe

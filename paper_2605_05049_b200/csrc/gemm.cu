@@ -63,6 +63,13 @@ struct KParams {
   int64_t scatter_off;
   const int32_t* scatter_layout;
   CommArgs comm;
+  // kEpiSwiGLUDisp (NEXT-1): the dispatch fused in front of GEMM1 (see disp_prologue)
+  const uint16_t* disp_src;
+  const int32_t* disp_counts;
+  int32_t* disp_layout;
+  int64_t disp_dst_off;
+  int64_t arrive_off;
+  int32_t* work;
 };
 
 // STG = staging boxes per epilogue warp.  2 double-buffers the fp32 wgrad epilogue (its K is
@@ -70,7 +77,7 @@ struct KParams {
 // on the V3-like rank slice (ncu, profiles/r01/README.md): wgrad 1.63 -> 1.70 ms and
 // 3.29 -> 3.41 ms, i.e. slower -- the ring stage is worth more; kept at 1.
 constexpr int kWgradStaging = 1;
-template <int BN, int PAIR, int STG = 1>
+template <int BN, int PAIR, int STG = 1, int EXTRA = 0>
 struct Cfg {
   static constexpr int A_BYTES = kBM * kBK * 2;
   static constexpr int B_BYTES = (BN / PAIR) * kBK * 2;  // a CTA pair splits B along N
@@ -85,10 +92,14 @@ struct Cfg {
                                    : (2 * ACC_STRIDE <= 256) ? 256
                                                              : 512;
   // ring + epilogue staging + barriers/tables (incl. scatter tables) + alignment slack
-  static constexpr int SMEM = RING + 4 * STG * kStageBox + 6144 + 1024;
+  static constexpr int SMEM = RING + 4 * STG * kStageBox + 6144 + 1024 + EXTRA;
 };
 template <int EPI>
 __host__ __device__ constexpr int staging_boxes() { return EPI == kEpiF32Group ? kWgradStaging : 1; }
+// fused dispatch tables (6 E + E_l + 3 ints, E <= 256) beyond the common table area
+constexpr int kDispSmem = 8192;
+template <int EPI>
+__host__ __device__ constexpr int extra_smem() { return EPI == kEpiSwiGLUDisp ? kDispSmem : 0; }
 
 __device__ __forceinline__ int ceil_div(int a, int b) { return (a + b - 1) / b; }
 
@@ -154,6 +165,324 @@ __device__ __forceinline__ float rcp_approx(float x) {
 __device__ __forceinline__ float sigmoid_f(float g) { return rcp_approx(1.f + __expf(-g)); }
 __device__ __forceinline__ float silu_f(float g) { return g * sigmoid_f(g); }
 
+// ---------------------------------------------------------------- NEXT-1 fused dispatch
+// kEpiSwiGLUDisp runs the dispatch all-to-all (F3) INSIDE the GEMM1
+// launch, so GEMM1 tiles start as their rows land instead of after the whole exchange
+// ("computation-communication overlap within MoE layers"):
+//   * prologue (all threads of every CTA): the counts exchange and the forward-pattern tables
+//     of comm.cu's dispatch (same definitions: owner segments 128-aligned in slot order, rows
+//     of a slot ordered by source rank), from which the GEMM's own group tables follow;
+//   * warps 2-3 of every CTA (idle in a plain GEMM) push this rank's send rows into their
+//     owners' receive rows with 16-byte peer stores, 2 KB row parts claimed in chunks from a
+//     global counter (so CTAs that start late -- or never, beside another kernel -- cannot
+//     hold back a transfer), zero this rank's own padding rows, and count the parts done per
+//     (owner, slot) segment; the warp that completes a segment releases the arrival flag
+//     arrive[slot][source] = epoch in the owner's heap;
+//   * the TMA producer, before the first A box of a tile, waits for the flags of exactly the
+//     sources whose rows fall into its 128 rows (+ the padding flag), then orders the async
+//     proxy after the acquire.
+// The kernel ends the collective like comm.cu's dispatch: data flags to every peer, wait for
+// every peer's, commit the epoch -- so the next collectives see the same protocol state.
+struct DispTables {
+  int* rows;     // [E]     rows of expert e over all sources
+  int* dst;      // [E]     receive row of this rank's first row of expert e at its owner
+  int* off;      // [E+1]   this rank's send layout (exclusive scan of its counts)
+  int* sg_pre;   // [E+1]   transfer order i (owner rank+1 first, self last): row prefix
+  int* sg_src;   // [E]
+  int* sg_dst;   // [E]
+  int* pad_pre;  // [E_l+1] padding rows of this rank's slots, prefix
+  uint64_t* epoch;   // [1]
+  int* first;        // [1] this CTA won the counts ticket
+};
+constexpr int kDispChunk = 8;   // row parts (2 KB each) claimed per atomic
+
+__device__ __forceinline__ uint64_t* arrive_flag(const KParams& p, int q, int el, int src) {
+  return reinterpret_cast<uint64_t*>(peer_base(p.comm, q) + p.arrive_off) + el * (p.comm.ep + 1) + src;
+}
+
+__device__ __forceinline__ void spin_flag(const uint64_t* f, uint64_t v, int32_t* err) {
+  const uint64_t t0 = globaltimer_ns();
+  while (ld_acquire_sys(f) < v) {
+    if (globaltimer_ns() - t0 > 10ull * 1000 * 1000 * 1000) {
+      set_device_error(err, kDevTimeout);   // a peer never arrived: sticky fault (comm.cu)
+      __threadfence_system();
+      __trap();
+    }
+    __nanosleep(64);
+  }
+}
+
+// All threads of the CTA.  Fills the GEMM group tables (s_rows/s_seg/s_tile_prefix over the
+// E_l local slots), s_pre[r][el] (rows of slot el from sources < r), and t.
+template <int TILE_M, int BN>
+__device__ void disp_prologue(const KParams& p, const DispTables& t, int* s_rows, int* s_seg,
+                              int* s_tile_prefix, int* s_pre, int* s_arrived) {
+  const CommArgs& a = p.comm;
+  const int E = a.E, EP = a.ep, E_l = a.E_l, me = a.rank;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    *t.epoch = *reinterpret_cast<volatile const uint64_t*>(a.epoch_ptr) + 1;
+    *t.first = atomicAdd(p.work + 1, 1) == 0;
+  }
+  __syncthreads();
+  const uint64_t epoch = *t.epoch;
+  if (*t.first) {   // counts exchange: this rank's row of every peer's count matrix
+    for (int i = threadIdx.x; i < EP * E; i += blockDim.x) {
+      const int q = i / E, e = i % E;
+      reinterpret_cast<int32_t*>(peer_base(a, q) + a.countmat_off)[me * E + e] = p.disp_counts[e];
+    }
+    __syncthreads();   // orders the block's count stores before the lanes' releases
+    if (threadIdx.x < EP)
+      st_release_sys(reinterpret_cast<uint64_t*>(peer_base(a, threadIdx.x) + a.flags_off) +
+                         kSlotCounts * EP + me, epoch);
+  }
+  if (threadIdx.x < EP) spin_flag(a.flags + kSlotCounts * EP + threadIdx.x, epoch, a.err);
+  __threadfence();
+  __syncthreads();
+  const int32_t* cm = a.countmat;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int all = 0, before = 0;
+    for (int r = 0; r < EP; ++r) {
+      const int c = cm[r * E + e];
+      all += c;
+      if (r < me) before += c;
+    }
+    t.rows[e] = all;
+    t.dst[e] = before;
+  }
+  for (int el = threadIdx.x; el < E_l; el += blockDim.x) s_arrived[el] = 0;
+  __syncthreads();
+  for (int q = warp; q < EP; q += kThreads / 32) {   // owner q's 128-aligned slot segments
+    const int32_t total = warp_scan(
+        E_l,
+        [&](int el) {
+          const int32_t r = t.rows[a.expert_at[q * E_l + el]];
+          return (r + MOE_ALIGN_ROWS - 1) / MOE_ALIGN_ROWS * MOE_ALIGN_ROWS;
+        },
+        [&](int el, int32_t pre) {
+          if (q == me) s_seg[el] = pre;
+          t.dst[a.expert_at[q * E_l + el]] += pre;
+        });
+    if (q == me && lane == 0) s_seg[E_l] = total;
+  }
+  __syncthreads();
+  if (warp == 0) {          // send layout
+    const int32_t total = warp_scan(
+        E, [&](int e) { return cm[me * E + e]; }, [&](int e, int32_t pre) { t.off[e] = pre; });
+    if (lane == 0) t.off[E] = total;
+  } else if (warp == 1) {   // GEMM group tables of the local slots
+    const int NT = ceil_div(p.N, BN);
+    const int32_t total = warp_scan(
+        E_l,
+        [&](int el) {
+          const int r = t.rows[a.expert_at[me * E_l + el]];
+          s_rows[el] = r;
+          return ceil_div(r, TILE_M) * NT;
+        },
+        [&](int el, int32_t pre) { s_tile_prefix[el] = pre; });
+    if (lane == 0) s_tile_prefix[E_l] = total;
+  } else if (warp == 2) {   // padding rows of the local slots
+    const int32_t total = warp_scan(
+        E_l,
+        [&](int el) {
+          const int r = t.rows[a.expert_at[me * E_l + el]];
+          return (r + MOE_ALIGN_ROWS - 1) / MOE_ALIGN_ROWS * MOE_ALIGN_ROWS - r;
+        },
+        [&](int el, int32_t pre) { t.pad_pre[el] = pre; });
+    if (lane == 0) t.pad_pre[E_l] = total;
+  } else if (warp == 3) {   // receive order inside a slot: rows from sources < r
+    for (int el = lane; el < E_l; el += 32) {
+      const int e = a.expert_at[me * E_l + el];
+      int run = 0;
+      for (int r = 0; r < EP; ++r) {
+        s_pre[r * E_l + el] = run;
+        run += cm[r * E + e];
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < E; i += blockDim.x) {   // transfer order
+    const int q = (me + 1 + i / E_l) % EP, el = i % E_l, e = a.expert_at[q * E_l + el];
+    t.sg_src[i] = t.off[e];
+    t.sg_dst[i] = t.dst[e];
+  }
+  if (warp == 0) {
+    const int32_t total = warp_scan(
+        E,
+        [&](int i) {
+          const int q = (me + 1 + i / E_l) % EP, e = a.expert_at[q * E_l + i % E_l];
+          return t.off[e + 1] - t.off[e];
+        },
+        [&](int i, int32_t pre) { t.sg_pre[i] = pre; });
+    if (lane == 0) t.sg_pre[E] = total;
+  }
+  if (*t.first) {   // layout record for the later calls of this layer (as comm.cu's dispatch)
+    for (int i = threadIdx.x; i < EP * E; i += blockDim.x) p.disp_layout[i] = cm[i];
+    for (int el = threadIdx.x; el < E_l; el += blockDim.x) p.disp_layout[EP * E + el] = s_rows[el];
+    for (int el = threadIdx.x; el <= E_l; el += blockDim.x) p.disp_layout[EP * E + E_l + el] = s_seg[el];
+    if (threadIdx.x == 0 && s_seg[E_l] > p.rows_cap) set_device_error(a.err, kDevOverflow);
+  }
+  __syncthreads();
+}
+
+// Warps 2-3: the transfer (see above), then the end of the collective.
+__device__ void disp_copy(const KParams& p, const DispTables& t, const int* s_rows,
+                          const int* s_seg) {
+  const CommArgs& a = p.comm;
+  const int E = a.E, EP = a.ep, E_l = a.E_l, me = a.rank;
+  const int lane = threadIdx.x & 31;
+  const uint64_t epoch = *t.epoch;
+  const int nvec = a.d / 8;
+  const int parts = (nvec + 127) / 128;
+  const int64_t row_bytes = static_cast<int64_t>(a.d) * 2;
+  const int n_pad = t.pad_pre[E_l] * parts;
+  const int n_items = n_pad + t.sg_pre[E] * parts;
+  int32_t* segcnt = p.work + 4;
+  char* xr_local = peer_base(a, me) + p.disp_dst_off;
+  // segment sid (< E: transfer segment, >= E: padding of slot sid - E) gained n parts
+  auto flush = [&](int sid, int n) {
+    __syncwarp();   // the warp's stores are ordered before lane 0's system fence
+    if (lane == 0 && n > 0) {
+      __threadfence_system();
+      const int target = sid < E ? (t.sg_pre[sid + 1] - t.sg_pre[sid]) * parts
+                                 : (t.pad_pre[sid - E + 1] - t.pad_pre[sid - E]) * parts;
+      if (atomicAdd(segcnt + sid, n) + n == target) {
+        __threadfence_system();
+        st_release_sys(sid < E ? arrive_flag(p, (me + 1 + sid / E_l) % EP, sid % E_l, me)
+                               : arrive_flag(p, me, sid - E, EP),
+                       epoch);
+      }
+    }
+    __syncwarp();
+  };
+  for (;;) {
+    int base = 0;
+    if (lane == 0) base = atomicAdd(p.work, kDispChunk);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (base >= n_items) break;
+    const int end = min(base + kDispChunk, n_items);
+    int cur = -1, ncur = 0;
+    for (int it = base; it < end; it += 2) {
+      // two row parts in flight per lane (8 x 16 B loads before the stores)
+      uint4 v[2][4];
+      uint4* dst[2] = {nullptr, nullptr};
+      int v0[2] = {0, 0}, sid[2] = {-1, -1};
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int item = it + h;
+        if (item >= end) break;
+        const uint4* src = nullptr;
+        int part;
+        if (item < n_pad) {
+          const int r = item / parts;
+          part = item - r * parts;
+          const int el = upper_bound_idx(t.pad_pre, E_l + 1, r);
+          const int64_t row = s_seg[el] + s_rows[el] + (r - t.pad_pre[el]);
+          dst[h] = reinterpret_cast<uint4*>(xr_local + row * row_bytes);
+          sid[h] = E + el;
+        } else {
+          const int j = item - n_pad;
+          const int r = j / parts;
+          part = j - r * parts;
+          const int i = upper_bound_idx(t.sg_pre, E + 1, r);
+          const int within = r - t.sg_pre[i];
+          const int q = (me + 1 + i / E_l) % EP;
+          dst[h] = reinterpret_cast<uint4*>(peer_base(a, q) + p.disp_dst_off +
+                                            static_cast<int64_t>(t.sg_dst[i] + within) * row_bytes);
+          src = reinterpret_cast<const uint4*>(p.disp_src + static_cast<int64_t>(t.sg_src[i] + within) * a.d);
+          sid[h] = i;
+        }
+        v0[h] = part * 128 + lane;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int vi = v0[h] + 32 * u;
+          v[h][u] = make_uint4(0u, 0u, 0u, 0u);
+          if (src && vi < nvec && vi < (part + 1) * 128) v[h][u] = ld_nc_v4(src + vi);
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (!dst[h]) continue;
+        const int part_end = (v0[h] - lane) + 128;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int vi = v0[h] + 32 * u;
+          if (vi < nvec && vi < part_end) st_v4(dst[h] + vi, v[h][u]);
+        }
+        if (sid[h] != cur) {
+          flush(cur, ncur);
+          cur = sid[h];
+          ncur = 0;
+        }
+        ++ncur;
+      }
+    }
+    flush(cur, ncur);
+  }
+  // both transfer warps of this CTA are done; the last CTA ends the collective
+  asm volatile("bar.sync 1, 64;" ::: "memory");
+  if ((threadIdx.x >> 5) == 2) {
+    int last = 0;
+    if (lane == 0) {
+      __threadfence_system();
+      last = atomicAdd(p.work + 2, 1) == static_cast<int>(gridDim.x) - 1;
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last) {
+      // every row of this rank has landed at its owner: data flag to every peer, then wait for
+      // every peer's (the count-matrix reuse argument of comm.cu's publish_counts needs it)
+      if (lane < EP) {
+        st_release_sys(reinterpret_cast<uint64_t*>(peer_base(a, lane) + a.flags_off) + kSlotData * EP + me,
+                       epoch);
+        spin_flag(a.flags + kSlotData * EP + lane, epoch, a.err);
+      }
+      __syncwarp();
+      for (int i = lane; i < 4 + E + E_l; i += 32) p.work[i] = 0;   // every CTA is past its uses
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) *reinterpret_cast<volatile uint64_t*>(a.epoch_ptr) = epoch;
+    }
+  }
+}
+
+// TMA producer of a fused-dispatch GEMM1: before the first A box of this CTA's 128 rows
+// [lo, lo + 128) of slot el, wait for the arrival flags of the sources whose rows (and of the
+// padding, which this rank zeroes) intersect them.  s_arrived caches flags already seen.
+__device__ __forceinline__ void disp_wait_rows(const KParams& p, int el, int lo, int rows_el,
+                                               const int* s_pre, int* s_arrived, uint64_t epoch) {
+  const int EP = p.comm.ep, E_l = p.comm.E_l;
+  const int alig = (rows_el + MOE_ALIGN_ROWS - 1) / MOE_ALIGN_ROWS * MOE_ALIGN_ROWS;
+  const int hi = min(lo + kBM, alig);
+  if (lo >= hi) return;
+  uint32_t need = 0;
+  for (int r = 0; r < EP; ++r) {
+    const int b = s_pre[r * E_l + el];
+    const int e = (r + 1 < EP) ? s_pre[(r + 1) * E_l + el] : rows_el;
+    if (b < e && b < hi && e > lo) need |= 1u << r;
+  }
+  if (rows_el < hi && rows_el < alig) need |= 1u << EP;
+  need &= ~static_cast<uint32_t>(s_arrived[el]);
+  if (!need) return;
+  const uint64_t* f = arrive_flag(p, p.comm.rank, el, 0);
+  const uint64_t t0 = globaltimer_ns();
+  while (need) {
+    for (int r = 0; r <= EP; ++r)
+      if (((need >> r) & 1u) && ld_acquire_sys(f + r) >= epoch) {
+        need &= ~(1u << r);
+        s_arrived[el] |= 1 << r;
+      }
+    if (need) {
+      if (globaltimer_ns() - t0 > 10ull * 1000 * 1000 * 1000) {
+        set_device_error(p.comm.err, kDevTimeout);
+        __threadfence_system();
+        __trap();
+      }
+      __nanosleep(32);
+    }
+  }
+  fence_async_global();   // the TMA (async proxy) reads below come after the acquire
+}
+
 // PAIR = 2: a cluster of two CTAs on one TPC runs tcgen05.mma.cta_group::2 with M = 256;
 // each CTA stages its own 128 A rows and half of the B tile, the leader (rank 0) issues the
 // MMAs for both, and each CTA's TMEM holds its 128 accumulator rows.
@@ -168,7 +497,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   // tail; every global access (group tables, operands, outputs) comes after the wait
   pdl_trigger();
   constexpr int STG = staging_boxes<EPI>();
-  using C = Cfg<BN, PAIR, STG>;
+  using C = Cfg<BN, PAIR, STG, extra_smem<EPI>()>;
+  constexpr bool DISP = (EPI == kEpiSwiGLUDisp);
+  constexpr bool SWIGLU = (EPI == kEpiSwiGLU || DISP);
   constexpr bool KGROUPED = (EPI == kEpiF32Group);
   constexpr int TILE_M = kBM * PAIR;
   constexpr uint32_t IDESC = idesc_bf16(TILE_M, BN, A_MN, B_MN);
@@ -192,6 +523,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   int* s_rows = s_seg + kMaxGroups + 1;                          // [kMaxGroups]
   int* s_pre = s_rows + kMaxGroups;                              // scatter: [EP][E_l] (<= 256)
   int* s_soff = s_pre + kMaxGroups;                              // scatter: [EP][E_l]
+  // DISP: s_soff holds the arrival cache; the transfer tables follow
+  DispTables dt;
+  if constexpr (DISP) {
+    int* q = s_soff + kMaxGroups;
+    dt.epoch = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(q) + 7) & ~uintptr_t(7));
+    dt.first = reinterpret_cast<int*>(dt.epoch + 1);
+    dt.rows = dt.first + 1;
+    dt.dst = dt.rows + kMaxGroups;
+    dt.off = dt.dst + kMaxGroups;
+    dt.sg_pre = dt.off + kMaxGroups + 1;
+    dt.sg_src = dt.sg_pre + kMaxGroups + 1;
+    dt.sg_dst = dt.sg_src + kMaxGroups;
+    dt.pad_pre = dt.sg_dst + kMaxGroups;
+  }
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -223,6 +568,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   pdl_wait();   // the previous kernel's outputs (this launch's inputs) are complete and visible
+  if constexpr (DISP) {
+    disp_prologue<TILE_M, BN>(p, dt, s_rows, s_seg, s_tile_prefix, s_pre, s_soff);
+  } else {
   // ---- group tables: seg_base = 128-aligned prefix of rows; tile prefix
   if (warp == 3) {
     const int NT = ceil_div(p.N, BN);
@@ -279,6 +627,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   }
+  }  // !DISP
   tc_fence_before();
   if (PAIR == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
@@ -303,6 +652,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (t < 0) break;
         const Tile tl = decode_tile<KGROUPED, BN, TILE_M>(t, s_tile_prefix, s_seg, s_rows,
                                                           n_groups, p);
+        if constexpr (DISP)
+          disp_wait_rows(p, tl.g, tl.m * TILE_M + static_cast<int>(rank) * kBM, tl.rows_g, s_pre,
+                         s_soff, *dt.epoch);
         for (int kb = 0; kb < tl.nkb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint32_t bar_addr = smem_u32(&full[stage]);
@@ -342,7 +694,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int i = 0; i < BNC / 64; ++i)
               load(b_dst + i * 8192, &tmB, tl.n * BN + static_cast<int>(rank) * BNC + i * 64, krow);
-          } else if (EPI == kEpiSwiGLU) {
+          } else if (SWIGLU) {
             const int r0 = static_cast<int>(tl.g * p.b_group_stride) + tl.n * (BN / 2);
             if (PAIR == 2) {  // rank 0: W_gate rows (acc cols [0,BN/2)), rank 1: W_up rows
               load(b_dst, &tmB, kb * kBK, r0 + (rank ? static_cast<int>(p.b_split) : 0));
@@ -403,6 +755,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
+  } else if (DISP && warp < 4) {
+    // ===================== fused dispatch (warps 2-3) =====================
+    if constexpr (DISP) disp_copy(p, dt, s_rows, s_seg);
   } else if (warp >= 4) {
     // ===================== epilogue =====================
     const int ew = warp - 4;  // TMEM lane quadrant ew*32 .. ew*32+31
@@ -437,7 +792,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t tacc =
           tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * C::ACC_STRIDE;
       if (box_in) {
-      if (EPI == kEpiSwiGLU) {
+      if (SWIGLU) {
         // acc cols [0, BN/2) = G, [BN/2, BN) = U for f-columns n*BN/2 ...; write G, U, H
 #pragma unroll 1
         for (int c0 = 0; c0 < BN / 2; c0 += 64) {
@@ -759,12 +1114,13 @@ bool make_tmap_bf16(CUtensorMap* tm, const void* ptr, int64_t rows, int64_t cols
 
 template <int BN, bool A_MN, bool B_MN, int EPI, int PAIR>
 cudaError_t launch_impl(const GemmProblem& g, cudaStream_t stream) {
-  using C = Cfg<BN, PAIR, staging_boxes<EPI>()>;
+  using C = Cfg<BN, PAIR, staging_boxes<EPI>(), extra_smem<EPI>()>;
+  constexpr bool SWIGLU = (EPI == kEpiSwiGLU || EPI == kEpiSwiGLUDisp);
   CUtensorMap ta, tb, tc;
   // A box: K-major {64 k, 128 rows}; MN-major {64 m, 64 k}
   if (!make_tmap_bf16(&ta, g.a_ptr, g.a_rows, g.a_cols, g.a_ld, 64, A_MN ? 64 : kBM))
     return cudaErrorInvalidValue;
-  const int b_box_rows = B_MN ? 64 : (EPI == kEpiSwiGLU ? BN / 2 : BN / PAIR);
+  const int b_box_rows = B_MN ? 64 : (SWIGLU ? BN / 2 : BN / PAIR);
   if (!make_tmap_bf16(&tb, g.b_ptr, g.b_rows, g.b_cols, g.b_ld, 64, b_box_rows))
     return cudaErrorInvalidValue;
   KParams kp;
@@ -785,7 +1141,7 @@ cudaError_t launch_impl(const GemmProblem& g, cudaStream_t stream) {
       tc = ta;
     }
   } else {
-    const int64_t cols = (EPI == kEpiSwiGLU) ? 3 * static_cast<int64_t>(g.f)
+    const int64_t cols = SWIGLU ? 3 * static_cast<int64_t>(g.f)
                          : (EPI == kEpiDSwiGLU) ? 2 * static_cast<int64_t>(g.f)
                                                 : g.N;
     if (!make_tmap_bf16(&tc, g.out, g.rows_cap, cols, g.ld_out, 64, 32)) return cudaErrorInvalidValue;
@@ -821,6 +1177,18 @@ cudaError_t launch_impl(const GemmProblem& g, cudaStream_t stream) {
     kp.scatter_off = g.scatter_off;
     kp.scatter_layout = g.scatter_layout;
     kp.comm = *g.comm;
+  }
+  if (EPI == kEpiSwiGLUDisp) {
+    if (!g.comm || !g.disp_counts || !g.disp_layout || !g.disp_work || g.n_groups != g.comm->E_l ||
+        g.comm->E > kMaxGroups)
+      return cudaErrorInvalidValue;
+    kp.comm = *g.comm;
+    kp.disp_src = static_cast<const uint16_t*>(g.disp_src);
+    kp.disp_counts = g.disp_counts;
+    kp.disp_layout = g.disp_layout;
+    kp.disp_dst_off = g.disp_dst_off;
+    kp.arrive_off = g.arrive_off;
+    kp.work = g.disp_work;
   }
   auto kern = grouped_gemm_kernel<BN, A_MN, B_MN, EPI, PAIR>;
   // launch state is per device (a process may drive several GPUs, one ctx each)
@@ -892,6 +1260,7 @@ cudaError_t launch_grouped_gemm(const GemmProblem& g, cudaStream_t s) {
   if (g.n_groups <= 0 || g.n_groups > kMaxGroups) return cudaErrorInvalidValue;
   MOE_GEMM_CASE(256, false, false, kEpiSwiGLU)
   MOE_GEMM_CASE(128, false, false, kEpiSwiGLU)
+  MOE_GEMM_CASE(256, false, false, kEpiSwiGLUDisp)
   MOE_GEMM_CASE(256, false, false, kEpiBF16)
   MOE_GEMM_CASE(128, false, false, kEpiBF16)
   MOE_GEMM_CASE(64, false, false, kEpiBF16)

@@ -52,6 +52,9 @@ enum Epilogue : int {
   kEpiDSwiGLU = 2,  // dgrad-1: acc = dH; reads G,U -> dG,dU bf16 into dgu
   kEpiF32Group = 3, // wgrad: fp32 [M,N] per group (K = the group's rows), optional accumulate
   kEpiF32Rows = 4,  // router logits: fp32 [rows,N] + bias
+  kEpiSwiGLUDisp = 5,  // GEMM1 + SwiGLU with the dispatch all-to-all fused in (NEXT-1):
+                       // warps 2-3 push this rank's send rows to their owners while the
+                       // producer starts each A tile as soon as its source rows have landed
 };
 
 struct GemmProblem {
@@ -86,6 +89,13 @@ struct GemmProblem {
   int64_t scatter_off = 0;
   const int32_t* scatter_layout = nullptr;  // counts_all [EP x E]
   const struct CommArgs* comm = nullptr;
+  // kEpiSwiGLUDisp only (group_rows unused: the group tables come from the counts exchange)
+  const void* disp_src = nullptr;      // send layout xs [T*k, d] (this rank's rows)
+  const int32_t* disp_counts = nullptr;  // this rank's per-expert counts [E]
+  int32_t* disp_layout = nullptr;      // layout record written by the kernel
+  int64_t disp_dst_off = 0;            // byte offset of xr (= a_ptr) inside every heap
+  int64_t arrive_off = 0;              // heap offset of the arrival flags [E_l][EP+1]
+  int32_t* disp_work = nullptr;        // local scratch, zero between calls: [4 + E + E_l]
 };
 
 cudaError_t launch_grouped_gemm(const GemmProblem& p, cudaStream_t stream);

@@ -17,6 +17,8 @@ from __future__ import annotations
 
 import dataclasses
 
+import os
+
 import torch
 
 from . import _lib as L
@@ -195,6 +197,11 @@ class MoELayer:
     # EP = 1: moe_permute_dispatch_local (no send-layout copy, no transfer); False = the
     # general permute + dispatch path (tests compare the two)
     local_fast_path = True
+    # NEXT-1 tile-granular overlap (fused path, EP > 1, no dedup): the dispatch runs inside
+    # the GEMM1 launch and every GEMM1 tile starts when its rows have arrived
+    # (moe_dispatch_expert_ffn_up); False = moe_dispatch, then GEMM1.  MOE_TILE_OVERLAP=0/1
+    # overrides.
+    tile_overlap = os.environ.get("MOE_TILE_OVERLAP", "1") != "0"
     # per-phase CUDA-event markers (bench.py --breakdown); off by default
     marks = None
     # SMs given to an all-to-all that runs beside a GEMM (the GEMM gets the rest).  Measured on
@@ -272,6 +279,20 @@ class MoELayer:
         L.moe_permute(c, x, self.topk_idx, self.counts, self.dest_row, self.xs)
         self._mark("F2 permute")
         y_extra = None
+        if self._tile_overlap():
+            # F3 + F4 up in one launch: GEMM1 tiles start as their rows land (NEXT-1)
+            L.moe_dispatch_expert_ffn_up(c, self.xs, self.counts, self.layout, self.xr, self.w_gu,
+                                         self.g_u_h)
+            self._mark("F3+F4 dispatch + GEMM1 (tile-granular overlap)")
+            if self.fs:
+                L.moe_expert_ffn(c, x, self.rows_T, 1, T, self.fs, self.w_gu_s, self.w_down_s,
+                                 self.g_u_h_s, self.y_s)
+                y_extra = self.y_s
+                self._mark("F4s shared ffn")
+            L.moe_expert_ffn_down_combine(c, self.layout, self.w_down, self.g_u_h, self.ys,
+                                          self.gates, self.dest_row, y_extra, self.y)
+            self._mark("F4+F5+F6 GEMM2 + combine")
+            return self.y
         if self.fs and self.overlap:
             # shared experts (local tokens, no exchange) run beside the dispatch all-to-all on
             # disjoint SMs: dispatch on a side stream, shared GEMMs on this one
@@ -615,6 +636,10 @@ class MoELayer:
         r, E_l = self.dims.ep_rank, self.E_l
         return inv[r * E_l:(r + 1) * E_l]
 
+    def _tile_overlap(self) -> bool:
+        # (EP = 1 reaches the general path only with local_fast_path = False, i.e. in tests)
+        return self.tile_overlap and self.fused and not self.dedup
+
     def kernel_launches(self, fwd=True, bwd=True) -> int:
         """Number of libmoe kernels one forward / backward launches (for bench.py)."""
         n = 0
@@ -641,6 +666,8 @@ class MoELayer:
         if fwd:
             # router GEMM, route, permute (3), dispatch (1 fused launch), ffn (2), combine (2)
             n += 1 + 1 + 3 + 1 + 2 + 2 + (2 if self.fs else 0)
+            if self._tile_overlap():
+                n -= 1   # dispatch + GEMM1 are one launch
         if bwd:
             # combine_bwd (1), ffn_bwd (4), dispatch_bwd (1), route_bwd,
             # router bwd (hi/lo split, split-K dW_r GEMM, partial sum; k = 1 adds the

@@ -100,7 +100,10 @@ def main():
             for el in range(E_l):
                 state_ok &= bool(torch.equal(t[el], code(inv[rank * E_l + el]) * (i + 1)))
     outs = []
-    for _ in range(args.iters):  # epoch reuse: repeated calls must be bit-identical
+    for it in range(args.iters):  # epoch reuse: repeated calls must be bit-identical
+        # alternate the NEXT-1 tile-granular dispatch -> GEMM1 launch with the separate
+        # dispatch + GEMM1 (fused path): both must give the same bits
+        layer.tile_overlap = it % 2 == 0
         y = layer.forward(x).clone()
         dx = layer.backward(dy).clone()
         outs.append((y, dx, layer.dw_gu.clone()))

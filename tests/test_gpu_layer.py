@@ -327,3 +327,42 @@ def test_ep1_local_path_bit_identical(name):
             layer.close()
         for a, b in zip(*outs):
             assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("name", ["mixtral_small", "dsmoe_small", "drops", "v3_small_zipf"])
+def test_tile_overlap_bit_identical(name):
+    """NEXT-1 tile-granular overlap (moe_dispatch_expert_ffn_up: the dispatch inside the GEMM1
+    launch, tiles gated by per-(slot, source) arrival flags) against moe_dispatch +
+    moe_expert_ffn_up on the general path at EP = 1 (the transfer then targets this rank's
+    own heap): layout record, xr incl. zeroed padding, G|U|H, y, dx and the weight gradients
+    bit for bit, over repeated steps (the flag epochs and the work counters must reset) and
+    under a migrated placement."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    cfg = CASES[name]
+    x = synth.tokens(cfg).cuda()
+    dy = synth.grad_output(cfg).cuda()
+    perm = np.random.default_rng(5).permutation(cfg.E)
+    for place in (None, perm):
+        outs = []
+        for tile in (True, False):
+            layer = build_layer(cfg)
+            layer.local_fast_path = False
+            layer.tile_overlap = tile
+            if place is not None:
+                layer.migrate(place)
+            for step in range(3):
+                layer.xr.fill_(3.0)          # stale rows must be overwritten or zeroed
+                layer.g_u_h.fill_(5.0)
+                y = layer.forward(x).clone()
+                dx = layer.backward(dy).clone()
+                torch.cuda.synchronize()
+                layer.ctx.check_device_error()
+                n = int(layer.layout[-1].item())
+                outs.append((y, dx, layer.dw_gu.clone(), layer.dw_down.clone(),
+                             layer.layout.clone(), layer.xr[:n].clone(), layer.g_u_h[:n].clone()))
+            layer.close()
+        ref = outs[0]
+        for o in outs[1:]:
+            for a, b in zip(ref, o):
+                assert torch.equal(a, b)
