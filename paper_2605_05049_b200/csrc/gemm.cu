@@ -194,7 +194,14 @@ struct DispTables {
   uint64_t* epoch;   // [1]
   int* first;        // [1] this CTA won the counts ticket
 };
-constexpr int kDispChunk = 8;   // row parts (2 KB each) claimed per atomic
+constexpr int kDispChunk = 16;  // row parts (2 KB each) claimed per atomic
+constexpr int kDispInFlight = 4; // row parts a warp loads before storing them
+// Transfer order i: slot-major (el = i / EP), owners rotated inside a slot (owner rank+1
+// first, self last) -- every owner's slot 0 completes first, from all sources at once, which
+// is the order GEMM1 consumes its tiles in (groups ascending); the rotation keeps the sources
+// of a moment on different receivers' links.
+__device__ __forceinline__ int seg_owner(int i, int me, int EP) { return (me + 1 + i % EP) % EP; }
+__device__ __forceinline__ int seg_slot(int i, int EP) { return i / EP; }
 
 __device__ __forceinline__ uint64_t* arrive_flag(const KParams& p, int q, int el, int src) {
   return reinterpret_cast<uint64_t*>(peer_base(p.comm, q) + p.arrive_off) + el * (p.comm.ep + 1) + src;
@@ -302,7 +309,7 @@ __device__ void disp_prologue(const KParams& p, const DispTables& t, int* s_rows
   }
   __syncthreads();
   for (int i = threadIdx.x; i < E; i += blockDim.x) {   // transfer order
-    const int q = (me + 1 + i / E_l) % EP, el = i % E_l, e = a.expert_at[q * E_l + el];
+    const int q = seg_owner(i, me, EP), el = seg_slot(i, EP), e = a.expert_at[q * E_l + el];
     t.sg_src[i] = t.off[e];
     t.sg_dst[i] = t.dst[e];
   }
@@ -310,7 +317,7 @@ __device__ void disp_prologue(const KParams& p, const DispTables& t, int* s_rows
     const int32_t total = warp_scan(
         E,
         [&](int i) {
-          const int q = (me + 1 + i / E_l) % EP, e = a.expert_at[q * E_l + i % E_l];
+          const int e = a.expert_at[seg_owner(i, me, EP) * E_l + seg_slot(i, EP)];
           return t.off[e + 1] - t.off[e];
         },
         [&](int i, int32_t pre) { t.sg_pre[i] = pre; });
@@ -348,7 +355,7 @@ __device__ void disp_copy(const KParams& p, const DispTables& t, const int* s_ro
                                  : (t.pad_pre[sid - E + 1] - t.pad_pre[sid - E]) * parts;
       if (atomicAdd(segcnt + sid, n) + n == target) {
         __threadfence_system();
-        st_release_sys(sid < E ? arrive_flag(p, (me + 1 + sid / E_l) % EP, sid % E_l, me)
+        st_release_sys(sid < E ? arrive_flag(p, seg_owner(sid, me, EP), seg_slot(sid, EP), me)
                                : arrive_flag(p, me, sid - E, EP),
                        epoch);
       }
@@ -362,15 +369,18 @@ __device__ void disp_copy(const KParams& p, const DispTables& t, const int* s_ro
     if (base >= n_items) break;
     const int end = min(base + kDispChunk, n_items);
     int cur = -1, ncur = 0;
-    for (int it = base; it < end; it += 2) {
-      // two row parts in flight per lane (8 x 16 B loads before the stores)
-      uint4 v[2][4];
-      uint4* dst[2] = {nullptr, nullptr};
-      int v0[2] = {0, 0}, sid[2] = {-1, -1};
+    for (int it = base; it < end; it += kDispInFlight) {
+      // kDispInFlight row parts in flight per lane (16 B x 4 each, all loads before the stores)
+      uint4 v[kDispInFlight][4];
+      uint4* dst[kDispInFlight];
+      int v0[kDispInFlight], sid[kDispInFlight];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < kDispInFlight; ++h) {
         const int item = it + h;
-        if (item >= end) break;
+        dst[h] = nullptr;
+        v0[h] = 0;
+        sid[h] = -1;
+        if (item >= end) continue;
         const uint4* src = nullptr;
         int part;
         if (item < n_pad) {
@@ -386,7 +396,7 @@ __device__ void disp_copy(const KParams& p, const DispTables& t, const int* s_ro
           part = j - r * parts;
           const int i = upper_bound_idx(t.sg_pre, E + 1, r);
           const int within = r - t.sg_pre[i];
-          const int q = (me + 1 + i / E_l) % EP;
+          const int q = seg_owner(i, me, EP);
           dst[h] = reinterpret_cast<uint4*>(peer_base(a, q) + p.disp_dst_off +
                                             static_cast<int64_t>(t.sg_dst[i] + within) * row_bytes);
           src = reinterpret_cast<const uint4*>(p.disp_src + static_cast<int64_t>(t.sg_src[i] + within) * a.d);
@@ -401,7 +411,7 @@ __device__ void disp_copy(const KParams& p, const DispTables& t, const int* s_ro
         }
       }
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < kDispInFlight; ++h) {
         if (!dst[h]) continue;
         const int part_end = (v0[h] - lane) + 128;
 #pragma unroll
@@ -767,7 +777,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t aph = 0;   // dSwiGLU: parity of this warp's G / U box barrier
     int acc = 0;
     uint32_t acc_phase = 0;
-    constexpr int kArrive = 4 * PAIR;  // epilogue warps of a cluster
     for (int w = 0;; ++w) {
       const int t = next_tile(w);
       if (t < 0) break;

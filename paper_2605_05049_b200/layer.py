@@ -197,11 +197,15 @@ class MoELayer:
     # EP = 1: moe_permute_dispatch_local (no send-layout copy, no transfer); False = the
     # general permute + dispatch path (tests compare the two)
     local_fast_path = True
-    # NEXT-1 tile-granular overlap (fused path, EP > 1, no dedup): the dispatch runs inside
-    # the GEMM1 launch and every GEMM1 tile starts when its rows have arrived
-    # (moe_dispatch_expert_ffn_up); False = moe_dispatch, then GEMM1.  MOE_TILE_OVERLAP=0/1
-    # overrides.
-    tile_overlap = os.environ.get("MOE_TILE_OVERLAP", "1") != "0"
+    # NEXT-1 tile-granular overlap (fused path, no dedup): the dispatch runs inside the GEMM1
+    # launch and every GEMM1 tile starts when its rows have arrived
+    # (moe_dispatch_expert_ffn_up); False = moe_dispatch, then GEMM1.  None = auto: on when a
+    # rank owns >= 8 experts -- GEMM1's first tiles wait for 1/E_l of the transfer (slot-major
+    # order), so fine-grained layers gain (4-GPU box, profiles/r02/tile_overlap: DS-MoE N=4
+    # 1.80 vs 1.84 ms, V3-like N=4 25.6-26.5 vs 26.5 ms) and coarse ones lose (Mixtral N=4,
+    # E_l = 2: 3.59-3.60 vs 3.52-3.55 ms).  MOE_TILE_OVERLAP=0/1 forces it.
+    tile_overlap = {"0": False, "1": True}.get(os.environ.get("MOE_TILE_OVERLAP", ""))
+    tile_overlap_min_experts = 8
     # per-phase CUDA-event markers (bench.py --breakdown); off by default
     marks = None
     # SMs given to an all-to-all that runs beside a GEMM (the GEMM gets the rest).  Measured on
@@ -638,7 +642,10 @@ class MoELayer:
 
     def _tile_overlap(self) -> bool:
         # (EP = 1 reaches the general path only with local_fast_path = False, i.e. in tests)
-        return self.tile_overlap and self.fused and not self.dedup
+        on = self.tile_overlap
+        if on is None:
+            on = self.E_l >= self.tile_overlap_min_experts
+        return bool(on) and self.fused and not self.dedup
 
     def kernel_launches(self, fwd=True, bwd=True) -> int:
         """Number of libmoe kernels one forward / backward launches (for bench.py)."""
