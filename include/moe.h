@@ -361,6 +361,21 @@ moe_status moe_expert_ffn_combine(moe_ctx* ctx, const moe_bf16* xr, const int32_
 moe_status moe_dispatch_expert_ffn_up(moe_ctx* ctx, const moe_bf16* xs, const int32_t* counts,
                                       int32_t* layout, moe_bf16* xr, const moe_bf16* w_gu,
                                       moe_bf16* g_u_h, moe_stream stream);
+/* Collective.  B6+B5 + B4 (dgrad-1) in ONE launch, the backward twin of
+ * moe_dispatch_expert_ffn_up: same arguments and results as moe_combine_bwd(dy, gates,
+ * dest_row, ys, layout, dgates, dout_r) followed by moe_expert_ffn_bwd_dh(layout, 0, E_l,
+ * w_down, g_u_h, dout_r, dgu) -- dout_r, dgates and dgu bit-identical -- with the transfer
+ * run by two warps of every dgrad-1 CTA in slot-major order (row r of the send layout carries
+ * bf16(g[t,j] dy[t]) for the slot (t,j) that moe_permute placed there; dgates[t,j] =
+ * <dy[t], ys[r]>) and every dO tile started as soon as its rows have arrived.  Requires the
+ * moe_permute of the same step (its row -> slot map) and the forward's layout record;
+ * dout_r symmetric of moe_recv_rows_max rows; f % 128 == 0.  Follow with
+ * moe_expert_ffn_bwd_dx_dispatch. */
+moe_status moe_combine_bwd_expert_ffn_dh(moe_ctx* ctx, const moe_bf16* dy, const float* gates,
+                                         const int32_t* dest_row, const moe_bf16* ys,
+                                         const int32_t* layout, float* dgates, moe_bf16* dout_r,
+                                         const moe_bf16* w_down, const moe_bf16* g_u_h,
+                                         moe_bf16* dgu, moe_stream stream);
 /* Collective.  B4 + B3 in one call: as moe_expert_ffn_bwd for the routed experts, but the
  * dgrad-2 epilogue stores every dX row straight into its source rank's dxs (symmetric) at
  * the send-layout row; the weight-gradient GEMMs run while those stores drain, and the call

@@ -98,6 +98,7 @@ _SIGS = {
     "moe_combine_bwd_range": [P, P, P, P, P, P, P, P, I32, I32, P],
     "moe_expert_ffn_up": [P, P, P, I32, I32, P, P, P],
     "moe_dispatch_expert_ffn_up": [P, P, P, P, P, P, P, P],
+    "moe_combine_bwd_expert_ffn_dh": [P] * 12,
     "moe_expert_ffn_down_combine": [P, P, P, P, P, P, P, P, P, P],
     "moe_expert_ffn_bwd_dh": [P, P, I32, I32, P, P, P, P, P],
     "moe_expert_ffn_bwd_dx_dispatch": [P, P, P, P, P, P, P, P, P, P, ctypes.c_int, P],
@@ -481,6 +482,15 @@ def moe_dispatch_expert_ffn_up(ctx, xs, counts, layout, xr, w_gu, g_u_h, stream=
         ctx.handle, _ptr(xs, BF16, "xs"), _ptr(counts, I32T, "counts"),
         _ptr(layout, I32T, "layout"), _ptr(xr, BF16, "xr"), _ptr(w_gu, BF16, "w_gu"),
         _ptr(g_u_h, BF16, "g_u_h"), _stream(stream)))
+
+
+def moe_combine_bwd_expert_ffn_dh(ctx, dy, gates, dest_row, ys, layout, dgates, dout_r, w_down,
+                                  g_u_h, dgu, stream=None):
+    _check("moe_combine_bwd_expert_ffn_dh", _lib.moe_combine_bwd_expert_ffn_dh(
+        ctx.handle, _ptr(dy, BF16, "dy"), _ptr(gates, F32, "gates"), _ptr(dest_row, I32T, "dest_row"),
+        _ptr(ys, BF16, "ys"), _ptr(layout, I32T, "layout"), _ptr(dgates, F32, "dgates"),
+        _ptr(dout_r, BF16, "dout_r"), _ptr(w_down, BF16, "w_down"), _ptr(g_u_h, BF16, "g_u_h"),
+        _ptr(dgu, BF16, "dgu"), _stream(stream)))
 
 
 def moe_expert_ffn_down_combine(ctx, layout, w_down, g_u_h, ys, gates, dest_row, y_extra, y,

@@ -36,6 +36,7 @@ struct moe_ctx {
   int32_t* d_dedup_scratch = nullptr;   // dedup pairs workspace (masks, block bases, ticket)
   int32_t* d_rows_T = nullptr;    // one int32 = T_local (router GEMM group size)
   int32_t* d_disp_work = nullptr; // fused dispatch counters [4 + E + E_l] (zero between calls)
+  int32_t* d_slot_of_row = nullptr; // [T*k] send-layout row -> slot t*k+j (moe_permute)
   uint16_t* d_dl_split = nullptr; // router backward: [T, 2*Ep] bf16 = [hi | lo] of dlogits
   uint16_t* d_wr2 = nullptr;      // [2*Ep, d] bf16 = [W_r; W_r] (dense dx_router path)
   float* d_dwr_part = nullptr;    // [S, 2*Ep, d] fp32 split-K partials of dW_r
@@ -294,6 +295,9 @@ moe_status moe_ctx_create(moe_ctx** out, const moe_shape* shape, int device, siz
   const size_t work_bytes = static_cast<size_t>(4 + shape->E + c->E_l) * 4;
   if (e == cudaSuccess) e = ctx_malloc(c, &c->d_disp_work, work_bytes);
   if (e == cudaSuccess) e = cudaMemset(c->d_disp_work, 0, work_bytes);
+  if (e == cudaSuccess)
+    e = ctx_malloc(c, &c->d_slot_of_row,
+                   static_cast<size_t>(shape->T_local > 0 ? shape->T_local * shape->k : 1) * 4);
   if (e == cudaSuccess) e = ctx_malloc(c, &c->d_rows_T, 16);
   int32_t tl = static_cast<int32_t>(shape->T_local);
   if (e == cudaSuccess) e = cudaMemcpy(c->d_rows_T, &tl, 4, cudaMemcpyHostToDevice);
@@ -548,6 +552,7 @@ moe_status moe_ctx_destroy(moe_ctx* c) {
   cudaFree(c->d_dedup_scratch);
   cudaFree(c->d_rows_T);
   cudaFree(c->d_disp_work);
+  cudaFree(c->d_slot_of_row);
   cudaFree(c->d_dl_split);
   cudaFree(c->d_wr2);
   cudaFree(c->d_dwr_part);
@@ -647,7 +652,8 @@ moe_status moe_permute(moe_ctx* c, const moe_bf16* x, const int32_t* topk_idx, i
                        int32_t* dest_row, moe_bf16* xs, moe_stream s) {
   MOE_REQUIRE(c && TOKP(x) && TOKP(topk_idx) && counts && TOKP(dest_row));   // xs NULL: indices only
   return cuda_status(moe::launch_permute(x, topk_idx, c->s.T_local, c->s.d, c->s.E, c->s.k, c->C,
-                                         counts, dest_row, xs, c->d_scratch, st(s)));
+                                         counts, dest_row, xs, c->d_scratch, st(s), nullptr,
+                                         nullptr, 0, c->d_slot_of_row));
 }
 
 moe_status moe_permute_dispatch_local(moe_ctx* c, const moe_bf16* x, const int32_t* topk_idx,
@@ -942,6 +948,40 @@ moe_status moe_dispatch_expert_ffn_up(moe_ctx* c, const moe_bf16* xs, const int3
   g1.arrive_off = c->arrive_off;
   g1.disp_work = c->d_disp_work;
   return cuda_status(moe::launch_grouped_gemm(g1, st(s)));
+}
+
+moe_status moe_combine_bwd_expert_ffn_dh(moe_ctx* c, const moe_bf16* dy, const float* gates,
+                                         const int32_t* dest_row, const moe_bf16* ys,
+                                         const int32_t* layout, float* dgates, moe_bf16* dout_r,
+                                         const moe_bf16* w_down, const moe_bf16* g_u_h,
+                                         moe_bf16* dgu, moe_stream s) {
+  MOE_REQUIRE(c && TOKP(dy) && TOKP(gates) && TOKP(dest_row) && TOKP(ys) && layout && TOKP(dgates) &&
+              dout_r && w_down && g_u_h && dgu);
+  MOE_REQUIRE(c->s.f % 128 == 0);
+  if (!c->peers_ready) return MOE_ERR_NOT_READY;
+  if (!in_heap(c, dout_r, recv_bytes(c))) return MOE_ERR_NOT_SYMMETRIC;
+  CommArgs a = comm_args(c);
+  const int d = c->s.d, f = c->s.f;
+  const int64_t F = f;
+  moe::GemmProblem g;
+  g.epi = moe::kEpiDSwiGLUComb;
+  g.BN = f >= 256 ? 256 : 128;   // as ffn_bwd_dh
+  g.b_mn = true;
+  g.a_ptr = dout_r; g.a_rows = c->recv_rows; g.a_cols = d; g.a_ld = d;
+  g.b_ptr = w_down; g.b_rows = static_cast<int64_t>(c->E_l) * d; g.b_cols = f; g.b_ld = f;
+  g.b_group_stride = d;
+  g.N = f; g.K = d;
+  g.n_groups = c->E_l; g.rows_cap = c->recv_rows;
+  g.pair = gemm_pair();
+  g.max_ctas = c->gemm_sms;
+  g.out = dgu; g.ld_out = 2 * F; g.aux = g_u_h; g.ld_aux = 3 * F; g.f = f;
+  g.comm = &a;
+  g.disp_dst_off = heap_off(c, dout_r);
+  g.arrive_off = c->arrive_off;
+  g.disp_work = c->d_disp_work;
+  g.cb_dy = dy; g.cb_gates = gates; g.cb_ys = ys; g.cb_dgates = dgates;
+  g.cb_slot_of_row = c->d_slot_of_row; g.cb_dest_row = dest_row; g.cb_layout = layout;
+  return cuda_status(moe::launch_grouped_gemm(g, st(s)));
 }
 
 moe_status moe_expert_ffn_down_combine(moe_ctx* c, const int32_t* layout, const moe_bf16* w_down,

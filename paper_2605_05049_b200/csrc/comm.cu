@@ -257,23 +257,11 @@ __device__ __forceinline__ float dot_scale_row(const uint4* __restrict__ a,
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       if (v0 + 32 * u >= nvec) break;
-      const uint32_t aw[4] = {av[u].x, av[u].y, av[u].z, av[u].w};
-      uint32_t ow[4];
-#pragma unroll
-      for (int q2 = 0; q2 < 4; ++q2) {
-        const float y0 = bf16_lo(aw[q2]), y1 = bf16_hi(aw[q2]);
-        if (b) {
-          const uint32_t bw = q2 == 0 ? bv[u].x : q2 == 1 ? bv[u].y : q2 == 2 ? bv[u].z : bv[u].w;
-          dot += y0 * bf16_lo(bw) + y1 * bf16_hi(bw);
-        }
-        ow[q2] = pack_bf16(g * y0, g * y1);
-      }
-      if (dst) st_v4(dst + v0 + 32 * u, make_uint4(ow[0], ow[1], ow[2], ow[3]));
+      const uint4 o = combine_bwd_vec(av[u], b ? bv[u] : make_uint4(0u, 0u, 0u, 0u), g, dot);
+      if (dst) st_v4(dst + v0 + 32 * u, o);
     }
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-  return dot;
+  return warp_sum(dot);
 }
 
 // Forward pattern.  mode 0: payload = src send row.  mode 1 (combine_bwd): payload of
@@ -410,25 +398,14 @@ __global__ void __launch_bounds__(512) forward_transfer_kernel(CommArgs a, int32
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             if (v0 + 32 * u >= nvec) break;
-            const uint32_t aw[4] = {av[u].x, av[u].y, av[u].z, av[u].w};
-            const uint32_t bw[4] = {bv[u].x, bv[u].y, bv[u].z, bv[u].w};
-            uint32_t ow[4];
-#pragma unroll
-            for (int q2 = 0; q2 < 4; ++q2) {
-              const float y0 = bf16_lo(aw[q2]), y1 = bf16_hi(aw[q2]);
-              dot[j] += y0 * bf16_lo(bw[q2]) + y1 * bf16_hi(bw[q2]);
-              ow[q2] = pack_bf16(gj[j] * y0, gj[j] * y1);
-            }
-            st_v4(dstp[j] + v0 + 32 * u, make_uint4(ow[0], ow[1], ow[2], ow[3]));
+            st_v4(dstp[j] + v0 + 32 * u, combine_bwd_vec(av[u], bv[u], gj[j], dot[j]));
           }
         }
       }
 #pragma unroll
       for (int j = 0; j < kDyK; ++j) {
         if (ysp[j] == nullptr) continue;
-        float v = dot[j];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        const float v = warp_sum(dot[j]);
         if (lane == 0) dgates[t * k + j] = v;
       }
     } else {

@@ -370,6 +370,30 @@ __device__ __forceinline__ void acc_bf16x8(float (&acc)[8], uint4 v, float scale
   }
 }
 
+// ---------------------------------------------------------------- combine_bwd arithmetic
+// One 16-byte vector of B6 (the combine in reverse): dot += <a, b> over its 8
+// bf16 pairs in a fixed order with explicit FMAs, and returns bf16(g * a).  Every combine_bwd
+// variant (transfer kernel, EP = 1 local kernel, the dgrad-1 fused transfer, dedup) uses it,
+// visiting a lane's vectors in increasing index and reducing over the warp with xor shuffles,
+// so all give identical dgates and dO bits.
+MOE_DEVINL uint4 combine_bwd_vec(uint4 a, uint4 b, float g, float& dot) {
+  const uint32_t aw[4] = {a.x, a.y, a.z, a.w};
+  const uint32_t bw[4] = {b.x, b.y, b.z, b.w};
+  uint32_t ow[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float y0 = bf16_lo(aw[q]), y1 = bf16_hi(aw[q]);
+    dot = __fmaf_rn(y1, bf16_hi(bw[q]), __fmaf_rn(y0, bf16_lo(bw[q]), dot));
+    ow[q] = pack_bf16(__fmul_rn(g, y0), __fmul_rn(g, y1));
+  }
+  return make_uint4(ow[0], ow[1], ow[2], ow[3]);
+}
+MOE_DEVINL float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 // largest i in [0, n) with arr[i] <= v  (arr ascending, arr[0] = 0)
 MOE_DEVINL int upper_bound_idx(const int32_t* arr, int n, int64_t v) {
   int lo = 0, hi = n;

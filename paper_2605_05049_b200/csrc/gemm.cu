@@ -70,6 +70,14 @@ struct KParams {
   int64_t disp_dst_off;
   int64_t arrive_off;
   int32_t* work;
+  // kEpiDSwiGLUComb
+  const uint16_t* cb_dy;
+  const float* cb_gates;
+  const uint16_t* cb_ys;
+  float* cb_dgates;
+  const int32_t* cb_slot_of_row;
+  const int32_t* cb_dest_row;
+  const int32_t* cb_layout;
 };
 
 // STG = staging boxes per epilogue warp.  2 double-buffers the fp32 wgrad epilogue (its K is
@@ -99,7 +107,9 @@ __host__ __device__ constexpr int staging_boxes() { return EPI == kEpiF32Group ?
 // fused dispatch tables (6 E + E_l + 3 ints, E <= 256) beyond the common table area
 constexpr int kDispSmem = 8192;
 template <int EPI>
-__host__ __device__ constexpr int extra_smem() { return EPI == kEpiSwiGLUDisp ? kDispSmem : 0; }
+__host__ __device__ constexpr int extra_smem() {
+  return (EPI == kEpiSwiGLUDisp || EPI == kEpiDSwiGLUComb) ? kDispSmem : 0;
+}
 
 __device__ __forceinline__ int ceil_div(int a, int b) { return (a + b - 1) / b; }
 
@@ -221,7 +231,9 @@ __device__ __forceinline__ void spin_flag(const uint64_t* f, uint64_t v, int32_t
 
 // All threads of the CTA.  Fills the GEMM group tables (s_rows/s_seg/s_tile_prefix over the
 // E_l local slots), s_pre[r][el] (rows of slot el from sources < r), and t.
-template <int TILE_M, int BN>
+// EXCH (dispatch): the counts exchange first; else (combine_bwd) the count matrix is the
+// forward's layout record and the dropped slots' dgates are zeroed here.
+template <int TILE_M, int BN, bool EXCH>
 __device__ void disp_prologue(const KParams& p, const DispTables& t, int* s_rows, int* s_seg,
                               int* s_tile_prefix, int* s_pre, int* s_arrived) {
   const CommArgs& a = p.comm;
@@ -229,11 +241,17 @@ __device__ void disp_prologue(const KParams& p, const DispTables& t, int* s_rows
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     *t.epoch = *reinterpret_cast<volatile const uint64_t*>(a.epoch_ptr) + 1;
-    *t.first = atomicAdd(p.work + 1, 1) == 0;
+    *t.first = EXCH ? atomicAdd(p.work + 1, 1) == 0 : 0;
   }
   __syncthreads();
   const uint64_t epoch = *t.epoch;
-  if (*t.first) {   // counts exchange: this rank's row of every peer's count matrix
+  if (!EXCH) {
+    const int64_t n = a.T * a.k;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+      if (p.cb_dest_row[i] < 0) p.cb_dgates[i] = 0.f;
+  }
+  if (EXCH && *t.first) {   // counts exchange: this rank's row of every peer's count matrix
     for (int i = threadIdx.x; i < EP * E; i += blockDim.x) {
       const int q = i / E, e = i % E;
       reinterpret_cast<int32_t*>(peer_base(a, q) + a.countmat_off)[me * E + e] = p.disp_counts[e];
@@ -243,10 +261,10 @@ __device__ void disp_prologue(const KParams& p, const DispTables& t, int* s_rows
       st_release_sys(reinterpret_cast<uint64_t*>(peer_base(a, threadIdx.x) + a.flags_off) +
                          kSlotCounts * EP + me, epoch);
   }
-  if (threadIdx.x < EP) spin_flag(a.flags + kSlotCounts * EP + threadIdx.x, epoch, a.err);
+  if (EXCH && threadIdx.x < EP) spin_flag(a.flags + kSlotCounts * EP + threadIdx.x, epoch, a.err);
   __threadfence();
   __syncthreads();
-  const int32_t* cm = a.countmat;
+  const int32_t* cm = EXCH ? a.countmat : p.cb_layout;
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
     int all = 0, before = 0;
     for (int r = 0; r < EP; ++r) {
@@ -323,7 +341,7 @@ __device__ void disp_prologue(const KParams& p, const DispTables& t, int* s_rows
         [&](int i, int32_t pre) { t.sg_pre[i] = pre; });
     if (lane == 0) t.sg_pre[E] = total;
   }
-  if (*t.first) {   // layout record for the later calls of this layer (as comm.cu's dispatch)
+  if (EXCH && *t.first) {   // layout record for the later calls of this layer (as comm.cu)
     for (int i = threadIdx.x; i < EP * E; i += blockDim.x) p.disp_layout[i] = cm[i];
     for (int el = threadIdx.x; el < E_l; el += blockDim.x) p.disp_layout[EP * E + el] = s_rows[el];
     for (int el = threadIdx.x; el <= E_l; el += blockDim.x) p.disp_layout[EP * E + E_l + el] = s_seg[el];
@@ -332,7 +350,11 @@ __device__ void disp_prologue(const KParams& p, const DispTables& t, int* s_rows
   __syncthreads();
 }
 
-// Warps 2-3: the transfer (see above), then the end of the collective.
+// Warps 2-3: the transfer (see above), then the end of the collective.  COMB (combine_bwd):
+// items are whole rows -- send-layout row r of slot (t, j) carries bf16(g[t,j] * dy[t]) and
+// yields dgates[t,j] = <dy[t], ys[r]> (combine_bwd_vec, the transfer kernel's arithmetic).
+constexpr int kCombChunk = 4;   // rows claimed per atomic (combine_bwd)
+template <bool COMB>
 __device__ void disp_copy(const KParams& p, const DispTables& t, const int* s_rows,
                           const int* s_seg) {
   const CommArgs& a = p.comm;
@@ -340,7 +362,7 @@ __device__ void disp_copy(const KParams& p, const DispTables& t, const int* s_ro
   const int lane = threadIdx.x & 31;
   const uint64_t epoch = *t.epoch;
   const int nvec = a.d / 8;
-  const int parts = (nvec + 127) / 128;
+  const int parts = COMB ? 1 : (nvec + 127) / 128;
   const int64_t row_bytes = static_cast<int64_t>(a.d) * 2;
   const int n_pad = t.pad_pre[E_l] * parts;
   const int n_items = n_pad + t.sg_pre[E] * parts;
@@ -362,13 +384,62 @@ __device__ void disp_copy(const KParams& p, const DispTables& t, const int* s_ro
     }
     __syncwarp();
   };
+  constexpr int kChunk = COMB ? kCombChunk : kDispChunk;
   for (;;) {
     int base = 0;
-    if (lane == 0) base = atomicAdd(p.work, kDispChunk);
+    if (lane == 0) base = atomicAdd(p.work, kChunk);
     base = __shfl_sync(0xffffffffu, base, 0);
     if (base >= n_items) break;
-    const int end = min(base + kDispChunk, n_items);
+    const int end = min(base + kChunk, n_items);
     int cur = -1, ncur = 0;
+    if constexpr (COMB) {
+      for (int it = base; it < end; ++it) {
+        int sid;
+        if (it < n_pad) {
+          const int el = upper_bound_idx(t.pad_pre, E_l + 1, it);
+          const int64_t row = s_seg[el] + s_rows[el] + (it - t.pad_pre[el]);
+          uint4* z = reinterpret_cast<uint4*>(xr_local + row * row_bytes);
+          for (int v = lane; v < nvec; v += 32) st_v4(z + v, make_uint4(0u, 0u, 0u, 0u));
+          sid = E + el;
+        } else {
+          const int r = it - n_pad;
+          const int i = upper_bound_idx(t.sg_pre, E + 1, r);
+          const int within = r - t.sg_pre[i];
+          const int64_t srow = t.sg_src[i] + within;
+          const int tj = p.cb_slot_of_row[srow];
+          const int64_t tok = tj / a.k;
+          const float g = p.cb_gates[tj];
+          const uint4* pdy = reinterpret_cast<const uint4*>(p.cb_dy + tok * a.d);
+          const uint4* pys = reinterpret_cast<const uint4*>(p.cb_ys + srow * a.d);
+          uint4* dst = reinterpret_cast<uint4*>(peer_base(a, seg_owner(i, me, EP)) + p.disp_dst_off +
+                                                static_cast<int64_t>(t.sg_dst[i] + within) * row_bytes);
+          float dot = 0.f;
+          for (int v0 = lane; v0 < nvec; v0 += 128) {
+            uint4 av[4], bv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (v0 + 32 * u < nvec) {
+                av[u] = ld_nc_v4(pdy + v0 + 32 * u);
+                bv[u] = ld_nc_v4(pys + v0 + 32 * u);
+              }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              if (v0 + 32 * u >= nvec) break;
+              st_v4(dst + v0 + 32 * u, combine_bwd_vec(av[u], bv[u], g, dot));
+            }
+          }
+          dot = warp_sum(dot);
+          if (lane == 0) p.cb_dgates[tj] = dot;
+          sid = i;
+        }
+        if (sid != cur) {
+          flush(cur, ncur);
+          cur = sid;
+          ncur = 0;
+        }
+        ++ncur;
+      }
+    } else
     for (int it = base; it < end; it += kDispInFlight) {
       // kDispInFlight row parts in flight per lane (16 B x 4 each, all loads before the stores)
       uint4 v[kDispInFlight][4];
@@ -509,7 +580,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int STG = staging_boxes<EPI>();
   using C = Cfg<BN, PAIR, STG, extra_smem<EPI>()>;
   constexpr bool DISP = (EPI == kEpiSwiGLUDisp);
+  constexpr bool COMB = (EPI == kEpiDSwiGLUComb);
+  constexpr bool XFER = DISP || COMB;      // a transfer fused in front of the GEMM
   constexpr bool SWIGLU = (EPI == kEpiSwiGLU || DISP);
+  constexpr bool DSW = (EPI == kEpiDSwiGLU || COMB);
   constexpr bool KGROUPED = (EPI == kEpiF32Group);
   constexpr int TILE_M = kBM * PAIR;
   constexpr uint32_t IDESC = idesc_bf16(TILE_M, BN, A_MN, B_MN);
@@ -533,9 +607,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   int* s_rows = s_seg + kMaxGroups + 1;                          // [kMaxGroups]
   int* s_pre = s_rows + kMaxGroups;                              // scatter: [EP][E_l] (<= 256)
   int* s_soff = s_pre + kMaxGroups;                              // scatter: [EP][E_l]
-  // DISP: s_soff holds the arrival cache; the transfer tables follow
+  // XFER: s_soff holds the arrival cache; the transfer tables follow
   DispTables dt;
-  if constexpr (DISP) {
+  if constexpr (XFER) {
     int* q = s_soff + kMaxGroups;
     dt.epoch = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(q) + 7) & ~uintptr_t(7));
     dt.first = reinterpret_cast<int*>(dt.epoch + 1);
@@ -556,7 +630,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
     tma_prefetch_desc(&tmC);
-    if (EPI == kEpiDSwiGLU) tma_prefetch_desc(&tmX);
+    if (DSW) tma_prefetch_desc(&tmX);
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], PAIR);     // leader: one arrival per producer of the pair
       mbar_init(&empty[s], 1);
@@ -578,8 +652,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   pdl_wait();   // the previous kernel's outputs (this launch's inputs) are complete and visible
-  if constexpr (DISP) {
-    disp_prologue<TILE_M, BN>(p, dt, s_rows, s_seg, s_tile_prefix, s_pre, s_soff);
+  if constexpr (XFER) {
+    disp_prologue<TILE_M, BN, DISP>(p, dt, s_rows, s_seg, s_tile_prefix, s_pre, s_soff);
   } else {
   // ---- group tables: seg_base = 128-aligned prefix of rows; tile prefix
   if (warp == 3) {
@@ -637,7 +711,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   }
-  }  // !DISP
+  }  // !XFER
   tc_fence_before();
   if (PAIR == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
@@ -662,7 +736,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (t < 0) break;
         const Tile tl = decode_tile<KGROUPED, BN, TILE_M>(t, s_tile_prefix, s_seg, s_rows,
                                                           n_groups, p);
-        if constexpr (DISP)
+        if constexpr (XFER)
           disp_wait_rows(p, tl.g, tl.m * TILE_M + static_cast<int>(rank) * kBM, tl.rows_g, s_pre,
                          s_soff, *dt.epoch);
         for (int kb = 0; kb < tl.nkb; ++kb) {
@@ -765,9 +839,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
-  } else if (DISP && warp < 4) {
-    // ===================== fused dispatch (warps 2-3) =====================
-    if constexpr (DISP) disp_copy(p, dt, s_rows, s_seg);
+  } else if (XFER && warp < 4) {
+    // ===================== fused transfer (warps 2-3) =====================
+    if constexpr (XFER) disp_copy<COMB>(p, dt, s_rows, s_seg);
   } else if (warp >= 4) {
     // ===================== epilogue =====================
     const int ew = warp - 4;  // TMEM lane quadrant ew*32 .. ew*32+31
@@ -790,7 +864,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // the next group and are not written here (whole 32-row boxes, segments are 128-aligned).
       const bool box_in = KGROUPED || m_box < ((tl.rows_g + kBM - 1) / kBM) * kBM;
       const int64_t grow = static_cast<int64_t>(tl.seg) + mi;
-      if (EPI == kEpiDSwiGLU && valid && grow < p.rows_cap) {
+      if (DSW && valid && grow < p.rows_cap) {
         // warm L2 with this row's saved G and U segments while the MMAs run
         const uint16_t* a = reinterpret_cast<const uint16_t*>(p.aux) + grow * p.ld_aux + tl.n * BN;
         prefetch_l2_bulk(a, BN * 2);
@@ -886,7 +960,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
-      } else if (EPI == kEpiDSwiGLU) {
+      } else if (DSW) {
         // acc = dH for f-columns n*BN ...; dG = dH*U*silu'(G), dU = dH*silu(G) -> dgu
 #pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += 64) {
@@ -1125,6 +1199,7 @@ template <int BN, bool A_MN, bool B_MN, int EPI, int PAIR>
 cudaError_t launch_impl(const GemmProblem& g, cudaStream_t stream) {
   using C = Cfg<BN, PAIR, staging_boxes<EPI>(), extra_smem<EPI>()>;
   constexpr bool SWIGLU = (EPI == kEpiSwiGLU || EPI == kEpiSwiGLUDisp);
+  constexpr bool DSW = (EPI == kEpiDSwiGLU || EPI == kEpiDSwiGLUComb);
   CUtensorMap ta, tb, tc;
   // A box: K-major {64 k, 128 rows}; MN-major {64 m, 64 k}
   if (!make_tmap_bf16(&ta, g.a_ptr, g.a_rows, g.a_cols, g.a_ld, 64, A_MN ? 64 : kBM))
@@ -1151,13 +1226,13 @@ cudaError_t launch_impl(const GemmProblem& g, cudaStream_t stream) {
     }
   } else {
     const int64_t cols = SWIGLU ? 3 * static_cast<int64_t>(g.f)
-                         : (EPI == kEpiDSwiGLU) ? 2 * static_cast<int64_t>(g.f)
+                         : DSW ? 2 * static_cast<int64_t>(g.f)
                                                 : g.N;
     if (!make_tmap_bf16(&tc, g.out, g.rows_cap, cols, g.ld_out, 64, 32)) return cudaErrorInvalidValue;
   }
   // dSwiGLU: the saved G | U | H rows as 32 x 64 boxes for the epilogue's TMA loads
   CUtensorMap tx = tc;
-  if (EPI == kEpiDSwiGLU) {
+  if (DSW) {
     static int tma_aux = -1;   // MOE_DSWIGLU_TMA=0: per-lane global loads (measurements)
     if (tma_aux < 0) {
       const char* e = getenv("MOE_DSWIGLU_TMA");
@@ -1187,10 +1262,21 @@ cudaError_t launch_impl(const GemmProblem& g, cudaStream_t stream) {
     kp.scatter_layout = g.scatter_layout;
     kp.comm = *g.comm;
   }
-  if (EPI == kEpiSwiGLUDisp) {
-    if (!g.comm || !g.disp_counts || !g.disp_layout || !g.disp_work || g.n_groups != g.comm->E_l ||
-        g.comm->E > kMaxGroups)
+  if (EPI == kEpiSwiGLUDisp || EPI == kEpiDSwiGLUComb) {
+    const bool comb = EPI == kEpiDSwiGLUComb;
+    if (!g.comm || !g.disp_work || g.n_groups != g.comm->E_l || g.comm->E > kMaxGroups ||
+        (!comb && (!g.disp_counts || !g.disp_layout)) ||
+        (comb && (!g.cb_layout || (g.comm->T > 0 && (!g.cb_dy || !g.cb_gates || !g.cb_ys ||
+                                                     !g.cb_dgates || !g.cb_slot_of_row ||
+                                                     !g.cb_dest_row)))))
       return cudaErrorInvalidValue;
+    kp.cb_dy = static_cast<const uint16_t*>(g.cb_dy);
+    kp.cb_gates = g.cb_gates;
+    kp.cb_ys = static_cast<const uint16_t*>(g.cb_ys);
+    kp.cb_dgates = g.cb_dgates;
+    kp.cb_slot_of_row = g.cb_slot_of_row;
+    kp.cb_dest_row = g.cb_dest_row;
+    kp.cb_layout = g.cb_layout;
     kp.comm = *g.comm;
     kp.disp_src = static_cast<const uint16_t*>(g.disp_src);
     kp.disp_counts = g.disp_counts;
@@ -1278,6 +1364,8 @@ cudaError_t launch_grouped_gemm(const GemmProblem& g, cudaStream_t s) {
   MOE_GEMM_CASE(64, false, true, kEpiBF16)
   MOE_GEMM_CASE(256, false, true, kEpiDSwiGLU)
   MOE_GEMM_CASE(128, false, true, kEpiDSwiGLU)
+  MOE_GEMM_CASE(256, false, true, kEpiDSwiGLUComb)
+  MOE_GEMM_CASE(128, false, true, kEpiDSwiGLUComb)
   MOE_GEMM_CASE(256, true, true, kEpiF32Group)
   MOE_GEMM_CASE(128, true, true, kEpiF32Group)
   MOE_GEMM_CASE(64, true, true, kEpiF32Group)

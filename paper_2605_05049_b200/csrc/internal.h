@@ -55,6 +55,9 @@ enum Epilogue : int {
   kEpiSwiGLUDisp = 5,  // GEMM1 + SwiGLU with the dispatch all-to-all fused in (NEXT-1):
                        // warps 2-3 push this rank's send rows to their owners while the
                        // producer starts each A tile as soon as its source rows have landed
+  kEpiDSwiGLUComb = 6, // dgrad-1 + dSwiGLU with combine_bwd fused in (NEXT-1, backward twin):
+                       // warps 2-3 push g * dy rows (and compute dgates), each dO tile starts
+                       // when its rows have landed
 };
 
 struct GemmProblem {
@@ -96,6 +99,14 @@ struct GemmProblem {
   int64_t disp_dst_off = 0;            // byte offset of xr (= a_ptr) inside every heap
   int64_t arrive_off = 0;              // heap offset of the arrival flags [E_l][EP+1]
   int32_t* disp_work = nullptr;        // local scratch, zero between calls: [4 + E + E_l]
+  // kEpiDSwiGLUComb: combine_bwd payload sources (disp_dst_off = dout_r, arrive/work as above)
+  const void* cb_dy = nullptr;            // dy [T_local, d]
+  const float* cb_gates = nullptr;        // [T_local * k]
+  const void* cb_ys = nullptr;            // ys [T_local * k, d] (send layout, forward outputs)
+  float* cb_dgates = nullptr;             // [T_local * k] out
+  const int32_t* cb_slot_of_row = nullptr;  // send-layout row -> slot t*k+j
+  const int32_t* cb_dest_row = nullptr;   // [T_local * k] (-1: dropped -> dgates 0)
+  const int32_t* cb_layout = nullptr;     // layout record of the forward dispatch
 };
 
 cudaError_t launch_grouped_gemm(const GemmProblem& p, cudaStream_t stream);
@@ -125,7 +136,8 @@ int64_t permute_scratch_ints(int64_t T, int k, int E);
 cudaError_t launch_permute(const uint16_t* x, const int32_t* topk_idx, int64_t T, int d, int E,
                            int k, int64_t C, int32_t* counts, int32_t* dest_row, uint16_t* xs,
                            int32_t* scratch, cudaStream_t s, int32_t* layout = nullptr,
-                           const int32_t* expert_at = nullptr, int64_t pad_rows_max = 0);
+                           const int32_t* expert_at = nullptr, int64_t pad_rows_max = 0,
+                           int32_t* slot_of_row = nullptr);
 cudaError_t launch_permute_bwd(const uint16_t* dxs, const int32_t* dest_row, const float* dx_acc,
                                const uint16_t* dx_extra, int64_t T, int d, int k, uint16_t* dx,
                                cudaStream_t s);

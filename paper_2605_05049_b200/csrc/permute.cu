@@ -103,7 +103,7 @@ __global__ void hist_scan_kernel(const int32_t* __restrict__ idx, int64_t T, int
 // Pass 2: stable rank inside the chunk -> p, kept, dest_row.
 __global__ void rank_kernel(const int32_t* __restrict__ idx, int64_t T, int k, int E, int64_t C,
                             const int32_t* __restrict__ chunk_base, const int32_t* __restrict__ off,
-                            int32_t* __restrict__ dest_row) {
+                            int32_t* __restrict__ dest_row, int32_t* __restrict__ slot_of_row) {
   pdl_wait();
   pdl_trigger();
   extern __shared__ int32_t s_wcnt[];  // [32 warps][E]
@@ -132,6 +132,9 @@ __global__ void rank_kernel(const int32_t* __restrict__ idx, int64_t T, int k, i
   const bool kept = (C < 0) || (p < C);
   const int64_t t = a % T, j = a / T;
   dest_row[t * k + j] = kept ? static_cast<int32_t>(off[e] + p) : -1;
+  // inverse map (send-layout row -> slot t*k+j) for the row-ordered combine_bwd fused into
+  // dgrad-1 (moe_combine_bwd_expert_ffn_dh)
+  if (kept && slot_of_row) slot_of_row[off[e] + p] = static_cast<int32_t>(t * k + j);
 }
 
 // Pass 3: warp per token; read x_t once (4 x 16 B in flight per lane), write each kept row.
@@ -259,16 +262,7 @@ __global__ void combine_bwd_local_kernel(const uint16_t* __restrict__ dy,
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         if (v0 + 32 * u >= nvec) break;
-        const uint32_t aw[4] = {av[u].x, av[u].y, av[u].z, av[u].w};
-        const uint32_t bw[4] = {bv[u].x, bv[u].y, bv[u].z, bv[u].w};
-        uint32_t ow[4];
-#pragma unroll
-        for (int q2 = 0; q2 < 4; ++q2) {
-          const float y0 = bf16_lo(aw[q2]), y1 = bf16_hi(aw[q2]);
-          dot[j] += y0 * bf16_lo(bw[q2]) + y1 * bf16_hi(bw[q2]);
-          ow[q2] = pack_bf16(g[j] * y0, g[j] * y1);
-        }
-        pd[v0 + 32 * u] = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+        pd[v0 + 32 * u] = combine_bwd_vec(av[u], bv[u], g[j], dot[j]);
       }
     }
   }
@@ -598,7 +592,7 @@ int64_t permute_scratch_ints(int64_t T, int k, int E) {
 cudaError_t launch_permute(const uint16_t* x, const int32_t* topk_idx, int64_t T, int d, int E,
                            int k, int64_t C, int32_t* counts, int32_t* dest_row, uint16_t* xs,
                            int32_t* scratch, cudaStream_t s, int32_t* layout,
-                           const int32_t* expert_at, int64_t pad_rows_max) {
+                           const int32_t* expert_at, int64_t pad_rows_max, int32_t* slot_of_row) {
   const int64_t nA = T * k;
   const int nchunks = static_cast<int>((nA + kChunk - 1) / kChunk);
   int32_t* chunk_hist = scratch;
@@ -619,7 +613,7 @@ cudaError_t launch_permute(const uint16_t* x, const int32_t* topk_idx, int64_t T
     if (e != cudaSuccess) return e;
   }
   launch_k(rank_kernel, dim3(nchunks), dim3(kChunk), smem, s, topk_idx, T, k, E, C, chunk_hist, off,
-      dest_row);
+      dest_row, slot_of_row);
   const int threads = 256;
   if (!xs) return cudaGetLastError();   // indices only (the dedup dispatch reads x directly)
   const int64_t warps = T + (layout ? pad_rows_max : 0);

@@ -419,6 +419,17 @@ class MoELayer:
                                  self.dw_gu, self.dw_down, accumulate)
             self._mark("B4 expert ffn_bwd")
             return self._backward_tail(dy, accumulate, False, rows=self.dxr)
+        if self._tile_overlap():
+            # B6+B5 + dgrad-1 in one launch: dO tiles start as their rows land (NEXT-1)
+            L.moe_combine_bwd_expert_ffn_dh(c, dy, self.gates, self.dest_row, self.ys, self.layout,
+                                            self.dgates, self.dout_r, self.w_down, self.g_u_h,
+                                            self.dgu)
+            self._mark("B6+B5+B4 combine_bwd + dgrad-1 (tile-granular overlap)")
+            L.moe_expert_ffn_bwd_dx_dispatch(c, self.xr, self.layout, self.w_gu, self.g_u_h,
+                                             self.dout_r, self.dgu, self.dxs, self.dw_gu,
+                                             self.dw_down, accumulate)
+            self._mark("B4+B3 dgrad-2 + wgrads + dispatch_bwd")
+            return self._backward_tail(dy, accumulate, False)
         shared_done = False
         if self.fs and self.overlap:
             # shared-expert backward (needs only dy) beside the combine_bwd all-to-all
@@ -680,6 +691,8 @@ class MoELayer:
             # router bwd (hi/lo split, split-K dW_r GEMM, partial sum; k = 1 adds the
             # stacked-W_r copy and the dense dgrad GEMM), permute_bwd
             n += 1 + 4 + 1 + 1 + 3 + (0 if self.dims.k > 1 else 2) + 1 + (4 if self.fs else 0)
+            if self._tile_overlap():
+                n -= 1   # combine_bwd + dgrad-1 are one launch
         return n
 
     def close(self):

@@ -331,12 +331,13 @@ def test_ep1_local_path_bit_identical(name):
 
 @pytest.mark.parametrize("name", ["mixtral_small", "dsmoe_small", "drops", "v3_small_zipf"])
 def test_tile_overlap_bit_identical(name):
-    """NEXT-1 tile-granular overlap (moe_dispatch_expert_ffn_up: the dispatch inside the GEMM1
-    launch, tiles gated by per-(slot, source) arrival flags) against moe_dispatch +
-    moe_expert_ffn_up on the general path at EP = 1 (the transfer then targets this rank's
-    own heap): layout record, xr incl. zeroed padding, G|U|H, y, dx and the weight gradients
-    bit for bit, over repeated steps (the flag epochs and the work counters must reset) and
-    under a migrated placement."""
+    """NEXT-1 tile-granular overlap -- moe_dispatch_expert_ffn_up (the dispatch inside the GEMM1
+    launch) and moe_combine_bwd_expert_ffn_dh (combine_bwd inside dgrad-1), tiles gated by
+    per-(slot, source) arrival flags -- against the separate transfer + GEMM calls on the
+    general path at EP = 1 (the transfers then target this rank's own heap): layout record,
+    xr and dO incl. zeroed padding, G|U|H, dG|dU, dgates, y, dx and the weight gradients bit
+    for bit, over repeated steps (the flag epochs and the work counters must reset) and under
+    a migrated placement."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     cfg = CASES[name]
@@ -353,6 +354,7 @@ def test_tile_overlap_bit_identical(name):
                 layer.migrate(place)
             for step in range(3):
                 layer.xr.fill_(3.0)          # stale rows must be overwritten or zeroed
+                layer.dout_r.fill_(7.0)
                 layer.g_u_h.fill_(5.0)
                 y = layer.forward(x).clone()
                 dx = layer.backward(dy).clone()
@@ -360,7 +362,8 @@ def test_tile_overlap_bit_identical(name):
                 layer.ctx.check_device_error()
                 n = int(layer.layout[-1].item())
                 outs.append((y, dx, layer.dw_gu.clone(), layer.dw_down.clone(),
-                             layer.layout.clone(), layer.xr[:n].clone(), layer.g_u_h[:n].clone()))
+                             layer.layout.clone(), layer.xr[:n].clone(), layer.g_u_h[:n].clone(),
+                             layer.dgates.clone(), layer.dout_r[:n].clone(), layer.dgu[:n].clone()))
             layer.close()
         ref = outs[0]
         for o in outs[1:]:
