@@ -206,6 +206,18 @@ class MoELayer:
     # E_l = 2: 3.59-3.60 vs 3.52-3.55 ms).  MOE_TILE_OVERLAP=0/1 forces it.
     tile_overlap = {"0": False, "1": True}.get(os.environ.get("MOE_TILE_OVERLAP", ""))
     tile_overlap_min_experts = 8
+    # the backward twin (combine_bwd inside dgrad-1) with tile_overlap.  None = auto: only
+    # without shared experts -- with them the separate combine_bwd runs beside the shared-expert
+    # backward GEMMs, which the fused launch would serialise (4-GPU box,
+    # profiles/r02/tile_overlap/run4: DS-MoE N=4 2.03 ms fwd+bwd fused vs 1.80 forward only vs
+    # 1.84 off; V3-like N=4 25.6-25.8 vs 26.9 off).  MOE_TILE_OVERLAP_BWD=0/1 forces it.
+    tile_overlap_bwd = {"0": False, "1": True}.get(os.environ.get("MOE_TILE_OVERLAP_BWD", ""))
+
+    def _tile_overlap_bwd(self) -> bool:
+        on = self.tile_overlap_bwd
+        if on is None:
+            on = not self.fs
+        return bool(on) and self._tile_overlap()
     # per-phase CUDA-event markers (bench.py --breakdown); off by default
     marks = None
     # SMs given to an all-to-all that runs beside a GEMM (the GEMM gets the rest).  Measured on
@@ -419,7 +431,7 @@ class MoELayer:
                                  self.dw_gu, self.dw_down, accumulate)
             self._mark("B4 expert ffn_bwd")
             return self._backward_tail(dy, accumulate, False, rows=self.dxr)
-        if self._tile_overlap():
+        if self._tile_overlap_bwd():
             # B6+B5 + dgrad-1 in one launch: dO tiles start as their rows land (NEXT-1)
             L.moe_combine_bwd_expert_ffn_dh(c, dy, self.gates, self.dest_row, self.ys, self.layout,
                                             self.dgates, self.dout_r, self.w_down, self.g_u_h,
@@ -691,7 +703,7 @@ class MoELayer:
             # router bwd (hi/lo split, split-K dW_r GEMM, partial sum; k = 1 adds the
             # stacked-W_r copy and the dense dgrad GEMM), permute_bwd
             n += 1 + 4 + 1 + 1 + 3 + (0 if self.dims.k > 1 else 2) + 1 + (4 if self.fs else 0)
-            if self._tile_overlap():
+            if self._tile_overlap_bwd():
                 n -= 1   # combine_bwd + dgrad-1 are one launch
         return n
 

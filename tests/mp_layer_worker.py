@@ -103,7 +103,7 @@ def main():
     for it in range(args.iters):  # epoch reuse: repeated calls must be bit-identical
         # alternate the NEXT-1 tile-granular dispatch -> GEMM1 launch with the separate
         # dispatch + GEMM1 (fused path): both must give the same bits
-        layer.tile_overlap = it % 2 == 0
+        layer.tile_overlap = layer.tile_overlap_bwd = it % 2 == 0
         y = layer.forward(x).clone()
         dx = layer.backward(dy).clone()
         outs.append((y, dx, layer.dw_gu.clone()))

@@ -349,7 +349,7 @@ def test_tile_overlap_bit_identical(name):
         for tile in (True, False):
             layer = build_layer(cfg)
             layer.local_fast_path = False
-            layer.tile_overlap = tile
+            layer.tile_overlap = layer.tile_overlap_bwd = tile
             if place is not None:
                 layer.migrate(place)
             for step in range(3):
