@@ -196,7 +196,9 @@ moe_status moe_migrate(moe_ctx* ctx, const int32_t* old_placement, const int32_t
 /* SM budgets for the calls issued after it (0 = all SMs): grouped-GEMM launches use at most
  * gemm_sms SMs and all-to-all transfer launches 2 blocks on each of comm_sms SMs, so that a
  * GEMM and a transfer issued on two streams run concurrently on disjoint SMs (used to overlap
- * the shared-expert GEMMs with dispatch / combine_bwd). */
+ * the shared-expert GEMMs with dispatch / combine_bwd).  The GEMM
+ * launches that carry a transfer (moe_dispatch_expert_ffn_up, moe_combine_bwd_expert_ffn_dh)
+ * use gemm_sms SMs if it is set, else comm_sms. */
 moe_status moe_ctx_set_sm_limits(moe_ctx* ctx, int gemm_sms, int comm_sms);
 /* Synchronises the device; returns MOE_OK or the first device-side error recorded. */
 moe_status moe_ctx_get_device_error(moe_ctx* ctx);

@@ -940,7 +940,9 @@ moe_status moe_dispatch_expert_ffn_up(moe_ctx* c, const moe_bf16* xs, const int3
   g1.N = 2 * f; g1.K = d;
   g1.n_groups = c->E_l; g1.rows_cap = c->recv_rows;
   g1.pair = gemm_pair();
-  g1.max_ctas = c->gemm_sms;
+  // a launch that carries a collective spins on peers: it obeys the transfer SM budget too
+  // (the PP x EP executor keeps SMs free for the NCCL stage hand-offs, moe_ctx_set_sm_limits)
+  g1.max_ctas = c->gemm_sms > 0 ? c->gemm_sms : c->comm_sms;
   g1.out = g_u_h; g1.ld_out = 3 * static_cast<int64_t>(f); g1.f = f;
   g1.comm = &a;
   g1.disp_src = xs; g1.disp_counts = counts; g1.disp_layout = layout;
@@ -973,7 +975,9 @@ moe_status moe_combine_bwd_expert_ffn_dh(moe_ctx* c, const moe_bf16* dy, const f
   g.N = f; g.K = d;
   g.n_groups = c->E_l; g.rows_cap = c->recv_rows;
   g.pair = gemm_pair();
-  g.max_ctas = c->gemm_sms;
+  // a launch that carries a collective spins on peers: it obeys the transfer SM budget too
+  // (the PP x EP executor keeps SMs free for the NCCL stage hand-offs, moe_ctx_set_sm_limits)
+  g.max_ctas = c->gemm_sms > 0 ? c->gemm_sms : c->comm_sms;
   g.out = dgu; g.ld_out = 2 * F; g.aux = g_u_h; g.ld_aux = 3 * F; g.f = f;
   g.comm = &a;
   g.disp_dst_off = heap_off(c, dout_r);
