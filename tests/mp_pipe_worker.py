@@ -49,6 +49,9 @@ def main():
                          "stage's EP subgroup)")
     ap.add_argument("--graph", action="store_true",
                     help="also replay the step from a CUDA graph: bitwise equal to eager")
+    ap.add_argument("--tile", action="store_true",
+                    help="force the tile-granular transfers (dispatch inside GEMM1, combine_bwd "
+                         "inside dgrad-1) in every layer of the stack (NEXT-1 x NEXT-3)")
     args = ap.parse_args()
     local, shared = mp_common.init()
     world, rank = dist.get_world_size(), dist.get_rank()
@@ -62,6 +65,10 @@ def main():
     T_r = cfg.T // ep
     dims = LayerDims(T_r, cfg.d, cfg.E, cfg.k, cfg.f, 0, cfg.cf, ep, e)
     stack = PipelineStack(dims, Lyr, pp, M, device=local, dedup=args.dedup)
+    if args.tile:
+        for slots in stack.layers:
+            for s_ in slots:
+                s_.tile_overlap = s_.tile_overlap_bwd = True
     E_l = cfg.E // ep
     dev = torch.device(f"cuda:{local}")
     per = Lyr // pp

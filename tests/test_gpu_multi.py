@@ -143,7 +143,8 @@ def test_layer_ep_parity_dedup(nproc, config, extra, mode):
 
 @pytest.mark.parametrize("nproc,pp,extra", [(2, 2, ()), (4, 2, ()), (4, 4, ()),
                                             (4, 2, ("--dedup", "dispatch")), (4, 2, ("--graph",)),
-                                            (4, 2, ("--migrate",)), (8, 2, ())])
+                                            (4, 2, ("--migrate",)), (8, 2, ()),
+                                            (4, 2, ("--tile",))])
 def test_pipeline_pp_x_ep(nproc, pp, extra):
     """NEXT-3 PP x EP executor (1F1B PAPER.md:282-288): a 4-layer stack over
     4 micro-batches; every (layer, micro-batch) against the teacher-forced fp64 oracle, the
