@@ -425,7 +425,10 @@ def run_ours(args):
     # forward-pattern all-to-alls (NVLink).  Not part of `value`.
     hooked = ["moe_expert_ffn", "moe_expert_ffn_bwd", "moe_expert_ffn_combine",
               "moe_expert_ffn_bwd_dispatch", "moe_expert_ffn_up", "moe_expert_ffn_down_combine",
-              "moe_expert_ffn_bwd_dh", "moe_expert_ffn_bwd_dx_dispatch"]
+              "moe_expert_ffn_bwd_dh", "moe_expert_ffn_bwd_dx_dispatch",
+              # GEMM1 / dgrad-1 launches that carry the dispatch / combine_bwd (NEXT-1): their
+              # time counts as GEMM time, the transfer regions then stay empty
+              "moe_dispatch_expert_ffn_up", "moe_combine_bwd_expert_ffn_dh"]
     buckets = {"moe_permute": "permute", "moe_permute_dispatch_local": "permute",
                "moe_dispatch": "dispatch",
                "moe_combine_bwd": "combine_bwd", "moe_combine_bwd_local": "combine_bwd",
@@ -566,6 +569,10 @@ def run_ours(args):
             "parallelism": f"ep{world}", "tokens_per_rank": T_r,
             "expert_migration": rebal,
             "dedup_a2a": layer.dedup_mode,
+            # NEXT-1 tile-granular transfers (dispatch inside GEMM1 / combine_bwd inside
+            # dgrad-1); only on the EP > 1 path
+            "tile_overlap": {"fwd": world > 1 and layer._tile_overlap(),
+                             "bwd": world > 1 and layer._tile_overlap_bwd()},
             "cuda_graph": use_graph,
             "eager_ms_per_step": eager_ms,
             "graph_ms_per_step": graph_ms if args.graph else None,
