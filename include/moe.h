@@ -30,7 +30,8 @@
  *   collective calls still take part in the exchange.
  * - Collective calls (moe_dispatch, moe_dispatch_bwd, moe_combine,
  *   moe_combine_bwd, their _range variants, the fused *_combine / *_dispatch FFN
- *   calls, the moe_dedup_* all-to-alls, moe_symm_alloc) must be issued by every EP
+ *   calls, moe_dispatch_expert_ffn_up, moe_combine_bwd_expert_ffn_dh, the moe_dedup_*
+ *   all-to-alls, moe_migrate, moe_all_to_all, moe_symm_alloc) must be issued by every EP
  *   rank in the same order, like NCCL collectives.  Not thread-safe; one ctx per
  *   (process, GPU, layer activation context) -- several ctxs per process are fine
  *   (the PP x EP executor keeps one per layer and in-flight micro-batch).
