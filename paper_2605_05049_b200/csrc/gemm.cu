@@ -193,11 +193,13 @@ __device__ __forceinline__ float silu_f(float g) { return g * sigmoid_f(g); }
 //     proxy after the acquire.
 // The kernel ends the collective like comm.cu's dispatch: data flags to every peer, wait for
 // every peer's, commit the epoch -- so the next collectives see the same protocol state.
+// kEpiDSwiGLUComb is the backward twin (combine_bwd inside dgrad-1): no counts exchange (the
+// forward's layout record), whole-row items carrying bf16(g dy) plus the dgates dot products.
 struct DispTables {
   int* rows;     // [E]     rows of expert e over all sources
   int* dst;      // [E]     receive row of this rank's first row of expert e at its owner
   int* off;      // [E+1]   this rank's send layout (exclusive scan of its counts)
-  int* sg_pre;   // [E+1]   transfer order i (owner rank+1 first, self last): row prefix
+  int* sg_pre;   // [E+1]   row prefix over transfer segments i (seg_owner / seg_slot order)
   int* sg_src;   // [E]
   int* sg_dst;   // [E]
   int* pad_pre;  // [E_l+1] padding rows of this rank's slots, prefix
