@@ -117,3 +117,22 @@ def test_load_imbalance_matches_oracle(lib, seed):
     place = rng.permutation(E)
     assert lib.moe_load_imbalance(loads, place, ep) == mig.imbalance(loads, place, ep)
     assert lib.moe_load_imbalance([0] * E, list(range(E)), ep) == 1.0
+
+
+def test_binding_signatures_match_the_header():
+    """Every ctypes signature in _lib.py has the arity of its include/moe.h declaration, with
+    pointers (incl. the moe_stream handle) where the header has pointers."""
+    import ctypes
+    import re
+    from paper_2605_05049_b200 import _lib as L
+    h = re.sub(r"/\*.*?\*/", "", open(os.path.join(ROOT, "include", "moe.h")).read(), flags=re.S)
+    decls = {m.group(1): m.group(2) for m in re.finditer(
+        r"\b(?:moe_status|int64_t|int)\s+(moe_\w+)\s*\(([^;]*?)\)\s*;", h)}
+    for name, args in L._SIGS.items():
+        assert name in decls, name
+        params = [p.strip() for p in decls[name].split(",") if p.strip() not in ("", "void")]
+        assert len(params) == len(args), (name, params, args)
+        for p, a in zip(params, args):
+            is_ptr = "*" in p or p.startswith("moe_stream")
+            a_ptr = a is ctypes.c_void_p or (isinstance(a, type) and issubclass(a, ctypes._Pointer))
+            assert is_ptr == a_ptr, (name, p, a)

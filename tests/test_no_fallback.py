@@ -1,13 +1,10 @@
 """The product path has no CPU or oracle fallback (CPU tests): a missing libmoe.so fails the
-import, CPU tensors are rejected before any call, and nothing in the package imports the
+import (CPU tensors are rejected: tests/test_abi.py), and nothing in the package imports the
 oracle (only tests/, __graft_entry__.smoke() and bench.py's CPU arms may)."""
 import ast
 import os
 import subprocess
 import sys
-
-import pytest
-import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 PKG = os.path.join(ROOT, "paper_2605_05049_b200")
@@ -19,18 +16,6 @@ def test_missing_library_fails_the_import():
                        capture_output=True, text=True, timeout=300)
     assert p.returncode != 0
     assert "ImportError" in p.stderr or "OSError" in p.stderr
-
-
-def test_cpu_tensors_are_rejected():
-    from paper_2605_05049_b200 import _lib as L
-
-    class Ctx:   # never reached: the argument check comes first
-        handle = None
-    logits = torch.zeros((4, 8), dtype=torch.float32)
-    idx = torch.zeros((4, 2), dtype=torch.int32)
-    gates = torch.zeros((4, 2), dtype=torch.float32)
-    with pytest.raises(ValueError, match="no CPU path"):
-        L.moe_route(Ctx(), logits, idx, gates)
 
 
 def test_package_never_imports_the_oracle():
